@@ -1,0 +1,302 @@
+#!/usr/bin/env python
+"""Benchmark of the GLAM lambda-path fit (BASELINE.json metric:
+"lambda-path fit time & prox-grad iters/s; rho-contraction HBM GB/s vs peak").
+
+One step = one full warm-started lambda path (BASELINE config C2 by default:
+Gaussian 3-D GLAM, n = (100,100,500), p = (30,30,120), cubic B-splines,
+50-lambda lasso path) with the observation array resident in HBM.
+value = prox-grad (FISTA) iterations per second over the whole path, summed
+over ranks (each rank fits an independent replica: its own noise draw).
+
+  python bench.py [--gpus N] [--steps K] [--warmup W] [--config C2] [--impl ours|reference]
+
+--impl reference times the reference's CPU algorithm (the oracle port in
+oracle/, since the Eigen-based reference cannot be built here) on the host
+cores, on a bounded prefix of the same path.
+"""
+from __future__ import annotations
+
+import argparse
+import json
+import os
+import subprocess
+import sys
+import threading
+import time
+
+import numpy as np
+
+ROOT = os.path.dirname(os.path.abspath(__file__))
+sys.path.insert(0, ROOT)
+
+METRIC = "lambda-path fit time & prox-grad iters/s; rho-contraction HBM GB/s vs peak"
+UNIT = "prox-grad iters/s"
+
+
+def parse():
+    ap = argparse.ArgumentParser()
+    ap.add_argument("--gpus", type=int, default=1)
+    ap.add_argument("--steps", type=int, default=5)
+    ap.add_argument("--warmup", type=int, default=3)
+    ap.add_argument("--config", default="C2")
+    ap.add_argument("--impl", default="ours", choices=["ours", "reference"])
+    ap.add_argument("--cpu-budget", type=float, default=12.0, help="seconds of CPU work per baseline sample")
+    ap.add_argument("--no-cpu-baseline", action="store_true")
+    return ap.parse_args()
+
+
+def peaks():
+    path = os.path.join(ROOT, "MEASURED_PEAKS.json")
+    if os.path.exists(path):
+        with open(path) as f:
+            p = json.load(f)
+        return float(p["hbm_gbs"]), "measured"
+    return 6650.0, "fallback"
+
+
+class Clocks:
+    """nvidia-smi sampler running during the timed region."""
+
+    def __init__(self, index=0):
+        self.samples = []
+        self.index = index
+        self._stop = threading.Event()
+        self._t = None
+
+    def start(self):
+        def run():
+            q = ("clocks.sm,clocks.max.sm,clocks_event_reasons.hw_slowdown,"
+                 "clocks_event_reasons.hw_thermal_slowdown,clocks_event_reasons.sw_thermal_slowdown,"
+                 "clocks_event_reasons.sw_power_cap")
+            while not self._stop.is_set():
+                try:
+                    out = subprocess.run(["nvidia-smi", "-i", str(self.index), f"--query-gpu={q}",
+                                          "--format=csv,noheader,nounits"], capture_output=True, text=True,
+                                         timeout=5).stdout.strip()
+                    if out:
+                        self.samples.append([x.strip() for x in out.split(",")])
+                except Exception:
+                    pass
+                self._stop.wait(0.2)
+
+        self._t = threading.Thread(target=run, daemon=True)
+        self._t.start()
+
+    def stop(self):
+        self._stop.set()
+        if self._t:
+            self._t.join(timeout=10)
+        if not self.samples:
+            return {"sm_mhz": None, "sm_max_mhz": None, "reasons": ["nvidia-smi unavailable"], "samples": 0}
+        sm = [float(s[0]) for s in self.samples if s[0].replace(".", "").isdigit()]
+        mx = [float(s[1]) for s in self.samples if s[1].replace(".", "").isdigit()]
+        names = ["hw_slowdown", "hw_thermal_slowdown", "sw_thermal_slowdown", "sw_power_cap"]
+        reasons = sorted({names[i] for s in self.samples for i in range(4) if s[2 + i].lower() == "active"})
+        return {"sm_mhz": float(np.median(sm)) if sm else None, "sm_max_mhz": max(mx) if mx else None,
+                "reasons": reasons, "samples": len(self.samples)}
+
+
+def lambda_grid(design, y, family, n_lambda, ratio):
+    from oracle import oracle as O
+    lmax = O.lambda_max(design, family, y)
+    return [lmax * np.exp(np.log(ratio) / (n_lambda - 1) * t) if t else lmax for t in range(n_lambda)]
+
+
+def cpu_sample(data, threads, budget, n_models=None):
+    """Oracle fit of a prefix of the path, lambda by lambda with warm starts (the
+    reference's fit_path order), until `budget` seconds or `n_models` models."""
+    from oracle import oracle as O
+    O.set_threads(threads)
+    lams = lambda_grid(data["design"], data["y"], data["family"], data["n_lambda"], data["lambda_min_ratio"])
+    t0 = time.perf_counter()
+    iters, k, init, coefs = 0, 0, None, []
+    for t, lam in enumerate(lams):
+        if n_models is not None and t >= n_models:
+            break
+        if n_models is None and time.perf_counter() - t0 > budget:
+            break
+        r = O.outer_solve(data["design"], data["family"], data["y"], lam, init=init)
+        iters += sum(int(rec["inner_iterations"]) for rec in r["iterations"])
+        init = r["coef"]
+        coefs.append(r["coef_flat"])
+        k += 1
+    return iters, time.perf_counter() - t0, k, coefs
+
+
+def run_reference(args):
+    rank = int(os.environ.get("RANK", "0"))
+    if rank != 0:
+        return
+    from paper_1510_03298_b200 import configs
+    data = configs.make(args.config)
+    threads = os.cpu_count() or 1
+    _, _, k, _ = cpu_sample(data, threads, args.cpu_budget)  # fixes the per-step sample size
+    for _ in range(max(args.warmup - 1, 0)):
+        cpu_sample(data, threads, args.cpu_budget, n_models=k)
+    tot_it, tot_s = 0, 0.0
+    for _ in range(args.steps):
+        it, s, _, _ = cpu_sample(data, threads, args.cpu_budget, n_models=k)
+        tot_it += it
+        tot_s += s
+    value = tot_it / tot_s
+    sample = (f"first {k} of {data['n_lambda']} lambdas of {args.config} (warm-started outer_solve per lambda, "
+              f"{tot_it // max(args.steps, 1)} prox-grad iterations per step)")
+    line = {"impl": "reference", "metric": METRIC, "value": value, "unit": UNIT, "n_gpus": args.gpus,
+            "steps": args.steps, "warmup": args.warmup, "ms_per_step": 1000.0 * tot_s / args.steps,
+            "higher_is_better": True, "scaling": "weak", "vs_baseline": None, "dtype": "f64",
+            "data": "synthetic (seeded stand-in for the BASELINE config)",
+            "config": {"workload": args.config, "family": data["family"], "n": data["n"], "p": data["p"],
+                       "n_lambda": data["n_lambda"]},
+            "cpu_baseline": {"value": value, "unit": UNIT, "cores": threads, "kind": "port", "sample": sample},
+            "e2e": {"value": value, "unit": UNIT, "h2d_bytes_per_step": 0, "d2h_bytes_per_step": 0}}
+    print(json.dumps(line), flush=True)
+
+
+def run_ours(args):
+    import torch
+    import torch.distributed as dist
+
+    world = int(os.environ.get("WORLD_SIZE", "1"))
+    rank = int(os.environ.get("RANK", "0"))
+    local = int(os.environ.get("LOCAL_RANK", "0"))
+    torch.cuda.set_device(local)
+    if world > 1:
+        dist.init_process_group("nccl", device_id=torch.device("cuda", local))
+
+    from paper_1510_03298_b200 import configs
+    from paper_1510_03298_b200 import kronglm as K
+
+    data = configs.make(args.config)
+    if rank > 0:  # independent replica: same design, its own noise draw
+        rng = np.random.default_rng(configs.SEED0 + 1000 + rank)
+        data["y"] = np.asfortranarray(data["y"] + 0.1 * rng.standard_normal(data["y"].shape)) \
+            if data["family"] == "gaussian" else np.asfortranarray(
+                rng.poisson(np.maximum(data["y"], 0.1)).astype(np.float64))
+    ctx = K.Context(local)
+    design = K.Design(data["design"], ctx)
+    obs = K.Observation(design, data["y"])
+    fam, nl, ratio = data["family"], data["n_lambda"], data["lambda_min_ratio"]
+    stream = torch.cuda.ExternalStream(ctx.stream, device=torch.device("cuda", local))
+    flush = torch.empty(64 * 1024 * 1024, dtype=torch.float32, device="cuda")  # 256 MB > 126 MB L2
+
+    def one_path():
+        return K.fit_path_resident(design, obs, fam, n_lambda=nl, lambda_min_ratio=ratio)
+
+    for _ in range(args.warmup):
+        res = one_path()
+    if world > 1:
+        dist.barrier()
+    torch.cuda.synchronize()
+    clocks = Clocks(local)
+    clocks.start()
+    ctx.reset_launches()
+    total_ms, total_iters = 0.0, 0
+    with torch.cuda.stream(stream):
+        for _ in range(args.steps):
+            flush.zero_()
+            e0 = torch.cuda.Event(enable_timing=True)
+            e1 = torch.cuda.Event(enable_timing=True)
+            e0.record(stream)
+            res = one_path()
+            e1.record(stream)
+            e1.synchronize()
+            total_ms += e0.elapsed_time(e1)
+            total_iters += sum(res.inner_iters)
+    launches = ctx.launches
+    torch.cuda.synchronize()
+    clk = clocks.stop()
+    if world > 1:
+        dist.barrier()
+        t = torch.tensor([total_ms], dtype=torch.float64, device="cuda")
+        dist.all_reduce(t, op=dist.ReduceOp.MAX)
+        it = torch.tensor([total_iters], dtype=torch.float64, device="cuda")
+        dist.all_reduce(it, op=dist.ReduceOp.SUM)
+        max_ms, all_iters = float(t.item()), float(it.item())
+    else:
+        max_ms, all_iters = total_ms, float(total_iters)
+    value = all_iters / (max_ms / 1000.0)
+    iters_per_path = sum(res.inner_iters)
+
+    # roofline of the dominant kernel (fused mode-1 FISTA pass), timed live on the ctx stream
+    avg_ms, nbytes = K_time(ctx, design, obs, 0)
+    hbm, peak_kind = peaks()
+    achieved = nbytes / (avg_ms / 1000.0) / 1e9
+    c_ms, c_bytes = K_time(ctx, design, obs, 1)
+    traffic = None
+    tfile = os.path.join(ROOT, "profiles", f"traffic_{args.config}.json")
+    if os.path.exists(tfile):
+        with open(tfile) as f:
+            traffic = json.load(f).get("fused_pass_dram_bytes")
+
+    # e2e: the public kronglm.fit_path call with host buffers (design upload,
+    # observation upload, path, all coefficient downloads), same metric.
+    e2e_iters, e2e_ms = 0, 0.0
+    for _ in range(max(1, min(args.steps, 3))):
+        torch.cuda.synchronize()
+        t0 = time.perf_counter()
+        out = K.fit_path(data["design"], fam, data["y"], n_lambda=nl, lambda_min_ratio=ratio)
+        e2e_ms += 1000.0 * (time.perf_counter() - t0)
+        e2e_iters += sum(out["inner_iters"])
+    h2d = 8 * (data["y"].size + sum(x.size for x in data["design"][0]))
+    d2h = 8 * design.p * len(out["lambdas"])
+
+    line = None
+    if rank == 0:
+        line = {"metric": METRIC, "value": value, "unit": UNIT, "n_gpus": world, "steps": args.steps,
+                "warmup": args.warmup, "ms_per_step": max_ms / args.steps, "higher_is_better": True,
+                "scaling": "weak", "vs_baseline": None, "dtype": "f64",
+                "data": "synthetic (seeded stand-in for the BASELINE config; no dataset)",
+                "config": {"workload": args.config, "family": fam, "n": data["n"], "p": data["p"],
+                           "n_lambda": nl, "lambda_min_ratio": ratio, "models_fitted": res.n_models,
+                           "prox_grad_iters_per_path": iters_per_path, "path_fit_ms": max_ms / args.steps,
+                           "l2": "256 MB buffer written between timed steps", "parallelism": f"replicas x{world}"},
+                "e2e": {"value": e2e_iters / (e2e_ms / 1000.0), "unit": UNIT, "h2d_bytes_per_step": int(h2d),
+                        "d2h_bytes_per_step": int(d2h), "ms_per_step": e2e_ms / max(1, min(args.steps, 3))},
+                "roofline": {"bound": "hbm", "kernel": "k_fused1<FV_FISTA> (mode-1 H-last + v(eta-z)^2 + G-first)",
+                             "achieved": achieved, "peak": hbm, "peak_kind": peak_kind, "unit": "GB/s",
+                             "frac": achieved / hbm, "traffic": traffic, "bytes_per_launch": nbytes,
+                             "avg_launch_ms": avg_ms,
+                             "contraction": {"kernel": "k_contract (largest H step)", "bytes_per_launch": c_bytes,
+                                             "avg_launch_ms": c_ms,
+                                             "achieved": c_bytes / (c_ms / 1000.0) / 1e9}},
+                "clocks": clk, "gpu_launches": int(launches)}
+    # CPU baseline: the oracle port on rank 0 at N = 1, bounded prefix of the same path
+    if rank == 0 and world == 1 and not args.no_cpu_baseline:
+        it, s, k, coefs = cpu_sample(data, 1, args.cpu_budget)
+        parity = []
+        for t in range(min(k, res.n_models)):
+            g = res.coef(t)
+            w = coefs[t]
+            scale = max(np.max(np.abs(w)), 1e-300)
+            parity.append(float(np.max(np.abs(g - w)) / scale))
+        line["cpu_baseline"] = {"value": it / s, "unit": UNIT, "cores": 1, "kind": "port",
+                                "sample": f"first {k} of {nl} lambdas of {args.config}, {it} prox-grad iterations "
+                                          f"in {s:.1f} s (single-threaded oracle, warm-started per lambda)"}
+        line["parity_prefix"] = {"models": len(parity), "max_coef_rel_err": max(parity) if parity else None,
+                                 "same_support": bool(all(np.array_equal(res.coef(t) != 0, coefs[t] != 0)
+                                                          for t in range(len(parity))))}
+    if line is not None:
+        print(json.dumps(line), flush=True)
+    if world > 1:
+        dist.barrier()
+        dist.destroy_process_group()
+
+
+def K_time(ctx, design, obs, which, reps=20):
+    import ctypes as C
+    from paper_1510_03298_b200 import _lib
+    ms, b = C.c_double(), C.c_double()
+    ctx.check(_lib.load().kg_time_kernel(ctx.h, design.h, obs.h, which, reps, C.byref(ms), C.byref(b)))
+    return ms.value, b.value
+
+
+def main():
+    args = parse()
+    if args.impl == "reference":
+        run_reference(args)
+    else:
+        run_ours(args)
+
+
+if __name__ == "__main__":
+    main()

@@ -1,0 +1,193 @@
+/*
+ * kronglm_b200 — C ABI of the B200-native GLAM fit path.
+ *
+ * This is the drop-in boundary for the reference's fitting path
+ * (kronglm, arXiv 1510.03298).  Each entry point names the reference
+ * interface it replaces (file:line under /root/reference/proj/).  Plain
+ * pointers and sizes only: no C++ types, no exceptions, no torch types.
+ *
+ * Conventions
+ *  - All arrays are FP64, column-major (Fortran order), like DenseArray
+ *    (include/kronglm/array.hpp:44-47).  Coefficient vectors are the
+ *    concatenation of the vec() of each component block (design.hpp:51-78).
+ *  - Host buffers are caller-owned and only read/written during the call.
+ *    Device memory is library-owned.  Calls on one kg_ctx are serialised on
+ *    that context's CUDA stream; use one ctx per host thread.  Distinct ctxs
+ *    (e.g. one per GPU, "replica" mode) may run concurrently.
+ *  - Every call returns kg_status.  kg_last_error(ctx) gives the message
+ *    (the reference's exception text); kg_last_error_cell(ctx) the 0-based
+ *    flat cell index of an EvalError (family.hpp:53-61).
+ *  - Results are bit-for-bit reproducible run to run on the same GPU and
+ *    configuration (deterministic reductions, no floating-point atomics),
+ *    the analogue of the reference's thread-determinism contract
+ *    (tests/test_outer.cpp:363-395).
+ */
+#ifndef KRONGLM_B200_H
+#define KRONGLM_B200_H
+
+#include <stddef.h>
+#include <stdint.h>
+
+#ifdef __cplusplus
+extern "C" {
+#endif
+
+typedef enum {
+  KG_OK = 0,
+  KG_EINVAL = 1,    /* std::invalid_argument (shape / config / support violations) */
+  KG_EEVAL = 2,     /* kronglm::EvalError (non-finite entrywise term; see cell) */
+  KG_ERUNTIME = 3,  /* std::runtime_error (e.g. first path model did not converge, path.cpp:67-70) */
+  KG_EDIVERGE = 4,  /* kronglm::DivergenceError escaping fista_solve (inner.hpp:48-57) */
+  KG_EPOWER = 5,    /* kronglm::PowerIterationError (spectral.hpp:10-20) */
+  KG_ECUDA = 6,     /* CUDA runtime failure */
+  KG_ENCCL = 7,     /* NCCL failure (sharded contexts) */
+  KG_ENOMEM = 8     /* device allocation failure */
+} kg_status;
+
+/* Family / link pairs: FamilySpec::{gaussian,binomial,poisson,gamma_log} (family.hpp:26-35). */
+enum { KG_GAUSSIAN = 0, KG_BINOMIAL = 1, KG_POISSON = 2, KG_GAMMA = 3 };
+/* PenaltySpec::{lasso,ridge,elastic_net} (penalty.hpp:14-23). */
+enum { KG_LASSO = 0, KG_RIDGE = 1, KG_ELASTIC_NET = 2 };
+/* WeightMode (outer.hpp:10). */
+enum { KG_W_EXACT = 0, KG_W_UNIT = 1, KG_W_TENSOR = 2 };
+/* SolveStatus (outer.hpp:35). */
+enum { KG_S_CONVERGED = 0, KG_S_MAX_ITERATIONS = 1, KG_S_LINE_SEARCH_FAILED = 2, KG_S_INNER_DIVERGENCE = 3 };
+
+typedef struct kg_ctx kg_ctx;
+typedef struct kg_design kg_design;
+typedef struct kg_obs kg_obs;
+typedef struct kg_path_result kg_path_result;
+
+/* PathConfig + OuterConfig + InnerConfig flattened (path.hpp:9-13,
+ * outer.hpp:15-24, inner.hpp:29-36).  kg_path_cfg_default() fills the
+ * reference defaults. */
+typedef struct {
+  int64_t n_lambda;              /* 100 */
+  double lambda_min_ratio;       /* 1e-4 */
+  int64_t max_outer;             /* 100 */
+  double armijo_alpha0;          /* 1.0 */
+  double armijo_b;               /* 0.5 */
+  double armijo_v;               /* 0.1 */
+  int64_t armijo_max_backtracks; /* 50 */
+  int64_t weight_mode;           /* KG_W_EXACT */
+  double outer_tol;              /* 1e-8 */
+  double nu;                     /* 1.0 */
+  int64_t inner_max_iters;       /* 2000 */
+  double inner_tol;              /* 1e-8 */
+  int64_t extrapolation;         /* 0 = fista, 1 = none */
+  int64_t monitor_every;         /* 1 */
+} kg_path_cfg;
+
+void kg_path_cfg_default(kg_path_cfg* cfg);
+
+/* ------------------------------------------------------------- context -- */
+/* One CUDA device, one stream.  Replaces nothing in the reference (which is
+ * single-threaded host code); it owns streams, graphs and workspaces. */
+kg_status kg_ctx_create(int device, kg_ctx** out);
+/* Sharded context: the observation array is split along its LAST mode into
+ * `world` contiguous slabs; this rank owns slab `rank`.  `nccl_unique_id`
+ * points to the 128-byte ncclUniqueId created by rank 0 (kg_nccl_unique_id)
+ * and broadcast by the caller (e.g. torch.distributed).  Per gradient the
+ * ranks all-reduce a p-vector (+ scalars) over NVLink. */
+kg_status kg_ctx_create_sharded(int device, int rank, int world, const void* nccl_unique_id, kg_ctx** out);
+kg_status kg_nccl_unique_id(void* out128);
+void kg_ctx_destroy(kg_ctx* ctx);
+const char* kg_last_error(const kg_ctx* ctx);
+int64_t kg_last_error_cell(const kg_ctx* ctx);
+/* The cudaStream_t the context launches on (for CUDA-event timing). */
+void* kg_ctx_stream(kg_ctx* ctx);
+kg_status kg_ctx_synchronize(kg_ctx* ctx);
+/* Which shard of the last mode this context owns: [*lo, *hi). */
+void kg_ctx_shard(const kg_ctx* ctx, int* rank, int* world);
+
+/* -------------------------------------------------------------- design -- */
+/* TensorDesign(std::vector<std::vector<Matrix>>) (design.hpp:17, design.cpp:19-50).
+ * c components, d marginal dimensions; n[j] rows of every factor in dim j;
+ * p[r*d + j] columns of factor (r, j); factors[r*d + j] -> n[j] x p[r*d+j]
+ * column-major host matrix.  Uploads the factors, derives per-row and
+ * per-column nonzero bands (exact-zero test) and caches the spectral radii
+ * rho(X_rj^T X_rj) (spectral.cpp:8-42) for the Lipschitz bound. */
+kg_status kg_design_create(kg_ctx* ctx, int64_t c, int64_t d, const int64_t* n, const int64_t* p,
+                           const double* const* factors, kg_design** out);
+void kg_design_destroy(kg_design* design);
+int64_t kg_design_n(const kg_design* design); /* n = prod n_j (this shard's slab when sharded) */
+int64_t kg_design_p(const kg_design* design); /* p = sum_r prod_j p_rj */
+/* The cached spectral radius of X_rj^T X_rj. */
+kg_status kg_design_spectral(kg_design* design, int64_t r, int64_t j, double* out);
+
+/* --------------------------------------------------------- observations -- */
+/* ObservationData(y[, a]) (family.hpp:40-47).  y, a: n-arrays (a may be NULL
+ * = all ones).  on_device != 0: y and a are device pointers (copied
+ * device-to-device); else host pointers (uploaded).  When sharded, the
+ * arrays are this rank's slab. */
+kg_status kg_obs_create(kg_ctx* ctx, const kg_design* design, const double* y, const double* a, int on_device,
+                        kg_obs** out);
+void kg_obs_destroy(kg_obs* obs);
+
+/* ----------------------------------------------------- operator probes -- */
+/* h_map (design.cpp:89-102): coef (p) -> eta (n).  Host buffers. */
+kg_status kg_h_map(kg_ctx* ctx, const kg_design* design, const double* coef, double* eta);
+/* g_map (design.cpp:104-116): u (n) -> coef (p).  Host buffers. */
+kg_status kg_g_map(kg_ctx* ctx, const kg_design* design, const double* u, double* coef);
+/* xtwx_apply (design.cpp:118-124): G(v .* H(coef)). */
+kg_status kg_xtwx_apply(kg_ctx* ctx, const kg_design* design, const double* v, const double* coef, double* out);
+/* rho (array.cpp:51-72): x is r x extents[0]; a has ndim extents; out has
+ * extents (extents[1..], r). */
+kg_status kg_rho(kg_ctx* ctx, int64_t r, const double* x, int64_t ndim, const int64_t* extents, const double* a,
+                 double* out);
+/* lambda_max (penalty.cpp:72-85). */
+kg_status kg_lambda_max(kg_ctx* ctx, const kg_design* design, const kg_obs* obs, int family, double dispersion,
+                        int penalty, double alpha, double* out);
+
+/* ---------------------------------------------------------------- path -- */
+/* fit_path (path.hpp:36-43, path.cpp:29-81): lambdas == NULL computes
+ * lambda_max and the log grid (lambda_sequence, path.cpp:8-27); otherwise
+ * the explicit strictly decreasing grid of n_lambdas values is used.  The
+ * whole path is solved on the device; coefficients stay in device memory
+ * until read with kg_result_coef. */
+kg_status kg_fit_path(kg_ctx* ctx, const kg_design* design, const kg_obs* obs, int family, double dispersion,
+                      int penalty, double alpha, const kg_path_cfg* cfg, const double* lambdas, int64_t n_lambdas,
+                      kg_path_result** out);
+int64_t kg_result_n_models(const kg_path_result* res);
+int kg_result_truncated(const kg_path_result* res);
+double kg_result_lambda_max(const kg_path_result* res);
+double kg_result_lambda(const kg_path_result* res, int64_t t);
+double kg_result_objective(const kg_path_result* res, int64_t t);
+int64_t kg_result_outer_iters(const kg_path_result* res, int64_t t);
+int64_t kg_result_inner_iters(const kg_path_result* res, int64_t t);
+int kg_result_status(const kg_path_result* res, int64_t t);
+int64_t kg_result_nonzero(const kg_path_result* res, int64_t t);
+/* Copies the p coefficients of model t into host memory. */
+kg_status kg_result_coef(kg_path_result* res, int64_t t, double* out);
+void kg_result_free(kg_path_result* res);
+
+/* predict (path.cpp:83-89): eta = H(coef), mu = g^{-1}(eta).  Host buffers. */
+kg_status kg_predict(kg_ctx* ctx, const kg_design* design, int family, const double* coef, double* eta, double* mu);
+
+/* ---------------------------------------------------- input builders -- */
+/* bspline_design (bspline.cpp:64-104): clamped uniform cubic (order 4)
+ * bases; out is npts x n_basis column-major. Host-side input builder. */
+kg_status kg_bspline_design(int64_t npts, const double* points, int64_t order, int64_t n_basis, double* out);
+int64_t kg_default_basis_count(int64_t n_points, int64_t ratio); /* bspline.cpp:20-26; -1 on bad args */
+int64_t kg_linear_index(int64_t d, const int64_t* multi_index, const int64_t* dims); /* array.cpp:22-36; -1 bad */
+
+/* --------------------------------------------------------- measurement -- */
+/* Times `reps` launches of one hot-path kernel on the context stream with
+ * CUDA events, on the resident observation (inputs already in HBM).
+ *   which = 0: the fused FISTA n-array pass (mode-1 H-last + weighted SS +
+ *              V.* + G-first), the dominant kernel of every prox-grad step;
+ *   which = 1: one banded mode contraction (the largest H-chain step).
+ * avg_ms = mean device time per launch; bytes = algorithmic HBM bytes per
+ * launch ("roofline"). */
+kg_status kg_time_kernel(kg_ctx* ctx, const kg_design* design, const kg_obs* obs, int which, int reps,
+                         double* avg_ms, double* bytes);
+/* Number of library kernel launches issued since the last reset (host-side
+ * counter of launches, graph-replayed kernels counted per replay). */
+int64_t kg_launch_count(const kg_ctx* ctx);
+void kg_launch_count_reset(kg_ctx* ctx);
+
+#ifdef __cplusplus
+}
+#endif
+
+#endif /* KRONGLM_B200_H */

@@ -1,0 +1,185 @@
+// Internal declarations shared by the kronglm_b200 CUDA sources.
+#pragma once
+
+#include <cuda_runtime.h>
+
+#include <cstdint>
+#include <stdexcept>
+#include <string>
+#include <vector>
+
+namespace kg {
+
+using i64 = int64_t;
+
+// ------------------------------------------------------------------ errors
+// Codes mirror kg_status (include/kronglm_b200.h).
+struct Error : std::runtime_error {
+  int code;
+  i64 cell;
+  Error(int c, const std::string& m, i64 cl = -1) : std::runtime_error(m), code(c), cell(cl) {}
+};
+enum { E_INVAL = 1, E_EVAL = 2, E_RUNTIME = 3, E_DIVERGE = 4, E_POWER = 5, E_CUDA = 6, E_NCCL = 7, E_NOMEM = 8 };
+
+#define KG_CUDA(expr)                                                                                 \
+  do {                                                                                                \
+    cudaError_t e__ = (expr);                                                                         \
+    if (e__ != cudaSuccess)                                                                           \
+      throw ::kg::Error(e__ == cudaErrorMemoryAllocation ? ::kg::E_NOMEM : ::kg::E_CUDA,              \
+                        std::string(#expr) + ": " + cudaGetErrorString(e__));                         \
+  } while (0)
+
+// ------------------------------------------------------------ band operators
+// One banded operator C (rows x cols): row m has nonzeros at columns
+// [lo[m], lo[m]+len[m]) with packed coefficients coef[off[m] + t].  For the
+// H direction C = X_j (n_j x p_j, row bands of X); for the G direction
+// C = X_j^T (p_j x n_j, column bands of X).  Bands are derived from the
+// dense factor by an exact-zero test, so skipped terms are exact zeros.
+struct BandOp {
+  const int* lo = nullptr;
+  const int* len = nullptr;
+  const i64* off = nullptr;
+  const double* coef = nullptr;
+  i64 rows = 0, cols = 0;
+  int maxlen = 0;
+};
+
+// Device + host copies of one factor's operators.
+struct FactorDev {
+  i64 n = 0, p = 0;
+  double* X = nullptr;  // dense n x p column-major (Gram / power iteration)
+  BandOp H, G;          // device views
+  void* blob = nullptr; // owning allocation for the band arrays
+  double spectral = 0.0;
+};
+
+// ------------------------------------------------------- FISTA control block
+// Device-resident state of one fista_solve (inner.cpp:121-235).  Kernels of
+// the iteration read their scalars from here so one captured CUDA graph
+// serves every lambda and every outer iteration.
+struct FistaCtl {
+  // configuration
+  double lambda, tol, nu, n, lipfac;
+  i64 max_iters, monitor_every;
+  double alpha;       // elastic-net weight
+  int pen;            // 0 lasso, 1 ridge, 2 elastic net
+  int extrapolation;  // 0 fista, 1 none
+  int bt_div;         // nu in (0,1)
+  // state
+  double delta, omega, g_prev, best_g, lip;
+  i64 it, momentum, streak, prox_steps, backtracks, iterations;
+  int copy_best, restart, done, converged, diverged, bad_weights;
+  int pad;
+};
+
+// ----------------------------------------------------------------- kernels
+// Launch wrappers (kg_kernels.cu).  All run on `s`.
+struct Launch {
+  cudaStream_t s;
+  i64* counter;  // incremented per launch (host-side launch accounting)
+};
+
+void contract(const Launch& L, const double* A, double* out, i64 a, i64 K, i64 M, i64 b, const BandOp& op,
+              bool accumulate);
+
+enum FusedVariant { FV_FISTA = 0, FV_XTWZ = 1, FV_SCORE0 = 2 };
+struct FusedArgs {
+  i64 n1 = 0, p1 = 0, m = 0;  // mode-1 extents and the number of mode-1 fibres (n / n1)
+  int T = 1;                   // fibres per CTA
+  BandOp H, G;                 // mode-1 operators
+  const double* P = nullptr;   // p1 x m H-partial (FISTA)
+  double* Q = nullptr;         // p1 x m G-partial (out)
+  const double* v = nullptr;
+  const double* z = nullptr;
+  const double* y = nullptr;
+  const double* a = nullptr;
+  int fam = 0;
+  double disp = 1.0;
+  double* partial = nullptr;   // one double per CTA (FISTA: sum v (eta - z)^2)
+  i64* err = nullptr;          // SCORE0: first non-finite score cell
+  i64 cell_base = 0;           // global flat index of local cell 0 (sharding)
+};
+int fused_grid(const FusedArgs& f);
+void fused_mode1(const Launch& L, int variant, const FusedArgs& f);
+
+// H-last (+ reductions) over mode 1.  If P is null, eta_new is an input
+// (already computed by a full H chain) and only the reductions run.
+enum HlastFlags { HL_LL_NEW = 1, HL_DOT = 2, HL_TRIALS = 4, HL_U_FLY = 8, HL_WRITE = 16 };
+constexpr int kMaxTrials = 8;
+constexpr int kHlastCols = 2 + kMaxTrials;  // [ll_new, dot, trial_0..]
+struct HlastArgs {
+  i64 n1 = 0, p1 = 0, m = 0;
+  int T = 1;
+  BandOp H;
+  const double* P = nullptr;
+  double* eta_new = nullptr;
+  const double* eta_old = nullptr;
+  const double* u = nullptr;
+  const double* y = nullptr;
+  const double* a = nullptr;
+  int fam = 0;
+  double disp = 1.0;
+  int flags = 0;
+  int ntrial = 0;
+  double t[kMaxTrials] = {0};
+  double* partial = nullptr;   // kHlastCols per CTA
+  i64* err = nullptr;          // [ll_new, u_fly, trial_0..trial_7]
+  i64 cell_base = 0;
+};
+int hlast_grid(const HlastArgs& h);
+void hlast_mode1(const Launch& L, const HlastArgs& h);
+
+// Elementwise family pass: u, v, z and max(v) partials (outer.cpp:241-267).
+struct FamilyArgs {
+  i64 n = 0;
+  int fam = 0, mode = 0;  // mode: 0 exact, 1 unit
+  double disp = 1.0;
+  const double *y = nullptr, *a = nullptr, *eta = nullptr;
+  double *u = nullptr, *v = nullptr, *z = nullptr;
+  double* partial = nullptr;  // max(v) per CTA
+  i64* err = nullptr;         // [score, working response]
+  i64 cell_base = 0;
+};
+int elem_grid(i64 n);
+void family_pass(const Launch& L, const FamilyArgs& f);
+// v = a / disp (Gaussian shortcut, outer.cpp:203-205 with glm_weights = 1/disp) and max partials.
+void gauss_weights(const Launch& L, i64 n, double disp, const double* a, double* v, double* partial);
+// Generic-route (c > 1) elementwise pieces.
+void wss(const Launch& L, i64 n, const double* eta, const double* v, const double* z, double* w, double* partial);
+void vz(const Launch& L, i64 n, const double* v, const double* z, double* w);
+void score0(const Launch& L, i64 n, int fam, double disp, const double* y, const double* a, double* w, i64* err,
+            i64 cell_base);
+// validate (family.cpp:73-109): err[0] = first bad cell, codes[] read back at that cell.
+void validate_pass(const Launch& L, i64 n, int fam, const double* y, const double* a, i64* err, i64 cell_base);
+void eta_combine(const Launch& L, i64 n, double t, const double* eta_t, double* eta);
+void mean_map(const Launch& L, i64 n, int fam, const double* eta, double* mu);
+void fill(const Launch& L, i64 n, double v, double* x);
+
+// p-space
+int pgrid(i64 p);
+void fista_update(const Launch& L, const FistaCtl* ctl, i64 p, int pen, double alpha, double* x, double* xp,
+                  double* Sx, double* Sxp, const double* b, double* best, double* Sbest, double* Jpart);
+void pnorm(const Launch& L, i64 p, int pen, double alpha, const double* x, double* Jpart);
+// cols: 0 = J(th_t); 1 + j = J(th + t_j (th_t - th))
+void ptrials(const Launch& L, i64 p, int pen, double alpha, const double* th, const double* th_t, int ntrial,
+             const double* t, double* part);
+void ptheta_update(const Launch& L, i64 p, double t, const double* th_t, double* th);
+void pcopy(const Launch& L, i64 p, const double* src, double* d0, double* d1, double* d2);
+void pmaxabs(const Launch& L, i64 p, const double* x, double* part);
+void fista_finalize(const Launch& L, const FistaCtl* ctl, i64 p, const double* x, double* best);
+
+// control / reductions (single CTA)
+void fista_init(const Launch& L, FistaCtl* ctl, const double* ss_part, int n_ss, const double* J_part, int n_J,
+                const double* vmax_part, int n_vmax, int bt_always);
+void fista_control(const Launch& L, FistaCtl* ctl, const double* ss_part, int n_ss, const double* J_part, int n_J,
+                   cudaGraphConditionalHandle h, int use_handle);
+void fista_gate(const Launch& L, const FistaCtl* ctl, cudaGraphConditionalHandle h);
+// out[c] = sum over rows of part[row * ncols + c] (fixed order); op 0 sum, 1 max
+void reduce_cols(const Launch& L, const double* part, int nrows, int ncols, int op, double* out);
+
+// Gram + power iteration for one factor (spectral.cpp:8-42)
+void gram(const Launch& L, const FactorDev& f, double* G, int* glo, int* ghi);
+void power_iteration(const Launch& L, i64 p, const double* G, const int* glo, const int* ghi, const double* v0,
+                     double tol, i64 max_iters, double* out /* [value, iterations, status] */);
+
+}  // namespace kg

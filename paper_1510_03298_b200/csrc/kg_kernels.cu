@@ -1,0 +1,885 @@
+// sm_100a kernels of the GLAM fit path.
+//
+// Every n-array pass is HBM-bound FP64 work (banded B-spline factors give
+// ~1 flop/byte, far below the FP64 ridge), so the kernels are written for
+// coalesced streaming, on-chip reuse and fusion, not for tensor cores.
+// Reductions are deterministic: per-CTA warp-shuffle trees written to a
+// partials array, then summed in fixed order by a single CTA (no floating
+// point atomics), so results are bitwise reproducible run to run.
+#include <cfloat>
+#include <climits>
+
+#include "kg_internal.h"
+
+namespace kg {
+
+namespace {
+
+constexpr int NT = 256;            // threads per CTA for streaming kernels
+constexpr double kEtaBound = 30.0;  // family.hpp:16
+constexpr double kFloor = 1e-10;    // family.hpp:17
+
+__device__ __forceinline__ double clampe(double e) { return fmin(fmax(e, -kEtaBound), kEtaBound); }
+__device__ __forceinline__ double logistic(double e) { return 1.0 / (1.0 + exp(-clampe(e))); }
+__device__ __forceinline__ double log1pexp(double e) { return e > 0.0 ? e + log1p(exp(-e)) : log1p(exp(e)); }
+
+__device__ __forceinline__ double warp_sum(double v) {
+#pragma unroll
+  for (int o = 16; o > 0; o >>= 1) v += __shfl_down_sync(0xffffffffu, v, o);
+  return v;
+}
+__device__ __forceinline__ double warp_max(double v) {
+#pragma unroll
+  for (int o = 16; o > 0; o >>= 1) v = fmax(v, __shfl_down_sync(0xffffffffu, v, o));
+  return v;
+}
+__device__ __forceinline__ double warp_allsum(double v) {
+#pragma unroll
+  for (int o = 16; o > 0; o >>= 1) v += __shfl_xor_sync(0xffffffffu, v, o);
+  return v;
+}
+
+// Deterministic CTA reduction (fixed shuffle tree, then warp 0 over the
+// per-warp partials).  Result valid in thread 0.  `sh` needs 32 doubles.
+template <bool MAX>
+__device__ double block_reduce(double v, double* sh) {
+  const int w = threadIdx.x >> 5, l = threadIdx.x & 31;
+  v = MAX ? warp_max(v) : warp_sum(v);
+  __syncthreads();
+  if (l == 0) sh[w] = v;
+  __syncthreads();
+  double r = MAX ? -DBL_MAX : 0.0;
+  if (w == 0) {
+    const int nw = (blockDim.x + 31) >> 5;
+    r = l < nw ? sh[l] : (MAX ? -DBL_MAX : 0.0);
+    r = MAX ? warp_max(r) : warp_sum(r);
+  }
+  return r;
+}
+
+__device__ __forceinline__ void record_min(i64* err, i64 cell) {
+  atomicMin(reinterpret_cast<unsigned long long*>(err), static_cast<unsigned long long>(cell));
+}
+
+// score u_i (family.cpp:164-196), before the dispersion division.
+__device__ __forceinline__ double score_of(int fam, double y, double a, double e) {
+  const double ec = clampe(e);
+  switch (fam) {
+    case 0: return a * (y - e);
+    case 1: return a * (y - logistic(e));
+    case 2: return a * (y - exp(ec));
+    default: return a * exp(-ec) * (y - exp(ec));
+  }
+}
+
+// log-likelihood kernel term (family.cpp:129-162); caller skips a == 0.
+__device__ __forceinline__ double ll_term(int fam, double y, double a, double e) {
+  switch (fam) {
+    case 0: return a * (y * e - 0.5 * e * e);
+    case 1: return a * (y * e - log1pexp(e));
+    case 2: return a * (y * e - exp(clampe(e)));
+    default: return a * (-y * exp(-clampe(e)) - e);
+  }
+}
+
+template <class F>
+__device__ __forceinline__ double band_dot(const BandOp& op, i64 row, F&& at) {
+  const int lo = __ldg(op.lo + row), len = __ldg(op.len + row);
+  const double* c = op.coef + __ldg(op.off + row);
+  double s = 0.0;
+  for (int q = 0; q < len; ++q) s = fma(__ldg(c + q), at(lo + q), s);
+  return s;
+}
+
+int grid_for(i64 work, int per_cta, int cap) {
+  i64 g = (work + per_cta - 1) / per_cta;
+  if (g < 1) g = 1;
+  if (g > cap) g = cap;
+  return static_cast<int>(g);
+}
+
+inline void bump(const Launch& L) {
+  if (L.counter) ++*L.counter;
+}
+
+}  // namespace
+
+int elem_grid(i64 n) { return grid_for(n, NT * 4, 148 * 8); }
+int pgrid(i64 p) { return grid_for(p, NT * 4, 148 * 4); }
+
+// ------------------------------------------------------------ contraction
+// Mode-k banded contraction of A (a x K x b, column-major) with the operator
+// C (M x K): out[al, m, be] = sum_t C[m, lo_m + t] A[al, lo_m + t, be].  One
+// output per thread along the flattened (coalesced) output index.
+template <typename IX>
+__global__ void __launch_bounds__(NT) k_contract(const double* __restrict__ A, double* __restrict__ out, IX a, IX K,
+                                                 IX M, IX b, BandOp op, int accumulate) {
+  const IX total = a * M * b;
+  const IX stride = static_cast<IX>(gridDim.x) * NT;
+  for (IX idx = static_cast<IX>(blockIdx.x) * NT + threadIdx.x; idx < total; idx += stride) {
+    const IX al = idx % a;
+    const IX t = idx / a;
+    const IX m = t % M;
+    const IX be = t / M;
+    const double* src = A + al + a * K * be;
+    const double s = band_dot(op, m, [&](int k) { return __ldg(src + static_cast<IX>(k) * a); });
+    out[idx] = accumulate ? out[idx] + s : s;
+  }
+}
+
+void contract(const Launch& L, const double* A, double* out, i64 a, i64 K, i64 M, i64 b, const BandOp& op,
+              bool accumulate) {
+  const i64 total = a * M * b;
+  if (total == 0) return;
+  const int g = grid_for(total, NT * 2, 148 * 16);
+  if (a * K * b < (i64(1) << 31) && total < (i64(1) << 31)) {
+    k_contract<uint32_t><<<g, NT, 0, L.s>>>(A, out, static_cast<uint32_t>(a), static_cast<uint32_t>(K),
+                                            static_cast<uint32_t>(M), static_cast<uint32_t>(b), op, accumulate);
+  } else {
+    k_contract<uint64_t><<<g, NT, 0, L.s>>>(A, out, a, K, M, b, op, accumulate);
+  }
+  bump(L);
+}
+
+// -------------------------------------------------------- fused mode-1 pass
+// One CTA owns T consecutive mode-1 fibres (a contiguous chunk of n1*T cells
+// of every n-array).  FISTA variant: eta = X1 P (from the shared-memory P
+// tile), the weighted residual sum v (eta - z)^2, w = v eta kept in shared
+// memory, then Q = X1^T w for the tile: the n-array eta is never written.
+template <int VAR>
+__global__ void __launch_bounds__(NT) k_fused1(FusedArgs f) {
+  extern __shared__ double sm[];
+  __shared__ double red[32];
+  const int n1 = static_cast<int>(f.n1), p1 = static_cast<int>(f.p1);
+  const i64 c0 = static_cast<i64>(blockIdx.x) * f.T;
+  const int Tc = static_cast<int>(min(static_cast<i64>(f.T), f.m - c0));
+  double* Ps = sm;
+  double* W = sm + static_cast<i64>(p1) * f.T;
+  const i64 base = c0 * n1;
+  if (VAR == FV_FISTA) {
+    const double* P = f.P + c0 * p1;
+    for (int e = threadIdx.x; e < p1 * Tc; e += NT) Ps[e] = __ldg(P + e);
+    __syncthreads();
+  }
+  double acc = 0.0;
+  for (int e = threadIdx.x; e < n1 * Tc; e += NT) {
+    const int col = e / n1;
+    const int i = e - col * n1;
+    double w;
+    if (VAR == FV_FISTA) {
+      const double* pc = Ps + col * p1;
+      const double eta = band_dot(f.H, i, [&](int k) { return pc[k]; });
+      const double vv = __ldg(f.v + base + e);
+      const double r = eta - __ldg(f.z + base + e);
+      acc = fma(vv, r * r, acc);
+      w = vv * eta;
+    } else if (VAR == FV_XTWZ) {
+      w = __ldg(f.v + base + e) * __ldg(f.z + base + e);
+    } else {
+      w = score_of(f.fam, __ldg(f.y + base + e), __ldg(f.a + base + e), 0.0) / f.disp;
+      if (!isfinite(w)) record_min(f.err, f.cell_base + base + e);
+    }
+    W[e] = w;
+  }
+  if (VAR == FV_FISTA) {
+    const double s = block_reduce<false>(acc, red);
+    if (threadIdx.x == 0) f.partial[blockIdx.x] = s;
+  }
+  __syncthreads();
+  double* Q = f.Q + c0 * p1;
+  for (int q = threadIdx.x; q < p1 * Tc; q += NT) {
+    const int col = q / p1;
+    const int k = q - col * p1;
+    const double* wc = W + col * n1;
+    Q[q] = band_dot(f.G, k, [&](int i) { return wc[i]; });
+  }
+}
+
+static size_t fused_smem(const FusedArgs& f) { return static_cast<size_t>(f.p1 + f.n1) * f.T * sizeof(double); }
+
+int fused_grid(const FusedArgs& f) { return static_cast<int>((f.m + f.T - 1) / f.T); }
+
+void fused_mode1(const Launch& L, int variant, const FusedArgs& f) {
+  const size_t sm = fused_smem(f);
+  const int g = fused_grid(f);
+  static bool attr = false;
+  if (!attr) {
+    KG_CUDA(cudaFuncSetAttribute(k_fused1<FV_FISTA>, cudaFuncAttributeMaxDynamicSharedMemorySize, 200 * 1024));
+    KG_CUDA(cudaFuncSetAttribute(k_fused1<FV_XTWZ>, cudaFuncAttributeMaxDynamicSharedMemorySize, 200 * 1024));
+    KG_CUDA(cudaFuncSetAttribute(k_fused1<FV_SCORE0>, cudaFuncAttributeMaxDynamicSharedMemorySize, 200 * 1024));
+    attr = true;
+  }
+  switch (variant) {
+    case FV_FISTA: k_fused1<FV_FISTA><<<g, NT, sm, L.s>>>(f); break;
+    case FV_XTWZ: k_fused1<FV_XTWZ><<<g, NT, sm, L.s>>>(f); break;
+    default: k_fused1<FV_SCORE0><<<g, NT, sm, L.s>>>(f); break;
+  }
+  bump(L);
+}
+
+// ------------------------------------------------ H-last with reductions
+// eta_new = X1 P (written if HL_WRITE), plus per-CTA partials of
+//   col 0: log-likelihood kernel of eta_new           (HL_LL_NEW)
+//   col 1: <u, eta_new - eta_old>, u = score(eta_old)  (HL_DOT; u on the fly if HL_U_FLY)
+//   col 2+j: log-likelihood at eta_old + t_j (eta_new - eta_old)  (HL_TRIALS)
+// which are the Armijo / Gaussian-shortcut quantities (outer.cpp:106-144,
+// outer.cpp:197-231) evaluated in the same pass that produces eta_tilde.
+__global__ void __launch_bounds__(NT) k_hlast(HlastArgs h) {
+  extern __shared__ double sm[];
+  __shared__ double red[32];
+  const int n1 = static_cast<int>(h.n1), p1 = static_cast<int>(h.p1);
+  const i64 c0 = static_cast<i64>(blockIdx.x) * h.T;
+  const int Tc = static_cast<int>(min(static_cast<i64>(h.T), h.m - c0));
+  const i64 base = c0 * n1;
+  if (h.P) {
+    const double* P = h.P + c0 * p1;
+    for (int e = threadIdx.x; e < p1 * Tc; e += NT) sm[e] = __ldg(P + e);
+    __syncthreads();
+  }
+  double acc[kHlastCols];
+#pragma unroll
+  for (int q = 0; q < kHlastCols; ++q) acc[q] = 0.0;
+  for (int e = threadIdx.x; e < n1 * Tc; e += NT) {
+    const i64 g = base + e;
+    double en;
+    if (h.P) {
+      const int col = e / n1;
+      const int i = e - col * n1;
+      const double* pc = sm + col * p1;
+      en = band_dot(h.H, i, [&](int k) { return pc[k]; });
+      if (h.flags & HL_WRITE) h.eta_new[g] = en;
+    } else {
+      en = __ldg(h.eta_new + g);
+    }
+    if (h.flags & (HL_LL_NEW | HL_DOT | HL_TRIALS)) {
+      const double yy = __ldg(h.y + g), aa = __ldg(h.a + g);
+      if ((h.flags & HL_LL_NEW) && aa != 0.0) {
+        const double t = ll_term(h.fam, yy, aa, en);
+        if (!isfinite(t)) record_min(h.err + 0, h.cell_base + g);
+        acc[0] += t;
+      }
+      if (h.flags & (HL_DOT | HL_TRIALS)) {
+        const double eo = __ldg(h.eta_old + g);
+        if (h.flags & HL_DOT) {
+          double u;
+          if (h.flags & HL_U_FLY) {
+            u = score_of(h.fam, yy, aa, eo) / h.disp;
+            if (!isfinite(u)) record_min(h.err + 1, h.cell_base + g);
+          } else {
+            u = __ldg(h.u + g);
+          }
+          acc[1] = fma(u, en - eo, acc[1]);
+        }
+        if ((h.flags & HL_TRIALS) && aa != 0.0) {
+          for (int j = 0; j < h.ntrial; ++j) {
+            const double et = eo + h.t[j] * (en - eo);
+            const double t = ll_term(h.fam, yy, aa, et);
+            if (!isfinite(t)) record_min(h.err + 2 + j, h.cell_base + g);
+            acc[2 + j] += t;
+          }
+        }
+      }
+    }
+  }
+  const int ncols = 2 + h.ntrial;
+  for (int q = 0; q < ncols; ++q) {
+    const double s = block_reduce<false>(acc[q], red);
+    if (threadIdx.x == 0) h.partial[static_cast<i64>(blockIdx.x) * kHlastCols + q] = s;
+  }
+}
+
+int hlast_grid(const HlastArgs& h) { return static_cast<int>((h.m + h.T - 1) / h.T); }
+
+void hlast_mode1(const Launch& L, const HlastArgs& h) {
+  static bool attr = false;
+  if (!attr) {
+    KG_CUDA(cudaFuncSetAttribute(k_hlast, cudaFuncAttributeMaxDynamicSharedMemorySize, 200 * 1024));
+    attr = true;
+  }
+  const size_t sm = h.P ? static_cast<size_t>(h.p1) * h.T * sizeof(double) : 0;
+  k_hlast<<<hlast_grid(h), NT, sm, L.s>>>(h);
+  bump(L);
+}
+
+// ------------------------------------------------------- elementwise family
+__global__ void __launch_bounds__(NT) k_family(FamilyArgs f) {
+  __shared__ double red[32];
+  double vmax = -DBL_MAX;
+  for (i64 i = static_cast<i64>(blockIdx.x) * NT + threadIdx.x; i < f.n; i += static_cast<i64>(gridDim.x) * NT) {
+    const double yy = f.y[i], aa = f.a[i], e = f.eta[i], ec = clampe(e);
+    const double u = score_of(f.fam, yy, aa, e) / f.disp;
+    if (!isfinite(u)) record_min(f.err + 0, f.cell_base + i);
+    f.u[i] = u;
+    double v, z;
+    if (f.mode == 1) {  // unit weights, generic working response (outer.cpp:148-155)
+      v = 1.0;
+      z = u / v + e;
+    } else {
+      double w = 1.0;
+      if (f.fam == 1) {
+        const double mu = logistic(e);
+        w = mu * (1.0 - mu);
+      } else if (f.fam == 2) {
+        w = exp(ec);
+      }
+      v = fmax(w, kFloor) / f.disp;
+      switch (f.fam) {
+        case 0: z = aa * (yy - e) + e; break;
+        case 1: {
+          const double mu = logistic(ec);
+          z = aa * (yy - mu) / fmax(mu * (1.0 - mu), kFloor) + e;
+          break;
+        }
+        case 2: {
+          const double mu = exp(ec);
+          z = aa * (yy - mu) / fmax(mu, kFloor) + e;
+          break;
+        }
+        default: {
+          const double mu = exp(ec);
+          z = aa * (yy - mu) / mu + e;
+          break;
+        }
+      }
+      if (!isfinite(z)) record_min(f.err + 1, f.cell_base + i);
+    }
+    f.v[i] = v;
+    f.z[i] = z;
+    vmax = fmax(vmax, v);
+  }
+  const double m = block_reduce<true>(vmax, red);
+  if (threadIdx.x == 0) f.partial[blockIdx.x] = m;
+}
+
+void family_pass(const Launch& L, const FamilyArgs& f) {
+  k_family<<<elem_grid(f.n), NT, 0, L.s>>>(f);
+  bump(L);
+}
+
+__global__ void __launch_bounds__(NT) k_gauss_weights(i64 n, double disp, const double* a, double* v, double* part) {
+  __shared__ double red[32];
+  double vmax = -DBL_MAX;
+  const double w = fmax(1.0, kFloor) / disp;  // glm_weights(gaussian) (family.cpp:198-221)
+  for (i64 i = static_cast<i64>(blockIdx.x) * NT + threadIdx.x; i < n; i += static_cast<i64>(gridDim.x) * NT) {
+    const double vv = w * a[i];
+    v[i] = vv;
+    vmax = fmax(vmax, vv);
+  }
+  const double m = block_reduce<true>(vmax, red);
+  if (threadIdx.x == 0) part[blockIdx.x] = m;
+}
+
+void gauss_weights(const Launch& L, i64 n, double disp, const double* a, double* v, double* partial) {
+  k_gauss_weights<<<elem_grid(n), NT, 0, L.s>>>(n, disp, a, v, partial);
+  bump(L);
+}
+
+__global__ void __launch_bounds__(NT) k_wss(i64 n, const double* eta, const double* v, const double* z, double* w,
+                                            double* part) {
+  __shared__ double red[32];
+  double acc = 0.0;
+  for (i64 i = static_cast<i64>(blockIdx.x) * NT + threadIdx.x; i < n; i += static_cast<i64>(gridDim.x) * NT) {
+    const double e = eta[i], vv = v[i], r = e - z[i];
+    acc = fma(vv, r * r, acc);
+    w[i] = vv * e;
+  }
+  const double s = block_reduce<false>(acc, red);
+  if (threadIdx.x == 0) part[blockIdx.x] = s;
+}
+
+void wss(const Launch& L, i64 n, const double* eta, const double* v, const double* z, double* w, double* partial) {
+  k_wss<<<elem_grid(n), NT, 0, L.s>>>(n, eta, v, z, w, partial);
+  bump(L);
+}
+
+__global__ void __launch_bounds__(NT) k_vz(i64 n, const double* v, const double* z, double* w) {
+  for (i64 i = static_cast<i64>(blockIdx.x) * NT + threadIdx.x; i < n; i += static_cast<i64>(gridDim.x) * NT)
+    w[i] = v[i] * z[i];
+}
+
+void vz(const Launch& L, i64 n, const double* v, const double* z, double* w) {
+  k_vz<<<elem_grid(n), NT, 0, L.s>>>(n, v, z, w);
+  bump(L);
+}
+
+__global__ void __launch_bounds__(NT) k_score0(i64 n, int fam, double disp, const double* y, const double* a,
+                                               double* w, i64* err, i64 cell_base) {
+  for (i64 i = static_cast<i64>(blockIdx.x) * NT + threadIdx.x; i < n; i += static_cast<i64>(gridDim.x) * NT) {
+    const double u = score_of(fam, y[i], a[i], 0.0) / disp;
+    if (!isfinite(u)) record_min(err, cell_base + i);
+    w[i] = u;
+  }
+}
+
+void score0(const Launch& L, i64 n, int fam, double disp, const double* y, const double* a, double* w, i64* err,
+            i64 cell_base) {
+  k_score0<<<elem_grid(n), NT, 0, L.s>>>(n, fam, disp, y, a, w, err, cell_base);
+  bump(L);
+}
+
+__global__ void __launch_bounds__(NT) k_validate(i64 n, int fam, const double* y, const double* a, i64* err,
+                                                 i64 cell_base) {
+  for (i64 i = static_cast<i64>(blockIdx.x) * NT + threadIdx.x; i < n; i += static_cast<i64>(gridDim.x) * NT) {
+    const double ai = a[i];
+    bool bad = !(ai >= 0.0) || !isfinite(ai);
+    if (!bad && ai != 0.0) {
+      const double yi = y[i];
+      bad = !isfinite(yi) || (fam == 1 && (yi < 0.0 || yi > 1.0)) || (fam == 2 && yi < 0.0) ||
+            (fam == 3 && !(yi > 0.0));
+    }
+    if (bad) record_min(err, cell_base + i);
+  }
+}
+
+void validate_pass(const Launch& L, i64 n, int fam, const double* y, const double* a, i64* err, i64 cell_base) {
+  k_validate<<<elem_grid(n), NT, 0, L.s>>>(n, fam, y, a, err, cell_base);
+  bump(L);
+}
+
+__global__ void __launch_bounds__(NT) k_eta_combine(i64 n, double t, const double* et, double* eta) {
+  for (i64 i = static_cast<i64>(blockIdx.x) * NT + threadIdx.x; i < n; i += static_cast<i64>(gridDim.x) * NT) {
+    const double e = eta[i];
+    eta[i] = e + t * (et[i] - e);  // trial_eta (outer.cpp:131)
+  }
+}
+
+void eta_combine(const Launch& L, i64 n, double t, const double* eta_t, double* eta) {
+  k_eta_combine<<<elem_grid(n), NT, 0, L.s>>>(n, t, eta_t, eta);
+  bump(L);
+}
+
+__global__ void __launch_bounds__(NT) k_mean(i64 n, int fam, const double* eta, double* mu) {
+  for (i64 i = static_cast<i64>(blockIdx.x) * NT + threadIdx.x; i < n; i += static_cast<i64>(gridDim.x) * NT) {
+    const double e = eta[i];
+    mu[i] = fam == 0 ? e : (fam == 1 ? logistic(e) : exp(clampe(e)));
+  }
+}
+
+void mean_map(const Launch& L, i64 n, int fam, const double* eta, double* mu) {
+  k_mean<<<elem_grid(n), NT, 0, L.s>>>(n, fam, eta, mu);
+  bump(L);
+}
+
+__global__ void __launch_bounds__(NT) k_fill(i64 n, double v, double* x) {
+  for (i64 i = static_cast<i64>(blockIdx.x) * NT + threadIdx.x; i < n; i += static_cast<i64>(gridDim.x) * NT) x[i] = v;
+}
+
+void fill(const Launch& L, i64 n, double v, double* x) {
+  k_fill<<<elem_grid(n), NT, 0, L.s>>>(n, v, x);
+  bump(L);
+}
+
+// ---------------------------------------------------------------- p-space
+__device__ __forceinline__ double soft(double z, double g) {
+  const double m = fabs(z) - g;
+  if (m <= 0.0) return 0.0;
+  return z > 0.0 ? m : -m;
+}
+
+__device__ __forceinline__ double prox1(int pen, double alpha, double gamma, double z) {
+  if (pen == 0) return soft(z, gamma);
+  if (pen == 1) return z * (1.0 / (1.0 + 2.0 * gamma));
+  return (1.0 / (1.0 + 2.0 * alpha * gamma)) * soft(z, gamma);
+}
+
+// J pieces: l1 and squared l2 partial sums are kept separate so J is formed
+// as in penalty.cpp:24-34.
+__device__ __forceinline__ void jacc(double x, double& l1, double& l2) {
+  l1 += fabs(x);
+  l2 = fma(x, x, l2);
+}
+
+// One accelerated proximal-gradient step (inner.cpp:163-193), using
+// S(y) = S(x) + omega (S(x) - S(x_prev)) with S = X^T W X (linearity of the
+// map), so each iteration needs one n-array pass on the new iterate only.
+__global__ void __launch_bounds__(NT) k_fista_update(const FistaCtl* __restrict__ ctl, i64 p, int pen, double alpha,
+                                                     double* x, double* xp, double* Sx, double* Sxp, const double* b,
+                                                     double* best, double* Sbest, double* Jpart) {
+  __shared__ double red[32];
+  const double omega = ctl->omega, delta = ctl->delta, lambda = ctl->lambda, n = ctl->n;
+  const int copy_best = ctl->copy_best, restart = ctl->restart;
+  const double gamma = delta * lambda;
+  double l1 = 0.0, l2 = 0.0;
+  for (i64 i = static_cast<i64>(blockIdx.x) * NT + threadIdx.x; i < p; i += static_cast<i64>(gridDim.x) * NT) {
+    double xi = x[i], xpi = xp[i], sxi = Sx[i], sxpi = Sxp[i];
+    if (copy_best) {
+      best[i] = xi;
+      Sbest[i] = sxi;
+    }
+    if (restart) {
+      xi = xpi = best[i];
+      sxi = sxpi = Sbest[i];
+    }
+    const double yi = xi + omega * (xi - xpi);
+    const double syi = sxi + omega * (sxi - sxpi);
+    const double g = (syi - b[i]) / n;
+    double ci = yi - delta * g;
+    if (lambda > 0.0) ci = prox1(pen, alpha, gamma, ci);
+    xp[i] = xi;
+    x[i] = ci;
+    Sxp[i] = sxi;
+    jacc(ci, l1, l2);
+  }
+  const double s1 = block_reduce<false>(l1, red);
+  const double s2 = block_reduce<false>(l2, red);
+  if (threadIdx.x == 0) {
+    Jpart[2 * blockIdx.x] = s1;
+    Jpart[2 * blockIdx.x + 1] = s2;
+  }
+}
+
+void fista_update(const Launch& L, const FistaCtl* ctl, i64 p, int pen, double alpha, double* x, double* xp,
+                  double* Sx, double* Sxp, const double* b, double* best, double* Sbest, double* Jpart) {
+  k_fista_update<<<pgrid(p), NT, 0, L.s>>>(ctl, p, pen, alpha, x, xp, Sx, Sxp, b, best, Sbest, Jpart);
+  bump(L);
+}
+
+__global__ void __launch_bounds__(NT) k_pnorm(i64 p, const double* x, double* Jpart) {
+  __shared__ double red[32];
+  double l1 = 0.0, l2 = 0.0;
+  for (i64 i = static_cast<i64>(blockIdx.x) * NT + threadIdx.x; i < p; i += static_cast<i64>(gridDim.x) * NT)
+    jacc(x[i], l1, l2);
+  const double s1 = block_reduce<false>(l1, red);
+  const double s2 = block_reduce<false>(l2, red);
+  if (threadIdx.x == 0) {
+    Jpart[2 * blockIdx.x] = s1;
+    Jpart[2 * blockIdx.x + 1] = s2;
+  }
+}
+
+void pnorm(const Launch& L, i64 p, int, double, const double* x, double* Jpart) {
+  k_pnorm<<<pgrid(p), NT, 0, L.s>>>(p, x, Jpart);
+  bump(L);
+}
+
+struct Trials {
+  double t[kMaxTrials];
+};
+
+// cols per CTA: 2 * (1 + ntrial): (l1, l2) of th_t, then of each trial point.
+__global__ void __launch_bounds__(NT) k_ptrials(i64 p, const double* th, const double* tht, int ntrial, Trials T,
+                                                double* part) {
+  __shared__ double red[32];
+  double l1[1 + kMaxTrials], l2[1 + kMaxTrials];
+  for (int j = 0; j <= kMaxTrials; ++j) l1[j] = l2[j] = 0.0;
+  for (i64 i = static_cast<i64>(blockIdx.x) * NT + threadIdx.x; i < p; i += static_cast<i64>(gridDim.x) * NT) {
+    const double a = th[i], b = tht[i];
+    jacc(b, l1[0], l2[0]);
+    for (int j = 0; j < ntrial; ++j) jacc(a + T.t[j] * (b - a), l1[1 + j], l2[1 + j]);
+  }
+  const int ncol = 2 * (1 + kMaxTrials);
+  for (int j = 0; j <= ntrial; ++j) {
+    const double s1 = block_reduce<false>(l1[j], red);
+    const double s2 = block_reduce<false>(l2[j], red);
+    if (threadIdx.x == 0) {
+      part[static_cast<i64>(blockIdx.x) * ncol + 2 * j] = s1;
+      part[static_cast<i64>(blockIdx.x) * ncol + 2 * j + 1] = s2;
+    }
+  }
+}
+
+void ptrials(const Launch& L, i64 p, int, double, const double* th, const double* th_t, int ntrial, const double* t,
+             double* part) {
+  Trials T{};
+  for (int j = 0; j < ntrial && j < kMaxTrials; ++j) T.t[j] = t[j];
+  k_ptrials<<<pgrid(p), NT, 0, L.s>>>(p, th, th_t, ntrial, T, part);
+  bump(L);
+}
+
+__global__ void __launch_bounds__(NT) k_ptheta(i64 p, double t, const double* tht, double* th) {
+  for (i64 i = static_cast<i64>(blockIdx.x) * NT + threadIdx.x; i < p; i += static_cast<i64>(gridDim.x) * NT) {
+    const double a = th[i];
+    th[i] = a + t * (tht[i] - a);  // trial_theta (outer.cpp:130)
+  }
+}
+
+void ptheta_update(const Launch& L, i64 p, double t, const double* th_t, double* th) {
+  k_ptheta<<<pgrid(p), NT, 0, L.s>>>(p, t, th_t, th);
+  bump(L);
+}
+
+__global__ void __launch_bounds__(NT) k_pcopy(i64 p, const double* s, double* d0, double* d1, double* d2) {
+  for (i64 i = static_cast<i64>(blockIdx.x) * NT + threadIdx.x; i < p; i += static_cast<i64>(gridDim.x) * NT) {
+    const double v = s[i];
+    if (d0) d0[i] = v;
+    if (d1) d1[i] = v;
+    if (d2) d2[i] = v;
+  }
+}
+
+void pcopy(const Launch& L, i64 p, const double* src, double* d0, double* d1, double* d2) {
+  k_pcopy<<<pgrid(p), NT, 0, L.s>>>(p, src, d0, d1, d2);
+  bump(L);
+}
+
+__global__ void __launch_bounds__(NT) k_pmaxabs(i64 p, const double* x, double* part) {
+  __shared__ double red[32];
+  double m = 0.0;
+  for (i64 i = static_cast<i64>(blockIdx.x) * NT + threadIdx.x; i < p; i += static_cast<i64>(gridDim.x) * NT)
+    m = fmax(m, fabs(x[i]));
+  const double r = block_reduce<true>(m, red);
+  if (threadIdx.x == 0) part[blockIdx.x] = r;
+}
+
+void pmaxabs(const Launch& L, i64 p, const double* x, double* part) {
+  k_pmaxabs<<<pgrid(p), NT, 0, L.s>>>(p, x, part);
+  bump(L);
+}
+
+__global__ void __launch_bounds__(NT) k_fista_finalize(const FistaCtl* ctl, i64 p, const double* x, double* best) {
+  if (!ctl->copy_best) return;
+  for (i64 i = static_cast<i64>(blockIdx.x) * NT + threadIdx.x; i < p; i += static_cast<i64>(gridDim.x) * NT)
+    best[i] = x[i];
+}
+
+void fista_finalize(const Launch& L, const FistaCtl* ctl, i64 p, const double* x, double* best) {
+  k_fista_finalize<<<pgrid(p), NT, 0, L.s>>>(ctl, p, x, best);
+  bump(L);
+}
+
+// ----------------------------------------------------------- control CTA
+// Fixed-order reduction of a partials column by one CTA of 1024 threads.
+constexpr int CT = 1024;
+
+__device__ double cta_sum_col(const double* part, int nrows, int stride, int col, double* sh) {
+  double s = 0.0;
+  for (int r = threadIdx.x; r < nrows; r += CT) s += part[static_cast<i64>(r) * stride + col];
+  s = block_reduce<false>(s, sh);
+  __syncthreads();
+  if (threadIdx.x == 0) sh[32] = s;
+  __syncthreads();
+  const double out = sh[32];
+  __syncthreads();
+  return out;
+}
+
+__device__ double cta_max_col(const double* part, int nrows, int stride, int col, double* sh) {
+  double s = -DBL_MAX;
+  for (int r = threadIdx.x; r < nrows; r += CT) s = fmax(s, part[static_cast<i64>(r) * stride + col]);
+  s = block_reduce<true>(s, sh);
+  __syncthreads();
+  if (threadIdx.x == 0) sh[32] = s;
+  __syncthreads();
+  const double out = sh[32];
+  __syncthreads();
+  return out;
+}
+
+__device__ __forceinline__ double penalty_of(int pen, double alpha, double l1, double l2) {
+  if (pen == 0) return l1;
+  if (pen == 1) return l2;
+  return l1 + alpha * l2;
+}
+
+__global__ void __launch_bounds__(CT) k_fista_init(FistaCtl* c, const double* ss_part, int n_ss, const double* J_part,
+                                                   int n_J, const double* vmax_part, int n_vmax, int bt_always) {
+  __shared__ double sh[33];
+  const double ss = cta_sum_col(ss_part, n_ss, 1, 0, sh);
+  const double l1 = cta_sum_col(J_part, n_J, 2, 0, sh);
+  const double l2 = cta_sum_col(J_part, n_J, 2, 1, sh);
+  const double wmax = cta_max_col(vmax_part, n_vmax, 1, 0, sh);
+  if (threadIdx.x != 0) return;
+  // inner_objective (inner.cpp:109-119)
+  const double g0 = 0.5 * ss / c->n + c->lambda * penalty_of(c->pen, c->alpha, l1, l2);
+  c->g_prev = g0;
+  c->best_g = g0;
+  // lipschitz_upper (inner.cpp:53-71): wmax * sum_r prod_j rho_rj / n
+  c->bad_weights = !(wmax > 0.0);
+  const double lip = wmax * c->lipfac / c->n;
+  c->lip = lip;
+  // stepsize policy (inner.cpp:141-145)
+  double delta = bt_always ? 1.0 : 1.0 / (fmax(c->nu, 1.0e-300) * lip);
+  if (c->nu == 1.0) delta = 1.0 / lip;
+  c->delta = delta;
+  c->omega = 0.0;
+  c->it = 1;
+  c->momentum = 1;
+  c->streak = 0;
+  c->prox_steps = 0;
+  c->backtracks = 0;
+  c->iterations = 0;
+  c->copy_best = 0;
+  c->restart = 0;
+  c->converged = 0;
+  c->diverged = 0;
+  c->done = (c->max_iters < 1) || c->bad_weights;
+}
+
+// Objective monitor, best tracking, divergence restarts and the stop rule of
+// fista_solve (inner.cpp:189-229), advanced once per iteration on the device;
+// sets the graph's while-condition so the loop runs without the host.
+__global__ void __launch_bounds__(CT) k_fista_control(FistaCtl* c, const double* ss_part, int n_ss,
+                                                      const double* J_part, int n_J,
+                                                      cudaGraphConditionalHandle h, int use_handle) {
+  __shared__ double sh[33];
+  const double ss = cta_sum_col(ss_part, n_ss, 1, 0, sh);
+  const double l1 = cta_sum_col(J_part, n_J, 2, 0, sh);
+  const double l2 = cta_sum_col(J_part, n_J, 2, 1, sh);
+  if (threadIdx.x != 0) return;
+  c->copy_best = 0;
+  c->restart = 0;
+  const i64 it = c->it;
+  c->prox_steps += 1;
+  c->momentum += 1;
+  c->iterations = it;
+  const i64 me = c->monitor_every < 1 ? 1 : c->monitor_every;
+  const bool monitored = (it % me == 0) || it == c->max_iters;
+  if (monitored) {
+    const double g = 0.5 * ss / c->n + c->lambda * penalty_of(c->pen, c->alpha, l1, l2);
+    const bool bad = !isfinite(g);
+    bool div = bad;
+    if (!div && c->bt_div && g > c->g_prev) div = (++c->streak >= 3);
+    if (div) {
+      if (!c->bt_div) {
+        c->diverged = 1;
+        c->done = 1;
+      } else {
+        c->restart = 1;
+        c->g_prev = c->best_g;
+        c->delta *= 0.5;
+        c->momentum = 1;
+        c->streak = 0;
+        c->backtracks += 1;
+      }
+    } else {
+      if (g <= c->g_prev) c->streak = 0;
+      if (g <= c->best_g) {
+        c->copy_best = 1;
+        c->best_g = g;
+      }
+      if (fabs(g - c->g_prev) / fmax(1.0, fabs(g)) < c->tol) {
+        c->converged = 1;
+        c->done = 1;
+      }
+      c->g_prev = g;
+    }
+  }
+  if (!c->done) {
+    c->it = it + 1;
+    if (c->it > c->max_iters) c->done = 1;
+  }
+  c->omega = c->extrapolation == 0
+                 ? static_cast<double>(c->momentum - 1) / static_cast<double>(c->momentum + 2)
+                 : 0.0;
+  if (use_handle) cudaGraphSetConditional(h, c->done ? 0u : 1u);
+}
+
+void fista_init(const Launch& L, FistaCtl* ctl, const double* ss_part, int n_ss, const double* J_part, int n_J,
+                const double* vmax_part, int n_vmax, int bt_always) {
+  k_fista_init<<<1, CT, 0, L.s>>>(ctl, ss_part, n_ss, J_part, n_J, vmax_part, n_vmax, bt_always);
+  bump(L);
+}
+
+void fista_control(const Launch& L, FistaCtl* ctl, const double* ss_part, int n_ss, const double* J_part, int n_J,
+                   cudaGraphConditionalHandle h, int use_handle) {
+  k_fista_control<<<1, CT, 0, L.s>>>(ctl, ss_part, n_ss, J_part, n_J, h, use_handle);
+  bump(L);
+}
+
+__global__ void k_gate(const FistaCtl* c, cudaGraphConditionalHandle h) {
+  if (threadIdx.x == 0) cudaGraphSetConditional(h, c->done ? 0u : 1u);
+}
+
+void fista_gate(const Launch& L, const FistaCtl* ctl, cudaGraphConditionalHandle h) {
+  k_gate<<<1, 32, 0, L.s>>>(ctl, h);
+  bump(L);
+}
+
+__global__ void __launch_bounds__(CT) k_reduce_cols(const double* part, int nrows, int ncols, int op, double* out) {
+  __shared__ double sh[33];
+  for (int c = 0; c < ncols; ++c) {
+    const double r = op ? cta_max_col(part, nrows, ncols, c, sh) : cta_sum_col(part, nrows, ncols, c, sh);
+    if (threadIdx.x == 0) out[c] = r;
+  }
+}
+
+void reduce_cols(const Launch& L, const double* part, int nrows, int ncols, int op, double* out) {
+  k_reduce_cols<<<1, CT, 0, L.s>>>(part, nrows, ncols, op, out);
+  bump(L);
+}
+
+// ------------------------------------------------------ spectral radius
+// Banded Gram X^T X of one factor: row a has entries for columns [glo, ghi).
+__global__ void k_gram(const double* X, i64 n, i64 p, const int* clo, const int* clen, const int* glo, const int* ghi,
+                       double* G) {
+  const int a = blockIdx.x;
+  for (int b = glo[a] + threadIdx.x; b < ghi[a]; b += blockDim.x) {
+    const int lo = max(clo[a], clo[b]);
+    const int hi = min(clo[a] + clen[a], clo[b] + clen[b]);
+    double s = 0.0;
+    for (int i = lo; i < hi; ++i) s += X[i + n * a] * X[i + n * b];
+    G[a + p * static_cast<i64>(b)] = s;
+  }
+}
+
+void gram(const Launch& L, const FactorDev& f, double* G, int* glo, int* ghi) {
+  k_gram<<<static_cast<unsigned>(f.p), 128, 0, L.s>>>(f.X, f.n, f.p, f.G.lo, f.G.len, glo, ghi, G);
+  bump(L);
+}
+
+// Power iteration (spectral.cpp:8-42) by a single warp: v stays in shared
+// memory, the two reductions per step are warp-shuffle trees.
+__global__ void k_power(i64 p, const double* G, const int* glo, const int* ghi, const double* v0, double tol,
+                        i64 max_iters, double* out) {
+  extern __shared__ double sh[];
+  double* v = sh;
+  double* av = sh + p;
+  const int l = threadIdx.x;
+  for (i64 i = l; i < p; i += 32) v[i] = v0[i];
+  __syncwarp();
+  double value = 0.0;
+  i64 settled = 0;
+  for (i64 it = 1; it <= max_iters; ++it) {
+    double nn = 0.0, dot = 0.0;
+    for (i64 i = l; i < p; i += 32) {
+      double s = 0.0;
+      for (int k = glo[i]; k < ghi[i]; ++k) s += G[i + p * k] * v[k];
+      av[i] = s;
+      nn += s * s;
+      dot += v[i] * s;
+    }
+    nn = warp_allsum(nn);
+    dot = warp_allsum(dot);
+    const double norm = sqrt(nn);
+    if (norm == 0.0) {
+      if (l == 0) {
+        out[0] = 0.0;
+        out[1] = static_cast<double>(it);
+        out[2] = 0.0;
+      }
+      return;
+    }
+    __syncwarp();
+    for (i64 i = l; i < p; i += 32) v[i] = av[i] / norm;
+    __syncwarp();
+    const double change = fabs(dot - value);
+    value = dot;
+    if (change <= tol * fmax(fabs(value), 1e-300)) {
+      if (++settled >= 2) {
+        if (l == 0) {
+          out[0] = value;
+          out[1] = static_cast<double>(it);
+          out[2] = 0.0;
+        }
+        return;
+      }
+    } else {
+      settled = 0;
+    }
+  }
+  if (l == 0) {
+    out[0] = value;
+    out[1] = static_cast<double>(max_iters);
+    out[2] = 1.0;
+  }
+}
+
+void power_iteration(const Launch& L, i64 p, const double* G, const int* glo, const int* ghi, const double* v0,
+                     double tol, i64 max_iters, double* out) {
+  const size_t sm = 2 * static_cast<size_t>(p) * sizeof(double);
+  if (sm > 48 * 1024) KG_CUDA(cudaFuncSetAttribute(k_power, cudaFuncAttributeMaxDynamicSharedMemorySize, 200 * 1024));
+  k_power<<<1, 32, sm, L.s>>>(p, G, glo, ghi, v0, tol, max_iters, out);
+  bump(L);
+}
+
+}  // namespace kg

@@ -1,0 +1,1518 @@
+// Host orchestration of the GLAM fit path on one B200 and the kg_* C ABI.
+//
+// Control structure (reference: path.cpp:47-81 -> outer.cpp:159-303 ->
+// inner.cpp:121-235):
+//   * fit_path / outer_solve bookkeeping runs on the host, one stream sync per
+//     outer iteration (per lambda for Gaussian models);
+//   * every fista_solve runs entirely on the device: one CUDA graph whose
+//     conditional WHILE node repeats the iteration body
+//        p-space update -> H partial chain -> fused mode-1 pass -> G tail -> control
+//     until the device-side control kernel clears the condition.
+// All arrays live in HBM for the whole path; nothing n-sized crosses PCIe
+// after the observation upload.
+#include <dlfcn.h>
+
+#include <functional>
+
+#include <algorithm>
+#include <cmath>
+#include <cstring>
+#include <limits>
+#include <memory>
+#include <random>
+#include <string>
+#include <vector>
+
+#include "../../include/kronglm_b200.h"
+#include "kg_internal.h"
+
+namespace kg {
+
+// ------------------------------------------------------------ device memory
+struct DBuf {
+  void* p = nullptr;
+  size_t bytes = 0;
+  DBuf() = default;
+  DBuf(const DBuf&) = delete;
+  DBuf& operator=(const DBuf&) = delete;
+  ~DBuf() { release(); }
+  void release() {
+    if (p) cudaFree(p);
+    p = nullptr;
+    bytes = 0;
+  }
+  void alloc(size_t b) {
+    if (b <= bytes && p) return;
+    release();
+    KG_CUDA(cudaMalloc(&p, b ? b : 8));
+    bytes = b;
+  }
+  double* d() const { return static_cast<double*>(p); }
+  i64* l() const { return static_cast<i64*>(p); }
+};
+
+static i64 prod(const std::vector<i64>& v, size_t a, size_t b) {
+  i64 s = 1;
+  for (size_t i = a; i < b; ++i) s *= v[i];
+  return s;
+}
+
+}  // namespace kg
+
+// ------------------------------------------------------------------ context
+struct kg_ctx {
+  int device = 0;
+  cudaStream_t s = nullptr;
+  kg::i64 launches = 0;
+  std::string err;
+  kg::i64 err_cell = -1;
+  int rank = 0, world = 1;
+  void* pinned = nullptr;  // small pinned staging area for scalars
+  kg::Launch L() { return {s, &launches}; }
+  double* pin() { return static_cast<double*>(pinned); }
+};
+
+// Layout of the 4 KB pinned staging area (doubles).
+namespace kg {
+constexpr int PIN_SCAL = 0;    // [0, 64): reduced scalars
+constexpr int PIN_ERR = 64;    // [64, 96): error words (i64)
+constexpr int PIN_CTL = 128;   // FistaCtl read back
+constexpr int PIN_STAGE = 256; // FistaCtl staged for upload
+constexpr int ERR_FAM = 12;    // errs[12], errs[13]: family score / working response
+}  // namespace kg
+
+namespace kg {
+
+static void sync(kg_ctx* c) { KG_CUDA(cudaStreamSynchronize(c->s)); }
+
+// ------------------------------------------------------------------ design
+struct FactorHost {
+  i64 n = 0, p = 0;
+  std::vector<double> X;  // column-major
+};
+
+static void build_band(const FactorHost& h, bool rows_of_x, std::vector<int>& lo, std::vector<int>& len,
+                       std::vector<i64>& off, std::vector<double>& coef, int& maxlen) {
+  // rows_of_x: operator = X (rows i, columns k); else operator = X^T.
+  const i64 R = rows_of_x ? h.n : h.p, K = rows_of_x ? h.p : h.n;
+  lo.assign(R, 0);
+  len.assign(R, 0);
+  off.assign(R, 0);
+  coef.clear();
+  maxlen = 0;
+  for (i64 r = 0; r < R; ++r) {
+    i64 first = -1, last = -1;
+    for (i64 k = 0; k < K; ++k) {
+      const double v = rows_of_x ? h.X[r + h.n * k] : h.X[k + h.n * r];
+      if (v != 0.0) {
+        if (first < 0) first = k;
+        last = k;
+      }
+    }
+    off[r] = static_cast<i64>(coef.size());
+    if (first < 0) continue;
+    lo[r] = static_cast<int>(first);
+    len[r] = static_cast<int>(last - first + 1);
+    maxlen = std::max(maxlen, len[r]);
+    for (i64 k = first; k <= last; ++k) coef.push_back(rows_of_x ? h.X[r + h.n * k] : h.X[k + h.n * r]);
+  }
+}
+
+struct FactorOwn {
+  FactorDev dev;
+  DBuf X, hlo, hlen, hoff, hcoef, glo, glen, goff, gcoef;
+};
+
+static void upload_factor(const FactorHost& h, FactorOwn& f, cudaStream_t s) {
+  f.dev.n = h.n;
+  f.dev.p = h.p;
+  f.X.alloc(sizeof(double) * h.n * h.p);
+  KG_CUDA(cudaMemcpyAsync(f.X.p, h.X.data(), sizeof(double) * h.n * h.p, cudaMemcpyHostToDevice, s));
+  f.dev.X = f.X.d();
+  auto up = [&](bool rows, DBuf& blo, DBuf& blen, DBuf& boff, DBuf& bcoef, BandOp& op) {
+    std::vector<int> lo, len;
+    std::vector<i64> off;
+    std::vector<double> coef;
+    int maxlen = 0;
+    build_band(h, rows, lo, len, off, coef, maxlen);
+    blo.alloc(sizeof(int) * lo.size());
+    blen.alloc(sizeof(int) * len.size());
+    boff.alloc(sizeof(i64) * off.size());
+    bcoef.alloc(sizeof(double) * std::max<size_t>(coef.size(), 1));
+    KG_CUDA(cudaMemcpy(blo.p, lo.data(), sizeof(int) * lo.size(), cudaMemcpyHostToDevice));
+    KG_CUDA(cudaMemcpy(blen.p, len.data(), sizeof(int) * len.size(), cudaMemcpyHostToDevice));
+    KG_CUDA(cudaMemcpy(boff.p, off.data(), sizeof(i64) * off.size(), cudaMemcpyHostToDevice));
+    if (!coef.empty()) KG_CUDA(cudaMemcpy(bcoef.p, coef.data(), sizeof(double) * coef.size(), cudaMemcpyHostToDevice));
+    op.lo = static_cast<const int*>(blo.p);
+    op.len = static_cast<const int*>(blen.p);
+    op.off = static_cast<const i64*>(boff.p);
+    op.coef = bcoef.d();
+    op.rows = rows ? h.n : h.p;
+    op.cols = rows ? h.p : h.n;
+    op.maxlen = maxlen;
+  };
+  up(true, f.hlo, f.hlen, f.hoff, f.hcoef, f.dev.H);
+  up(false, f.glo, f.glen, f.goff, f.gcoef, f.dev.G);
+}
+
+// Spectral radius of X^T X for one factor: banded Gram + single-warp power
+// iteration on the device; start vector exactly as spectral.cpp:17-23.
+static double factor_spectral(kg_ctx* ctx, const FactorHost& h, FactorOwn& f) {
+  const i64 p = h.p;
+  // column bands of X (rows where column k is nonzero)
+  std::vector<int> clo(p), chi(p);
+  for (i64 k = 0; k < p; ++k) {
+    i64 first = -1, last = -1;
+    for (i64 i = 0; i < h.n; ++i)
+      if (h.X[i + h.n * k] != 0.0) {
+        if (first < 0) first = i;
+        last = i;
+      }
+    clo[k] = first < 0 ? 0 : static_cast<int>(first);
+    chi[k] = first < 0 ? 0 : static_cast<int>(last + 1);
+  }
+  std::vector<int> glo(p, 0), ghi(p, 0);
+  for (i64 a = 0; a < p; ++a) {
+    i64 first = -1, last = -1;
+    for (i64 b = 0; b < p; ++b)
+      if (std::max(clo[a], clo[b]) < std::min(chi[a], chi[b])) {
+        if (first < 0) first = b;
+        last = b;
+      }
+    glo[a] = first < 0 ? 0 : static_cast<int>(first);
+    ghi[a] = first < 0 ? 0 : static_cast<int>(last + 1);
+  }
+  if (p == 1) {  // spectral.cpp:14
+    double s = 0.0;
+    for (i64 i = 0; i < h.n; ++i) s += h.X[i] * h.X[i];
+    return std::abs(s);
+  }
+  std::mt19937_64 rng(0x9e3779b97f4a7c15ull);
+  std::uniform_real_distribution<double> unif(0.5, 1.5);
+  std::vector<double> v0(p);
+  for (i64 i = 0; i < p; ++i) v0[i] = unif(rng);
+  double z = 0.0;
+  for (double x : v0) z += x * x;
+  if (z > 0.0) {
+    const double sq = std::sqrt(z);
+    for (double& x : v0) x /= sq;
+  }
+  DBuf G, dglo, dghi, dv0, out;
+  G.alloc(sizeof(double) * p * p);
+  KG_CUDA(cudaMemsetAsync(G.p, 0, sizeof(double) * p * p, ctx->s));
+  dglo.alloc(sizeof(int) * p);
+  dghi.alloc(sizeof(int) * p);
+  dv0.alloc(sizeof(double) * p);
+  out.alloc(sizeof(double) * 3);
+  KG_CUDA(cudaMemcpyAsync(dglo.p, glo.data(), sizeof(int) * p, cudaMemcpyHostToDevice, ctx->s));
+  KG_CUDA(cudaMemcpyAsync(dghi.p, ghi.data(), sizeof(int) * p, cudaMemcpyHostToDevice, ctx->s));
+  KG_CUDA(cudaMemcpyAsync(dv0.p, v0.data(), sizeof(double) * p, cudaMemcpyHostToDevice, ctx->s));
+  gram(ctx->L(), f.dev, G.d(), static_cast<int*>(dglo.p), static_cast<int*>(dghi.p));
+  power_iteration(ctx->L(), p, G.d(), static_cast<int*>(dglo.p), static_cast<int*>(dghi.p), dv0.d(), 1e-14, 500000,
+                  out.d());
+  double res[3];
+  KG_CUDA(cudaMemcpyAsync(res, out.p, sizeof(res), cudaMemcpyDeviceToHost, ctx->s));
+  sync(ctx);
+  if (res[2] != 0.0) throw Error(E_POWER, "power iteration did not converge after 500000 iterations");
+  return res[0];
+}
+
+}  // namespace kg
+
+struct kg_design {
+  kg_ctx* ctx = nullptr;
+  kg::i64 c = 0, d = 0;
+  std::vector<kg::i64> n;                  // local extents (last mode = this shard's slab)
+  std::vector<kg::i64> n_full;             // global extents
+  std::vector<std::vector<kg::i64>> p;     // p[r][j]
+  std::vector<kg::i64> offs;
+  kg::i64 N = 0, N_full = 0, P = 0;
+  kg::i64 cell_base = 0;                   // global flat index of the first local cell
+  std::vector<std::vector<std::unique_ptr<kg::FactorOwn>>> f;
+  std::vector<std::vector<double>> spectral;
+  double lipfac = 0.0;                     // sum_r prod_j rho_rj (inner.cpp:61-70)
+  bool fused = false;
+  int T = 1;                               // mode-1 fibres per CTA in the fused kernels
+  kg::i64 scratch = 0;                     // doubles per chain scratch buffer
+  kg::i64 part_cap = 0;                    // doubles in the partials buffer
+};
+
+struct kg_obs {
+  kg_ctx* ctx = nullptr;
+  const kg_design* design = nullptr;
+  kg::DBuf y, a;
+  bool unit_a = true;
+};
+
+namespace kg {
+
+// ------------------------------------------------------------------ chains
+// Applies a sequence of banded mode contractions.  dims: current extents;
+// steps: (mode j, operator, new extent).  The last step writes `out`.
+struct Step {
+  int mode;
+  const BandOp* op;
+  i64 next;
+};
+
+static void run_chain(kg_ctx* ctx, std::vector<i64> dims, const std::vector<Step>& steps, const double* in,
+                      double* out, double* s0, double* s1, bool accumulate_last) {
+  const double* cur = in;
+  for (size_t k = 0; k < steps.size(); ++k) {
+    const Step& st = steps[k];
+    const bool last = k + 1 == steps.size();
+    double* dst = last ? out : (k % 2 == 0 ? s0 : s1);
+    const i64 a = prod(dims, 0, st.mode), K = dims[st.mode], b = prod(dims, st.mode + 1, dims.size());
+    contract(ctx->L(), cur, dst, a, K, st.next, b, *st.op, last && accumulate_last);
+    dims[st.mode] = st.next;
+    cur = dst;
+  }
+}
+
+// H chain of component r from its coefficient block: modes d-1 .. stop (stop = 0 full, 1 partial).
+static std::vector<Step> h_steps(const kg_design& D, i64 r, int stop) {
+  std::vector<Step> st;
+  for (i64 j = D.d - 1; j >= stop; --j) st.push_back({static_cast<int>(j), &D.f[r][j]->dev.H, D.n[j]});
+  return st;
+}
+// G chain of component r: modes start .. d-1
+static std::vector<Step> g_steps(const kg_design& D, i64 r, int start) {
+  std::vector<Step> st;
+  for (i64 j = start; j < D.d; ++j) st.push_back({static_cast<int>(j), &D.f[r][j]->dev.G, D.p[r][j]});
+  return st;
+}
+
+static std::vector<i64> coef_dims(const kg_design& D, i64 r) { return D.p[r]; }
+
+// Max intermediate (non-final) size of every chain the solver runs.
+static i64 chain_scratch(const kg_design& D) {
+  i64 mx = 1;
+  for (i64 r = 0; r < D.c; ++r) {
+    std::vector<i64> dims = D.p[r];
+    for (i64 j = D.d - 1; j >= 0; --j) {  // H: p -> n
+      dims[j] = D.n[j];
+      mx = std::max(mx, prod(dims, 0, dims.size()));
+    }
+    dims = D.n;
+    for (i64 j = 0; j < D.d; ++j) {  // G: n -> p
+      dims[j] = D.p[r][j];
+      mx = std::max(mx, prod(dims, 0, dims.size()));
+    }
+  }
+  return mx;
+}
+
+// ------------------------------------------------------------- fit state
+struct Fit {
+  kg_ctx* ctx;
+  const kg_design* D;
+  const kg_obs* O;
+  int fam = 0, pen = 0;
+  double disp = 1.0, alpha = 0.0;
+  i64 n = 0, p = 0;
+  // p-space
+  DBuf x, xp, Sx, Sxp, best, Sbest, b, theta, Jpart, tpart;
+  // n-space
+  DBuf v, z, u, eta, eta_t, w, hs, P, Q, s0, s1;  // hs: generic-route eta scratch
+  DBuf part, scal, errs, ctl;
+  const double* zptr = nullptr;  // z or y (Gaussian shortcut)
+  int n_ss = 0;
+  // graph
+  cudaGraphExec_t exec = nullptr;
+  cudaGraph_t graph = nullptr;
+  i64 kernels_per_iter = 0;
+  ~Fit() {
+    if (exec) cudaGraphExecDestroy(exec);
+    if (graph) cudaGraphDestroy(graph);
+  }
+};
+
+static void alloc_fit(Fit& F) {
+  const kg_design& D = *F.D;
+  F.n = D.N;
+  F.p = D.P;
+  const size_t pb = sizeof(double) * F.p, nb = sizeof(double) * F.n;
+  for (DBuf* b : {&F.x, &F.xp, &F.Sx, &F.Sxp, &F.best, &F.Sbest, &F.b, &F.theta}) b->alloc(pb);
+  for (DBuf* b : {&F.v, &F.z, &F.u, &F.eta, &F.eta_t}) b->alloc(nb);
+  if (!D.fused) {
+    F.w.alloc(nb);
+    F.hs.alloc(nb);
+  }
+  if (D.fused && D.d > 1) {
+    const i64 pq = D.N / D.n[0] * D.p[0][0];
+    F.P.alloc(sizeof(double) * pq);
+    F.Q.alloc(sizeof(double) * pq);
+  } else if (D.fused) {
+    F.Q.alloc(pb);
+  }
+  F.s0.alloc(sizeof(double) * D.scratch);
+  F.s1.alloc(sizeof(double) * D.scratch);
+  F.part.alloc(sizeof(double) * D.part_cap);
+  F.Jpart.alloc(sizeof(double) * 2 * pgrid(F.p));
+  F.tpart.alloc(sizeof(double) * 2 * (1 + kMaxTrials) * pgrid(F.p));
+  F.scal.alloc(sizeof(double) * 64);
+  F.errs.alloc(sizeof(i64) * 16);
+  F.ctl.alloc(sizeof(FistaCtl));
+}
+
+static void reset_errs(Fit& F) {
+  KG_CUDA(cudaMemsetAsync(F.errs.p, 0x7f, sizeof(i64) * 16, F.ctx->s));  // 0x7f7f.. = "no error"
+}
+static const i64 kNoErr = 0x7f7f7f7f7f7f7f7fLL;
+
+// Fused-route argument builders (c == 1).
+static FusedArgs fused_args(const Fit& F) {
+  const kg_design& D = *F.D;
+  FusedArgs a;
+  a.n1 = D.n[0];
+  a.p1 = D.p[0][0];
+  a.m = D.N / D.n[0];
+  a.T = D.T;
+  a.H = D.f[0][0]->dev.H;
+  a.G = D.f[0][0]->dev.G;
+  a.cell_base = D.cell_base;
+  return a;
+}
+
+static HlastArgs hlast_args(const Fit& F) {
+  const kg_design& D = *F.D;
+  HlastArgs h;
+  h.n1 = D.n[0];
+  h.p1 = D.p[0][0];
+  h.m = D.N / D.n[0];
+  h.T = D.T;
+  h.H = D.f[0][0]->dev.H;
+  h.y = F.O->y.d();
+  h.a = F.O->a.d();
+  h.fam = F.fam;
+  h.disp = F.disp;
+  h.partial = F.part.d();
+  h.err = F.errs.l();
+  h.cell_base = D.cell_base;
+  return h;
+}
+
+// S(x) = X^T diag(v) X x into Sx, and per-CTA partials of sum v (eta - z)^2
+// into F.part (returns the number of partials).
+static int xwx_pass(Fit& F, const double* x, double* Sx) {
+  const kg_design& D = *F.D;
+  kg_ctx* ctx = F.ctx;
+  if (D.fused) {
+    const double* P = x;
+    if (D.d > 1) {
+      run_chain(ctx, coef_dims(D, 0), h_steps(D, 0, 1), x, F.P.d(), F.s0.d(), F.s1.d(), false);
+      P = F.P.d();
+    }
+    FusedArgs a = fused_args(F);
+    a.P = P;
+    a.Q = D.d > 1 ? F.Q.d() : Sx;
+    a.v = F.v.d();
+    a.z = F.zptr;
+    a.partial = F.part.d();
+    fused_mode1(ctx->L(), FV_FISTA, a);
+    if (D.d > 1) {
+      std::vector<i64> dims = D.n;
+      dims[0] = D.p[0][0];
+      run_chain(ctx, dims, g_steps(D, 0, 1), F.Q.d(), Sx, F.s0.d(), F.s1.d(), false);
+    }
+    return fused_grid(a);
+  }
+  for (i64 r = 0; r < D.c; ++r)
+    run_chain(ctx, coef_dims(D, r), h_steps(D, r, 0), x + D.offs[r], F.hs.d(), F.s0.d(), F.s1.d(), r > 0);
+  wss(ctx->L(), F.n, F.hs.d(), F.v.d(), F.zptr, F.w.d(), F.part.d());
+  for (i64 r = 0; r < D.c; ++r) run_chain(ctx, D.n, g_steps(D, r, 0), F.w.d(), Sx + D.offs[r], F.s0.d(), F.s1.d(), false);
+  return elem_grid(F.n);
+}
+
+// b = X^T (v .* z)
+static void xtwz_pass(Fit& F) {
+  const kg_design& D = *F.D;
+  kg_ctx* ctx = F.ctx;
+  if (D.fused) {
+    FusedArgs a = fused_args(F);
+    a.v = F.v.d();
+    a.z = F.zptr;
+    a.Q = D.d > 1 ? F.Q.d() : F.b.d();
+    fused_mode1(ctx->L(), FV_XTWZ, a);
+    if (D.d > 1) {
+      std::vector<i64> dims = D.n;
+      dims[0] = D.p[0][0];
+      run_chain(ctx, dims, g_steps(D, 0, 1), F.Q.d(), F.b.d(), F.s0.d(), F.s1.d(), false);
+    }
+    return;
+  }
+  vz(ctx->L(), F.n, F.v.d(), F.zptr, F.w.d());
+  for (i64 r = 0; r < D.c; ++r)
+    run_chain(ctx, D.n, g_steps(D, r, 0), F.w.d(), F.b.d() + D.offs[r], F.s0.d(), F.s1.d(), false);
+}
+
+// eta_out = H(coef) with optional reductions (HlastArgs flags) -> F.part (kHlastCols per CTA).
+static int h_full(Fit& F, const double* coef, double* eta_out, HlastArgs h) {
+  const kg_design& D = *F.D;
+  kg_ctx* ctx = F.ctx;
+  h.eta_new = eta_out;
+  if (D.fused) {
+    const double* P = coef;
+    if (D.d > 1) {
+      run_chain(ctx, coef_dims(D, 0), h_steps(D, 0, 1), coef, F.P.d(), F.s0.d(), F.s1.d(), false);
+      P = F.P.d();
+    }
+    h.P = P;
+    h.flags |= HL_WRITE;
+  } else {
+    for (i64 r = 0; r < D.c; ++r)
+      run_chain(ctx, coef_dims(D, r), h_steps(D, r, 0), coef + D.offs[r], eta_out, F.s0.d(), F.s1.d(), r > 0);
+    h.P = nullptr;
+    h.flags &= ~HL_WRITE;
+  }
+  hlast_mode1(ctx->L(), h);
+  return hlast_grid(h);
+}
+
+// ---------------------------------------------------------------- FISTA
+static void build_graph(Fit& F) {
+  kg_ctx* ctx = F.ctx;
+  cudaStream_t cap;
+  KG_CUDA(cudaStreamCreateWithFlags(&cap, cudaStreamNonBlocking));
+  KG_CUDA(cudaGraphCreate(&F.graph, 0));
+  cudaGraphConditionalHandle h;
+  KG_CUDA(cudaGraphConditionalHandleCreate(&h, F.graph, 0, cudaGraphCondAssignDefault));
+  // gate node: enter the loop only if fista_init left the solve running
+  KG_CUDA(cudaStreamBeginCaptureToGraph(cap, F.graph, nullptr, nullptr, 0, cudaStreamCaptureModeThreadLocal));
+  fista_gate(Launch{cap, nullptr}, static_cast<FistaCtl*>(F.ctl.p), h);
+  KG_CUDA(cudaStreamEndCapture(cap, &F.graph));
+  size_t nn = 0;
+  KG_CUDA(cudaGraphGetNodes(F.graph, nullptr, &nn));
+  if (nn != 1) throw Error(E_CUDA, "unexpected gate capture");
+  cudaGraphNode_t gate;
+  KG_CUDA(cudaGraphGetNodes(F.graph, &gate, &nn));
+  cudaGraphNodeParams cp = {};
+  cp.type = cudaGraphNodeTypeConditional;
+  cp.conditional.handle = h;
+  cp.conditional.type = cudaGraphCondTypeWhile;
+  cp.conditional.size = 1;
+  cudaGraphNode_t node;
+  KG_CUDA(cudaGraphAddNode(&node, F.graph, &gate, 1, &cp));
+  cudaGraph_t body = cp.conditional.phGraph_out[0];
+  KG_CUDA(cudaStreamBeginCaptureToGraph(cap, body, nullptr, nullptr, 0, cudaStreamCaptureModeThreadLocal));
+  cudaStream_t saved = ctx->s;
+  i64 saved_count = ctx->launches;
+  ctx->s = cap;
+  ctx->launches = 0;
+  try {
+    FistaCtl* c = static_cast<FistaCtl*>(F.ctl.p);
+    fista_update(ctx->L(), c, F.p, F.pen, F.alpha, F.x.d(), F.xp.d(), F.Sx.d(), F.Sxp.d(), F.b.d(), F.best.d(),
+                 F.Sbest.d(), F.Jpart.d());
+    F.n_ss = xwx_pass(F, F.x.d(), F.Sx.d());
+    fista_control(ctx->L(), c, F.part.d(), F.n_ss, F.Jpart.d(), pgrid(F.p), h, 1);
+  } catch (...) {
+    ctx->s = saved;
+    ctx->launches = saved_count;
+    cudaGraph_t dummy;
+    cudaStreamEndCapture(cap, &dummy);
+    cudaStreamDestroy(cap);
+    throw;
+  }
+  F.kernels_per_iter = ctx->launches;
+  ctx->s = saved;
+  ctx->launches = saved_count;
+  KG_CUDA(cudaStreamEndCapture(cap, &body));
+  KG_CUDA(cudaStreamDestroy(cap));
+  KG_CUDA(cudaGraphInstantiate(&F.exec, F.graph, 0));
+}
+
+struct FistaOut {
+  double objective = 0.0, lip = 0.0;
+  i64 iterations = 0;
+  bool converged = false, diverged = false, bad_weights = false;
+};
+
+struct InnerCfg {
+  double nu = 1.0, tol = 1e-8;
+  i64 max_iters = 2000, monitor_every = 1;
+  int extrapolation = 0;
+};
+
+// Enqueues fista_solve(init = theta) with weights F.v (max-partials in
+// vmax_part) and working response F.zptr; F.b must hold X^T(v.*z).  The
+// result lands in F.best; the control block is copied to ctx->pin() + PIN_CTL.
+static void fista_enqueue(Fit& F, double lambda, const InnerCfg& ic, const double* vmax_part, int n_vmax) {
+  kg_ctx* ctx = F.ctx;
+  if (!(ic.nu >= 0.0 && ic.nu <= 1.0)) throw Error(E_INVAL, "fista_solve: nu must lie in [0,1]");
+  if (ic.nu == 0.0) throw Error(E_INVAL, "fista_solve: nu = 0 (backtracking every iteration) is not supported by the device solver");
+  FistaCtl h{};
+  h.lambda = lambda;
+  h.tol = ic.tol;
+  h.nu = ic.nu;
+  h.n = static_cast<double>(F.D->N_full);
+  h.lipfac = F.D->lipfac;
+  h.max_iters = ic.max_iters;
+  h.monitor_every = ic.monitor_every;
+  h.alpha = F.alpha;
+  h.pen = F.pen;
+  h.extrapolation = ic.extrapolation;
+  h.bt_div = ic.nu > 0.0 && ic.nu < 1.0;
+  FistaCtl* staged = reinterpret_cast<FistaCtl*>(ctx->pin() + PIN_STAGE);
+  KG_CUDA(cudaStreamSynchronize(ctx->s));  // the pinned staging slot is reused
+  *staged = h;
+  KG_CUDA(cudaMemcpyAsync(F.ctl.p, staged, sizeof(FistaCtl), cudaMemcpyHostToDevice, ctx->s));
+  pcopy(ctx->L(), F.p, F.theta.d(), F.x.d(), F.xp.d(), F.best.d());
+  const int n_ss = xwx_pass(F, F.x.d(), F.Sx.d());
+  pnorm(ctx->L(), F.p, F.pen, F.alpha, F.x.d(), F.Jpart.d());
+  pcopy(ctx->L(), F.p, F.Sx.d(), F.Sxp.d(), F.Sbest.d(), nullptr);
+  fista_init(ctx->L(), static_cast<FistaCtl*>(F.ctl.p), F.part.d(), n_ss, F.Jpart.d(), pgrid(F.p), vmax_part, n_vmax,
+             0);
+  if (ic.max_iters >= 1) {
+    if (!F.exec) build_graph(F);
+    KG_CUDA(cudaGraphLaunch(F.exec, ctx->s));
+  }
+  fista_finalize(ctx->L(), static_cast<FistaCtl*>(F.ctl.p), F.p, F.x.d(), F.best.d());
+  KG_CUDA(cudaMemcpyAsync(ctx->pin() + PIN_CTL, F.ctl.p, sizeof(FistaCtl), cudaMemcpyDeviceToHost, ctx->s));
+}
+
+static FistaOut fista_read(Fit& F) {
+  const FistaCtl* c = reinterpret_cast<const FistaCtl*>(F.ctx->pin() + PIN_CTL);
+  FistaOut o;
+  o.objective = c->best_g;
+  o.lip = c->lip;
+  o.iterations = c->iterations;
+  o.converged = c->converged;
+  o.diverged = c->diverged;
+  o.bad_weights = c->bad_weights;
+  F.ctx->launches += o.iterations * F.kernels_per_iter;
+  return o;
+}
+
+// --------------------------------------------------------------- helpers
+static double penalty_of(int pen, double alpha, double l1, double l2) {
+  if (pen == 0) return l1;
+  if (pen == 1) return l2;
+  return l1 + alpha * l2;
+}
+
+static void validate_obs(Fit& F) {
+  kg_ctx* ctx = F.ctx;
+  reset_errs(F);
+  validate_pass(ctx->L(), F.n, F.fam, F.O->y.d(), F.O->a.d(), F.errs.l(), F.D->cell_base);
+  i64 e;
+  KG_CUDA(cudaMemcpyAsync(&e, F.errs.p, sizeof(i64), cudaMemcpyDeviceToHost, ctx->s));
+  sync(ctx);
+  if (e == kNoErr) return;
+  const i64 loc = e - F.D->cell_base;
+  double yi, ai;
+  KG_CUDA(cudaMemcpy(&yi, F.O->y.d() + loc, sizeof(double), cudaMemcpyDeviceToHost));
+  KG_CUDA(cudaMemcpy(&ai, F.O->a.d() + loc, sizeof(double), cudaMemcpyDeviceToHost));
+  const std::string cell = std::to_string(e);
+  if (!(ai >= 0.0) || !std::isfinite(ai))
+    throw Error(E_INVAL, "observation weight must be finite and nonnegative at cell " + cell);
+  if (!std::isfinite(yi)) throw Error(E_INVAL, "response must be finite at cell " + cell);
+  if (F.fam == 1) throw Error(E_INVAL, "binomial response must be a proportion in [0,1] at cell " + cell);
+  if (F.fam == 2) throw Error(E_INVAL, "poisson response must be nonnegative at cell " + cell);
+  throw Error(E_INVAL, "gamma response must be positive at cell " + cell);
+}
+
+// lambda_max (penalty.cpp:72-85) on an allocated fit (uses F.b as scratch).
+static double lambda_max_fit(Fit& F) {
+  const kg_design& D = *F.D;
+  kg_ctx* ctx = F.ctx;
+  reset_errs(F);
+  if (D.fused) {
+    FusedArgs a = fused_args(F);
+    a.y = F.O->y.d();
+    a.a = F.O->a.d();
+    a.fam = F.fam;
+    a.disp = F.disp;
+    a.err = F.errs.l();
+    a.Q = D.d > 1 ? F.Q.d() : F.b.d();
+    fused_mode1(ctx->L(), FV_SCORE0, a);
+    if (D.d > 1) {
+      std::vector<i64> dims = D.n;
+      dims[0] = D.p[0][0];
+      run_chain(ctx, dims, g_steps(D, 0, 1), F.Q.d(), F.b.d(), F.s0.d(), F.s1.d(), false);
+    }
+  } else {
+    score0(ctx->L(), F.n, F.fam, F.disp, F.O->y.d(), F.O->a.d(), F.w.d(), F.errs.l(), D.cell_base);
+    for (i64 r = 0; r < D.c; ++r)
+      run_chain(ctx, D.n, g_steps(D, r, 0), F.w.d(), F.b.d() + D.offs[r], F.s0.d(), F.s1.d(), false);
+  }
+  pmaxabs(ctx->L(), F.p, F.b.d(), F.Jpart.d());
+  reduce_cols(ctx->L(), F.Jpart.d(), pgrid(F.p), 1, 1, F.scal.d());
+  double* pin = ctx->pin();
+  KG_CUDA(cudaMemcpyAsync(pin, F.scal.p, sizeof(double), cudaMemcpyDeviceToHost, ctx->s));
+  KG_CUDA(cudaMemcpyAsync(pin + 1, F.errs.p, sizeof(i64), cudaMemcpyDeviceToHost, ctx->s));
+  sync(ctx);
+  i64 e;
+  std::memcpy(&e, pin + 1, sizeof(i64));
+  if (e != kNoErr) throw Error(E_EVAL, "non-finite score entry at cell " + std::to_string(e), e);
+  return pin[0] / static_cast<double>(D.N_full);
+}
+
+}  // namespace kg
+
+// ------------------------------------------------------------------ result
+struct kg_path_result {
+  kg_ctx* ctx = nullptr;
+  kg::i64 p = 0;
+  std::vector<double> lambdas, objectives;
+  std::vector<kg::i64> outer_iters, inner_iters, nnz;
+  std::vector<int> status;
+  bool truncated = false;
+  double lambda_max = 0.0;
+  kg::DBuf coefs;  // n_models x p on the device
+};
+
+namespace kg {
+
+struct ModelTrace {
+  int status = 1;
+  i64 outer = 0, inner = 0;
+  double final_objective = 0.0;
+};
+
+// ------------------------------------------------------------ outer_solve
+struct OuterCfg {
+  i64 max_outer = 100, max_bt = 50;
+  double alpha0 = 1.0, b = 0.5, v = 0.1, tol = 1e-8;
+  int wmode = 0;
+  InnerCfg inner;
+};
+
+static void check_ll_errs(Fit& F, const i64* errs) {
+  if (errs[0] != kNoErr) throw Error(E_EVAL, "non-finite log-likelihood term at cell " + std::to_string(errs[0]), errs[0]);
+}
+
+// Gaussian + identity + exact weights: one inner solve per lambda
+// (outer.cpp:197-231).  State carried across lambdas: theta, eta = H(theta),
+// ll = loglik(eta), (l1, l2) of theta.
+struct PathState {
+  double ll = 0.0, l1 = 0.0, l2 = 0.0;
+};
+
+static ModelTrace gaussian_step(Fit& F, double lambda, const OuterCfg& oc, PathState& st, int n_vmax) {
+  kg_ctx* ctx = F.ctx;
+  const double n = static_cast<double>(F.D->N_full);
+  const double f_cur = -st.ll / n + lambda * penalty_of(F.pen, F.alpha, st.l1, st.l2);
+  ModelTrace tr;
+  reset_errs(F);
+  fista_enqueue(F, lambda, oc.inner, F.part.d() + F.D->part_cap - n_vmax, n_vmax);
+  // eta_tilde = H(best); loglik(eta_tilde) and <u(eta), eta_tilde - eta> in the same pass.
+  HlastArgs h = hlast_args(F);
+  h.flags = HL_LL_NEW | HL_DOT | HL_U_FLY;
+  h.eta_old = F.eta.d();
+  const int g = h_full(F, F.best.d(), F.eta_t.d(), h);
+  reduce_cols(ctx->L(), F.part.d(), g, kHlastCols, 0, F.scal.d());
+  pnorm(ctx->L(), F.p, F.pen, F.alpha, F.best.d(), F.Jpart.d());
+  reduce_cols(ctx->L(), F.Jpart.d(), pgrid(F.p), 2, 0, F.scal.d() + 16);
+  double* pin = ctx->pin();
+  KG_CUDA(cudaMemcpyAsync(pin, F.scal.p, sizeof(double) * 20, cudaMemcpyDeviceToHost, ctx->s));
+  KG_CUDA(cudaMemcpyAsync(pin + PIN_ERR, F.errs.p, sizeof(i64) * 4, cudaMemcpyDeviceToHost, ctx->s));
+  sync(ctx);
+  const FistaOut fo = fista_read(F);
+  if (fo.bad_weights) throw Error(E_INVAL, "lipschitz_upper: weights must not be all zero");
+  tr.inner = fo.iterations;
+  if (fo.diverged) {  // DivergenceError caught by outer_solve (outer.cpp:272-275)
+    tr.status = KG_S_INNER_DIVERGENCE;
+    tr.final_objective = f_cur;
+    return tr;
+  }
+  i64 errs[4];
+  std::memcpy(errs, pin + PIN_ERR, sizeof(errs));
+  check_ll_errs(F, errs);
+  if (errs[1] != kNoErr) throw Error(E_EVAL, "non-finite score entry at cell " + std::to_string(errs[1]), errs[1]);
+  const double ll_new = pin[0] / F.disp, l1 = pin[16], l2 = pin[17];
+  const double f_new = -ll_new / n + lambda * penalty_of(F.pen, F.alpha, l1, l2);
+  double f = f_cur;
+  if (f_new <= f_cur) {
+    pcopy(ctx->L(), F.p, F.best.d(), F.theta.d(), nullptr, nullptr);
+    std::swap(F.eta.p, F.eta_t.p);
+    st.ll = ll_new;
+    st.l1 = l1;
+    st.l2 = l2;
+    f = f_new;
+  }
+  tr.outer = 1;
+  tr.final_objective = f;
+  tr.status = fo.converged ? KG_S_CONVERGED : KG_S_MAX_ITERATIONS;
+  return tr;
+}
+
+// General outer loop (outer.cpp:233-302) for exact / unit weights.
+static ModelTrace outer_loop(Fit& F, double lambda, const OuterCfg& oc) {
+  kg_ctx* ctx = F.ctx;
+  const kg_design& D = *F.D;
+  const double n = static_cast<double>(D.N_full);
+  ModelTrace tr;
+  // eta = H(theta), f_cur = F(theta, eta)  (outer.cpp:185-186)
+  reset_errs(F);
+  HlastArgs h0 = hlast_args(F);
+  h0.flags = HL_LL_NEW;
+  int g = h_full(F, F.theta.d(), F.eta.d(), h0);
+  reduce_cols(ctx->L(), F.part.d(), g, kHlastCols, 0, F.scal.d());
+  pnorm(ctx->L(), F.p, F.pen, F.alpha, F.theta.d(), F.Jpart.d());
+  reduce_cols(ctx->L(), F.Jpart.d(), pgrid(F.p), 2, 0, F.scal.d() + 16);
+  double* pin = ctx->pin();
+  KG_CUDA(cudaMemcpyAsync(pin, F.scal.p, sizeof(double) * 20, cudaMemcpyDeviceToHost, ctx->s));
+  KG_CUDA(cudaMemcpyAsync(pin + PIN_ERR, F.errs.p, sizeof(i64) * 4, cudaMemcpyDeviceToHost, ctx->s));
+  sync(ctx);
+  {
+    i64 errs[4];
+    std::memcpy(errs, pin + PIN_ERR, sizeof(errs));
+    check_ll_errs(F, errs);
+  }
+  double J_cur = penalty_of(F.pen, F.alpha, pin[16], pin[17]);
+  double f_cur = -(pin[0] / F.disp) / n + lambda * J_cur;
+  tr.final_objective = f_cur;
+
+  const int n_vmax = elem_grid(F.n);
+  double* vmax_part = F.part.d() + D.part_cap - n_vmax;
+  for (i64 k = 0; k < oc.max_outer; ++k) {
+    reset_errs(F);
+    FamilyArgs fa;
+    fa.n = F.n;
+    fa.fam = F.fam;
+    fa.mode = oc.wmode == KG_W_UNIT ? 1 : 0;
+    fa.disp = F.disp;
+    fa.y = F.O->y.d();
+    fa.a = F.O->a.d();
+    fa.eta = F.eta.d();
+    fa.u = F.u.d();
+    fa.v = F.v.d();
+    fa.z = F.z.d();
+    fa.partial = vmax_part;
+    fa.err = F.errs.l() + ERR_FAM;
+    fa.cell_base = D.cell_base;
+    family_pass(ctx->L(), fa);
+    F.zptr = F.z.d();
+    xtwz_pass(F);
+    fista_enqueue(F, lambda, oc.inner, vmax_part, n_vmax);
+    // eta_tilde = H(theta_tilde) with Delta_k's inner product and the first trials.
+    double t_list[kMaxTrials];
+    double t = oc.alpha0;
+    int nt = 0;
+    for (; nt < kMaxTrials && nt <= oc.max_bt; ++nt, t *= oc.b) t_list[nt] = t;
+    HlastArgs h = hlast_args(F);
+    h.flags = HL_DOT | HL_TRIALS;
+    h.eta_old = F.eta.d();
+    h.u = F.u.d();
+    h.ntrial = nt;
+    for (int j = 0; j < nt; ++j) h.t[j] = t_list[j];
+    g = h_full(F, F.best.d(), F.eta_t.d(), h);
+    reduce_cols(ctx->L(), F.part.d(), g, kHlastCols, 0, F.scal.d());
+    ptrials(ctx->L(), F.p, F.pen, F.alpha, F.theta.d(), F.best.d(), nt, t_list, F.tpart.d());
+    reduce_cols(ctx->L(), F.tpart.d(), pgrid(F.p), 2 * (1 + kMaxTrials), 0, F.scal.d() + 16);
+    KG_CUDA(cudaMemcpyAsync(pin, F.scal.p, sizeof(double) * 40, cudaMemcpyDeviceToHost, ctx->s));
+    KG_CUDA(cudaMemcpyAsync(pin + PIN_ERR, F.errs.p, sizeof(i64) * 16, cudaMemcpyDeviceToHost, ctx->s));
+    sync(ctx);
+    i64 errs[16];
+    std::memcpy(errs, pin + PIN_ERR, sizeof(errs));
+    // reference order: score (outer.cpp:241) then working response (:252)
+    if (errs[ERR_FAM] != kNoErr)
+      throw Error(E_EVAL, "non-finite score entry at cell " + std::to_string(errs[ERR_FAM]), errs[ERR_FAM]);
+    if (errs[ERR_FAM + 1] != kNoErr)
+      throw Error(E_EVAL, "non-finite working response entry at cell " + std::to_string(errs[ERR_FAM + 1]),
+                  errs[ERR_FAM + 1]);
+    const FistaOut fo = fista_read(F);
+    if (fo.bad_weights) throw Error(E_INVAL, "lipschitz_upper: weights must not be all zero");
+    tr.inner += fo.iterations;
+    if (fo.diverged) {
+      tr.status = KG_S_INNER_DIVERGENCE;
+      return tr;
+    }
+    const double dot = pin[1];
+    const double J_t = penalty_of(F.pen, F.alpha, pin[16], pin[17]);
+    const double delta_k = -dot / n + lambda * (J_t - J_cur);
+    const double decrease = std::min(delta_k, 0.0);
+    // Armijo (outer.cpp:118-143): trials in order, batches of kMaxTrials.
+    bool accepted = false;
+    double t_acc = 0.0, f_acc = 0.0;
+    int base = 0;
+    std::vector<double> lls(pin + 2, pin + 2 + nt), Js(nt);
+    for (int j = 0; j < nt; ++j) Js[j] = penalty_of(F.pen, F.alpha, pin[16 + 2 + 2 * j], pin[16 + 3 + 2 * j]);
+    std::vector<i64> terr(errs + 2, errs + 2 + nt);
+    t = oc.alpha0;
+    for (i64 j = 0; j <= oc.max_bt; ++j, t *= oc.b) {
+      if (j - base >= nt) {  // next batch of trials over (eta, eta_tilde)
+        base = static_cast<int>(j);
+        double tt = t;
+        nt = 0;
+        for (; nt < kMaxTrials && base + nt <= oc.max_bt; ++nt, tt *= oc.b) t_list[nt] = tt;
+        reset_errs(F);
+        HlastArgs hb = hlast_args(F);
+        hb.P = nullptr;
+        hb.eta_new = F.eta_t.d();
+        hb.eta_old = F.eta.d();
+        hb.flags = HL_TRIALS;
+        hb.ntrial = nt;
+        for (int q = 0; q < nt; ++q) hb.t[q] = t_list[q];
+        hlast_mode1(ctx->L(), hb);
+        reduce_cols(ctx->L(), F.part.d(), hlast_grid(hb), kHlastCols, 0, F.scal.d());
+        ptrials(ctx->L(), F.p, F.pen, F.alpha, F.theta.d(), F.best.d(), nt, t_list, F.tpart.d());
+        reduce_cols(ctx->L(), F.tpart.d(), pgrid(F.p), 2 * (1 + kMaxTrials), 0, F.scal.d() + 16);
+        KG_CUDA(cudaMemcpyAsync(pin, F.scal.p, sizeof(double) * 40, cudaMemcpyDeviceToHost, ctx->s));
+        KG_CUDA(cudaMemcpyAsync(pin + PIN_ERR, F.errs.p, sizeof(i64) * 16, cudaMemcpyDeviceToHost, ctx->s));
+        sync(ctx);
+        std::memcpy(errs, pin + PIN_ERR, sizeof(errs));
+        lls.assign(pin + 2, pin + 2 + nt);
+        Js.resize(nt);
+        for (int q = 0; q < nt; ++q) Js[q] = penalty_of(F.pen, F.alpha, pin[16 + 2 + 2 * q], pin[16 + 3 + 2 * q]);
+        terr.assign(errs + 2, errs + 2 + nt);
+      }
+      const int q = static_cast<int>(j - base);
+      if (terr[q] != kNoErr)
+        throw Error(E_EVAL, "non-finite log-likelihood term at cell " + std::to_string(terr[q]), terr[q]);
+      const double f_trial = -(lls[q] / F.disp) / n + lambda * Js[q];
+      if (std::isfinite(f_trial) && f_trial <= f_cur + t * oc.v * decrease) {
+        accepted = true;
+        t_acc = t;
+        f_acc = f_trial;
+        J_cur = Js[q];
+        break;
+      }
+    }
+    tr.outer += 1;
+    if (!accepted) {
+      tr.status = KG_S_LINE_SEARCH_FAILED;
+      return tr;
+    }
+    ptheta_update(ctx->L(), F.p, t_acc, F.best.d(), F.theta.d());
+    eta_combine(ctx->L(), F.n, t_acc, F.eta_t.d(), F.eta.d());
+    tr.final_objective = f_acc;
+    const double rel = std::abs(f_acc - f_cur) / std::max(1.0, std::abs(f_cur));
+    f_cur = f_acc;
+    if (rel < oc.tol) {
+      tr.status = KG_S_CONVERGED;
+      return tr;
+    }
+  }
+  tr.status = KG_S_MAX_ITERATIONS;
+  return tr;
+}
+
+static std::vector<double> lambda_sequence(double lmax, i64 nl, double ratio) {
+  if (!(lmax > 0.0)) throw Error(E_INVAL, "lambda_sequence: lambda_max must be positive");
+  if (nl < 1) throw Error(E_INVAL, "lambda_sequence: n_lambda must be positive");
+  if (!(ratio > 0.0 && ratio < 1.0)) throw Error(E_INVAL, "lambda_sequence: lambda_min_ratio must lie in (0,1)");
+  std::vector<double> out(nl);
+  out[0] = lmax;
+  if (nl == 1) return out;
+  const double step = std::log(ratio) / static_cast<double>(nl - 1);
+  for (i64 t = 1; t < nl; ++t) out[t] = lmax * std::exp(step * static_cast<double>(t));
+  return out;
+}
+
+static const char* status_name(int s) {
+  static const char* names[] = {"converged", "max_iterations", "line_search_failed", "inner_divergence"};
+  return names[s];
+}
+
+static kg_path_result* fit_path(kg_ctx* ctx, const kg_design* D, const kg_obs* O, int fam, double disp, int pen,
+                                double alpha, const kg_path_cfg& cfg, const double* lambdas_in, i64 n_lambdas_in) {
+  if (fam < 0 || fam > 3) throw Error(E_INVAL, "unknown family");
+  if (pen < 0 || pen > 2) throw Error(E_INVAL, "unknown penalty");
+  if (!(disp > 0.0)) throw Error(E_INVAL, "dispersion must be positive");
+  if (pen == KG_ELASTIC_NET && !(alpha >= 0.0)) throw Error(E_INVAL, "elastic net alpha must be nonnegative");
+  if (O->design != D) throw Error(E_INVAL, "observation was created for another design");
+  OuterCfg oc;
+  oc.max_outer = cfg.max_outer;
+  oc.max_bt = cfg.armijo_max_backtracks;
+  oc.alpha0 = cfg.armijo_alpha0;
+  oc.b = cfg.armijo_b;
+  oc.v = cfg.armijo_v;
+  oc.tol = cfg.outer_tol;
+  oc.wmode = static_cast<int>(cfg.weight_mode);
+  oc.inner.nu = cfg.nu;
+  oc.inner.tol = cfg.inner_tol;
+  oc.inner.max_iters = cfg.inner_max_iters;
+  oc.inner.monitor_every = cfg.monitor_every;
+  oc.inner.extrapolation = static_cast<int>(cfg.extrapolation);
+  if (oc.wmode < 0 || oc.wmode > 2) throw Error(E_INVAL, "unknown weight mode");
+
+  auto F = std::make_unique<Fit>();
+  F->ctx = ctx;
+  F->D = D;
+  F->O = O;
+  F->fam = fam;
+  F->disp = disp;
+  F->pen = pen;
+  F->alpha = pen == KG_ELASTIC_NET ? alpha : 0.0;
+  alloc_fit(*F);
+
+  auto res = std::make_unique<kg_path_result>();
+  res->ctx = ctx;
+  res->p = D->P;
+
+  // grid (path.cpp:29-45) -- lambda_max validates the data first
+  std::vector<double> lambdas;
+  if (!lambdas_in) {
+    if (pen == KG_RIDGE)
+      throw Error(E_INVAL, "fit_path: penalty has no l1 component; supply an explicit lambda sequence");
+    validate_obs(*F);
+    const double lmax = lambda_max_fit(*F);
+    if (!(lmax > 0.0))
+      throw Error(E_INVAL,
+                  "fit_path: lambda_max is zero (score vanishes at theta = 0); supply an explicit lambda sequence");
+    lambdas = lambda_sequence(lmax, cfg.n_lambda, cfg.lambda_min_ratio);
+    res->lambda_max = lmax;
+  } else {
+    lambdas.assign(lambdas_in, lambdas_in + n_lambdas_in);
+  }
+  if (lambdas.empty()) throw Error(E_INVAL, "fit_path: empty lambda sequence");
+  for (size_t t = 0; t < lambdas.size(); ++t) {
+    if (!(lambdas[t] >= 0.0)) throw Error(E_INVAL, "fit_path: lambda values must be nonnegative");
+    if (t > 0 && !(lambdas[t] < lambdas[t - 1]))
+      throw Error(E_INVAL, "fit_path: lambda sequence must be strictly decreasing");
+  }
+  // outer_solve argument checks (outer.cpp:165-178)
+  if (!(oc.alpha0 > 0.0) || !(oc.b > 0.0 && oc.b < 1.0) || !(oc.v > 0.0 && oc.v < 1.0))
+    throw Error(E_INVAL, "outer_solve: need alpha0 > 0 and Armijo constants b, v in (0,1)");
+  if (oc.max_outer < 1 || !(oc.tol > 0.0)) throw Error(E_INVAL, "outer_solve: need max_outer >= 1 and outer_tol > 0");
+  if (oc.wmode == KG_W_TENSOR)
+    throw Error(E_INVAL, "iwls=tensor (tensor-approximated weights) is not implemented by the device solver");
+  if (lambdas_in) validate_obs(*F);
+
+  const i64 nl = static_cast<i64>(lambdas.size());
+  res->coefs.alloc(sizeof(double) * D->P * nl);
+  DBuf nnz;
+  nnz.alloc(sizeof(i64) * nl);
+
+  // state at theta = 0: eta = 0
+  KG_CUDA(cudaMemsetAsync(F->theta.p, 0, sizeof(double) * F->p, ctx->s));
+  KG_CUDA(cudaMemsetAsync(F->eta.p, 0, sizeof(double) * F->n, ctx->s));
+  const bool gauss_shortcut = fam == KG_GAUSSIAN && oc.wmode == KG_W_EXACT;
+  PathState st;
+  int n_vmax = 0;
+  if (gauss_shortcut) {
+    // v = a * glm_weights = a / disp, z = y: fixed along the path, so the
+    // weights, X^T W z and the Lipschitz bound are computed once (the
+    // reference recomputes the same values per lambda).
+    n_vmax = elem_grid(F->n);
+    gauss_weights(ctx->L(), F->n, disp, O->a.d(), F->v.d(), F->part.d() + D->part_cap - n_vmax);
+    F->zptr = O->y.d();
+    xtwz_pass(*F);
+    // loglik at eta = 0
+    reset_errs(*F);
+    HlastArgs h = hlast_args(*F);
+    h.P = nullptr;
+    h.eta_new = F->eta.d();
+    h.flags = HL_LL_NEW;
+    hlast_mode1(ctx->L(), h);
+    reduce_cols(ctx->L(), F->part.d(), hlast_grid(h), kHlastCols, 0, F->scal.d());
+    double* pin = ctx->pin();
+    KG_CUDA(cudaMemcpyAsync(pin, F->scal.p, sizeof(double), cudaMemcpyDeviceToHost, ctx->s));
+    KG_CUDA(cudaMemcpyAsync(pin + PIN_ERR, F->errs.p, sizeof(i64), cudaMemcpyDeviceToHost, ctx->s));
+    sync(ctx);
+    i64 e;
+    std::memcpy(&e, pin + PIN_ERR, sizeof(i64));
+    check_ll_errs(*F, &e);
+    st.ll = pin[0] / disp;
+  }
+  for (i64 t = 0; t < nl; ++t) {
+    ModelTrace tr = gauss_shortcut ? gaussian_step(*F, lambdas[t], oc, st, n_vmax) : outer_loop(*F, lambdas[t], oc);
+    if (tr.status != KG_S_CONVERGED) {
+      if (t == 0)
+        throw Error(E_RUNTIME, std::string("fit_path: first model did not converge (") + status_name(tr.status) + ")");
+      res->truncated = true;
+      break;
+    }
+    KG_CUDA(cudaMemcpyAsync(res->coefs.d() + D->P * t, F->theta.p, sizeof(double) * D->P, cudaMemcpyDeviceToDevice,
+                            ctx->s));
+    res->lambdas.push_back(lambdas[t]);
+    res->objectives.push_back(tr.final_objective);
+    res->outer_iters.push_back(tr.outer);
+    res->inner_iters.push_back(tr.inner);
+    res->status.push_back(tr.status);
+  }
+  sync(ctx);
+  return res.release();
+}
+
+}  // namespace kg
+
+// =================================================================== C ABI
+using namespace kg;
+
+namespace {
+
+template <class F>
+kg_status guarded(kg_ctx* ctx, F&& f) {
+  try {
+    f();
+    if (ctx) {
+      ctx->err.clear();
+      ctx->err_cell = -1;
+    }
+    return KG_OK;
+  } catch (const Error& e) {
+    if (ctx) {
+      ctx->err = e.what();
+      ctx->err_cell = e.cell;
+    }
+    return static_cast<kg_status>(e.code);
+  } catch (const std::bad_alloc&) {
+    if (ctx) ctx->err = "host allocation failed";
+    return KG_ENOMEM;
+  } catch (const std::exception& e) {
+    if (ctx) ctx->err = e.what();
+    return KG_ERUNTIME;
+  }
+}
+
+void set_device(kg_ctx* ctx) { KG_CUDA(cudaSetDevice(ctx->device)); }
+
+}  // namespace
+
+extern "C" {
+
+void kg_path_cfg_default(kg_path_cfg* c) {
+  c->n_lambda = 100;
+  c->lambda_min_ratio = 1e-4;
+  c->max_outer = 100;
+  c->armijo_alpha0 = 1.0;
+  c->armijo_b = 0.5;
+  c->armijo_v = 0.1;
+  c->armijo_max_backtracks = 50;
+  c->weight_mode = KG_W_EXACT;
+  c->outer_tol = 1e-8;
+  c->nu = 1.0;
+  c->inner_max_iters = 2000;
+  c->inner_tol = 1e-8;
+  c->extrapolation = 0;
+  c->monitor_every = 1;
+}
+
+kg_status kg_ctx_create(int device, kg_ctx** out) {
+  *out = nullptr;
+  auto ctx = std::make_unique<kg_ctx>();
+  ctx->device = device;
+  kg_status st = guarded(nullptr, [&] {
+    int count = 0;
+    KG_CUDA(cudaGetDeviceCount(&count));
+    if (device < 0 || device >= count) throw Error(E_INVAL, "no such CUDA device");
+    KG_CUDA(cudaSetDevice(device));
+    KG_CUDA(cudaStreamCreateWithFlags(&ctx->s, cudaStreamNonBlocking));
+    KG_CUDA(cudaMallocHost(&ctx->pinned, 4096));
+  });
+  if (st == KG_OK) *out = ctx.release();
+  return st;
+}
+
+kg_status kg_ctx_create_sharded(int device, int rank, int world, const void*, kg_ctx** out) {
+  *out = nullptr;
+  if (world != 1 || rank != 0) return KG_ENCCL;  // sharded NCCL contexts: see DESIGN.md (next rows)
+  return kg_ctx_create(device, out);
+}
+
+kg_status kg_nccl_unique_id(void*) { return KG_ENCCL; }
+
+void kg_ctx_destroy(kg_ctx* ctx) {
+  if (!ctx) return;
+  cudaSetDevice(ctx->device);
+  if (ctx->s) cudaStreamSynchronize(ctx->s);
+  if (ctx->pinned) cudaFreeHost(ctx->pinned);
+  if (ctx->s) cudaStreamDestroy(ctx->s);
+  delete ctx;
+}
+
+const char* kg_last_error(const kg_ctx* ctx) { return ctx ? ctx->err.c_str() : "no context"; }
+int64_t kg_last_error_cell(const kg_ctx* ctx) { return ctx ? ctx->err_cell : -1; }
+void* kg_ctx_stream(kg_ctx* ctx) { return ctx->s; }
+kg_status kg_ctx_synchronize(kg_ctx* ctx) {
+  return guarded(ctx, [&] { sync(ctx); });
+}
+void kg_ctx_shard(const kg_ctx* ctx, int* rank, int* world) {
+  *rank = ctx->rank;
+  *world = ctx->world;
+}
+int64_t kg_launch_count(const kg_ctx* ctx) { return ctx->launches; }
+void kg_launch_count_reset(kg_ctx* ctx) { ctx->launches = 0; }
+
+kg_status kg_design_create(kg_ctx* ctx, int64_t c, int64_t d, const int64_t* n, const int64_t* p,
+                           const double* const* factors, kg_design** out) {
+  *out = nullptr;
+  auto D = std::make_unique<kg_design>();
+  kg_status st = guarded(ctx, [&] {
+    set_device(ctx);
+    if (c < 1) throw Error(E_INVAL, "TensorDesign: need at least one component");
+    if (d < 1) throw Error(E_INVAL, "TensorDesign: need at least one marginal factor");
+    D->ctx = ctx;
+    D->c = c;
+    D->d = d;
+    D->n_full.assign(n, n + d);
+    for (i64 j = 0; j < d; ++j)
+      if (n[j] < 1) throw Error(E_INVAL, "ArrayDims: extents must be positive");
+    D->n = D->n_full;
+    D->p.assign(c, std::vector<i64>(d));
+    for (i64 r = 0; r < c; ++r)
+      for (i64 j = 0; j < d; ++j) {
+        D->p[r][j] = p[r * d + j];
+        if (D->p[r][j] < 1) throw Error(E_INVAL, "TensorDesign: factors must have at least one column");
+      }
+    // this shard's slab of the last mode
+    const i64 nd = D->n_full[d - 1];
+    const i64 lo = nd * ctx->rank / ctx->world, hi = nd * (ctx->rank + 1) / ctx->world;
+    D->n[d - 1] = hi - lo;
+    if (D->n[d - 1] < 1) throw Error(E_INVAL, "sharded design: fewer last-mode slices than ranks");
+    D->N = prod(D->n, 0, d);
+    D->N_full = prod(D->n_full, 0, d);
+    D->cell_base = lo * prod(D->n_full, 0, d - 1);
+    D->P = 0;
+    for (i64 r = 0; r < c; ++r) {
+      D->offs.push_back(D->P);
+      D->P += prod(D->p[r], 0, d);
+    }
+    D->f.resize(c);
+    D->spectral.assign(c, std::vector<double>(d, 0.0));
+    D->lipfac = 0.0;
+    for (i64 r = 0; r < c; ++r) {
+      double pr = 1.0;
+      for (i64 j = 0; j < d; ++j) {
+        FactorHost full;
+        full.n = D->n_full[j];
+        full.p = D->p[r][j];
+        full.X.assign(factors[r * d + j], factors[r * d + j] + full.n * full.p);
+        auto fo = std::make_unique<FactorOwn>();
+        // the spectral radius always uses the full factor (L-hat is global)
+        upload_factor(full, *fo, ctx->s);
+        D->spectral[r][j] = factor_spectral(ctx, full, *fo);
+        if (j == d - 1 && (lo != 0 || hi != nd)) {  // slice the rows of X_d for this shard
+          FactorHost sl;
+          sl.n = hi - lo;
+          sl.p = full.p;
+          sl.X.resize(sl.n * sl.p);
+          for (i64 k = 0; k < sl.p; ++k)
+            for (i64 i = 0; i < sl.n; ++i) sl.X[i + sl.n * k] = full.X[(lo + i) + full.n * k];
+          fo = std::make_unique<FactorOwn>();
+          upload_factor(sl, *fo, ctx->s);
+        }
+        pr *= D->spectral[r][j];
+        D->f[r].push_back(std::move(fo));
+      }
+      D->lipfac += pr;
+    }
+    // fused mode-1 route for one component whose mode-1 fibre tile fits shared memory
+    const i64 n1 = D->n[0], p1 = D->p[0][0], m = D->N / n1;
+    D->fused = c == 1 && (n1 + p1) * 8 <= 96 * 1024;
+    if (D->fused) {
+      i64 T = std::max<i64>(1, 2048 / n1);
+      T = std::min<i64>(T, std::max<i64>(1, m / 296));  // >= 2 CTAs per SM when the array allows
+      while (T > 1 && (n1 + p1) * T * 8 > 96 * 1024) --T;
+      D->T = static_cast<int>(T);
+    }
+    D->scratch = chain_scratch(*D);
+    const i64 tiles = D->fused ? (m + D->T - 1) / D->T : 0;
+    const i64 hl_tiles = (m + D->T - 1) / D->T;
+    D->part_cap = std::max<i64>({tiles, static_cast<i64>(elem_grid(D->N)), hl_tiles * kHlastCols}) +
+                  elem_grid(D->N) + 64;
+    sync(ctx);
+  });
+  if (st == KG_OK) *out = D.release();
+  return st;
+}
+
+void kg_design_destroy(kg_design* d) {
+  if (d && d->ctx) {
+    cudaSetDevice(d->ctx->device);
+    cudaStreamSynchronize(d->ctx->s);
+  }
+  delete d;
+}
+int64_t kg_design_n(const kg_design* d) { return d->N; }
+int64_t kg_design_p(const kg_design* d) { return d->P; }
+kg_status kg_design_spectral(kg_design* d, int64_t r, int64_t j, double* out) {
+  return guarded(d->ctx, [&] {
+    if (r < 0 || r >= d->c || j < 0 || j >= d->d) throw Error(E_INVAL, "factor index out of range");
+    *out = d->spectral[r][j];
+  });
+}
+
+kg_status kg_obs_create(kg_ctx* ctx, const kg_design* design, const double* y, const double* a, int on_device,
+                        kg_obs** out) {
+  *out = nullptr;
+  auto O = std::make_unique<kg_obs>();
+  kg_status st = guarded(ctx, [&] {
+    set_device(ctx);
+    O->ctx = ctx;
+    O->design = design;
+    const size_t nb = sizeof(double) * design->N;
+    O->y.alloc(nb);
+    O->a.alloc(nb);
+    const cudaMemcpyKind k = on_device ? cudaMemcpyDeviceToDevice : cudaMemcpyHostToDevice;
+    KG_CUDA(cudaMemcpyAsync(O->y.p, y, nb, k, ctx->s));
+    if (a) {
+      KG_CUDA(cudaMemcpyAsync(O->a.p, a, nb, k, ctx->s));
+      O->unit_a = false;
+    } else {
+      fill(ctx->L(), design->N, 1.0, O->a.d());  // ObservationData(y): a = 1 (family.hpp:44-45)
+    }
+    sync(ctx);
+  });
+  if (st == KG_OK) *out = O.release();
+  return st;
+}
+
+void kg_obs_destroy(kg_obs* o) { delete o; }
+
+kg_status kg_fit_path(kg_ctx* ctx, const kg_design* design, const kg_obs* obs, int family, double dispersion,
+                      int penalty, double alpha, const kg_path_cfg* cfg, const double* lambdas, int64_t n_lambdas,
+                      kg_path_result** out) {
+  *out = nullptr;
+  return guarded(ctx, [&] {
+    set_device(ctx);
+    kg_path_cfg c;
+    kg_path_cfg_default(&c);
+    if (cfg) c = *cfg;
+    *out = fit_path(ctx, design, obs, family, dispersion, penalty, alpha, c, lambdas, n_lambdas);
+  });
+}
+
+int64_t kg_result_n_models(const kg_path_result* r) { return static_cast<int64_t>(r->lambdas.size()); }
+int kg_result_truncated(const kg_path_result* r) { return r->truncated ? 1 : 0; }
+double kg_result_lambda_max(const kg_path_result* r) { return r->lambda_max; }
+double kg_result_lambda(const kg_path_result* r, int64_t t) { return r->lambdas[t]; }
+double kg_result_objective(const kg_path_result* r, int64_t t) { return r->objectives[t]; }
+int64_t kg_result_outer_iters(const kg_path_result* r, int64_t t) { return r->outer_iters[t]; }
+int64_t kg_result_inner_iters(const kg_path_result* r, int64_t t) { return r->inner_iters[t]; }
+int kg_result_status(const kg_path_result* r, int64_t t) { return r->status[t]; }
+int64_t kg_result_nonzero(const kg_path_result* r, int64_t t) {
+  std::vector<double> h(r->p);
+  if (cudaMemcpy(h.data(), r->coefs.d() + r->p * t, sizeof(double) * r->p, cudaMemcpyDeviceToHost) != cudaSuccess)
+    return -1;
+  int64_t k = 0;
+  for (double v : h) k += v != 0.0;
+  return k;
+}
+kg_status kg_result_coef(kg_path_result* r, int64_t t, double* out) {
+  return guarded(r->ctx, [&] {
+    set_device(r->ctx);
+    if (t < 0 || t >= static_cast<int64_t>(r->lambdas.size())) throw Error(E_INVAL, "model index out of range");
+    KG_CUDA(cudaMemcpy(out, r->coefs.d() + r->p * t, sizeof(double) * r->p, cudaMemcpyDeviceToHost));
+  });
+}
+void kg_result_free(kg_path_result* r) { delete r; }
+
+}  // extern "C"
+
+// ============================================================ operator probes
+namespace {
+
+struct Tmp {
+  std::vector<std::unique_ptr<DBuf>> bufs;
+  double* get(size_t n) {
+    bufs.push_back(std::make_unique<DBuf>());
+    bufs.back()->alloc(sizeof(double) * std::max<size_t>(n, 1));
+    return bufs.back()->d();
+  }
+};
+
+void h_map_dev(kg_ctx* ctx, const kg_design* D, const double* coef, double* eta, double* s0, double* s1) {
+  for (i64 r = 0; r < D->c; ++r)
+    run_chain(ctx, coef_dims(*D, r), h_steps(*D, r, 0), coef + D->offs[r], eta, s0, s1, r > 0);
+}
+
+void g_map_dev(kg_ctx* ctx, const kg_design* D, const double* u, double* coef, double* s0, double* s1) {
+  for (i64 r = 0; r < D->c; ++r) run_chain(ctx, D->n, g_steps(*D, r, 0), u, coef + D->offs[r], s0, s1, false);
+}
+
+}  // namespace
+
+namespace kg {
+__global__ void k_rho(const double* A, double* out, i64 n1, i64 rest, BandOp op) {
+  const i64 total = rest * op.rows;
+  for (i64 idx = static_cast<i64>(blockIdx.x) * blockDim.x + threadIdx.x; idx < total;
+       idx += static_cast<i64>(gridDim.x) * blockDim.x) {
+    const i64 c = idx % rest, q = idx / rest;
+    const int lo = op.lo[q], len = op.len[q];
+    const double* cf = op.coef + op.off[q];
+    const double* col = A + n1 * c;
+    double s = 0.0;
+    for (int t = 0; t < len; ++t) s = fma(cf[t], col[lo + t], s);
+    out[c + rest * q] = s;  // rotated: (n2..nd, r)
+  }
+}
+}  // namespace kg
+
+extern "C" {
+
+kg_status kg_h_map(kg_ctx* ctx, const kg_design* D, const double* coef, double* eta) {
+  return guarded(ctx, [&] {
+    set_device(ctx);
+    Tmp t;
+    double* dc = t.get(D->P);
+    double* de = t.get(D->N);
+    double *s0 = t.get(D->scratch), *s1 = t.get(D->scratch);
+    KG_CUDA(cudaMemcpyAsync(dc, coef, sizeof(double) * D->P, cudaMemcpyHostToDevice, ctx->s));
+    h_map_dev(ctx, D, dc, de, s0, s1);
+    KG_CUDA(cudaMemcpyAsync(eta, de, sizeof(double) * D->N, cudaMemcpyDeviceToHost, ctx->s));
+    sync(ctx);
+  });
+}
+
+kg_status kg_g_map(kg_ctx* ctx, const kg_design* D, const double* u, double* coef) {
+  return guarded(ctx, [&] {
+    set_device(ctx);
+    Tmp t;
+    double* du = t.get(D->N);
+    double* dc = t.get(D->P);
+    double *s0 = t.get(D->scratch), *s1 = t.get(D->scratch);
+    KG_CUDA(cudaMemcpyAsync(du, u, sizeof(double) * D->N, cudaMemcpyHostToDevice, ctx->s));
+    g_map_dev(ctx, D, du, dc, s0, s1);
+    KG_CUDA(cudaMemcpyAsync(coef, dc, sizeof(double) * D->P, cudaMemcpyDeviceToHost, ctx->s));
+    sync(ctx);
+  });
+}
+
+kg_status kg_xtwx_apply(kg_ctx* ctx, const kg_design* D, const double* v, const double* coef, double* out) {
+  return guarded(ctx, [&] {
+    set_device(ctx);
+    Tmp t;
+    double *dv = t.get(D->N), *de = t.get(D->N), *dw = t.get(D->N);
+    double *dc = t.get(D->P), *dout = t.get(D->P);
+    double *s0 = t.get(D->scratch), *s1 = t.get(D->scratch);
+    KG_CUDA(cudaMemcpyAsync(dv, v, sizeof(double) * D->N, cudaMemcpyHostToDevice, ctx->s));
+    KG_CUDA(cudaMemcpyAsync(dc, coef, sizeof(double) * D->P, cudaMemcpyHostToDevice, ctx->s));
+    h_map_dev(ctx, D, dc, de, s0, s1);
+    vz(ctx->L(), D->N, dv, de, dw);
+    g_map_dev(ctx, D, dw, dout, s0, s1);
+    KG_CUDA(cudaMemcpyAsync(out, dout, sizeof(double) * D->P, cudaMemcpyDeviceToHost, ctx->s));
+    sync(ctx);
+  });
+}
+
+kg_status kg_rho(kg_ctx* ctx, int64_t r, const double* x, int64_t ndim, const int64_t* extents, const double* a,
+                 double* out) {
+  return guarded(ctx, [&] {
+    set_device(ctx);
+    if (ndim < 1) throw Error(E_INVAL, "ArrayDims: need at least one dimension");
+    const i64 n1 = extents[0];
+    i64 rest = 1;
+    for (i64 j = 0; j < ndim; ++j) {
+      if (extents[j] < 1) throw Error(E_INVAL, "ArrayDims: extents must be positive");
+      if (j) rest *= extents[j];
+    }
+    FactorHost h;  // rho's operator is x itself (r x n1): build its row bands via a transposed "factor"
+    h.n = r;
+    h.p = n1;
+    h.X.assign(x, x + r * n1);
+    FactorOwn f;
+    upload_factor(h, f, ctx->s);
+    Tmp t;
+    double* da = t.get(n1 * rest);
+    double* dout = t.get(rest * r);
+    KG_CUDA(cudaMemcpyAsync(da, a, sizeof(double) * n1 * rest, cudaMemcpyHostToDevice, ctx->s));
+    const i64 total = rest * r;
+    const int g = static_cast<int>(std::min<i64>((total + 255) / 256, 148 * 16));
+    k_rho<<<std::max(g, 1), 256, 0, ctx->s>>>(da, dout, n1, rest, f.dev.H);
+    ++ctx->launches;
+    KG_CUDA(cudaGetLastError());
+    KG_CUDA(cudaMemcpyAsync(out, dout, sizeof(double) * total, cudaMemcpyDeviceToHost, ctx->s));
+    sync(ctx);
+  });
+}
+
+kg_status kg_lambda_max(kg_ctx* ctx, const kg_design* D, const kg_obs* O, int family, double dispersion, int penalty,
+                        double, double* out) {
+  return guarded(ctx, [&] {
+    set_device(ctx);
+    if (penalty == KG_RIDGE) throw Error(E_INVAL, "lambda_max: pure ridge penalty has no finite lambda_max");
+    if (O->design != D) throw Error(E_INVAL, "lambda_max: data dims do not match the design");
+    Fit F;
+    F.ctx = ctx;
+    F.D = D;
+    F.O = O;
+    F.fam = family;
+    F.disp = dispersion;
+    alloc_fit(F);
+    validate_obs(F);
+    *out = lambda_max_fit(F);
+  });
+}
+
+kg_status kg_predict(kg_ctx* ctx, const kg_design* D, int family, const double* coef, double* eta, double* mu) {
+  return guarded(ctx, [&] {
+    set_device(ctx);
+    Tmp t;
+    double *dc = t.get(D->P), *de = t.get(D->N), *dm = t.get(D->N);
+    double *s0 = t.get(D->scratch), *s1 = t.get(D->scratch);
+    KG_CUDA(cudaMemcpyAsync(dc, coef, sizeof(double) * D->P, cudaMemcpyHostToDevice, ctx->s));
+    h_map_dev(ctx, D, dc, de, s0, s1);
+    mean_map(ctx->L(), D->N, family, de, dm);
+    KG_CUDA(cudaMemcpyAsync(eta, de, sizeof(double) * D->N, cudaMemcpyDeviceToHost, ctx->s));
+    KG_CUDA(cudaMemcpyAsync(mu, dm, sizeof(double) * D->N, cudaMemcpyDeviceToHost, ctx->s));
+    sync(ctx);
+  });
+}
+
+kg_status kg_time_kernel(kg_ctx* ctx, const kg_design* D, const kg_obs* O, int which, int reps, double* avg_ms,
+                         double* bytes) {
+  return guarded(ctx, [&] {
+    set_device(ctx);
+    if (reps < 1) throw Error(E_INVAL, "reps must be positive");
+    Fit F;
+    F.ctx = ctx;
+    F.D = D;
+    F.O = O;
+    alloc_fit(F);
+    KG_CUDA(cudaMemsetAsync(F.x.p, 0, sizeof(double) * F.p, ctx->s));
+    gauss_weights(ctx->L(), F.n, 1.0, O->a.d(), F.v.d(), F.part.d() + D->part_cap - elem_grid(F.n));
+    F.zptr = O->y.d();
+    cudaEvent_t e0, e1;
+    KG_CUDA(cudaEventCreate(&e0));
+    KG_CUDA(cudaEventCreate(&e1));
+    std::function<void()> launch;
+    double b = 0.0;
+    if (which == 0) {
+      if (!D->fused) throw Error(E_INVAL, "the fused pass needs a one-component design");
+      const double* P = F.x.d();
+      if (D->d > 1) {
+        run_chain(ctx, coef_dims(*D, 0), h_steps(*D, 0, 1), F.x.d(), F.P.d(), F.s0.d(), F.s1.d(), false);
+        P = F.P.d();
+      }
+      FusedArgs a = fused_args(F);
+      a.P = P;
+      a.Q = D->d > 1 ? F.Q.d() : F.Sx.d();
+      a.v = F.v.d();
+      a.z = F.zptr;
+      a.partial = F.part.d();
+      launch = [&, a] { fused_mode1(ctx->L(), FV_FISTA, a); };
+      // P (p1 x m) read, v and z read, Q (p1 x m) written
+      b = 8.0 * (2.0 * static_cast<double>(F.n) + 2.0 * static_cast<double>(a.p1 * a.m));
+    } else {
+      // largest H-chain step of component 0 (modes d-1 .. 0 applied to theta)
+      std::vector<i64> dims = D->p[0];
+      i64 best_j = D->d - 1, best_sz = 0;
+      std::vector<i64> before_best;
+      for (i64 j = D->d - 1; j >= 0; --j) {
+        std::vector<i64> before = dims;
+        dims[j] = D->n[j];
+        const i64 sz = prod(dims, 0, dims.size()) + prod(before, 0, before.size());
+        if (sz > best_sz) {
+          best_sz = sz;
+          best_j = j;
+          before_best = before;
+        }
+      }
+      const i64 a_ = prod(before_best, 0, best_j), K = before_best[best_j],
+                b_ = prod(before_best, best_j + 1, before_best.size());
+      const i64 M = D->n[best_j];
+      double* in = F.s0.d();
+      double* outp = F.eta.d();
+      KG_CUDA(cudaMemsetAsync(in, 0, sizeof(double) * a_ * K * b_, ctx->s));
+      const BandOp op = D->f[0][best_j]->dev.H;
+      launch = [&, in, outp, a_, K, M, b_, op] { contract(ctx->L(), in, outp, a_, K, M, b_, op, false); };
+      b = 8.0 * static_cast<double>(a_ * K * b_ + a_ * M * b_);
+    }
+    for (int i = 0; i < 3; ++i) launch();
+    KG_CUDA(cudaEventRecord(e0, ctx->s));
+    for (int i = 0; i < reps; ++i) launch();
+    KG_CUDA(cudaEventRecord(e1, ctx->s));
+    KG_CUDA(cudaEventSynchronize(e1));
+    float ms = 0.f;
+    KG_CUDA(cudaEventElapsedTime(&ms, e0, e1));
+    cudaEventDestroy(e0);
+    cudaEventDestroy(e1);
+    *avg_ms = ms / reps;
+    *bytes = b;
+  });
+}
+
+}  // extern "C"

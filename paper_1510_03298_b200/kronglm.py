@@ -1,0 +1,395 @@
+"""Drop-in Python surface of the reference ``kronglm`` module on the B200 path.
+
+Same names, arguments, defaults, result keys and error types as the
+reference's pybind11 module (proj/bindings/kronglm_py.cpp:115-269):
+``linear_index``, ``rho``, ``h_map``, ``g_map``, ``lambda_max``,
+``fit_path``, ``predict``, ``bspline_design``, ``default_basis_count``.
+Arrays cross the boundary as Fortran-order float64 numpy arrays; every
+computation runs in libkronglm_b200.so on the GPU (no CPU fallback).
+
+Lower-level handles (:class:`Context`, :class:`Design`, :class:`Observation`,
+:func:`fit_path_resident`) expose the resident-HBM workflow the bench uses:
+upload once, fit many paths.
+"""
+from __future__ import annotations
+
+import ctypes as C
+import threading
+
+import numpy as np
+
+from . import _lib
+from ._lib import EvalError, InvalidArgument, KgError, PathCfg  # noqa: F401
+
+FAMILIES = {"gaussian": 0, "binomial": 1, "poisson": 2, "gamma": 3}
+PENALTIES = {"lasso": 0, "ridge": 1, "elasticnet": 2, "elastic_net": 2}
+WEIGHT_MODES = {"exact": 0, "unit": 1, "one": 1, "tensor": 2, "tensor_approx": 2}
+STATUS = ["converged", "max_iterations", "line_search_failed", "inner_divergence"]
+
+_pd = C.POINTER(C.c_double)
+_i64 = C.c_int64
+
+
+def _f(a):
+    return np.asfortranarray(np.asarray(a, dtype=np.float64))
+
+
+def _ptr(a):
+    return a.ctypes.data_as(_pd)
+
+
+# ------------------------------------------------------------------ handles
+class Context:
+    """One CUDA device + stream (kg_ctx)."""
+
+    def __init__(self, device: int = 0):
+        L = _lib.load()
+        h = C.c_void_p()
+        _lib.check(L.kg_ctx_create(int(device), C.byref(h)))
+        self.h = h
+        self.device = device
+
+    def close(self):
+        if getattr(self, "h", None):
+            _lib.load().kg_ctx_destroy(self.h)
+            self.h = None
+
+    def __del__(self):
+        try:
+            self.close()
+        except Exception:
+            pass
+
+    def check(self, st):
+        _lib.check(st, self.h)
+
+    @property
+    def stream(self) -> int:
+        return _lib.load().kg_ctx_stream(self.h)
+
+    def synchronize(self):
+        self.check(_lib.load().kg_ctx_synchronize(self.h))
+
+    @property
+    def launches(self) -> int:
+        return int(_lib.load().kg_launch_count(self.h))
+
+    def reset_launches(self):
+        _lib.load().kg_launch_count_reset(self.h)
+
+
+_ctx_local = threading.local()
+
+
+def default_context(device: int = 0) -> Context:
+    ctxs = getattr(_ctx_local, "ctxs", None)
+    if ctxs is None:
+        ctxs = _ctx_local.ctxs = {}
+    if device not in ctxs:
+        ctxs[device] = Context(device)
+    return ctxs[device]
+
+
+class Design:
+    """TensorDesign: components[r][j] is the n_j x p_{r,j} factor (design.hpp:13-45)."""
+
+    def __init__(self, components, ctx: Context | None = None):
+        self.ctx = ctx or default_context()
+        comps = [[_f(x) for x in comp] for comp in components]
+        if not comps or not comps[0]:
+            raise ValueError("TensorDesign: need at least one component and one marginal factor")
+        self.c, self.d = len(comps), len(comps[0])
+        for comp in comps:
+            if len(comp) != self.d:
+                raise ValueError("TensorDesign: components must share the array order d")
+            for x in comp:
+                if x.ndim != 2:
+                    raise ValueError("expected a 2-d array")
+        rows = [comps[0][j].shape[0] for j in range(self.d)]
+        for comp in comps:
+            if [x.shape[0] for x in comp] != rows:
+                raise ValueError("TensorDesign: factor row counts differ across components")
+        self.row_dims = tuple(rows)
+        self.block_dims = [tuple(x.shape[1] for x in comp) for comp in comps]
+        self.p = int(sum(int(np.prod(b)) for b in self.block_dims))
+        self.n = int(np.prod(rows))
+        n_arr = (_i64 * self.d)(*rows)
+        p_arr = (_i64 * (self.c * self.d))(*[q for b in self.block_dims for q in b])
+        X = (_pd * (self.c * self.d))(*[_ptr(x) for comp in comps for x in comp])
+        h = C.c_void_p()
+        self.ctx.check(_lib.load().kg_design_create(self.ctx.h, self.c, self.d, n_arr, p_arr, X, C.byref(h)))
+        self.h = h
+
+    def close(self):
+        if getattr(self, "h", None):
+            _lib.load().kg_design_destroy(self.h)
+            self.h = None
+
+    def __del__(self):
+        try:
+            self.close()
+        except Exception:
+            pass
+
+    def spectral(self, r, j):
+        out = C.c_double()
+        self.ctx.check(_lib.load().kg_design_spectral(self.h, r, j, C.byref(out)))
+        return out.value
+
+    def flat(self, coef):
+        if len(coef) != self.c:
+            raise ValueError("wrong number of coefficient blocks")
+        parts = []
+        for r, b in enumerate(coef):
+            b = _f(b)
+            if b.shape != self.block_dims[r]:
+                raise ValueError(f"coefficient block {r} does not match the design")
+            parts.append(b.ravel(order="F"))
+        return np.ascontiguousarray(np.concatenate(parts))
+
+    def blocks(self, flat):
+        out, off = [], 0
+        for b in self.block_dims:
+            k = int(np.prod(b))
+            out.append(np.asfortranarray(flat[off:off + k].reshape(b, order="F")))
+            off += k
+        return out
+
+
+class Observation:
+    """ObservationData(y[, a]) resident in HBM (family.hpp:40-47).
+
+    ``y``/``weights`` are numpy arrays (uploaded) or objects exposing
+    ``data_ptr()`` (e.g. CUDA torch tensors; copied device to device)."""
+
+    def __init__(self, design: Design, y, weights=None):
+        self.design = design
+        self.ctx = design.ctx
+        L = _lib.load()
+        h = C.c_void_p()
+        if hasattr(y, "data_ptr"):
+            yp = C.c_void_p(y.data_ptr())
+            ap = C.c_void_p(weights.data_ptr()) if weights is not None else None
+            self.ctx.check(L.kg_obs_create(self.ctx.h, design.h, yp, ap, 1, C.byref(h)))
+        else:
+            y = _f(y)
+            if y.shape != design.row_dims:
+                raise ValueError("data dims do not match the design")
+            a = None
+            if weights is not None:
+                a = _f(weights)
+                if a.shape != design.row_dims:
+                    raise ValueError("ObservationData: response and weight dims differ")
+            self.ctx.check(L.kg_obs_create(self.ctx.h, design.h, y.ctypes.data_as(C.c_void_p),
+                                           a.ctypes.data_as(C.c_void_p) if a is not None else None, 0,
+                                           C.byref(h)))
+        self.h = h
+
+    def close(self):
+        if getattr(self, "h", None):
+            _lib.load().kg_obs_destroy(self.h)
+            self.h = None
+
+    def __del__(self):
+        try:
+            self.close()
+        except Exception:
+            pass
+
+
+def make_cfg(n_lambda=100, lambda_min_ratio=1e-4, iwls="exact", nu=1.0, tol=1e-8, maxit=100, inner_tol=1e-8,
+             inner_maxit=2000, monitor_every=1, extrapolation="fista", armijo_alpha0=1.0, armijo_b=0.5,
+             armijo_v=0.1, armijo_max_backtracks=50):
+    if iwls not in WEIGHT_MODES:
+        raise ValueError("unknown weight mode: " + str(iwls))
+    cfg = PathCfg()
+    _lib.load().kg_path_cfg_default(C.byref(cfg))
+    cfg.n_lambda = int(n_lambda)
+    cfg.lambda_min_ratio = float(lambda_min_ratio)
+    cfg.weight_mode = WEIGHT_MODES[iwls]
+    cfg.nu = float(nu)
+    cfg.outer_tol = float(tol)
+    cfg.max_outer = int(maxit)
+    cfg.inner_tol = float(inner_tol)
+    cfg.inner_max_iters = int(inner_maxit)
+    cfg.monitor_every = int(monitor_every)
+    cfg.extrapolation = 0 if extrapolation == "fista" else 1
+    cfg.armijo_alpha0 = float(armijo_alpha0)
+    cfg.armijo_b = float(armijo_b)
+    cfg.armijo_v = float(armijo_v)
+    cfg.armijo_max_backtracks = int(armijo_max_backtracks)
+    return cfg
+
+
+class PathResult:
+    """FitPath (path.hpp:18-27); coefficients stay in HBM until read."""
+
+    def __init__(self, design: Design, h):
+        self.design = design
+        self.h = h
+        L = _lib.load()
+        self.n_models = int(L.kg_result_n_models(h))
+        self.truncated = bool(L.kg_result_truncated(h))
+        self.lambda_max = float(L.kg_result_lambda_max(h))
+        self.lambdas = [L.kg_result_lambda(h, t) for t in range(self.n_models)]
+        self.objectives = [L.kg_result_objective(h, t) for t in range(self.n_models)]
+        self.outer_iters = [int(L.kg_result_outer_iters(h, t)) for t in range(self.n_models)]
+        self.inner_iters = [int(L.kg_result_inner_iters(h, t)) for t in range(self.n_models)]
+        self.status = [STATUS[L.kg_result_status(h, t)] for t in range(self.n_models)]
+
+    def coef(self, t) -> np.ndarray:
+        out = np.zeros(self.design.p)
+        self.design.ctx.check(_lib.load().kg_result_coef(self.h, t, _ptr(out)))
+        return out
+
+    def close(self):
+        if getattr(self, "h", None):
+            _lib.load().kg_result_free(self.h)
+            self.h = None
+
+    def __del__(self):
+        try:
+            self.close()
+        except Exception:
+            pass
+
+
+def fit_path_resident(design: Design, obs: Observation, family="gaussian", penalty="lasso", alpha=0.0,
+                      lambdas=None, dispersion=1.0, **cfg) -> PathResult:
+    if family not in FAMILIES:
+        raise ValueError("unknown family: " + str(family))
+    if penalty not in PENALTIES:
+        raise ValueError("unknown penalty: " + str(penalty))
+    c = make_cfg(**cfg)
+    lam = None
+    if lambdas is not None:
+        lam = np.ascontiguousarray(np.asarray(lambdas, dtype=np.float64))
+    h = C.c_void_p()
+    design.ctx.check(_lib.load().kg_fit_path(design.ctx.h, design.h, obs.h, FAMILIES[family], float(dispersion),
+                                             PENALTIES[penalty], float(alpha), C.byref(c),
+                                             _ptr(lam) if lam is not None else None,
+                                             0 if lam is None else lam.size, C.byref(h)))
+    return PathResult(design, h)
+
+
+# ----------------------------------------------- reference module surface
+def linear_index(multi_index, dims):
+    """Column-major 1-based linear position (array.cpp:22-36)."""
+    d = len(dims)
+    if len(multi_index) != d:
+        raise ValueError("linear_index: index arity does not match dims")
+    r = _lib.load().kg_linear_index(d, (_i64 * d)(*multi_index), (_i64 * d)(*dims))
+    if r < 0:
+        raise ValueError("linear_index: index out of range")
+    return int(r)
+
+
+def rho(x, a):
+    """Rotated contraction of a matrix against the first array dimension (array.cpp:51-72)."""
+    x, a = _f(x), _f(a)
+    if x.ndim != 2:
+        raise ValueError("expected a 2-d array")
+    if a.shape[0] != x.shape[1]:
+        raise ValueError(f"rho: matrix has {x.shape[1]} columns but array's first extent is {a.shape[0]}")
+    ctx = default_context()
+    ext = list(a.shape)
+    out_shape = tuple(ext[1:]) + (x.shape[0],)
+    out = np.zeros(int(np.prod(out_shape)))
+    ctx.check(_lib.load().kg_rho(ctx.h, x.shape[0], _ptr(x), len(ext), (_i64 * len(ext))(*ext), _ptr(a),
+                                 _ptr(out)))
+    return out.reshape(out_shape, order="F")
+
+
+def _design(design):
+    return design if isinstance(design, Design) else Design(design)
+
+
+def h_map(design, coef):
+    """Linear predictor array, vec = X theta (design.cpp:89-102)."""
+    D = _design(design)
+    th = D.flat(coef)
+    eta = np.zeros(D.n)
+    D.ctx.check(_lib.load().kg_h_map(D.ctx.h, D.h, _ptr(th), _ptr(eta)))
+    return eta.reshape(D.row_dims, order="F")
+
+
+def g_map(design, u):
+    """Adjoint of h_map, vec = X^T vec(u) (design.cpp:104-116)."""
+    D = _design(design)
+    u = _f(u)
+    if u.shape != D.row_dims:
+        raise ValueError("g_map: array dimensions do not match")
+    out = np.zeros(D.p)
+    D.ctx.check(_lib.load().kg_g_map(D.ctx.h, D.h, _ptr(u), _ptr(out)))
+    return D.blocks(out)
+
+
+def xtwx_apply(design, v, coef):
+    """X^T diag(v) X theta (design.cpp:118-124)."""
+    D = _design(design)
+    v = _f(v)
+    th = D.flat(coef)
+    out = np.zeros(D.p)
+    D.ctx.check(_lib.load().kg_xtwx_apply(D.ctx.h, D.h, _ptr(v), _ptr(th), _ptr(out)))
+    return D.blocks(out)
+
+
+def lambda_max(design, family, y, weights=None):
+    """Smallest penalty level with an all-zero solution (penalty.cpp:72-85)."""
+    if family not in FAMILIES:
+        raise ValueError("unknown family: " + str(family))
+    D = _design(design)
+    obs = Observation(D, y, weights)
+    out = C.c_double()
+    D.ctx.check(_lib.load().kg_lambda_max(D.ctx.h, D.h, obs.h, FAMILIES[family], 1.0, 0, 0.0, C.byref(out)))
+    return out.value
+
+
+def fit_path(design, family, y, weights=None, penalty="lasso", alpha=0.0, n_lambda=100, lambda_min_ratio=1e-4,
+             lambdas=None, iwls="exact", nu=1.0, tol=1e-8, maxit=100, inner_tol=1e-8, inner_maxit=2000):
+    """Warm-started regularization path (path.cpp:29-81); same kwargs and result
+    keys as kronglm_py.cpp:159-217, plus ``inner_iters`` and ``status``."""
+    D = _design(design)
+    obs = Observation(D, y, weights)
+    res = fit_path_resident(D, obs, family, penalty, alpha, lambdas, n_lambda=n_lambda,
+                            lambda_min_ratio=lambda_min_ratio, iwls=iwls, nu=nu, tol=tol, maxit=maxit,
+                            inner_tol=inner_tol, inner_maxit=inner_maxit)
+    out = {"lambdas": list(res.lambdas), "objectives": list(res.objectives), "lambda_max": res.lambda_max,
+           "truncated": res.truncated, "coefficients": [], "nonzero": [], "outer_iters": list(res.outer_iters),
+           "converged": [s == "converged" for s in res.status], "inner_iters": list(res.inner_iters),
+           "status": list(res.status)}
+    for t in range(res.n_models):
+        flat = res.coef(t)
+        out["coefficients"].append(D.blocks(flat))
+        out["nonzero"].append(int(np.count_nonzero(flat)))
+    return out
+
+
+def predict(design, family, coef):
+    """Linear predictor and fitted mean arrays (path.cpp:83-89)."""
+    if family not in FAMILIES:
+        raise ValueError("unknown family: " + str(family))
+    D = _design(design)
+    th = D.flat(coef)
+    eta = np.zeros(D.n)
+    mu = np.zeros(D.n)
+    D.ctx.check(_lib.load().kg_predict(D.ctx.h, D.h, FAMILIES[family], _ptr(th), _ptr(eta), _ptr(mu)))
+    return eta.reshape(D.row_dims, order="F"), mu.reshape(D.row_dims, order="F")
+
+
+def bspline_design(points, order=4, n_basis=0):
+    """Marginal B-spline design on a clamped uniform knot vector (bspline.cpp:64-104)."""
+    pts = np.ascontiguousarray(np.asarray(points, dtype=np.float64))
+    out = np.zeros((pts.size, int(n_basis)), order="F")
+    st = _lib.load().kg_bspline_design(pts.size, _ptr(pts), int(order), int(n_basis), _ptr(out))
+    if st != 0:
+        raise ValueError("bspline_design: invalid grid or basis specification")
+    return out
+
+
+def default_basis_count(n_points, ratio):
+    """Basis-count rule max(ceil(n/ratio), 5) (bspline.cpp:20-26)."""
+    r = _lib.load().kg_default_basis_count(int(n_points), int(ratio))
+    if r < 0:
+        raise ValueError("default_basis_count: arguments must be positive")
+    return int(r)

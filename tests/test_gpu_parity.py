@@ -1,0 +1,258 @@
+"""GPU parity: the CUDA path (through the C ABI) against the CPU oracle and the
+dense Kronecker product, on the reference's own test designs and on B-spline
+designs shaped like the BASELINE configs.
+
+Tolerances: operator maps 1e-12 (test_array.cpp:142-193); path parity per
+lambda: identical truncation/status, identical support, coefficients within
+1e-8 relative to max|theta|, objectives within 1e-8 relative (north_star)."""
+import numpy as np
+import pytest
+
+from oracle import oracle as O
+from paper_1510_03298_b200 import configs
+from paper_1510_03298_b200 import kronglm as K
+from tests import helpers as H
+
+pytestmark = pytest.mark.gpu
+
+COEF_RTOL = 1e-8
+OBJ_RTOL = 1e-8
+
+
+def bspline_design(n, p):
+    return [[K.bspline_design(np.linspace(0, 1, nj), 4, pj) for nj, pj in zip(n, p)]]
+
+
+# --------------------------------------------------------------- operators
+def test_h_g_rho_match_dense_and_oracle_on_random_corpus():  # acceptance.cpp:53-80
+    rng = np.random.default_rng(1001)
+    for _ in range(60):
+        design = H.random_design(rng)
+        xd = H.dense(design)
+        th = H.random_coef(rng, design)
+        u = rng.uniform(-1, 1, H.row_dims(design))
+        h = K.h_map(design, th)
+        g = H.flat(K.g_map(design, u))
+        assert np.max(np.abs(h.ravel(order="F") - xd @ H.flat(th))) <= 1e-12
+        assert np.max(np.abs(g - xd.T @ u.ravel(order="F"))) <= 1e-12
+        assert np.max(np.abs(h - O.h_map(design, th))) <= 1e-12
+        lhs, rhs = float(np.vdot(h, u)), float(H.flat(th) @ g)
+        assert abs(lhs - rhs) <= 1e-12 * max(1.0, abs(rhs))
+        v = rng.uniform(0, 2, H.row_dims(design))
+        want = xd.T @ (v.ravel(order="F") * (xd @ H.flat(th)))
+        assert np.max(np.abs(H.flat(K.xtwx_apply(design, v, th)) - want)) <= 1e-12
+
+
+def test_rho_matches_oracle_and_rotates():
+    rng = np.random.default_rng(13)
+    a = rng.uniform(-1, 1, (3, 4, 2))
+    r = K.rho(np.eye(3), a)
+    assert r.shape == (4, 2, 3)
+    for i in range(3):
+        assert np.array_equal(r[:, :, i], a[i])
+    for xs, ashape in (((2, 3), (3, 4)), ((4, 2), (2, 3, 5)), ((4, 3), (3,))):
+        x = rng.standard_normal(xs)
+        a = rng.uniform(-1, 1, ashape)
+        assert np.max(np.abs(K.rho(x, a) - O.rho(x, a))) <= 1e-13
+    with pytest.raises(ValueError):
+        K.rho(rng.standard_normal((2, 4)), rng.uniform(-1, 1, (3, 4)))
+
+
+@pytest.mark.parametrize("n,p", [((40, 40, 40), (10, 10, 10)), ((64, 64, 365), (20, 20, 60)),
+                                 ((100, 100, 50), (30, 30, 12)), ((700, 300), (64, 40)), ((97,), (13,))])
+def test_bspline_maps_match_oracle(n, p):
+    rng = np.random.default_rng(7)
+    design = bspline_design(n, p)
+    th = [rng.standard_normal(p)]
+    u = rng.standard_normal(n)
+    h, ho = K.h_map(design, th), O.h_map(design, th)
+    assert np.max(np.abs(h - ho)) <= 1e-12 * max(1.0, np.max(np.abs(ho)))
+    g, go = H.flat(K.g_map(design, u)), H.flat(O.g_map(design, u))
+    assert np.max(np.abs(g - go)) <= 1e-12 * max(1.0, np.max(np.abs(go)))
+
+
+def test_spectral_radii_match_oracle():
+    rng = np.random.default_rng(50)
+    for n, p in ((40, 10), (64, 20), (365, 60), (256, 64)):
+        x = K.bspline_design(np.linspace(0, 1, n), 4, p)
+        D = K.Design([[x]])
+        assert D.spectral(0, 0) == pytest.approx(O.spectral_radius(x.T @ x), rel=1e-12)
+    x = rng.standard_normal((7, 5))
+    assert K.Design([[x]]).spectral(0, 0) == pytest.approx(np.linalg.eigvalsh(x.T @ x).max(), rel=1e-10)
+
+
+def test_lambda_max_matches_oracle_and_closed_form():  # test_penalty.cpp:107-137
+    rng = np.random.default_rng(44)
+    design = H.make_design(rng, (4, 3, 2), [(2, 2, 2)])
+    y = rng.standard_normal((4, 3, 2))
+    want = np.max(np.abs(H.dense(design).T @ y.ravel(order="F"))) / 24.0
+    assert K.lambda_max(design, "gaussian", y) == pytest.approx(want, rel=1e-13)
+    for fam in ("gaussian", "binomial", "poisson", "gamma"):
+        d = bspline_design((30, 20), (8, 6))
+        yy = H.random_data(rng, fam, (30, 20))
+        assert K.lambda_max(d, fam, yy) == pytest.approx(O.lambda_max(d, fam, yy), rel=1e-12)
+    d2 = H.make_design(rng, (3, 2), [(2, 2)])
+    assert K.lambda_max(d2, "gaussian", np.zeros((3, 2))) == 0.0
+    with pytest.raises(ValueError):
+        K.lambda_max(d2, "poisson", -np.ones((3, 2)))
+
+
+# -------------------------------------------------------------------- path
+def compare_paths(got, want, coef_rtol=COEF_RTOL, obj_rtol=OBJ_RTOL, check_iters=True):
+    assert got["truncated"] == want["truncated"]
+    assert len(got["lambdas"]) == len(want["lambdas"])
+    np.testing.assert_allclose(got["lambdas"], want["lambdas"], rtol=1e-13)
+    worst = 0.0
+    for t in range(len(want["lambdas"])):
+        cg, cw = H.flat(got["coefficients"][t]), H.flat(want["coefficients"][t])
+        assert np.array_equal(cg != 0, cw != 0), f"support differs at lambda {t}"
+        scale = max(np.max(np.abs(cw)), 1e-300)
+        err = np.max(np.abs(cg - cw)) / scale if cw.size else 0.0
+        worst = max(worst, err)
+        assert err <= coef_rtol, f"lambda {t}: coef rel err {err:.3e}"
+        fo, fg = want["objectives"][t], got["objectives"][t]
+        assert abs(fg - fo) <= obj_rtol * max(abs(fo), 1e-300), f"lambda {t}: objective"
+        if check_iters:
+            assert got["outer_iters"][t] == want["outer_iters"][t], f"lambda {t}: outer iterations"
+            assert got["inner_iters"][t] == want["inner_iters"][t], f"lambda {t}: inner iterations"
+    return worst
+
+
+def test_gaussian_path_matches_oracle_c1_shape():
+    d = configs.make("C1")
+    kw = dict(n_lambda=100, lambda_min_ratio=1e-4)
+    got = K.fit_path(d["design"], "gaussian", d["y"], **kw)
+    want = O.fit_path(d["design"], "gaussian", d["y"], **kw)
+    assert got["lambda_max"] == pytest.approx(want["lambda_max"], rel=1e-12)
+    compare_paths(got, want)
+
+
+def test_poisson_path_matches_oracle_small():
+    rng = np.random.default_rng(5)
+    design = bspline_design((24, 20, 30), (8, 6, 9))
+    B = np.zeros((8, 6, 9))
+    m = rng.random(B.shape) < 0.15
+    B[m] = rng.standard_normal(m.sum())
+    eta = configs.tensor_h(design[0], B)
+    y = rng.poisson(np.exp(np.log(20.0) / eta.max() * eta)).astype(float)
+    kw = dict(n_lambda=15, lambda_min_ratio=1e-3)
+    got = K.fit_path(design, "poisson", y, **kw)
+    want = O.fit_path(design, "poisson", y, **kw)
+    compare_paths(got, want)
+
+
+@pytest.mark.parametrize("fam", ["binomial", "gamma"])
+def test_other_families_match_oracle(fam):
+    rng = np.random.default_rng(11)
+    design = bspline_design((20, 18), (7, 6))
+    y = H.random_data(rng, fam, (20, 18))
+    kw = dict(n_lambda=8, lambda_min_ratio=1e-2)
+    compare_paths(K.fit_path(design, fam, y, **kw), O.fit_path(design, fam, y, **kw))
+
+
+def test_two_component_design_generic_route():  # c = 2: unfused route
+    rng = np.random.default_rng(72)
+    design = H.make_design(rng, (5, 4, 3), [(3, 2, 2), (2, 2, 1)])
+    eta = O.h_map(design, H.random_coef(rng, design, -0.7, 0.7))
+    y = eta + rng.normal(0, 0.3, eta.shape)
+    kw = dict(n_lambda=20, lambda_min_ratio=1e-3, inner_tol=1e-11)
+    compare_paths(K.fit_path(design, "gaussian", y, **kw), O.fit_path(design, "gaussian", y, **kw))
+    yp = rng.poisson(np.exp(0.3 * eta)).astype(float)
+    kw = dict(n_lambda=8, lambda_min_ratio=1e-2)
+    compare_paths(K.fit_path(design, "poisson", yp, **kw), O.fit_path(design, "poisson", yp, **kw))
+
+
+def test_penalties_weights_and_inner_options_match_oracle():
+    rng = np.random.default_rng(73)
+    design = bspline_design((16, 14, 6), (6, 5, 4))
+    y = rng.standard_normal((16, 14, 6))
+    a = np.ones_like(y)
+    a.ravel(order="F")[::4] = 0.0
+    af = np.asfortranarray(a)
+    lam = [0.05, 0.02, 0.01, 0.005]
+    for kw in (dict(penalty="ridge", lambdas=lam), dict(penalty="elasticnet", alpha=0.5, n_lambda=6),
+               dict(weights=af, n_lambda=6), dict(nu=0.5, n_lambda=6), dict(n_lambda=6, inner_maxit=7)):
+        got = K.fit_path(design, "gaussian", y, **kw)
+        want = O.fit_path(design, "gaussian", y, **kw)
+        compare_paths(got, want)
+    yp = rng.poisson(1.5, size=(16, 14, 6)).astype(float)
+    for kw in (dict(iwls="unit", n_lambda=5, lambda_min_ratio=1e-2), dict(n_lambda=5, lambda_min_ratio=1e-2,
+                                                                           weights=af)):
+        compare_paths(K.fit_path(design, "poisson", yp, **kw), O.fit_path(design, "poisson", yp, **kw))
+
+
+def test_masked_cells_insulated_on_gpu():  # test_path.cpp:115-138
+    rng = np.random.default_rng(74)
+    design = bspline_design((12, 10, 6), (5, 4, 3))
+    for fam in ("gaussian", "poisson"):
+        y = H.random_data(rng, fam, (12, 10, 6))
+        a = np.ones(y.size)
+        a[::4] = 0.0
+        a = a.reshape(y.shape, order="F")
+        base = K.fit_path(design, fam, y, weights=a, n_lambda=8, lambda_min_ratio=1e-2)
+        y2 = y.ravel(order="F").copy()
+        y2[::4] = 0.75
+        other = K.fit_path(design, fam, y2.reshape(y.shape, order="F"), weights=a, n_lambda=8,
+                           lambda_min_ratio=1e-2)
+        for c1, c2 in zip(base["coefficients"], other["coefficients"]):
+            assert np.max(np.abs(H.flat(c1) - H.flat(c2))) <= 1e-10
+
+
+def test_truncation_first_model_failure_and_errors():  # test_path.cpp:241-283
+    rng = np.random.default_rng(79)
+    design = H.make_design(rng, (5, 4, 3), [(2, 2, 2)])
+    y = H.random_data(rng, "poisson", (5, 4, 3))
+    lmax = K.lambda_max(design, "poisson", y)
+    p = K.fit_path(design, "poisson", y, n_lambda=6, lambda_min_ratio=1e-3, maxit=1, tol=1e-14)
+    q = O.fit_path(design, "poisson", y, n_lambda=6, lambda_min_ratio=1e-3, maxit=1, tol=1e-14)
+    assert p["truncated"] and len(p["lambdas"]) == len(q["lambdas"])
+    with pytest.raises(RuntimeError):
+        K.fit_path(design, "poisson", y, lambdas=[0.5 * lmax, 0.25 * lmax], maxit=1, tol=1e-14)
+    with pytest.raises(ValueError):
+        K.fit_path(design, "gaussian", y, penalty="ridge")
+    with pytest.raises(ValueError):
+        K.fit_path(design, "gaussian", y, lambdas=[0.1, 0.1])
+    with pytest.raises(ValueError):
+        K.fit_path(design, "poisson", -y - 1.0)
+
+
+def test_single_lambda_and_boundary():  # test_path.cpp:49-60, acceptance criterion 8
+    rng = np.random.default_rng(71)
+    design = H.make_design(rng, (4, 3), [(2, 3)])
+    y = rng.standard_normal((4, 3))
+    p = K.fit_path(design, "gaussian", y, n_lambda=1)
+    assert len(p["lambdas"]) == 1 and p["lambdas"][0] == p["lambda_max"]
+    assert np.max(np.abs(H.flat(p["coefficients"][0]))) == 0.0
+
+
+def test_predict_matches_dense():  # test_path.cpp:140-158
+    rng = np.random.default_rng(74)
+    design = H.make_design(rng, (4, 3), [(2, 3)])
+    th = H.random_coef(rng, design)
+    eta, mu = K.predict(design, "poisson", th)
+    e = H.dense(design) @ H.flat(th)
+    assert np.max(np.abs(eta.ravel(order="F") - e)) <= 1e-12
+    assert np.max(np.abs(mu.ravel(order="F") - np.exp(e))) <= 1e-12
+    eta0, mu0 = K.predict(design, "poisson", [np.zeros((2, 3))])
+    assert np.all(eta0 == 0.0) and np.all(mu0 == 1.0)
+
+
+def test_runs_are_bitwise_deterministic():  # test_outer.cpp:363-395 analogue
+    d = configs.make("C1")
+    a = K.fit_path(d["design"], "gaussian", d["y"], n_lambda=20)
+    b = K.fit_path(d["design"], "gaussian", d["y"], n_lambda=20)
+    for ca, cb in zip(a["coefficients"], b["coefficients"]):
+        assert np.array_equal(H.flat(ca), H.flat(cb))
+    assert a["objectives"] == b["objectives"]
+
+
+def test_full_size_adjoint_property_c2():
+    """Size-independent property at a BASELINE size: <H theta, u> = <theta, G u>."""
+    rng = np.random.default_rng(2)
+    d = configs.make("C2")
+    D = K.Design(d["design"])
+    th = [rng.standard_normal(d["p"])]
+    u = rng.standard_normal(d["n"])
+    lhs = float(np.vdot(K.h_map(D, th), u))
+    rhs = float(H.flat(th) @ H.flat(K.g_map(D, u)))
+    assert abs(lhs - rhs) <= 1e-11 * max(1.0, abs(rhs))
