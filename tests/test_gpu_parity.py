@@ -183,7 +183,7 @@ def test_penalties_weights_and_inner_options_match_oracle():
 
 def test_masked_cells_insulated_on_gpu():  # test_path.cpp:115-138
     rng = np.random.default_rng(74)
-    design = bspline_design((12, 10, 6), (5, 4, 3))
+    design = bspline_design((12, 10, 6), (5, 4, 4))
     for fam in ("gaussian", "poisson"):
         y = H.random_data(rng, fam, (12, 10, 6))
         a = np.ones(y.size)
