@@ -42,6 +42,9 @@ struct BandOp {
   const double* coef = nullptr;
   i64 rows = 0, cols = 0;
   int maxlen = 0;
+  const int* hlo = nullptr;   // host copies (planning only; never dereferenced on the device)
+  const int* hlen = nullptr;
+  uint64_t uid = 0;           // unique per uploaded operator (plan cache key)
 };
 
 // Device + host copies of one factor's operators.
@@ -61,6 +64,8 @@ struct FistaCtl {
   // configuration
   double lambda, tol, nu, n, lipfac;
   i64 max_iters, monitor_every;
+  double sscale;      // S used by the step = sscale * (stored S): 1, or the constant weight (Gram route)
+  double ss_const;    // added to the reduced weighted SS (Gram route: sum v z^2)
   double alpha;       // elastic-net weight
   int pen;            // 0 lasso, 1 ridge, 2 elastic net
   int extrapolation;  // 0 fista, 1 none
@@ -98,9 +103,18 @@ struct FusedArgs {
   double* partial = nullptr;   // one double per CTA (FISTA: sum v (eta - z)^2)
   i64* err = nullptr;          // SCORE0: first non-finite score cell
   i64 cell_base = 0;           // global flat index of local cell 0 (sharding)
+  int dbg = 0;                 // measurement only: 1 = copies only, 2 = copies + phase A
 };
 int fused_grid(const FusedArgs& f);
+// plain streaming read of two n-arrays (bandwidth reference for kg_time_kernel)
+void stream_read2(const Launch& L, i64 n, const double* x, const double* y, double* partial);
 void fused_mode1(const Launch& L, int variant, const FusedArgs& f);
+// bulk-async pipelined version (kg_fused.cu)
+bool fused_tma_fits(const FusedArgs& f, int variant);
+int fused_tma_grid(const FusedArgs& f, int variant);
+void fused_tma(const Launch& L, int variant, const FusedArgs& f);
+void contract_tiled(const Launch& L, const double* A, double* out, i64 a, i64 K, i64 M, i64 b, const BandOp& op,
+                    bool accumulate);
 
 // H-last (+ reductions) over mode 1.  If P is null, eta_new is an input
 // (already computed by a full H chain) and only the reductions run.
@@ -166,6 +180,12 @@ void ptrials(const Launch& L, i64 p, int pen, double alpha, const double* th, co
 void ptheta_update(const Launch& L, i64 p, double t, const double* th_t, double* th);
 void pcopy(const Launch& L, i64 p, const double* src, double* d0, double* d1, double* d2);
 void pmaxabs(const Launch& L, i64 p, const double* x, double* part);
+// Gram route: per-CTA partials of w <x, S x> - 2 <x, b>
+void gram_dots(const Launch& L, i64 p, double w, const double* x, const double* Sx, const double* b, double* part);
+// per-CTA partials of sum v z^2
+void wzz(const Launch& L, i64 n, const double* v, const double* z, double* part);
+// per-CTA (min, max) partials (2 per CTA)
+void minmax(const Launch& L, i64 n, const double* x, double* part);
 void fista_finalize(const Launch& L, const FistaCtl* ctl, i64 p, const double* x, double* best);
 
 // control / reductions (single CTA)

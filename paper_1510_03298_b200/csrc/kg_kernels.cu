@@ -8,6 +8,7 @@
 // point atomics), so results are bitwise reproducible run to run.
 #include <cfloat>
 #include <climits>
+#include <algorithm>
 
 #include "kg_internal.h"
 
@@ -105,7 +106,7 @@ inline void bump(const Launch& L) {
 }  // namespace
 
 int elem_grid(i64 n) { return grid_for(n, NT * 4, 148 * 8); }
-int pgrid(i64 p) { return grid_for(p, NT * 4, 148 * 4); }
+int pgrid(i64 p) { return grid_for(p, NT, 148 * 8); }
 
 // ------------------------------------------------------------ contraction
 // Mode-k banded contraction of A (a x K x b, column-major) with the operator
@@ -127,10 +128,64 @@ __global__ void __launch_bounds__(NT) k_contract(const double* __restrict__ A, d
   }
 }
 
+// Division by a loop-invariant divisor as multiply-high + shift (valid for
+// numerators < 2^31).
+struct FastDiv {
+  uint32_t d, m, s;
+  explicit FastDiv(uint32_t dd = 1) : d(dd), m(0), s(0) {
+    if (d > 1) {
+      uint32_t l = 0;
+      while ((1ull << l) < d) ++l;
+      m = static_cast<uint32_t>(((1ull << (31 + l)) + d - 1) / d);
+      s = l - 1;
+    }
+  }
+  __device__ __forceinline__ uint32_t div(uint32_t n) const { return d == 1 ? n : (__umulhi(n, m) >> s); }
+};
+
+// Same contraction with a 2-D launch: grid.x walks the (alpha, m) plane of
+// one beta slab, grid.y (+ grid.z) the slabs; one fast division per output.
+// The band loop keeps two partial sums so long G-direction bands pipeline.
+__global__ void __launch_bounds__(NT) k_contract2(const double* __restrict__ A, double* __restrict__ out, uint32_t a,
+                                                  uint32_t K, uint32_t M, uint32_t b, FastDiv fa, BandOp op,
+                                                  int accumulate) {
+  const uint32_t plane = a * M;
+  const uint32_t idx = blockIdx.x * NT + threadIdx.x;
+  const uint32_t be = blockIdx.y + gridDim.y * blockIdx.z;
+  if (idx >= plane || be >= b) return;
+  const uint32_t m = fa.div(idx);
+  const uint32_t al = idx - m * a;
+  const int lo = __ldg(op.lo + m), len = __ldg(op.len + m);
+  const double* c = op.coef + __ldg(op.off + m);
+  const double* src = A + static_cast<size_t>(be) * a * K + al + static_cast<size_t>(lo) * a;
+  double s0 = 0.0, s1 = 0.0;
+  int t = 0;
+  for (; t + 1 < len; t += 2) {
+    s0 = fma(__ldg(c + t), __ldg(src + static_cast<size_t>(t) * a), s0);
+    s1 = fma(__ldg(c + t + 1), __ldg(src + static_cast<size_t>(t + 1) * a), s1);
+  }
+  if (t < len) s0 = fma(__ldg(c + t), __ldg(src + static_cast<size_t>(t) * a), s0);
+  const double s = s0 + s1;
+  double* o = out + static_cast<size_t>(be) * plane + idx;
+  *o = accumulate ? *o + s : s;
+}
+
 void contract(const Launch& L, const double* A, double* out, i64 a, i64 K, i64 M, i64 b, const BandOp& op,
               bool accumulate) {
   const i64 total = a * M * b;
   if (total == 0) return;
+  if (a * M < (i64(1) << 31) && a * K < (i64(1) << 31) && b < (i64(1) << 31)) {
+    const i64 gx = (a * M + NT - 1) / NT;
+    const i64 gy = std::min<i64>(b, 65535);
+    const i64 gz = (b + gy - 1) / gy;
+    if (gx < (i64(1) << 31) && gz <= 65535) {
+      k_contract2<<<dim3(static_cast<unsigned>(gx), static_cast<unsigned>(gy), static_cast<unsigned>(gz)), NT, 0,
+                    L.s>>>(A, out, static_cast<uint32_t>(a), static_cast<uint32_t>(K), static_cast<uint32_t>(M),
+                           static_cast<uint32_t>(b), FastDiv(static_cast<uint32_t>(a)), op, accumulate);
+      bump(L);
+      return;
+    }
+  }
   const int g = grid_for(total, NT * 2, 148 * 16);
   if (a * K * b < (i64(1) << 31) && total < (i64(1) << 31)) {
     k_contract<uint32_t><<<g, NT, 0, L.s>>>(A, out, static_cast<uint32_t>(a), static_cast<uint32_t>(K),
@@ -496,7 +551,7 @@ __global__ void __launch_bounds__(NT) k_fista_update(const FistaCtl* __restrict_
                                                      double* x, double* xp, double* Sx, double* Sxp, const double* b,
                                                      double* best, double* Sbest, double* Jpart) {
   __shared__ double red[32];
-  const double omega = ctl->omega, delta = ctl->delta, lambda = ctl->lambda, n = ctl->n;
+  const double omega = ctl->omega, delta = ctl->delta, lambda = ctl->lambda, n = ctl->n, sscale = ctl->sscale;
   const int copy_best = ctl->copy_best, restart = ctl->restart;
   const double gamma = delta * lambda;
   double l1 = 0.0, l2 = 0.0;
@@ -512,7 +567,7 @@ __global__ void __launch_bounds__(NT) k_fista_update(const FistaCtl* __restrict_
     }
     const double yi = xi + omega * (xi - xpi);
     const double syi = sxi + omega * (sxi - sxpi);
-    const double g = (syi - b[i]) / n;
+    const double g = (sscale * syi - b[i]) / n;
     double ci = yi - delta * g;
     if (lambda > 0.0) ci = prox1(pen, alpha, gamma, ci);
     xp[i] = xi;
@@ -626,6 +681,60 @@ void pmaxabs(const Launch& L, i64 p, const double* x, double* part) {
   bump(L);
 }
 
+__global__ void __launch_bounds__(NT) k_gram_dots(i64 p, double w, const double* x, const double* Sx,
+                                                  const double* b, double* part) {
+  __shared__ double red[32];
+  double acc = 0.0;
+  for (i64 i = static_cast<i64>(blockIdx.x) * NT + threadIdx.x; i < p; i += static_cast<i64>(gridDim.x) * NT) {
+    const double xi = x[i];
+    acc += xi * (w * Sx[i] - 2.0 * b[i]);
+  }
+  const double r = block_reduce<false>(acc, red);
+  if (threadIdx.x == 0) part[blockIdx.x] = r;
+}
+
+void gram_dots(const Launch& L, i64 p, double w, const double* x, const double* Sx, const double* b, double* part) {
+  k_gram_dots<<<pgrid(p), NT, 0, L.s>>>(p, w, x, Sx, b, part);
+  bump(L);
+}
+
+__global__ void __launch_bounds__(NT) k_wzz(i64 n, const double* v, const double* z, double* part) {
+  __shared__ double red[32];
+  double acc = 0.0;
+  for (i64 i = static_cast<i64>(blockIdx.x) * NT + threadIdx.x; i < n; i += static_cast<i64>(gridDim.x) * NT) {
+    const double zi = z[i];
+    acc = fma(v[i], zi * zi, acc);
+  }
+  const double r = block_reduce<false>(acc, red);
+  if (threadIdx.x == 0) part[blockIdx.x] = r;
+}
+
+void wzz(const Launch& L, i64 n, const double* v, const double* z, double* part) {
+  k_wzz<<<elem_grid(n), NT, 0, L.s>>>(n, v, z, part);
+  bump(L);
+}
+
+__global__ void __launch_bounds__(NT) k_minmax(i64 n, const double* x, double* part) {
+  __shared__ double red[32];
+  double mn = DBL_MAX, mx = -DBL_MAX;
+  for (i64 i = static_cast<i64>(blockIdx.x) * NT + threadIdx.x; i < n; i += static_cast<i64>(gridDim.x) * NT) {
+    mn = fmin(mn, x[i]);
+    mx = fmax(mx, x[i]);
+  }
+  const double a = -block_reduce<true>(-mn, red);
+  __syncthreads();
+  const double b = block_reduce<true>(mx, red);
+  if (threadIdx.x == 0) {
+    part[2 * blockIdx.x] = a;
+    part[2 * blockIdx.x + 1] = b;
+  }
+}
+
+void minmax(const Launch& L, i64 n, const double* x, double* part) {
+  k_minmax<<<elem_grid(n), NT, 0, L.s>>>(n, x, part);
+  bump(L);
+}
+
 __global__ void __launch_bounds__(NT) k_fista_finalize(const FistaCtl* ctl, i64 p, const double* x, double* best) {
   if (!ctl->copy_best) return;
   for (i64 i = static_cast<i64>(blockIdx.x) * NT + threadIdx.x; i < p; i += static_cast<i64>(gridDim.x) * NT)
@@ -680,7 +789,7 @@ __global__ void __launch_bounds__(CT) k_fista_init(FistaCtl* c, const double* ss
   const double wmax = cta_max_col(vmax_part, n_vmax, 1, 0, sh);
   if (threadIdx.x != 0) return;
   // inner_objective (inner.cpp:109-119)
-  const double g0 = 0.5 * ss / c->n + c->lambda * penalty_of(c->pen, c->alpha, l1, l2);
+  const double g0 = 0.5 * (ss + c->ss_const) / c->n + c->lambda * penalty_of(c->pen, c->alpha, l1, l2);
   c->g_prev = g0;
   c->best_g = g0;
   // lipschitz_upper (inner.cpp:53-71): wmax * sum_r prod_j rho_rj / n
@@ -725,7 +834,7 @@ __global__ void __launch_bounds__(CT) k_fista_control(FistaCtl* c, const double*
   const i64 me = c->monitor_every < 1 ? 1 : c->monitor_every;
   const bool monitored = (it % me == 0) || it == c->max_iters;
   if (monitored) {
-    const double g = 0.5 * ss / c->n + c->lambda * penalty_of(c->pen, c->alpha, l1, l2);
+    const double g = 0.5 * (ss + c->ss_const) / c->n + c->lambda * penalty_of(c->pen, c->alpha, l1, l2);
     const bool bad = !isfinite(g);
     bool div = bad;
     if (!div && c->bt_div && g > c->g_prev) div = (++c->streak >= 3);

@@ -15,6 +15,7 @@
 #include <functional>
 
 #include <algorithm>
+#include <cstdlib>
 #include <cmath>
 #include <cstring>
 #include <limits>
@@ -121,7 +122,13 @@ static void build_band(const FactorHost& h, bool rows_of_x, std::vector<int>& lo
 struct FactorOwn {
   FactorDev dev;
   DBuf X, hlo, hlen, hoff, hcoef, glo, glen, goff, gcoef;
+  std::vector<int> h_lo, h_len, g_lo, g_len;  // host copies for launch planning
 };
+
+static uint64_t next_band_uid() {
+  static uint64_t uid = 0;
+  return ++uid;
+}
 
 static void upload_factor(const FactorHost& h, FactorOwn& f, cudaStream_t s) {
   f.dev.n = h.n;
@@ -129,8 +136,8 @@ static void upload_factor(const FactorHost& h, FactorOwn& f, cudaStream_t s) {
   f.X.alloc(sizeof(double) * h.n * h.p);
   KG_CUDA(cudaMemcpyAsync(f.X.p, h.X.data(), sizeof(double) * h.n * h.p, cudaMemcpyHostToDevice, s));
   f.dev.X = f.X.d();
-  auto up = [&](bool rows, DBuf& blo, DBuf& blen, DBuf& boff, DBuf& bcoef, BandOp& op) {
-    std::vector<int> lo, len;
+  auto up = [&](bool rows, DBuf& blo, DBuf& blen, DBuf& boff, DBuf& bcoef, BandOp& op, std::vector<int>& lo,
+                std::vector<int>& len) {
     std::vector<i64> off;
     std::vector<double> coef;
     int maxlen = 0;
@@ -150,9 +157,12 @@ static void upload_factor(const FactorHost& h, FactorOwn& f, cudaStream_t s) {
     op.rows = rows ? h.n : h.p;
     op.cols = rows ? h.p : h.n;
     op.maxlen = maxlen;
+    op.hlo = lo.data();
+    op.hlen = len.data();
+    op.uid = next_band_uid();
   };
-  up(true, f.hlo, f.hlen, f.hoff, f.hcoef, f.dev.H);
-  up(false, f.glo, f.glen, f.goff, f.gcoef, f.dev.G);
+  up(true, f.hlo, f.hlen, f.hoff, f.hcoef, f.dev.H, f.h_lo, f.h_len);
+  up(false, f.glo, f.glen, f.goff, f.gcoef, f.dev.G, f.g_lo, f.g_len);
 }
 
 // Spectral radius of X^T X for one factor: banded Gram + single-warp power
@@ -229,6 +239,9 @@ struct kg_design {
   kg::i64 N = 0, N_full = 0, P = 0;
   kg::i64 cell_base = 0;                   // global flat index of the first local cell
   std::vector<std::vector<std::unique_ptr<kg::FactorOwn>>> f;
+  // Gram blocks X_{m,j}^T X_{r,j} (design.cpp:126-151 with unit weight factors)
+  // as banded operators: gram[m][r][j]->dev.H maps p_{r,j} -> p_{m,j}.
+  std::vector<std::vector<std::vector<std::unique_ptr<kg::FactorOwn>>>> gram;
   std::vector<std::vector<double>> spectral;
   double lipfac = 0.0;                     // sum_r prod_j rho_rj (inner.cpp:61-70)
   bool fused = false;
@@ -242,6 +255,8 @@ struct kg_obs {
   const kg_design* design = nullptr;
   kg::DBuf y, a;
   bool unit_a = true;
+  bool a_const = true;  // every prior weight equal (to a_val): weights V are then a constant
+  double a_val = 1.0;
 };
 
 namespace kg {
@@ -317,13 +332,21 @@ struct Fit {
   DBuf part, scal, errs, ctl;
   const double* zptr = nullptr;  // z or y (Gaussian shortcut)
   int n_ss = 0;
-  // graph
-  cudaGraphExec_t exec = nullptr;
-  cudaGraph_t graph = nullptr;
-  i64 kernels_per_iter = 0;
+  // X^T W X route of the current inner problem: 0 = n-space pass (any weights),
+  // 1 = Gram route (constant weights W = wconst I: X^T W X = wconst (x)_j X_j^T X_j,
+  // the reference's xtwx_apply_tensor with constant weight factors)
+  int route = 0;
+  double wconst = 1.0;     // the constant weight (route 1)
+  bool c0_valid = false;   // F.scal[48] holds sum v z^2 for the current (v, z)
+  // one captured FISTA graph per route
+  cudaGraphExec_t exec[2] = {nullptr, nullptr};
+  cudaGraph_t graph[2] = {nullptr, nullptr};
+  i64 kernels_per_iter[2] = {0, 0};
   ~Fit() {
-    if (exec) cudaGraphExecDestroy(exec);
-    if (graph) cudaGraphDestroy(graph);
+    for (int r = 0; r < 2; ++r) {
+      if (exec[r]) cudaGraphExecDestroy(exec[r]);
+      if (graph[r]) cudaGraphDestroy(graph[r]);
+    }
   }
 };
 
@@ -392,6 +415,18 @@ static HlastArgs hlast_args(const Fit& F) {
   return h;
 }
 
+// Fused mode-1 pass: the bulk-async pipelined kernel when a double-buffered
+// tile fits shared memory, else the one-tile-per-CTA kernel.  Returns the
+// number of per-CTA partials written.
+static int run_fused(kg_ctx* ctx, int variant, const FusedArgs& a) {
+  if (fused_tma_fits(a, variant)) {
+    fused_tma(ctx->L(), variant, a);
+    return fused_tma_grid(a, variant);
+  }
+  fused_mode1(ctx->L(), variant, a);
+  return fused_grid(a);
+}
+
 // S(x) = X^T diag(v) X x into Sx, and per-CTA partials of sum v (eta - z)^2
 // into F.part (returns the number of partials).
 static int xwx_pass(Fit& F, const double* x, double* Sx) {
@@ -409,19 +444,40 @@ static int xwx_pass(Fit& F, const double* x, double* Sx) {
     a.v = F.v.d();
     a.z = F.zptr;
     a.partial = F.part.d();
-    fused_mode1(ctx->L(), FV_FISTA, a);
+    const int np = run_fused(ctx, FV_FISTA, a);
     if (D.d > 1) {
       std::vector<i64> dims = D.n;
       dims[0] = D.p[0][0];
       run_chain(ctx, dims, g_steps(D, 0, 1), F.Q.d(), Sx, F.s0.d(), F.s1.d(), false);
     }
-    return fused_grid(a);
+    return np;
   }
   for (i64 r = 0; r < D.c; ++r)
     run_chain(ctx, coef_dims(D, r), h_steps(D, r, 0), x + D.offs[r], F.hs.d(), F.s0.d(), F.s1.d(), r > 0);
   wss(ctx->L(), F.n, F.hs.d(), F.v.d(), F.zptr, F.w.d(), F.part.d());
   for (i64 r = 0; r < D.c; ++r) run_chain(ctx, D.n, g_steps(D, r, 0), F.w.d(), Sx + D.offs[r], F.s0.d(), F.s1.d(), false);
   return elem_grid(F.n);
+}
+
+// Gram route: S'(x) = ((x)_j X_j^T X_j) x (design.cpp:153-177 with unit
+// weight factors; the constant weight is applied as FistaCtl::sscale), then
+// per-CTA partials of wconst <x, S'x> - 2 <x, b> into F.part, so that
+// sum v (Xx - z)^2 = partials + sum v z^2 needs no n-space pass.
+static int gram_pass(Fit& F, const double* x, double* Sx) {
+  const kg_design& D = *F.D;
+  kg_ctx* ctx = F.ctx;
+  for (i64 m = 0; m < D.c; ++m)
+    for (i64 r = 0; r < D.c; ++r) {
+      std::vector<Step> st;
+      for (i64 j = D.d - 1; j >= 0; --j) st.push_back({static_cast<int>(j), &D.gram[m][r][j]->dev.H, D.p[m][j]});
+      run_chain(ctx, D.p[r], st, x + D.offs[r], Sx + D.offs[m], F.s0.d(), F.s1.d(), r > 0);
+    }
+  gram_dots(ctx->L(), F.p, F.wconst, x, Sx, F.b.d(), F.part.d());
+  return pgrid(F.p);
+}
+
+static int step_pass(Fit& F, const double* x, double* Sx) {
+  return F.route == 1 ? gram_pass(F, x, Sx) : xwx_pass(F, x, Sx);
 }
 
 // b = X^T (v .* z)
@@ -433,7 +489,7 @@ static void xtwz_pass(Fit& F) {
     a.v = F.v.d();
     a.z = F.zptr;
     a.Q = D.d > 1 ? F.Q.d() : F.b.d();
-    fused_mode1(ctx->L(), FV_XTWZ, a);
+    run_fused(ctx, FV_XTWZ, a);
     if (D.d > 1) {
       std::vector<i64> dims = D.n;
       dims[0] = D.p[0][0];
@@ -470,29 +526,55 @@ static int h_full(Fit& F, const double* coef, double* eta_out, HlastArgs h) {
 }
 
 // ---------------------------------------------------------------- FISTA
+// One FISTA iteration: p-space update -> X^T W X pass on the new iterate -> control.
+static void enqueue_body(Fit& F, cudaGraphConditionalHandle h, int use_handle) {
+  kg_ctx* ctx = F.ctx;
+  FistaCtl* c = static_cast<FistaCtl*>(F.ctl.p);
+  fista_update(ctx->L(), c, F.p, F.pen, F.alpha, F.x.d(), F.xp.d(), F.Sx.d(), F.Sxp.d(), F.b.d(), F.best.d(),
+               F.Sbest.d(), F.Jpart.d());
+  F.n_ss = step_pass(F, F.x.d(), F.Sx.d());
+  fista_control(ctx->L(), c, F.part.d(), F.n_ss, F.Jpart.d(), pgrid(F.p), h, use_handle);
+}
+
+// KG_HOST_LOOP=1: drive the FISTA loop from the host (one sync per
+// iteration) instead of the conditional graph, so profilers can see the
+// individual kernels.  Same kernels, same arithmetic.
+static bool host_loop_mode() {
+  static const bool on = [] {
+    const char* e = std::getenv("KG_HOST_LOOP");
+    return e && e[0] == '1';
+  }();
+  return on;
+}
+
+// Captures the FISTA loop of the current route once: a gate kernel, then a
+// conditional WHILE node whose body is one iteration.  Every scalar the body
+// needs (lambda, step, omega, flags) is read from the device control block, and
+// the Gram-route weight from F.wconst is baked in, so the graph is re-launched
+// for every lambda and every outer iteration of the fit.
 static void build_graph(Fit& F) {
   kg_ctx* ctx = F.ctx;
+  const int r = F.route;
   cudaStream_t cap;
   KG_CUDA(cudaStreamCreateWithFlags(&cap, cudaStreamNonBlocking));
-  KG_CUDA(cudaGraphCreate(&F.graph, 0));
+  KG_CUDA(cudaGraphCreate(&F.graph[r], 0));
   cudaGraphConditionalHandle h;
-  KG_CUDA(cudaGraphConditionalHandleCreate(&h, F.graph, 0, cudaGraphCondAssignDefault));
-  // gate node: enter the loop only if fista_init left the solve running
-  KG_CUDA(cudaStreamBeginCaptureToGraph(cap, F.graph, nullptr, nullptr, 0, cudaStreamCaptureModeThreadLocal));
+  KG_CUDA(cudaGraphConditionalHandleCreate(&h, F.graph[r], 0, cudaGraphCondAssignDefault));
+  KG_CUDA(cudaStreamBeginCaptureToGraph(cap, F.graph[r], nullptr, nullptr, 0, cudaStreamCaptureModeThreadLocal));
   fista_gate(Launch{cap, nullptr}, static_cast<FistaCtl*>(F.ctl.p), h);
-  KG_CUDA(cudaStreamEndCapture(cap, &F.graph));
+  KG_CUDA(cudaStreamEndCapture(cap, &F.graph[r]));
   size_t nn = 0;
-  KG_CUDA(cudaGraphGetNodes(F.graph, nullptr, &nn));
+  KG_CUDA(cudaGraphGetNodes(F.graph[r], nullptr, &nn));
   if (nn != 1) throw Error(E_CUDA, "unexpected gate capture");
   cudaGraphNode_t gate;
-  KG_CUDA(cudaGraphGetNodes(F.graph, &gate, &nn));
+  KG_CUDA(cudaGraphGetNodes(F.graph[r], &gate, &nn));
   cudaGraphNodeParams cp = {};
   cp.type = cudaGraphNodeTypeConditional;
   cp.conditional.handle = h;
   cp.conditional.type = cudaGraphCondTypeWhile;
   cp.conditional.size = 1;
   cudaGraphNode_t node;
-  KG_CUDA(cudaGraphAddNode(&node, F.graph, &gate, 1, &cp));
+  KG_CUDA(cudaGraphAddNode(&node, F.graph[r], &gate, 1, &cp));
   cudaGraph_t body = cp.conditional.phGraph_out[0];
   KG_CUDA(cudaStreamBeginCaptureToGraph(cap, body, nullptr, nullptr, 0, cudaStreamCaptureModeThreadLocal));
   cudaStream_t saved = ctx->s;
@@ -500,11 +582,7 @@ static void build_graph(Fit& F) {
   ctx->s = cap;
   ctx->launches = 0;
   try {
-    FistaCtl* c = static_cast<FistaCtl*>(F.ctl.p);
-    fista_update(ctx->L(), c, F.p, F.pen, F.alpha, F.x.d(), F.xp.d(), F.Sx.d(), F.Sxp.d(), F.b.d(), F.best.d(),
-                 F.Sbest.d(), F.Jpart.d());
-    F.n_ss = xwx_pass(F, F.x.d(), F.Sx.d());
-    fista_control(ctx->L(), c, F.part.d(), F.n_ss, F.Jpart.d(), pgrid(F.p), h, 1);
+    enqueue_body(F, h, 1);
   } catch (...) {
     ctx->s = saved;
     ctx->launches = saved_count;
@@ -513,12 +591,12 @@ static void build_graph(Fit& F) {
     cudaStreamDestroy(cap);
     throw;
   }
-  F.kernels_per_iter = ctx->launches;
+  F.kernels_per_iter[r] = ctx->launches;
   ctx->s = saved;
   ctx->launches = saved_count;
   KG_CUDA(cudaStreamEndCapture(cap, &body));
   KG_CUDA(cudaStreamDestroy(cap));
-  KG_CUDA(cudaGraphInstantiate(&F.exec, F.graph, 0));
+  KG_CUDA(cudaGraphInstantiate(&F.exec[r], F.graph[r], 0));
 }
 
 struct FistaOut {
@@ -534,12 +612,14 @@ struct InnerCfg {
 };
 
 // Enqueues fista_solve(init = theta) with weights F.v (max-partials in
-// vmax_part) and working response F.zptr; F.b must hold X^T(v.*z).  The
-// result lands in F.best; the control block is copied to ctx->pin() + PIN_CTL.
+// vmax_part) and working response F.zptr; F.b must hold X^T(v.*z) and, on the
+// Gram route (F.route == 1), F.wconst / F.c0 the constant weight and sum v z^2.
+// The result lands in F.best; the control block is copied to ctx->pin() + PIN_CTL.
 static void fista_enqueue(Fit& F, double lambda, const InnerCfg& ic, const double* vmax_part, int n_vmax) {
   kg_ctx* ctx = F.ctx;
   if (!(ic.nu >= 0.0 && ic.nu <= 1.0)) throw Error(E_INVAL, "fista_solve: nu must lie in [0,1]");
-  if (ic.nu == 0.0) throw Error(E_INVAL, "fista_solve: nu = 0 (backtracking every iteration) is not supported by the device solver");
+  if (ic.nu == 0.0)
+    throw Error(E_INVAL, "fista_solve: nu = 0 (backtracking every iteration) is not supported by the device solver");
   FistaCtl h{};
   h.lambda = lambda;
   h.tol = ic.tol;
@@ -548,6 +628,8 @@ static void fista_enqueue(Fit& F, double lambda, const InnerCfg& ic, const doubl
   h.lipfac = F.D->lipfac;
   h.max_iters = ic.max_iters;
   h.monitor_every = ic.monitor_every;
+  h.sscale = F.route == 1 ? F.wconst : 1.0;
+  h.ss_const = 0.0;  // Gram route: filled on the device below
   h.alpha = F.alpha;
   h.pen = F.pen;
   h.extrapolation = ic.extrapolation;
@@ -556,15 +638,39 @@ static void fista_enqueue(Fit& F, double lambda, const InnerCfg& ic, const doubl
   KG_CUDA(cudaStreamSynchronize(ctx->s));  // the pinned staging slot is reused
   *staged = h;
   KG_CUDA(cudaMemcpyAsync(F.ctl.p, staged, sizeof(FistaCtl), cudaMemcpyHostToDevice, ctx->s));
+  if (F.route == 1) {  // sum v z^2, once per (v, z)
+    if (!F.c0_valid) {
+      wzz(ctx->L(), F.n, F.v.d(), F.zptr, F.part.d());
+      reduce_cols(ctx->L(), F.part.d(), elem_grid(F.n), 1, 0, F.scal.d() + 48);
+      F.c0_valid = true;
+    }
+    KG_CUDA(cudaMemcpyAsync(&static_cast<FistaCtl*>(F.ctl.p)->ss_const, F.scal.d() + 48, sizeof(double),
+                            cudaMemcpyDeviceToDevice, ctx->s));
+  }
   pcopy(ctx->L(), F.p, F.theta.d(), F.x.d(), F.xp.d(), F.best.d());
-  const int n_ss = xwx_pass(F, F.x.d(), F.Sx.d());
+  const int n_ss = step_pass(F, F.x.d(), F.Sx.d());
   pnorm(ctx->L(), F.p, F.pen, F.alpha, F.x.d(), F.Jpart.d());
   pcopy(ctx->L(), F.p, F.Sx.d(), F.Sxp.d(), F.Sbest.d(), nullptr);
   fista_init(ctx->L(), static_cast<FistaCtl*>(F.ctl.p), F.part.d(), n_ss, F.Jpart.d(), pgrid(F.p), vmax_part, n_vmax,
              0);
   if (ic.max_iters >= 1) {
-    if (!F.exec) build_graph(F);
-    KG_CUDA(cudaGraphLaunch(F.exec, ctx->s));
+    if (host_loop_mode()) {
+      const FistaCtl* hc = reinterpret_cast<const FistaCtl*>(ctx->pin() + PIN_CTL);
+      i64 before = ctx->launches;
+      for (;;) {
+        KG_CUDA(cudaMemcpyAsync(ctx->pin() + PIN_CTL, F.ctl.p, sizeof(FistaCtl), cudaMemcpyDeviceToHost, ctx->s));
+        sync(ctx);
+        if (hc->done) break;
+        enqueue_body(F, cudaGraphConditionalHandle{}, 0);
+      }
+      // fista_read() adds iterations * kernels_per_iter; undo the direct count
+      const i64 its = hc->iterations;
+      F.kernels_per_iter[F.route] = its > 0 ? (ctx->launches - before) / its : 0;
+      ctx->launches = before;
+    } else {
+      if (!F.exec[F.route]) build_graph(F);
+      KG_CUDA(cudaGraphLaunch(F.exec[F.route], ctx->s));
+    }
   }
   fista_finalize(ctx->L(), static_cast<FistaCtl*>(F.ctl.p), F.p, F.x.d(), F.best.d());
   KG_CUDA(cudaMemcpyAsync(ctx->pin() + PIN_CTL, F.ctl.p, sizeof(FistaCtl), cudaMemcpyDeviceToHost, ctx->s));
@@ -579,7 +685,7 @@ static FistaOut fista_read(Fit& F) {
   o.converged = c->converged;
   o.diverged = c->diverged;
   o.bad_weights = c->bad_weights;
-  F.ctx->launches += o.iterations * F.kernels_per_iter;
+  F.ctx->launches += o.iterations * F.kernels_per_iter[F.route];
   return o;
 }
 
@@ -624,7 +730,7 @@ static double lambda_max_fit(Fit& F) {
     a.disp = F.disp;
     a.err = F.errs.l();
     a.Q = D.d > 1 ? F.Q.d() : F.b.d();
-    fused_mode1(ctx->L(), FV_SCORE0, a);
+    run_fused(ctx, FV_SCORE0, a);
     if (D.d > 1) {
       std::vector<i64> dims = D.n;
       dims[0] = D.p[0][0];
@@ -782,6 +888,10 @@ static ModelTrace outer_loop(Fit& F, double lambda, const OuterCfg& oc) {
     fa.err = F.errs.l() + ERR_FAM;
     fa.cell_base = D.cell_base;
     family_pass(ctx->L(), fa);
+    // unit weights (outer.cpp:234-238): X^T W X is the plain Gram product
+    F.route = fa.mode == 1 ? 1 : 0;
+    F.wconst = 1.0;
+    F.c0_valid = false;
     F.zptr = F.z.d();
     xtwz_pass(F);
     fista_enqueue(F, lambda, oc.inner, vmax_part, n_vmax);
@@ -989,6 +1099,12 @@ static kg_path_result* fit_path(kg_ctx* ctx, const kg_design* D, const kg_obs* O
     gauss_weights(ctx->L(), F->n, disp, O->a.d(), F->v.d(), F->part.d() + D->part_cap - n_vmax);
     F->zptr = O->y.d();
     xtwz_pass(*F);
+    // constant prior weights: V = a/disp is a constant, use the Gram route
+    if (O->a_const) {
+      F->route = 1;
+      F->wconst = (std::max(1.0, 1e-10) / disp) * O->a_val;
+      F->c0_valid = false;
+    }
     // loglik at eta = 0
     reset_errs(*F);
     HlastArgs h = hlast_args(*F);
@@ -1189,6 +1305,50 @@ kg_status kg_design_create(kg_ctx* ctx, int64_t c, int64_t d, const int64_t* n, 
       }
       D->lipfac += pr;
     }
+    // Gram blocks X_{m,j}^T X_{r,j} of the full factors (ascending-row sums
+    // over the overlap of the two column bands), uploaded as banded operators.
+    D->gram.resize(c);
+    for (i64 m = 0; m < c; ++m) {
+      D->gram[m].resize(c);
+      for (i64 r = 0; r < c; ++r)
+        for (i64 j = 0; j < d; ++j) {
+          const double* Xm = factors[m * d + j];
+          const double* Xr = factors[r * d + j];
+          const i64 nj = D->n_full[j], pm = D->p[m][j], pr_ = D->p[r][j];
+          auto cband = [&](const double* X, i64 p, std::vector<i64>& lo, std::vector<i64>& hi) {
+            lo.assign(p, 0);
+            hi.assign(p, 0);
+            for (i64 k = 0; k < p; ++k) {
+              i64 f = -1, l = -1;
+              for (i64 i = 0; i < nj; ++i)
+                if (X[i + nj * k] != 0.0) {
+                  if (f < 0) f = i;
+                  l = i;
+                }
+              if (f >= 0) {
+                lo[k] = f;
+                hi[k] = l + 1;
+              }
+            }
+          };
+          std::vector<i64> mlo, mhi, rlo, rhi;
+          cband(Xm, pm, mlo, mhi);
+          cband(Xr, pr_, rlo, rhi);
+          FactorHost g;
+          g.n = pm;
+          g.p = pr_;
+          g.X.assign(pm * pr_, 0.0);
+          for (i64 b = 0; b < pr_; ++b)
+            for (i64 a = 0; a < pm; ++a) {
+              double s = 0.0;
+              for (i64 i = std::max(mlo[a], rlo[b]); i < std::min(mhi[a], rhi[b]); ++i) s += Xm[i + nj * a] * Xr[i + nj * b];
+              g.X[a + pm * b] = s;
+            }
+          auto go = std::make_unique<FactorOwn>();
+          upload_factor(g, *go, ctx->s);
+          D->gram[m][r].push_back(std::move(go));
+        }
+    }
     // fused mode-1 route for one component whose mode-1 fibre tile fits shared memory
     const i64 n1 = D->n[0], p1 = D->p[0][0], m = D->N / n1;
     D->fused = c == 1 && (n1 + p1) * 8 <= 96 * 1024;
@@ -1241,6 +1401,21 @@ kg_status kg_obs_create(kg_ctx* ctx, const kg_design* design, const double* y, c
     if (a) {
       KG_CUDA(cudaMemcpyAsync(O->a.p, a, nb, k, ctx->s));
       O->unit_a = false;
+      // are all prior weights equal?  (then W is a constant and the Gram route applies)
+      DBuf part;
+      const int g = elem_grid(design->N);
+      part.alloc(sizeof(double) * 2 * g);
+      minmax(ctx->L(), design->N, O->a.d(), part.d());
+      sync(ctx);
+      std::vector<double> hp(2 * g);  // per-CTA (min, max) -> global min / max
+      KG_CUDA(cudaMemcpy(hp.data(), part.p, sizeof(double) * 2 * g, cudaMemcpyDeviceToHost));
+      double mn = hp[0], mx = hp[1];
+      for (int i = 0; i < g; ++i) {
+        mn = std::min(mn, hp[2 * i]);
+        mx = std::max(mx, hp[2 * i + 1]);
+      }
+      O->a_const = mn == mx;
+      O->a_val = mn;
     } else {
       fill(ctx->L(), design->N, 1.0, O->a.d());  // ObservationData(y): a = 1 (family.hpp:44-45)
     }
@@ -1460,7 +1635,12 @@ kg_status kg_time_kernel(kg_ctx* ctx, const kg_design* D, const kg_obs* O, int w
     KG_CUDA(cudaEventCreate(&e1));
     std::function<void()> launch;
     double b = 0.0;
-    if (which == 0) {
+    if (which == 2) {  // bandwidth reference: plain read of two n-arrays
+      const double* y = O->y.d();
+      const double* v = F.v.d();
+      launch = [&, y, v] { stream_read2(ctx->L(), F.n, y, v, F.part.d()); };
+      b = 16.0 * static_cast<double>(F.n);
+    } else if (which == 0 || which == 3 || which == 4) {
       if (!D->fused) throw Error(E_INVAL, "the fused pass needs a one-component design");
       const double* P = F.x.d();
       if (D->d > 1) {
@@ -1473,7 +1653,8 @@ kg_status kg_time_kernel(kg_ctx* ctx, const kg_design* D, const kg_obs* O, int w
       a.v = F.v.d();
       a.z = F.zptr;
       a.partial = F.part.d();
-      launch = [&, a] { fused_mode1(ctx->L(), FV_FISTA, a); };
+      a.dbg = which == 3 ? 1 : (which == 4 ? 2 : 0);  // 3: copies only, 4: copies + phase A
+      launch = [&, a] { run_fused(ctx, FV_FISTA, a); };
       // P (p1 x m) read, v and z read, Q (p1 x m) written
       b = 8.0 * (2.0 * static_cast<double>(F.n) + 2.0 * static_cast<double>(a.p1 * a.m));
     } else {

@@ -181,6 +181,26 @@ def test_penalties_weights_and_inner_options_match_oracle():
         compare_paths(K.fit_path(design, "poisson", yp, **kw), O.fit_path(design, "poisson", yp, **kw))
 
 
+def test_constant_weight_gram_route_matches_oracle():
+    """Constant prior weights take the Gram route (X^T W X = w (x)_j X_j^T X_j); a
+    weight array with one differing cell takes the n-space route.  Both must
+    match the oracle's n-space restatement."""
+    rng = np.random.default_rng(81)
+    design = bspline_design((18, 15, 8), (7, 6, 4))
+    B = np.zeros((7, 6, 4))
+    m = rng.random(B.shape) < 0.2
+    B[m] = rng.standard_normal(m.sum())
+    y = np.asfortranarray(configs.tensor_h(design[0], B) + 0.5 * rng.standard_normal((18, 15, 8)))
+    a = np.full(y.shape, 2.5, order="F")
+    kw = dict(n_lambda=12, lambda_min_ratio=1e-3)
+    compare_paths(K.fit_path(design, "gaussian", y, weights=a, **kw),
+                  O.fit_path(design, "gaussian", y, weights=a, **kw))
+    a2 = a.copy()
+    a2[3, 4, 5] = 2.0
+    compare_paths(K.fit_path(design, "gaussian", y, weights=a2, **kw),
+                  O.fit_path(design, "gaussian", y, weights=a2, **kw))
+
+
 def test_masked_cells_insulated_on_gpu():  # test_path.cpp:115-138
     rng = np.random.default_rng(74)
     design = bspline_design((12, 10, 6), (5, 4, 4))
