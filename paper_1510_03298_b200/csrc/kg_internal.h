@@ -186,7 +186,36 @@ void gram_dots(const Launch& L, i64 p, double w, const double* x, const double* 
 void wzz(const Launch& L, i64 n, const double* v, const double* z, double* part);
 // per-CTA (min, max) partials (2 per CTA)
 void minmax(const Launch& L, i64 n, const double* x, double* part);
-void fista_finalize(const Launch& L, const FistaCtl* ctl, i64 p, const double* x, double* best);
+void fista_finalize(const Launch& L, const FistaCtl* ctl, i64 p, const double* x, double* best, const double* Sx,
+                    double* Sbest);
+
+// One-kernel FISTA iteration on the constant-weight Gram route (kg_gram.cu).
+struct GramStepArgs {
+  FistaCtl* ctl = nullptr;
+  int d = 0;           // number of modes (<= 4)
+  int q = 1;           // slab size p_1 ... p_{d-1}
+  i64 pd = 1;          // slabs (p_d)
+  int dims[4] = {1, 1, 1, 1};
+  BandOp Gd;           // Gram of the last mode
+  BandOp G[3];         // Grams of modes 0 .. d-2
+  double* X[3] = {nullptr, nullptr, nullptr};
+  double* S[3] = {nullptr, nullptr, nullptr};
+  const double* b = nullptr;
+  double* best = nullptr;
+  double* Sbest = nullptr;
+  int pen = 0;
+  double alpha = 0.0;
+  double* part = nullptr;      // 3 per CTA
+  unsigned* counter = nullptr;  // zero-initialised ticket
+  cudaGraphConditionalHandle handle = 0;
+  int use_handle = 0;
+  int init = 0;                // 1: compute S'(x_0) and the fista_solve setup, no step
+};
+bool gram_step_fits(i64 q);
+void gram_step(const Launch& L, const GramStepArgs& A);
+void gram_finalize(const Launch& L, const FistaCtl* ctl, i64 p, const GramStepArgs& A);
+int gauss_dots(const Launch& L, i64 p, double w, const double* th, const double* Sth, const double* bt,
+               const double* Sbt, const double* b, double* part);
 
 // control / reductions (single CTA)
 void fista_init(const Launch& L, FistaCtl* ctl, const double* ss_part, int n_ss, const double* J_part, int n_J,

@@ -735,14 +735,19 @@ void minmax(const Launch& L, i64 n, const double* x, double* part) {
   bump(L);
 }
 
-__global__ void __launch_bounds__(NT) k_fista_finalize(const FistaCtl* ctl, i64 p, const double* x, double* best) {
+// best := x (and S(best) := S(x)) when the last monitor left a copy pending
+__global__ void __launch_bounds__(NT) k_fista_finalize(const FistaCtl* ctl, i64 p, const double* x, double* best,
+                                                       const double* Sx, double* Sbest) {
   if (!ctl->copy_best) return;
-  for (i64 i = static_cast<i64>(blockIdx.x) * NT + threadIdx.x; i < p; i += static_cast<i64>(gridDim.x) * NT)
+  for (i64 i = static_cast<i64>(blockIdx.x) * NT + threadIdx.x; i < p; i += static_cast<i64>(gridDim.x) * NT) {
     best[i] = x[i];
+    Sbest[i] = Sx[i];
+  }
 }
 
-void fista_finalize(const Launch& L, const FistaCtl* ctl, i64 p, const double* x, double* best) {
-  k_fista_finalize<<<pgrid(p), NT, 0, L.s>>>(ctl, p, x, best);
+void fista_finalize(const Launch& L, const FistaCtl* ctl, i64 p, const double* x, double* best, const double* Sx,
+                    double* Sbest) {
+  k_fista_finalize<<<pgrid(p), NT, 0, L.s>>>(ctl, p, x, best, Sx, Sbest);
   bump(L);
 }
 

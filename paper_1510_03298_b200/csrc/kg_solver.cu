@@ -338,6 +338,9 @@ struct Fit {
   int route = 0;
   double wconst = 1.0;     // the constant weight (route 1)
   bool c0_valid = false;   // F.scal[48] holds sum v z^2 for the current (v, z)
+  // route 1 with one component: one fused kernel per iteration (kg_gram.cu)
+  bool gstep = false;
+  DBuf X3[3], S3[3], gpart, gcount, stheta;
   // one captured FISTA graph per route
   cudaGraphExec_t exec[2] = {nullptr, nullptr};
   cudaGraph_t graph[2] = {nullptr, nullptr};
@@ -376,6 +379,19 @@ static void alloc_fit(Fit& F) {
   F.scal.alloc(sizeof(double) * 64);
   F.errs.alloc(sizeof(i64) * 16);
   F.ctl.alloc(sizeof(FistaCtl));
+  F.stheta.alloc(pb);
+  // one-kernel Gram step: one component, d <= 4, slab fits shared memory
+  const i64 pd = D.p[0][D.d - 1];
+  F.gstep = D.c == 1 && D.d <= 4 && gram_step_fits(D.P / pd);
+  if (F.gstep) {
+    for (int r = 0; r < 3; ++r) {
+      F.X3[r].alloc(pb);
+      F.S3[r].alloc(pb);
+    }
+    F.gpart.alloc(sizeof(double) * 3 * pd);
+    F.gcount.alloc(sizeof(unsigned) * 4);
+    KG_CUDA(cudaMemsetAsync(F.gcount.p, 0, sizeof(unsigned) * 4, F.ctx->s));
+  }
 }
 
 static void reset_errs(Fit& F) {
@@ -526,9 +542,42 @@ static int h_full(Fit& F, const double* coef, double* eta_out, HlastArgs h) {
 }
 
 // ---------------------------------------------------------------- FISTA
+static GramStepArgs gstep_args(Fit& F) {
+  const kg_design& D = *F.D;
+  GramStepArgs A;
+  A.ctl = static_cast<FistaCtl*>(F.ctl.p);
+  A.d = static_cast<int>(D.d);
+  A.pd = D.p[0][D.d - 1];
+  A.q = static_cast<int>(D.P / A.pd);
+  for (i64 j = 0; j + 1 < D.d; ++j) {
+    A.dims[j] = static_cast<int>(D.p[0][j]);
+    A.G[j] = D.gram[0][0][j]->dev.H;
+  }
+  A.Gd = D.gram[0][0][D.d - 1]->dev.H;
+  for (int r = 0; r < 3; ++r) {
+    A.X[r] = F.X3[r].d();
+    A.S[r] = F.S3[r].d();
+  }
+  A.b = F.b.d();
+  A.best = F.best.d();
+  A.Sbest = F.Sbest.d();
+  A.pen = F.pen;
+  A.alpha = F.alpha;
+  A.part = F.gpart.d();
+  A.counter = static_cast<unsigned*>(F.gcount.p);
+  return A;
+}
+
 // One FISTA iteration: p-space update -> X^T W X pass on the new iterate -> control.
 static void enqueue_body(Fit& F, cudaGraphConditionalHandle h, int use_handle) {
   kg_ctx* ctx = F.ctx;
+  if (F.route == 1 && F.gstep) {
+    GramStepArgs A = gstep_args(F);
+    A.handle = h;
+    A.use_handle = use_handle;
+    gram_step(ctx->L(), A);
+    return;
+  }
   FistaCtl* c = static_cast<FistaCtl*>(F.ctl.p);
   fista_update(ctx->L(), c, F.p, F.pen, F.alpha, F.x.d(), F.xp.d(), F.Sx.d(), F.Sxp.d(), F.b.d(), F.best.d(),
                F.Sbest.d(), F.Jpart.d());
@@ -647,12 +696,20 @@ static void fista_enqueue(Fit& F, double lambda, const InnerCfg& ic, const doubl
     KG_CUDA(cudaMemcpyAsync(&static_cast<FistaCtl*>(F.ctl.p)->ss_const, F.scal.d() + 48, sizeof(double),
                             cudaMemcpyDeviceToDevice, ctx->s));
   }
-  pcopy(ctx->L(), F.p, F.theta.d(), F.x.d(), F.xp.d(), F.best.d());
-  const int n_ss = step_pass(F, F.x.d(), F.Sx.d());
-  pnorm(ctx->L(), F.p, F.pen, F.alpha, F.x.d(), F.Jpart.d());
-  pcopy(ctx->L(), F.p, F.Sx.d(), F.Sxp.d(), F.Sbest.d(), nullptr);
-  fista_init(ctx->L(), static_cast<FistaCtl*>(F.ctl.p), F.part.d(), n_ss, F.Jpart.d(), pgrid(F.p), vmax_part, n_vmax,
-             0);
+  const bool one_kernel = F.route == 1 && F.gstep;
+  if (one_kernel) {  // x_0 -> X3[2]; the init launch computes S'(x_0), g_0 and the step size
+    pcopy(ctx->L(), F.p, F.theta.d(), F.X3[2].d(), nullptr, nullptr);
+    GramStepArgs A = gstep_args(F);
+    A.init = 1;
+    gram_step(ctx->L(), A);
+  } else {
+    pcopy(ctx->L(), F.p, F.theta.d(), F.x.d(), F.xp.d(), F.best.d());
+    const int n_ss = step_pass(F, F.x.d(), F.Sx.d());
+    pnorm(ctx->L(), F.p, F.pen, F.alpha, F.x.d(), F.Jpart.d());
+    pcopy(ctx->L(), F.p, F.Sx.d(), F.Sxp.d(), F.Sbest.d(), nullptr);
+    fista_init(ctx->L(), static_cast<FistaCtl*>(F.ctl.p), F.part.d(), n_ss, F.Jpart.d(), pgrid(F.p), vmax_part,
+               n_vmax, 0);
+  }
   if (ic.max_iters >= 1) {
     if (host_loop_mode()) {
       const FistaCtl* hc = reinterpret_cast<const FistaCtl*>(ctx->pin() + PIN_CTL);
@@ -672,7 +729,10 @@ static void fista_enqueue(Fit& F, double lambda, const InnerCfg& ic, const doubl
       KG_CUDA(cudaGraphLaunch(F.exec[F.route], ctx->s));
     }
   }
-  fista_finalize(ctx->L(), static_cast<FistaCtl*>(F.ctl.p), F.p, F.x.d(), F.best.d());
+  if (one_kernel)
+    gram_finalize(ctx->L(), static_cast<FistaCtl*>(F.ctl.p), F.p, gstep_args(F));
+  else
+    fista_finalize(ctx->L(), static_cast<FistaCtl*>(F.ctl.p), F.p, F.x.d(), F.best.d(), F.Sx.d(), F.Sbest.d());
   KG_CUDA(cudaMemcpyAsync(ctx->pin() + PIN_CTL, F.ctl.p, sizeof(FistaCtl), cudaMemcpyDeviceToHost, ctx->s));
 }
 
@@ -792,9 +852,56 @@ static void check_ll_errs(Fit& F, const i64* errs) {
 // ll = loglik(eta), (l1, l2) of theta.
 struct PathState {
   double ll = 0.0, l1 = 0.0, l2 = 0.0;
+  double tb = 0.0, tst = 0.0;  // Gram route: <theta, b>, <theta, S' theta>
 };
 
+// Gaussian shortcut on the constant-weight route, all in p-space: with
+// eta = X theta and V = w I,  loglik = <theta, b> - w/2 <theta, S' theta>
+// (b = X^T V y, S' = (x)_j X_j^T X_j theta) and
+// <u(eta), eta_t - eta> = <b - w S' theta, theta_t - theta>.
+static ModelTrace gaussian_step_gram(Fit& F, double lambda, const OuterCfg& oc, PathState& st, int n_vmax) {
+  kg_ctx* ctx = F.ctx;
+  const double n = static_cast<double>(F.D->N_full);
+  const double w = F.wconst;
+  const double ll_cur = st.tb - 0.5 * w * st.tst;
+  const double f_cur = -ll_cur / n + lambda * penalty_of(F.pen, F.alpha, st.l1, st.l2);
+  ModelTrace tr;
+  fista_enqueue(F, lambda, oc.inner, F.part.d() + F.D->part_cap - n_vmax, n_vmax);
+  const int g = gauss_dots(ctx->L(), F.p, w, F.theta.d(), F.stheta.d(), F.best.d(), F.Sbest.d(), F.b.d(),
+                           F.part.d());
+  reduce_cols(ctx->L(), F.part.d(), g, 9, 0, F.scal.d());
+  double* pin = ctx->pin();
+  KG_CUDA(cudaMemcpyAsync(pin, F.scal.p, sizeof(double) * 9, cudaMemcpyDeviceToHost, ctx->s));
+  sync(ctx);
+  const FistaOut fo = fista_read(F);
+  if (fo.bad_weights) throw Error(E_INVAL, "lipschitz_upper: weights must not be all zero");
+  tr.inner = fo.iterations;
+  if (fo.diverged) {
+    tr.status = KG_S_INNER_DIVERGENCE;
+    tr.final_objective = f_cur;
+    return tr;
+  }
+  const double tb = pin[2], tst = pin[3], l1 = pin[5], l2 = pin[6];
+  const double ll_new = tb - 0.5 * w * tst;
+  const double f_new = -ll_new / n + lambda * penalty_of(F.pen, F.alpha, l1, l2);
+  double f = f_cur;
+  if (f_new <= f_cur) {
+    pcopy(ctx->L(), F.p, F.best.d(), F.theta.d(), nullptr, nullptr);
+    pcopy(ctx->L(), F.p, F.Sbest.d(), F.stheta.d(), nullptr, nullptr);
+    st.tb = tb;
+    st.tst = tst;
+    st.l1 = l1;
+    st.l2 = l2;
+    f = f_new;
+  }
+  tr.outer = 1;
+  tr.final_objective = f;
+  tr.status = fo.converged ? KG_S_CONVERGED : KG_S_MAX_ITERATIONS;
+  return tr;
+}
+
 static ModelTrace gaussian_step(Fit& F, double lambda, const OuterCfg& oc, PathState& st, int n_vmax) {
+  if (F.route == 1) return gaussian_step_gram(F, lambda, oc, st, n_vmax);
   kg_ctx* ctx = F.ctx;
   const double n = static_cast<double>(F.D->N_full);
   const double f_cur = -st.ll / n + lambda * penalty_of(F.pen, F.alpha, st.l1, st.l2);
@@ -1088,6 +1195,7 @@ static kg_path_result* fit_path(kg_ctx* ctx, const kg_design* D, const kg_obs* O
   // state at theta = 0: eta = 0
   KG_CUDA(cudaMemsetAsync(F->theta.p, 0, sizeof(double) * F->p, ctx->s));
   KG_CUDA(cudaMemsetAsync(F->eta.p, 0, sizeof(double) * F->n, ctx->s));
+  KG_CUDA(cudaMemsetAsync(F->stheta.p, 0, sizeof(double) * F->p, ctx->s));  // S'(0) = 0
   const bool gauss_shortcut = fam == KG_GAUSSIAN && oc.wmode == KG_W_EXACT;
   PathState st;
   int n_vmax = 0;

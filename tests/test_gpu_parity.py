@@ -162,23 +162,43 @@ def test_two_component_design_generic_route():  # c = 2: unfused route
     compare_paths(K.fit_path(design, "poisson", yp, **kw), O.fit_path(design, "poisson", yp, **kw))
 
 
-def test_penalties_weights_and_inner_options_match_oracle():
+def _masked_weights(shape):
+    a = np.ones(int(np.prod(shape)))
+    a[::4] = 0.0
+    return np.asfortranarray(a.reshape(shape, order="F"))
+
+
+GAUSS_CASES = {
+    "ridge": dict(penalty="ridge", lambdas=[0.05, 0.02, 0.01, 0.005]),
+    "elasticnet": dict(penalty="elasticnet", alpha=0.5, n_lambda=6),
+    "masked_weights": dict(weights="masked", n_lambda=6),
+    "nu_half": dict(nu=0.5, n_lambda=6),
+    "inner_maxit": dict(n_lambda=6, inner_maxit=7),
+}
+
+
+@pytest.mark.parametrize("case", sorted(GAUSS_CASES))
+def test_gaussian_options_match_oracle(case):
     rng = np.random.default_rng(73)
     design = bspline_design((16, 14, 6), (6, 5, 4))
     y = rng.standard_normal((16, 14, 6))
-    a = np.ones_like(y)
-    a.ravel(order="F")[::4] = 0.0
-    af = np.asfortranarray(a)
-    lam = [0.05, 0.02, 0.01, 0.005]
-    for kw in (dict(penalty="ridge", lambdas=lam), dict(penalty="elasticnet", alpha=0.5, n_lambda=6),
-               dict(weights=af, n_lambda=6), dict(nu=0.5, n_lambda=6), dict(n_lambda=6, inner_maxit=7)):
-        got = K.fit_path(design, "gaussian", y, **kw)
-        want = O.fit_path(design, "gaussian", y, **kw)
-        compare_paths(got, want)
+    kw = dict(GAUSS_CASES[case])
+    if kw.get("weights") == "masked":
+        kw["weights"] = _masked_weights(y.shape)
+    compare_paths(K.fit_path(design, "gaussian", y, **kw), O.fit_path(design, "gaussian", y, **kw))
+
+
+@pytest.mark.parametrize("case", ["unit", "masked_weights"])
+def test_poisson_options_match_oracle(case):
+    rng = np.random.default_rng(73)
+    design = bspline_design((16, 14, 6), (6, 5, 4))
     yp = rng.poisson(1.5, size=(16, 14, 6)).astype(float)
-    for kw in (dict(iwls="unit", n_lambda=5, lambda_min_ratio=1e-2), dict(n_lambda=5, lambda_min_ratio=1e-2,
-                                                                           weights=af)):
-        compare_paths(K.fit_path(design, "poisson", yp, **kw), O.fit_path(design, "poisson", yp, **kw))
+    kw = dict(n_lambda=5, lambda_min_ratio=1e-2)
+    if case == "unit":
+        kw["iwls"] = "unit"
+    else:
+        kw["weights"] = _masked_weights(yp.shape)
+    compare_paths(K.fit_path(design, "poisson", yp, **kw), O.fit_path(design, "poisson", yp, **kw))
 
 
 def test_constant_weight_gram_route_matches_oracle():
