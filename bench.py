@@ -64,6 +64,9 @@ class Clocks:
         self._t = None
 
     def start(self):
+        if os.environ.get("BENCH_NO_CLOCKS") == "1":
+            return
+
         def run():
             q = ("clocks.sm,clocks.max.sm,clocks_event_reasons.hw_slowdown,"
                  "clocks_event_reasons.hw_thermal_slowdown,clocks_event_reasons.sw_thermal_slowdown,"

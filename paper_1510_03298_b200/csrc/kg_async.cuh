@@ -1,0 +1,75 @@
+// Bulk-async copy (TMA engine) + mbarrier helpers shared by the kernels.
+#pragma once
+
+#include <cstdint>
+
+namespace kg {
+namespace async {
+
+__device__ __forceinline__ unsigned smem_u32(const void* p) {
+  return static_cast<unsigned>(__cvta_generic_to_shared(p));
+}
+
+__device__ __forceinline__ void mbar_init(unsigned long long* bar, unsigned count) {
+  asm volatile("mbarrier.init.shared::cta.b64 [%0], %1;" ::"r"(smem_u32(bar)), "r"(count));
+}
+
+__device__ __forceinline__ void mbar_init_fence() { asm volatile("fence.mbarrier_init.release.cluster;" ::: "memory"); }
+
+__device__ __forceinline__ void mbar_expect_tx(unsigned long long* bar, unsigned bytes) {
+  asm volatile("mbarrier.arrive.expect_tx.shared::cta.b64 _, [%0], %1;" ::"r"(smem_u32(bar)), "r"(bytes)
+               : "memory");
+}
+
+__device__ __forceinline__ void mbar_wait(unsigned long long* bar, unsigned parity) {
+  asm volatile(
+      "{\n"
+      ".reg .pred p;\n"
+      "WAIT_%=:\n"
+      "mbarrier.try_wait.parity.shared::cta.b64 p, [%0], %1;\n"
+      "@!p bra WAIT_%=;\n"
+      "}\n" ::"r"(smem_u32(bar)),
+      "r"(parity)
+      : "memory");
+}
+
+__device__ __forceinline__ void bulk_g2s(void* dst, const void* src, unsigned bytes, unsigned long long* bar) {
+  asm volatile(
+      "cp.async.bulk.shared::cluster.global.mbarrier::complete_tx::bytes [%0], [%1], %2, [%3];" ::"r"(
+          smem_u32(dst)),
+      "l"(src), "r"(bytes), "r"(smem_u32(bar))
+      : "memory");
+}
+
+__device__ __forceinline__ void fence_proxy_async() { asm volatile("fence.proxy.async.shared::cta;" ::: "memory"); }
+
+// A shared buffer `base` with one spare double receives n doubles of src at
+// view = base + shift(src), so that view and src share their 16-byte phase;
+// the misaligned head and odd tail element are copied by the calling thread
+// (stage_manual, before the arrive), the rest by the bulk engine (stage_bulk).
+__device__ __forceinline__ int stage_shift(const double* src) {
+  return (reinterpret_cast<uintptr_t>(src) & 15) ? 1 : 0;
+}
+
+__device__ __forceinline__ unsigned stage_manual(double* base, const double* src, int64_t n) {
+  double* dst = base + stage_shift(src);
+  int64_t head = stage_shift(src);
+  if (head > n) head = n;
+  int64_t body = n - head;
+  body -= body & 1;
+  if (head) dst[0] = src[0];
+  if (head + body < n) dst[n - 1] = src[n - 1];
+  return static_cast<unsigned>(body * 8);
+}
+
+__device__ __forceinline__ void stage_bulk(double* base, const double* src, int64_t n, unsigned long long* bar) {
+  double* dst = base + stage_shift(src);
+  int64_t head = stage_shift(src);
+  if (head > n) head = n;
+  int64_t body = n - head;
+  body -= body & 1;
+  if (body > 0) bulk_g2s(dst + head, src + head, static_cast<unsigned>(body * 8), bar);
+}
+
+}  // namespace async
+}  // namespace kg

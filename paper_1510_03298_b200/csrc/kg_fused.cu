@@ -314,7 +314,7 @@ void fused_tma(const Launch& L, int variant, const FusedArgs& f) {
     case FV_XTWZ: k_fused_tma<FV_XTWZ><<<g, NT, sm, L.s>>>(f, pl, ntiles); break;
     default: k_fused_tma<FV_SCORE0><<<g, NT, sm, L.s>>>(f, pl, ntiles); break;
   }
-  if (L.counter) ++*L.counter;
+  launched(L);
 }
 
 // Bandwidth reference: grid-stride 16-byte loads of two arrays.
@@ -332,7 +332,7 @@ __global__ void __launch_bounds__(NT) k_stream_read2(i64 n2, const double2* x, c
 void stream_read2(const Launch& L, i64 n, const double* x, const double* y, double* partial) {
   k_stream_read2<<<148 * 8, NT, 0, L.s>>>(n / 2, reinterpret_cast<const double2*>(x),
                                           reinterpret_cast<const double2*>(y), partial);
-  if (L.counter) ++*L.counter;
+  launched(L);
 }
 
 // ----------------------------------------------------- tiled contraction
@@ -422,7 +422,7 @@ void contract_tiled(const Launch& L, const double* A, double* out, i64 a, i64 K,
     attr = true;
   }
   k_contract_tiled<<<g, NT, sm, L.s>>>(A, out, a, K, M, op, pl, accumulate);
-  if (L.counter) ++*L.counter;
+  launched(L);
 }
 
 // Chooses the m-block so that the union of the staged input rows of every

@@ -1,29 +1,24 @@
-// One-kernel FISTA iteration for the constant-weight (Gram) route.
+// Constant-weight (Gram) route of the FISTA iteration.
 //
 // With W = w I, X^T W X = w (x)_j X_j^T X_j (the reference's
 // xtwx_apply_tensor with constant weight factors, design.cpp:153-177), so a
-// FISTA step needs only p-space work.  k_gram_step does a whole iteration in
-// one launch:
-//   * CTA s owns slab s of the last coefficient mode (q = p_1..p_{d-1}
-//     contiguous values).  S_new[:, s] = (G_{d-1..1}) sum_t G_d[s, t] x_new[:, t],
-//     so the CTA recomputes the elementwise FISTA update (inner.cpp:163-187)
-//     for every neighbour slab t in the band of G_d row s on the fly;
-//   * iterates rotate through three buffers (x_{l+1} overwrites x_{l-2}), so
-//     the redundant neighbour updates only ever read the previous two
-//     iterates, never a slab another CTA is writing;
-//   * per-CTA partials of w<x,S'x> - 2<x,b>, |x|_1 and |x|_2^2 feed the
-//     objective; the last CTA to finish (atomic ticket) reduces them in fixed
-//     order and runs the monitor / best / restart / stop logic of
-//     fista_solve (inner.cpp:195-229), then sets the graph's while-condition.
+// FISTA step needs only p-space work: the elementwise update kernel
+// (k_fista_update) followed by k_gram_apply, which applies the banded Gram
+// product slab by slab (one CTA per slab of the last coefficient mode, the
+// other modes contracted in shared memory), emits the objective partials, and
+// lets the last CTA to finish (atomic ticket) reduce every partial in fixed
+// order and advance the fista_solve control block on the device.
 #include <cfloat>
+#include <cstdlib>
 
+#include "kg_async.cuh"
 #include "kg_internal.h"
 
 namespace kg {
 
 namespace {
 
-constexpr int NT = 256;
+constexpr int NT = 256;  // p-space reduction kernels
 
 __device__ __forceinline__ double soft(double z, double g) {
   const double m = fabs(z) - g;
@@ -50,6 +45,7 @@ __device__ __forceinline__ double warp_sum(double v) {
 }
 
 // deterministic CTA sum, result broadcast to all threads
+template <int BS = NT>
 __device__ double cta_sum(double v, double* sh) {
   const int w = threadIdx.x >> 5, l = threadIdx.x & 31;
   v = warp_sum(v);
@@ -57,7 +53,7 @@ __device__ double cta_sum(double v, double* sh) {
   if (l == 0) sh[w] = v;
   __syncthreads();
   if (w == 0) {
-    double r = l < (NT >> 5) ? sh[l] : 0.0;
+    double r = l < (BS >> 5) ? sh[l] : 0.0;
     r = warp_sum(r);
     if (l == 0) sh[32] = r;
   }
@@ -67,15 +63,16 @@ __device__ double cta_sum(double v, double* sh) {
 
 // in-shared-memory mode-j contraction of a q-array with extents dims (all
 // modes < d-1 keep their extent because G_j is square)
-__device__ void smem_mode(const double* in, double* out, const int* dims, int nd, int j, const BandOp& op, int q) {
-  int a = 1;
-  for (int i = 0; i < j; ++i) a *= dims[i];
+template <int BS>
+__device__ void smem_mode(const double* in, double* out, const int* dims, int j, const BandOp& op, int q,
+                          const FastDiv& fa, const FastDiv& fk) {
+  const int a = static_cast<int>(fa.d);
   const int K = dims[j];
-  for (int e = threadIdx.x; e < q; e += NT) {
-    const int al = e % a;
-    const int rest = e / a;
-    const int m = rest % K;
-    const int be = rest / K;
+  for (int e = threadIdx.x; e < q; e += BS) {
+    const int rest = static_cast<int>(fa.div(static_cast<uint32_t>(e)));
+    const int al = e - rest * a;
+    const int be = static_cast<int>(fk.div(static_cast<uint32_t>(rest)));
+    const int m = rest - be * K;
     const int lo = __ldg(op.lo + m), len = __ldg(op.len + m);
     const double* c = op.coef + __ldg(op.off + m);
     const double* src = in + al + a * (lo + K * be);
@@ -87,113 +84,88 @@ __device__ void smem_mode(const double* in, double* out, const int* dims, int nd
 
 }  // namespace
 
-__global__ void __launch_bounds__(NT) k_gram_step(GramStepArgs A) {
-  extern __shared__ double sm[];
+// S'(x)[:, s] = (G_{d-2..0}) sum_t G_d[s, t] x[:, t] for slab s of the last
+// mode, then per-CTA partials of w<x,S'x> - 2<x,b>; the last CTA to finish
+// reduces them (and the |x| partials of the preceding update kernel) in fixed
+// order and runs the fista_solve monitor / control (or its setup, init mode).
+// STAGED: the band of neighbour slabs of x (one contiguous range) and b's own
+// slab arrive in shared memory through one bulk-async copy each, so the whole
+// input is a single round trip; otherwise the loads go through L1/L2.
+template <int BS, bool STAGED>
+__global__ void __launch_bounds__(BS) k_gram_apply(GramStepArgs A) {
+  extern __shared__ __align__(16) double sm[];
   __shared__ double red[33];
   __shared__ int am_last;
+  __shared__ unsigned long long bar;
   FistaCtl* c = A.ctl;
   const int q = A.q;
   const int s = blockIdx.x;
-  const i64 it = A.init ? 0 : c->it;
-  const int cur = static_cast<int>((it + 2) % 3);  // x_{it-1}
-  const int prv = static_cast<int>((it + 1) % 3);  // x_{it-2}
-  const int nxt = static_cast<int>(it % 3);        // x_it
-  const double omega = c->omega, delta = c->delta, lambda = c->lambda, n = c->n, w = c->sscale;
-  const int restart = A.init ? 0 : c->restart, copy_best = A.init ? 0 : c->copy_best;
-  const double gamma = delta * lambda;
-  const double* Xc = A.X[cur];
-  const double* Xp = A.X[prv];
-  const double* Sc = A.S[cur];
-  const double* Sp = A.S[prv];
-
-  double* u = sm;           // sum_t G_d[s,t] x_new[:, t]
-  double* t0 = sm + q;      // chain scratch
-  double* t1 = sm + 2 * q;
-  double* xs = sm + 3 * q;  // x_new[:, s]
-
-  auto xnew = [&](i64 idx) -> double {
-    if (A.init) return Xc[idx];
-    double xi, xpi, sxi, sxpi;
-    if (restart) {
-      xi = xpi = A.best[idx];
-      sxi = sxpi = A.Sbest[idx];
-    } else {
-      xi = Xc[idx];
-      xpi = Xp[idx];
-      sxi = Sc[idx];
-      sxpi = Sp[idx];
-    }
-    const double yi = xi + omega * (xi - xpi);
-    const double syi = sxi + omega * (sxi - sxpi);
-    const double g = (w * syi - A.b[idx]) / n;
-    double ci = yi - delta * g;
-    if (lambda > 0.0) ci = prox1(A.pen, A.alpha, gamma, ci);
-    return ci;
-  };
-
-  // pending best copy from the previous monitor (owner slab only)
-  if (copy_best) {
-    for (int e = threadIdx.x; e < q; e += NT) {
-      const i64 idx = static_cast<i64>(s) * q + e;
-      A.best[idx] = Xc[idx];
-      A.Sbest[idx] = Sc[idx];
-    }
-  }
-  // restart (inner.cpp:207-216): x = x_prev = best.  This step reads best
-  // instead of the cur/prv buffers, and the cur buffer becomes the next
-  // step's x_prev, so the owner slab of cur is overwritten with best.
-  if (restart) {
-    for (int e = threadIdx.x; e < q; e += NT) {
-      const i64 idx = static_cast<i64>(s) * q + e;
-      A.X[cur][idx] = A.best[idx];
-      A.S[cur][idx] = A.Sbest[idx];
-    }
-  }
+  const double* x = A.X[0];
+  double* Sx = A.S[0];
   const int lo = __ldg(A.Gd.lo + s), len = __ldg(A.Gd.len + s);
   const double* gc = A.Gd.coef + __ldg(A.Gd.off + s);
-  for (int e = threadIdx.x; e < q; e += NT) {
-    double acc = 0.0;
-    for (int t = 0; t < len; ++t) {
-      const int sl = lo + t;
-      const double xn = xnew(static_cast<i64>(sl) * q + e);
-      acc = fma(__ldg(gc + t), xn, acc);
-      if (sl == s) xs[e] = xn;
+  // shared layout: [u q][t0 q][t1 q] then, staged: [x band  maxlen*q + 2][b slab q + 2]
+  double* u = sm;
+  double* t0 = sm + q;
+  double* t1 = sm + 2 * q;
+  const double* xb = x + static_cast<i64>(lo) * q;  // neighbour band, contiguous
+  const double* bsrc = A.b + static_cast<i64>(s) * q;
+  const double* xv_s = x + static_cast<i64>(s) * q;
+  const double* bv = bsrc;
+  const double* xin = xb;
+  if (STAGED) {
+    double* xbase = sm + 3 * q;
+    double* bbase = xbase + (static_cast<i64>(A.Gd.maxlen) * q + 2);
+    if (threadIdx.x == 0) {
+      async::mbar_init(&bar, 1);
+      async::mbar_init_fence();
+      unsigned bytes = async::stage_manual(xbase, xb, static_cast<i64>(len) * q);
+      bytes += async::stage_manual(bbase, bsrc, q);
+      async::fence_proxy_async();
+      async::mbar_expect_tx(&bar, bytes);
+      async::stage_bulk(xbase, xb, static_cast<i64>(len) * q, &bar);
+      async::stage_bulk(bbase, bsrc, q, &bar);
     }
-    if (s < lo || s >= lo + len) xs[e] = xnew(static_cast<i64>(s) * q + e);
-    u[e] = acc;
+    __syncthreads();  // barrier initialised before anyone waits on it
+    async::mbar_wait(&bar, 0);
+    xin = xbase + async::stage_shift(xb);
+    bv = bbase + async::stage_shift(bsrc);
+    xv_s = xin + static_cast<i64>(s - lo) * q;  // own slab inside the band (s is in its Gram band)
+  }
+  for (int e = threadIdx.x; e < q; e += BS) {
+    const double* xe = xin + e;
+    double a0 = 0.0, a1 = 0.0;
+    int t = 0;
+    for (; t + 1 < len; t += 2) {
+      a0 = fma(__ldg(gc + t), xe[static_cast<i64>(t) * q], a0);
+      a1 = fma(__ldg(gc + t + 1), xe[static_cast<i64>(t + 1) * q], a1);
+    }
+    if (t < len) a0 = fma(__ldg(gc + t), xe[static_cast<i64>(t) * q], a0);
+    u[e] = a0 + a1;
   }
   __syncthreads();
-  // S'_new[:, s] = (G_{d-2} .. G_0 applied to u)
   const double* res = u;
   double* bufs[2] = {t0, t1};
   int which = 0;
   for (int j = A.d - 2; j >= 0; --j) {
-    smem_mode(res, bufs[which], A.dims, A.d - 1, j, A.G[j], q);
+    smem_mode<BS>(res, bufs[which], A.dims, j, A.G[j], q, A.fa[j], A.fk[j]);
     __syncthreads();
     res = bufs[which];
     which ^= 1;
   }
+  const double w = c->sscale;
   double dots = 0.0, l1 = 0.0, l2 = 0.0;
-  double* Xn = A.X[nxt];
-  double* Sn = A.S[nxt];
-  for (int e = threadIdx.x; e < q; e += NT) {
+  for (int e = threadIdx.x; e < q; e += BS) {
     const i64 idx = static_cast<i64>(s) * q + e;
-    const double xv = xs[e], sv = res[e];
-    Xn[idx] = xv;
-    Sn[idx] = sv;
-    if (A.init) {  // x_{-1} := x_0, S_{-1} := S_0, best := x_0
-      A.X[2][idx] = xv;
-      A.S[2][idx] = sv;
-      A.best[idx] = xv;
-      A.Sbest[idx] = sv;
-    }
-    dots += xv * (w * sv - 2.0 * A.b[idx]);
+    const double sv = res[e], xv = xv_s[e];
+    Sx[idx] = sv;
+    dots += xv * (w * sv - 2.0 * bv[e]);
     l1 += fabs(xv);
     l2 = fma(xv, xv, l2);
   }
-  dots = cta_sum(dots, red);
-  l1 = cta_sum(l1, red);
-  l2 = cta_sum(l2, red);
+  dots = cta_sum<BS>(dots, red);
+  l1 = cta_sum<BS>(l1, red);
+  l2 = cta_sum<BS>(l2, red);
   if (threadIdx.x == 0) {
     A.part[3 * s] = dots;
     A.part[3 * s + 1] = l1;
@@ -205,18 +177,19 @@ __global__ void __launch_bounds__(NT) k_gram_step(GramStepArgs A) {
   __syncthreads();
   if (!am_last) return;
   __threadfence();
-  // ---- last CTA: fixed-order reduction of the partials + control
+  // ---- last CTA: fixed-order reductions + control
   double sd = 0.0, s1 = 0.0, s2 = 0.0;
-  for (int r = threadIdx.x; r < static_cast<int>(gridDim.x); r += NT) {
+  for (int r = threadIdx.x; r < static_cast<int>(gridDim.x); r += BS) {
     sd += __ldcg(A.part + 3 * r);
     s1 += __ldcg(A.part + 3 * r + 1);
     s2 += __ldcg(A.part + 3 * r + 2);
   }
-  sd = cta_sum(sd, red);
-  s1 = cta_sum(s1, red);
-  s2 = cta_sum(s2, red);
+  sd = cta_sum<BS>(sd, red);
+  s1 = cta_sum<BS>(s1, red);
+  s2 = cta_sum<BS>(s2, red);
   if (threadIdx.x != 0) return;
   *A.counter = 0u;
+  const double n = c->n, lambda = c->lambda;
   const double g = 0.5 * (sd + c->ss_const) / n + lambda * penalty_of(A.pen, A.alpha, s1, s2);
   if (A.init) {  // fista_solve setup (inner.cpp:132-161)
     c->g_prev = g;
@@ -242,6 +215,7 @@ __global__ void __launch_bounds__(NT) k_gram_step(GramStepArgs A) {
     c->done = (c->max_iters < 1) || c->bad_weights;
     return;
   }
+  const i64 it = c->it;
   c->copy_best = 0;
   c->restart = 0;
   c->prox_steps += 1;
@@ -286,33 +260,23 @@ __global__ void __launch_bounds__(NT) k_gram_step(GramStepArgs A) {
   if (A.use_handle) cudaGraphSetConditional(A.handle, c->done ? 0u : 1u);
 }
 
-bool gram_step_fits(i64 q) { return 4 * q * static_cast<i64>(sizeof(double)) <= 200 * 1024; }
+bool gram_step_fits(i64 q) { return 3 * q * static_cast<i64>(sizeof(double)) <= 200 * 1024; }
 
 void gram_step(const Launch& L, const GramStepArgs& A) {
   static bool attr = false;
   if (!attr) {
-    KG_CUDA(cudaFuncSetAttribute(k_gram_step, cudaFuncAttributeMaxDynamicSharedMemorySize, 210 * 1024));
+    KG_CUDA(cudaFuncSetAttribute(k_gram_apply<256, true>, cudaFuncAttributeMaxDynamicSharedMemorySize, 210 * 1024));
+    KG_CUDA(cudaFuncSetAttribute(k_gram_apply<256, false>, cudaFuncAttributeMaxDynamicSharedMemorySize, 210 * 1024));
     attr = true;
   }
-  const size_t sm = 4 * static_cast<size_t>(A.q) * sizeof(double);
-  k_gram_step<<<static_cast<unsigned>(A.pd), NT, sm, L.s>>>(A);
-  if (L.counter) ++*L.counter;
-}
-
-// x_final = X[iterations % 3]; best := x_final (and Sbest) if the last monitor left a copy pending
-__global__ void k_gram_finalize(const FistaCtl* c, i64 p, GramStepArgs A) {
-  const int fin = static_cast<int>(c->iterations % 3);
-  if (!c->copy_best) return;
-  for (i64 i = static_cast<i64>(blockIdx.x) * blockDim.x + threadIdx.x; i < p;
-       i += static_cast<i64>(gridDim.x) * blockDim.x) {
-    A.best[i] = A.X[fin][i];
-    A.Sbest[i] = A.S[fin][i];
+  const size_t base = 3 * static_cast<size_t>(A.q) * sizeof(double);
+  const size_t staged = base + (static_cast<size_t>(A.Gd.maxlen + 1) * A.q + 4) * sizeof(double);
+  if (staged <= 200 * 1024) {
+    k_gram_apply<256, true><<<static_cast<unsigned>(A.pd), 256, staged, L.s>>>(A);
+  } else {
+    k_gram_apply<256, false><<<static_cast<unsigned>(A.pd), 256, base, L.s>>>(A);
   }
-}
-
-void gram_finalize(const Launch& L, const FistaCtl* ctl, i64 p, const GramStepArgs& A) {
-  k_gram_finalize<<<static_cast<unsigned>(std::min<i64>((p + 255) / 256, 1184)), 256, 0, L.s>>>(ctl, p, A);
-  if (L.counter) ++*L.counter;
+  launched(L);
 }
 
 // Gaussian constant-weight bookkeeping in p-space (outer.cpp:197-231 via
@@ -346,7 +310,7 @@ int gauss_dots(const Launch& L, i64 p, double w, const double* th, const double*
                const double* Sbt, const double* b, double* part) {
   const int g = static_cast<int>(std::min<i64>(std::max<i64>((p + 1023) / 1024, 1), 296));
   k_gauss_dots<<<g, NT, 0, L.s>>>(p, w, th, Sth, bt, Sbt, b, part);
-  if (L.counter) ++*L.counter;
+  launched(L);
   return g;
 }
 

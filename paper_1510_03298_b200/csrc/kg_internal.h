@@ -29,6 +29,23 @@ enum { E_INVAL = 1, E_EVAL = 2, E_RUNTIME = 3, E_DIVERGE = 4, E_POWER = 5, E_CUD
                         std::string(#expr) + ": " + cudaGetErrorString(e__));                         \
   } while (0)
 
+// Division by a loop-invariant divisor as multiply-high + shift (valid for
+// numerators < 2^31); built on the host, used in kernels.
+struct FastDiv {
+  uint32_t d, m, s;
+  __host__ __device__ explicit FastDiv(uint32_t dd = 1) : d(dd), m(0), s(0) {
+    if (d > 1) {
+      uint32_t l = 0;
+      while ((1ull << l) < d) ++l;
+      m = static_cast<uint32_t>(((1ull << (31 + l)) + d - 1) / d);
+      s = l - 1;
+    }
+  }
+#ifdef __CUDACC__
+  __device__ __forceinline__ uint32_t div(uint32_t n) const { return d == 1 ? n : (__umulhi(n, m) >> s); }
+#endif
+};
+
 // ------------------------------------------------------------ band operators
 // One banded operator C (rows x cols): row m has nonzeros at columns
 // [lo[m], lo[m]+len[m]) with packed coefficients coef[off[m] + t].  For the
@@ -83,6 +100,14 @@ struct Launch {
   cudaStream_t s;
   i64* counter;  // incremented per launch (host-side launch accounting)
 };
+
+// After every kernel launch: surface launch-configuration errors immediately
+// (they are otherwise silent) and count the launch.
+inline void launched(const Launch& L) {
+  const cudaError_t e = cudaGetLastError();
+  if (e != cudaSuccess) throw Error(E_CUDA, std::string("kernel launch failed: ") + cudaGetErrorString(e));
+  if (L.counter) ++*L.counter;
+}
 
 void contract(const Launch& L, const double* A, double* out, i64 a, i64 K, i64 M, i64 b, const BandOp& op,
               bool accumulate);
@@ -189,7 +214,8 @@ void minmax(const Launch& L, i64 n, const double* x, double* part);
 void fista_finalize(const Launch& L, const FistaCtl* ctl, i64 p, const double* x, double* best, const double* Sx,
                     double* Sbest);
 
-// One-kernel FISTA iteration on the constant-weight Gram route (kg_gram.cu).
+// Gram product + objective partials + control in one kernel on the
+// constant-weight route (kg_gram.cu); follows k_fista_update in the body.
 struct GramStepArgs {
   FistaCtl* ctl = nullptr;
   int d = 0;           // number of modes (<= 4)
@@ -198,22 +224,20 @@ struct GramStepArgs {
   int dims[4] = {1, 1, 1, 1};
   BandOp Gd;           // Gram of the last mode
   BandOp G[3];         // Grams of modes 0 .. d-2
-  double* X[3] = {nullptr, nullptr, nullptr};
-  double* S[3] = {nullptr, nullptr, nullptr};
+  double* X[1] = {nullptr};  // the new iterate x
+  double* S[1] = {nullptr};  // S'(x) (out)
   const double* b = nullptr;
-  double* best = nullptr;
-  double* Sbest = nullptr;
+  FastDiv fa[3], fk[3];        // in-slab mode j: divide by prod_{i<j} p_i and by p_j
   int pen = 0;
   double alpha = 0.0;
   double* part = nullptr;      // 3 per CTA
   unsigned* counter = nullptr;  // zero-initialised ticket
   cudaGraphConditionalHandle handle = 0;
   int use_handle = 0;
-  int init = 0;                // 1: compute S'(x_0) and the fista_solve setup, no step
+  int init = 0;                // 1: fista_solve setup instead of a monitor step
 };
 bool gram_step_fits(i64 q);
 void gram_step(const Launch& L, const GramStepArgs& A);
-void gram_finalize(const Launch& L, const FistaCtl* ctl, i64 p, const GramStepArgs& A);
 int gauss_dots(const Launch& L, i64 p, double w, const double* th, const double* Sth, const double* bt,
                const double* Sbt, const double* b, double* part);
 

@@ -100,7 +100,7 @@ int grid_for(i64 work, int per_cta, int cap) {
 }
 
 inline void bump(const Launch& L) {
-  if (L.counter) ++*L.counter;
+  launched(L);
 }
 
 }  // namespace
@@ -130,19 +130,6 @@ __global__ void __launch_bounds__(NT) k_contract(const double* __restrict__ A, d
 
 // Division by a loop-invariant divisor as multiply-high + shift (valid for
 // numerators < 2^31).
-struct FastDiv {
-  uint32_t d, m, s;
-  explicit FastDiv(uint32_t dd = 1) : d(dd), m(0), s(0) {
-    if (d > 1) {
-      uint32_t l = 0;
-      while ((1ull << l) < d) ++l;
-      m = static_cast<uint32_t>(((1ull << (31 + l)) + d - 1) / d);
-      s = l - 1;
-    }
-  }
-  __device__ __forceinline__ uint32_t div(uint32_t n) const { return d == 1 ? n : (__umulhi(n, m) >> s); }
-};
-
 // Same contraction with a 2-D launch: grid.x walks the (alpha, m) plane of
 // one beta slab, grid.y (+ grid.z) the slabs; one fast division per output.
 // The band loop keeps two partial sums so long G-direction bands pipeline.
@@ -899,16 +886,24 @@ void fista_gate(const Launch& L, const FistaCtl* ctl, cudaGraphConditionalHandle
   bump(L);
 }
 
-__global__ void __launch_bounds__(CT) k_reduce_cols(const double* part, int nrows, int ncols, int op, double* out) {
-  __shared__ double sh[33];
-  for (int c = 0; c < ncols; ++c) {
-    const double r = op ? cta_max_col(part, nrows, ncols, c, sh) : cta_sum_col(part, nrows, ncols, c, sh);
-    if (threadIdx.x == 0) out[c] = r;
+// One warp per column: lanes sum strided rows sequentially, then a fixed
+// shuffle tree (deterministic); no block barriers.
+__global__ void k_reduce_cols(const double* part, int nrows, int ncols, int op, double* out) {
+  const int w = threadIdx.x >> 5, l = threadIdx.x & 31, nw = blockDim.x >> 5;
+  for (int c = w; c < ncols; c += nw) {
+    double r = op ? -DBL_MAX : 0.0;
+    for (int i = l; i < nrows; i += 32) {
+      const double v = part[static_cast<i64>(i) * ncols + c];
+      r = op ? fmax(r, v) : r + v;
+    }
+    r = op ? warp_max(r) : warp_sum(r);
+    if (l == 0) out[c] = r;
   }
 }
 
 void reduce_cols(const Launch& L, const double* part, int nrows, int ncols, int op, double* out) {
-  k_reduce_cols<<<1, CT, 0, L.s>>>(part, nrows, ncols, op, out);
+  const int warps = ncols < 16 ? ncols : 16;
+  k_reduce_cols<<<1, 32 * warps, 0, L.s>>>(part, nrows, ncols, op, out);
   bump(L);
 }
 

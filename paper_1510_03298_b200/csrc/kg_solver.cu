@@ -340,7 +340,7 @@ struct Fit {
   bool c0_valid = false;   // F.scal[48] holds sum v z^2 for the current (v, z)
   // route 1 with one component: one fused kernel per iteration (kg_gram.cu)
   bool gstep = false;
-  DBuf X3[3], S3[3], gpart, gcount, stheta;
+  DBuf gpart, gcount, stheta;
   // one captured FISTA graph per route
   cudaGraphExec_t exec[2] = {nullptr, nullptr};
   cudaGraph_t graph[2] = {nullptr, nullptr};
@@ -384,10 +384,6 @@ static void alloc_fit(Fit& F) {
   const i64 pd = D.p[0][D.d - 1];
   F.gstep = D.c == 1 && D.d <= 4 && gram_step_fits(D.P / pd);
   if (F.gstep) {
-    for (int r = 0; r < 3; ++r) {
-      F.X3[r].alloc(pb);
-      F.S3[r].alloc(pb);
-    }
     F.gpart.alloc(sizeof(double) * 3 * pd);
     F.gcount.alloc(sizeof(unsigned) * 4);
     KG_CUDA(cudaMemsetAsync(F.gcount.p, 0, sizeof(unsigned) * 4, F.ctx->s));
@@ -549,18 +545,18 @@ static GramStepArgs gstep_args(Fit& F) {
   A.d = static_cast<int>(D.d);
   A.pd = D.p[0][D.d - 1];
   A.q = static_cast<int>(D.P / A.pd);
+  uint32_t before = 1;
   for (i64 j = 0; j + 1 < D.d; ++j) {
     A.dims[j] = static_cast<int>(D.p[0][j]);
     A.G[j] = D.gram[0][0][j]->dev.H;
+    A.fa[j] = FastDiv(before);
+    A.fk[j] = FastDiv(static_cast<uint32_t>(D.p[0][j]));
+    before *= static_cast<uint32_t>(D.p[0][j]);
   }
   A.Gd = D.gram[0][0][D.d - 1]->dev.H;
-  for (int r = 0; r < 3; ++r) {
-    A.X[r] = F.X3[r].d();
-    A.S[r] = F.S3[r].d();
-  }
+  A.X[0] = F.x.d();
+  A.S[0] = F.Sx.d();
   A.b = F.b.d();
-  A.best = F.best.d();
-  A.Sbest = F.Sbest.d();
   A.pen = F.pen;
   A.alpha = F.alpha;
   A.part = F.gpart.d();
@@ -571,7 +567,9 @@ static GramStepArgs gstep_args(Fit& F) {
 // One FISTA iteration: p-space update -> X^T W X pass on the new iterate -> control.
 static void enqueue_body(Fit& F, cudaGraphConditionalHandle h, int use_handle) {
   kg_ctx* ctx = F.ctx;
-  if (F.route == 1 && F.gstep) {
+  if (F.route == 1 && F.gstep) {  // update kernel + one Gram/objective/control kernel
+    fista_update(ctx->L(), static_cast<FistaCtl*>(F.ctl.p), F.p, F.pen, F.alpha, F.x.d(), F.xp.d(), F.Sx.d(),
+                 F.Sxp.d(), F.b.d(), F.best.d(), F.Sbest.d(), F.Jpart.d());
     GramStepArgs A = gstep_args(F);
     A.handle = h;
     A.use_handle = use_handle;
@@ -697,13 +695,13 @@ static void fista_enqueue(Fit& F, double lambda, const InnerCfg& ic, const doubl
                             cudaMemcpyDeviceToDevice, ctx->s));
   }
   const bool one_kernel = F.route == 1 && F.gstep;
-  if (one_kernel) {  // x_0 -> X3[2]; the init launch computes S'(x_0), g_0 and the step size
-    pcopy(ctx->L(), F.p, F.theta.d(), F.X3[2].d(), nullptr, nullptr);
+  pcopy(ctx->L(), F.p, F.theta.d(), F.x.d(), F.xp.d(), F.best.d());
+  if (one_kernel) {  // S'(x_0), g_0 and the step size in one launch
     GramStepArgs A = gstep_args(F);
     A.init = 1;
     gram_step(ctx->L(), A);
+    pcopy(ctx->L(), F.p, F.Sx.d(), F.Sxp.d(), F.Sbest.d(), nullptr);
   } else {
-    pcopy(ctx->L(), F.p, F.theta.d(), F.x.d(), F.xp.d(), F.best.d());
     const int n_ss = step_pass(F, F.x.d(), F.Sx.d());
     pnorm(ctx->L(), F.p, F.pen, F.alpha, F.x.d(), F.Jpart.d());
     pcopy(ctx->L(), F.p, F.Sx.d(), F.Sxp.d(), F.Sbest.d(), nullptr);
@@ -729,10 +727,7 @@ static void fista_enqueue(Fit& F, double lambda, const InnerCfg& ic, const doubl
       KG_CUDA(cudaGraphLaunch(F.exec[F.route], ctx->s));
     }
   }
-  if (one_kernel)
-    gram_finalize(ctx->L(), static_cast<FistaCtl*>(F.ctl.p), F.p, gstep_args(F));
-  else
-    fista_finalize(ctx->L(), static_cast<FistaCtl*>(F.ctl.p), F.p, F.x.d(), F.best.d(), F.Sx.d(), F.Sbest.d());
+  fista_finalize(ctx->L(), static_cast<FistaCtl*>(F.ctl.p), F.p, F.x.d(), F.best.d(), F.Sx.d(), F.Sbest.d());
   KG_CUDA(cudaMemcpyAsync(ctx->pin() + PIN_CTL, F.ctl.p, sizeof(FistaCtl), cudaMemcpyDeviceToHost, ctx->s));
 }
 

@@ -3,10 +3,9 @@
 import argparse
 import os
 import sys
+import time
 
 sys.path.insert(0, os.path.dirname(os.path.dirname(os.path.abspath(__file__))))
-
-import numpy as np  # noqa: E402
 
 from paper_1510_03298_b200 import configs  # noqa: E402
 from paper_1510_03298_b200 import kronglm as K  # noqa: E402
@@ -22,6 +21,9 @@ D = K.Design(d["design"], ctx)
 O = K.Observation(D, d["y"])
 for i in range(args.paths):
     ctx.reset_launches()
+    t0 = time.perf_counter()
     r = K.fit_path_resident(D, O, d["family"], n_lambda=args.n_lambda or d["n_lambda"],
                             lambda_min_ratio=d["lambda_min_ratio"])
-    print(f"path {i}: models={r.n_models} inner={sum(r.inner_iters)} launches={ctx.launches}", flush=True)
+    dt = time.perf_counter() - t0
+    print(f"path {i}: models={r.n_models} inner={sum(r.inner_iters)} launches={ctx.launches} "
+          f"wall={dt * 1000:.1f} ms per-model-inner={r.inner_iters[:8]}", flush=True)
