@@ -12,10 +12,11 @@
 //    (alpha block x m block x beta) output tile, stages the union of the input
 //    rows its band touches in shared memory, then every warp produces whole
 //    coalesced output rows.
+#include <algorithm>
 #include <cfloat>
 #include <climits>
+#include <cstdlib>
 #include <vector>
-#include <algorithm>
 
 #include "kg_internal.h"
 
@@ -128,10 +129,12 @@ __device__ __forceinline__ double score0_of(int fam, double y, double a) {
 }  // namespace
 
 // --------------------------------------------------------------- fused pass
+constexpr int kMaxStages = 4;
 struct FusedPlan {
   int T;        // fibres per tile
   int stage;    // doubles per stage
   int offP, offA, offB;  // stage-relative offsets (doubles) of P, stream A (v|y), stream B (z|a)
+  int nst;      // pipeline depth (stages in flight) of the register-hoisted kernel
 };
 
 template <int VAR>
@@ -268,10 +271,160 @@ __global__ void __launch_bounds__(NT) k_fused_tma(FusedArgs f, FusedPlan pl, i64
   }
 }
 
+// Register-hoisted variant for n1 <= NT, p1 <= NT, H bands <= 4 wide and G
+// bands <= MAXG wide (every cubic B-spline factor in the BASELINE configs).
+// Each thread's X1 row (phase A) and X1^T row (phase B) are fixed for the
+// whole persistent kernel, so their band coefficients live in registers and
+// the per-cell work is a handful of shared-memory loads and FMAs.
+template <int VAR, int MAXG, int BS>
+__global__ void __launch_bounds__(BS) k_fused_fast(FusedArgs f, FusedPlan pl, i64 ntiles) {
+  extern __shared__ __align__(128) double sm[];
+  __shared__ unsigned long long bar[kMaxStages];
+  __shared__ double red[32];
+  const int n1 = static_cast<int>(f.n1), p1 = static_cast<int>(f.p1), T = pl.T;
+  const int nst = pl.nst;
+  constexpr bool hasP = VAR == FV_FISTA;
+  if (threadIdx.x == 0) {
+    for (int k = 0; k < nst; ++k) mbar_init(&bar[k], 1);
+    asm volatile("fence.mbarrier_init.release.cluster;" ::: "memory");
+  }
+  const double* srcA = VAR == FV_SCORE0 ? f.y : f.v;
+  const double* srcB = VAR == FV_SCORE0 ? f.a : f.z;
+  auto issue = [&](i64 tile, int s) {
+    const i64 c0 = tile * T;
+    const i64 Tc = min(static_cast<i64>(T), f.m - c0);
+    double* st = sm + static_cast<i64>(s) * pl.stage;
+    unsigned bytes = 0;
+    if (hasP) bytes += stage_manual(st + pl.offP, f.P + c0 * p1, p1 * Tc);
+    bytes += stage_manual(st + pl.offA, srcA + c0 * n1, n1 * Tc);
+    bytes += stage_manual(st + pl.offB, srcB + c0 * n1, n1 * Tc);
+    fence_proxy_async();
+    mbar_expect_tx(&bar[s], bytes);
+    if (hasP) stage_bulk(st + pl.offP, f.P + c0 * p1, p1 * Tc, &bar[s]);
+    stage_bulk(st + pl.offA, srcA + c0 * n1, n1 * Tc, &bar[s]);
+    stage_bulk(st + pl.offB, srcB + c0 * n1, n1 * Tc, &bar[s]);
+  };
+  const int tid = static_cast<int>(threadIdx.x);
+  // phase A: row i of X1, fibres cgA, cgA + CGA, ...
+  const int CGA = BS / n1;
+  const bool actA = tid < n1 * CGA;
+  const int iA = actA ? tid % n1 : 0, cgA = actA ? tid / n1 : 0;
+  int loA = 0, lenA = 0;
+  double cA[4] = {0.0, 0.0, 0.0, 0.0};
+  if (hasP && actA) {
+    loA = __ldg(f.H.lo + iA);
+    lenA = __ldg(f.H.len + iA);
+    const double* cf = f.H.coef + __ldg(f.H.off + iA);
+#pragma unroll
+    for (int t = 0; t < 4; ++t) cA[t] = t < lenA ? __ldg(cf + t) : 0.0;
+  }
+  // phase B: row k of X1^T, fibres cgB, cgB + CGB, ...
+  const int CGB = BS / p1;
+  const bool actB = tid < p1 * CGB;
+  const int kB = actB ? tid % p1 : 0, cgB = actB ? tid / p1 : 0;
+  int loB = 0, lenB = 0;
+  double g[MAXG];
+#pragma unroll
+  for (int t = 0; t < MAXG; ++t) g[t] = 0.0;
+  if (actB) {
+    loB = __ldg(f.G.lo + kB);
+    lenB = __ldg(f.G.len + kB);
+    const double* cf = f.G.coef + __ldg(f.G.off + kB);
+#pragma unroll
+    for (int t = 0; t < MAXG; ++t)
+      if (t < lenB) g[t] = __ldg(cf + t);
+  }
+  __syncthreads();
+
+  double acc = 0.0;
+  int s = 0;
+  unsigned phase_bits = 0u;  // bit k: parity of stage k's next completion
+  i64 tile = blockIdx.x;
+  if (threadIdx.x == 0)
+    for (int k = 0; k < nst; ++k)
+      if (tile + static_cast<i64>(k) * gridDim.x < ntiles) issue(tile + static_cast<i64>(k) * gridDim.x, k);
+  for (; tile < ntiles; tile += gridDim.x) {
+    const i64 c0 = tile * T;
+    const int Tc = static_cast<int>(min(static_cast<i64>(T), f.m - c0));
+    double* st = sm + static_cast<i64>(s) * pl.stage;
+    const double* Ps = st + pl.offP + (hasP ? stage_shift(f.P + c0 * p1) : 0);
+    double* As = st + pl.offA + stage_shift(srcA + c0 * n1);  // v (or y); overwritten in place by w
+    const double* Bs = st + pl.offB + stage_shift(srcB + c0 * n1);
+    mbar_wait(&bar[s], (phase_bits >> s) & 1u);
+    phase_bits ^= 1u << s;
+    if (actA && f.dbg != 1) {
+      auto cell = [&](int col) {
+        const int e = iA + n1 * col;
+        double w;
+        if (VAR == FV_FISTA) {
+          const double* pc = Ps + p1 * col + loA;
+          double e0 = 0.0, e1 = 0.0;
+          if (lenA > 0) e0 = cA[0] * pc[0];
+          if (lenA > 1) e1 = cA[1] * pc[1];
+          if (lenA > 2) e0 = fma(cA[2], pc[2], e0);
+          if (lenA > 3) e1 = fma(cA[3], pc[3], e1);
+          const double eta = e0 + e1;
+          const double vv = As[e];
+          const double r = eta - Bs[e];
+          acc = fma(vv, r * r, acc);
+          w = vv * eta;
+        } else if (VAR == FV_XTWZ) {
+          w = As[e] * Bs[e];
+        } else {
+          w = score0_of(f.fam, As[e], Bs[e]) / f.disp;
+          if (!isfinite(w))
+            atomicMin(reinterpret_cast<unsigned long long*>(f.err),
+                      static_cast<unsigned long long>(f.cell_base + c0 * n1 + e));
+        }
+        As[e] = w;
+      };
+      int col = cgA;
+      for (; col + CGA < Tc; col += 2 * CGA) {  // two fibres per step: independent loads in flight
+        cell(col);
+        cell(col + CGA);
+      }
+      if (col < Tc) cell(col);
+    }
+    __syncthreads();
+    if (actB && f.dbg == 0) {
+      double* Q = f.Q + c0 * p1;
+      for (int col = cgB; col < Tc; col += CGB) {
+        const double* wr = As + loB + n1 * col;
+        double o0 = 0.0, o1 = 0.0;
+#pragma unroll
+        for (int t = 0; t < MAXG; t += 2) {
+          if (t < lenB) o0 = fma(g[t], wr[t], o0);
+          if (t + 1 < lenB) o1 = fma(g[t + 1], wr[t + 1], o1);
+        }
+        Q[kB + p1 * col] = o0 + o1;
+      }
+    }
+    __syncthreads();  // stage s is free again
+    const i64 next = tile + static_cast<i64>(nst) * gridDim.x;
+    if (threadIdx.x == 0 && next < ntiles) issue(next, s);
+    s = s + 1 == nst ? 0 : s + 1;
+  }
+  if (VAR == FV_FISTA) {
+    const double r = block_sum(acc, red);
+    if (threadIdx.x == 0) f.partial[blockIdx.x] = r;
+  }
+}
+
 static FusedPlan plan_for(const FusedArgs& f, int variant) {
   FusedPlan pl;
   const i64 per_col = (variant == FV_FISTA ? f.p1 : 0) + 2 * f.n1;
-  i64 T = std::max<i64>(1, (16 * 1024 / 8) / per_col);  // ~16 KB stages: 6 CTAs (48 warps) per SM
+  static const i64 stage_kb = [] {
+    const char* e = std::getenv("KG_FUSED_STAGE_KB");
+    const long v = e ? std::atol(e) : 48;
+    return static_cast<i64>(v >= 4 && v <= 100 ? v : 48);
+  }();
+  static const int stages = [] {
+    const char* e = std::getenv("KG_FUSED_STAGES");
+    const int v = e ? std::atoi(e) : 2;
+    return v >= 2 && v <= kMaxStages ? v : 2;
+  }();
+  pl.nst = stages;
+  i64 T = std::max<i64>(1, (stage_kb * 1024 / 8) / per_col);
   T = std::min<i64>(T, f.m);
   pl.T = static_cast<int>(T);
   // 16-byte aligned sub-buffers, each with one spare double for the phase shift
@@ -287,20 +440,66 @@ static FusedPlan plan_for(const FusedArgs& f, int variant) {
 int fused_tma_grid(const FusedArgs& f, int variant) {
   const FusedPlan pl = plan_for(f, variant);
   const i64 ntiles = (f.m + pl.T - 1) / pl.T;
-  const size_t sm = 2 * static_cast<size_t>(pl.stage) * sizeof(double);
+  const size_t sm = static_cast<size_t>(pl.nst) * pl.stage * sizeof(double);
   const int per_sm = std::max<int>(1, std::min<int>(8, static_cast<int>((220 * 1024) / (sm + 2048))));
   return static_cast<int>(std::min<i64>(ntiles, 148LL * per_sm));
 }
 
 bool fused_tma_fits(const FusedArgs& f, int variant) {
   const FusedPlan pl = plan_for(f, variant);
-  return 2 * static_cast<size_t>(pl.stage) * sizeof(double) <= 200 * 1024;
+  return static_cast<size_t>(pl.nst) * pl.stage * sizeof(double) <= 200 * 1024;
+}
+
+// Block size of the register-hoisted fused kernel (KG_FUSED_BS = 256 | 512).
+static int fused_bs() {
+  static const int bs = [] {
+    const char* e = std::getenv("KG_FUSED_BS");
+    return (e && std::atoi(e) == 512) ? 512 : 256;
+  }();
+  return bs;
+}
+
+template <int VAR, int MG>
+static void launch_fast_one(const Launch& L, const FusedArgs& f, const FusedPlan& pl, i64 ntiles, int g, size_t sm) {
+  static bool attr = false;
+  if (!attr) {
+    KG_CUDA(cudaFuncSetAttribute(k_fused_fast<VAR, MG, 256>, cudaFuncAttributeMaxDynamicSharedMemorySize,
+                                 210 * 1024));
+    KG_CUDA(cudaFuncSetAttribute(k_fused_fast<VAR, MG, 512>, cudaFuncAttributeMaxDynamicSharedMemorySize,
+                                 210 * 1024));
+    attr = true;
+  }
+  if (fused_bs() == 512 && f.n1 <= 512 && f.p1 <= 512)
+    k_fused_fast<VAR, MG, 512><<<g, 512, sm, L.s>>>(f, pl, ntiles);
+  else
+    k_fused_fast<VAR, MG, 256><<<g, 256, sm, L.s>>>(f, pl, ntiles);
+}
+
+template <int VAR>
+static void launch_fast_var(const Launch& L, int mg, const FusedArgs& f, const FusedPlan& pl, i64 ntiles, int g,
+                            size_t sm) {
+  switch (mg) {
+    case 8: launch_fast_one<VAR, 8>(L, f, pl, ntiles, g, sm); break;
+    case 16: launch_fast_one<VAR, 16>(L, f, pl, ntiles, g, sm); break;
+    case 24: launch_fast_one<VAR, 24>(L, f, pl, ntiles, g, sm); break;
+    case 32: launch_fast_one<VAR, 32>(L, f, pl, ntiles, g, sm); break;
+    default: launch_fast_one<VAR, 64>(L, f, pl, ntiles, g, sm); break;
+  }
+}
+
+static void launch_fast(const Launch& L, int variant, int mg, const FusedArgs& f, const FusedPlan& pl, i64 ntiles,
+                        int g, size_t sm) {
+  switch (variant) {
+    case FV_FISTA: launch_fast_var<FV_FISTA>(L, mg, f, pl, ntiles, g, sm); break;
+    case FV_XTWZ: launch_fast_var<FV_XTWZ>(L, mg, f, pl, ntiles, g, sm); break;
+    default: launch_fast_var<FV_SCORE0>(L, mg, f, pl, ntiles, g, sm); break;
+  }
 }
 
 void fused_tma(const Launch& L, int variant, const FusedArgs& f) {
   const FusedPlan pl = plan_for(f, variant);
   const i64 ntiles = (f.m + pl.T - 1) / pl.T;
-  const size_t sm = 2 * static_cast<size_t>(pl.stage) * sizeof(double);
+  const size_t sm = static_cast<size_t>(pl.nst) * pl.stage * sizeof(double);
   const int g = fused_tma_grid(f, variant);
   static bool attr = false;
   if (!attr) {
@@ -309,10 +508,16 @@ void fused_tma(const Launch& L, int variant, const FusedArgs& f) {
     KG_CUDA(cudaFuncSetAttribute(k_fused_tma<FV_SCORE0>, cudaFuncAttributeMaxDynamicSharedMemorySize, 210 * 1024));
     attr = true;
   }
-  switch (variant) {
-    case FV_FISTA: k_fused_tma<FV_FISTA><<<g, NT, sm, L.s>>>(f, pl, ntiles); break;
-    case FV_XTWZ: k_fused_tma<FV_XTWZ><<<g, NT, sm, L.s>>>(f, pl, ntiles); break;
-    default: k_fused_tma<FV_SCORE0><<<g, NT, sm, L.s>>>(f, pl, ntiles); break;
+  const bool fast = f.n1 <= NT && f.p1 <= NT && f.H.maxlen <= 4 && f.G.maxlen <= 64;
+  if (fast) {
+    const int mg = f.G.maxlen <= 8 ? 8 : f.G.maxlen <= 16 ? 16 : f.G.maxlen <= 24 ? 24 : f.G.maxlen <= 32 ? 32 : 64;
+    launch_fast(L, variant, mg, f, pl, ntiles, g, sm);
+  } else {
+    switch (variant) {
+      case FV_FISTA: k_fused_tma<FV_FISTA><<<g, NT, sm, L.s>>>(f, pl, ntiles); break;
+      case FV_XTWZ: k_fused_tma<FV_XTWZ><<<g, NT, sm, L.s>>>(f, pl, ntiles); break;
+      default: k_fused_tma<FV_SCORE0><<<g, NT, sm, L.s>>>(f, pl, ntiles); break;
+    }
   }
   launched(L);
 }

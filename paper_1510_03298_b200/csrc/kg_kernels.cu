@@ -157,10 +157,71 @@ __global__ void __launch_bounds__(NT) k_contract2(const double* __restrict__ A, 
   *o = accumulate ? *o + s : s;
 }
 
+// Row-stationary banded contraction: a thread owns one output row (alpha, m)
+// for the whole launch -- its band coefficients live in registers -- and
+// streams over a chunk of beta slabs.  Per output: `len` coalesced loads,
+// `len` FMAs and one coalesced store.
+template <int MAXB>
+__global__ void __launch_bounds__(NT) k_contract_rs(const double* __restrict__ A, double* __restrict__ out,
+                                                    uint32_t a, uint32_t K, uint32_t M, uint32_t b, uint32_t bch,
+                                                    FastDiv fa, BandOp op, int accumulate) {
+  const uint32_t pairs = a * M;
+  const uint32_t pi = blockIdx.x * NT + threadIdx.x;
+  if (pi >= pairs) return;
+  const uint32_t m = fa.div(pi);
+  const uint32_t al = pi - m * a;
+  const int lo = __ldg(op.lo + m), len = __ldg(op.len + m);
+  const double* cf = op.coef + __ldg(op.off + m);
+  double c[MAXB];
+#pragma unroll
+  for (int t = 0; t < MAXB; ++t) c[t] = t < len ? __ldg(cf + t) : 0.0;
+  const uint32_t b0 = blockIdx.y * bch;
+  const uint32_t b1 = min(b, b0 + bch);
+  const size_t in_step = static_cast<size_t>(a) * K, out_step = pairs;
+  const double* src = A + al + static_cast<size_t>(a) * lo + in_step * b0;
+  double* dst = out + pi + out_step * b0;
+  for (uint32_t be = b0; be < b1; ++be, src += in_step, dst += out_step) {
+    double s0 = 0.0, s1 = 0.0;
+#pragma unroll
+    for (int t = 0; t < MAXB; t += 2) {
+      if (t < len) s0 = fma(c[t], __ldg(src + static_cast<size_t>(t) * a), s0);
+      if (t + 1 < len) s1 = fma(c[t + 1], __ldg(src + static_cast<size_t>(t + 1) * a), s1);
+    }
+    const double s = s0 + s1;
+    *dst = accumulate ? *dst + s : s;
+  }
+}
+
+template <int MAXB>
+static void launch_rs(const Launch& L, const double* A, double* out, i64 a, i64 K, i64 M, i64 b, const BandOp& op,
+                      bool accumulate) {
+  const i64 pairs = a * M;
+  const i64 gx = (pairs + NT - 1) / NT;
+  i64 gy = std::max<i64>(1, (148 * 16 + gx - 1) / gx);
+  gy = std::min<i64>(gy, std::min<i64>(b, 65535));
+  const i64 bch = (b + gy - 1) / gy;
+  gy = (b + bch - 1) / bch;
+  k_contract_rs<MAXB><<<dim3(static_cast<unsigned>(gx), static_cast<unsigned>(gy)), NT, 0, L.s>>>(
+      A, out, static_cast<uint32_t>(a), static_cast<uint32_t>(K), static_cast<uint32_t>(M),
+      static_cast<uint32_t>(b), static_cast<uint32_t>(bch), FastDiv(static_cast<uint32_t>(a)), op, accumulate);
+}
+
 void contract(const Launch& L, const double* A, double* out, i64 a, i64 K, i64 M, i64 b, const BandOp& op,
               bool accumulate) {
   const i64 total = a * M * b;
   if (total == 0) return;
+  // register-hoisted row-stationary kernel for banded operators (all B-spline factors)
+  if (op.maxlen <= 64 && a * M < (i64(1) << 31) && a * K * b < (i64(1) << 31) * 4 && b < (i64(1) << 31) &&
+      (a * M + NT - 1) / NT < (i64(1) << 31)) {
+    if (op.maxlen <= 4) launch_rs<4>(L, A, out, a, K, M, b, op, accumulate);
+    else if (op.maxlen <= 8) launch_rs<8>(L, A, out, a, K, M, b, op, accumulate);
+    else if (op.maxlen <= 16) launch_rs<16>(L, A, out, a, K, M, b, op, accumulate);
+    else if (op.maxlen <= 24) launch_rs<24>(L, A, out, a, K, M, b, op, accumulate);
+    else if (op.maxlen <= 32) launch_rs<32>(L, A, out, a, K, M, b, op, accumulate);
+    else launch_rs<64>(L, A, out, a, K, M, b, op, accumulate);
+    bump(L);
+    return;
+  }
   if (a * M < (i64(1) << 31) && a * K < (i64(1) << 31) && b < (i64(1) << 31)) {
     const i64 gx = (a * M + NT - 1) / NT;
     const i64 gy = std::min<i64>(b, 65535);
