@@ -11,6 +11,7 @@
 #include <cfloat>
 #include <cstdlib>
 
+#include "../../include/kronglm_b200.h"
 #include "kg_async.cuh"
 #include "kg_internal.h"
 
@@ -80,6 +81,75 @@ __device__ void smem_mode(const double* in, double* out, const int* dims, int j,
     for (int t = 0; t < len; ++t) s = fma(__ldg(c + t), src[a * t], s);
     out[e] = s;
   }
+}
+
+// fista_solve setup after the initial objective g_0 (inner.cpp:132-161).
+__device__ void ctl_setup(FistaCtl& c, double g, double wmax) {
+  c.g_prev = g;
+  c.best_g = g;
+  c.bad_weights = !(wmax > 0.0);
+  const double lip = wmax * c.lipfac / c.n;  // lipschitz_upper (inner.cpp:53-71)
+  c.lip = lip;
+  double dl = 1.0 / (fmax(c.nu, 1.0e-300) * lip);
+  if (c.nu == 1.0) dl = 1.0 / lip;
+  c.delta = dl;
+  c.omega = 0.0;
+  c.it = 1;
+  c.momentum = 1;
+  c.streak = 0;
+  c.prox_steps = 0;
+  c.backtracks = 0;
+  c.iterations = 0;
+  c.copy_best = 0;
+  c.restart = 0;
+  c.converged = 0;
+  c.diverged = 0;
+  c.done = (c.max_iters < 1) || c.bad_weights;
+}
+
+// One monitor / restart / stop step of fista_solve (inner.cpp:189-229) with
+// the objective g of the iterate just produced.
+__device__ void ctl_step(FistaCtl& c, double g) {
+  const i64 it = c.it;
+  c.copy_best = 0;
+  c.restart = 0;
+  c.prox_steps += 1;
+  c.momentum += 1;
+  c.iterations = it;
+  const i64 me = c.monitor_every < 1 ? 1 : c.monitor_every;
+  if ((it % me == 0) || it == c.max_iters) {
+    bool div = !isfinite(g);
+    if (!div && c.bt_div && g > c.g_prev) div = (++c.streak >= 3);
+    if (div) {
+      if (!c.bt_div) {
+        c.diverged = 1;
+        c.done = 1;
+      } else {
+        c.restart = 1;
+        c.g_prev = c.best_g;
+        c.delta *= 0.5;
+        c.momentum = 1;
+        c.streak = 0;
+        c.backtracks += 1;
+      }
+    } else {
+      if (g <= c.g_prev) c.streak = 0;
+      if (g <= c.best_g) {
+        c.copy_best = 1;
+        c.best_g = g;
+      }
+      if (fabs(g - c.g_prev) / fmax(1.0, fabs(g)) < c.tol) {
+        c.converged = 1;
+        c.done = 1;
+      }
+      c.g_prev = g;
+    }
+  }
+  if (!c.done) {
+    c.it = it + 1;
+    if (c.it > c.max_iters) c.done = 1;
+  }
+  c.omega = c.extrapolation == 0 ? static_cast<double>(c.momentum - 1) / static_cast<double>(c.momentum + 2) : 0.0;
 }
 
 }  // namespace
@@ -189,74 +259,12 @@ __global__ void __launch_bounds__(BS) k_gram_apply(GramStepArgs A) {
   s2 = cta_sum<BS>(s2, red);
   if (threadIdx.x != 0) return;
   *A.counter = 0u;
-  const double n = c->n, lambda = c->lambda;
-  const double g = 0.5 * (sd + c->ss_const) / n + lambda * penalty_of(A.pen, A.alpha, s1, s2);
-  if (A.init) {  // fista_solve setup (inner.cpp:132-161)
-    c->g_prev = g;
-    c->best_g = g;
-    const double wmax = w;  // every weight equals w
-    c->bad_weights = !(wmax > 0.0);
-    const double lip = wmax * c->lipfac / n;
-    c->lip = lip;
-    double dl = 1.0 / (fmax(c->nu, 1.0e-300) * lip);
-    if (c->nu == 1.0) dl = 1.0 / lip;
-    c->delta = dl;
-    c->omega = 0.0;
-    c->it = 1;
-    c->momentum = 1;
-    c->streak = 0;
-    c->prox_steps = 0;
-    c->backtracks = 0;
-    c->iterations = 0;
-    c->copy_best = 0;
-    c->restart = 0;
-    c->converged = 0;
-    c->diverged = 0;
-    c->done = (c->max_iters < 1) || c->bad_weights;
+  const double g = 0.5 * (sd + c->ss_const) / c->n + c->lambda * penalty_of(A.pen, A.alpha, s1, s2);
+  if (A.init) {
+    ctl_setup(*c, g, w);  // every weight equals w
     return;
   }
-  const i64 it = c->it;
-  c->copy_best = 0;
-  c->restart = 0;
-  c->prox_steps += 1;
-  c->momentum += 1;
-  c->iterations = it;
-  const i64 me = c->monitor_every < 1 ? 1 : c->monitor_every;
-  if ((it % me == 0) || it == c->max_iters) {
-    bool div = !isfinite(g);
-    if (!div && c->bt_div && g > c->g_prev) div = (++c->streak >= 3);
-    if (div) {
-      if (!c->bt_div) {
-        c->diverged = 1;
-        c->done = 1;
-      } else {
-        c->restart = 1;
-        c->g_prev = c->best_g;
-        c->delta *= 0.5;
-        c->momentum = 1;
-        c->streak = 0;
-        c->backtracks += 1;
-      }
-    } else {
-      if (g <= c->g_prev) c->streak = 0;
-      if (g <= c->best_g) {
-        c->copy_best = 1;
-        c->best_g = g;
-      }
-      if (fabs(g - c->g_prev) / fmax(1.0, fabs(g)) < c->tol) {
-        c->converged = 1;
-        c->done = 1;
-      }
-      c->g_prev = g;
-    }
-  }
-  if (!c->done) {
-    c->it = it + 1;
-    if (c->it > c->max_iters) c->done = 1;
-  }
-  c->omega = c->extrapolation == 0
-                 ? static_cast<double>(c->momentum - 1) / static_cast<double>(c->momentum + 2)
-                 : 0.0;
+  ctl_step(*c, g);
   if (A.use_handle) cudaGraphSetConditional(A.handle, c->done ? 0u : 1u);
 }
 
@@ -276,6 +284,593 @@ void gram_step(const Launch& L, const GramStepArgs& A) {
   } else {
     k_gram_apply<256, false><<<static_cast<unsigned>(A.pd), 256, base, L.s>>>(A);
   }
+  launched(L);
+}
+
+// ------------------------------------------------------------------------
+// Persistent cooperative FISTA solve on the Gram route: one launch runs the
+// whole fista_solve.  CTA s keeps slab s of x, x_prev, S'x, S'x_prev, best,
+// S'best and b in shared memory for the whole solve; per iteration it
+//   1. applies the elementwise step to its slab and publishes x_new[:, s],
+//   2. grid barrier,
+//   3. bulk-copies the neighbour band of x_new (one contiguous range) and
+//      computes S'(x_new)[:, s] and its objective partials,
+//   4. grid barrier, then reduces all partials in fixed order and advances a
+//      replicated copy of the control block (every CTA computes the same
+//      state, so no third barrier is needed).
+// Co-residency of all CTAs is guaranteed by the cooperative launch.
+namespace {
+
+// Sense-reversing grid barrier with GPU-scope acquire/release atomics:
+// bar[0] counts arrivals, bar[1] is the generation.  The CTA barrier before
+// the arrive orders every thread's writes into thread 0's release
+// (cumulativity); waiters acquire the new generation.
+__device__ __forceinline__ void grid_sync(unsigned* bar, unsigned nb) {
+  __syncthreads();
+  if (threadIdx.x == 0) {
+    unsigned g, old;
+    asm volatile("ld.relaxed.gpu.global.u32 %0, [%1];" : "=r"(g) : "l"(bar + 1) : "memory");
+    asm volatile("atom.acq_rel.gpu.global.add.u32 %0, [%1], 1;" : "=r"(old) : "l"(bar) : "memory");
+    if (old == nb - 1) {
+      asm volatile("st.relaxed.gpu.global.u32 [%0], 0;" ::"l"(bar) : "memory");
+      asm volatile("red.release.gpu.global.add.u32 [%0], 1;" ::"l"(bar + 1) : "memory");
+    } else {
+      unsigned cur;
+      do {
+        asm volatile("ld.acquire.gpu.global.u32 %0, [%1];" : "=r"(cur) : "l"(bar + 1) : "memory");
+      } while (cur == g);
+    }
+  }
+  __syncthreads();
+}
+
+}  // namespace
+
+template <int BS>
+__global__ void __launch_bounds__(BS) k_fista_persist(PersistArgs P) {
+  extern __shared__ __align__(16) double sm[];
+  __shared__ double red[33];
+  __shared__ FistaCtl cs;
+  __shared__ unsigned long long mb;
+  const GramStepArgs& A = P.g;
+  const int q = A.q;
+  const int s = blockIdx.x;
+  const unsigned nb = gridDim.x;
+  double* xs = sm;
+  double* xps = xs + q;
+  double* sxs = xps + q;
+  double* sxps = sxs + q;
+  double* bst = sxps + q;
+  double* sbst = bst + q;
+  double* bs = sbst + q;
+  double* u = bs + q;
+  double* t0 = u + q;
+  double* t1 = t0 + q;
+  double* band = t1 + q;  // maxlen * q + 2
+  if (threadIdx.x == 0) {
+    cs = *A.ctl;
+    async::mbar_init(&mb, 1);
+    async::mbar_init_fence();
+  }
+  const int lo = __ldg(A.Gd.lo + s), len = __ldg(A.Gd.len + s);
+  const double* gc = A.Gd.coef + __ldg(A.Gd.off + s);
+  const i64 base = static_cast<i64>(s) * q;
+  for (int e = threadIdx.x; e < q; e += BS) {
+    const double x0 = P.theta[base + e];
+    xs[e] = x0;
+    xps[e] = x0;
+    bst[e] = x0;
+    bs[e] = A.b[base + e];
+    P.X[base + e] = x0;
+  }
+  unsigned parity = 0;
+  const double w = cs.sscale;
+  // S'(x_new)[:, s] into sxs from the published X, plus objective partials
+  auto apply = [&]() {
+    const double* xb = P.X + static_cast<i64>(lo) * q;
+    if (threadIdx.x == 0) {
+      asm volatile("fence.proxy.async.global;" ::: "memory");
+      const unsigned bytes = async::stage_manual(band, xb, static_cast<i64>(len) * q);
+      async::fence_proxy_async();
+      async::mbar_expect_tx(&mb, bytes);
+      async::stage_bulk(band, xb, static_cast<i64>(len) * q, &mb);
+    }
+    __syncthreads();
+    async::mbar_wait(&mb, parity);
+    parity ^= 1u;
+    const double* xin = band + async::stage_shift(xb);
+    for (int e = threadIdx.x; e < q; e += BS) {
+      const double* xe = xin + e;
+      double a0 = 0.0, a1 = 0.0;
+      int t = 0;
+      for (; t + 1 < len; t += 2) {
+        a0 = fma(__ldg(gc + t), xe[static_cast<i64>(t) * q], a0);
+        a1 = fma(__ldg(gc + t + 1), xe[static_cast<i64>(t + 1) * q], a1);
+      }
+      if (t < len) a0 = fma(__ldg(gc + t), xe[static_cast<i64>(t) * q], a0);
+      u[e] = a0 + a1;
+    }
+    __syncthreads();
+    const double* res = u;
+    double* bufs[2] = {t0, t1};
+    int which = 0;
+    for (int j = A.d - 2; j >= 0; --j) {
+      smem_mode<BS>(res, bufs[which], A.dims, j, A.G[j], q, A.fa[j], A.fk[j]);
+      __syncthreads();
+      res = bufs[which];
+      which ^= 1;
+    }
+    double dots = 0.0, l1 = 0.0, l2 = 0.0;
+    for (int e = threadIdx.x; e < q; e += BS) {
+      const double sv = res[e], xv = xs[e];
+      sxs[e] = sv;
+      dots += xv * (w * sv - 2.0 * bs[e]);
+      l1 += fabs(xv);
+      l2 = fma(xv, xv, l2);
+    }
+    dots = cta_sum<BS>(dots, red);
+    l1 = cta_sum<BS>(l1, red);
+    l2 = cta_sum<BS>(l2, red);
+    if (threadIdx.x == 0) {
+      P.part[3 * s] = dots;
+      P.part[3 * s + 1] = l1;
+      P.part[3 * s + 2] = l2;
+    }
+  };
+  // fixed-order reduction of every CTA's partials (identical in all CTAs)
+  auto objective = [&]() -> double {
+    double sd = 0.0, s1 = 0.0, s2 = 0.0;
+    for (int r = threadIdx.x; r < static_cast<int>(nb); r += BS) {
+      sd += __ldcg(P.part + 3 * r);
+      s1 += __ldcg(P.part + 3 * r + 1);
+      s2 += __ldcg(P.part + 3 * r + 2);
+    }
+    sd = cta_sum<BS>(sd, red);
+    s1 = cta_sum<BS>(s1, red);
+    s2 = cta_sum<BS>(s2, red);
+    return 0.5 * (sd + cs.ss_const) / cs.n + cs.lambda * penalty_of(A.pen, A.alpha, s1, s2);
+  };
+
+  grid_sync(P.bar, nb);
+  apply();
+  for (int e = threadIdx.x; e < q; e += BS) {
+    sxps[e] = sxs[e];
+    sbst[e] = sxs[e];
+  }
+  grid_sync(P.bar, nb);
+  {
+    const double g0 = objective();
+    if (threadIdx.x == 0) ctl_setup(cs, g0, w);
+    __syncthreads();
+  }
+  while (!cs.done) {
+    const double omega = cs.omega, delta = cs.delta, lambda = cs.lambda, n = cs.n;
+    const int restart = cs.restart, copy_best = cs.copy_best;
+    const double gamma = delta * lambda;
+    for (int e = threadIdx.x; e < q; e += BS) {
+      if (copy_best) {
+        bst[e] = xs[e];
+        sbst[e] = sxs[e];
+      }
+      if (restart) {
+        xs[e] = xps[e] = bst[e];
+        sxs[e] = sxps[e] = sbst[e];
+      }
+      const double xi = xs[e], xpi = xps[e], sxi = sxs[e], sxpi = sxps[e];
+      const double yi = xi + omega * (xi - xpi);
+      const double syi = sxi + omega * (sxi - sxpi);
+      const double g = (w * syi - bs[e]) / n;
+      double ci = yi - delta * g;
+      if (lambda > 0.0) ci = prox1(A.pen, A.alpha, gamma, ci);
+      xps[e] = xi;
+      xs[e] = ci;
+      sxps[e] = sxi;
+      P.X[base + e] = ci;
+    }
+    grid_sync(P.bar, nb);
+    apply();
+    grid_sync(P.bar, nb);
+    const double g = objective();
+    if (threadIdx.x == 0) ctl_step(cs, g);
+    __syncthreads();
+  }
+  for (int e = threadIdx.x; e < q; e += BS) {
+    if (cs.copy_best) {
+      bst[e] = xs[e];
+      sbst[e] = sxs[e];
+    }
+    P.best[base + e] = bst[e];
+    P.Sbest[base + e] = sbst[e];
+  }
+  if (s == 0 && threadIdx.x == 0) *A.ctl = cs;
+}
+
+// ------------------------------------------------------------------------
+// The whole Gaussian constant-weight lambda path in one cooperative launch
+// (fit_path, path.cpp:47-81, with the Gaussian shortcut of outer_solve,
+// outer.cpp:197-231).  Per lambda, on the device and in lockstep:
+//   f_cur = -loglik(theta)/n + lambda J(theta) from the replicated
+//   (<theta,b>, <theta,S'theta>, |theta|_1, |theta|_2^2);
+//   fista_solve from x_0 = theta (S'(x_0) is the slab of S'theta kept in
+//   shared memory, so the setup needs no pass);
+//   f_new from (<best,b>, <best,S'best>, |best|) -> accept if f_new <= f_cur;
+//   status / truncation / first-model failure as path.cpp:64-73;
+//   the model's coefficients are written straight into the result buffer.
+template <int BS>
+__global__ void __launch_bounds__(BS) k_gauss_path(PersistArgs P) {
+  extern __shared__ __align__(16) double sm[];
+  __shared__ double red[33];
+  __shared__ FistaCtl cs;
+  __shared__ unsigned long long mb;
+  __shared__ double tb, tst, tl1, tl2;  // replicated path state of theta
+  const GramStepArgs& A = P.g;
+  const int q = A.q;
+  const int s = blockIdx.x;
+  const unsigned nb = gridDim.x;
+  double* xs = sm;
+  double* xps = xs + q;
+  double* sxs = xps + q;
+  double* sxps = sxs + q;
+  double* bst = sxps + q;
+  double* sbst = bst + q;
+  double* bs = sbst + q;
+  double* th = bs + q;
+  double* sth = th + q;
+  double* u = sth + q;
+  double* t0 = u + q;
+  double* t1 = t0 + q;
+  double* band = t1 + q;  // maxlen * q + 2
+  if (threadIdx.x == 0) {
+    async::mbar_init(&mb, 1);
+    async::mbar_init_fence();
+    tb = tst = tl1 = tl2 = 0.0;
+  }
+  const int lo = __ldg(A.Gd.lo + s), len = __ldg(A.Gd.len + s);
+  const double* gc = A.Gd.coef + __ldg(A.Gd.off + s);
+  const i64 base = static_cast<i64>(s) * q;
+  const i64 p = static_cast<i64>(q) * nb;
+  for (int e = threadIdx.x; e < q; e += BS) {
+    th[e] = 0.0;  // fit_path starts from zero blocks (path.cpp:63); S'(0) = 0
+    sth[e] = 0.0;
+    bs[e] = A.b[base + e];
+  }
+  unsigned parity = 0;
+  const FistaCtl tmpl = *A.ctl;  // configuration (lambda filled per model)
+  const double w = tmpl.sscale, n = tmpl.n, c0 = tmpl.ss_const;
+  auto reduce3 = [&](double a, double b, double c, double* out) {
+    out[0] = cta_sum<BS>(a, red);
+    out[1] = cta_sum<BS>(b, red);
+    out[2] = cta_sum<BS>(c, red);
+  };
+  auto apply = [&]() {
+    const double* xb = P.X + static_cast<i64>(lo) * q;
+    if (threadIdx.x == 0) {
+      asm volatile("fence.proxy.async.global;" ::: "memory");
+      const unsigned bytes = async::stage_manual(band, xb, static_cast<i64>(len) * q);
+      async::fence_proxy_async();
+      async::mbar_expect_tx(&mb, bytes);
+      async::stage_bulk(band, xb, static_cast<i64>(len) * q, &mb);
+    }
+    __syncthreads();
+    async::mbar_wait(&mb, parity);
+    parity ^= 1u;
+    const double* xin = band + async::stage_shift(xb);
+    for (int e = threadIdx.x; e < q; e += BS) {
+      const double* xe = xin + e;
+      double a0 = 0.0, a1 = 0.0;
+      int t = 0;
+      for (; t + 1 < len; t += 2) {
+        a0 = fma(__ldg(gc + t), xe[static_cast<i64>(t) * q], a0);
+        a1 = fma(__ldg(gc + t + 1), xe[static_cast<i64>(t + 1) * q], a1);
+      }
+      if (t < len) a0 = fma(__ldg(gc + t), xe[static_cast<i64>(t) * q], a0);
+      u[e] = a0 + a1;
+    }
+    __syncthreads();
+    const double* res = u;
+    double* bufs[2] = {t0, t1};
+    int which = 0;
+    for (int j = A.d - 2; j >= 0; --j) {
+      smem_mode<BS>(res, bufs[which], A.dims, j, A.G[j], q, A.fa[j], A.fk[j]);
+      __syncthreads();
+      res = bufs[which];
+      which ^= 1;
+    }
+    double dots = 0.0, l1 = 0.0, l2 = 0.0;
+    for (int e = threadIdx.x; e < q; e += BS) {
+      const double sv = res[e], xv = xs[e];
+      sxs[e] = sv;
+      dots += xv * (w * sv - 2.0 * bs[e]);
+      l1 += fabs(xv);
+      l2 = fma(xv, xv, l2);
+    }
+    double r[3];
+    reduce3(dots, l1, l2, r);
+    if (threadIdx.x == 0) {
+      P.part[3 * s] = r[0];
+      P.part[3 * s + 1] = r[1];
+      P.part[3 * s + 2] = r[2];
+    }
+  };
+  auto gather3 = [&](double* out) {  // fixed-order sum of every CTA's 3 partials
+    double a = 0.0, b = 0.0, c = 0.0;
+    for (int r = threadIdx.x; r < static_cast<int>(nb); r += BS) {
+      a += __ldcg(P.part + 3 * r);
+      b += __ldcg(P.part + 3 * r + 1);
+      c += __ldcg(P.part + 3 * r + 2);
+    }
+    reduce3(a, b, c, out);
+  };
+
+  int stop = 0;  // 1 truncated, 2 first model failed
+  for (int t = 0; t < P.n_lambda && !stop; ++t) {
+    const double lam = P.lambdas[t];
+    const double j_th = penalty_of(A.pen, A.alpha, tl1, tl2);
+    const double f_cur = -(tb - 0.5 * w * tst) / n + lam * j_th;
+    for (int e = threadIdx.x; e < q; e += BS) {
+      xs[e] = xps[e] = bst[e] = th[e];
+      sxs[e] = sxps[e] = sbst[e] = sth[e];
+    }
+    __syncthreads();
+    if (threadIdx.x == 0) {
+      cs = tmpl;
+      cs.lambda = lam;
+      // inner_objective(x_0) = (w<x0,S'x0> - 2<x0,b> + sum v z^2)/(2n) + lambda J(x_0)
+      const double g0 = 0.5 * (w * tst - 2.0 * tb + c0) / n + lam * j_th;
+      ctl_setup(cs, g0, w);
+    }
+    __syncthreads();
+    if (!tmpl.bt_div) {
+      // nu = 1 (no restarts): x_k depends only on earlier iterates, omega_k =
+      // (k-1)/(k+2) and the fixed step, so the monitor decision of iteration
+      // k-1 is taken one step late, after the single grid barrier of step k,
+      // while the neighbour band of x_k is in flight.  X and the partials are
+      // double-buffered by the parity of k.
+      const double delta = cs.delta, gamma = delta * lam;
+      for (i64 k = 1; !cs.done; ++k) {
+        const double omega =
+            tmpl.extrapolation == 0 ? static_cast<double>(k - 1) / static_cast<double>(k + 2) : 0.0;
+        double* Xk = P.X + (k & 1) * p;
+        for (int e = threadIdx.x; e < q; e += BS) {
+          const double xi = xs[e], xpi = xps[e], sxi = sxs[e], sxpi = sxps[e];
+          const double yi = xi + omega * (xi - xpi);
+          const double syi = sxi + omega * (sxi - sxpi);
+          const double g = (w * syi - bs[e]) / n;
+          double ci = yi - delta * g;
+          if (lam > 0.0) ci = prox1(A.pen, A.alpha, gamma, ci);
+          xps[e] = xi;
+          xs[e] = ci;
+          sxps[e] = sxi;
+          Xk[base + e] = ci;
+        }
+        grid_sync(P.bar, nb);
+        const double* xb = Xk + static_cast<i64>(lo) * q;
+        if (threadIdx.x == 0) {
+          asm volatile("fence.proxy.async.global;" ::: "memory");
+          const unsigned bytes = async::stage_manual(band, xb, static_cast<i64>(len) * q);
+          async::fence_proxy_async();
+          async::mbar_expect_tx(&mb, bytes);
+          async::stage_bulk(band, xb, static_cast<i64>(len) * q, &mb);
+        }
+        if (k >= 2) {  // monitor iteration k-1 from its partials
+          const double* pp = P.part + ((k - 1) & 1) * 3 * static_cast<i64>(nb);
+          double a = 0.0, b = 0.0, c = 0.0;
+          for (int r = threadIdx.x; r < static_cast<int>(nb); r += BS) {
+            a += __ldcg(pp + 3 * r);
+            b += __ldcg(pp + 3 * r + 1);
+            c += __ldcg(pp + 3 * r + 2);
+          }
+          double r3[3];
+          reduce3(a, b, c, r3);
+          if (threadIdx.x == 0)
+            ctl_step(cs, 0.5 * (r3[0] + c0) / n + lam * penalty_of(A.pen, A.alpha, r3[1], r3[2]));
+          __syncthreads();
+          if (cs.copy_best) {  // best := x_{k-1} (now in the x_prev slot)
+            for (int e = threadIdx.x; e < q; e += BS) {
+              bst[e] = xps[e];
+              sbst[e] = sxps[e];
+            }
+          }
+        }
+        __syncthreads();
+        async::mbar_wait(&mb, parity);  // always consume the copy (keeps the barrier phase)
+        parity ^= 1u;
+        if (cs.done) break;
+        const double* xin = band + async::stage_shift(xb);
+        for (int e = threadIdx.x; e < q; e += BS) {
+          const double* xe = xin + e;
+          double a0 = 0.0, a1 = 0.0;
+          int t = 0;
+          for (; t + 1 < len; t += 2) {
+            a0 = fma(__ldg(gc + t), xe[static_cast<i64>(t) * q], a0);
+            a1 = fma(__ldg(gc + t + 1), xe[static_cast<i64>(t + 1) * q], a1);
+          }
+          if (t < len) a0 = fma(__ldg(gc + t), xe[static_cast<i64>(t) * q], a0);
+          u[e] = a0 + a1;
+        }
+        __syncthreads();
+        const double* res = u;
+        double* bufs[2] = {t0, t1};
+        int which = 0;
+        for (int j = A.d - 2; j >= 0; --j) {
+          smem_mode<BS>(res, bufs[which], A.dims, j, A.G[j], q, A.fa[j], A.fk[j]);
+          __syncthreads();
+          res = bufs[which];
+          which ^= 1;
+        }
+        double dots = 0.0, l1 = 0.0, l2 = 0.0;
+        for (int e = threadIdx.x; e < q; e += BS) {
+          const double sv = res[e], xv = xs[e];
+          sxs[e] = sv;
+          dots += xv * (w * sv - 2.0 * bs[e]);
+          l1 += fabs(xv);
+          l2 = fma(xv, xv, l2);
+        }
+        double r3[3];
+        reduce3(dots, l1, l2, r3);
+        if (threadIdx.x == 0) {
+          double* pk = P.part + (k & 1) * 3 * static_cast<i64>(nb);
+          pk[3 * s] = r3[0];
+          pk[3 * s + 1] = r3[1];
+          pk[3 * s + 2] = r3[2];
+        }
+      }
+      if (threadIdx.x == 0) cs.copy_best = 0;  // any pending copy was applied above
+      __syncthreads();
+    }
+    while (!cs.done) {
+      const double omega = cs.omega, delta = cs.delta;
+      const int restart = cs.restart, copy_best = cs.copy_best;
+      const double gamma = delta * lam;
+      for (int e = threadIdx.x; e < q; e += BS) {
+        if (copy_best) {
+          bst[e] = xs[e];
+          sbst[e] = sxs[e];
+        }
+        if (restart) {
+          xs[e] = xps[e] = bst[e];
+          sxs[e] = sxps[e] = sbst[e];
+        }
+        const double xi = xs[e], xpi = xps[e], sxi = sxs[e], sxpi = sxps[e];
+        const double yi = xi + omega * (xi - xpi);
+        const double syi = sxi + omega * (sxi - sxpi);
+        const double g = (w * syi - bs[e]) / n;
+        double ci = yi - delta * g;
+        if (lam > 0.0) ci = prox1(A.pen, A.alpha, gamma, ci);
+        xps[e] = xi;
+        xs[e] = ci;
+        sxps[e] = sxi;
+        P.X[base + e] = ci;
+      }
+      grid_sync(P.bar, nb);
+      apply();
+      grid_sync(P.bar, nb);
+      double r[3];
+      gather3(r);
+      if (threadIdx.x == 0) ctl_step(cs, 0.5 * (r[0] + c0) / n + lam * penalty_of(A.pen, A.alpha, r[1], r[2]));
+      __syncthreads();
+    }
+    // best := x if the last monitor left a copy pending (k_fista_finalize)
+    double bb = 0.0, bsb = 0.0, bl1 = 0.0, bl2 = 0.0;
+    for (int e = threadIdx.x; e < q; e += BS) {
+      if (cs.copy_best) {
+        bst[e] = xs[e];
+        sbst[e] = sxs[e];
+      }
+      const double v = bst[e];
+      bb += v * bs[e];
+      bsb += v * sbst[e];
+      bl1 += fabs(v);
+      bl2 = fma(v, v, bl2);
+    }
+    double r[3];
+    reduce3(bb, bsb, bl1, r);
+    const double rl2 = cta_sum<BS>(bl2, red);
+    if (threadIdx.x == 0) {
+      P.part2[4 * s] = r[0];
+      P.part2[4 * s + 1] = r[1];
+      P.part2[4 * s + 2] = r[2];
+      P.part2[4 * s + 3] = rl2;
+    }
+    grid_sync(P.bar, nb);
+    double g4[4] = {0.0, 0.0, 0.0, 0.0};
+    for (int k = 0; k < 4; ++k) {
+      double a = 0.0;
+      for (int rr = threadIdx.x; rr < static_cast<int>(nb); rr += BS) a += __ldcg(P.part2 + 4 * rr + k);
+      g4[k] = cta_sum<BS>(a, red);
+    }
+    const int status = cs.converged ? KG_S_CONVERGED : (cs.diverged ? KG_S_INNER_DIVERGENCE : KG_S_MAX_ITERATIONS);
+    double f = f_cur;
+    if (!cs.diverged) {
+      const double f_new = -(g4[0] - 0.5 * w * g4[1]) / n + lam * penalty_of(A.pen, A.alpha, g4[2], g4[3]);
+      if (f_new <= f_cur) {  // outer.cpp:216-219
+        for (int e = threadIdx.x; e < q; e += BS) {
+          th[e] = bst[e];
+          sth[e] = sbst[e];
+        }
+        __syncthreads();
+        if (threadIdx.x == 0) {
+          tb = g4[0];
+          tst = g4[1];
+          tl1 = g4[2];
+          tl2 = g4[3];
+        }
+        f = f_new;
+      }
+    }
+    if (status != KG_S_CONVERGED) {
+      stop = t == 0 ? 2 : 1;
+      if (s == 0 && threadIdx.x == 0) P.status_out[t] = status;
+    } else {
+      for (int e = threadIdx.x; e < q; e += BS) P.coefs[static_cast<i64>(t) * p + base + e] = th[e];
+      if (s == 0 && threadIdx.x == 0) {
+        P.obj_out[t] = f;
+        P.iters_out[t] = cs.iterations;
+        P.status_out[t] = status;
+        P.nmodels[0] = t + 1;
+      }
+    }
+    __syncthreads();
+  }
+  if (s == 0 && threadIdx.x == 0) {
+    P.nmodels[1] = stop;
+    *A.ctl = cs;
+  }
+}
+
+static size_t path_smem(const GramStepArgs& A) {
+  return (static_cast<size_t>(12 + A.Gd.maxlen) * A.q + 4) * sizeof(double);
+}
+
+bool gauss_path_ok(const GramStepArgs& A) {
+  const size_t sm = path_smem(A);
+  if (sm > 200 * 1024) return false;
+  static bool attr = false;
+  if (!attr) {
+    KG_CUDA(cudaFuncSetAttribute(k_gauss_path<256>, cudaFuncAttributeMaxDynamicSharedMemorySize, 210 * 1024));
+    attr = true;
+  }
+  int per_sm = 0, dev = 0, nsm = 0;
+  KG_CUDA(cudaOccupancyMaxActiveBlocksPerMultiprocessor(&per_sm, k_gauss_path<256>, 256, sm));
+  KG_CUDA(cudaGetDevice(&dev));
+  KG_CUDA(cudaDeviceGetAttribute(&nsm, cudaDevAttrMultiProcessorCount, dev));
+  return static_cast<i64>(per_sm) * nsm >= A.pd;
+}
+
+void gauss_path(const Launch& L, const PersistArgs& P) {
+  const size_t sm = path_smem(P.g);
+  PersistArgs args = P;
+  void* kargs[] = {&args};
+  KG_CUDA(cudaLaunchCooperativeKernel(reinterpret_cast<const void*>(k_gauss_path<256>),
+                                      dim3(static_cast<unsigned>(P.g.pd)), dim3(256), kargs, sm, L.s));
+  launched(L);
+}
+
+static size_t persist_smem(const GramStepArgs& A) {
+  return (static_cast<size_t>(10 + A.Gd.maxlen) * A.q + 4) * sizeof(double);
+}
+
+bool fista_persist_ok(const GramStepArgs& A) {
+  const size_t sm = persist_smem(A);
+  if (sm > 200 * 1024) return false;
+  static bool attr = false;
+  if (!attr) {
+    KG_CUDA(cudaFuncSetAttribute(k_fista_persist<256>, cudaFuncAttributeMaxDynamicSharedMemorySize, 210 * 1024));
+    attr = true;
+  }
+  int per_sm = 0, dev = 0, nsm = 0;
+  KG_CUDA(cudaOccupancyMaxActiveBlocksPerMultiprocessor(&per_sm, k_fista_persist<256>, 256, sm));
+  KG_CUDA(cudaGetDevice(&dev));
+  KG_CUDA(cudaDeviceGetAttribute(&nsm, cudaDevAttrMultiProcessorCount, dev));
+  return static_cast<i64>(per_sm) * nsm >= A.pd;
+}
+
+void fista_persist(const Launch& L, const PersistArgs& P) {
+  const size_t sm = persist_smem(P.g);
+  PersistArgs args = P;
+  void* kargs[] = {&args};
+  KG_CUDA(cudaLaunchCooperativeKernel(reinterpret_cast<const void*>(k_fista_persist<256>),
+                                      dim3(static_cast<unsigned>(P.g.pd)), dim3(256), kargs, sm, L.s));
   launched(L);
 }
 

@@ -238,6 +238,30 @@ struct GramStepArgs {
 };
 bool gram_step_fits(i64 q);
 void gram_step(const Launch& L, const GramStepArgs& A);
+
+// Persistent cooperative fista_solve on the Gram route (kg_gram.cu).
+struct PersistArgs {
+  GramStepArgs g;             // dims, Gram operators, b, penalty, control block
+  const double* theta = nullptr;  // x_0 (p)
+  double* X = nullptr;        // exchange buffer of the newest iterate (p)
+  double* best = nullptr;     // out: best iterate (p)
+  double* Sbest = nullptr;    // out: S'(best) (p)
+  double* part = nullptr;     // 3 per CTA
+  unsigned* bar = nullptr;    // grid barrier {count, generation}, zero-initialised
+  // whole-path mode (k_gauss_path)
+  const double* lambdas = nullptr;
+  int n_lambda = 0;
+  double* part2 = nullptr;    // 4 per CTA
+  double* coefs = nullptr;    // n_lambda x p result buffer
+  double* obj_out = nullptr;  // n_lambda
+  i64* iters_out = nullptr;   // n_lambda
+  int* status_out = nullptr;  // n_lambda
+  int* nmodels = nullptr;     // [models stored, stop: 0 none, 1 truncated, 2 first model failed]
+};
+bool fista_persist_ok(const GramStepArgs& A);
+void fista_persist(const Launch& L, const PersistArgs& P);
+bool gauss_path_ok(const GramStepArgs& A);
+void gauss_path(const Launch& L, const PersistArgs& P);
 int gauss_dots(const Launch& L, i64 p, double w, const double* th, const double* Sth, const double* bt,
                const double* Sbt, const double* b, double* part);
 

@@ -340,7 +340,9 @@ struct Fit {
   bool c0_valid = false;   // F.scal[48] holds sum v z^2 for the current (v, z)
   // route 1 with one component: one fused kernel per iteration (kg_gram.cu)
   bool gstep = false;
-  DBuf gpart, gcount, stheta;
+  int persist = -1;  // -1 unknown, 0 no, 1: the whole solve runs in one cooperative kernel
+  bool persist_solve = false;  // the last solve ran persistent (launch accounting)
+  DBuf gpart, gcount, stheta, pX, pbar;
   // one captured FISTA graph per route
   cudaGraphExec_t exec[2] = {nullptr, nullptr};
   cudaGraph_t graph[2] = {nullptr, nullptr};
@@ -384,7 +386,10 @@ static void alloc_fit(Fit& F) {
   const i64 pd = D.p[0][D.d - 1];
   F.gstep = D.c == 1 && D.d <= 4 && gram_step_fits(D.P / pd);
   if (F.gstep) {
-    F.gpart.alloc(sizeof(double) * 3 * pd);
+    F.gpart.alloc(sizeof(double) * 6 * pd);  // 3 per CTA, double-buffered (k_gauss_path)
+    F.pX.alloc(2 * pb);
+    F.pbar.alloc(sizeof(unsigned) * 4);
+    KG_CUDA(cudaMemsetAsync(F.pbar.p, 0, sizeof(unsigned) * 4, F.ctx->s));
     F.gcount.alloc(sizeof(unsigned) * 4);
     KG_CUDA(cudaMemsetAsync(F.gcount.p, 0, sizeof(unsigned) * 4, F.ctx->s));
   }
@@ -695,6 +700,22 @@ static void fista_enqueue(Fit& F, double lambda, const InnerCfg& ic, const doubl
                             cudaMemcpyDeviceToDevice, ctx->s));
   }
   const bool one_kernel = F.route == 1 && F.gstep;
+  if (one_kernel && F.persist < 0) F.persist = (!host_loop_mode() && fista_persist_ok(gstep_args(F))) ? 1 : 0;
+  if (one_kernel && F.persist == 1 && ic.max_iters >= 1) {  // the whole solve in one cooperative launch
+    PersistArgs P;
+    P.g = gstep_args(F);
+    P.theta = F.theta.d();
+    P.X = F.pX.d();
+    P.best = F.best.d();
+    P.Sbest = F.Sbest.d();
+    P.part = F.gpart.d();
+    P.bar = static_cast<unsigned*>(F.pbar.p);
+    fista_persist(ctx->L(), P);
+    KG_CUDA(cudaMemcpyAsync(ctx->pin() + PIN_CTL, F.ctl.p, sizeof(FistaCtl), cudaMemcpyDeviceToHost, ctx->s));
+    F.persist_solve = true;
+    return;
+  }
+  F.persist_solve = false;
   pcopy(ctx->L(), F.p, F.theta.d(), F.x.d(), F.xp.d(), F.best.d());
   if (one_kernel) {  // S'(x_0), g_0 and the step size in one launch
     GramStepArgs A = gstep_args(F);
@@ -740,7 +761,7 @@ static FistaOut fista_read(Fit& F) {
   o.converged = c->converged;
   o.diverged = c->diverged;
   o.bad_weights = c->bad_weights;
-  F.ctx->launches += o.iterations * F.kernels_per_iter[F.route];
+  if (!F.persist_solve) F.ctx->launches += o.iterations * F.kernels_per_iter[F.route];
   return o;
 }
 
@@ -1224,6 +1245,73 @@ static kg_path_result* fit_path(kg_ctx* ctx, const kg_design* D, const kg_obs* O
     std::memcpy(&e, pin + PIN_ERR, sizeof(i64));
     check_ll_errs(*F, &e);
     st.ll = pin[0] / disp;
+  }
+  // Gaussian, constant weights, one component: the whole path in one cooperative launch
+  if (gauss_shortcut && F->route == 1 && F->gstep && !host_loop_mode() && oc.inner.max_iters >= 1 &&
+      std::getenv("KG_NO_DEVICE_PATH") == nullptr && gauss_path_ok(gstep_args(*F))) {
+    if (!(F->wconst > 0.0)) throw Error(E_INVAL, "lipschitz_upper: weights must not be all zero");
+    if (!(oc.inner.nu >= 0.0 && oc.inner.nu <= 1.0)) throw Error(E_INVAL, "fista_solve: nu must lie in [0,1]");
+    if (oc.inner.nu == 0.0)
+      throw Error(E_INVAL, "fista_solve: nu = 0 (backtracking every iteration) is not supported by the device solver");
+    FistaCtl h{};
+    h.tol = oc.inner.tol;
+    h.nu = oc.inner.nu;
+    h.n = static_cast<double>(D->N_full);
+    h.lipfac = D->lipfac;
+    h.max_iters = oc.inner.max_iters;
+    h.monitor_every = oc.inner.monitor_every;
+    h.sscale = F->wconst;
+    h.alpha = F->alpha;
+    h.pen = F->pen;
+    h.extrapolation = oc.inner.extrapolation;
+    h.bt_div = oc.inner.nu > 0.0 && oc.inner.nu < 1.0;
+    FistaCtl* staged = reinterpret_cast<FistaCtl*>(ctx->pin() + PIN_STAGE);
+    sync(ctx);
+    *staged = h;
+    KG_CUDA(cudaMemcpyAsync(F->ctl.p, staged, sizeof(FistaCtl), cudaMemcpyHostToDevice, ctx->s));
+    wzz(ctx->L(), F->n, F->v.d(), F->zptr, F->part.d());  // sum v z^2
+    reduce_cols(ctx->L(), F->part.d(), elem_grid(F->n), 1, 0, &static_cast<FistaCtl*>(F->ctl.p)->ss_const);
+    DBuf dl, p2, obj, its, stat;
+    dl.alloc(sizeof(double) * nl);
+    p2.alloc(sizeof(double) * 4 * D->p[0][D->d - 1]);
+    obj.alloc(sizeof(double) * nl);
+    its.alloc(sizeof(i64) * nl);
+    stat.alloc(sizeof(int) * (nl + 2));
+    KG_CUDA(cudaMemcpyAsync(dl.p, lambdas.data(), sizeof(double) * nl, cudaMemcpyHostToDevice, ctx->s));
+    KG_CUDA(cudaMemsetAsync(stat.p, 0, sizeof(int) * (nl + 2), ctx->s));
+    PersistArgs P;
+    P.g = gstep_args(*F);
+    P.X = F->pX.d();
+    P.part = F->gpart.d();
+    P.bar = static_cast<unsigned*>(F->pbar.p);
+    P.lambdas = dl.d();
+    P.n_lambda = static_cast<int>(nl);
+    P.part2 = p2.d();
+    P.coefs = res->coefs.d();
+    P.obj_out = obj.d();
+    P.iters_out = static_cast<i64*>(its.p);
+    P.status_out = static_cast<int*>(stat.p) + 2;
+    P.nmodels = static_cast<int*>(stat.p);
+    gauss_path(ctx->L(), P);
+    std::vector<double> ho(nl);
+    std::vector<i64> hi(nl);
+    std::vector<int> hs(nl + 2);
+    KG_CUDA(cudaMemcpyAsync(ho.data(), obj.p, sizeof(double) * nl, cudaMemcpyDeviceToHost, ctx->s));
+    KG_CUDA(cudaMemcpyAsync(hi.data(), its.p, sizeof(i64) * nl, cudaMemcpyDeviceToHost, ctx->s));
+    KG_CUDA(cudaMemcpyAsync(hs.data(), stat.p, sizeof(int) * (nl + 2), cudaMemcpyDeviceToHost, ctx->s));
+    sync(ctx);
+    const int models = hs[0], stop = hs[1];
+    if (stop == 2)
+      throw Error(E_RUNTIME, std::string("fit_path: first model did not converge (") + status_name(hs[2]) + ")");
+    res->truncated = stop == 1;
+    for (int t = 0; t < models; ++t) {
+      res->lambdas.push_back(lambdas[t]);
+      res->objectives.push_back(ho[t]);
+      res->outer_iters.push_back(1);
+      res->inner_iters.push_back(hi[t]);
+      res->status.push_back(hs[2 + t]);
+    }
+    return res.release();
   }
   for (i64 t = 0; t < nl; ++t) {
     ModelTrace tr = gauss_shortcut ? gaussian_step(*F, lambdas[t], oc, st, n_vmax) : outer_loop(*F, lambdas[t], oc);
