@@ -62,6 +62,64 @@ __device__ double cta_sum(double v, double* sh) {
   return sh[32];
 }
 
+// Three deterministic CTA sums at once (same trees as three cta_sum calls,
+// one third of the barriers).  sh needs 3 * 32 + 3 doubles.
+template <int BS>
+__device__ void cta_sum3(double a, double b, double c, double* sh, double* out) {
+  const int w = threadIdx.x >> 5, l = threadIdx.x & 31;
+  a = warp_sum(a);
+  b = warp_sum(b);
+  c = warp_sum(c);
+  __syncthreads();
+  if (l == 0) {
+    sh[w] = a;
+    sh[32 + w] = b;
+    sh[64 + w] = c;
+  }
+  __syncthreads();
+  if (w == 0) {
+    double r0 = l < (BS >> 5) ? sh[l] : 0.0;
+    double r1 = l < (BS >> 5) ? sh[32 + l] : 0.0;
+    double r2 = l < (BS >> 5) ? sh[64 + l] : 0.0;
+    r0 = warp_sum(r0);
+    r1 = warp_sum(r1);
+    r2 = warp_sum(r2);
+    if (l == 0) {
+      sh[96] = r0;
+      sh[97] = r1;
+      sh[98] = r2;
+    }
+  }
+  __syncthreads();
+  out[0] = sh[96];
+  out[1] = sh[97];
+  out[2] = sh[98];
+}
+
+// Mode-j contraction like smem_mode with the band rows staged in shared
+// memory (sc: K x MB coefficients, slo/slen: row ranges) and the taps unrolled
+// to MB with predication; the summation order is smem_mode's.
+template <int BS, int MB>
+__device__ __forceinline__ void smem_mode_st(const double* in, double* out, int K, int q, const FastDiv& fa,
+                                             const FastDiv& fk, const double* sc, const int* slo,
+                                             const int* slen) {
+  const int a = static_cast<int>(fa.d);
+  for (int e = threadIdx.x; e < q; e += BS) {
+    const int rest = static_cast<int>(fa.div(static_cast<uint32_t>(e)));
+    const int al = e - rest * a;
+    const int be = static_cast<int>(fk.div(static_cast<uint32_t>(rest)));
+    const int m = rest - be * K;
+    const int lo = slo[m], len = slen[m];
+    const double* c = sc + m * MB;
+    const double* src = in + al + a * (lo + K * be);
+    double s = 0.0;
+#pragma unroll
+    for (int t = 0; t < MB; ++t)
+      if (t < len) s = fma(c[t], src[a * t], s);
+    out[e] = s;
+  }
+}
+
 // in-shared-memory mode-j contraction of a q-array with extents dims (all
 // modes < d-1 keep their extent because G_j is square)
 template <int BS>
@@ -316,8 +374,13 @@ __device__ __forceinline__ void grid_sync(unsigned* bar, unsigned nb) {
       asm volatile("red.release.gpu.global.add.u32 [%0], 1;" ::"l"(bar + 1) : "memory");
     } else {
       unsigned cur;
+      const long long t0 = clock64();
       do {
         asm volatile("ld.acquire.gpu.global.u32 %0, [%1];" : "=r"(cur) : "l"(bar + 1) : "memory");
+        if (clock64() - t0 > async::kWatchdogCycles) {
+          printf("kg watchdog: grid barrier (block %d of %u, generation %u)\n", blockIdx.x, nb, g);
+          __trap();
+        }
       } while (cur == g);
     }
   }
@@ -363,6 +426,7 @@ __global__ void __launch_bounds__(BS) k_fista_persist(PersistArgs P) {
     bs[e] = A.b[base + e];
     P.X[base + e] = x0;
   }
+  __syncthreads();  // cs and the mbarrier are read by every warp
   unsigned parity = 0;
   const double w = cs.sscale;
   // S'(x_new)[:, s] into sxs from the published X, plus objective partials
@@ -498,8 +562,9 @@ __global__ void __launch_bounds__(BS) k_fista_persist(PersistArgs P) {
 //   the model's coefficients are written straight into the result buffer.
 template <int BS>
 __global__ void __launch_bounds__(BS) k_gauss_path(PersistArgs P) {
+  constexpr int MB = kPathTaps;
   extern __shared__ __align__(16) double sm[];
-  __shared__ double red[33];
+  __shared__ double red[3 * 32 + 3];
   __shared__ FistaCtl cs;
   __shared__ unsigned long long mb;
   __shared__ double tb, tst, tl1, tl2;  // replicated path state of theta
@@ -520,6 +585,31 @@ __global__ void __launch_bounds__(BS) k_gauss_path(PersistArgs P) {
   double* t0 = u + q;
   double* t1 = t0 + q;
   double* band = t1 + q;  // maxlen * q + 2
+  // Gram bands of modes 0 .. d-2 staged in shared memory (K_j x MB
+  // coefficients, zero padded, then lo / len per row); mode j starts at
+  // sg + MB * (dims[0] + .. + dims[j-1]) and sgi + 2 * (same)
+  double* sg = band + static_cast<i64>(A.Gd.maxlen) * q + 2;
+  int rows_all = 0;
+  bool staged = true;
+  for (int j = 0; j < A.d - 1; ++j) {
+    rows_all += A.dims[j];
+    staged = staged && A.G[j].maxlen <= MB && !(P.dbg & 1);
+  }
+  int* sgi = reinterpret_cast<int*>(sg + static_cast<i64>(rows_all) * MB);
+  if (staged) {
+    int r0 = 0;
+    for (int j = 0; j < A.d - 1; ++j) {
+      const int K = A.dims[j];
+      for (int r = threadIdx.x; r < K; r += BS) {
+        const int ln = __ldg(A.G[j].len + r);
+        const double* c = A.G[j].coef + __ldg(A.G[j].off + r);
+        sgi[2 * r0 + r] = __ldg(A.G[j].lo + r);
+        sgi[2 * r0 + K + r] = ln;
+        for (int t = 0; t < MB; ++t) sg[static_cast<i64>(r0 + r) * MB + t] = t < ln ? c[t] : 0.0;
+      }
+      r0 += K;
+    }
+  }
   if (threadIdx.x == 0) {
     async::mbar_init(&mb, 1);
     async::mbar_init_fence();
@@ -527,6 +617,10 @@ __global__ void __launch_bounds__(BS) k_gauss_path(PersistArgs P) {
   }
   const int lo = __ldg(A.Gd.lo + s), len = __ldg(A.Gd.len + s);
   const double* gc = A.Gd.coef + __ldg(A.Gd.off + s);
+  const bool hoist = len <= MB && !(P.dbg & 2);  // uniform per CTA
+  double gr[MB];
+#pragma unroll
+  for (int t = 0; t < MB; ++t) gr[t] = (hoist && t < len) ? __ldg(gc + t) : 0.0;
   const i64 base = static_cast<i64>(s) * q;
   const i64 p = static_cast<i64>(q) * nb;
   for (int e = threadIdx.x; e < q; e += BS) {
@@ -534,16 +628,23 @@ __global__ void __launch_bounds__(BS) k_gauss_path(PersistArgs P) {
     sth[e] = 0.0;
     bs[e] = A.b[base + e];
   }
+  __syncthreads();  // staged bands, mbarrier and the replicated theta state are read by every warp
   unsigned parity = 0;
-  const FistaCtl tmpl = *A.ctl;  // configuration (lambda filled per model)
-  const double w = tmpl.sscale, n = tmpl.n, c0 = tmpl.ss_const;
+  const FistaCtl* tmpl = A.ctl;  // configuration (lambda filled per model); written back only at exit
+  const double w = tmpl->sscale, n = tmpl->n, c0 = tmpl->ss_const;
+  const int bt_div = tmpl->bt_div, extrapolation = tmpl->extrapolation;
   auto reduce3 = [&](double a, double b, double c, double* out) {
-    out[0] = cta_sum<BS>(a, red);
-    out[1] = cta_sum<BS>(b, red);
-    out[2] = cta_sum<BS>(c, red);
+    if (P.dbg & 4) {
+      out[0] = cta_sum<BS>(a, red);
+      out[1] = cta_sum<BS>(b, red);
+      out[2] = cta_sum<BS>(c, red);
+    } else {
+      cta_sum3<BS>(a, b, c, red, out);
+    }
   };
-  auto apply = [&]() {
-    const double* xb = P.X + static_cast<i64>(lo) * q;
+  // bulk-async copy of the neighbour band of slabs [lo, lo + len) of xsrc
+  auto issue = [&](const double* xsrc) {
+    const double* xb = xsrc + static_cast<i64>(lo) * q;
     if (threadIdx.x == 0) {
       asm volatile("fence.proxy.async.global;" ::: "memory");
       const unsigned bytes = async::stage_manual(band, xb, static_cast<i64>(len) * q);
@@ -551,29 +652,48 @@ __global__ void __launch_bounds__(BS) k_gauss_path(PersistArgs P) {
       async::mbar_expect_tx(&mb, bytes);
       async::stage_bulk(band, xb, static_cast<i64>(len) * q, &mb);
     }
-    __syncthreads();
+  };
+  auto wait_band = [&]() {
     async::mbar_wait(&mb, parity);
     parity ^= 1u;
-    const double* xin = band + async::stage_shift(xb);
+  };
+  // S'(x) of this slab from the staged band -> sxs; objective partials of xs -> dst
+  auto compute = [&](const double* xsrc, double* dst) {
+    const double* xin = band + async::stage_shift(xsrc + static_cast<i64>(lo) * q);
     for (int e = threadIdx.x; e < q; e += BS) {
       const double* xe = xin + e;
       double a0 = 0.0, a1 = 0.0;
-      int t = 0;
-      for (; t + 1 < len; t += 2) {
-        a0 = fma(__ldg(gc + t), xe[static_cast<i64>(t) * q], a0);
-        a1 = fma(__ldg(gc + t + 1), xe[static_cast<i64>(t + 1) * q], a1);
+      if (hoist) {
+#pragma unroll
+        for (int t = 0; t < MB; t += 2) {
+          if (t < len) a0 = fma(gr[t], xe[static_cast<i64>(t) * q], a0);
+          if (t + 1 < len) a1 = fma(gr[t + 1], xe[static_cast<i64>(t + 1) * q], a1);
+        }
+      } else {
+        int t = 0;
+        for (; t + 1 < len; t += 2) {
+          a0 = fma(__ldg(gc + t), xe[static_cast<i64>(t) * q], a0);
+          a1 = fma(__ldg(gc + t + 1), xe[static_cast<i64>(t + 1) * q], a1);
+        }
+        if (t < len) a0 = fma(__ldg(gc + t), xe[static_cast<i64>(t) * q], a0);
       }
-      if (t < len) a0 = fma(__ldg(gc + t), xe[static_cast<i64>(t) * q], a0);
       u[e] = a0 + a1;
     }
     __syncthreads();
     const double* res = u;
-    double* bufs[2] = {t0, t1};
     int which = 0;
+    int r0 = rows_all;
     for (int j = A.d - 2; j >= 0; --j) {
-      smem_mode<BS>(res, bufs[which], A.dims, j, A.G[j], q, A.fa[j], A.fk[j]);
+      double* dst2 = which ? t1 : t0;
+      const int K = A.dims[j];
+      r0 -= K;
+      if (staged)
+        smem_mode_st<BS, MB>(res, dst2, K, q, A.fa[j], A.fk[j], sg + static_cast<i64>(r0) * MB, sgi + 2 * r0,
+                             sgi + 2 * r0 + K);
+      else
+        smem_mode<BS>(res, dst2, A.dims, j, A.G[j], q, A.fa[j], A.fk[j]);
       __syncthreads();
-      res = bufs[which];
+      res = dst2;
       which ^= 1;
     }
     double dots = 0.0, l1 = 0.0, l2 = 0.0;
@@ -587,10 +707,16 @@ __global__ void __launch_bounds__(BS) k_gauss_path(PersistArgs P) {
     double r[3];
     reduce3(dots, l1, l2, r);
     if (threadIdx.x == 0) {
-      P.part[3 * s] = r[0];
-      P.part[3 * s + 1] = r[1];
-      P.part[3 * s + 2] = r[2];
+      dst[3 * s] = r[0];
+      dst[3 * s + 1] = r[1];
+      dst[3 * s + 2] = r[2];
     }
+  };
+  auto apply = [&]() {
+    issue(P.X);
+    __syncthreads();
+    wait_band();
+    compute(P.X, P.part);
   };
   auto gather3 = [&](double* out) {  // fixed-order sum of every CTA's 3 partials
     double a = 0.0, b = 0.0, c = 0.0;
@@ -613,14 +739,14 @@ __global__ void __launch_bounds__(BS) k_gauss_path(PersistArgs P) {
     }
     __syncthreads();
     if (threadIdx.x == 0) {
-      cs = tmpl;
+      cs = *tmpl;
       cs.lambda = lam;
       // inner_objective(x_0) = (w<x0,S'x0> - 2<x0,b> + sum v z^2)/(2n) + lambda J(x_0)
       const double g0 = 0.5 * (w * tst - 2.0 * tb + c0) / n + lam * j_th;
       ctl_setup(cs, g0, w);
     }
     __syncthreads();
-    if (!tmpl.bt_div) {
+    if (!bt_div) {
       // nu = 1 (no restarts): x_k depends only on earlier iterates, omega_k =
       // (k-1)/(k+2) and the fixed step, so the monitor decision of iteration
       // k-1 is taken one step late, after the single grid barrier of step k,
@@ -629,7 +755,7 @@ __global__ void __launch_bounds__(BS) k_gauss_path(PersistArgs P) {
       const double delta = cs.delta, gamma = delta * lam;
       for (i64 k = 1; !cs.done; ++k) {
         const double omega =
-            tmpl.extrapolation == 0 ? static_cast<double>(k - 1) / static_cast<double>(k + 2) : 0.0;
+            extrapolation == 0 ? static_cast<double>(k - 1) / static_cast<double>(k + 2) : 0.0;
         double* Xk = P.X + (k & 1) * p;
         for (int e = threadIdx.x; e < q; e += BS) {
           const double xi = xs[e], xpi = xps[e], sxi = sxs[e], sxpi = sxps[e];
@@ -644,14 +770,7 @@ __global__ void __launch_bounds__(BS) k_gauss_path(PersistArgs P) {
           Xk[base + e] = ci;
         }
         grid_sync(P.bar, nb);
-        const double* xb = Xk + static_cast<i64>(lo) * q;
-        if (threadIdx.x == 0) {
-          asm volatile("fence.proxy.async.global;" ::: "memory");
-          const unsigned bytes = async::stage_manual(band, xb, static_cast<i64>(len) * q);
-          async::fence_proxy_async();
-          async::mbar_expect_tx(&mb, bytes);
-          async::stage_bulk(band, xb, static_cast<i64>(len) * q, &mb);
-        }
+        issue(Xk);
         if (k >= 2) {  // monitor iteration k-1 from its partials
           const double* pp = P.part + ((k - 1) & 1) * 3 * static_cast<i64>(nb);
           double a = 0.0, b = 0.0, c = 0.0;
@@ -662,8 +781,12 @@ __global__ void __launch_bounds__(BS) k_gauss_path(PersistArgs P) {
           }
           double r3[3];
           reduce3(a, b, c, r3);
-          if (threadIdx.x == 0)
-            ctl_step(cs, 0.5 * (r3[0] + c0) / n + lam * penalty_of(A.pen, A.alpha, r3[1], r3[2]));
+          if (threadIdx.x == 0) {
+            const double gk = 0.5 * (r3[0] + c0) / n + lam * penalty_of(A.pen, A.alpha, r3[1], r3[2]);
+            ctl_step(cs, gk);
+            if ((P.dbg & 8) && t < 2 && k < 8)
+              printf("s=%d t=%d k=%lld g=%.17g done=%d\n", s, t, static_cast<long long>(k), gk, cs.done);
+          }
           __syncthreads();
           if (cs.copy_best) {  // best := x_{k-1} (now in the x_prev slot)
             for (int e = threadIdx.x; e < q; e += BS) {
@@ -676,44 +799,7 @@ __global__ void __launch_bounds__(BS) k_gauss_path(PersistArgs P) {
         async::mbar_wait(&mb, parity);  // always consume the copy (keeps the barrier phase)
         parity ^= 1u;
         if (cs.done) break;
-        const double* xin = band + async::stage_shift(xb);
-        for (int e = threadIdx.x; e < q; e += BS) {
-          const double* xe = xin + e;
-          double a0 = 0.0, a1 = 0.0;
-          int t = 0;
-          for (; t + 1 < len; t += 2) {
-            a0 = fma(__ldg(gc + t), xe[static_cast<i64>(t) * q], a0);
-            a1 = fma(__ldg(gc + t + 1), xe[static_cast<i64>(t + 1) * q], a1);
-          }
-          if (t < len) a0 = fma(__ldg(gc + t), xe[static_cast<i64>(t) * q], a0);
-          u[e] = a0 + a1;
-        }
-        __syncthreads();
-        const double* res = u;
-        double* bufs[2] = {t0, t1};
-        int which = 0;
-        for (int j = A.d - 2; j >= 0; --j) {
-          smem_mode<BS>(res, bufs[which], A.dims, j, A.G[j], q, A.fa[j], A.fk[j]);
-          __syncthreads();
-          res = bufs[which];
-          which ^= 1;
-        }
-        double dots = 0.0, l1 = 0.0, l2 = 0.0;
-        for (int e = threadIdx.x; e < q; e += BS) {
-          const double sv = res[e], xv = xs[e];
-          sxs[e] = sv;
-          dots += xv * (w * sv - 2.0 * bs[e]);
-          l1 += fabs(xv);
-          l2 = fma(xv, xv, l2);
-        }
-        double r3[3];
-        reduce3(dots, l1, l2, r3);
-        if (threadIdx.x == 0) {
-          double* pk = P.part + (k & 1) * 3 * static_cast<i64>(nb);
-          pk[3 * s] = r3[0];
-          pk[3 * s + 1] = r3[1];
-          pk[3 * s + 2] = r3[2];
-        }
+        compute(Xk, P.part + (k & 1) * 3 * static_cast<i64>(nb));
       }
       if (threadIdx.x == 0) cs.copy_best = 0;  // any pending copy was applied above
       __syncthreads();
@@ -819,7 +905,9 @@ __global__ void __launch_bounds__(BS) k_gauss_path(PersistArgs P) {
 }
 
 static size_t path_smem(const GramStepArgs& A) {
-  return (static_cast<size_t>(12 + A.Gd.maxlen) * A.q + 4) * sizeof(double);
+  size_t staged = 0;  // staged Gram bands of modes 0 .. d-2
+  for (int j = 0; j < A.d - 1; ++j) staged += static_cast<size_t>(A.dims[j]) * (kPathTaps * sizeof(double) + 2 * sizeof(int));
+  return (static_cast<size_t>(12 + A.Gd.maxlen) * A.q + 4) * sizeof(double) + staged;
 }
 
 bool gauss_path_ok(const GramStepArgs& A) {

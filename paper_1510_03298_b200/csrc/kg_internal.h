@@ -145,6 +145,7 @@ void contract_tiled(const Launch& L, const double* A, double* out, i64 a, i64 K,
 // (already computed by a full H chain) and only the reductions run.
 enum HlastFlags { HL_LL_NEW = 1, HL_DOT = 2, HL_TRIALS = 4, HL_U_FLY = 8, HL_WRITE = 16 };
 constexpr int kMaxTrials = 8;
+constexpr int kPathTaps = 8;  // unrolled Gram band taps of k_gauss_path (cubic B-splines: 7)
 constexpr int kHlastCols = 2 + kMaxTrials;  // [ll_new, dot, trial_0..]
 struct HlastArgs {
   i64 n1 = 0, p1 = 0, m = 0;
@@ -257,6 +258,7 @@ struct PersistArgs {
   i64* iters_out = nullptr;   // n_lambda
   int* status_out = nullptr;  // n_lambda
   int* nmodels = nullptr;     // [models stored, stop: 0 none, 1 truncated, 2 first model failed]
+  int dbg = 0;                // debug switches (KG_PATH_DBG)
 };
 bool fista_persist_ok(const GramStepArgs& A);
 void fista_persist(const Launch& L, const PersistArgs& P);

@@ -1292,6 +1292,7 @@ static kg_path_result* fit_path(kg_ctx* ctx, const kg_design* D, const kg_obs* O
     P.iters_out = static_cast<i64*>(its.p);
     P.status_out = static_cast<int*>(stat.p) + 2;
     P.nmodels = static_cast<int*>(stat.p);
+    if (const char* e = std::getenv("KG_PATH_DBG")) P.dbg = std::atoi(e);
     gauss_path(ctx->L(), P);
     std::vector<double> ho(nl);
     std::vector<i64> hi(nl);
