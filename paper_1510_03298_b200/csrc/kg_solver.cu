@@ -20,6 +20,8 @@
 #include <cstring>
 #include <limits>
 #include <memory>
+#include <mutex>
+#include <unordered_set>
 #include <random>
 #include <string>
 #include <vector>
@@ -30,22 +32,47 @@
 namespace kg {
 
 // ------------------------------------------------------------ device memory
+// Workspaces come from the device's stream-ordered pool (cudaMallocAsync on
+// the context stream, release threshold raised in kg_ctx_create), so repeated
+// fits reuse cached memory instead of paying cudaMalloc / synchronising
+// cudaFree.  g_stream is the ordering stream of the current C-ABI call; a
+// buffer whose stream has been destroyed is freed synchronously.
+thread_local cudaStream_t g_stream = nullptr;
+std::mutex g_live_mu;
+std::unordered_set<cudaStream_t> g_live_streams;
+
+static bool stream_live(cudaStream_t s) {
+  std::lock_guard<std::mutex> lk(g_live_mu);
+  return g_live_streams.count(s) != 0;
+}
+
 struct DBuf {
   void* p = nullptr;
   size_t bytes = 0;
+  cudaStream_t s = nullptr;  // stream the allocation is ordered on (nullptr: plain cudaMalloc)
   DBuf() = default;
   DBuf(const DBuf&) = delete;
   DBuf& operator=(const DBuf&) = delete;
   ~DBuf() { release(); }
   void release() {
-    if (p) cudaFree(p);
+    if (p) {
+      if (s && stream_live(s))
+        cudaFreeAsync(p, s);
+      else
+        cudaFree(p);
+    }
     p = nullptr;
     bytes = 0;
+    s = nullptr;
   }
   void alloc(size_t b) {
     if (b <= bytes && p) return;
     release();
-    KG_CUDA(cudaMalloc(&p, b ? b : 8));
+    s = g_stream;
+    if (s)
+      KG_CUDA(cudaMallocAsync(&p, b ? b : 8, s));
+    else
+      KG_CUDA(cudaMalloc(&p, b ? b : 8));
     bytes = b;
   }
   double* d() const { return static_cast<double*>(p); }
@@ -146,10 +173,12 @@ static void upload_factor(const FactorHost& h, FactorOwn& f, cudaStream_t s) {
     blen.alloc(sizeof(int) * len.size());
     boff.alloc(sizeof(i64) * off.size());
     bcoef.alloc(sizeof(double) * std::max<size_t>(coef.size(), 1));
-    KG_CUDA(cudaMemcpy(blo.p, lo.data(), sizeof(int) * lo.size(), cudaMemcpyHostToDevice));
-    KG_CUDA(cudaMemcpy(blen.p, len.data(), sizeof(int) * len.size(), cudaMemcpyHostToDevice));
-    KG_CUDA(cudaMemcpy(boff.p, off.data(), sizeof(i64) * off.size(), cudaMemcpyHostToDevice));
-    if (!coef.empty()) KG_CUDA(cudaMemcpy(bcoef.p, coef.data(), sizeof(double) * coef.size(), cudaMemcpyHostToDevice));
+    // pageable sources: cudaMemcpyAsync returns once the host data is staged
+    KG_CUDA(cudaMemcpyAsync(blo.p, lo.data(), sizeof(int) * lo.size(), cudaMemcpyHostToDevice, blo.s));
+    KG_CUDA(cudaMemcpyAsync(blen.p, len.data(), sizeof(int) * len.size(), cudaMemcpyHostToDevice, blen.s));
+    KG_CUDA(cudaMemcpyAsync(boff.p, off.data(), sizeof(i64) * off.size(), cudaMemcpyHostToDevice, boff.s));
+    if (!coef.empty())
+      KG_CUDA(cudaMemcpyAsync(bcoef.p, coef.data(), sizeof(double) * coef.size(), cudaMemcpyHostToDevice, bcoef.s));
     op.lo = static_cast<const int*>(blo.p);
     op.len = static_cast<const int*>(blen.p);
     op.off = static_cast<const i64*>(boff.p);
@@ -1343,6 +1372,11 @@ namespace {
 
 template <class F>
 kg_status guarded(kg_ctx* ctx, F&& f) {
+  struct StreamScope {  // pool allocations of this call are ordered on the context stream
+    cudaStream_t saved;
+    explicit StreamScope(kg_ctx* c) : saved(g_stream) { g_stream = c ? c->s : nullptr; }
+    ~StreamScope() { g_stream = saved; }
+  } scope(ctx);
   try {
     f();
     if (ctx) {
@@ -1399,6 +1433,12 @@ kg_status kg_ctx_create(int device, kg_ctx** out) {
     KG_CUDA(cudaSetDevice(device));
     KG_CUDA(cudaStreamCreateWithFlags(&ctx->s, cudaStreamNonBlocking));
     KG_CUDA(cudaMallocHost(&ctx->pinned, 4096));
+    cudaMemPool_t pool;
+    KG_CUDA(cudaDeviceGetDefaultMemPool(&pool, device));
+    uint64_t keep = UINT64_MAX;  // keep freed workspaces cached between fits
+    KG_CUDA(cudaMemPoolSetAttribute(pool, cudaMemPoolAttrReleaseThreshold, &keep));
+    std::lock_guard<std::mutex> lk(g_live_mu);
+    g_live_streams.insert(ctx->s);
   });
   if (st == KG_OK) *out = ctx.release();
   return st;
@@ -1417,7 +1457,13 @@ void kg_ctx_destroy(kg_ctx* ctx) {
   cudaSetDevice(ctx->device);
   if (ctx->s) cudaStreamSynchronize(ctx->s);
   if (ctx->pinned) cudaFreeHost(ctx->pinned);
-  if (ctx->s) cudaStreamDestroy(ctx->s);
+  if (ctx->s) {
+    {
+      std::lock_guard<std::mutex> lk(g_live_mu);
+      g_live_streams.erase(ctx->s);
+    }
+    cudaStreamDestroy(ctx->s);
+  }
   delete ctx;
 }
 
