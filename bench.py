@@ -194,6 +194,7 @@ def run_ours(args):
     clocks.start()
     ctx.reset_launches()
     total_ms, total_iters = 0.0, 0
+    pk_ms, pk_bytes, pk_launches = 0.0, 0.0, 0
     with torch.cuda.stream(stream):
         for _ in range(args.steps):
             flush.zero_()
@@ -205,8 +206,15 @@ def run_ours(args):
             e1.synchronize()
             total_ms += e0.elapsed_time(e1)
             total_iters += sum(res.inner_iters)
+            st = path_kernel_stats(ctx)
+            if st is not None:
+                pk_ms += st[0]
+                pk_bytes += st[1]
+                pk_launches += 1
     launches = ctx.launches
     torch.cuda.synchronize()
+    # the whole-path kernel of the last timed step (one cooperative launch per path)
+    pk = path_kernel_stats(ctx)
     clk = clocks.stop()
     if world > 1:
         dist.barrier()
@@ -220,16 +228,41 @@ def run_ours(args):
     value = all_iters / (max_ms / 1000.0)
     iters_per_path = sum(res.inner_iters)
 
-    # roofline of the dominant kernel (fused mode-1 FISTA pass), timed live on the ctx stream
-    avg_ms, nbytes = K_time(ctx, design, obs, 0)
+    # roofline.  Dominant kernel of the step: the whole-path kernel (Gaussian
+    # constant-weight paths, one cooperative launch per path), event-timed on
+    # the ctx stream inside the timed steps above; otherwise the fused n-space
+    # FISTA pass.  The rho-contraction passes (the n-array traffic of every
+    # n-space step) are timed live here with kg_time_kernel.
     hbm, peak_kind = peaks()
-    achieved = nbytes / (avg_ms / 1000.0) / 1e9
+    f_ms, f_bytes = K_time(ctx, design, obs, 0)
     c_ms, c_bytes = K_time(ctx, design, obs, 1)
     traffic = None
     tfile = os.path.join(ROOT, "profiles", f"traffic_{args.config}.json")
     if os.path.exists(tfile):
         with open(tfile) as f:
-            traffic = json.load(f).get("fused_pass_dram_bytes")
+            traffic = json.load(f)
+    rho = {"fused_pass": {"kernel": "k_fused_fast (mode-1 H-last + v(eta-z)^2 + V.* + G-first, one n-array pass)",
+                          "bytes_per_launch": f_bytes, "avg_launch_ms": f_ms,
+                          "achieved": f_bytes / (f_ms / 1000.0) / 1e9, "frac": f_bytes / (f_ms / 1000.0) / 1e9 / hbm},
+           "contraction": {"kernel": "k_contract_rs (largest banded H-chain step)", "bytes_per_launch": c_bytes,
+                           "avg_launch_ms": c_ms, "achieved": c_bytes / (c_ms / 1000.0) / 1e9,
+                           "frac": c_bytes / (c_ms / 1000.0) / 1e9 / hbm},
+           "peak": hbm, "unit": "GB/s",
+           "dram_bytes_ncu": traffic.get("fused_pass_dram_bytes") if traffic else None}
+    if pk_launches:
+        achieved = pk_bytes / (pk_ms / 1000.0) / 1e9
+        roof = {"bound": "hbm", "kernel": "k_gauss_path (whole lambda path, one cooperative launch)",
+                "achieved": achieved, "peak": hbm, "peak_kind": peak_kind, "unit": "GB/s", "frac": achieved / hbm,
+                "traffic": traffic.get("path_kernel_dram_bytes") if traffic else None,
+                "bytes_per_launch": pk_bytes / pk_launches, "avg_launch_ms": pk_ms / pk_launches,
+                "share_of_step": pk_ms / max_ms if world == 1 else None,
+                "note": "latency-bound: one grid barrier per prox-grad step; its bytes are p-space (x bands, "
+                        "partials, coefficients) and mostly L2-resident"}
+    else:
+        achieved = f_bytes / (f_ms / 1000.0) / 1e9
+        roof = {"bound": "hbm", "kernel": rho["fused_pass"]["kernel"], "achieved": achieved, "peak": hbm,
+                "peak_kind": peak_kind, "unit": "GB/s", "frac": achieved / hbm,
+                "traffic": rho["dram_bytes_ncu"], "bytes_per_launch": f_bytes, "avg_launch_ms": f_ms}
 
     # e2e: the public kronglm.fit_path call with host buffers (design upload,
     # observation upload, path, all coefficient downloads), same metric.
@@ -255,13 +288,7 @@ def run_ours(args):
                            "l2": "256 MB buffer written between timed steps", "parallelism": f"replicas x{world}"},
                 "e2e": {"value": e2e_iters / (e2e_ms / 1000.0), "unit": UNIT, "h2d_bytes_per_step": int(h2d),
                         "d2h_bytes_per_step": int(d2h), "ms_per_step": e2e_ms / max(1, min(args.steps, 3))},
-                "roofline": {"bound": "hbm", "kernel": "k_fused1<FV_FISTA> (mode-1 H-last + v(eta-z)^2 + G-first)",
-                             "achieved": achieved, "peak": hbm, "peak_kind": peak_kind, "unit": "GB/s",
-                             "frac": achieved / hbm, "traffic": traffic, "bytes_per_launch": nbytes,
-                             "avg_launch_ms": avg_ms,
-                             "contraction": {"kernel": "k_contract (largest H step)", "bytes_per_launch": c_bytes,
-                                             "avg_launch_ms": c_ms,
-                                             "achieved": c_bytes / (c_ms / 1000.0) / 1e9}},
+                "roofline": roof, "rho_contraction": rho,
                 "clocks": clk, "gpu_launches": int(launches)}
     # CPU baseline: the oracle port on rank 0 at N = 1, bounded prefix of the same path
     if rank == 0 and world == 1 and not args.no_cpu_baseline:
@@ -283,6 +310,15 @@ def run_ours(args):
     if world > 1:
         dist.barrier()
         dist.destroy_process_group()
+
+
+def path_kernel_stats(ctx):
+    import ctypes as C
+    from paper_1510_03298_b200 import _lib
+    ms, b, st = C.c_double(), C.c_double(), C.c_int64()
+    if _lib.load().kg_path_kernel_stats(ctx.h, C.byref(ms), C.byref(b), C.byref(st)) != 0:
+        return None
+    return ms.value, b.value, st.value
 
 
 def K_time(ctx, design, obs, which, reps=20):

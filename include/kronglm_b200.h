@@ -159,6 +159,9 @@ int kg_result_status(const kg_path_result* res, int64_t t);
 int64_t kg_result_nonzero(const kg_path_result* res, int64_t t);
 /* Copies the p coefficients of model t into host memory. */
 kg_status kg_result_coef(kg_path_result* res, int64_t t, double* out);
+/* Coefficients of models [first, first + count) in one copy: out is
+ * count x p, model-major (the rows kg_result_coef returns one by one). */
+kg_status kg_result_coefs(kg_path_result* res, int64_t first, int64_t count, double* out);
 void kg_result_free(kg_path_result* res);
 
 /* predict (path.cpp:83-89): eta = H(coef), mu = g^{-1}(eta).  Host buffers. */
@@ -181,6 +184,14 @@ int64_t kg_linear_index(int64_t d, const int64_t* multi_index, const int64_t* di
  * launch ("roofline"). */
 kg_status kg_time_kernel(kg_ctx* ctx, const kg_design* design, const kg_obs* obs, int which, int reps,
                          double* avg_ms, double* bytes);
+/* Device time of the last whole-path kernel (k_gauss_path: one cooperative
+ * launch runs every FISTA step of a Gaussian constant-weight lambda path),
+ * measured with CUDA events around that launch on the context stream, and its
+ * algorithmic bytes: per prox-grad step the neighbour bands of x read by every
+ * slab, the x slabs written and the per-slab partials exchanged, plus the
+ * coefficient rows stored per model ("roofline").  Returns
+ * KG_EINVAL when no such launch has run on this context. */
+kg_status kg_path_kernel_stats(const kg_ctx* ctx, double* ms, double* bytes, int64_t* steps);
 /* Number of library kernel launches issued since the last reset (host-side
  * counter of launches, graph-replayed kernels counted per replay). */
 int64_t kg_launch_count(const kg_ctx* ctx);

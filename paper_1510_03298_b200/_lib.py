@@ -77,12 +77,14 @@ _SIGS = {
     "kg_result_status": (C.c_int, [_vp, _i64]),
     "kg_result_nonzero": (_i64, [_vp, _i64]),
     "kg_result_coef": (C.c_int, [_vp, _i64, _pd]),
+    "kg_result_coefs": (C.c_int, [_vp, _i64, _i64, _pd]),
     "kg_result_free": (None, [_vp]),
     "kg_predict": (C.c_int, [_vp, _vp, C.c_int, _pd, _pd, _pd]),
     "kg_bspline_design": (C.c_int, [_i64, _pd, _i64, _i64, _pd]),
     "kg_default_basis_count": (_i64, [_i64, _i64]),
     "kg_linear_index": (_i64, [_i64, _pi, _pi]),
     "kg_time_kernel": (C.c_int, [_vp, _vp, _vp, C.c_int, C.c_int, _pd, _pd]),
+    "kg_path_kernel_stats": (C.c_int, [_vp, _pd, _pd, C.POINTER(_i64)]),
     "kg_launch_count": (_i64, [_vp]),
     "kg_launch_count_reset": (None, [_vp]),
 }

@@ -886,7 +886,10 @@ __global__ void __launch_bounds__(BS) k_gauss_path(PersistArgs P) {
     }
     if (status != KG_S_CONVERGED) {
       stop = t == 0 ? 2 : 1;
-      if (s == 0 && threadIdx.x == 0) P.status_out[t] = status;
+      if (s == 0 && threadIdx.x == 0) {
+        P.status_out[t] = status;
+        P.iters_out[t] = cs.iterations;
+      }
     } else {
       for (int e = threadIdx.x; e < q; e += BS) P.coefs[static_cast<i64>(t) * p + base + e] = th[e];
       if (s == 0 && threadIdx.x == 0) {

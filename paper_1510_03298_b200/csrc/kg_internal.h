@@ -278,7 +278,17 @@ void reduce_cols(const Launch& L, const double* part, int nrows, int ncols, int 
 
 // Gram + power iteration for one factor (spectral.cpp:8-42)
 void gram(const Launch& L, const FactorDev& f, double* G, int* glo, int* ghi);
-void power_iteration(const Launch& L, i64 p, const double* G, const int* glo, const int* ghi, const double* v0,
-                     double tol, i64 max_iters, double* out /* [value, iterations, status] */);
+// One power iteration per job, all jobs in one launch (one warp each).
+struct PowerJob {
+  i64 p = 0;
+  const double* G = nullptr;  // dense p x p Gram, column-major
+  const int* glo = nullptr;   // row band [glo, ghi)
+  const int* ghi = nullptr;
+  const double* v0 = nullptr;
+  double* out = nullptr;      // [value, iterations, status]
+  int band = 0;               // max row band width (register path when <= kPowerTaps and p <= 32 * kPowerRows)
+};
+constexpr int kPowerTaps = 8, kPowerRows = 8;
+void power_iterations(const Launch& L, const PowerJob* jobs_dev, int njobs, i64 max_p, double tol, i64 max_iters);
 
 }  // namespace kg

@@ -987,49 +987,91 @@ void gram(const Launch& L, const FactorDev& f, double* G, int* glo, int* ghi) {
   bump(L);
 }
 
-// Power iteration (spectral.cpp:8-42) by a single warp: v stays in shared
-// memory, the two reductions per step are warp-shuffle trees.
-__global__ void k_power(i64 p, const double* G, const int* glo, const int* ghi, const double* v0, double tol,
-                        i64 max_iters, double* out) {
+// Power iteration (spectral.cpp:8-42), one warp per job (blockIdx.x), every
+// factor of a design in one launch.  v stays in shared memory; the two
+// reductions per step are warp-shuffle trees.  Register path: each lane keeps
+// its rows i = lane + 32 r of the Gram band in registers (B-spline Grams are
+// 7 wide), so a step is kPowerRows x kPowerTaps FMAs on shared v; the per-row
+// summation order (ascending column) is the same on both paths.
+__global__ void k_power(const PowerJob* jobs, double tol, i64 max_iters) {
   extern __shared__ double sh[];
+  const PowerJob J = jobs[blockIdx.x];
+  const i64 p = J.p;
   double* v = sh;
   double* av = sh + p;
   const int l = threadIdx.x;
-  for (i64 i = l; i < p; i += 32) v[i] = v0[i];
+  const bool reg = J.band <= kPowerTaps && p <= 32 * kPowerRows;
+  double c[kPowerRows][kPowerTaps];
+  int lo[kPowerRows], ln[kPowerRows];
+#pragma unroll
+  for (int r = 0; r < kPowerRows; ++r) {
+    const i64 i = l + 32 * r;
+    lo[r] = 0;
+    ln[r] = 0;
+    if (reg && i < p) {
+      lo[r] = J.glo[i];
+      ln[r] = J.ghi[i] - lo[r];
+    }
+#pragma unroll
+    for (int t = 0; t < kPowerTaps; ++t) c[r][t] = t < ln[r] ? J.G[i + p * (lo[r] + t)] : 0.0;
+  }
+  for (i64 i = l; i < p; i += 32) v[i] = J.v0[i];
   __syncwarp();
   double value = 0.0;
   i64 settled = 0;
   for (i64 it = 1; it <= max_iters; ++it) {
     double nn = 0.0, dot = 0.0;
-    for (i64 i = l; i < p; i += 32) {
-      double s = 0.0;
-      for (int k = glo[i]; k < ghi[i]; ++k) s += G[i + p * k] * v[k];
-      av[i] = s;
-      nn += s * s;
-      dot += v[i] * s;
+    double a[kPowerRows];
+    if (reg) {
+#pragma unroll
+      for (int r = 0; r < kPowerRows; ++r) {
+        double s = 0.0;
+#pragma unroll
+        for (int t = 0; t < kPowerTaps; ++t)
+          if (t < ln[r]) s += c[r][t] * v[lo[r] + t];
+        a[r] = s;
+        if (l + 32 * r < p) {
+          nn += s * s;
+          dot += v[l + 32 * r] * s;
+        }
+      }
+    } else {
+      for (i64 i = l; i < p; i += 32) {
+        double s = 0.0;
+        for (int k = J.glo[i]; k < J.ghi[i]; ++k) s += J.G[i + p * k] * v[k];
+        av[i] = s;
+        nn += s * s;
+        dot += v[i] * s;
+      }
     }
     nn = warp_allsum(nn);
     dot = warp_allsum(dot);
     const double norm = sqrt(nn);
     if (norm == 0.0) {
       if (l == 0) {
-        out[0] = 0.0;
-        out[1] = static_cast<double>(it);
-        out[2] = 0.0;
+        J.out[0] = 0.0;
+        J.out[1] = static_cast<double>(it);
+        J.out[2] = 0.0;
       }
       return;
     }
     __syncwarp();
-    for (i64 i = l; i < p; i += 32) v[i] = av[i] / norm;
+    if (reg) {
+#pragma unroll
+      for (int r = 0; r < kPowerRows; ++r)
+        if (l + 32 * r < p) v[l + 32 * r] = a[r] / norm;
+    } else {
+      for (i64 i = l; i < p; i += 32) v[i] = av[i] / norm;
+    }
     __syncwarp();
     const double change = fabs(dot - value);
     value = dot;
     if (change <= tol * fmax(fabs(value), 1e-300)) {
       if (++settled >= 2) {
         if (l == 0) {
-          out[0] = value;
-          out[1] = static_cast<double>(it);
-          out[2] = 0.0;
+          J.out[0] = value;
+          J.out[1] = static_cast<double>(it);
+          J.out[2] = 0.0;
         }
         return;
       }
@@ -1038,17 +1080,17 @@ __global__ void k_power(i64 p, const double* G, const int* glo, const int* ghi, 
     }
   }
   if (l == 0) {
-    out[0] = value;
-    out[1] = static_cast<double>(max_iters);
-    out[2] = 1.0;
+    J.out[0] = value;
+    J.out[1] = static_cast<double>(max_iters);
+    J.out[2] = 1.0;
   }
 }
 
-void power_iteration(const Launch& L, i64 p, const double* G, const int* glo, const int* ghi, const double* v0,
-                     double tol, i64 max_iters, double* out) {
-  const size_t sm = 2 * static_cast<size_t>(p) * sizeof(double);
+void power_iterations(const Launch& L, const PowerJob* jobs_dev, int njobs, i64 max_p, double tol, i64 max_iters) {
+  if (njobs < 1) return;
+  const size_t sm = 2 * static_cast<size_t>(max_p) * sizeof(double);
   if (sm > 48 * 1024) KG_CUDA(cudaFuncSetAttribute(k_power, cudaFuncAttributeMaxDynamicSharedMemorySize, 200 * 1024));
-  k_power<<<1, 32, sm, L.s>>>(p, G, glo, ghi, v0, tol, max_iters, out);
+  k_power<<<njobs, 32, sm, L.s>>>(jobs_dev, tol, max_iters);
   bump(L);
 }
 

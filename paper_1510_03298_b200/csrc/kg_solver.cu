@@ -96,6 +96,10 @@ struct kg_ctx {
   kg::i64 err_cell = -1;
   int rank = 0, world = 1;
   void* pinned = nullptr;  // small pinned staging area for scalars
+  // last whole-path kernel: event-timed device ms, algorithmic bytes, FISTA steps
+  double path_ms = -1.0, path_bytes = 0.0;
+  kg::i64 path_steps = 0;
+  cudaEvent_t ev[2] = {nullptr, nullptr};
   kg::Launch L() { return {s, &launches}; }
   double* pin() { return static_cast<double*>(pinned); }
 };
@@ -196,8 +200,19 @@ static void upload_factor(const FactorHost& h, FactorOwn& f, cudaStream_t s) {
 
 // Spectral radius of X^T X for one factor: banded Gram + single-warp power
 // iteration on the device; start vector exactly as spectral.cpp:17-23.
-static double factor_spectral(kg_ctx* ctx, const FactorHost& h, FactorOwn& f) {
+// Spectral radius of X^T X for one factor (spectral.cpp:8-42): the Gram and
+// start vector are prepared per factor; every factor of a design then runs its
+// power iteration in one batched launch (spectral_run).
+struct SpectralJob {
+  i64 p = 0;
+  double immediate = -1.0;  // p == 1: |sum x^2| directly (spectral.cpp:14)
+  DBuf G, glo, ghi, v0;
+  int band = 0;
+};
+
+static void spectral_prepare(kg_ctx* ctx, const FactorHost& h, FactorOwn& f, SpectralJob& J) {
   const i64 p = h.p;
+  J.p = p;
   // column bands of X (rows where column k is nonzero)
   std::vector<int> clo(p), chi(p);
   for (i64 k = 0; k < p; ++k) {
@@ -211,6 +226,7 @@ static double factor_spectral(kg_ctx* ctx, const FactorHost& h, FactorOwn& f) {
     chi[k] = first < 0 ? 0 : static_cast<int>(last + 1);
   }
   std::vector<int> glo(p, 0), ghi(p, 0);
+  int band = 0;
   for (i64 a = 0; a < p; ++a) {
     i64 first = -1, last = -1;
     for (i64 b = 0; b < p; ++b)
@@ -220,11 +236,14 @@ static double factor_spectral(kg_ctx* ctx, const FactorHost& h, FactorOwn& f) {
       }
     glo[a] = first < 0 ? 0 : static_cast<int>(first);
     ghi[a] = first < 0 ? 0 : static_cast<int>(last + 1);
+    band = std::max(band, ghi[a] - glo[a]);
   }
+  J.band = band;
   if (p == 1) {  // spectral.cpp:14
     double s = 0.0;
     for (i64 i = 0; i < h.n; ++i) s += h.X[i] * h.X[i];
-    return std::abs(s);
+    J.immediate = std::abs(s);
+    return;
   }
   std::mt19937_64 rng(0x9e3779b97f4a7c15ull);
   std::uniform_real_distribution<double> unif(0.5, 1.5);
@@ -236,24 +255,54 @@ static double factor_spectral(kg_ctx* ctx, const FactorHost& h, FactorOwn& f) {
     const double sq = std::sqrt(z);
     for (double& x : v0) x /= sq;
   }
-  DBuf G, dglo, dghi, dv0, out;
-  G.alloc(sizeof(double) * p * p);
-  KG_CUDA(cudaMemsetAsync(G.p, 0, sizeof(double) * p * p, ctx->s));
-  dglo.alloc(sizeof(int) * p);
-  dghi.alloc(sizeof(int) * p);
-  dv0.alloc(sizeof(double) * p);
-  out.alloc(sizeof(double) * 3);
-  KG_CUDA(cudaMemcpyAsync(dglo.p, glo.data(), sizeof(int) * p, cudaMemcpyHostToDevice, ctx->s));
-  KG_CUDA(cudaMemcpyAsync(dghi.p, ghi.data(), sizeof(int) * p, cudaMemcpyHostToDevice, ctx->s));
-  KG_CUDA(cudaMemcpyAsync(dv0.p, v0.data(), sizeof(double) * p, cudaMemcpyHostToDevice, ctx->s));
-  gram(ctx->L(), f.dev, G.d(), static_cast<int*>(dglo.p), static_cast<int*>(dghi.p));
-  power_iteration(ctx->L(), p, G.d(), static_cast<int*>(dglo.p), static_cast<int*>(dghi.p), dv0.d(), 1e-14, 500000,
-                  out.d());
-  double res[3];
-  KG_CUDA(cudaMemcpyAsync(res, out.p, sizeof(res), cudaMemcpyDeviceToHost, ctx->s));
+  J.G.alloc(sizeof(double) * p * p);
+  KG_CUDA(cudaMemsetAsync(J.G.p, 0, sizeof(double) * p * p, ctx->s));
+  J.glo.alloc(sizeof(int) * p);
+  J.ghi.alloc(sizeof(int) * p);
+  J.v0.alloc(sizeof(double) * p);
+  KG_CUDA(cudaMemcpyAsync(J.glo.p, glo.data(), sizeof(int) * p, cudaMemcpyHostToDevice, ctx->s));
+  KG_CUDA(cudaMemcpyAsync(J.ghi.p, ghi.data(), sizeof(int) * p, cudaMemcpyHostToDevice, ctx->s));
+  KG_CUDA(cudaMemcpyAsync(J.v0.p, v0.data(), sizeof(double) * p, cudaMemcpyHostToDevice, ctx->s));
+  gram(ctx->L(), f.dev, J.G.d(), static_cast<int*>(J.glo.p), static_cast<int*>(J.ghi.p));
+}
+
+static std::vector<double> spectral_run(kg_ctx* ctx, std::vector<std::unique_ptr<SpectralJob>>& jobs) {
+  std::vector<PowerJob> pj;
+  std::vector<size_t> idx;
+  i64 max_p = 1;
+  for (size_t k = 0; k < jobs.size(); ++k) {
+    SpectralJob& J = *jobs[k];
+    if (J.immediate >= 0.0) continue;
+    PowerJob q;
+    q.p = J.p;
+    q.G = J.G.d();
+    q.glo = static_cast<const int*>(J.glo.p);
+    q.ghi = static_cast<const int*>(J.ghi.p);
+    q.v0 = J.v0.d();
+    q.band = J.band;
+    pj.push_back(q);
+    idx.push_back(k);
+    max_p = std::max(max_p, J.p);
+  }
+  std::vector<double> vals(jobs.size(), 0.0);
+  for (size_t k = 0; k < jobs.size(); ++k)
+    if (jobs[k]->immediate >= 0.0) vals[k] = jobs[k]->immediate;
+  if (pj.empty()) return vals;
+  DBuf out, djobs;
+  out.alloc(sizeof(double) * 3 * pj.size());
+  for (size_t k = 0; k < pj.size(); ++k) pj[k].out = out.d() + 3 * k;
+  djobs.alloc(sizeof(PowerJob) * pj.size());
+  KG_CUDA(cudaMemcpyAsync(djobs.p, pj.data(), sizeof(PowerJob) * pj.size(), cudaMemcpyHostToDevice, ctx->s));
+  power_iterations(ctx->L(), static_cast<const PowerJob*>(djobs.p), static_cast<int>(pj.size()), max_p, 1e-14,
+                   500000);
+  std::vector<double> res(3 * pj.size());
+  KG_CUDA(cudaMemcpyAsync(res.data(), out.p, sizeof(double) * res.size(), cudaMemcpyDeviceToHost, ctx->s));
   sync(ctx);
-  if (res[2] != 0.0) throw Error(E_POWER, "power iteration did not converge after 500000 iterations");
-  return res[0];
+  for (size_t k = 0; k < pj.size(); ++k) {
+    if (res[3 * k + 2] != 0.0) throw Error(E_POWER, "power iteration did not converge after 500000 iterations");
+    vals[idx[k]] = res[3 * k];
+  }
+  return vals;
 }
 
 }  // namespace kg
@@ -1322,7 +1371,13 @@ static kg_path_result* fit_path(kg_ctx* ctx, const kg_design* D, const kg_obs* O
     P.status_out = static_cast<int*>(stat.p) + 2;
     P.nmodels = static_cast<int*>(stat.p);
     if (const char* e = std::getenv("KG_PATH_DBG")) P.dbg = std::atoi(e);
+    if (!ctx->ev[0]) {
+      KG_CUDA(cudaEventCreate(&ctx->ev[0]));
+      KG_CUDA(cudaEventCreate(&ctx->ev[1]));
+    }
+    KG_CUDA(cudaEventRecord(ctx->ev[0], ctx->s));
     gauss_path(ctx->L(), P);
+    KG_CUDA(cudaEventRecord(ctx->ev[1], ctx->s));
     std::vector<double> ho(nl);
     std::vector<i64> hi(nl);
     std::vector<int> hs(nl + 2);
@@ -1331,6 +1386,21 @@ static kg_path_result* fit_path(kg_ctx* ctx, const kg_design* D, const kg_obs* O
     KG_CUDA(cudaMemcpyAsync(hs.data(), stat.p, sizeof(int) * (nl + 2), cudaMemcpyDeviceToHost, ctx->s));
     sync(ctx);
     const int models = hs[0], stop = hs[1];
+    {  // kg_path_kernel_stats
+      float ms = 0.0f;
+      KG_CUDA(cudaEventElapsedTime(&ms, ctx->ev[0], ctx->ev[1]));
+      i64 steps = 0;
+      const int ran = models + (stop != 0 ? 1 : 0);  // a failed model's iterations count too
+      for (int t = 0; t < ran && t < nl; ++t) steps += hi[t] > 0 ? hi[t] : 0;
+      const GramStepArgs& g = P.g;
+      double band = 0.0;  // sum over slabs of the neighbour band length
+      for (i64 sl = 0; sl < g.pd; ++sl) band += g.Gd.hlen[sl];
+      const double nb = static_cast<double>(g.pd);
+      const double per_step = 8.0 * (band * g.q + static_cast<double>(D->P)) + 24.0 * nb * nb;
+      ctx->path_ms = ms;
+      ctx->path_steps = steps;
+      ctx->path_bytes = per_step * static_cast<double>(steps) + 8.0 * static_cast<double>(D->P) * (models + 2);
+    }
     if (stop == 2)
       throw Error(E_RUNTIME, std::string("fit_path: first model did not converge (") + status_name(hs[2]) + ")");
     res->truncated = stop == 1;
@@ -1457,6 +1527,8 @@ void kg_ctx_destroy(kg_ctx* ctx) {
   cudaSetDevice(ctx->device);
   if (ctx->s) cudaStreamSynchronize(ctx->s);
   if (ctx->pinned) cudaFreeHost(ctx->pinned);
+  for (cudaEvent_t e : ctx->ev)
+    if (e) cudaEventDestroy(e);
   if (ctx->s) {
     {
       std::lock_guard<std::mutex> lk(g_live_mu);
@@ -1476,6 +1548,13 @@ kg_status kg_ctx_synchronize(kg_ctx* ctx) {
 void kg_ctx_shard(const kg_ctx* ctx, int* rank, int* world) {
   *rank = ctx->rank;
   *world = ctx->world;
+}
+kg_status kg_path_kernel_stats(const kg_ctx* ctx, double* ms, double* bytes, int64_t* steps) {
+  if (!ctx || ctx->path_ms < 0.0) return KG_EINVAL;
+  *ms = ctx->path_ms;
+  *bytes = ctx->path_bytes;
+  *steps = ctx->path_steps;
+  return KG_OK;
 }
 int64_t kg_launch_count(const kg_ctx* ctx) { return ctx->launches; }
 void kg_launch_count_reset(kg_ctx* ctx) { ctx->launches = 0; }
@@ -1517,8 +1596,8 @@ kg_status kg_design_create(kg_ctx* ctx, int64_t c, int64_t d, const int64_t* n, 
     D->f.resize(c);
     D->spectral.assign(c, std::vector<double>(d, 0.0));
     D->lipfac = 0.0;
+    std::vector<std::unique_ptr<SpectralJob>> sjobs;
     for (i64 r = 0; r < c; ++r) {
-      double pr = 1.0;
       for (i64 j = 0; j < d; ++j) {
         FactorHost full;
         full.n = D->n_full[j];
@@ -1527,7 +1606,8 @@ kg_status kg_design_create(kg_ctx* ctx, int64_t c, int64_t d, const int64_t* n, 
         auto fo = std::make_unique<FactorOwn>();
         // the spectral radius always uses the full factor (L-hat is global)
         upload_factor(full, *fo, ctx->s);
-        D->spectral[r][j] = factor_spectral(ctx, full, *fo);
+        sjobs.push_back(std::make_unique<SpectralJob>());
+        spectral_prepare(ctx, full, *fo, *sjobs.back());
         if (j == d - 1 && (lo != 0 || hi != nd)) {  // slice the rows of X_d for this shard
           FactorHost sl;
           sl.n = hi - lo;
@@ -1538,8 +1618,15 @@ kg_status kg_design_create(kg_ctx* ctx, int64_t c, int64_t d, const int64_t* n, 
           fo = std::make_unique<FactorOwn>();
           upload_factor(sl, *fo, ctx->s);
         }
-        pr *= D->spectral[r][j];
         D->f[r].push_back(std::move(fo));
+      }
+    }
+    const std::vector<double> rad = spectral_run(ctx, sjobs);  // every factor in one launch
+    for (i64 r = 0; r < c; ++r) {
+      double pr = 1.0;
+      for (i64 j = 0; j < d; ++j) {
+        D->spectral[r][j] = rad[r * d + j];
+        pr *= D->spectral[r][j];
       }
       D->lipfac += pr;
     }
@@ -1669,6 +1756,7 @@ kg_status kg_fit_path(kg_ctx* ctx, const kg_design* design, const kg_obs* obs, i
                       int penalty, double alpha, const kg_path_cfg* cfg, const double* lambdas, int64_t n_lambdas,
                       kg_path_result** out) {
   *out = nullptr;
+  if (ctx) ctx->path_ms = -1.0;  // kg_path_kernel_stats describes this fit only
   return guarded(ctx, [&] {
     set_device(ctx);
     kg_path_cfg c;
@@ -1699,6 +1787,15 @@ kg_status kg_result_coef(kg_path_result* r, int64_t t, double* out) {
     set_device(r->ctx);
     if (t < 0 || t >= static_cast<int64_t>(r->lambdas.size())) throw Error(E_INVAL, "model index out of range");
     KG_CUDA(cudaMemcpy(out, r->coefs.d() + r->p * t, sizeof(double) * r->p, cudaMemcpyDeviceToHost));
+  });
+}
+kg_status kg_result_coefs(kg_path_result* r, int64_t first, int64_t count, double* out) {
+  return guarded(r->ctx, [&] {
+    set_device(r->ctx);
+    const int64_t m = static_cast<int64_t>(r->lambdas.size());
+    if (first < 0 || count < 0 || first + count > m) throw Error(E_INVAL, "model range out of range");
+    if (count)
+      KG_CUDA(cudaMemcpy(out, r->coefs.d() + r->p * first, sizeof(double) * r->p * count, cudaMemcpyDeviceToHost));
   });
 }
 void kg_result_free(kg_path_result* r) { delete r; }

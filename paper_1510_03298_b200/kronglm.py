@@ -49,6 +49,13 @@ class Context:
         self.h = h
         self.device = device
 
+    def coefs(self) -> np.ndarray:
+        """All models' coefficients, n_models x p, in one device-to-host copy."""
+        out = np.zeros((self.n_models, self.design.p))
+        if self.n_models:
+            self.design.ctx.check(_lib.load().kg_result_coefs(self.h, 0, self.n_models, _ptr(out)))
+        return out
+
     def close(self):
         if getattr(self, "h", None):
             _lib.load().kg_ctx_destroy(self.h)
@@ -120,6 +127,13 @@ class Design:
         self.ctx.check(_lib.load().kg_design_create(self.ctx.h, self.c, self.d, n_arr, p_arr, X, C.byref(h)))
         self.h = h
 
+    def coefs(self) -> np.ndarray:
+        """All models' coefficients, n_models x p, in one device-to-host copy."""
+        out = np.zeros((self.n_models, self.design.p))
+        if self.n_models:
+            self.design.ctx.check(_lib.load().kg_result_coefs(self.h, 0, self.n_models, _ptr(out)))
+        return out
+
     def close(self):
         if getattr(self, "h", None):
             _lib.load().kg_design_destroy(self.h)
@@ -185,6 +199,13 @@ class Observation:
                                            C.byref(h)))
         self.h = h
 
+    def coefs(self) -> np.ndarray:
+        """All models' coefficients, n_models x p, in one device-to-host copy."""
+        out = np.zeros((self.n_models, self.design.p))
+        if self.n_models:
+            self.design.ctx.check(_lib.load().kg_result_coefs(self.h, 0, self.n_models, _ptr(out)))
+        return out
+
     def close(self):
         if getattr(self, "h", None):
             _lib.load().kg_obs_destroy(self.h)
@@ -240,6 +261,13 @@ class PathResult:
     def coef(self, t) -> np.ndarray:
         out = np.zeros(self.design.p)
         self.design.ctx.check(_lib.load().kg_result_coef(self.h, t, _ptr(out)))
+        return out
+
+    def coefs(self) -> np.ndarray:
+        """All models' coefficients, n_models x p, in one device-to-host copy."""
+        out = np.zeros((self.n_models, self.design.p))
+        if self.n_models:
+            self.design.ctx.check(_lib.load().kg_result_coefs(self.h, 0, self.n_models, _ptr(out)))
         return out
 
     def close(self):
@@ -358,8 +386,7 @@ def fit_path(design, family, y, weights=None, penalty="lasso", alpha=0.0, n_lamb
            "truncated": res.truncated, "coefficients": [], "nonzero": [], "outer_iters": list(res.outer_iters),
            "converged": [s == "converged" for s in res.status], "inner_iters": list(res.inner_iters),
            "status": list(res.status)}
-    for t in range(res.n_models):
-        flat = res.coef(t)
+    for flat in res.coefs():
         out["coefficients"].append(D.blocks(flat))
         out["nonzero"].append(int(np.count_nonzero(flat)))
     return out

@@ -5,6 +5,8 @@ designs shaped like the BASELINE configs.
 Tolerances: operator maps 1e-12 (test_array.cpp:142-193); path parity per
 lambda: identical truncation/status, identical support, coefficients within
 1e-8 relative to max|theta|, objectives within 1e-8 relative (north_star)."""
+import os
+
 import numpy as np
 import pytest
 
@@ -296,3 +298,29 @@ def test_full_size_adjoint_property_c2():
     lhs = float(np.vdot(K.h_map(D, th), u))
     rhs = float(H.flat(th) @ H.flat(K.g_map(D, u)))
     assert abs(lhs - rhs) <= 1e-11 * max(1.0, abs(rhs))
+
+
+def test_c2_full_size_path_prefix_matches_oracle():
+    """BASELINE config C2 at full size through the resident whole-path kernel:
+    the bulk coefficient copy equals the per-model reads, and the first models
+    of the path match the oracle's warm-started outer_solve (same support,
+    coefficients and objective within 1e-8, same inner iteration counts)."""
+    d = configs.make("C2")
+    ctx = K.Context(0)
+    D = K.Design(d["design"], ctx)
+    obs = K.Observation(D, d["y"])
+    res = K.fit_path_resident(D, obs, "gaussian", n_lambda=d["n_lambda"], lambda_min_ratio=d["lambda_min_ratio"])
+    assert res.n_models == d["n_lambda"] and not res.truncated
+    allc = res.coefs()
+    for t in (0, 1, res.n_models // 2, res.n_models - 1):
+        assert np.array_equal(allc[t], res.coef(t))
+    O.set_threads(os.cpu_count() or 1)
+    init = None
+    for t in range(3):
+        r = O.outer_solve(d["design"], "gaussian", d["y"], res.lambdas[t], init=init)
+        init = r["coef"]
+        w, g = r["coef_flat"], allc[t]
+        assert np.array_equal(g != 0, w != 0), f"support differs at lambda {t}"
+        assert np.max(np.abs(g - w)) <= COEF_RTOL * max(np.max(np.abs(w)), 1e-300)
+        assert abs(res.objectives[t] - r["final_objective"]) <= OBJ_RTOL * abs(r["final_objective"])
+        assert res.inner_iters[t] == sum(int(x["inner_iterations"]) for x in r["iterations"])
