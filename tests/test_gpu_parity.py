@@ -309,7 +309,11 @@ def test_c2_full_size_path_prefix_matches_oracle():
     ctx = K.Context(0)
     D = K.Design(d["design"], ctx)
     obs = K.Observation(D, d["y"])
-    res = K.fit_path_resident(D, obs, "gaussian", n_lambda=d["n_lambda"], lambda_min_ratio=d["lambda_min_ratio"])
+    lmax = O.lambda_max(d["design"], "gaussian", d["y"])
+    assert abs(K.lambda_max(D, "gaussian", d["y"]) - lmax) <= 1e-13 * lmax
+    nl, ratio = d["n_lambda"], d["lambda_min_ratio"]
+    lams = [lmax * np.exp(np.log(ratio) / (nl - 1) * t) if t else lmax for t in range(nl)]
+    res = K.fit_path_resident(D, obs, "gaussian", lambdas=lams)  # the same inputs on both sides
     assert res.n_models == d["n_lambda"] and not res.truncated
     allc = res.coefs()
     for t in (0, 1, res.n_models // 2, res.n_models - 1):
