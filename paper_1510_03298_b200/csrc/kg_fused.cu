@@ -283,7 +283,8 @@ __global__ void __launch_bounds__(BS) k_fused_fast(FusedArgs f, FusedPlan pl, i6
   __shared__ double red[32];
   const int n1 = static_cast<int>(f.n1), p1 = static_cast<int>(f.p1), T = pl.T;
   const int nst = pl.nst;
-  constexpr bool hasP = VAR == FV_FISTA;
+  constexpr bool hasP = VAR == FV_FISTA || VAR == FV_FISTA_EXP;
+  constexpr bool hasB = VAR != FV_FISTA_EXP;
   if (threadIdx.x == 0) {
     for (int k = 0; k < nst; ++k) mbar_init(&bar[k], 1);
     asm volatile("fence.mbarrier_init.release.cluster;" ::: "memory");
@@ -297,12 +298,12 @@ __global__ void __launch_bounds__(BS) k_fused_fast(FusedArgs f, FusedPlan pl, i6
     unsigned bytes = 0;
     if (hasP) bytes += stage_manual(st + pl.offP, f.P + c0 * p1, p1 * Tc);
     bytes += stage_manual(st + pl.offA, srcA + c0 * n1, n1 * Tc);
-    bytes += stage_manual(st + pl.offB, srcB + c0 * n1, n1 * Tc);
+    if (hasB) bytes += stage_manual(st + pl.offB, srcB + c0 * n1, n1 * Tc);
     fence_proxy_async();
     mbar_expect_tx(&bar[s], bytes);
     if (hasP) stage_bulk(st + pl.offP, f.P + c0 * p1, p1 * Tc, &bar[s]);
     stage_bulk(st + pl.offA, srcA + c0 * n1, n1 * Tc, &bar[s]);
-    stage_bulk(st + pl.offB, srcB + c0 * n1, n1 * Tc, &bar[s]);
+    if (hasB) stage_bulk(st + pl.offB, srcB + c0 * n1, n1 * Tc, &bar[s]);
   };
   const int tid = static_cast<int>(threadIdx.x);
   // phase A: row i of X1, fibres cgA, cgA + CGA, ...
@@ -349,14 +350,14 @@ __global__ void __launch_bounds__(BS) k_fused_fast(FusedArgs f, FusedPlan pl, i6
     double* st = sm + static_cast<i64>(s) * pl.stage;
     const double* Ps = st + pl.offP + (hasP ? stage_shift(f.P + c0 * p1) : 0);
     double* As = st + pl.offA + stage_shift(srcA + c0 * n1);  // v (or y); overwritten in place by w
-    const double* Bs = st + pl.offB + stage_shift(srcB + c0 * n1);
+    const double* Bs = hasB ? st + pl.offB + stage_shift(srcB + c0 * n1) : nullptr;
     mbar_wait(&bar[s], (phase_bits >> s) & 1u);
     phase_bits ^= 1u << s;
     if (actA && f.dbg != 1) {
       auto cell = [&](int col) {
         const int e = iA + n1 * col;
         double w;
-        if (VAR == FV_FISTA) {
+        if (VAR == FV_FISTA || VAR == FV_FISTA_EXP) {
           const double* pc = Ps + p1 * col + loA;
           double e0 = 0.0, e1 = 0.0;
           if (lenA > 0) e0 = cA[0] * pc[0];
@@ -365,9 +366,13 @@ __global__ void __launch_bounds__(BS) k_fused_fast(FusedArgs f, FusedPlan pl, i6
           if (lenA > 3) e1 = fma(cA[3], pc[3], e1);
           const double eta = e0 + e1;
           const double vv = As[e];
-          const double r = eta - Bs[e];
-          acc = fma(vv, r * r, acc);
           w = vv * eta;
+          if (VAR == FV_FISTA) {
+            const double r = eta - Bs[e];
+            acc = fma(vv, r * r, acc);
+          } else {
+            acc = fma(w, eta, acc);
+          }
         } else if (VAR == FV_XTWZ) {
           w = As[e] * Bs[e];
         } else {
@@ -404,7 +409,7 @@ __global__ void __launch_bounds__(BS) k_fused_fast(FusedArgs f, FusedPlan pl, i6
     if (threadIdx.x == 0 && next < ntiles) issue(next, s);
     s = s + 1 == nst ? 0 : s + 1;
   }
-  if (VAR == FV_FISTA) {
+  if (VAR == FV_FISTA || VAR == FV_FISTA_EXP) {
     const double r = block_sum(acc, red);
     if (threadIdx.x == 0) f.partial[blockIdx.x] = r;
   }
@@ -412,7 +417,9 @@ __global__ void __launch_bounds__(BS) k_fused_fast(FusedArgs f, FusedPlan pl, i6
 
 static FusedPlan plan_for(const FusedArgs& f, int variant) {
   FusedPlan pl;
-  const i64 per_col = (variant == FV_FISTA ? f.p1 : 0) + 2 * f.n1;
+  const bool hasP = variant == FV_FISTA || variant == FV_FISTA_EXP;
+  const i64 nB = variant == FV_FISTA_EXP ? 1 : 2;  // staged n-arrays per fibre
+  const i64 per_col = (hasP ? f.p1 : 0) + nB * f.n1;
   static const i64 stage_kb = [] {
     const char* e = std::getenv("KG_FUSED_STAGE_KB");
     const long v = e ? std::atol(e) : 48;
@@ -430,10 +437,10 @@ static FusedPlan plan_for(const FusedArgs& f, int variant) {
   // 16-byte aligned sub-buffers, each with one spare double for the phase shift
   auto up2 = [](i64 x) { return (x + 2) & ~i64(1); };
   pl.offP = 0;
-  const i64 nP = variant == FV_FISTA ? up2(f.p1 * T) : 0;
+  const i64 nP = hasP ? up2(f.p1 * T) : 0;
   pl.offA = static_cast<int>(nP);
   pl.offB = static_cast<int>(nP + up2(f.n1 * T));
-  pl.stage = static_cast<int>(nP + 2 * up2(f.n1 * T));
+  pl.stage = static_cast<int>(nP + nB * up2(f.n1 * T));
   return pl;
 }
 
@@ -491,9 +498,14 @@ static void launch_fast(const Launch& L, int variant, int mg, const FusedArgs& f
                         int g, size_t sm) {
   switch (variant) {
     case FV_FISTA: launch_fast_var<FV_FISTA>(L, mg, f, pl, ntiles, g, sm); break;
+    case FV_FISTA_EXP: launch_fast_var<FV_FISTA_EXP>(L, mg, f, pl, ntiles, g, sm); break;
     case FV_XTWZ: launch_fast_var<FV_XTWZ>(L, mg, f, pl, ntiles, g, sm); break;
     default: launch_fast_var<FV_SCORE0>(L, mg, f, pl, ntiles, g, sm); break;
   }
+}
+
+bool fused_fast_ok(const FusedArgs& f, int variant) {
+  return fused_tma_fits(f, variant) && f.n1 <= NT && f.p1 <= NT && f.H.maxlen <= 4 && f.G.maxlen <= 64;
 }
 
 void fused_tma(const Launch& L, int variant, const FusedArgs& f) {
@@ -513,6 +525,7 @@ void fused_tma(const Launch& L, int variant, const FusedArgs& f) {
     const int mg = f.G.maxlen <= 8 ? 8 : f.G.maxlen <= 16 ? 16 : f.G.maxlen <= 24 ? 24 : f.G.maxlen <= 32 ? 32 : 64;
     launch_fast(L, variant, mg, f, pl, ntiles, g, sm);
   } else {
+    if (variant == FV_FISTA_EXP) throw Error(E_CUDA, "fused_tma: FV_FISTA_EXP needs the register-hoisted kernel");
     switch (variant) {
       case FV_FISTA: k_fused_tma<FV_FISTA><<<g, NT, sm, L.s>>>(f, pl, ntiles); break;
       case FV_XTWZ: k_fused_tma<FV_XTWZ><<<g, NT, sm, L.s>>>(f, pl, ntiles); break;

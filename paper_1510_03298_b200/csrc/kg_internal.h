@@ -112,7 +112,11 @@ inline void launched(const Launch& L) {
 void contract(const Launch& L, const double* A, double* out, i64 a, i64 K, i64 M, i64 b, const BandOp& op,
               bool accumulate);
 
-enum FusedVariant { FV_FISTA = 0, FV_XTWZ = 1, FV_SCORE0 = 2 };
+// FV_FISTA: partials of sum v (eta - z)^2 (the reference's inner_quadratic);
+// FV_FISTA_EXP: partials of sum v eta^2 only (z is not read), for the expanded
+// objective sum v (eta - z)^2 = sum v eta^2 - 2 <b, x> + sum v z^2 with
+// b = X^T (v .* z) (the Gram route's identity, applied on the n-space route).
+enum FusedVariant { FV_FISTA = 0, FV_XTWZ = 1, FV_SCORE0 = 2, FV_FISTA_EXP = 3 };
 struct FusedArgs {
   i64 n1 = 0, p1 = 0, m = 0;  // mode-1 extents and the number of mode-1 fibres (n / n1)
   int T = 1;                   // fibres per CTA
@@ -138,8 +142,27 @@ void fused_mode1(const Launch& L, int variant, const FusedArgs& f);
 bool fused_tma_fits(const FusedArgs& f, int variant);
 int fused_tma_grid(const FusedArgs& f, int variant);
 void fused_tma(const Launch& L, int variant, const FusedArgs& f);
+// the register-hoisted kernel applies (required for FV_FISTA_EXP)
+bool fused_fast_ok(const FusedArgs& f, int variant);
 void contract_tiled(const Launch& L, const double* A, double* out, i64 a, i64 K, i64 M, i64 b, const BandOp& op,
                     bool accumulate);
+
+// Modes 1 and 2 of one prox-grad step fused per last-mode slab (kg_slab.cu):
+// B1[:, :, k3] = X1^T V X1-and-X2 contractions of A1[:, :, k3] (d = 3),
+// partial[cta] = sum v eta^2 of the CTA's cells (expanded objective).
+struct SlabArgs {
+  int n1 = 0, n2 = 0, p1 = 0, p2 = 0;
+  i64 n3 = 0;                   // slabs (local extent of the last mode)
+  BandOp H1, G1, H2, G2;        // X1 rows, X1^T rows, X2 rows, X2^T rows
+  const double* A1 = nullptr;   // p1 x p2 x n3
+  double* B1 = nullptr;         // p1 x p2 x n3 (out)
+  const double* v = nullptr;    // n1 x n2 x n3
+  double* partial = nullptr;    // one per CTA
+  int CG = 0;                   // column groups of 32 per tile (set by the launcher)
+};
+bool slab_ok(const SlabArgs& a);
+int slab_grid(const SlabArgs& a);
+void slab12(const Launch& L, const SlabArgs& a);
 
 // H-last (+ reductions) over mode 1.  If P is null, eta_new is an input
 // (already computed by a full H chain) and only the reductions run.
@@ -197,8 +220,11 @@ void fill(const Launch& L, i64 n, double v, double* x);
 
 // p-space
 int pgrid(i64 p);
+// bxpart (nullable): per-CTA partials of <b, x_new> for the expanded objective
 void fista_update(const Launch& L, const FistaCtl* ctl, i64 p, int pen, double alpha, double* x, double* xp,
-                  double* Sx, double* Sxp, const double* b, double* best, double* Sbest, double* Jpart);
+                  double* Sx, double* Sxp, const double* b, double* best, double* Sbest, double* Jpart,
+                  double* bxpart = nullptr);
+void pdot(const Launch& L, i64 p, const double* a, const double* b, double* part);
 void pnorm(const Launch& L, i64 p, int pen, double alpha, const double* x, double* Jpart);
 // cols: 0 = J(th_t); 1 + j = J(th + t_j (th_t - th))
 void ptrials(const Launch& L, i64 p, int pen, double alpha, const double* th, const double* th_t, int ntrial,
@@ -268,10 +294,11 @@ int gauss_dots(const Launch& L, i64 p, double w, const double* th, const double*
                const double* Sbt, const double* b, double* part);
 
 // control / reductions (single CTA)
+// bx_part (nullable): objective partials sum = ss - 2 <b, x> (+ ss_const), the expanded form
 void fista_init(const Launch& L, FistaCtl* ctl, const double* ss_part, int n_ss, const double* J_part, int n_J,
-                const double* vmax_part, int n_vmax, int bt_always);
+                const double* vmax_part, int n_vmax, int bt_always, const double* bx_part = nullptr, int n_bx = 0);
 void fista_control(const Launch& L, FistaCtl* ctl, const double* ss_part, int n_ss, const double* J_part, int n_J,
-                   cudaGraphConditionalHandle h, int use_handle);
+                   cudaGraphConditionalHandle h, int use_handle, const double* bx_part = nullptr, int n_bx = 0);
 void fista_gate(const Launch& L, const FistaCtl* ctl, cudaGraphConditionalHandle h);
 // out[c] = sum over rows of part[row * ncols + c] (fixed order); op 0 sum, 1 max
 void reduce_cols(const Launch& L, const double* part, int nrows, int ncols, int op, double* out);

@@ -597,12 +597,13 @@ __device__ __forceinline__ void jacc(double x, double& l1, double& l2) {
 // map), so each iteration needs one n-array pass on the new iterate only.
 __global__ void __launch_bounds__(NT) k_fista_update(const FistaCtl* __restrict__ ctl, i64 p, int pen, double alpha,
                                                      double* x, double* xp, double* Sx, double* Sxp, const double* b,
-                                                     double* best, double* Sbest, double* Jpart) {
+                                                     double* best, double* Sbest, double* Jpart,
+                                                     double* bxpart) {
   __shared__ double red[32];
   const double omega = ctl->omega, delta = ctl->delta, lambda = ctl->lambda, n = ctl->n, sscale = ctl->sscale;
   const int copy_best = ctl->copy_best, restart = ctl->restart;
   const double gamma = delta * lambda;
-  double l1 = 0.0, l2 = 0.0;
+  double l1 = 0.0, l2 = 0.0, bx = 0.0;
   for (i64 i = static_cast<i64>(blockIdx.x) * NT + threadIdx.x; i < p; i += static_cast<i64>(gridDim.x) * NT) {
     double xi = x[i], xpi = xp[i], sxi = Sx[i], sxpi = Sxp[i];
     if (copy_best) {
@@ -622,6 +623,7 @@ __global__ void __launch_bounds__(NT) k_fista_update(const FistaCtl* __restrict_
     x[i] = ci;
     Sxp[i] = sxi;
     jacc(ci, l1, l2);
+    if (bxpart) bx = fma(b[i], ci, bx);
   }
   const double s1 = block_reduce<false>(l1, red);
   const double s2 = block_reduce<false>(l2, red);
@@ -629,11 +631,31 @@ __global__ void __launch_bounds__(NT) k_fista_update(const FistaCtl* __restrict_
     Jpart[2 * blockIdx.x] = s1;
     Jpart[2 * blockIdx.x + 1] = s2;
   }
+  if (bxpart) {
+    const double s3 = block_reduce<false>(bx, red);
+    if (threadIdx.x == 0) bxpart[blockIdx.x] = s3;
+  }
 }
 
 void fista_update(const Launch& L, const FistaCtl* ctl, i64 p, int pen, double alpha, double* x, double* xp,
-                  double* Sx, double* Sxp, const double* b, double* best, double* Sbest, double* Jpart) {
-  k_fista_update<<<pgrid(p), NT, 0, L.s>>>(ctl, p, pen, alpha, x, xp, Sx, Sxp, b, best, Sbest, Jpart);
+                  double* Sx, double* Sxp, const double* b, double* best, double* Sbest, double* Jpart,
+                  double* bxpart) {
+  k_fista_update<<<pgrid(p), NT, 0, L.s>>>(ctl, p, pen, alpha, x, xp, Sx, Sxp, b, best, Sbest, Jpart, bxpart);
+  bump(L);
+}
+
+// per-CTA partials of <a, b> (p-space)
+__global__ void __launch_bounds__(NT) k_pdot(i64 p, const double* a, const double* b, double* part) {
+  __shared__ double red[32];
+  double s = 0.0;
+  for (i64 i = static_cast<i64>(blockIdx.x) * NT + threadIdx.x; i < p; i += static_cast<i64>(gridDim.x) * NT)
+    s = fma(a[i], b[i], s);
+  const double r = block_reduce<false>(s, red);
+  if (threadIdx.x == 0) part[blockIdx.x] = r;
+}
+
+void pdot(const Launch& L, i64 p, const double* a, const double* b, double* part) {
+  k_pdot<<<pgrid(p), NT, 0, L.s>>>(p, a, b, part);
   bump(L);
 }
 
@@ -834,9 +856,11 @@ __device__ __forceinline__ double penalty_of(int pen, double alpha, double l1, d
 }
 
 __global__ void __launch_bounds__(CT) k_fista_init(FistaCtl* c, const double* ss_part, int n_ss, const double* J_part,
-                                                   int n_J, const double* vmax_part, int n_vmax, int bt_always) {
+                                                   int n_J, const double* vmax_part, int n_vmax, int bt_always,
+                                                   const double* bx_part, int n_bx) {
   __shared__ double sh[33];
-  const double ss = cta_sum_col(ss_part, n_ss, 1, 0, sh);
+  double ss = cta_sum_col(ss_part, n_ss, 1, 0, sh);
+  if (bx_part) ss += -2.0 * cta_sum_col(bx_part, n_bx, 1, 0, sh);  // expanded objective (FV_FISTA_EXP)
   const double l1 = cta_sum_col(J_part, n_J, 2, 0, sh);
   const double l2 = cta_sum_col(J_part, n_J, 2, 1, sh);
   const double wmax = cta_max_col(vmax_part, n_vmax, 1, 0, sh);
@@ -872,9 +896,11 @@ __global__ void __launch_bounds__(CT) k_fista_init(FistaCtl* c, const double* ss
 // sets the graph's while-condition so the loop runs without the host.
 __global__ void __launch_bounds__(CT) k_fista_control(FistaCtl* c, const double* ss_part, int n_ss,
                                                       const double* J_part, int n_J,
-                                                      cudaGraphConditionalHandle h, int use_handle) {
+                                                      cudaGraphConditionalHandle h, int use_handle,
+                                                      const double* bx_part, int n_bx) {
   __shared__ double sh[33];
-  const double ss = cta_sum_col(ss_part, n_ss, 1, 0, sh);
+  double ss = cta_sum_col(ss_part, n_ss, 1, 0, sh);
+  if (bx_part) ss += -2.0 * cta_sum_col(bx_part, n_bx, 1, 0, sh);  // expanded objective (FV_FISTA_EXP)
   const double l1 = cta_sum_col(J_part, n_J, 2, 0, sh);
   const double l2 = cta_sum_col(J_part, n_J, 2, 1, sh);
   if (threadIdx.x != 0) return;
@@ -927,14 +953,14 @@ __global__ void __launch_bounds__(CT) k_fista_control(FistaCtl* c, const double*
 }
 
 void fista_init(const Launch& L, FistaCtl* ctl, const double* ss_part, int n_ss, const double* J_part, int n_J,
-                const double* vmax_part, int n_vmax, int bt_always) {
-  k_fista_init<<<1, CT, 0, L.s>>>(ctl, ss_part, n_ss, J_part, n_J, vmax_part, n_vmax, bt_always);
+                const double* vmax_part, int n_vmax, int bt_always, const double* bx_part, int n_bx) {
+  k_fista_init<<<1, CT, 0, L.s>>>(ctl, ss_part, n_ss, J_part, n_J, vmax_part, n_vmax, bt_always, bx_part, n_bx);
   bump(L);
 }
 
 void fista_control(const Launch& L, FistaCtl* ctl, const double* ss_part, int n_ss, const double* J_part, int n_J,
-                   cudaGraphConditionalHandle h, int use_handle) {
-  k_fista_control<<<1, CT, 0, L.s>>>(ctl, ss_part, n_ss, J_part, n_J, h, use_handle);
+                   cudaGraphConditionalHandle h, int use_handle, const double* bx_part, int n_bx) {
+  k_fista_control<<<1, CT, 0, L.s>>>(ctl, ss_part, n_ss, J_part, n_J, h, use_handle, bx_part, n_bx);
   bump(L);
 }
 

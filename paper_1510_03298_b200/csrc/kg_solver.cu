@@ -414,6 +414,13 @@ struct Fit {
   // 1 = Gram route (constant weights W = wconst I: X^T W X = wconst (x)_j X_j^T X_j,
   // the reference's xtwx_apply_tensor with constant weight factors)
   int route = 0;
+  // route 0 on the fused design: objective sum v eta^2 - 2 <b, x> + sum v z^2
+  // (FV_FISTA_EXP, z is not read per iteration); KG_ROUTE0_DIRECT=1 keeps sum v (eta - z)^2
+  bool expand = false;
+  // d = 3, banded: modes 1 and 2 fused per last-mode slab (kg_slab.cu); opt-in with KG_SLAB=1
+  // (experimental: parity-tested, slower than the fused-pass route so far)
+  bool slab = false;
+  DBuf bxpart;
   double wconst = 1.0;     // the constant weight (route 1)
   bool c0_valid = false;   // F.scal[48] holds sum v z^2 for the current (v, z)
   // route 1 with one component: one fused kernel per iteration (kg_gram.cu)
@@ -432,6 +439,23 @@ struct Fit {
     }
   }
 };
+
+static FusedArgs fused_args(const Fit& F);
+
+static SlabArgs slab_args(const Fit& F) {
+  const kg_design& D = *F.D;
+  SlabArgs a;
+  a.n1 = static_cast<int>(D.n[0]);
+  a.n2 = static_cast<int>(D.n[1]);
+  a.p1 = static_cast<int>(D.p[0][0]);
+  a.p2 = static_cast<int>(D.p[0][1]);
+  a.n3 = D.n[2];
+  a.H1 = D.f[0][0]->dev.H;
+  a.G1 = D.f[0][0]->dev.G;
+  a.H2 = D.f[0][1]->dev.H;
+  a.G2 = D.f[0][1]->dev.G;
+  return a;
+}
 
 static void alloc_fit(Fit& F) {
   const kg_design& D = *F.D;
@@ -455,6 +479,17 @@ static void alloc_fit(Fit& F) {
   F.s1.alloc(sizeof(double) * D.scratch);
   F.part.alloc(sizeof(double) * D.part_cap);
   F.Jpart.alloc(sizeof(double) * 2 * pgrid(F.p));
+  F.bxpart.alloc(sizeof(double) * pgrid(F.p));
+  F.expand = false;
+  F.slab = false;
+  if (D.fused && std::getenv("KG_ROUTE0_DIRECT") == nullptr) {
+    FusedArgs a = fused_args(F);
+    F.expand = fused_fast_ok(a, FV_FISTA_EXP);
+    if (D.d == 3 && std::getenv("KG_SLAB") != nullptr && std::getenv("KG_SLAB")[0] == '1') {  // experimental
+      F.slab = slab_ok(slab_args(F));
+      if (F.slab) F.expand = true;
+    }
+  }
   F.tpart.alloc(sizeof(double) * 2 * (1 + kMaxTrials) * pgrid(F.p));
   F.scal.alloc(sizeof(double) * 64);
   F.errs.alloc(sizeof(i64) * 16);
@@ -527,6 +562,18 @@ static int run_fused(kg_ctx* ctx, int variant, const FusedArgs& a) {
 static int xwx_pass(Fit& F, const double* x, double* Sx) {
   const kg_design& D = *F.D;
   kg_ctx* ctx = F.ctx;
+  if (F.slab) {  // A1 = x x_3 X3 -> slab kernel (modes 1, 2, v) -> S x = B1 x_3 X3^T
+    const i64 pp = D.p[0][0] * D.p[0][1], p3 = D.p[0][2], n3 = D.n[2];
+    contract(ctx->L(), x, F.P.d(), pp, p3, n3, 1, D.f[0][2]->dev.H, false);
+    SlabArgs a = slab_args(F);
+    a.A1 = F.P.d();
+    a.B1 = F.Q.d();
+    a.v = F.v.d();
+    a.partial = F.part.d();
+    slab12(ctx->L(), a);
+    contract(ctx->L(), F.Q.d(), Sx, pp, n3, p3, 1, D.f[0][2]->dev.G, false);
+    return slab_grid(a);
+  }
   if (D.fused) {
     const double* P = x;
     if (D.d > 1) {
@@ -539,7 +586,7 @@ static int xwx_pass(Fit& F, const double* x, double* Sx) {
     a.v = F.v.d();
     a.z = F.zptr;
     a.partial = F.part.d();
-    const int np = run_fused(ctx, FV_FISTA, a);
+    const int np = run_fused(ctx, F.expand ? FV_FISTA_EXP : FV_FISTA, a);
     if (D.d > 1) {
       std::vector<i64> dims = D.n;
       dims[0] = D.p[0][0];
@@ -660,10 +707,12 @@ static void enqueue_body(Fit& F, cudaGraphConditionalHandle h, int use_handle) {
     return;
   }
   FistaCtl* c = static_cast<FistaCtl*>(F.ctl.p);
+  const bool ex = F.route == 0 && F.expand;
   fista_update(ctx->L(), c, F.p, F.pen, F.alpha, F.x.d(), F.xp.d(), F.Sx.d(), F.Sxp.d(), F.b.d(), F.best.d(),
-               F.Sbest.d(), F.Jpart.d());
+               F.Sbest.d(), F.Jpart.d(), ex ? F.bxpart.d() : nullptr);
   F.n_ss = step_pass(F, F.x.d(), F.Sx.d());
-  fista_control(ctx->L(), c, F.part.d(), F.n_ss, F.Jpart.d(), pgrid(F.p), h, use_handle);
+  fista_control(ctx->L(), c, F.part.d(), F.n_ss, F.Jpart.d(), pgrid(F.p), h, use_handle,
+                ex ? F.bxpart.d() : nullptr, pgrid(F.p));
 }
 
 // KG_HOST_LOOP=1: drive the FISTA loop from the host (one sync per
@@ -768,7 +817,7 @@ static void fista_enqueue(Fit& F, double lambda, const InnerCfg& ic, const doubl
   KG_CUDA(cudaStreamSynchronize(ctx->s));  // the pinned staging slot is reused
   *staged = h;
   KG_CUDA(cudaMemcpyAsync(F.ctl.p, staged, sizeof(FistaCtl), cudaMemcpyHostToDevice, ctx->s));
-  if (F.route == 1) {  // sum v z^2, once per (v, z)
+  if (F.route == 1 || F.expand) {  // sum v z^2, once per (v, z)
     if (!F.c0_valid) {
       wzz(ctx->L(), F.n, F.v.d(), F.zptr, F.part.d());
       reduce_cols(ctx->L(), F.part.d(), elem_grid(F.n), 1, 0, F.scal.d() + 48);
@@ -804,8 +853,10 @@ static void fista_enqueue(Fit& F, double lambda, const InnerCfg& ic, const doubl
     const int n_ss = step_pass(F, F.x.d(), F.Sx.d());
     pnorm(ctx->L(), F.p, F.pen, F.alpha, F.x.d(), F.Jpart.d());
     pcopy(ctx->L(), F.p, F.Sx.d(), F.Sxp.d(), F.Sbest.d(), nullptr);
+    const bool ex = F.route == 0 && F.expand;
+    if (ex) pdot(ctx->L(), F.p, F.b.d(), F.x.d(), F.bxpart.d());
     fista_init(ctx->L(), static_cast<FistaCtl*>(F.ctl.p), F.part.d(), n_ss, F.Jpart.d(), pgrid(F.p), vmax_part,
-               n_vmax, 0);
+               n_vmax, 0, ex ? F.bxpart.d() : nullptr, pgrid(F.p));
   }
   if (ic.max_iters >= 1) {
     if (host_loop_mode()) {
@@ -1989,9 +2040,19 @@ kg_status kg_time_kernel(kg_ctx* ctx, const kg_design* D, const kg_obs* O, int w
       a.z = F.zptr;
       a.partial = F.part.d();
       a.dbg = which == 3 ? 1 : (which == 4 ? 2 : 0);  // 3: copies only, 4: copies + phase A
-      launch = [&, a] { run_fused(ctx, FV_FISTA, a); };
-      // P (p1 x m) read, v and z read, Q (p1 x m) written
-      b = 8.0 * (2.0 * static_cast<double>(F.n) + 2.0 * static_cast<double>(a.p1 * a.m));
+      const int var = F.expand ? FV_FISTA_EXP : FV_FISTA;  // the variant the fits run
+      launch = [&, a, var] { run_fused(ctx, var, a); };
+      // P (p1 x m) read, v (and z unless expanded) read, Q (p1 x m) written
+      b = 8.0 * ((F.expand ? 1.0 : 2.0) * static_cast<double>(F.n) + 2.0 * static_cast<double>(a.p1 * a.m));
+      if (F.slab && which == 0) {  // the slab kernel: v read, A1 read, B1 written
+        SlabArgs sa = slab_args(F);
+        sa.A1 = F.P.d();
+        sa.B1 = F.Q.d();
+        sa.v = F.v.d();
+        sa.partial = F.part.d();
+        launch = [&, sa] { slab12(ctx->L(), sa); };
+        b = 8.0 * (static_cast<double>(F.n) + 2.0 * static_cast<double>(sa.p1) * sa.p2 * static_cast<double>(sa.n3));
+      }
     } else {
       // largest H-chain step of component 0 (modes d-1 .. 0 applied to theta)
       std::vector<i64> dims = D->p[0];

@@ -328,3 +328,43 @@ def test_c2_full_size_path_prefix_matches_oracle():
         assert np.max(np.abs(g - w)) <= COEF_RTOL * max(np.max(np.abs(w)), 1e-300)
         assert abs(res.objectives[t] - r["final_objective"]) <= OBJ_RTOL * abs(r["final_objective"])
         assert res.inner_iters[t] == sum(int(x["inner_iterations"]) for x in r["iterations"])
+
+
+def _fused_pass_bytes(D, obs):
+    import ctypes as C
+    from paper_1510_03298_b200 import _lib
+    ms, b = C.c_double(), C.c_double()
+    D.ctx.check(_lib.load().kg_time_kernel(D.ctx.h, D.h, obs.h, 0, 2, C.byref(ms), C.byref(b)))
+    return b.value
+
+
+def test_slab_route_matches_oracle(monkeypatch):
+    """d = 3 n-space route through the slab kernel (modes 1 and 2 fused per
+    last-mode slab, expanded objective): Poisson path and a non-constant-weight
+    Gaussian path against the oracle, and against the unfused kernels."""
+    rng = np.random.default_rng(91)
+    n, p = (64, 24, 20), (20, 8, 6)
+    design = bspline_design(n, p)
+    B = np.zeros(p)
+    m = rng.random(p) < 0.15
+    B[m] = rng.standard_normal(m.sum())
+    eta = configs.tensor_h(design[0], B)
+    y = rng.poisson(np.exp(np.log(30.0) / eta.max() * eta)).astype(float)
+    monkeypatch.setenv("KG_SLAB", "1")  # opt-in route
+    D = K.Design(design)
+    obs = K.Observation(D, y)
+    N = int(np.prod(n))
+    assert _fused_pass_bytes(D, obs) == 8.0 * (N + 2 * p[0] * p[1] * n[2])  # the slab kernel is in use
+    kw = dict(n_lambda=10, lambda_min_ratio=1e-3)
+    got = K.fit_path(design, "poisson", y, **kw)
+    compare_paths(got, O.fit_path(design, "poisson", y, **kw))
+    monkeypatch.delenv("KG_SLAB")
+    ref = K.fit_path(design, "poisson", y, **kw)  # default route
+    monkeypatch.setenv("KG_SLAB", "1")
+    compare_paths(got, ref)
+    # Gaussian, weights not all equal: the n-space route with v = a
+    yg = eta + rng.normal(0, 0.3, n)
+    w = np.asfortranarray(rng.uniform(0.5, 2.0, n))
+    kw = dict(n_lambda=8, lambda_min_ratio=1e-3)
+    compare_paths(K.fit_path(design, "gaussian", yg, weights=w, **kw),
+                  O.fit_path(design, "gaussian", yg, weights=w, **kw))
