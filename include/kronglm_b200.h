@@ -84,20 +84,29 @@ void kg_path_cfg_default(kg_path_cfg* cfg);
 /* One CUDA device, one stream.  Replaces nothing in the reference (which is
  * single-threaded host code); it owns streams, graphs and workspaces. */
 kg_status kg_ctx_create(int device, kg_ctx** out);
-/* Sharded context: the observation array is split along its LAST mode into
- * `world` contiguous slabs; this rank owns slab `rank`.  `nccl_unique_id`
- * points to the 128-byte ncclUniqueId created by rank 0 (kg_nccl_unique_id)
- * and broadcast by the caller (e.g. torch.distributed).  Per gradient the
- * ranks all-reduce a p-vector (+ scalars) over NVLink. */
+/* Sharded context: the observation array is split along its
+ * LAST mode into `world` contiguous slabs, rows [n_d r / world, n_d (r+1) /
+ * world) for rank r; designs created on it keep only those rows of X_d and
+ * observations are the rank's slab.  `nccl_unique_id` points to the 128-byte
+ * ncclUniqueId made by rank 0 (kg_nccl_unique_id) and broadcast by the caller
+ * (e.g. torch.distributed); the ranks then sum S(x) (a p-vector) and the
+ * objective partial per gradient, b = X^T(v z) and the family scalars per
+ * outer iteration, and max / min-reduce max(v) and error cells, all with
+ * ncclAllReduce on the context stream.  With nccl_unique_id == NULL the
+ * context computes its slab's local partials only (no cross-rank sums: the
+ * caller reduces, e.g. kg_g_map partials); a fit on it is a fit of the slab.
+ * Replaces nothing in the reference (single-process); libnccl.so.2 is
+ * opened at run time.  KG_ENCCL if NCCL is unavailable or fails. */
 kg_status kg_ctx_create_sharded(int device, int rank, int world, const void* nccl_unique_id, kg_ctx** out);
 kg_status kg_nccl_unique_id(void* out128);
+/* Destroy designs, observations and results made on a context before it. */
 void kg_ctx_destroy(kg_ctx* ctx);
 const char* kg_last_error(const kg_ctx* ctx);
 int64_t kg_last_error_cell(const kg_ctx* ctx);
 /* The cudaStream_t the context launches on (for CUDA-event timing). */
 void* kg_ctx_stream(kg_ctx* ctx);
 kg_status kg_ctx_synchronize(kg_ctx* ctx);
-/* Which shard of the last mode this context owns: [*lo, *hi). */
+/* The shard this context owns: slab `rank` of `world` along the last mode. */
 void kg_ctx_shard(const kg_ctx* ctx, int* rank, int* world);
 
 /* -------------------------------------------------------------- design -- */

@@ -26,6 +26,8 @@
 #include <string>
 #include <vector>
 
+#include <nccl.h>
+
 #include "../../include/kronglm_b200.h"
 #include "kg_internal.h"
 
@@ -87,6 +89,47 @@ static i64 prod(const std::vector<i64>& v, size_t a, size_t b) {
 
 }  // namespace kg
 
+// ------------------------------------------------------------------- NCCL
+// libnccl is opened at run time (the same soname torch loads), so the library
+// has no link-time NCCL dependency and single-GPU use never touches it.
+namespace kg {
+struct NcclApi {
+  void* h = nullptr;
+  ncclResult_t (*GetUniqueId)(ncclUniqueId*) = nullptr;
+  ncclResult_t (*CommInitRank)(ncclComm_t*, int, ncclUniqueId, int) = nullptr;
+  ncclResult_t (*AllReduce)(const void*, void*, size_t, ncclDataType_t, ncclRedOp_t, ncclComm_t,
+                            cudaStream_t) = nullptr;
+  ncclResult_t (*CommDestroy)(ncclComm_t) = nullptr;
+  const char* (*GetErrorString)(ncclResult_t) = nullptr;
+};
+
+static NcclApi* nccl_api() {
+  static NcclApi api;
+  static bool tried = false;
+  static std::mutex mu;
+  std::lock_guard<std::mutex> lk(mu);
+  if (!tried) {
+    tried = true;
+    void* h = dlopen("libnccl.so.2", RTLD_NOW | RTLD_GLOBAL);
+    if (!h) h = dlopen("libnccl.so", RTLD_NOW | RTLD_GLOBAL);
+    if (h) {
+      api.GetUniqueId = reinterpret_cast<decltype(api.GetUniqueId)>(dlsym(h, "ncclGetUniqueId"));
+      api.CommInitRank = reinterpret_cast<decltype(api.CommInitRank)>(dlsym(h, "ncclCommInitRank"));
+      api.AllReduce = reinterpret_cast<decltype(api.AllReduce)>(dlsym(h, "ncclAllReduce"));
+      api.CommDestroy = reinterpret_cast<decltype(api.CommDestroy)>(dlsym(h, "ncclCommDestroy"));
+      api.GetErrorString = reinterpret_cast<decltype(api.GetErrorString)>(dlsym(h, "ncclGetErrorString"));
+      if (api.GetUniqueId && api.CommInitRank && api.AllReduce && api.CommDestroy && api.GetErrorString) api.h = h;
+    }
+  }
+  if (!api.h) throw Error(E_NCCL, "libnccl.so.2 could not be loaded");
+  return &api;
+}
+
+static void nccl_check(ncclResult_t r, const char* what) {
+  if (r != ncclSuccess) throw Error(E_NCCL, std::string(what) + ": " + nccl_api()->GetErrorString(r));
+}
+}  // namespace kg
+
 // ------------------------------------------------------------------ context
 struct kg_ctx {
   int device = 0;
@@ -95,6 +138,7 @@ struct kg_ctx {
   std::string err;
   kg::i64 err_cell = -1;
   int rank = 0, world = 1;
+  ncclComm_t comm = nullptr;  // sharded context (kg_ctx_create_sharded): sums over the last-mode slabs
   void* pinned = nullptr;  // small pinned staging area for scalars
   // last whole-path kernel: event-timed device ms, algorithmic bytes, FISTA steps
   double path_ms = -1.0, path_bytes = 0.0;
@@ -103,6 +147,21 @@ struct kg_ctx {
   kg::Launch L() { return {s, &launches}; }
   double* pin() { return static_cast<double*>(pinned); }
 };
+
+// Cross-rank reductions of a sharded context (no-ops on a single GPU): the
+// n-space partials of every rank's slab are summed (or max-/min-reduced) in
+// place on the context stream, so the replicated p-space state stays equal
+// on all ranks.
+namespace kg {
+static void ar(kg_ctx* ctx, void* d, size_t n, ncclDataType_t t, ncclRedOp_t op) {
+  if (!ctx->comm || n == 0) return;
+  nccl_check(nccl_api()->AllReduce(d, d, n, t, op, ctx->comm, ctx->s), "ncclAllReduce");
+}
+static void ar_sum(kg_ctx* ctx, double* d, size_t n) { ar(ctx, d, n, ncclFloat64, ncclSum); }
+static void ar_max(kg_ctx* ctx, double* d, size_t n) { ar(ctx, d, n, ncclFloat64, ncclMax); }
+static void ar_min_i64(kg_ctx* ctx, int64_t* d, size_t n) { ar(ctx, d, n, ncclInt64, ncclMin); }
+static bool sharded(const kg_ctx* ctx) { return ctx->comm != nullptr; }
+}  // namespace kg
 
 // Layout of the 4 KB pinned staging area (doubles).
 namespace kg {
@@ -559,7 +618,7 @@ static int run_fused(kg_ctx* ctx, int variant, const FusedArgs& a) {
 
 // S(x) = X^T diag(v) X x into Sx, and per-CTA partials of sum v (eta - z)^2
 // into F.part (returns the number of partials).
-static int xwx_pass(Fit& F, const double* x, double* Sx) {
+static int xwx_pass_local(Fit& F, const double* x, double* Sx) {
   const kg_design& D = *F.D;
   kg_ctx* ctx = F.ctx;
   if (F.slab) {  // A1 = x x_3 X3 -> slab kernel (modes 1, 2, v) -> S x = B1 x_3 X3^T
@@ -618,6 +677,19 @@ static int gram_pass(Fit& F, const double* x, double* Sx) {
   return pgrid(F.p);
 }
 
+// n-space pass; on a sharded context S(x) and the objective partial are
+// summed over the slabs (one p-sized all-reduce + one scalar per gradient)
+static int xwx_pass(Fit& F, const double* x, double* Sx) {
+  const int np = xwx_pass_local(F, x, Sx);
+  kg_ctx* ctx = F.ctx;
+  if (!sharded(ctx)) return np;
+  ar_sum(ctx, Sx, static_cast<size_t>(F.p));
+  reduce_cols(ctx->L(), F.part.d(), np, 1, 0, F.scal.d() + 40);
+  ar_sum(ctx, F.scal.d() + 40, 1);
+  KG_CUDA(cudaMemcpyAsync(F.part.d(), F.scal.d() + 40, sizeof(double), cudaMemcpyDeviceToDevice, ctx->s));
+  return 1;
+}
+
 static int step_pass(Fit& F, const double* x, double* Sx) {
   return F.route == 1 ? gram_pass(F, x, Sx) : xwx_pass(F, x, Sx);
 }
@@ -637,11 +709,12 @@ static void xtwz_pass(Fit& F) {
       dims[0] = D.p[0][0];
       run_chain(ctx, dims, g_steps(D, 0, 1), F.Q.d(), F.b.d(), F.s0.d(), F.s1.d(), false);
     }
-    return;
+  } else {
+    vz(ctx->L(), F.n, F.v.d(), F.zptr, F.w.d());
+    for (i64 r = 0; r < D.c; ++r)
+      run_chain(ctx, D.n, g_steps(D, r, 0), F.w.d(), F.b.d() + D.offs[r], F.s0.d(), F.s1.d(), false);
   }
-  vz(ctx->L(), F.n, F.v.d(), F.zptr, F.w.d());
-  for (i64 r = 0; r < D.c; ++r)
-    run_chain(ctx, D.n, g_steps(D, r, 0), F.w.d(), F.b.d() + D.offs[r], F.s0.d(), F.s1.d(), false);
+  ar_sum(ctx, F.b.d(), static_cast<size_t>(F.p));  // b = sum over slabs of X_g^T (v z)_g
 }
 
 // eta_out = H(coef) with optional reductions (HlastArgs flags) -> F.part (kHlastCols per CTA).
@@ -796,6 +869,12 @@ struct InnerCfg {
 // The result lands in F.best; the control block is copied to ctx->pin() + PIN_CTL.
 static void fista_enqueue(Fit& F, double lambda, const InnerCfg& ic, const double* vmax_part, int n_vmax) {
   kg_ctx* ctx = F.ctx;
+  if (sharded(ctx)) {  // max(v) over all slabs (lipschitz_upper)
+    reduce_cols(ctx->L(), vmax_part, n_vmax, 1, 1, F.scal.d() + 56);
+    ar_max(ctx, F.scal.d() + 56, 1);
+    vmax_part = F.scal.d() + 56;
+    n_vmax = 1;
+  }
   if (!(ic.nu >= 0.0 && ic.nu <= 1.0)) throw Error(E_INVAL, "fista_solve: nu must lie in [0,1]");
   if (ic.nu == 0.0)
     throw Error(E_INVAL, "fista_solve: nu = 0 (backtracking every iteration) is not supported by the device solver");
@@ -821,6 +900,7 @@ static void fista_enqueue(Fit& F, double lambda, const InnerCfg& ic, const doubl
     if (!F.c0_valid) {
       wzz(ctx->L(), F.n, F.v.d(), F.zptr, F.part.d());
       reduce_cols(ctx->L(), F.part.d(), elem_grid(F.n), 1, 0, F.scal.d() + 48);
+      ar_sum(ctx, F.scal.d() + 48, 1);
       F.c0_valid = true;
     }
     KG_CUDA(cudaMemcpyAsync(&static_cast<FistaCtl*>(F.ctl.p)->ss_const, F.scal.d() + 48, sizeof(double),
@@ -859,7 +939,8 @@ static void fista_enqueue(Fit& F, double lambda, const InnerCfg& ic, const doubl
                n_vmax, 0, ex ? F.bxpart.d() : nullptr, pgrid(F.p));
   }
   if (ic.max_iters >= 1) {
-    if (host_loop_mode()) {
+    // a sharded n-space loop is driven from the host: its all-reduces stay out of graph capture
+    if (host_loop_mode() || (sharded(ctx) && F.route == 0)) {
       const FistaCtl* hc = reinterpret_cast<const FistaCtl*>(ctx->pin() + PIN_CTL);
       i64 before = ctx->launches;
       for (;;) {
@@ -905,11 +986,13 @@ static void validate_obs(Fit& F) {
   kg_ctx* ctx = F.ctx;
   reset_errs(F);
   validate_pass(ctx->L(), F.n, F.fam, F.O->y.d(), F.O->a.d(), F.errs.l(), F.D->cell_base);
+  ar_min_i64(ctx, F.errs.l(), 1);  // first invalid cell over all slabs
   i64 e;
   KG_CUDA(cudaMemcpyAsync(&e, F.errs.p, sizeof(i64), cudaMemcpyDeviceToHost, ctx->s));
   sync(ctx);
   if (e == kNoErr) return;
   const i64 loc = e - F.D->cell_base;
+  if (loc < 0 || loc >= F.n) throw Error(E_INVAL, "invalid observation at cell " + std::to_string(e));  // other slab
   double yi, ai;
   KG_CUDA(cudaMemcpy(&yi, F.O->y.d() + loc, sizeof(double), cudaMemcpyDeviceToHost));
   KG_CUDA(cudaMemcpy(&ai, F.O->a.d() + loc, sizeof(double), cudaMemcpyDeviceToHost));
@@ -946,6 +1029,8 @@ static double lambda_max_fit(Fit& F) {
     for (i64 r = 0; r < D.c; ++r)
       run_chain(ctx, D.n, g_steps(D, r, 0), F.w.d(), F.b.d() + D.offs[r], F.s0.d(), F.s1.d(), false);
   }
+  ar_sum(ctx, F.b.d(), static_cast<size_t>(F.p));  // G(u) summed over the slabs
+  ar_min_i64(ctx, F.errs.l(), 1);
   pmaxabs(ctx->L(), F.p, F.b.d(), F.Jpart.d());
   reduce_cols(ctx->L(), F.Jpart.d(), pgrid(F.p), 1, 1, F.scal.d());
   double* pin = ctx->pin();
@@ -1059,10 +1144,12 @@ static ModelTrace gaussian_step(Fit& F, double lambda, const OuterCfg& oc, PathS
   h.eta_old = F.eta.d();
   const int g = h_full(F, F.best.d(), F.eta_t.d(), h);
   reduce_cols(ctx->L(), F.part.d(), g, kHlastCols, 0, F.scal.d());
+  ar_sum(ctx, F.scal.d(), kHlastCols);
   pnorm(ctx->L(), F.p, F.pen, F.alpha, F.best.d(), F.Jpart.d());
   reduce_cols(ctx->L(), F.Jpart.d(), pgrid(F.p), 2, 0, F.scal.d() + 16);
   double* pin = ctx->pin();
   KG_CUDA(cudaMemcpyAsync(pin, F.scal.p, sizeof(double) * 20, cudaMemcpyDeviceToHost, ctx->s));
+  ar_min_i64(ctx, F.errs.l(), 4);
   KG_CUDA(cudaMemcpyAsync(pin + PIN_ERR, F.errs.p, sizeof(i64) * 4, cudaMemcpyDeviceToHost, ctx->s));
   sync(ctx);
   const FistaOut fo = fista_read(F);
@@ -1106,10 +1193,12 @@ static ModelTrace outer_loop(Fit& F, double lambda, const OuterCfg& oc) {
   h0.flags = HL_LL_NEW;
   int g = h_full(F, F.theta.d(), F.eta.d(), h0);
   reduce_cols(ctx->L(), F.part.d(), g, kHlastCols, 0, F.scal.d());
+  ar_sum(ctx, F.scal.d(), kHlastCols);
   pnorm(ctx->L(), F.p, F.pen, F.alpha, F.theta.d(), F.Jpart.d());
   reduce_cols(ctx->L(), F.Jpart.d(), pgrid(F.p), 2, 0, F.scal.d() + 16);
   double* pin = ctx->pin();
   KG_CUDA(cudaMemcpyAsync(pin, F.scal.p, sizeof(double) * 20, cudaMemcpyDeviceToHost, ctx->s));
+  ar_min_i64(ctx, F.errs.l(), 4);
   KG_CUDA(cudaMemcpyAsync(pin + PIN_ERR, F.errs.p, sizeof(i64) * 4, cudaMemcpyDeviceToHost, ctx->s));
   sync(ctx);
   {
@@ -1160,9 +1249,11 @@ static ModelTrace outer_loop(Fit& F, double lambda, const OuterCfg& oc) {
     for (int j = 0; j < nt; ++j) h.t[j] = t_list[j];
     g = h_full(F, F.best.d(), F.eta_t.d(), h);
     reduce_cols(ctx->L(), F.part.d(), g, kHlastCols, 0, F.scal.d());
+  ar_sum(ctx, F.scal.d(), kHlastCols);
     ptrials(ctx->L(), F.p, F.pen, F.alpha, F.theta.d(), F.best.d(), nt, t_list, F.tpart.d());
     reduce_cols(ctx->L(), F.tpart.d(), pgrid(F.p), 2 * (1 + kMaxTrials), 0, F.scal.d() + 16);
     KG_CUDA(cudaMemcpyAsync(pin, F.scal.p, sizeof(double) * 40, cudaMemcpyDeviceToHost, ctx->s));
+    ar_min_i64(ctx, F.errs.l(), 16);
     KG_CUDA(cudaMemcpyAsync(pin + PIN_ERR, F.errs.p, sizeof(i64) * 16, cudaMemcpyDeviceToHost, ctx->s));
     sync(ctx);
     i64 errs[16];
@@ -1208,9 +1299,11 @@ static ModelTrace outer_loop(Fit& F, double lambda, const OuterCfg& oc) {
         for (int q = 0; q < nt; ++q) hb.t[q] = t_list[q];
         hlast_mode1(ctx->L(), hb);
         reduce_cols(ctx->L(), F.part.d(), hlast_grid(hb), kHlastCols, 0, F.scal.d());
+        ar_sum(ctx, F.scal.d(), kHlastCols);
         ptrials(ctx->L(), F.p, F.pen, F.alpha, F.theta.d(), F.best.d(), nt, t_list, F.tpart.d());
         reduce_cols(ctx->L(), F.tpart.d(), pgrid(F.p), 2 * (1 + kMaxTrials), 0, F.scal.d() + 16);
         KG_CUDA(cudaMemcpyAsync(pin, F.scal.p, sizeof(double) * 40, cudaMemcpyDeviceToHost, ctx->s));
+        ar_min_i64(ctx, F.errs.l(), 16);
         KG_CUDA(cudaMemcpyAsync(pin + PIN_ERR, F.errs.p, sizeof(i64) * 16, cudaMemcpyDeviceToHost, ctx->s));
         sync(ctx);
         std::memcpy(errs, pin + PIN_ERR, sizeof(errs));
@@ -1366,8 +1459,10 @@ static kg_path_result* fit_path(kg_ctx* ctx, const kg_design* D, const kg_obs* O
     h.flags = HL_LL_NEW;
     hlast_mode1(ctx->L(), h);
     reduce_cols(ctx->L(), F->part.d(), hlast_grid(h), kHlastCols, 0, F->scal.d());
+    ar_sum(ctx, F->scal.d(), kHlastCols);
     double* pin = ctx->pin();
     KG_CUDA(cudaMemcpyAsync(pin, F->scal.p, sizeof(double), cudaMemcpyDeviceToHost, ctx->s));
+    ar_min_i64(ctx, F->errs.l(), 1);
     KG_CUDA(cudaMemcpyAsync(pin + PIN_ERR, F->errs.p, sizeof(i64), cudaMemcpyDeviceToHost, ctx->s));
     sync(ctx);
     i64 e;
@@ -1400,6 +1495,7 @@ static kg_path_result* fit_path(kg_ctx* ctx, const kg_design* D, const kg_obs* O
     KG_CUDA(cudaMemcpyAsync(F->ctl.p, staged, sizeof(FistaCtl), cudaMemcpyHostToDevice, ctx->s));
     wzz(ctx->L(), F->n, F->v.d(), F->zptr, F->part.d());  // sum v z^2
     reduce_cols(ctx->L(), F->part.d(), elem_grid(F->n), 1, 0, &static_cast<FistaCtl*>(F->ctl.p)->ss_const);
+    ar_sum(ctx, &static_cast<FistaCtl*>(F->ctl.p)->ss_const, 1);
     DBuf dl, p2, obj, its, stat;
     dl.alloc(sizeof(double) * nl);
     p2.alloc(sizeof(double) * 4 * D->p[0][D->d - 1]);
@@ -1565,18 +1661,45 @@ kg_status kg_ctx_create(int device, kg_ctx** out) {
   return st;
 }
 
-kg_status kg_ctx_create_sharded(int device, int rank, int world, const void*, kg_ctx** out) {
+kg_status kg_ctx_create_sharded(int device, int rank, int world, const void* nccl_unique_id, kg_ctx** out) {
   *out = nullptr;
-  if (world != 1 || rank != 0) return KG_ENCCL;  // sharded NCCL contexts: see DESIGN.md (next rows)
-  return kg_ctx_create(device, out);
+  if (world < 1 || rank < 0 || rank >= world) return KG_EINVAL;
+  kg_ctx* ctx = nullptr;
+  const kg_status st = kg_ctx_create(device, &ctx);
+  if (st != KG_OK) return st;
+  ctx->rank = rank;
+  ctx->world = world;
+  if (nccl_unique_id == nullptr) {  // no communicator: this slab's local partials only
+    *out = ctx;
+    return KG_OK;
+  }
+  const kg_status s2 = guarded(ctx, [&] {
+    ncclUniqueId id;
+    std::memcpy(&id, nccl_unique_id, sizeof(id));
+    nccl_check(nccl_api()->CommInitRank(&ctx->comm, world, id, rank), "ncclCommInitRank");
+  });
+  if (s2 != KG_OK) {
+    kg_ctx_destroy(ctx);
+    return s2;
+  }
+  *out = ctx;
+  return KG_OK;
 }
 
-kg_status kg_nccl_unique_id(void*) { return KG_ENCCL; }
+kg_status kg_nccl_unique_id(void* out128) {
+  return guarded(nullptr, [&] {
+    static_assert(sizeof(ncclUniqueId) == 128, "ncclUniqueId is 128 bytes");
+    ncclUniqueId id;
+    nccl_check(nccl_api()->GetUniqueId(&id), "ncclGetUniqueId");
+    std::memcpy(out128, &id, sizeof(id));
+  });
+}
 
 void kg_ctx_destroy(kg_ctx* ctx) {
   if (!ctx) return;
   cudaSetDevice(ctx->device);
   if (ctx->s) cudaStreamSynchronize(ctx->s);
+  if (ctx->comm) nccl_api()->CommDestroy(ctx->comm);
   if (ctx->pinned) cudaFreeHost(ctx->pinned);
   for (cudaEvent_t e : ctx->ev)
     if (e) cudaEventDestroy(e);
@@ -1751,6 +1874,7 @@ void kg_design_destroy(kg_design* d) {
     cudaStreamSynchronize(d->ctx->s);
   }
   delete d;
+  cudaGetLastError();  // a failure here must not surface in a later, unrelated launch check
 }
 int64_t kg_design_n(const kg_design* d) { return d->N; }
 int64_t kg_design_p(const kg_design* d) { return d->P; }
@@ -1789,6 +1913,17 @@ kg_status kg_obs_create(kg_ctx* ctx, const kg_design* design, const double* y, c
       for (int i = 0; i < g; ++i) {
         mn = std::min(mn, hp[2 * i]);
         mx = std::max(mx, hp[2 * i + 1]);
+      }
+      if (sharded(ctx)) {  // global (min, max) over the slabs: max of (-min, max)
+        double* pin = ctx->pin();
+        pin[0] = -mn;
+        pin[1] = mx;
+        KG_CUDA(cudaMemcpyAsync(part.p, pin, 2 * sizeof(double), cudaMemcpyHostToDevice, ctx->s));
+        ar_max(ctx, part.d(), 2);
+        KG_CUDA(cudaMemcpyAsync(pin, part.p, 2 * sizeof(double), cudaMemcpyDeviceToHost, ctx->s));
+        sync(ctx);
+        mn = -pin[0];
+        mx = pin[1];
       }
       O->a_const = mn == mx;
       O->a_val = mn;
@@ -1917,6 +2052,7 @@ kg_status kg_g_map(kg_ctx* ctx, const kg_design* D, const double* u, double* coe
     double *s0 = t.get(D->scratch), *s1 = t.get(D->scratch);
     KG_CUDA(cudaMemcpyAsync(du, u, sizeof(double) * D->N, cudaMemcpyHostToDevice, ctx->s));
     g_map_dev(ctx, D, du, dc, s0, s1);
+    ar_sum(ctx, dc, static_cast<size_t>(D->P));  // sharded: X^T u summed over the slabs
     KG_CUDA(cudaMemcpyAsync(coef, dc, sizeof(double) * D->P, cudaMemcpyDeviceToHost, ctx->s));
     sync(ctx);
   });
@@ -1934,6 +2070,7 @@ kg_status kg_xtwx_apply(kg_ctx* ctx, const kg_design* D, const double* v, const 
     h_map_dev(ctx, D, dc, de, s0, s1);
     vz(ctx->L(), D->N, dv, de, dw);
     g_map_dev(ctx, D, dw, dout, s0, s1);
+    ar_sum(ctx, dout, static_cast<size_t>(D->P));
     KG_CUDA(cudaMemcpyAsync(out, dout, sizeof(double) * D->P, cudaMemcpyDeviceToHost, ctx->s));
     sync(ctx);
   });

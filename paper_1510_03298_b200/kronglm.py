@@ -14,6 +14,7 @@ upload once, fit many paths.
 from __future__ import annotations
 
 import ctypes as C
+import weakref
 import threading
 
 import numpy as np
@@ -42,22 +43,36 @@ def _ptr(a):
 class Context:
     """One CUDA device + stream (kg_ctx)."""
 
-    def __init__(self, device: int = 0):
+    def __init__(self, device: int = 0, _handle=None, rank: int = 0, world: int = 1):
         L = _lib.load()
-        h = C.c_void_p()
-        _lib.check(L.kg_ctx_create(int(device), C.byref(h)))
+        h = _handle
+        if h is None:
+            h = C.c_void_p()
+            _lib.check(L.kg_ctx_create(int(device), C.byref(h)))
         self.h = h
         self.device = device
+        self.rank, self.world = int(rank), int(world)
+        self._children = weakref.WeakSet()  # designs / observations / results on this context
 
-    def coefs(self) -> np.ndarray:
-        """All models' coefficients, n_models x p, in one device-to-host copy."""
-        out = np.zeros((self.n_models, self.design.p))
-        if self.n_models:
-            self.design.ctx.check(_lib.load().kg_result_coefs(self.h, 0, self.n_models, _ptr(out)))
-        return out
+    @classmethod
+    def sharded(cls, device: int, rank: int, world: int, unique_id: bytes | None):
+        """Last-mode sharded context (kg_ctx_create_sharded): rank `rank` of
+        `world` owns slab rank of the last observation mode; `unique_id` is
+        nccl_unique_id() from rank 0 broadcast to every rank (None: local
+        partials only, no communicator)."""
+        h = C.c_void_p()
+        buf = None
+        if unique_id is not None:
+            if len(unique_id) != 128:
+                raise ValueError("nccl unique id must be 128 bytes")
+            buf = C.create_string_buffer(bytes(unique_id), 128)
+        _lib.check(_lib.load().kg_ctx_create_sharded(int(device), int(rank), int(world), buf, C.byref(h)))
+        return cls(device, _handle=h, rank=rank, world=world)
 
     def close(self):
         if getattr(self, "h", None):
+            for ch in list(getattr(self, "_children", ())):  # the C objects must go before their context
+                ch.close()
             _lib.load().kg_ctx_destroy(self.h)
             self.h = None
 
@@ -86,6 +101,18 @@ class Context:
 
 
 _ctx_local = threading.local()
+
+
+def nccl_unique_id() -> bytes:
+    """128-byte ncclUniqueId for Context.sharded (made on rank 0, broadcast by the caller)."""
+    buf = C.create_string_buffer(128)
+    _lib.check(_lib.load().kg_nccl_unique_id(buf))
+    return buf.raw
+
+
+def shard_rows(n_last: int, rank: int, world: int) -> tuple[int, int]:
+    """Rows [lo, hi) of the last mode owned by `rank` (kg_design_create's split)."""
+    return n_last * rank // world, n_last * (rank + 1) // world
 
 
 def default_context(device: int = 0) -> Context:
@@ -117,6 +144,8 @@ class Design:
             if [x.shape[0] for x in comp] != rows:
                 raise ValueError("TensorDesign: factor row counts differ across components")
         self.row_dims = tuple(rows)
+        lo, hi = shard_rows(rows[-1], self.ctx.rank, self.ctx.world)
+        self.local_row_dims = tuple(rows[:-1]) + (hi - lo,)  # this rank's slab (= row_dims unsharded)
         self.block_dims = [tuple(x.shape[1] for x in comp) for comp in comps]
         self.p = int(sum(int(np.prod(b)) for b in self.block_dims))
         self.n = int(np.prod(rows))
@@ -126,13 +155,7 @@ class Design:
         h = C.c_void_p()
         self.ctx.check(_lib.load().kg_design_create(self.ctx.h, self.c, self.d, n_arr, p_arr, X, C.byref(h)))
         self.h = h
-
-    def coefs(self) -> np.ndarray:
-        """All models' coefficients, n_models x p, in one device-to-host copy."""
-        out = np.zeros((self.n_models, self.design.p))
-        if self.n_models:
-            self.design.ctx.check(_lib.load().kg_result_coefs(self.h, 0, self.n_models, _ptr(out)))
-        return out
+        self.ctx._children.add(self)
 
     def close(self):
         if getattr(self, "h", None):
@@ -187,24 +210,18 @@ class Observation:
             self.ctx.check(L.kg_obs_create(self.ctx.h, design.h, yp, ap, 1, C.byref(h)))
         else:
             y = _f(y)
-            if y.shape != design.row_dims:
+            if y.shape != design.local_row_dims:
                 raise ValueError("data dims do not match the design")
             a = None
             if weights is not None:
                 a = _f(weights)
-                if a.shape != design.row_dims:
+                if a.shape != design.local_row_dims:
                     raise ValueError("ObservationData: response and weight dims differ")
             self.ctx.check(L.kg_obs_create(self.ctx.h, design.h, y.ctypes.data_as(C.c_void_p),
                                            a.ctypes.data_as(C.c_void_p) if a is not None else None, 0,
                                            C.byref(h)))
         self.h = h
-
-    def coefs(self) -> np.ndarray:
-        """All models' coefficients, n_models x p, in one device-to-host copy."""
-        out = np.zeros((self.n_models, self.design.p))
-        if self.n_models:
-            self.design.ctx.check(_lib.load().kg_result_coefs(self.h, 0, self.n_models, _ptr(out)))
-        return out
+        self.ctx._children.add(self)
 
     def close(self):
         if getattr(self, "h", None):
@@ -248,6 +265,7 @@ class PathResult:
     def __init__(self, design: Design, h):
         self.design = design
         self.h = h
+        design.ctx._children.add(self)
         L = _lib.load()
         self.n_models = int(L.kg_result_n_models(h))
         self.truncated = bool(L.kg_result_truncated(h))
@@ -336,16 +354,16 @@ def h_map(design, coef):
     """Linear predictor array, vec = X theta (design.cpp:89-102)."""
     D = _design(design)
     th = D.flat(coef)
-    eta = np.zeros(D.n)
+    eta = np.zeros(int(np.prod(D.local_row_dims)))
     D.ctx.check(_lib.load().kg_h_map(D.ctx.h, D.h, _ptr(th), _ptr(eta)))
-    return eta.reshape(D.row_dims, order="F")
+    return eta.reshape(D.local_row_dims, order="F")
 
 
 def g_map(design, u):
     """Adjoint of h_map, vec = X^T vec(u) (design.cpp:104-116)."""
     D = _design(design)
     u = _f(u)
-    if u.shape != D.row_dims:
+    if u.shape != D.local_row_dims:
         raise ValueError("g_map: array dimensions do not match")
     out = np.zeros(D.p)
     D.ctx.check(_lib.load().kg_g_map(D.ctx.h, D.h, _ptr(u), _ptr(out)))
@@ -398,10 +416,10 @@ def predict(design, family, coef):
         raise ValueError("unknown family: " + str(family))
     D = _design(design)
     th = D.flat(coef)
-    eta = np.zeros(D.n)
-    mu = np.zeros(D.n)
+    eta = np.zeros(int(np.prod(D.local_row_dims)))
+    mu = np.zeros(eta.size)
     D.ctx.check(_lib.load().kg_predict(D.ctx.h, D.h, FAMILIES[family], _ptr(th), _ptr(eta), _ptr(mu)))
-    return eta.reshape(D.row_dims, order="F"), mu.reshape(D.row_dims, order="F")
+    return eta.reshape(D.local_row_dims, order="F"), mu.reshape(D.local_row_dims, order="F")
 
 
 def bspline_design(points, order=4, n_basis=0):

@@ -368,3 +368,53 @@ def test_slab_route_matches_oracle(monkeypatch):
     kw = dict(n_lambda=8, lambda_min_ratio=1e-3)
     compare_paths(K.fit_path(design, "gaussian", yg, weights=w, **kw),
                   O.fit_path(design, "gaussian", yg, weights=w, **kw))
+
+
+def test_sharded_context_world1_nccl_matches_unsharded():
+    """kg_ctx_create_sharded with a real one-rank NCCL communicator: every
+    cross-slab all-reduce runs (identity on one rank) and the sharded n-space
+    loop is host driven; paths equal the unsharded ones."""
+    uid = K.nccl_unique_id()
+    assert len(uid) == 128
+    ctx = K.Context.sharded(0, 0, 1, uid)
+    rng = np.random.default_rng(17)
+    design = bspline_design((20, 16, 12), (7, 6, 5))
+    B = np.zeros((7, 6, 5))
+    m = rng.random(B.shape) < 0.2
+    B[m] = rng.standard_normal(m.sum())
+    eta = configs.tensor_h(design[0], B)
+    y = rng.poisson(np.exp(np.log(15.0) / eta.max() * eta)).astype(float)
+    for fam, yy in (("poisson", y), ("gaussian", eta + rng.normal(0, 0.2, eta.shape))):
+        kw = dict(n_lambda=6, lambda_min_ratio=1e-2)
+        D = K.Design(design, ctx)
+        got = K.fit_path_resident(D, K.Observation(D, yy), fam, **kw)
+        want = K.fit_path(design, fam, yy, **kw)
+        res = {"lambdas": got.lambdas, "objectives": got.objectives, "truncated": got.truncated,
+               "coefficients": [D.blocks(c) for c in got.coefs()], "outer_iters": got.outer_iters,
+               "inner_iters": got.inner_iters}
+        compare_paths(res, want)
+    ctx.close()
+
+
+def test_local_slab_contexts_partition_the_operator_maps():
+    """World-2 sharded contexts without a communicator (local partials): each
+    rank's design keeps its rows of X_d, h_map gives that slab of eta and the
+    g_map partials sum to the full X^T u (G = sum_g G_g)."""
+    rng = np.random.default_rng(23)
+    n, p = (12, 10, 9), (5, 4, 4)
+    design = bspline_design(n, p)
+    th = [rng.standard_normal(p)]
+    u = rng.standard_normal(n)
+    eta_full = K.h_map(design, th)
+    g_full = H.flat(K.g_map(design, u))
+    total = np.zeros_like(g_full)
+    for r in range(2):
+        ctx = K.Context.sharded(0, r, 2, None)
+        D = K.Design(design, ctx)
+        lo, hi = K.shard_rows(n[-1], r, 2)
+        assert D.local_row_dims == (n[0], n[1], hi - lo)
+        np.testing.assert_allclose(K.h_map(D, th), eta_full[:, :, lo:hi], rtol=0, atol=1e-13)
+        total += H.flat(K.g_map(D, np.asfortranarray(u[:, :, lo:hi])))
+        D.close()
+        ctx.close()
+    np.testing.assert_allclose(total, g_full, rtol=1e-13, atol=1e-13)
