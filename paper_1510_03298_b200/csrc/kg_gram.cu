@@ -97,8 +97,9 @@ __device__ void cta_sum3(double a, double b, double c, double* sh, double* out) 
 }
 
 // Mode-j contraction like smem_mode with the band rows staged in shared
-// memory (sc: K x MB coefficients, slo/slen: row ranges) and the taps unrolled
-// to MB with predication; the summation order is smem_mode's.
+// memory (sc: MB x K coefficients, tap-major so that lanes on consecutive rows
+// read consecutive words; slo/slen: row ranges) and the taps unrolled to MB
+// with predication; the summation order is smem_mode's.
 template <int BS, int MB>
 __device__ __forceinline__ void smem_mode_st(const double* in, double* out, int K, int q, const FastDiv& fa,
                                              const FastDiv& fk, const double* sc, const int* slo,
@@ -110,12 +111,12 @@ __device__ __forceinline__ void smem_mode_st(const double* in, double* out, int 
     const int be = static_cast<int>(fk.div(static_cast<uint32_t>(rest)));
     const int m = rest - be * K;
     const int lo = slo[m], len = slen[m];
-    const double* c = sc + m * MB;
+    const double* c = sc + m;
     const double* src = in + al + a * (lo + K * be);
     double s = 0.0;
 #pragma unroll
     for (int t = 0; t < MB; ++t)
-      if (t < len) s = fma(c[t], src[a * t], s);
+      if (t < len) s = fma(c[t * K], src[a * t], s);
     out[e] = s;
   }
 }
@@ -605,7 +606,7 @@ __global__ void __launch_bounds__(BS) k_gauss_path(PersistArgs P) {
         const double* c = A.G[j].coef + __ldg(A.G[j].off + r);
         sgi[2 * r0 + r] = __ldg(A.G[j].lo + r);
         sgi[2 * r0 + K + r] = ln;
-        for (int t = 0; t < MB; ++t) sg[static_cast<i64>(r0 + r) * MB + t] = t < ln ? c[t] : 0.0;
+        for (int t = 0; t < MB; ++t) sg[static_cast<i64>(r0) * MB + t * K + r] = t < ln ? c[t] : 0.0;  // tap-major
       }
       r0 += K;
     }
@@ -704,12 +705,30 @@ __global__ void __launch_bounds__(BS) k_gauss_path(PersistArgs P) {
       l1 += fabs(xv);
       l2 = fma(xv, xv, l2);
     }
-    double r[3];
-    reduce3(dots, l1, l2, r);
-    if (threadIdx.x == 0) {
-      dst[3 * s] = r[0];
-      dst[3 * s + 1] = r[1];
-      dst[3 * s + 2] = r[2];
+    // CTA partials for thread 0 only: one barrier (red is next written after
+    // the following grid barrier)
+    const int wp = threadIdx.x >> 5, ln = threadIdx.x & 31;
+    dots = warp_sum(dots);
+    l1 = warp_sum(l1);
+    l2 = warp_sum(l2);
+    if (ln == 0) {
+      red[wp] = dots;
+      red[32 + wp] = l1;
+      red[64 + wp] = l2;
+    }
+    __syncthreads();
+    if (wp == 0) {
+      double r0 = ln < (BS >> 5) ? red[ln] : 0.0;
+      double r1 = ln < (BS >> 5) ? red[32 + ln] : 0.0;
+      double r2 = ln < (BS >> 5) ? red[64 + ln] : 0.0;
+      r0 = warp_sum(r0);
+      r1 = warp_sum(r1);
+      r2 = warp_sum(r2);
+      if (ln == 0) {
+        dst[3 * s] = r0;
+        dst[3 * s + 1] = r1;
+        dst[3 * s + 2] = r2;
+      }
     }
   };
   auto apply = [&]() {
@@ -771,31 +790,33 @@ __global__ void __launch_bounds__(BS) k_gauss_path(PersistArgs P) {
         }
         grid_sync(P.bar, nb);
         issue(Xk);
-        if (k >= 2) {  // monitor iteration k-1 from its partials
-          const double* pp = P.part + ((k - 1) & 1) * 3 * static_cast<i64>(nb);
-          double a = 0.0, b = 0.0, c = 0.0;
-          for (int r = threadIdx.x; r < static_cast<int>(nb); r += BS) {
-            a += __ldcg(pp + 3 * r);
-            b += __ldcg(pp + 3 * r + 1);
-            c += __ldcg(pp + 3 * r + 2);
+        if (k >= 2) {  // monitor iteration k-1 from its partials (warp 0, fixed order)
+          if (threadIdx.x < 32) {
+            const double* pp = P.part + ((k - 1) & 1) * 3 * static_cast<i64>(nb);
+            double a = 0.0, b = 0.0, c = 0.0;
+            for (int r = threadIdx.x; r < static_cast<int>(nb); r += 32) {
+              a += __ldcg(pp + 3 * r);
+              b += __ldcg(pp + 3 * r + 1);
+              c += __ldcg(pp + 3 * r + 2);
+            }
+            a = warp_sum(a);
+            b = warp_sum(b);
+            c = warp_sum(c);
+            if (threadIdx.x == 0) {
+              const double gk = 0.5 * (a + c0) / n + lam * penalty_of(A.pen, A.alpha, b, c);
+              ctl_step(cs, gk);
+              if ((P.dbg & 8) && t < 2 && k < 8)
+                printf("s=%d t=%d k=%lld g=%.17g done=%d\n", s, t, static_cast<long long>(k), gk, cs.done);
+            }
           }
-          double r3[3];
-          reduce3(a, b, c, r3);
-          if (threadIdx.x == 0) {
-            const double gk = 0.5 * (r3[0] + c0) / n + lam * penalty_of(A.pen, A.alpha, r3[1], r3[2]);
-            ctl_step(cs, gk);
-            if ((P.dbg & 8) && t < 2 && k < 8)
-              printf("s=%d t=%d k=%lld g=%.17g done=%d\n", s, t, static_cast<long long>(k), gk, cs.done);
-          }
-          __syncthreads();
-          if (cs.copy_best) {  // best := x_{k-1} (now in the x_prev slot)
+          __syncthreads();  // cs is read by every thread (written again only after the next grid barrier)
+          if (cs.copy_best) {  // best := x_{k-1} (now in the x_prev slot; own elements only)
             for (int e = threadIdx.x; e < q; e += BS) {
               bst[e] = xps[e];
               sbst[e] = sxps[e];
             }
           }
         }
-        __syncthreads();
         async::mbar_wait(&mb, parity);  // always consume the copy (keeps the barrier phase)
         parity ^= 1u;
         if (cs.done) break;
