@@ -20,6 +20,8 @@ namespace kg {
 namespace {
 
 constexpr int NT = 256;  // p-space reduction kernels
+constexpr int kPollRows = 10;  // partial / flag rows per lane: up to 320 CTAs
+constexpr int kFlagCTAs = 64;  // k_gauss_path uses the flag barrier up to this many CTAs (measured: C1 gains, C2/C4 do not)
 
 __device__ __forceinline__ double soft(double z, double g) {
   const double m = fabs(z) - g;
@@ -658,8 +660,9 @@ __global__ void __launch_bounds__(BS) k_gauss_path(PersistArgs P) {
     async::mbar_wait(&mb, parity);
     parity ^= 1u;
   };
+  unsigned gen = 0;  // flag-barrier generation (same sequence in every CTA)
   // S'(x) of this slab from the staged band -> sxs; objective partials of xs -> dst
-  auto compute = [&](const double* xsrc, double* dst) {
+  auto compute = [&](const double* xsrc, double* dst, int sc_, int ss_) {  // dst[c * sc_ + s * ss_]
     const double* xin = band + async::stage_shift(xsrc + static_cast<i64>(lo) * q);
     for (int e = threadIdx.x; e < q; e += BS) {
       const double* xe = xin + e;
@@ -725,9 +728,9 @@ __global__ void __launch_bounds__(BS) k_gauss_path(PersistArgs P) {
       r1 = warp_sum(r1);
       r2 = warp_sum(r2);
       if (ln == 0) {
-        dst[3 * s] = r0;
-        dst[3 * s + 1] = r1;
-        dst[3 * s + 2] = r2;
+        dst[s * ss_] = r0;
+        dst[sc_ + s * ss_] = r1;
+        dst[2 * sc_ + s * ss_] = r2;
       }
     }
   };
@@ -735,7 +738,7 @@ __global__ void __launch_bounds__(BS) k_gauss_path(PersistArgs P) {
     issue(P.X);
     __syncthreads();
     wait_band();
-    compute(P.X, P.part);
+    compute(P.X, P.part, 1, 3);
   };
   auto gather3 = [&](double* out) {  // fixed-order sum of every CTA's 3 partials
     double a = 0.0, b = 0.0, c = 0.0;
@@ -788,28 +791,70 @@ __global__ void __launch_bounds__(BS) k_gauss_path(PersistArgs P) {
           sxps[e] = sxi;
           Xk[base + e] = ci;
         }
-        grid_sync(P.bar, nb);
-        issue(Xk);
-        if (k >= 2) {  // monitor iteration k-1 from its partials (warp 0, fixed order)
-          if (threadIdx.x < 32) {
-            const double* pp = P.part + ((k - 1) & 1) * 3 * static_cast<i64>(nb);
-            double a = 0.0, b = 0.0, c = 0.0;
-            for (int r = threadIdx.x; r < static_cast<int>(nb); r += 32) {
-              a += __ldcg(pp + 3 * r);
-              b += __ldcg(pp + 3 * r + 1);
-              c += __ldcg(pp + 3 * r + 2);
+        // arrival: all of this CTA's x_k is written (barrier), then one release of
+        // the generation; warp 0 polls every CTA's flag (acquire) and, in the same
+        // pass, that CTA's objective partials of step k-1 (component-major,
+        // double-buffered by parity), so the grid barrier and the monitor gather
+        // cost one round trip after the last arrival
+        ++gen;
+        const bool flagbar = nb <= kFlagCTAs && !(P.dbg & 64);  // flag barrier for small grids, atomic otherwise
+        if (flagbar)
+          __syncthreads();
+        else
+          grid_sync(P.bar, nb);
+        if (threadIdx.x < 32) {
+          const int lane = threadIdx.x;
+          const double* pp = P.part + ((k - 1) & 1) * 3 * static_cast<i64>(nb);
+          if (flagbar) {
+            if (lane == 0) asm volatile("st.release.gpu.global.u32 [%0], %1;" ::"l"(P.flags + s), "r"(gen) : "memory");
+            const long long w0 = clock64();
+            for (;;) {  // flags only: light polling while the slowest CTA finishes
+              bool mine = true;
+#pragma unroll
+              for (int i = 0; i < kPollRows; ++i) {
+                const int r = lane + 32 * i;
+                if (r < static_cast<int>(nb)) {
+                  unsigned f;
+                  asm volatile("ld.acquire.gpu.global.u32 %0, [%1];" : "=r"(f) : "l"(P.flags + r) : "memory");
+                  mine = mine && f >= gen;
+                }
+              }
+              if (__all_sync(0xffffffffu, mine)) break;
+              __nanosleep(20);
+              if (clock64() - w0 > async::kWatchdogCycles) {
+                if (lane == 0) printf("kg watchdog: flag barrier (block %d, generation %u)\n", s, gen);
+                __trap();
+              }
             }
+          }
+          double a = 0.0, b = 0.0, c = 0.0;  // objective partials of step k-1 (after the barrier)
+          if (k >= 2) {
+#pragma unroll
+            for (int i = 0; i < kPollRows; ++i) {
+              const int r = lane + 32 * i;
+              if (r < static_cast<int>(nb)) {
+                a += __ldcg(pp + r);
+                b += __ldcg(pp + nb + r);
+                c += __ldcg(pp + 2 * nb + r);
+              }
+            }
+          }
+          __syncwarp();
+          if (lane == 0) issue(Xk);
+          if (k >= 2) {  // monitor iteration k-1: fixed-order sum (lane-ascending, then the warp tree)
             a = warp_sum(a);
             b = warp_sum(b);
             c = warp_sum(c);
-            if (threadIdx.x == 0) {
+            if (lane == 0) {
               const double gk = 0.5 * (a + c0) / n + lam * penalty_of(A.pen, A.alpha, b, c);
               ctl_step(cs, gk);
               if ((P.dbg & 8) && t < 2 && k < 8)
                 printf("s=%d t=%d k=%lld g=%.17g done=%d\n", s, t, static_cast<long long>(k), gk, cs.done);
             }
           }
-          __syncthreads();  // cs is read by every thread (written again only after the next grid barrier)
+        }
+        if (k >= 2) {
+          __syncthreads();  // cs is read by every thread (written again only after the next barrier)
           if (cs.copy_best) {  // best := x_{k-1} (now in the x_prev slot; own elements only)
             for (int e = threadIdx.x; e < q; e += BS) {
               bst[e] = xps[e];
@@ -820,7 +865,7 @@ __global__ void __launch_bounds__(BS) k_gauss_path(PersistArgs P) {
         async::mbar_wait(&mb, parity);  // always consume the copy (keeps the barrier phase)
         parity ^= 1u;
         if (cs.done) break;
-        compute(Xk, P.part + (k & 1) * 3 * static_cast<i64>(nb));
+        compute(Xk, P.part + (k & 1) * 3 * static_cast<i64>(nb), static_cast<int>(nb), 1);
       }
       if (threadIdx.x == 0) cs.copy_best = 0;  // any pending copy was applied above
       __syncthreads();
@@ -936,7 +981,7 @@ static size_t path_smem(const GramStepArgs& A) {
 
 bool gauss_path_ok(const GramStepArgs& A) {
   const size_t sm = path_smem(A);
-  if (sm > 200 * 1024) return false;
+  if (sm > 200 * 1024 || A.pd > 32 * kPollRows) return false;  // the flag barrier polls <= 320 CTAs
   static bool attr = false;
   if (!attr) {
     KG_CUDA(cudaFuncSetAttribute(k_gauss_path<256>, cudaFuncAttributeMaxDynamicSharedMemorySize, 210 * 1024));

@@ -275,6 +275,7 @@ struct PersistArgs {
   double* Sbest = nullptr;    // out: S'(best) (p)
   double* part = nullptr;     // 3 per CTA
   unsigned* bar = nullptr;    // grid barrier {count, generation}, zero-initialised
+  unsigned* flags = nullptr;  // k_gauss_path: per-CTA arrival generations (zeroed before each launch)
   // whole-path mode (k_gauss_path)
   const double* lambdas = nullptr;
   int n_lambda = 0;

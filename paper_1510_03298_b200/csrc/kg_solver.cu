@@ -486,7 +486,7 @@ struct Fit {
   bool gstep = false;
   int persist = -1;  // -1 unknown, 0 no, 1: the whole solve runs in one cooperative kernel
   bool persist_solve = false;  // the last solve ran persistent (launch accounting)
-  DBuf gpart, gcount, stheta, pX, pbar;
+  DBuf gpart, gcount, stheta, pX, pbar, pflags;
   // one captured FISTA graph per route
   cudaGraphExec_t exec[2] = {nullptr, nullptr};
   cudaGraph_t graph[2] = {nullptr, nullptr};
@@ -562,6 +562,7 @@ static void alloc_fit(Fit& F) {
     F.pX.alloc(2 * pb);
     F.pbar.alloc(sizeof(unsigned) * 4);
     KG_CUDA(cudaMemsetAsync(F.pbar.p, 0, sizeof(unsigned) * 4, F.ctx->s));
+    F.pflags.alloc(sizeof(unsigned) * pd);
     F.gcount.alloc(sizeof(unsigned) * 4);
     KG_CUDA(cudaMemsetAsync(F.gcount.p, 0, sizeof(unsigned) * 4, F.ctx->s));
   }
@@ -1509,6 +1510,8 @@ static kg_path_result* fit_path(kg_ctx* ctx, const kg_design* D, const kg_obs* O
     P.X = F->pX.d();
     P.part = F->gpart.d();
     P.bar = static_cast<unsigned*>(F->pbar.p);
+    P.flags = static_cast<unsigned*>(F->pflags.p);
+    KG_CUDA(cudaMemsetAsync(F->pflags.p, 0, F->pflags.bytes, ctx->s));
     P.lambdas = dl.d();
     P.n_lambda = static_cast<int>(nl);
     P.part2 = p2.d();
