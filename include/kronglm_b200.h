@@ -183,6 +183,15 @@ kg_status kg_bspline_design(int64_t npts, const double* points, int64_t order, i
 int64_t kg_default_basis_count(int64_t n_points, int64_t ratio); /* bspline.cpp:20-26; -1 on bad args */
 int64_t kg_linear_index(int64_t d, const int64_t* multi_index, const int64_t* dims); /* array.cpp:22-36; -1 bad */
 
+/* Held-out selection (mse_heldout, path.cpp:91-126, decl path.hpp:63): for
+ * every model of `res`, the sum over cells with mask == 1 of (mean(X theta_t)
+ * - y_full)^2 into mse[0 .. n_models), and the first minimizing model in
+ * *argmin.  y_full and mask are host arrays of this context's slab; mask
+ * entries must be 0 or 1 and at least one must be 1 (KG_EINVAL otherwise).
+ * Predictions are computed on the device from the resident coefficients. */
+kg_status kg_mse_heldout(kg_ctx* ctx, const kg_design* design, const kg_path_result* res, int family,
+                         const double* y_full, const double* mask, double* mse, int64_t* argmin);
+
 /* --------------------------------------------------------- measurement -- */
 /* Times `reps` launches of one hot-path kernel on the context stream with
  * CUDA events, on the resident observation (inputs already in HBM).

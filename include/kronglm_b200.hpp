@@ -228,6 +228,44 @@ inline std::vector<double> g_map(const TensorDesign& design, const std::vector<d
   return coef;
 }
 
+// mse_heldout (path.hpp:55-64, path.cpp:91-126): per model the sum over the
+// mask == 1 cells of (mean - y_full)^2 and the first minimizing model.  The
+// predictions (h_map + inverse link) run on the device via kg_predict.
+struct HeldoutMse {
+  std::vector<double> mse;
+  Index argmin = 0;
+};
+
+inline HeldoutMse mse_heldout(const FitPath& path, const TensorDesign& design, const FamilySpec& spec,
+                              const std::vector<double>& y_full, const std::vector<double>& heldout_mask) {
+  const size_t n = static_cast<size_t>(design.n());
+  if (y_full.size() != n || heldout_mask.size() != n)
+    throw std::invalid_argument("mse_heldout: array dims do not match the design");
+  Index n_held = 0;
+  for (double m : heldout_mask) {
+    if (m != 0.0 && m != 1.0) throw std::invalid_argument("mse_heldout: mask entries must be 0 or 1");
+    if (m == 1.0) ++n_held;
+  }
+  if (n_held == 0) throw std::invalid_argument("mse_heldout: empty held-out mask");
+  if (path.n_models() == 0) throw std::invalid_argument("mse_heldout: empty path");
+  HeldoutMse out;
+  std::vector<double> eta(n), mu(n);
+  for (Index t = 0; t < path.n_models(); ++t) {
+    check(kg_predict(design.ctx().get(), design.get(), static_cast<int>(spec.family),
+                     path.fits[static_cast<size_t>(t)].data(), eta.data(), mu.data()),
+          design.ctx().get());
+    double sum = 0.0;
+    for (size_t i = 0; i < n; ++i)
+      if (heldout_mask[i] == 1.0) {
+        const double diff = mu[i] - y_full[i];
+        sum += diff * diff;
+      }
+    out.mse.push_back(sum);
+    if (sum < out.mse[static_cast<size_t>(out.argmin)]) out.argmin = t;
+  }
+  return out;
+}
+
 // bspline_design (bspline.hpp:36): clamped uniform basis on the grid points.
 inline Matrix bspline_design(const std::vector<double>& points, Index order, Index n_basis) {
   Matrix m(static_cast<Index>(points.size()), n_basis);

@@ -1335,6 +1335,40 @@ int orc_xtwx_apply(int64_t c, int64_t d, const int64_t* n, const int64_t* p, con
 }
 
 // what: 0 mean, 1 score, 2 glm_weights, 3 working_response
+// mse_heldout (path.cpp:91-126): per model the sum over mask == 1 cells of
+// (mean(h_map(theta_t)) - y_full)^2, ascending cell order; argmin = first minimum.
+int orc_mse_heldout(int64_t c, int64_t d, const int64_t* n, const int64_t* p, const double* const* X, int fam,
+                    const double* coefs, int64_t n_models, const double* y_full, const double* mask, double* mse,
+                    int64_t* argmin) {
+  return guard([&] {
+    auto D = make_design(c, d, n, p, X);
+    const I N = D->n;
+    I n_held = 0;
+    for (I i = 0; i < N; ++i) {
+      const double m = mask[i];
+      if (m != 0.0 && m != 1.0) throw std::invalid_argument("mse_heldout: mask entries must be 0 or 1");
+      if (m == 1.0) ++n_held;
+    }
+    if (n_held == 0) throw std::invalid_argument("mse_heldout: empty held-out mask");
+    if (n_models == 0) throw std::invalid_argument("mse_heldout: empty path");
+    Spec s{fam, 1.0};
+    I best = 0;
+    for (I t = 0; t < n_models; ++t) {
+      std::vector<double> th(coefs + t * D->p, coefs + (t + 1) * D->p);
+      const Arr mu = mean(s, h_map(*D, th));
+      double sum = 0.0;
+      for (I i = 0; i < N; ++i)
+        if (mask[i] == 1.0) {
+          const double diff = mu.v[i] - y_full[i];
+          sum += diff * diff;
+        }
+      mse[t] = sum;
+      if (sum < mse[best]) best = t;
+    }
+    *argmin = best;
+  });
+}
+
 int orc_family_map(int fam, double disp, int64_t n, const double* y, const double* a, const double* eta, int what,
                    double* out) {
   return guard([&] {

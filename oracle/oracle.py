@@ -92,13 +92,14 @@ def _declare(L):
         "orc_path_model": [vp, _i64, pd], "orc_path_coef": [vp, _i64, pd], "orc_path_free": [vp],
         "orc_bspline_design": [_i64, pd, _i64, _i64, pd],
         "orc_default_basis_count": [_i64, _i64, pi],
+        "orc_mse_heldout": D + [C.c_int, pd, _i64, pd, pd, pd, pi],
     }
     for name, args in sig.items():
         getattr(L, name).argtypes = args
     for name in ["orc_linear_index", "orc_rho", "orc_h_map", "orc_g_map", "orc_xtwx_apply", "orc_family_map",
                  "orc_loglik", "orc_validate", "orc_penalty_value", "orc_prox", "orc_lambda_max",
                  "orc_spectral_radius", "orc_lipschitz_upper", "orc_fista_solve", "orc_outer_solve",
-                 "orc_fit_path", "orc_bspline_design", "orc_default_basis_count"]:
+                 "orc_fit_path", "orc_bspline_design", "orc_default_basis_count", "orc_mse_heldout"]:
         getattr(L, name).restype = C.c_int
 
 
@@ -224,6 +225,19 @@ def h_map(design, coef):
     eta = np.zeros(int(np.prod(D.row_dims)))
     _check(lib().orc_h_map(*D.args(), _ptr(th), _ptr(eta)))
     return eta.reshape(D.row_dims, order="F")
+
+
+def mse_heldout(design, family, coefficients, y_full, heldout_mask):
+    """kronglm::mse_heldout (path.cpp:91-126) over a list of coefficient sets."""
+    D = _Design(design)
+    flat = np.ascontiguousarray(np.stack([D.flat(c) for c in coefficients])) if coefficients else np.zeros((0, D.p_total))
+    y = _f(y_full).ravel(order="F")
+    m = _f(heldout_mask).ravel(order="F")
+    out = np.zeros(max(len(coefficients), 1))
+    arg = C.c_int64()
+    _check(lib().orc_mse_heldout(*D.args(), FAMILIES[family], _ptr(flat), len(coefficients), _ptr(y), _ptr(m),
+                                 _ptr(out), C.byref(arg)))
+    return {"mse": [float(v) for v in out[:len(coefficients)]], "argmin": int(arg.value)}
 
 
 def g_map(design, u):

@@ -85,6 +85,7 @@ _SIGS = {
     "kg_linear_index": (_i64, [_i64, _pi, _pi]),
     "kg_time_kernel": (C.c_int, [_vp, _vp, _vp, C.c_int, C.c_int, _pd, _pd]),
     "kg_path_kernel_stats": (C.c_int, [_vp, _pd, _pd, C.POINTER(_i64)]),
+    "kg_mse_heldout": (C.c_int, [_vp, _vp, _vp, C.c_int, _pd, _pd, _pd, C.POINTER(_i64)]),
     "kg_launch_count": (_i64, [_vp]),
     "kg_launch_count_reset": (None, [_vp]),
 }

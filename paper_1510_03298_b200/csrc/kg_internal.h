@@ -216,6 +216,8 @@ void score0(const Launch& L, i64 n, int fam, double disp, const double* y, const
 void validate_pass(const Launch& L, i64 n, int fam, const double* y, const double* a, i64* err, i64 cell_base);
 void eta_combine(const Launch& L, i64 n, double t, const double* eta_t, double* eta);
 void mean_map(const Launch& L, i64 n, int fam, const double* eta, double* mu);
+// per-CTA (elem_grid(n)) partials of sum_{mask == 1} (mu - y)^2
+void masked_sse(const Launch& L, i64 n, const double* mu, const double* y, const double* mask, double* part);
 void fill(const Launch& L, i64 n, double v, double* x);
 
 // p-space

@@ -644,6 +644,25 @@ void fista_update(const Launch& L, const FistaCtl* ctl, i64 p, int pen, double a
   bump(L);
 }
 
+// per-CTA partials of sum over mask == 1 of (mu - y)^2 (mse_heldout, path.cpp:111-119)
+__global__ void __launch_bounds__(NT) k_masked_sse(i64 n, const double* mu, const double* y, const double* mask,
+                                                   double* part) {
+  __shared__ double red[32];
+  double s = 0.0;
+  for (i64 i = static_cast<i64>(blockIdx.x) * NT + threadIdx.x; i < n; i += static_cast<i64>(gridDim.x) * NT)
+    if (mask[i] == 1.0) {
+      const double d = mu[i] - y[i];
+      s = fma(d, d, s);
+    }
+  const double r = block_reduce<false>(s, red);
+  if (threadIdx.x == 0) part[blockIdx.x] = r;
+}
+
+void masked_sse(const Launch& L, i64 n, const double* mu, const double* y, const double* mask, double* part) {
+  k_masked_sse<<<elem_grid(n), NT, 0, L.s>>>(n, mu, y, mask, part);
+  bump(L);
+}
+
 // per-CTA partials of <a, b> (p-space)
 __global__ void __launch_bounds__(NT) k_pdot(i64 p, const double* a, const double* b, double* part) {
   __shared__ double red[32];

@@ -2143,6 +2143,57 @@ kg_status kg_predict(kg_ctx* ctx, const kg_design* D, int family, const double* 
   });
 }
 
+kg_status kg_mse_heldout(kg_ctx* ctx, const kg_design* D, const kg_path_result* R, int family, const double* y_full,
+                         const double* mask, double* mse, int64_t* argmin) {
+  return guarded(ctx, [&] {
+    set_device(ctx);
+    if (family < KG_GAUSSIAN || family > KG_GAMMA) throw Error(E_INVAL, "unknown family");
+    // path.cpp:93-110 (validated on this rank's slab; the count is summed over the slabs)
+    i64 n_held = 0;
+    for (i64 i = 0; i < D->N; ++i) {
+      const double m = mask[i];
+      if (m != 0.0 && m != 1.0) throw Error(E_INVAL, "mse_heldout: mask entries must be 0 or 1");
+      if (m == 1.0) ++n_held;
+    }
+    Tmp t;
+    double *dy = t.get(D->N), *dmask = t.get(D->N), *de = t.get(D->N), *dm = t.get(D->N);
+    double *s0 = t.get(D->scratch), *s1 = t.get(D->scratch);
+    const i64 models = static_cast<i64>(R->lambdas.size());
+    const int g = elem_grid(D->N);
+    double* part = t.get(static_cast<i64>(g));
+    double* out = t.get(std::max<i64>(models, 1) + 1);
+    double* pin = ctx->pin();
+    if (sharded(ctx)) {
+      pin[0] = static_cast<double>(n_held);
+      KG_CUDA(cudaMemcpyAsync(out, pin, sizeof(double), cudaMemcpyHostToDevice, ctx->s));
+      ar_sum(ctx, out, 1);
+      KG_CUDA(cudaMemcpyAsync(pin, out, sizeof(double), cudaMemcpyDeviceToHost, ctx->s));
+      sync(ctx);
+      n_held = static_cast<i64>(pin[0]);
+    }
+    if (n_held == 0) throw Error(E_INVAL, "mse_heldout: empty held-out mask");
+    if (models == 0) throw Error(E_INVAL, "mse_heldout: empty path");
+    KG_CUDA(cudaMemcpyAsync(dy, y_full, sizeof(double) * D->N, cudaMemcpyHostToDevice, ctx->s));
+    KG_CUDA(cudaMemcpyAsync(dmask, mask, sizeof(double) * D->N, cudaMemcpyHostToDevice, ctx->s));
+    for (i64 m = 0; m < models; ++m) {  // predict (path.cpp:83-89) + masked SSE per model
+      h_map_dev(ctx, D, R->coefs.d() + R->p * m, de, s0, s1);
+      mean_map(ctx->L(), D->N, family, de, dm);
+      masked_sse(ctx->L(), D->N, dm, dy, dmask, part);
+      reduce_cols(ctx->L(), part, g, 1, 0, out + m);
+    }
+    ar_sum(ctx, out, static_cast<size_t>(models));
+    std::vector<double> h(models);
+    KG_CUDA(cudaMemcpyAsync(h.data(), out, sizeof(double) * models, cudaMemcpyDeviceToHost, ctx->s));
+    sync(ctx);
+    i64 best = 0;
+    for (i64 m = 0; m < models; ++m) {
+      mse[m] = h[m];
+      if (h[m] < h[best]) best = m;  // first minimum (path.cpp:120)
+    }
+    *argmin = best;
+  });
+}
+
 kg_status kg_time_kernel(kg_ctx* ctx, const kg_design* D, const kg_obs* O, int which, int reps, double* avg_ms,
                          double* bytes) {
   return guarded(ctx, [&] {

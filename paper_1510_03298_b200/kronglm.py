@@ -410,6 +410,24 @@ def fit_path(design, family, y, weights=None, penalty="lasso", alpha=0.0, n_lamb
     return out
 
 
+def mse_heldout(path, family, y_full, heldout_mask):
+    """Held-out sum of squared errors per model and the minimizing index
+    (kronglm::mse_heldout, path.cpp:91-126), from a PathResult (the
+    coefficients stay on the device).  Returns {"mse": [...], "argmin": t}."""
+    if family not in FAMILIES:
+        raise ValueError("unknown family: " + str(family))
+    D = path.design
+    y = _f(y_full)
+    m = _f(heldout_mask)
+    if y.shape != D.local_row_dims or m.shape != D.local_row_dims:
+        raise ValueError("mse_heldout: array dims do not match the design")
+    out = np.zeros(max(path.n_models, 1))
+    arg = _i64()
+    D.ctx.check(_lib.load().kg_mse_heldout(D.ctx.h, D.h, path.h, FAMILIES[family], _ptr(y), _ptr(m), _ptr(out),
+                                           C.byref(arg)))
+    return {"mse": [float(v) for v in out[:path.n_models]], "argmin": int(arg.value)}
+
+
 def predict(design, family, coef):
     """Linear predictor and fitted mean arrays (path.cpp:83-89)."""
     if family not in FAMILIES:

@@ -47,6 +47,18 @@ int main() {
     bad |= 32;
   } catch (const std::invalid_argument&) {
   }
+  // mse_heldout (path.cpp:91-126): a single held-out cell gives the squared residual
+  {
+    std::vector<double> mask(static_cast<size_t>(design.n()), 0.0);
+    mask[5] = 1.0;
+    const HeldoutMse ho = mse_heldout(path, design, FamilySpec::gaussian(), y, mask);
+    if (ho.mse.size() != static_cast<size_t>(path.n_models())) bad |= 64;
+    for (Index t = 0; t < path.n_models(); ++t) {
+      const std::vector<double> e = h_map(design, path.fits[static_cast<size_t>(t)]);
+      const double d = e[5] - y[5];
+      if (std::abs(ho.mse[static_cast<size_t>(t)] - d * d) > 1e-12 * std::max(1.0, d * d)) bad |= 64;
+    }
+  }
   std::printf("shim_path models=%lld lambda_max=%.6g final_objective=%.9g status=%d\n",
               static_cast<long long>(path.n_models()), path.lambda_max_value, path.objectives.back(), bad);
   return bad;

@@ -418,3 +418,37 @@ def test_local_slab_contexts_partition_the_operator_maps():
         D.close()
         ctx.close()
     np.testing.assert_allclose(total, g_full, rtol=1e-13, atol=1e-13)
+
+
+def test_mse_heldout_matches_oracle_and_is_u_shaped():
+    """kg_mse_heldout (path.cpp:91-126) on the device against the oracle, on the
+    reference's held-out workflow (test_path.cpp:195-237): held-out cells get
+    zero observation weight in the fit and the held-out SSE curve is U-shaped."""
+    rng = np.random.default_rng(76)
+    n1, n2 = 16, 14
+    X1 = K.bspline_design(np.arange(1.0, n1 + 1), 4, 10)
+    X2 = K.bspline_design(np.arange(1.0, n2 + 1), 4, 9)
+    design = [[X1, X2]]
+    i, j = np.meshgrid(np.arange(1, n1 + 1), np.arange(1, n2 + 1), indexing="ij")
+    truth = 3.0 * np.sin(2 * np.pi * i / 16.0) * np.cos(2 * np.pi * j / 14.0)
+    y = np.asfortranarray(truth + rng.standard_normal((n1, n2)))
+    mask = np.zeros(n1 * n2)
+    a = np.ones(n1 * n2)
+    mask[3::7] = 1.0
+    a[3::7] = 0.0
+    mask = np.asfortranarray(mask.reshape((n1, n2), order="F"))
+    a = np.asfortranarray(a.reshape((n1, n2), order="F"))
+    D = K.Design(design)
+    res = K.fit_path_resident(D, K.Observation(D, y, a), "gaussian", n_lambda=20, lambda_min_ratio=1e-5)
+    assert not res.truncated
+    got = K.mse_heldout(res, "gaussian", y, mask)
+    want = O.mse_heldout(design, "gaussian", [D.blocks(c) for c in res.coefs()], y, mask)
+    np.testing.assert_allclose(got["mse"], want["mse"], rtol=1e-12)
+    assert got["argmin"] == want["argmin"]
+    assert 0 < got["argmin"] < res.n_models - 1
+    with pytest.raises(ValueError):
+        K.mse_heldout(res, "gaussian", y, np.zeros_like(mask))
+    bad = mask.copy()
+    bad[0, 0] = 2.0
+    with pytest.raises(ValueError):
+        K.mse_heldout(res, "gaussian", y, bad)

@@ -515,3 +515,30 @@ def test_bspline_rows_and_counts():  # test_bspline.cpp, test_smoke.py:82-89, ac
         x = O.bspline_design(np.linspace(0, 1, n), 4, p)
         assert np.max((x != 0).sum(axis=1)) <= 4
         assert np.max(np.abs(x.sum(axis=1) - 1)) <= 1e-12
+
+
+def test_mse_heldout_known_answers():  # test_path.cpp:160-192
+    rng = np.random.default_rng(75)
+    design = H.make_design(rng, (4, 3), [(2, 2)])
+    y = rng.standard_normal((4, 3))
+    path = O.fit_path(design, "gaussian", y, n_lambda=5, lambda_min_ratio=0.05)
+    coefs = path["coefficients"]
+    with pytest.raises(ValueError):
+        O.mse_heldout(design, "gaussian", coefs, y, np.zeros((4, 3)))
+    mask = np.zeros(12)
+    mask[[3, 7]] = 1.0
+    mask = mask.reshape((4, 3), order="F")
+    truth = O.h_map(design, coefs[2])  # gaussian mean = eta
+    res = O.mse_heldout(design, "gaussian", coefs, truth, mask)
+    assert res["mse"][2] == 0.0 and res["argmin"] == 2
+    mask = np.zeros(12)
+    mask[5] = 1.0
+    mask = mask.reshape((4, 3), order="F")
+    res = O.mse_heldout(design, "gaussian", coefs, y, mask)
+    for t, c in enumerate(coefs):
+        mu = O.h_map(design, c).ravel(order="F")[5]
+        assert res["mse"][t] == pytest.approx((mu - y.ravel(order="F")[5]) ** 2, rel=1e-12)
+    bad = mask.copy()
+    bad[0, 0] = 0.5
+    with pytest.raises(ValueError):
+        O.mse_heldout(design, "gaussian", coefs, y, bad)
