@@ -216,6 +216,18 @@ void score0(const Launch& L, i64 n, int fam, double disp, const double* y, const
 void validate_pass(const Launch& L, i64 n, int fam, const double* y, const double* a, i64* err, i64 cell_base);
 void eta_combine(const Launch& L, i64 n, double t, const double* eta_t, double* eta);
 void mean_map(const Launch& L, i64 n, int fam, const double* eta, double* mu);
+// iwls = tensor (outer.cpp:53-103, design.cpp:126-151)
+struct TensorExt {
+  int d = 0;
+  i64 ext[4] = {1, 1, 1, 1};
+};
+void log_slab_sums(const Launch& L, const double* v, i64 a, i64 K, i64 b, double* S);
+void tensor_factors(const Launch& L, const double* S, const i64* ext_dev, int d, i64 n, double* f);
+void tensor_vz(const Launch& L, i64 n, const TensorExt& te, const double* f, const double* u, const double* eta,
+               double* v, double* z, double* vmax);
+void wgram_band(const Launch& L, const double* Xm, const double* Xr, i64 n, const double* w, const int* clo_m,
+                const int* clen_m, const int* clo_r, const int* clen_r, const BandOp& g, double* coef);
+void band_dense(const Launch& L, const BandOp& g, const double* coef, i64 p, double* G);
 // per-CTA (elem_grid(n)) partials of sum_{mask == 1} (mu - y)^2
 void masked_sse(const Launch& L, i64 n, const double* mu, const double* y, const double* mask, double* part);
 void fill(const Launch& L, i64 n, double v, double* x);

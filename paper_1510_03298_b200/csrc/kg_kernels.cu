@@ -644,6 +644,115 @@ void fista_update(const Launch& L, const FistaCtl* ctl, i64 p, int pen, double a
   bump(L);
 }
 
+// ---------------------------------------------- tensor weights (iwls = tensor)
+// compute_weights tensor branch (outer.cpp:53-103): slab sums of log v over
+// mode j, S[i] = sum over cells with i_j = i, for the array viewed as (a, K, b).
+__global__ void __launch_bounds__(NT) k_log_slab_sums(const double* v, i64 a, i64 K, i64 b, double* S) {
+  __shared__ double red[32];
+  const i64 i = blockIdx.x;
+  const i64 cnt = a * b;
+  double s = 0.0;
+  for (i64 e = threadIdx.x; e < cnt; e += NT) {
+    const i64 al = e % a, be = e / a;
+    s += log(v[al + a * (i + K * be)]);
+  }
+  const double r = block_reduce<false>(s, red);
+  if (threadIdx.x == 0) S[i] = r;
+}
+
+void log_slab_sums(const Launch& L, const double* v, i64 a, i64 K, i64 b, double* S) {
+  k_log_slab_sums<<<static_cast<unsigned>(K), NT, 0, L.s>>>(v, a, K, b, S);
+  bump(L);
+}
+
+// f_j[i] = exp(S_j[i] / m_j - log vbar + log vbar / d), log vbar = (sum of the
+// mode-0 slab sums) / n; S and f are the concatenation over modes.
+__global__ void k_tensor_factors(const double* S, const i64* ext, int d, i64 n, double* f) {
+  __shared__ double lvbar;
+  if (threadIdx.x == 0) {
+    double tot = 0.0;
+    for (i64 i = 0; i < ext[0]; ++i) tot += S[i];
+    lvbar = tot / static_cast<double>(n);
+  }
+  __syncthreads();
+  i64 off = 0;
+  for (int j = 0; j < d; ++j) {
+    const double mj = static_cast<double>(n / ext[j]);
+    for (i64 i = threadIdx.x; i < ext[j]; i += blockDim.x)
+      f[off + i] = exp(S[off + i] / mj - lvbar + lvbar / static_cast<double>(d));
+    off += ext[j];
+  }
+}
+
+void tensor_factors(const Launch& L, const double* S, const i64* ext_dev, int d, i64 n, double* f) {
+  k_tensor_factors<<<1, 256, 0, L.s>>>(S, ext_dev, d, n, f);
+  bump(L);
+}
+
+// v = outer product of the factors (prod = 1, *= f_0[i_0], ..., in mode order),
+// z = u / v + eta (generic working response, outer.cpp:148-155), max(v) partials.
+__global__ void __launch_bounds__(NT) k_tensor_vz(i64 n, TensorExt te, const double* f, const double* u,
+                                                  const double* eta, double* v, double* z, double* vmax) {
+  __shared__ double red[32];
+  double mx = -DBL_MAX;
+  for (i64 c = static_cast<i64>(blockIdx.x) * NT + threadIdx.x; c < n; c += static_cast<i64>(gridDim.x) * NT) {
+    i64 rest = c, off = 0;
+    double prod = 1.0;
+    for (int j = 0; j < te.d; ++j) {
+      const i64 ij = rest % te.ext[j];
+      rest /= te.ext[j];
+      prod *= f[off + ij];
+      off += te.ext[j];
+    }
+    v[c] = prod;
+    z[c] = u[c] / prod + eta[c];
+    mx = fmax(mx, prod);
+  }
+  const double r = block_reduce<true>(mx, red);
+  if (threadIdx.x == 0) vmax[blockIdx.x] = r;
+}
+
+void tensor_vz(const Launch& L, i64 n, const TensorExt& te, const double* f, const double* u, const double* eta,
+               double* v, double* z, double* vmax) {
+  k_tensor_vz<<<elem_grid(n), NT, 0, L.s>>>(n, te, f, u, eta, v, z, vmax);
+  bump(L);
+}
+
+// Weighted Gram band X_m^T diag(w) X_r (GramBlocks, design.cpp:126-151): for
+// band row a, entries b in [lo_a, lo_a + len_a): sum over the rows both columns
+// touch, ascending, of (X_m[i, a] w[i]) X_r[i, b].
+__global__ void k_wgram_band(const double* Xm, const double* Xr, i64 n, const double* w, const int* clo_m,
+                             const int* clen_m, const int* clo_r, const int* clen_r, BandOp g, double* coef) {
+  const int a = blockIdx.x;
+  const int lo = g.lo[a], len = g.len[a];
+  const i64 off = g.off[a];
+  for (int t = threadIdx.x; t < len; t += blockDim.x) {
+    const int b = lo + t;
+    const int i0 = max(clo_m[a], clo_r[b]), i1 = min(clo_m[a] + clen_m[a], clo_r[b] + clen_r[b]);
+    double s = 0.0;
+    for (int i = i0; i < i1; ++i) s += Xm[i + n * a] * w[i] * Xr[i + n * static_cast<i64>(b)];
+    coef[off + t] = s;
+  }
+}
+
+void wgram_band(const Launch& L, const double* Xm, const double* Xr, i64 n, const double* w, const int* clo_m,
+                const int* clen_m, const int* clo_r, const int* clen_r, const BandOp& g, double* coef) {
+  k_wgram_band<<<static_cast<unsigned>(g.rows), 64, 0, L.s>>>(Xm, Xr, n, w, clo_m, clen_m, clo_r, clen_r, g, coef);
+  bump(L);
+}
+
+// dense p x p copy of a band operator (power iteration input)
+__global__ void k_band_dense(BandOp g, const double* coef, i64 p, double* G) {
+  const int a = blockIdx.x;
+  for (int t = threadIdx.x; t < g.len[a]; t += blockDim.x) G[a + p * static_cast<i64>(g.lo[a] + t)] = coef[g.off[a] + t];
+}
+
+void band_dense(const Launch& L, const BandOp& g, const double* coef, i64 p, double* G) {
+  KG_CUDA(cudaMemsetAsync(G, 0, sizeof(double) * p * p, L.s));
+  k_band_dense<<<static_cast<unsigned>(g.rows), 64, 0, L.s>>>(g, coef, p, G);
+  bump(L);
+}
+
 // per-CTA partials of sum over mask == 1 of (mu - y)^2 (mse_heldout, path.cpp:111-119)
 __global__ void __launch_bounds__(NT) k_masked_sse(i64 n, const double* mu, const double* y, const double* mask,
                                                    double* part) {

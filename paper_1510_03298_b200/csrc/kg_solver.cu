@@ -267,6 +267,7 @@ struct SpectralJob {
   double immediate = -1.0;  // p == 1: |sum x^2| directly (spectral.cpp:14)
   DBuf G, glo, ghi, v0;
   int band = 0;
+  const double* Gview = nullptr;  // dense Gram owned elsewhere (tensor weights); p == 1: its single entry
 };
 
 static void spectral_prepare(kg_ctx* ctx, const FactorHost& h, FactorOwn& f, SpectralJob& J) {
@@ -325,6 +326,22 @@ static void spectral_prepare(kg_ctx* ctx, const FactorHost& h, FactorOwn& f, Spe
   gram(ctx->L(), f.dev, J.G.d(), static_cast<int*>(J.glo.p), static_cast<int*>(J.ghi.p));
 }
 
+static std::vector<double> spectral_run(kg_ctx* ctx, std::vector<std::unique_ptr<SpectralJob>>& jobs);
+
+// spectral_run over jobs whose Grams live in Gview (the 1 x 1 case reads its
+// device entry: spectral.cpp:14 returns |G|)
+static std::vector<double> spectral_run_views(kg_ctx* ctx, std::vector<std::unique_ptr<SpectralJob>>& jobs) {
+  for (auto& J : jobs) {
+    if (J->p == 1) {
+      double g = 0.0;
+      KG_CUDA(cudaMemcpyAsync(&g, J->Gview, sizeof(double), cudaMemcpyDeviceToHost, ctx->s));
+      sync(ctx);
+      J->immediate = std::abs(g);
+    }
+  }
+  return spectral_run(ctx, jobs);
+}
+
 static std::vector<double> spectral_run(kg_ctx* ctx, std::vector<std::unique_ptr<SpectralJob>>& jobs) {
   std::vector<PowerJob> pj;
   std::vector<size_t> idx;
@@ -334,7 +351,7 @@ static std::vector<double> spectral_run(kg_ctx* ctx, std::vector<std::unique_ptr
     if (J.immediate >= 0.0) continue;
     PowerJob q;
     q.p = J.p;
-    q.G = J.G.d();
+    q.G = J.Gview ? J.Gview : J.G.d();
     q.glo = static_cast<const int*>(J.glo.p);
     q.ghi = static_cast<const int*>(J.ghi.p);
     q.v0 = J.v0.d();
@@ -476,6 +493,15 @@ struct Fit {
   // route 0 on the fused design: objective sum v eta^2 - 2 <b, x> + sum v z^2
   // (FV_FISTA_EXP, z is not read per iteration); KG_ROUTE0_DIRECT=1 keeps sum v (eta - z)^2
   bool expand = false;
+  // iwls = tensor: the current outer iteration's weighted Gram blocks
+  // X_{m,j}^T diag(f_j) X_{r,j} (same band structure as design.gram) and the
+  // Lipschitz factor (prod_j rho(G_j(f_j)) for c = 1, max(v) L-hat otherwise)
+  bool tensor = false;
+  double lipfac_t = 0.0;
+  std::vector<BandOp> wg;             // [(m * c + r) * d + j]
+  std::vector<std::unique_ptr<DBuf>> wgcoef;
+  DBuf tS, tf, text, tdense;
+  std::vector<std::unique_ptr<SpectralJob>> tjobs;  // power iterations of the weighted Grams (c = 1)
   // d = 3, banded: modes 1 and 2 fused per last-mode slab (kg_slab.cu); opt-in with KG_SLAB=1
   // (experimental: parity-tested, slower than the fused-pass route so far)
   bool slab = false;
@@ -665,13 +691,21 @@ static int xwx_pass_local(Fit& F, const double* x, double* Sx) {
 // weight factors; the constant weight is applied as FistaCtl::sscale), then
 // per-CTA partials of wconst <x, S'x> - 2 <x, b> into F.part, so that
 // sum v (Xx - z)^2 = partials + sum v z^2 needs no n-space pass.
+// Gram block (m, r, j) of the current route-1 solve: the design's X^T X bands,
+// or this outer iteration's tensor-weighted ones.
+static const BandOp& gram_op(const Fit& F, i64 m, i64 r, i64 j) {
+  const kg_design& D = *F.D;
+  if (F.tensor) return F.wg[static_cast<size_t>((m * D.c + r) * D.d + j)];
+  return D.gram[m][r][j]->dev.H;
+}
+
 static int gram_pass(Fit& F, const double* x, double* Sx) {
   const kg_design& D = *F.D;
   kg_ctx* ctx = F.ctx;
   for (i64 m = 0; m < D.c; ++m)
     for (i64 r = 0; r < D.c; ++r) {
       std::vector<Step> st;
-      for (i64 j = D.d - 1; j >= 0; --j) st.push_back({static_cast<int>(j), &D.gram[m][r][j]->dev.H, D.p[m][j]});
+      for (i64 j = D.d - 1; j >= 0; --j) st.push_back({static_cast<int>(j), &gram_op(F, m, r, j), D.p[m][j]});
       run_chain(ctx, D.p[r], st, x + D.offs[r], Sx + D.offs[m], F.s0.d(), F.s1.d(), r > 0);
     }
   gram_dots(ctx->L(), F.p, F.wconst, x, Sx, F.b.d(), F.part.d());
@@ -752,12 +786,12 @@ static GramStepArgs gstep_args(Fit& F) {
   uint32_t before = 1;
   for (i64 j = 0; j + 1 < D.d; ++j) {
     A.dims[j] = static_cast<int>(D.p[0][j]);
-    A.G[j] = D.gram[0][0][j]->dev.H;
+    A.G[j] = gram_op(F, 0, 0, j);
     A.fa[j] = FastDiv(before);
     A.fk[j] = FastDiv(static_cast<uint32_t>(D.p[0][j]));
     before *= static_cast<uint32_t>(D.p[0][j]);
   }
-  A.Gd = D.gram[0][0][D.d - 1]->dev.H;
+  A.Gd = gram_op(F, 0, 0, D.d - 1);
   A.X[0] = F.x.d();
   A.S[0] = F.Sx.d();
   A.b = F.b.d();
@@ -870,6 +904,11 @@ struct InnerCfg {
 // The result lands in F.best; the control block is copied to ctx->pin() + PIN_CTL.
 static void fista_enqueue(Fit& F, double lambda, const InnerCfg& ic, const double* vmax_part, int n_vmax) {
   kg_ctx* ctx = F.ctx;
+  if (F.tensor && F.D->c == 1) {  // lipschitz_tensor_exact carries no max(v): unit weight scale
+    fill(ctx->L(), 1, 1.0, F.scal.d() + 60);
+    vmax_part = F.scal.d() + 60;
+    n_vmax = 1;
+  }
   if (sharded(ctx)) {  // max(v) over all slabs (lipschitz_upper)
     reduce_cols(ctx->L(), vmax_part, n_vmax, 1, 1, F.scal.d() + 56);
     ar_max(ctx, F.scal.d() + 56, 1);
@@ -884,7 +923,7 @@ static void fista_enqueue(Fit& F, double lambda, const InnerCfg& ic, const doubl
   h.tol = ic.tol;
   h.nu = ic.nu;
   h.n = static_cast<double>(F.D->N_full);
-  h.lipfac = F.D->lipfac;
+  h.lipfac = F.tensor ? F.lipfac_t : F.D->lipfac;
   h.max_iters = ic.max_iters;
   h.monitor_every = ic.monitor_every;
   h.sscale = F.route == 1 ? F.wconst : 1.0;
@@ -1183,6 +1222,132 @@ static ModelTrace gaussian_step(Fit& F, double lambda, const OuterCfg& oc, PathS
 }
 
 // General outer loop (outer.cpp:233-302) for exact / unit weights.
+// iwls = tensor for one outer iteration (outer.cpp:256-263 with
+// compute_weights' tensor branch, outer.cpp:53-103): F.v holds the exact GLM
+// weights and F.u the score on entry.  Leaves the rank-one weights in F.v,
+// z = u / v + eta in F.z, the weighted Gram blocks in F.wg and the Lipschitz
+// factor in F.lipfac_t (lipschitz_tensor_exact for c = 1, inner.cpp:73-91;
+// lipschitz_upper otherwise), and switches the fit to the Gram route.
+static void tensor_weights(Fit& F, double* vmax_part, int n_vmax) {
+  kg_ctx* ctx = F.ctx;
+  const kg_design& D = *F.D;
+  if (sharded(ctx)) throw Error(E_INVAL, "iwls=tensor is not supported on a sharded context");
+  if (D.d > 4) throw Error(E_INVAL, "iwls=tensor supports up to 4 modes on the device");
+  const int d = static_cast<int>(D.d);
+  i64 next = 0;
+  for (int j = 0; j < d; ++j) next += D.n[j];
+  if (!F.tS.p) {  // per-fit state, built on the first outer iteration
+    F.tS.alloc(sizeof(double) * next);
+    F.tf.alloc(sizeof(double) * next);
+    F.text.alloc(sizeof(i64) * d);
+    std::vector<i64> ext(D.n.begin(), D.n.end());
+    KG_CUDA(cudaMemcpyAsync(F.text.p, ext.data(), sizeof(i64) * d, cudaMemcpyHostToDevice, ctx->s));
+    for (i64 m = 0; m < D.c; ++m)
+      for (i64 r = 0; r < D.c; ++r)
+        for (i64 j = 0; j < D.d; ++j) {
+          const FactorOwn& g = *D.gram[m][r][j];
+          i64 cnt = 0;
+          for (size_t a = 0; a < g.h_len.size(); ++a) cnt += g.h_len[a];
+          auto c = std::make_unique<DBuf>();
+          c->alloc(sizeof(double) * std::max<i64>(cnt, 1));
+          BandOp op = g.dev.H;
+          op.coef = c->d();
+          F.wg.push_back(op);
+          F.wgcoef.push_back(std::move(c));
+        }
+    if (D.c == 1) {
+      i64 pmax = 1;
+      for (int j = 0; j < d; ++j) pmax = std::max(pmax, D.p[0][j]);
+      F.tdense.alloc(sizeof(double) * pmax * pmax * d);
+      for (int j = 0; j < d; ++j) {  // power-iteration jobs: band, seeded start (spectral.cpp:16-24)
+        const FactorOwn& g = *D.gram[0][0][j];
+        const i64 p = D.p[0][j];
+        auto J = std::make_unique<SpectralJob>();
+        J->p = p;
+        std::vector<int> glo(g.h_lo.begin(), g.h_lo.end()), ghi(static_cast<size_t>(p));
+        int band = 0;
+        for (i64 a = 0; a < p; ++a) {
+          ghi[a] = glo[a] + g.h_len[a];
+          band = std::max(band, g.h_len[a]);
+        }
+        J->band = band;
+        if (p == 1) {
+          F.tjobs.push_back(std::move(J));
+          continue;
+        }
+        std::mt19937_64 rng(0x9e3779b97f4a7c15ull);
+        std::uniform_real_distribution<double> unif(0.5, 1.5);
+        std::vector<double> v0(static_cast<size_t>(p));
+        for (auto& x : v0) x = unif(rng);
+        double z = 0.0;
+        for (double x : v0) z += x * x;
+        if (z > 0.0) {
+          const double sq = std::sqrt(z);
+          for (double& x : v0) x /= sq;
+        }
+        J->glo.alloc(sizeof(int) * p);
+        J->ghi.alloc(sizeof(int) * p);
+        J->v0.alloc(sizeof(double) * p);
+        KG_CUDA(cudaMemcpyAsync(J->glo.p, glo.data(), sizeof(int) * p, cudaMemcpyHostToDevice, ctx->s));
+        KG_CUDA(cudaMemcpyAsync(J->ghi.p, ghi.data(), sizeof(int) * p, cudaMemcpyHostToDevice, ctx->s));
+        KG_CUDA(cudaMemcpyAsync(J->v0.p, v0.data(), sizeof(double) * p, cudaMemcpyHostToDevice, ctx->s));
+        F.tjobs.push_back(std::move(J));
+      }
+    }
+  }
+  // geometric-mean factors of the exact weights, then v, z and max(v)
+  i64 off = 0;
+  for (int j = 0; j < d; ++j) {
+    const i64 a = prod(D.n, 0, j), b = prod(D.n, j + 1, d);
+    log_slab_sums(ctx->L(), F.v.d(), a, D.n[j], b, F.tS.d() + off);
+    off += D.n[j];
+  }
+  tensor_factors(ctx->L(), F.tS.d(), static_cast<const i64*>(F.text.p), d, F.n, F.tf.d());
+  TensorExt te;
+  te.d = d;
+  for (int j = 0; j < d; ++j) te.ext[j] = D.n[j];
+  tensor_vz(ctx->L(), F.n, te, F.tf.d(), F.u.d(), F.eta.d(), F.v.d(), F.z.d(), vmax_part);
+  // weighted Gram blocks
+  for (i64 m = 0; m < D.c; ++m)
+    for (i64 r = 0; r < D.c; ++r) {
+      i64 fo = 0;
+      for (i64 j = 0; j < D.d; ++j) {
+        const FactorDev& xm = D.f[m][j]->dev;
+        const FactorDev& xr = D.f[r][j]->dev;
+        const size_t idx = static_cast<size_t>((m * D.c + r) * D.d + j);
+        wgram_band(ctx->L(), xm.X, xr.X, D.n[j], F.tf.d() + fo, xm.G.lo, xm.G.len, xr.G.lo, xr.G.len, F.wg[idx],
+                   F.wgcoef[idx]->d());
+        fo += D.n[j];
+      }
+    }
+  // Lipschitz factor
+  if (D.c == 1) {
+    i64 pmax = 1;
+    for (int j = 0; j < d; ++j) pmax = std::max(pmax, D.p[0][j]);
+    for (int j = 0; j < d; ++j) {
+      SpectralJob& J = *F.tjobs[static_cast<size_t>(j)];
+      double* G = F.tdense.d() + pmax * pmax * j;
+      if (J.p == 1) {  // spectral.cpp:14: the 1 x 1 Gram itself
+        J.Gview = F.wgcoef[static_cast<size_t>(j)]->d();
+      } else {
+        band_dense(ctx->L(), F.wg[static_cast<size_t>(j)], F.wgcoef[static_cast<size_t>(j)]->d(), J.p, G);
+        J.Gview = G;
+      }
+    }
+    double lip = 1.0;
+    std::vector<double> rad = spectral_run_views(ctx, F.tjobs);
+    for (double r0 : rad) lip *= r0;
+    F.lipfac_t = lip;
+  } else {
+    F.lipfac_t = D.lipfac;  // lipschitz_upper: max(v) enters through the vmax partials (k_fista_init)
+  }
+  F.tensor = true;
+  F.route = 1;
+  F.wconst = 1.0;
+  F.c0_valid = false;
+  F.zptr = F.z.d();
+}
+
 static ModelTrace outer_loop(Fit& F, double lambda, const OuterCfg& oc) {
   kg_ctx* ctx = F.ctx;
   const kg_design& D = *F.D;
@@ -1235,6 +1400,8 @@ static ModelTrace outer_loop(Fit& F, double lambda, const OuterCfg& oc) {
     F.wconst = 1.0;
     F.c0_valid = false;
     F.zptr = F.z.d();
+    F.tensor = false;
+    if (oc.wmode == KG_W_TENSOR) tensor_weights(F, vmax_part, n_vmax);  // rank-one weights, Gram route
     xtwz_pass(F);
     fista_enqueue(F, lambda, oc.inner, vmax_part, n_vmax);
     // eta_tilde = H(theta_tilde) with Delta_k's inner product and the first trials.
@@ -1422,8 +1589,6 @@ static kg_path_result* fit_path(kg_ctx* ctx, const kg_design* D, const kg_obs* O
   if (!(oc.alpha0 > 0.0) || !(oc.b > 0.0 && oc.b < 1.0) || !(oc.v > 0.0 && oc.v < 1.0))
     throw Error(E_INVAL, "outer_solve: need alpha0 > 0 and Armijo constants b, v in (0,1)");
   if (oc.max_outer < 1 || !(oc.tol > 0.0)) throw Error(E_INVAL, "outer_solve: need max_outer >= 1 and outer_tol > 0");
-  if (oc.wmode == KG_W_TENSOR)
-    throw Error(E_INVAL, "iwls=tensor (tensor-approximated weights) is not implemented by the device solver");
   if (lambdas_in) validate_obs(*F);
 
   const i64 nl = static_cast<i64>(lambdas.size());

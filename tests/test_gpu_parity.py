@@ -452,3 +452,30 @@ def test_mse_heldout_matches_oracle_and_is_u_shaped():
     bad[0, 0] = 2.0
     with pytest.raises(ValueError):
         K.mse_heldout(res, "gaussian", y, bad)
+
+
+@pytest.mark.parametrize("case", ["poisson_c1", "binomial_2d", "two_component"])
+def test_tensor_weights_match_oracle(case):
+    """iwls = "tensor" (compute_weights' geometric-mean factors, GramBlocks,
+    xtwx_apply_tensor, lipschitz_tensor_exact; outer.cpp:53-103,
+    design.cpp:126-177, inner.cpp:73-91) against the oracle."""
+    rng = np.random.default_rng(31)
+    if case == "poisson_c1":
+        design = bspline_design((18, 14, 10), (6, 5, 4))
+        B = np.zeros((6, 5, 4))
+        m = rng.random(B.shape) < 0.3
+        B[m] = rng.standard_normal(m.sum())
+        eta = configs.tensor_h(design[0], B)
+        y = rng.poisson(np.exp(np.log(12.0) / eta.max() * eta)).astype(float)
+        fam = "poisson"
+    elif case == "binomial_2d":
+        design = bspline_design((20, 18), (7, 6))
+        y = H.random_data(rng, "binomial", (20, 18))
+        fam = "binomial"
+    else:
+        design = H.make_design(rng, (6, 5, 4), [(3, 2, 2), (2, 2, 2)])
+        eta = O.h_map(design, H.random_coef(rng, design, -0.5, 0.5))
+        y = rng.poisson(np.exp(0.4 * eta)).astype(float)
+        fam = "poisson"
+    kw = dict(n_lambda=6, lambda_min_ratio=1e-2, iwls="tensor")
+    compare_paths(K.fit_path(design, fam, y, **kw), O.fit_path(design, fam, y, **kw))
