@@ -239,6 +239,12 @@ void fista_update(const Launch& L, const FistaCtl* ctl, i64 p, int pen, double a
                   double* Sx, double* Sxp, const double* b, double* best, double* Sbest, double* Jpart,
                   double* bxpart = nullptr);
 void pdot(const Launch& L, i64 p, const double* a, const double* b, double* part);
+// nu = 0 (backtracking every iteration, inner.cpp:169-183), per-CTA partials
+void bt_prep(const Launch& L, i64 p, double omega, double sscale, double n, const double* x, const double* xp,
+             const double* Sx, const double* Sxp, const double* b, double* y, double* grad, double* part);
+void bt_trial(const Launch& L, i64 p, double delta, double lambda, int pen, double alpha, const double* y,
+              const double* grad, double* cand, double* part);
+void bt_dots(const Launch& L, i64 p, const double* x, const double* Sx, const double* b, double* part);
 void pnorm(const Launch& L, i64 p, int pen, double alpha, const double* x, double* Jpart);
 // cols: 0 = J(th_t); 1 + j = J(th + t_j (th_t - th))
 void ptrials(const Launch& L, i64 p, int pen, double alpha, const double* th, const double* th_t, int ntrial,

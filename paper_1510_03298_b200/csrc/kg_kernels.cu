@@ -772,6 +772,92 @@ void masked_sse(const Launch& L, i64 n, const double* mu, const double* y, const
   bump(L);
 }
 
+// ------------------------------------------ nu = 0 (backtracking every step)
+// inner.cpp:162-183: y = x + omega (x - x_prev), S y by linearity, grad =
+// (s S y - b) / n; partials [<y, S y>, <b, y>] for h(y).
+__global__ void __launch_bounds__(NT) k_bt_prep(i64 p, double omega, double sscale, double n, const double* x,
+                                                const double* xp, const double* Sx, const double* Sxp,
+                                                const double* b, double* y, double* grad, double* part) {
+  __shared__ double red[32];
+  double a0 = 0.0, a1 = 0.0;
+  for (i64 i = static_cast<i64>(blockIdx.x) * NT + threadIdx.x; i < p; i += static_cast<i64>(gridDim.x) * NT) {
+    const double yi = x[i] + omega * (x[i] - xp[i]);
+    const double syi = Sx[i] + omega * (Sx[i] - Sxp[i]);
+    y[i] = yi;
+    grad[i] = (sscale * syi - b[i]) / n;
+    a0 = fma(yi, syi, a0);
+    a1 = fma(b[i], yi, a1);
+  }
+  const double r0 = block_reduce<false>(a0, red);
+  const double r1 = block_reduce<false>(a1, red);
+  if (threadIdx.x == 0) {
+    part[2 * blockIdx.x] = r0;
+    part[2 * blockIdx.x + 1] = r1;
+  }
+}
+
+void bt_prep(const Launch& L, i64 p, double omega, double sscale, double n, const double* x, const double* xp,
+             const double* Sx, const double* Sxp, const double* b, double* y, double* grad, double* part) {
+  k_bt_prep<<<pgrid(p), NT, 0, L.s>>>(p, omega, sscale, n, x, xp, Sx, Sxp, b, y, grad, part);
+  bump(L);
+}
+
+// one trial: cand = prox(y - delta grad); partials [<grad, step>, |step|^2,
+// l1(cand), l2(cand)] with step = cand - y.
+__global__ void __launch_bounds__(NT) k_bt_trial(i64 p, double delta, double lambda, int pen, double alpha,
+                                                 const double* y, const double* grad, double* cand, double* part) {
+  __shared__ double red[32];
+  double a0 = 0.0, a1 = 0.0, l1 = 0.0, l2 = 0.0;
+  const double gamma = delta * lambda;
+  for (i64 i = static_cast<i64>(blockIdx.x) * NT + threadIdx.x; i < p; i += static_cast<i64>(gridDim.x) * NT) {
+    double c = y[i] - delta * grad[i];
+    if (lambda > 0.0) c = prox1(pen, alpha, gamma, c);
+    cand[i] = c;
+    const double st = c - y[i];
+    a0 = fma(grad[i], st, a0);
+    a1 = fma(st, st, a1);
+    jacc(c, l1, l2);
+  }
+  const double r0 = block_reduce<false>(a0, red);
+  const double r1 = block_reduce<false>(a1, red);
+  const double r2 = block_reduce<false>(l1, red);
+  const double r3 = block_reduce<false>(l2, red);
+  if (threadIdx.x == 0) {
+    part[4 * blockIdx.x] = r0;
+    part[4 * blockIdx.x + 1] = r1;
+    part[4 * blockIdx.x + 2] = r2;
+    part[4 * blockIdx.x + 3] = r3;
+  }
+}
+
+void bt_trial(const Launch& L, i64 p, double delta, double lambda, int pen, double alpha, const double* y,
+              const double* grad, double* cand, double* part) {
+  k_bt_trial<<<pgrid(p), NT, 0, L.s>>>(p, delta, lambda, pen, alpha, y, grad, cand, part);
+  bump(L);
+}
+
+// partials [<x, S x>, <b, x>] (h(x) = (s <x, S x> - 2 <b, x> + sum v z^2) / 2n)
+__global__ void __launch_bounds__(NT) k_bt_dots(i64 p, const double* x, const double* Sx, const double* b,
+                                                double* part) {
+  __shared__ double red[32];
+  double a0 = 0.0, a1 = 0.0;
+  for (i64 i = static_cast<i64>(blockIdx.x) * NT + threadIdx.x; i < p; i += static_cast<i64>(gridDim.x) * NT) {
+    a0 = fma(x[i], Sx[i], a0);
+    a1 = fma(b[i], x[i], a1);
+  }
+  const double r0 = block_reduce<false>(a0, red);
+  const double r1 = block_reduce<false>(a1, red);
+  if (threadIdx.x == 0) {
+    part[2 * blockIdx.x] = r0;
+    part[2 * blockIdx.x + 1] = r1;
+  }
+}
+
+void bt_dots(const Launch& L, i64 p, const double* x, const double* Sx, const double* b, double* part) {
+  k_bt_dots<<<pgrid(p), NT, 0, L.s>>>(p, x, Sx, b, part);
+  bump(L);
+}
+
 // per-CTA partials of <a, b> (p-space)
 __global__ void __launch_bounds__(NT) k_pdot(i64 p, const double* a, const double* b, double* part) {
   __shared__ double red[32];

@@ -498,6 +498,7 @@ struct Fit {
   // Lipschitz factor (prod_j rho(G_j(f_j)) for c = 1, max(v) L-hat otherwise)
   bool tensor = false;
   double lipfac_t = 0.0;
+  DBuf bt_y, bt_g, bt_c, bt_sc, bt_part;  // nu = 0: y, grad, candidate, S(candidate), partials
   std::vector<BandOp> wg;             // [(m * c + r) * d + j]
   std::vector<std::unique_ptr<DBuf>> wgcoef;
   DBuf tS, tf, text, tdense;
@@ -898,6 +899,124 @@ struct InnerCfg {
   int extrapolation = 0;
 };
 
+static int step_pass(Fit& F, const double* x, double* Sx);
+static double penalty_of(int pen, double alpha, double l1, double l2);
+
+// fista_solve with nu = 0 (inner.cpp:162-235, backtracking every iteration),
+// driven from the host: delta starts at 1 and is halved until the
+// majorization test holds; every quadratic is h(x) = (s <x, S x> - 2 <b, x> +
+// sum v z^2) / 2n with S x from the route's X^T W X pass (the accepted
+// candidate's S x is reused), so a trial costs one pass.  Results as the
+// other paths: F.best / F.Sbest and the control block at PIN_CTL.
+static void fista_bt0(Fit& F, double lambda, const InnerCfg& ic, const double* vmax_part, int n_vmax) {
+  kg_ctx* ctx = F.ctx;
+  const kg_design& D = *F.D;
+  const i64 p = F.p;
+  const double n = static_cast<double>(D.N_full);
+  const double sscale = F.route == 1 ? F.wconst : 1.0;
+  const size_t pb = sizeof(double) * static_cast<size_t>(p);
+  for (DBuf* b : {&F.bt_y, &F.bt_g, &F.bt_c, &F.bt_sc}) b->alloc(pb);
+  F.bt_part.alloc(sizeof(double) * 4 * pgrid(p));
+  double* pin = ctx->pin();
+  double* sc = F.scal.d();
+  auto rd = [&](const double* dev, int k) {  // read k device scalars into pin[20 ..)
+    KG_CUDA(cudaMemcpyAsync(pin + 20, dev, sizeof(double) * k, cudaMemcpyDeviceToHost, ctx->s));
+    sync(ctx);
+  };
+  if (!F.c0_valid) {  // sum v z^2
+    wzz(ctx->L(), F.n, F.v.d(), F.zptr, F.part.d());
+    reduce_cols(ctx->L(), F.part.d(), elem_grid(F.n), 1, 0, sc + 48);
+    ar_sum(ctx, sc + 48, 1);
+    F.c0_valid = true;
+  }
+  rd(sc + 48, 1);
+  const double c0 = pin[20];
+  reduce_cols(ctx->L(), vmax_part, n_vmax, 1, 1, sc + 56);  // lipschitz_upper / tensor_exact (reported)
+  ar_max(ctx, sc + 56, 1);
+  rd(sc + 56, 1);
+  const double wmax = (F.tensor && D.c == 1) ? 1.0 : pin[20];
+  FistaCtl out{};
+  out.lip = wmax * (F.tensor ? F.lipfac_t : D.lipfac) / n;
+  out.bad_weights = !(wmax > 0.0);
+  if (out.bad_weights) {
+    std::memcpy(pin + PIN_CTL, &out, sizeof(out));
+    return;
+  }
+  auto J = [&](double l1, double l2) { return penalty_of(F.pen, F.alpha, l1, l2); };
+  // x_0 = theta
+  pcopy(ctx->L(), p, F.theta.d(), F.x.d(), F.xp.d(), F.best.d());
+  step_pass(F, F.x.d(), F.Sx.d());
+  pcopy(ctx->L(), p, F.Sx.d(), F.Sxp.d(), F.Sbest.d(), nullptr);
+  bt_dots(ctx->L(), p, F.x.d(), F.Sx.d(), F.b.d(), F.bt_part.d());
+  reduce_cols(ctx->L(), F.bt_part.d(), pgrid(p), 2, 0, sc + 24);
+  pnorm(ctx->L(), p, F.pen, F.alpha, F.x.d(), F.Jpart.d());
+  reduce_cols(ctx->L(), F.Jpart.d(), pgrid(p), 2, 0, sc + 26);
+  rd(sc + 24, 4);
+  double g_prev = 0.5 * (sscale * pin[20] - 2.0 * pin[21] + c0) / n + lambda * J(pin[22], pin[23]);
+  double best_g = g_prev, delta = 1.0;
+  i64 momentum = 1;
+  const i64 me = ic.monitor_every < 1 ? 1 : ic.monitor_every;
+  for (i64 it = 1; it <= ic.max_iters; ++it) {
+    const double omega =
+        ic.extrapolation == 0 ? static_cast<double>(momentum - 1) / static_cast<double>(momentum + 2) : 0.0;
+    bt_prep(ctx->L(), p, omega, sscale, n, F.x.d(), F.xp.d(), F.Sx.d(), F.Sxp.d(), F.b.d(), F.bt_y.d(), F.bt_g.d(),
+            F.bt_part.d());
+    reduce_cols(ctx->L(), F.bt_part.d(), pgrid(p), 2, 0, sc + 24);
+    rd(sc + 24, 2);
+    const double h_y = 0.5 * (sscale * pin[20] - 2.0 * pin[21] + c0) / n;
+    double h_c = 0.0, l1c = 0.0, l2c = 0.0;
+    for (;;) {  // inner.cpp:170-183
+      bt_trial(ctx->L(), p, delta, lambda, F.pen, F.alpha, F.bt_y.d(), F.bt_g.d(), F.bt_c.d(), F.bt_part.d());
+      reduce_cols(ctx->L(), F.bt_part.d(), pgrid(p), 4, 0, sc + 24);
+      step_pass(F, F.bt_c.d(), F.bt_sc.d());
+      bt_dots(ctx->L(), p, F.bt_c.d(), F.bt_sc.d(), F.b.d(), F.bt_part.d());
+      reduce_cols(ctx->L(), F.bt_part.d(), pgrid(p), 2, 0, sc + 28);
+      rd(sc + 24, 6);
+      const double gstep = pin[20], ss = pin[21];
+      l1c = pin[22];
+      l2c = pin[23];
+      h_c = 0.5 * (sscale * pin[24] - 2.0 * pin[25] + c0) / n;
+      const double bound = h_y + gstep + ss / (2.0 * delta) + 1e-12 * std::max(1.0, std::abs(h_y));
+      if (h_c <= bound) break;
+      delta *= 0.5;
+      ++out.backtracks;
+      if (delta < 1e-300) {  // DivergenceError("stepsize underflow in backtracking")
+        out.diverged = 1;
+        out.iterations = it;
+        out.best_g = best_g;
+        std::memcpy(pin + PIN_CTL, &out, sizeof(out));
+        return;
+      }
+    }
+    // x_prev = x, x = cand (S as well)
+    KG_CUDA(cudaMemcpyAsync(F.xp.p, F.x.p, pb, cudaMemcpyDeviceToDevice, ctx->s));
+    KG_CUDA(cudaMemcpyAsync(F.x.p, F.bt_c.p, pb, cudaMemcpyDeviceToDevice, ctx->s));
+    KG_CUDA(cudaMemcpyAsync(F.Sxp.p, F.Sx.p, pb, cudaMemcpyDeviceToDevice, ctx->s));
+    KG_CUDA(cudaMemcpyAsync(F.Sx.p, F.bt_sc.p, pb, cudaMemcpyDeviceToDevice, ctx->s));
+    ++momentum;
+    out.prox_steps += 1;
+    out.iterations = it;
+    if (!(it % me == 0 || it == ic.max_iters)) continue;
+    const double g_cur = h_c + lambda * J(l1c, l2c);
+    if (!std::isfinite(g_cur)) {  // DivergenceError("non-finite inner objective")
+      out.diverged = 1;
+      break;
+    }
+    if (g_cur <= best_g) {
+      pcopy(ctx->L(), p, F.x.d(), F.best.d(), nullptr, nullptr);
+      pcopy(ctx->L(), p, F.Sx.d(), F.Sbest.d(), nullptr, nullptr);
+      best_g = g_cur;
+    }
+    if (std::abs(g_cur - g_prev) / std::max(1.0, std::abs(g_cur)) < ic.tol) {
+      out.converged = 1;
+      break;
+    }
+    g_prev = g_cur;
+  }
+  out.best_g = best_g;
+  std::memcpy(pin + PIN_CTL, &out, sizeof(out));
+}
+
 // Enqueues fista_solve(init = theta) with weights F.v (max-partials in
 // vmax_part) and working response F.zptr; F.b must hold X^T(v.*z) and, on the
 // Gram route (F.route == 1), F.wconst / F.c0 the constant weight and sum v z^2.
@@ -916,8 +1035,10 @@ static void fista_enqueue(Fit& F, double lambda, const InnerCfg& ic, const doubl
     n_vmax = 1;
   }
   if (!(ic.nu >= 0.0 && ic.nu <= 1.0)) throw Error(E_INVAL, "fista_solve: nu must lie in [0,1]");
-  if (ic.nu == 0.0)
-    throw Error(E_INVAL, "fista_solve: nu = 0 (backtracking every iteration) is not supported by the device solver");
+  if (ic.nu == 0.0) {  // backtracking every iteration: host-driven trials
+    fista_bt0(F, lambda, ic, vmax_part, n_vmax);
+    return;
+  }
   FistaCtl h{};
   h.lambda = lambda;
   h.tol = ic.tol;
@@ -1637,12 +1758,10 @@ static kg_path_result* fit_path(kg_ctx* ctx, const kg_design* D, const kg_obs* O
     st.ll = pin[0] / disp;
   }
   // Gaussian, constant weights, one component: the whole path in one cooperative launch
-  if (gauss_shortcut && F->route == 1 && F->gstep && !host_loop_mode() && oc.inner.max_iters >= 1 &&
+  if (gauss_shortcut && F->route == 1 && F->gstep && !host_loop_mode() && oc.inner.max_iters >= 1 && oc.inner.nu != 0.0 &&
       std::getenv("KG_NO_DEVICE_PATH") == nullptr && gauss_path_ok(gstep_args(*F))) {
     if (!(F->wconst > 0.0)) throw Error(E_INVAL, "lipschitz_upper: weights must not be all zero");
     if (!(oc.inner.nu >= 0.0 && oc.inner.nu <= 1.0)) throw Error(E_INVAL, "fista_solve: nu must lie in [0,1]");
-    if (oc.inner.nu == 0.0)
-      throw Error(E_INVAL, "fista_solve: nu = 0 (backtracking every iteration) is not supported by the device solver");
     FistaCtl h{};
     h.tol = oc.inner.tol;
     h.nu = oc.inner.nu;

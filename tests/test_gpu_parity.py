@@ -176,6 +176,7 @@ GAUSS_CASES = {
     "masked_weights": dict(weights="masked", n_lambda=6),
     "nu_half": dict(nu=0.5, n_lambda=6),
     "inner_maxit": dict(n_lambda=6, inner_maxit=7),
+    "nu_zero": dict(nu=0.0, n_lambda=6),  # backtracking every iteration (inner.cpp:169-183)
 }
 
 
@@ -190,7 +191,7 @@ def test_gaussian_options_match_oracle(case):
     compare_paths(K.fit_path(design, "gaussian", y, **kw), O.fit_path(design, "gaussian", y, **kw))
 
 
-@pytest.mark.parametrize("case", ["unit", "masked_weights"])
+@pytest.mark.parametrize("case", ["unit", "masked_weights", "nu_zero"])
 def test_poisson_options_match_oracle(case):
     rng = np.random.default_rng(73)
     design = bspline_design((16, 14, 6), (6, 5, 4))
@@ -198,6 +199,8 @@ def test_poisson_options_match_oracle(case):
     kw = dict(n_lambda=5, lambda_min_ratio=1e-2)
     if case == "unit":
         kw["iwls"] = "unit"
+    elif case == "nu_zero":
+        kw["nu"] = 0.0
     else:
         kw["weights"] = _masked_weights(yp.shape)
     compare_paths(K.fit_path(design, "poisson", yp, **kw), O.fit_path(design, "poisson", yp, **kw))
