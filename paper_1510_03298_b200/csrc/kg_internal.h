@@ -311,6 +311,25 @@ bool fista_persist_ok(const GramStepArgs& A);
 void fista_persist(const Launch& L, const PersistArgs& P);
 bool gauss_path_ok(const GramStepArgs& A);
 void gauss_path(const Launch& L, const PersistArgs& P);
+
+// Persistent cooperative n-space FISTA loop (route 0, d = 3, c = 1, nu = 1):
+// every phase of a step (update, H mode 3, H mode 2, fused mode-1 pass with
+// v, G mode 2, G mode 3) as a grid-stride loop between grid barriers, the
+// monitor replicated in every CTA.  For problems whose arrays sit in L2 (C3).
+struct NPersistArgs {
+  FistaCtl* ctl = nullptr;     // initialised (k_fista_init); state written back at exit
+  int n1 = 0, n2 = 0, n3 = 0, p1 = 0, p2 = 0, p3 = 0;
+  BandOp H1, G1, H2, G2, H3, G3;  // rows of X_j (H) and of X_j^T (G)
+  double *x = nullptr, *xp = nullptr, *Sx = nullptr, *Sxp = nullptr, *best = nullptr, *Sbest = nullptr;
+  const double* b = nullptr;   // X^T (v z)
+  const double* v = nullptr;   // n-array weights
+  double *A1 = nullptr, *P = nullptr, *Q = nullptr, *B1 = nullptr;  // p1p2n3, p1n2n3, p1n2n3, p1p2n3
+  double* part = nullptr;      // 4 per CTA: l1, l2, <b, x>, sum v eta^2
+  unsigned* bar = nullptr;     // grid barrier {count, generation}
+  int dbg = 0;                 // KG_NP_DBG=1: phase clocks of CTA 0
+};
+bool npersist_ok(const NPersistArgs& A, int* grid);
+void npersist(const Launch& L, const NPersistArgs& A, int grid);
 int gauss_dots(const Launch& L, i64 p, double w, const double* th, const double* Sth, const double* bt,
                const double* Sbt, const double* b, double* part);
 

@@ -499,6 +499,7 @@ struct Fit {
   bool tensor = false;
   double lipfac_t = 0.0;
   DBuf bt_y, bt_g, bt_c, bt_sc, bt_part;  // nu = 0: y, grad, candidate, S(candidate), partials
+  DBuf nppart, npbar;                     // persistent n-space loop (k_nspace_persist)
   std::vector<BandOp> wg;             // [(m * c + r) * d + j]
   std::vector<std::unique_ptr<DBuf>> wgcoef;
   DBuf tS, tf, text, tdense;
@@ -1099,7 +1100,54 @@ static void fista_enqueue(Fit& F, double lambda, const InnerCfg& ic, const doubl
     fista_init(ctx->L(), static_cast<FistaCtl*>(F.ctl.p), F.part.d(), n_ss, F.Jpart.d(), pgrid(F.p), vmax_part,
                n_vmax, 0, ex ? F.bxpart.d() : nullptr, pgrid(F.p));
   }
-  if (ic.max_iters >= 1) {
+  // small d = 3 n-space problems: the whole loop in one cooperative launch (experimental)
+  const kg_design& Dd = *F.D;
+  // opt-in (KG_NPERSIST=1): parity-tested, slower than the graph route so far
+  const char* npe = std::getenv("KG_NPERSIST");
+  const bool np_on = npe != nullptr && npe[0] == '1';
+  int np_grid = 0;
+  NPersistArgs NA;
+  const bool np = np_on && ic.max_iters >= 1 && F.route == 0 && F.expand && !F.slab && Dd.c == 1 && Dd.d == 3 &&
+                  !(ic.nu > 0.0 && ic.nu < 1.0) && !sharded(ctx) && !host_loop_mode() && F.n <= (i64(8) << 20);
+  if (np) {
+    NA.n1 = static_cast<int>(Dd.n[0]);
+    NA.n2 = static_cast<int>(Dd.n[1]);
+    NA.n3 = static_cast<int>(Dd.n[2]);
+    NA.p1 = static_cast<int>(Dd.p[0][0]);
+    NA.p2 = static_cast<int>(Dd.p[0][1]);
+    NA.p3 = static_cast<int>(Dd.p[0][2]);
+  }
+  if (np && npersist_ok(NA, &np_grid)) {
+    NA.ctl = static_cast<FistaCtl*>(F.ctl.p);
+    NA.H1 = Dd.f[0][0]->dev.H;
+    NA.G1 = Dd.f[0][0]->dev.G;
+    NA.H2 = Dd.f[0][1]->dev.H;
+    NA.G2 = Dd.f[0][1]->dev.G;
+    NA.H3 = Dd.f[0][2]->dev.H;
+    NA.G3 = Dd.f[0][2]->dev.G;
+    NA.x = F.x.d();
+    NA.xp = F.xp.d();
+    NA.Sx = F.Sx.d();
+    NA.Sxp = F.Sxp.d();
+    NA.best = F.best.d();
+    NA.Sbest = F.Sbest.d();
+    NA.b = F.b.d();
+    NA.v = F.v.d();
+    NA.A1 = F.s0.d();
+    NA.P = F.P.d();
+    NA.Q = F.Q.d();
+    NA.B1 = F.s1.d();
+    F.nppart.alloc(sizeof(double) * 4 * np_grid);
+    NA.part = F.nppart.d();
+    if (!F.npbar.p) {
+      F.npbar.alloc(sizeof(unsigned) * 4);
+      KG_CUDA(cudaMemsetAsync(F.npbar.p, 0, sizeof(unsigned) * 4, ctx->s));
+    }
+    NA.bar = static_cast<unsigned*>(F.npbar.p);
+    if (const char* e = std::getenv("KG_NP_DBG")) NA.dbg = std::atoi(e);
+    npersist(ctx->L(), NA, np_grid);
+    F.kernels_per_iter[F.route] = 0;  // one launch for the whole loop
+  } else if (ic.max_iters >= 1) {
     // a sharded n-space loop is driven from the host: its all-reduces stay out of graph capture
     if (host_loop_mode() || (sharded(ctx) && F.route == 0)) {
       const FistaCtl* hc = reinterpret_cast<const FistaCtl*>(ctx->pin() + PIN_CTL);

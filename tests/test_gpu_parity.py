@@ -482,3 +482,30 @@ def test_tensor_weights_match_oracle(case):
         fam = "poisson"
     kw = dict(n_lambda=6, lambda_min_ratio=1e-2, iwls="tensor")
     compare_paths(K.fit_path(design, fam, y, **kw), O.fit_path(design, fam, y, **kw))
+
+
+def test_persistent_nspace_loop_matches_oracle(monkeypatch):
+    """Opt-in cooperative n-space FISTA loop (k_nspace_persist, KG_NPERSIST=1):
+    a Poisson d = 3 path through it matches the oracle."""
+    rng = np.random.default_rng(5)
+    design = bspline_design((24, 20, 30), (8, 6, 9))
+    B = np.zeros((8, 6, 9))
+    m = rng.random(B.shape) < 0.15
+    B[m] = rng.standard_normal(m.sum())
+    eta = configs.tensor_h(design[0], B)
+    y = rng.poisson(np.exp(np.log(20.0) / eta.max() * eta)).astype(float)
+    kw = dict(n_lambda=8, lambda_min_ratio=1e-3)
+    ctx = K.Context(0)
+    D = K.Design(design, ctx)
+    obs = K.Observation(D, y)
+    ctx.reset_launches()
+    K.fit_path_resident(D, obs, "poisson", **kw)
+    graph_launches = ctx.launches
+    monkeypatch.setenv("KG_NPERSIST", "1")
+    ctx.reset_launches()
+    res = K.fit_path_resident(D, obs, "poisson", **kw)
+    assert ctx.launches < graph_launches / 2  # one launch per inner solve, not one per iteration
+    got = {"lambdas": res.lambdas, "objectives": res.objectives, "truncated": res.truncated,
+           "coefficients": [D.blocks(c) for c in res.coefs()], "outer_iters": res.outer_iters,
+           "inner_iters": res.inner_iters}
+    compare_paths(got, O.fit_path(design, "poisson", y, **kw))
