@@ -62,7 +62,13 @@ struct BandOp {
   const int* hlo = nullptr;   // host copies (planning only; never dereferenced on the device)
   const int* hlen = nullptr;
   uint64_t uid = 0;           // unique per uploaded operator (plan cache key)
+  // row-blocked form (H operators of B-spline factors): rows in groups of
+  // kRB; group g reads the input window [blo[g], blo[g] + kRW) and row
+  // 4g + r uses bcoef[(g * kRB + r) * kRW + w] (zero outside its band)
+  const int* blo = nullptr;
+  const double* bcoef = nullptr;
 };
+constexpr int kRB = 4, kRW = 8;
 
 // Device + host copies of one factor's operators.
 struct FactorDev {

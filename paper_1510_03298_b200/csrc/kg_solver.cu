@@ -16,6 +16,7 @@
 
 #include <algorithm>
 #include <cstdlib>
+#include <cstdint>
 #include <cmath>
 #include <cstring>
 #include <limits>
@@ -211,7 +212,7 @@ static void build_band(const FactorHost& h, bool rows_of_x, std::vector<int>& lo
 
 struct FactorOwn {
   FactorDev dev;
-  DBuf X, hlo, hlen, hoff, hcoef, glo, glen, goff, gcoef;
+  DBuf X, hlo, hlen, hoff, hcoef, glo, glen, goff, gcoef, rblo, rbcoef;
   std::vector<int> h_lo, h_len, g_lo, g_len;  // host copies for launch planning
 };
 
@@ -255,6 +256,37 @@ static void upload_factor(const FactorHost& h, FactorOwn& f, cudaStream_t s) {
   };
   up(true, f.hlo, f.hlen, f.hoff, f.hcoef, f.dev.H, f.h_lo, f.h_len);
   up(false, f.glo, f.glen, f.goff, f.gcoef, f.dev.G, f.g_lo, f.g_len);
+  // row-blocked copy of the H operator when every group of kRB rows reads a
+  // window of at most kRW inputs (B-spline rows: 4 nonzeros, slowly moving)
+  const i64 rows = h.n, groups = (rows + kRB - 1) / kRB;
+  bool ok = f.dev.H.maxlen <= kRW;
+  std::vector<int> wlo(static_cast<size_t>(groups), 0);
+  std::vector<double> wc(static_cast<size_t>(groups * kRB * kRW), 0.0);
+  for (i64 g = 0; g < groups && ok; ++g) {
+    int lo = INT32_MAX, hi = 0;
+    for (i64 r = g * kRB; r < std::min(rows, (g + 1) * kRB); ++r)
+      if (f.h_len[r] > 0) {
+        lo = std::min(lo, f.h_lo[r]);
+        hi = std::max(hi, f.h_lo[r] + f.h_len[r]);
+      }
+    if (lo == INT32_MAX) lo = hi = 0;
+    if (hi - lo > kRW || lo + kRW > h.p) {  // window must stay inside the input extent
+      lo = static_cast<int>(std::max<i64>(0, std::min<i64>(lo, h.p - kRW)));
+      if (hi - lo > kRW || h.p < kRW) ok = false;
+    }
+    wlo[static_cast<size_t>(g)] = lo;
+    for (i64 r = g * kRB; r < std::min(rows, (g + 1) * kRB) && ok; ++r)
+      for (int t = 0; t < f.h_len[r]; ++t)
+        wc[static_cast<size_t>(((g * kRB + (r - g * kRB)) * kRW) + (f.h_lo[r] + t - lo))] = h.X[r + h.n * (f.h_lo[r] + t)];
+  }
+  if (ok) {
+    f.rblo.alloc(sizeof(int) * groups);
+    f.rbcoef.alloc(sizeof(double) * wc.size());
+    KG_CUDA(cudaMemcpyAsync(f.rblo.p, wlo.data(), sizeof(int) * groups, cudaMemcpyHostToDevice, f.rblo.s));
+    KG_CUDA(cudaMemcpyAsync(f.rbcoef.p, wc.data(), sizeof(double) * wc.size(), cudaMemcpyHostToDevice, f.rbcoef.s));
+    f.dev.H.blo = static_cast<const int*>(f.rblo.p);
+    f.dev.H.bcoef = f.rbcoef.d();
+  }
 }
 
 // Spectral radius of X^T X for one factor: banded Gram + single-warp power
