@@ -260,9 +260,15 @@ static void launch_rs(const Launch& L, const double* A, double* out, i64 a, i64 
                       bool accumulate) {
   const i64 pairs = a * M;
   const i64 gx = (pairs + NT - 1) / NT;
-  i64 gy = std::max<i64>(1, (148 * 16 + gx - 1) / gx);
+  static const i64 cap = [] {
+    const char* e = std::getenv("KG_RS_BLOCKS");
+    return e ? std::max<i64>(148, std::atoll(e)) : 148 * 32;
+  }();
+  // ~cap CTAs; each thread's beta chunk a multiple of the 4-slab pass (no scalar tail)
+  i64 gy = std::max<i64>(1, (cap + gx - 1) / gx);
   gy = std::min<i64>(gy, std::min<i64>(b, 65535));
-  const i64 bch = (b + gy - 1) / gy;
+  i64 bch = (b + gy - 1) / gy;
+  if (MAXB <= 8 && b >= 4) bch = (bch + 3) / 4 * 4;
   gy = (b + bch - 1) / bch;
   k_contract_rs<MAXB><<<dim3(static_cast<unsigned>(gx), static_cast<unsigned>(gy)), NT, 0, L.s>>>(
       A, out, static_cast<uint32_t>(a), static_cast<uint32_t>(K), static_cast<uint32_t>(M),
