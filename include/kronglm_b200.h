@@ -181,6 +181,22 @@ kg_status kg_predict(kg_ctx* ctx, const kg_design* design, int family, const dou
  * bases; out is npts x n_basis column-major. Host-side input builder. */
 kg_status kg_bspline_design(int64_t npts, const double* points, int64_t order, int64_t n_basis, double* out);
 int64_t kg_default_basis_count(int64_t n_points, int64_t ratio); /* bspline.cpp:20-26; -1 on bad args */
+/* bin_scatter (bspline.cpp:106-153, decl bspline.hpp:38-45) on the device:
+ * npts points of d <= 8 coordinates (point-major, npts x d) binned on the
+ * regular grid bins[0] x ... x bins[d-1] over [lo_j, hi_j] (bins right-open
+ * except the last, right-closed); counts (prod bins, column-major) receive
+ * the counts, *dropped (may be NULL) the points outside the bounds.
+ * on_device != 0: points and counts are device pointers (the counts can feed
+ * kg_obs_create(on_device=1) directly); else host pointers.  lo/hi/bins are
+ * host arrays.  A NaN coordinate drops the point (the reference's
+ * static_cast of floor(NaN) is undefined).  Counts are exact integers. */
+kg_status kg_bin_scatter(kg_ctx* ctx, int64_t npts, int64_t d, const double* points, const double* lo,
+                         const double* hi, const int64_t* bins, int on_device, double* counts, int64_t* dropped);
+/* bspline_design on the device: bit-identical to kg_bspline_design (same
+ * knots, explicitly rounded FP64 recursion), order <= 16.  on_device: points
+ * (npts) and out (npts x n_basis, column-major) are device pointers. */
+kg_status kg_bspline_design_dev(kg_ctx* ctx, int64_t npts, const double* points, int64_t order, int64_t n_basis,
+                                int on_device, double* out);
 int64_t kg_linear_index(int64_t d, const int64_t* multi_index, const int64_t* dims); /* array.cpp:22-36; -1 bad */
 
 /* Held-out selection (mse_heldout, path.cpp:91-126, decl path.hpp:63): for

@@ -1557,6 +1557,46 @@ int orc_bspline_design(int64_t npts, const double* pts, int64_t order, int64_t n
   });
 }
 
+// bin_scatter (bspline.cpp:106-153): points (npts x d, point-major) -> counts
+// on the regular grid (column-major), bins right-open except the last.  A NaN
+// coordinate is dropped here (the reference's cast of floor(NaN) is UB).
+int orc_bin_scatter(int64_t npts, int64_t d, const double* pts, const double* lo, const double* hi,
+                    const int64_t* bins, double* counts, int64_t* dropped) {
+  return guard([&] {
+    if (d <= 0) throw std::invalid_argument("bin_scatter: bounds and bins must agree on the dimension");
+    int64_t cells = 1;
+    for (int64_t j = 0; j < d; ++j) {
+      if (bins[j] < 1) throw std::invalid_argument("bin_scatter: need at least one bin");
+      if (!(hi[j] > lo[j])) throw std::invalid_argument("bin_scatter: degenerate bounds");
+      cells *= bins[j];
+    }
+    std::fill(counts, counts + cells, 0.0);
+    int64_t drop = 0;
+    for (int64_t i = 0; i < npts; ++i) {
+      int64_t offset = 0, stride = 1;
+      bool keep = true;
+      for (int64_t j = 0; j < d; ++j) {
+        const double x = pts[i * d + j];
+        if (!(x >= lo[j] && x <= hi[j])) {
+          keep = false;
+          break;
+        }
+        const double width = (hi[j] - lo[j]) / static_cast<double>(bins[j]);
+        int64_t cell = static_cast<int64_t>(std::floor((x - lo[j]) / width));
+        if (cell >= bins[j]) cell = bins[j] - 1;
+        offset += cell * stride;
+        stride *= bins[j];
+      }
+      if (!keep) {
+        ++drop;
+        continue;
+      }
+      counts[offset] += 1.0;
+    }
+    *dropped = drop;
+  });
+}
+
 int orc_default_basis_count(int64_t n, int64_t ratio, int64_t* out) {
   return guard([&] { *out = default_basis_count(n, ratio); });
 }

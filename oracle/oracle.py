@@ -93,13 +93,14 @@ def _declare(L):
         "orc_bspline_design": [_i64, pd, _i64, _i64, pd],
         "orc_default_basis_count": [_i64, _i64, pi],
         "orc_mse_heldout": D + [C.c_int, pd, _i64, pd, pd, pd, pi],
+        "orc_bin_scatter": [_i64, _i64, pd, pd, pd, pi, pd, pi],
     }
     for name, args in sig.items():
         getattr(L, name).argtypes = args
     for name in ["orc_linear_index", "orc_rho", "orc_h_map", "orc_g_map", "orc_xtwx_apply", "orc_family_map",
                  "orc_loglik", "orc_validate", "orc_penalty_value", "orc_prox", "orc_lambda_max",
                  "orc_spectral_radius", "orc_lipschitz_upper", "orc_fista_solve", "orc_outer_solve",
-                 "orc_fit_path", "orc_bspline_design", "orc_default_basis_count", "orc_mse_heldout"]:
+                 "orc_fit_path", "orc_bspline_design", "orc_default_basis_count", "orc_mse_heldout", "orc_bin_scatter"]:
         getattr(L, name).restype = C.c_int
 
 
@@ -442,6 +443,24 @@ def bspline_design(points, order=4, n_basis=0):
     out = np.zeros((pts.size, n_basis), order="F")
     _check(lib().orc_bspline_design(pts.size, _ptr(pts), order, n_basis, _ptr(out)))
     return out
+
+
+def bin_scatter(points, bounds, bins):
+    """bin_scatter (bspline.cpp:106-153): (counts array, dropped)."""
+    pts = np.ascontiguousarray(np.asarray(points, np.float64))
+    bins = [int(b) for b in bins]
+    d = len(bins)
+    if d == 0 or len(bounds) != d:
+        raise ValueError("bin_scatter: bounds and bins must agree on the dimension")
+    pts = pts.reshape(-1, d) if pts.size else np.zeros((0, d))
+    lo = np.array([float(b[0]) for b in bounds])
+    hi = np.array([float(b[1]) for b in bounds])
+    bn = np.array(bins, dtype=np.int64)
+    counts = np.zeros(int(np.prod(bins)))
+    drop = _i64()
+    _check(lib().orc_bin_scatter(pts.shape[0], d, _ptr(pts), _ptr(lo), _ptr(hi),
+                                 bn.ctypes.data_as(_P(_i64)), _ptr(counts), C.byref(drop)))
+    return counts.reshape(bins, order="F"), drop.value
 
 
 def default_basis_count(n_points, ratio):

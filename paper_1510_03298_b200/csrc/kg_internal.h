@@ -364,4 +364,25 @@ struct PowerJob {
 constexpr int kPowerTaps = 8, kPowerRows = 8;
 void power_iterations(const Launch& L, const PowerJob* jobs_dev, int njobs, i64 max_p, double tol, i64 max_iters);
 
+// Input builders (kg_builders.cu): bin_scatter (bspline.cpp:106-153) and the
+// device bspline_design (bspline.cpp:64-104).
+constexpr int kMaxBinDims = 8, kBinThreads = 512, kMaxOrder = 16;
+constexpr int kBinTile = 1024, kBinStages = 3;  // points per staged tile, tiles in flight per CTA
+constexpr i64 kBinSmemBytes = 220 * 1024;     // counters + stages per CTA
+struct BinArgs {
+  int d = 0;
+  i64 npts = 0, cells = 0;
+  const double* pts = nullptr;  // npts x d, point-major
+  double lo[kMaxBinDims], hi[kMaxBinDims], width[kMaxBinDims], inv[kMaxBinDims];
+  int bmax[kMaxBinDims], stride[kMaxBinDims];  // bins - 1 and column-major strides (cells < 2^31)
+  // KG_BIN_MODE experiments: 1 direct loads (no staging), 4 force global
+  // atomics, 8 force smem counters
+  int mode = 0;
+  double* counts = nullptr;              // cells, zeroed by the caller
+  unsigned long long* dropped = nullptr;  // zeroed by the caller
+};
+void bin_scatter(const Launch& L, const BinArgs& A, int n_sm);
+void bspline_design_dev(const Launch& L, i64 npts, const double* pts, int order, i64 nb, const double* knots,
+                        double* out, int* bad);
+
 }  // namespace kg

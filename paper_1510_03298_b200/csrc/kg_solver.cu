@@ -2647,4 +2647,105 @@ kg_status kg_time_kernel(kg_ctx* ctx, const kg_design* D, const kg_obs* O, int w
   });
 }
 
+// ------------------------------------------------------- input builders
+kg_status kg_bin_scatter(kg_ctx* ctx, int64_t npts, int64_t d, const double* points, const double* lo,
+                         const double* hi, const int64_t* bins, int on_device, double* counts, int64_t* dropped) {
+  return guarded(ctx, [&] {
+    // bspline.cpp:109-121 (argument checks, same messages)
+    if (d <= 0 || !lo || !hi || !bins) throw Error(E_INVAL, "bin_scatter: bounds and bins must agree on the dimension");
+    if (d > kMaxBinDims) throw Error(E_INVAL, "bin_scatter: at most 8 dimensions");
+    if (npts < 0 || (npts > 0 && !points) || !counts) throw Error(E_INVAL, "bin_scatter: null buffer");
+    BinArgs A;
+    A.d = static_cast<int>(d);
+    A.npts = npts;
+    static const int bin_mode = [] { const char* e = std::getenv("KG_BIN_MODE"); return e ? std::atoi(e) : 0; }();
+    A.mode = bin_mode;
+    A.cells = 1;
+    for (int64_t j = 0; j < d; ++j) {
+      if (bins[j] < 1) throw Error(E_INVAL, "bin_scatter: need at least one bin");
+      if (!(hi[j] > lo[j])) throw Error(E_INVAL, "bin_scatter: degenerate bounds");
+      A.lo[j] = lo[j];
+      A.hi[j] = hi[j];
+      A.width[j] = (hi[j] - lo[j]) / static_cast<double>(bins[j]);
+      A.inv[j] = 1.0 / A.width[j];
+      if (bins[j] > INT32_MAX || A.cells > INT32_MAX / bins[j])
+        throw Error(E_INVAL, "bin_scatter: grid too large (at most 2^31 - 1 cells)");
+      A.bmax[j] = static_cast<int>(bins[j] - 1);
+      A.stride[j] = static_cast<int>(A.cells);  // column-major: the first index runs fastest (bspline.cpp:145-148)
+      A.cells *= bins[j];
+    }
+    set_device(ctx);
+    int n_sm = 148;
+    KG_CUDA(cudaDeviceGetAttribute(&n_sm, cudaDevAttrMultiProcessorCount, ctx->device));
+    Tmp t;
+    double* dcounts = on_device ? counts : t.get(A.cells);
+    const double* dpts = points;
+    if (!on_device && npts > 0) {
+      double* up = t.get(npts * d);
+      KG_CUDA(cudaMemcpyAsync(up, points, sizeof(double) * npts * d, cudaMemcpyHostToDevice, ctx->s));
+      dpts = up;
+    }
+    unsigned long long* ddrop = reinterpret_cast<unsigned long long*>(t.get(1));
+    KG_CUDA(cudaMemsetAsync(dcounts, 0, sizeof(double) * A.cells, ctx->s));
+    KG_CUDA(cudaMemsetAsync(ddrop, 0, sizeof(unsigned long long), ctx->s));
+    A.counts = dcounts;
+    A.dropped = ddrop;
+
+    // chunks keep every CTA's u32 counters far below 2^32
+    const int64_t chunk = int64_t(1) << 31;
+    for (int64_t first = 0; first < npts; first += chunk) {
+      BinArgs C = A;
+      C.pts = dpts + first * d;
+      C.npts = std::min(chunk, npts - first);
+      bin_scatter(ctx->L(), C, n_sm);
+    }
+    int64_t* pin = reinterpret_cast<int64_t*>(ctx->pin());
+    KG_CUDA(cudaMemcpyAsync(pin, ddrop, sizeof(int64_t), cudaMemcpyDeviceToHost, ctx->s));
+    if (!on_device) KG_CUDA(cudaMemcpyAsync(counts, dcounts, sizeof(double) * A.cells, cudaMemcpyDeviceToHost, ctx->s));
+    sync(ctx);
+    if (dropped) *dropped = pin[0];
+  });
+}
+
+kg_status kg_bspline_design_dev(kg_ctx* ctx, int64_t npts, const double* points, int64_t order, int64_t nb,
+                                int on_device, double* out) {
+  return guarded(ctx, [&] {
+    if (npts < 2) throw Error(E_INVAL, "MarginalGrid: need at least two grid points");
+    if (order < 1) throw Error(E_INVAL, "bspline_design: order must be at least 1");
+    if (nb < order) throw Error(E_INVAL, "bspline_design: need at least `order` basis functions");
+    if (order > kMaxOrder) throw Error(E_INVAL, "bspline_design: order above 16 is host-only");
+    set_device(ctx);
+    Tmp t;
+    const double* dpts = points;
+    if (!on_device) {
+      double* up = t.get(npts);
+      KG_CUDA(cudaMemcpyAsync(up, points, sizeof(double) * npts, cudaMemcpyHostToDevice, ctx->s));
+      dpts = up;
+    }
+    double* pin = ctx->pin();
+    KG_CUDA(cudaMemcpyAsync(pin, dpts, sizeof(double), cudaMemcpyDeviceToHost, ctx->s));
+    KG_CUDA(cudaMemcpyAsync(pin + 1, dpts + npts - 1, sizeof(double), cudaMemcpyDeviceToHost, ctx->s));
+    sync(ctx);
+    const double lo = pin[0], hi = pin[1];
+    // clamped uniform knots, computed exactly as the host builder (bspline.cpp:30-42)
+    const int64_t spans = nb - order + 1;
+    const double h = (hi - lo) / static_cast<double>(spans);
+    std::vector<double> knots(static_cast<size_t>(nb + order));
+    for (int64_t i = 0; i < order; ++i) knots[i] = lo;
+    for (int64_t i = 0; i < nb - order; ++i) knots[order + i] = lo + h * static_cast<double>(i + 1);
+    for (int64_t i = 0; i < order; ++i) knots[nb + i] = hi;
+    double* dk = t.get(knots.size());
+    KG_CUDA(cudaMemcpyAsync(dk, knots.data(), sizeof(double) * knots.size(), cudaMemcpyHostToDevice, ctx->s));
+    double* dout = on_device ? out : t.get(npts * nb);
+    int* bad = reinterpret_cast<int*>(t.get(1));
+    KG_CUDA(cudaMemsetAsync(bad, 0, sizeof(int), ctx->s));
+    bspline_design_dev(ctx->L(), npts, dpts, static_cast<int>(order), nb, dk, dout, bad);
+    int* pbad = reinterpret_cast<int*>(pin + 2);
+    KG_CUDA(cudaMemcpyAsync(pbad, bad, sizeof(int), cudaMemcpyDeviceToHost, ctx->s));
+    if (!on_device) KG_CUDA(cudaMemcpyAsync(out, dout, sizeof(double) * npts * nb, cudaMemcpyDeviceToHost, ctx->s));
+    sync(ctx);
+    if (*pbad) throw Error(E_INVAL, "MarginalGrid: points must be strictly increasing");
+  });
+}
+
 }  // extern "C"

@@ -29,6 +29,7 @@ STATUS = ["converged", "max_iterations", "line_search_failed", "inner_divergence
 
 _pd = C.POINTER(C.c_double)
 _i64 = C.c_int64
+_pi = C.POINTER(_i64)
 
 
 def _f(a):
@@ -447,6 +448,74 @@ def bspline_design(points, order=4, n_basis=0):
     st = _lib.load().kg_bspline_design(pts.size, _ptr(pts), int(order), int(n_basis), _ptr(out))
     if st != 0:
         raise ValueError("bspline_design: invalid grid or basis specification")
+    return out
+
+
+class BinnedCounts(tuple):
+    """BinnedCounts (bspline.hpp:33-36): ``counts`` array and ``dropped``."""
+    __slots__ = ()
+
+    def __new__(cls, counts, dropped):
+        return tuple.__new__(cls, (counts, dropped))
+
+    counts = property(lambda self: self[0])
+    dropped = property(lambda self: self[1])
+
+
+def _bin_args(bounds, bins):
+    bins = [int(b) for b in bins]
+    d = len(bins)
+    if d == 0 or len(bounds) != d:
+        raise ValueError("bin_scatter: bounds and bins must agree on the dimension")
+    lo = np.array([float(b[0]) for b in bounds])
+    hi = np.array([float(b[1]) for b in bounds])
+    return bins, d, lo, hi, np.array(bins, dtype=np.int64)
+
+
+def bin_scatter(points, bounds, bins, ctx: Context | None = None, out=None) -> BinnedCounts:
+    """Count points on a regular grid (bspline.cpp:106-153), on the device.
+
+    ``points``: (npts, d) array -- numpy (uploaded) or a CUDA tensor exposing
+    ``data_ptr()`` (row-major float64, read in place).  ``bounds``: d pairs
+    (lo, hi); ``bins``: d bin counts.  Returns BinnedCounts(counts, dropped),
+    counts shaped ``bins`` in column-major order.  For device points the
+    counts land in ``out`` (a CUDA float64 buffer of prod(bins) elements, e.g.
+    to feed ``Observation``) and ``counts`` is that buffer."""
+    ctx = ctx or default_context()
+    bins, d, lo, hi, bn = _bin_args(bounds, bins)
+    cells = int(np.prod(bins))
+    dropped = _i64()
+    L = _lib.load()
+    if hasattr(points, "data_ptr"):
+        if points.dim() != 2 or points.shape[1] != d:
+            raise ValueError("bin_scatter: point arity does not match the grid")
+        if not points.is_contiguous():
+            raise ValueError("bin_scatter: device points must be contiguous (npts x d)")
+        if out is None:
+            raise ValueError("bin_scatter: device points need a device `out` buffer")
+        if out.numel() != cells:
+            raise ValueError("bin_scatter: out must hold prod(bins) counts")
+        ctx.check(L.kg_bin_scatter(ctx.h, int(points.shape[0]), d, C.c_void_p(points.data_ptr()), _ptr(lo), _ptr(hi),
+                                   bn.ctypes.data_as(_pi), 1, C.c_void_p(out.data_ptr()), C.byref(dropped)))
+        return BinnedCounts(out, int(dropped.value))
+    pts = np.ascontiguousarray(np.asarray(points, dtype=np.float64))
+    if pts.size == 0:
+        pts = pts.reshape(0, d)
+    if pts.ndim != 2 or pts.shape[1] != d:
+        raise ValueError("bin_scatter: point arity does not match the grid")
+    counts = np.zeros(cells)
+    ctx.check(L.kg_bin_scatter(ctx.h, pts.shape[0], d, pts.ctypes.data_as(C.c_void_p), _ptr(lo), _ptr(hi),
+                               bn.ctypes.data_as(_pi), 0, counts.ctypes.data_as(C.c_void_p), C.byref(dropped)))
+    return BinnedCounts(counts.reshape(bins, order="F"), int(dropped.value))
+
+
+def bspline_design_device(points, order=4, n_basis=0, ctx: Context | None = None):
+    """bspline_design evaluated on the device (bit-identical to bspline_design)."""
+    ctx = ctx or default_context()
+    pts = np.ascontiguousarray(np.asarray(points, dtype=np.float64))
+    out = np.zeros((pts.size, int(n_basis)), order="F")
+    ctx.check(_lib.load().kg_bspline_design_dev(ctx.h, pts.size, pts.ctypes.data_as(C.c_void_p), int(order),
+                                                int(n_basis), 0, out.ctypes.data_as(C.c_void_p)))
     return out
 
 
