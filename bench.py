@@ -269,6 +269,8 @@ def run_ours(args):
                 "peak_kind": peak_kind, "unit": "GB/s", "frac": achieved / hbm,
                 "traffic": rho["dram_bytes_ncu"], "bytes_per_launch": f_bytes, "avg_launch_ms": f_ms}
 
+    builders = bin_scatter_stats(K, ctx, stream, list(data["y"].shape), hbm) if rank == 0 else None
+
     # e2e: the public kronglm.fit_path call with host buffers (design upload,
     # observation upload, path, all coefficient downloads), same metric.
     e2e_iters, e2e_ms = 0, 0.0
@@ -293,7 +295,7 @@ def run_ours(args):
                            "l2": "256 MB buffer written between timed steps", "parallelism": f"replicas x{world}"},
                 "e2e": {"value": e2e_iters / (e2e_ms / 1000.0), "unit": UNIT, "h2d_bytes_per_step": int(h2d),
                         "d2h_bytes_per_step": int(d2h), "ms_per_step": e2e_ms / max(1, min(args.steps, 3))},
-                "roofline": roof, "rho_contraction": rho,
+                "roofline": roof, "rho_contraction": rho, "input_builders": builders,
                 "clocks": clk, "gpu_launches": int(launches)}
     # CPU baseline: the oracle port on rank 0 at N = 1, bounded prefix of the same path
     if rank == 0 and world == 1 and not args.no_cpu_baseline:
@@ -402,6 +404,38 @@ def run_sharded(args, data, world, rank, local):
     if world > 1:
         dist.barrier()
         dist.destroy_process_group()
+
+
+def bin_scatter_stats(K, ctx, stream, grid, hbm, npts=50_000_000, reps=10):
+    """The device bin_scatter (the input builder in front of the path) on
+    HBM-resident uniform points over this config's response grid: algorithmic
+    bytes = 8 d per point read + 8 per cell written, per call (memsets, the
+    kernel, the dropped-count readback), CUDA events on the ctx stream."""
+    import torch
+    d = len(grid)
+    g = torch.Generator(device="cuda").manual_seed(11)
+    pts = torch.rand((npts, d), generator=g, device="cuda", dtype=torch.float64)
+    cells = int(np.prod(grid))
+    out = torch.empty(cells, device="cuda", dtype=torch.float64)
+    bounds = [(0.0, 1.0)] * d
+    for _ in range(3):
+        K.bin_scatter(pts, bounds, grid, ctx=ctx, out=out)
+    ms = []
+    for _ in range(reps):
+        e0, e1 = torch.cuda.Event(enable_timing=True), torch.cuda.Event(enable_timing=True)
+        e0.record(stream)
+        K.bin_scatter(pts, bounds, grid, ctx=ctx, out=out)
+        e1.record(stream)
+        e1.synchronize()
+        ms.append(e0.elapsed_time(e1))
+    med = float(np.median(ms))
+    byts = 8.0 * d * npts + 8.0 * cells
+    del pts, out
+    torch.cuda.empty_cache()
+    return {"bin_scatter": {"points": npts, "grid": grid, "ms": med, "gpoints_per_s": npts / med / 1e6,
+                            "achieved": byts / med / 1e6, "peak": hbm, "unit": "GB/s", "frac": byts / med / 1e6 / hbm,
+                            "path": "shared-memory counters" if 4 * cells + 3 * 1024 * 8 * d <= 220 * 1024
+                            and npts >= 8 * cells else "L2 atomics"}}
 
 
 def path_kernel_stats(ctx):

@@ -274,4 +274,45 @@ inline Matrix bspline_design(const std::vector<double>& points, Index order, Ind
   return m;
 }
 
+// bin_scatter (bspline.hpp:33-45) on the device: points are d-vectors, bounds
+// (lo, hi) per dimension, bins per dimension; counts are column-major over
+// the bins grid (prod bins entries), dropped = points outside the bounds.
+struct BinnedCounts {
+  std::vector<Index> dims;
+  std::vector<double> counts;
+  Index dropped = 0;
+};
+
+inline BinnedCounts bin_scatter(const Context& ctx, const std::vector<std::vector<double>>& points,
+                                const std::vector<std::pair<double, double>>& bounds,
+                                const std::vector<Index>& bins) {
+  const size_t d = bins.size();
+  if (d == 0 || bounds.size() != d)
+    throw std::invalid_argument("bin_scatter: bounds and bins must agree on the dimension");
+  std::vector<double> flat;
+  flat.reserve(points.size() * d);
+  for (const auto& pt : points) {
+    if (pt.size() != d) throw std::invalid_argument("bin_scatter: point arity does not match the grid");
+    flat.insert(flat.end(), pt.begin(), pt.end());
+  }
+  std::vector<double> lo(d), hi(d);
+  std::vector<int64_t> nb(d);
+  Index cells = 1;
+  for (size_t j = 0; j < d; ++j) {
+    lo[j] = bounds[j].first;
+    hi[j] = bounds[j].second;
+    nb[j] = bins[j];
+    cells *= bins[j] > 0 ? bins[j] : 1;
+  }
+  BinnedCounts out;
+  out.dims = bins;
+  out.counts.assign(static_cast<size_t>(cells), 0.0);
+  int64_t dropped = 0;
+  check(kg_bin_scatter(ctx.get(), static_cast<int64_t>(points.size()), static_cast<int64_t>(d), flat.data(),
+                       lo.data(), hi.data(), nb.data(), 0, out.counts.data(), &dropped),
+        ctx.get());
+  out.dropped = dropped;
+  return out;
+}
+
 }  // namespace kronglm_b200

@@ -359,9 +359,9 @@ struct PowerJob {
   const int* ghi = nullptr;
   const double* v0 = nullptr;
   double* out = nullptr;      // [value, iterations, status]
-  int band = 0;               // max row band width (register path when <= kPowerTaps and p <= 32 * kPowerRows)
+  int band = 0;               // max row band width (banded CTA path when <= kPowerTaps)
 };
-constexpr int kPowerTaps = 8, kPowerRows = 8;
+constexpr int kPowerTaps = 8, kPowerBlock = 8, kPowerThreads = 512, kPowerCtaRows = 2;
 void power_iterations(const Launch& L, const PowerJob* jobs_dev, int njobs, i64 max_p, double tol, i64 max_iters);
 
 // Input builders (kg_builders.cu): bin_scatter (bspline.cpp:106-153) and the

@@ -1311,55 +1311,64 @@ void gram(const Launch& L, const FactorDev& f, double* G, int* glo, int* ghi) {
   bump(L);
 }
 
-// Power iteration (spectral.cpp:8-42), one warp per job (blockIdx.x), every
-// factor of a design in one launch.  v stays in shared memory; the two
-// reductions per step are warp-shuffle trees.  Register path: each lane keeps
-// its rows i = lane + 32 r of the Gram band in registers (B-spline Grams are
-// 7 wide), so a step is kPowerRows x kPowerTaps FMAs on shared v; the per-row
-// summation order (ascending column) is the same on both paths.
-__global__ void k_power(const PowerJob* jobs, double tol, i64 max_iters) {
+// Power iteration (spectral.cpp:8-42), one CTA per job (blockIdx.x), every
+// factor of a design in one launch.
+//
+// Banded path (band <= kPowerTaps, kPowerTaps <= p <= blockDim.x *
+// kPowerCtaRows): each thread owns rows i = tid + blockDim.x * r with their
+// Gram band in registers, padded to kPowerTaps taps on a window clamped into
+// [0, p) (no predicates in the product).  Steps are taken kPowerBlock at a
+// time without renormalising: a_j = G a_{j-1} from a_0 = v, each a_j staged in
+// shared memory for the next product, while every thread accumulates |a_j|^2
+// and a_{j-1}.a_j.  One CTA reduction (warp shuffles, then a fixed-order sum
+// over warps) of those 2 kPowerBlock sums per block replays the reference's
+// per-step quantities exactly in exact arithmetic:
+//   norm_j = |a_j| / |a_{j-1}|,  next_j = a_{j-1}.a_j / |a_{j-1}|^2,
+// and applies its stop rule step by step (two quiet Rayleigh quotients), so
+// the returned value and iteration count follow the same sequence while the
+// reduction latency is paid once per block.  A block whose growth over- or
+// underflows is redone one step at a time.
+// Generic path (wide bands, tiny or huge p): warp 0 alone, one step at a time
+// on the dense band.
+__global__ void __launch_bounds__(kPowerThreads) k_power(const PowerJob* jobs, double tol, i64 max_iters,
+                                                         i64 sm_doubles) {
   extern __shared__ double sh[];
   const PowerJob J = jobs[blockIdx.x];
   const i64 p = J.p;
-  double* v = sh;
-  double* av = sh + p;
-  const int l = threadIdx.x;
-  const bool reg = J.band <= kPowerTaps && p <= 32 * kPowerRows;
-  double c[kPowerRows][kPowerTaps];
-  int lo[kPowerRows], ln[kPowerRows];
-#pragma unroll
-  for (int r = 0; r < kPowerRows; ++r) {
-    const i64 i = l + 32 * r;
-    lo[r] = 0;
-    ln[r] = 0;
-    if (reg && i < p) {
-      lo[r] = J.glo[i];
-      ln[r] = J.ghi[i] - lo[r];
-    }
-#pragma unroll
-    for (int t = 0; t < kPowerTaps; ++t) c[r][t] = t < ln[r] ? J.G[i + p * (lo[r] + t)] : 0.0;
-  }
-  for (i64 i = l; i < p; i += 32) v[i] = J.v0[i];
-  __syncwarp();
+  const int tid = threadIdx.x, l = tid & 31, warp = tid >> 5;
+  const bool banded = J.band <= kPowerTaps && p >= kPowerTaps && p <= static_cast<i64>(blockDim.x) * kPowerCtaRows &&
+                      (kPowerBlock + 1) * p + 2 * kPowerBlock * (blockDim.x + 1) <= sm_doubles;
   double value = 0.0;
   i64 settled = 0;
-  for (i64 it = 1; it <= max_iters; ++it) {
-    double nn = 0.0, dot = 0.0;
-    double a[kPowerRows];
-    if (reg) {
-#pragma unroll
-      for (int r = 0; r < kPowerRows; ++r) {
-        double s = 0.0;
-#pragma unroll
-        for (int t = 0; t < kPowerTaps; ++t)
-          if (t < ln[r]) s += c[r][t] * v[lo[r] + t];
-        a[r] = s;
-        if (l + 32 * r < p) {
-          nn += s * s;
-          dot += v[l + 32 * r] * s;
-        }
+  auto finish = [&](double val, i64 it, double status) {
+    if (tid == 0) {
+      J.out[0] = val;
+      J.out[1] = static_cast<double>(it);
+      J.out[2] = status;
+    }
+  };
+  // the reference's per-step bookkeeping; true when the iteration stops
+  auto step_done = [&](double next, i64 it) {
+    const double change = fabs(next - value);
+    value = next;
+    if (change <= tol * fmax(fabs(value), 1e-300)) {
+      if (++settled >= 2) {
+        finish(value, it, 0.0);
+        return true;
       }
     } else {
+      settled = 0;
+    }
+    return false;
+  };
+  if (!banded) {
+    if (warp != 0) return;
+    double* v = sh;
+    double* av = sh + p;
+    for (i64 i = l; i < p; i += 32) v[i] = J.v0[i];
+    __syncwarp();
+    for (i64 it = 1; it <= max_iters; ++it) {
+      double nn = 0.0, dot = 0.0;
       for (i64 i = l; i < p; i += 32) {
         double s = 0.0;
         for (int k = J.glo[i]; k < J.ghi[i]; ++k) s += J.G[i + p * k] * v[k];
@@ -1367,54 +1376,148 @@ __global__ void k_power(const PowerJob* jobs, double tol, i64 max_iters) {
         nn += s * s;
         dot += v[i] * s;
       }
-    }
-    nn = warp_allsum(nn);
-    dot = warp_allsum(dot);
-    const double norm = sqrt(nn);
-    if (norm == 0.0) {
-      if (l == 0) {
-        J.out[0] = 0.0;
-        J.out[1] = static_cast<double>(it);
-        J.out[2] = 0.0;
-      }
-      return;
-    }
-    __syncwarp();
-    if (reg) {
-#pragma unroll
-      for (int r = 0; r < kPowerRows; ++r)
-        if (l + 32 * r < p) v[l + 32 * r] = a[r] / norm;
-    } else {
-      for (i64 i = l; i < p; i += 32) v[i] = av[i] / norm;
-    }
-    __syncwarp();
-    const double change = fabs(dot - value);
-    value = dot;
-    if (change <= tol * fmax(fabs(value), 1e-300)) {
-      if (++settled >= 2) {
-        if (l == 0) {
-          J.out[0] = value;
-          J.out[1] = static_cast<double>(it);
-          J.out[2] = 0.0;
-        }
+      nn = warp_allsum(nn);
+      dot = warp_allsum(dot);
+      const double norm = sqrt(nn);
+      if (norm == 0.0) {
+        finish(0.0, it, 0.0);
         return;
       }
-    } else {
-      settled = 0;
+      __syncwarp();
+      for (i64 i = l; i < p; i += 32) v[i] = av[i] / norm;
+      __syncwarp();
+      if (step_done(dot, it)) return;
     }
+    finish(value, max_iters, 1.0);
+    return;
   }
-  if (l == 0) {
-    J.out[0] = value;
-    J.out[1] = static_cast<double>(max_iters);
-    J.out[2] = 1.0;
+  constexpr int KB = kPowerBlock;
+  double* red = sh + static_cast<i64>(KB + 1) * p;  // [2 KB][blockDim.x] partials, then tot[2 KB]
+  double* tot = red + 2 * KB * blockDim.x;
+  double c[kPowerCtaRows][kPowerTaps];
+  int base[kPowerCtaRows];
+  bool own[kPowerCtaRows];
+  double a[kPowerCtaRows];
+#pragma unroll
+  for (int r = 0; r < kPowerCtaRows; ++r) {
+    const i64 i = tid + static_cast<i64>(blockDim.x) * r;
+    own[r] = i < p;
+    int lo = 0, hi = 0;
+    if (own[r]) {
+      lo = J.glo[i];
+      hi = J.ghi[i];
+    }
+    base[r] = min(lo, static_cast<int>(p) - kPowerTaps);
+#pragma unroll
+    for (int t = 0; t < kPowerTaps; ++t) {
+      const int col = base[r] + t;
+      c[r][t] = (own[r] && col >= lo && col < hi) ? J.G[i + p * col] : 0.0;
+    }
+    a[r] = own[r] ? J.v0[i] : 0.0;
+    if (own[r]) sh[i] = a[r];
   }
+  __syncthreads();
+  bool blocked = true;
+  i64 it = 0;
+  while (it < max_iters) {
+    const int K = !blocked ? 1 : (max_iters - it < KB ? static_cast<int>(max_iters - it) : KB);
+    double ssum[KB], tsum[KB];
+#pragma unroll
+    for (int j = 0; j < KB; ++j) {
+      ssum[j] = 0.0;
+      tsum[j] = 0.0;
+      if (j < K) {
+        const double* ain = sh + j * p;
+        double* aout = sh + (j + 1) * p;
+#pragma unroll
+        for (int r = 0; r < kPowerCtaRows; ++r) {
+          if (own[r]) {
+            const i64 i = tid + static_cast<i64>(blockDim.x) * r;
+            double s = 0.0;
+#pragma unroll
+            for (int t = 0; t < kPowerTaps; ++t) s += c[r][t] * ain[base[r] + t];
+            ssum[j] += s * s;
+            tsum[j] += ain[i] * s;
+            aout[i] = s;
+            a[r] = s;
+          }
+        }
+        __syncthreads();
+      }
+    }
+    // CTA reduction of the 2 K sums through shared memory: every thread
+    // stores its partials, then 16 threads per sum add 1/16 of the rows each
+    // (fixed order) and a 16-lane shuffle tree finishes it.
+    {
+      const int nt = blockDim.x;
+#pragma unroll
+      for (int j = 0; j < KB; ++j) {
+        red[(2 * j) * nt + tid] = ssum[j];
+        red[(2 * j + 1) * nt + tid] = tsum[j];
+      }
+      __syncthreads();
+      // half-warps pair up on consecutive sums and 2 K is even, so a warp's
+      // halves take the same trips (the shuffles need the whole warp)
+      const int part = tid & 15;
+      for (int q = tid >> 4; q < 2 * K; q += nt >> 4) {
+        double acc = 0.0;
+        for (int k = part; k < nt; k += 16) acc += red[q * nt + k];
+#pragma unroll
+        for (int o = 8; o > 0; o >>= 1) acc += __shfl_xor_sync(0xffffffffu, acc, o, 16);
+        if (part == 0) tot[q] = acc;
+      }
+      __syncthreads();
+    }
+#pragma unroll
+    for (int j = 0; j < KB; ++j) {
+      if (j < K) {
+        ssum[j] = tot[2 * j];
+        tsum[j] = tot[2 * j + 1];
+      }
+    }
+    bool ok = true;
+#pragma unroll
+    for (int j = 0; j < KB; ++j)
+      if (j < K) ok = ok && isfinite(ssum[j]) && (ssum[j] > 0.0 || j == 0);
+    if (!ok && K > 1) {  // growth left the FP64 range inside the block: redo it one step at a time
+      blocked = false;
+      continue;
+    }
+    double prev = 1.0;  // a_0 is the unit-normalised v of the reference
+#pragma unroll
+    for (int j = 0; j < KB; ++j) {
+      if (j < K) {
+        ++it;
+        if (ssum[j] == 0.0) {
+          finish(0.0, it, 0.0);
+          return;
+        }
+        if (step_done(tsum[j] / prev, it)) return;
+        prev = ssum[j];
+      }
+    }
+    // the next block starts from v = a_K / |a_K| (a_K is the one left in registers)
+    const double norm = sqrt(prev);
+#pragma unroll
+    for (int r = 0; r < kPowerCtaRows; ++r)
+      if (own[r]) sh[tid + static_cast<i64>(blockDim.x) * r] = a[r] / norm;
+    __syncthreads();
+  }
+  finish(value, max_iters, 1.0);
 }
 
 void power_iterations(const Launch& L, const PowerJob* jobs_dev, int njobs, i64 max_p, double tol, i64 max_iters) {
   if (njobs < 1) return;
-  const size_t sm = 2 * static_cast<size_t>(max_p) * sizeof(double);
-  if (sm > 48 * 1024) KG_CUDA(cudaFuncSetAttribute(k_power, cudaFuncAttributeMaxDynamicSharedMemorySize, 200 * 1024));
-  k_power<<<njobs, 32, sm, L.s>>>(jobs_dev, tol, max_iters);
+  // one row per thread up to kPowerThreads rows, then up to kPowerCtaRows each
+  const i64 threads = std::min<i64>(kPowerThreads, std::max<i64>(32, (max_p + 31) / 32 * 32));
+  const i64 banded_p = std::min<i64>(max_p, threads * kPowerCtaRows);
+  i64 need = std::max<i64>(2 * max_p, (kPowerBlock + 1) * banded_p + 2 * kPowerBlock * (threads + 1));
+  need = std::min<i64>(need, 220 * 1024 / 8);
+  if (2 * max_p > need) throw Error(E_INVAL, "spectral_radius: factor too large for the device power iteration");
+  const size_t sm = sizeof(double) * static_cast<size_t>(need);
+  if (sm > 48 * 1024)
+    KG_CUDA(cudaFuncSetAttribute(k_power, cudaFuncAttributeMaxDynamicSharedMemorySize, static_cast<int>(sm)));
+  k_power<<<njobs, static_cast<unsigned>(threads), sm, L.s>>>(jobs_dev, tol, max_iters, need);
   bump(L);
 }
 

@@ -406,7 +406,11 @@ static std::vector<double> spectral_run(kg_ctx* ctx, std::vector<std::unique_ptr
   std::vector<double> res(3 * pj.size());
   KG_CUDA(cudaMemcpyAsync(res.data(), out.p, sizeof(double) * res.size(), cudaMemcpyDeviceToHost, ctx->s));
   sync(ctx);
+  static const bool trace = std::getenv("KG_POWER_TRACE") != nullptr;
   for (size_t k = 0; k < pj.size(); ++k) {
+    if (trace)
+      std::fprintf(stderr, "kg power job %zu: p=%lld band=%d value=%.17g iterations=%.0f\n", k,
+                   static_cast<long long>(pj[k].p), pj[k].band, res[3 * k], res[3 * k + 1]);
     if (res[3 * k + 2] != 0.0) throw Error(E_POWER, "power iteration did not converge after 500000 iterations");
     vals[idx[k]] = res[3 * k];
   }

@@ -14,8 +14,8 @@ upload once, fit many paths.
 from __future__ import annotations
 
 import ctypes as C
-import weakref
 import threading
+import weakref
 
 import numpy as np
 
@@ -282,9 +282,16 @@ class PathResult:
         self.design.ctx.check(_lib.load().kg_result_coef(self.h, t, _ptr(out)))
         return out
 
-    def coefs(self) -> np.ndarray:
-        """All models' coefficients, n_models x p, in one device-to-host copy."""
-        out = np.zeros((self.n_models, self.design.p))
+    def coefs(self, out=None) -> np.ndarray:
+        """All models' coefficients, n_models x p, in one device-to-host copy
+        (into ``out[:n_models]`` when given: C-contiguous float64, >= n_models rows)."""
+        if out is None:
+            out = np.zeros((self.n_models, self.design.p))
+        else:
+            if (out.dtype != np.float64 or not out.flags.c_contiguous or out.ndim != 2
+                    or out.shape[1] != self.design.p or out.shape[0] < self.n_models):
+                raise ValueError("coefs: out must be a C-contiguous float64 (>= n_models, p) array")
+            out = out[:self.n_models]
         if self.n_models:
             self.design.ctx.check(_lib.load().kg_result_coefs(self.h, 0, self.n_models, _ptr(out)))
         return out
@@ -398,14 +405,24 @@ def fit_path(design, family, y, weights=None, penalty="lasso", alpha=0.0, n_lamb
     keys as kronglm_py.cpp:159-217, plus ``inner_iters`` and ``status``."""
     D = _design(design)
     obs = Observation(D, y, weights)
-    res = fit_path_resident(D, obs, family, penalty, alpha, lambdas, n_lambda=n_lambda,
-                            lambda_min_ratio=lambda_min_ratio, iwls=iwls, nu=nu, tol=tol, maxit=maxit,
-                            inner_tol=inner_tol, inner_maxit=inner_maxit)
+    # The coefficient buffer's first-touch page faults (~9 ms for C2's 43 MB)
+    # are taken on a helper thread while the device fits the path (the ctypes
+    # calls release the GIL), so the download lands in resident pages.
+    n_max = len(lambdas) if lambdas is not None else int(n_lambda)
+    buf = np.empty((max(n_max, 1), D.p))
+    toucher = threading.Thread(target=C.memset, args=(buf.ctypes.data, 0, buf.nbytes), daemon=True)
+    toucher.start()
+    try:
+        res = fit_path_resident(D, obs, family, penalty, alpha, lambdas, n_lambda=n_lambda,
+                                lambda_min_ratio=lambda_min_ratio, iwls=iwls, nu=nu, tol=tol, maxit=maxit,
+                                inner_tol=inner_tol, inner_maxit=inner_maxit)
+    finally:
+        toucher.join()
     out = {"lambdas": list(res.lambdas), "objectives": list(res.objectives), "lambda_max": res.lambda_max,
            "truncated": res.truncated, "coefficients": [], "nonzero": [], "outer_iters": list(res.outer_iters),
            "converged": [s == "converged" for s in res.status], "inner_iters": list(res.inner_iters),
            "status": list(res.status)}
-    for flat in res.coefs():
+    for flat in res.coefs(out=buf):
         out["coefficients"].append(D.blocks(flat))
         out["nonzero"].append(int(np.count_nonzero(flat)))
     return out

@@ -59,6 +59,12 @@ int main() {
       if (std::abs(ho.mse[static_cast<size_t>(t)] - d * d) > 1e-12 * std::max(1.0, d * d)) bad |= 64;
     }
   }
+  // bin_scatter (test_bspline.cpp:123-130 corner and boundary conventions)
+  {
+    const BinnedCounts bc = bin_scatter(ctx, {{0.0, 0.0}, {1.0, 2.0}, {0.499, 1.999}, {1.5, 0.0}}, {{0.0, 1.0}, {0.0, 2.0}},
+                                        {2, 4});
+    if (bc.dropped != 1 || bc.counts[0] != 1.0 || bc.counts[1 + 2 * 3] != 1.0 || bc.counts[0 + 2 * 3] != 1.0) bad |= 128;
+  }
   std::printf("shim_path models=%lld lambda_max=%.6g final_objective=%.9g status=%d\n",
               static_cast<long long>(path.n_models()), path.lambda_max_value, path.objectives.back(), bad);
   return bad;
