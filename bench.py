@@ -246,7 +246,7 @@ def run_ours(args):
     if os.path.exists(tfile):
         with open(tfile) as f:
             traffic = json.load(f)
-    rho = {"fused_pass": {"kernel": "k_fused_fast (mode-1 H-last + v(eta-z)^2 + V.* + G-first, one n-array pass)",
+    rho = {"fused_pass": {"kernel": "k_fused_mma (mode-1 H-last + v eta^2 + V.* + G-first on DMMA m8n8k4, one n-array pass)",
                           "bytes_per_launch": f_bytes, "avg_launch_ms": f_ms,
                           "achieved": f_bytes / (f_ms / 1000.0) / 1e9, "frac": f_bytes / (f_ms / 1000.0) / 1e9 / hbm},
            "contraction": {"kernel": "k_contract_rs (largest banded H-chain step)", "bytes_per_launch": c_bytes,

@@ -444,7 +444,19 @@ static FusedPlan plan_for(const FusedArgs& f, int variant) {
   return pl;
 }
 
+struct LcPlan {  // DMMA fused pass (k_fused_mma)
+  FusedPlan pl;
+  int sw = 0, wp_off = 0, mw = 0, grid = 0, bs = 256;
+  size_t smem = 0;
+  bool ok = false;
+};
+static LcPlan lc_plan(const FusedArgs& f);
+
 int fused_tma_grid(const FusedArgs& f, int variant) {
+  if (variant == FV_FISTA_EXP) {
+    const LcPlan P = lc_plan(f);
+    if (P.ok) return P.grid;
+  }
   const FusedPlan pl = plan_for(f, variant);
   const i64 ntiles = (f.m + pl.T - 1) / pl.T;
   const size_t sm = static_cast<size_t>(pl.nst) * pl.stage * sizeof(double);
@@ -508,7 +520,221 @@ bool fused_fast_ok(const FusedArgs& f, int variant) {
   return fused_tma_fits(f, variant) && f.n1 <= NT && f.p1 <= NT && f.H.maxlen <= 4 && f.G.maxlen <= 64;
 }
 
+// ------------------------------------------------- DMMA fused pass
+// FV_FISTA_EXP with the X1^T phase on the FP64 tensor cores:
+//  * phase A (as k_fused_fast): thread row i of X1, eta = X1 P for its cells,
+//    w = v eta, the partial of sum w eta, and w written to a padded tile Wp
+//    whose fibre stride SW is = 4 (mod 16), so that a DMMA B fragment (4
+//    consecutive rows x 8 fibres) is read without bank conflicts;
+//  * phase B: Q (p1 x T) = X1^T W as m8n8k4 DMMA tiles: a warp owns a group
+//    of kMmaK output rows (its A fragments, the banded X1^T window of the
+//    group, sit in registers) and sweeps 8-fibre column blocks, ks DMMAs per
+//    block over the group's input window.  The band's zeros ride along in
+//    the tile; the tensor-core work is far below the pass's HBM time.
+__device__ __forceinline__ void dmma_884(double& d0, double& d1, double a, double b) {
+  asm volatile("mma.sync.aligned.m8n8k4.row.col.f64.f64.f64.f64 {%0, %1}, {%2}, {%3}, {%0, %1};"
+               : "+d"(d0), "+d"(d1)
+               : "d"(a), "d"(b));
+}
+
+template <int KS, int BS>
+__global__ void __launch_bounds__(BS) k_fused_mma(FusedArgs f, FusedPlan pl, i64 ntiles, int sw, int wp_off) {
+  extern __shared__ __align__(128) double sm[];
+  __shared__ unsigned long long bar[kMaxStages];
+  __shared__ double red[32];
+  constexpr int NW = BS / 32;
+  const int n1 = static_cast<int>(f.n1), p1 = static_cast<int>(f.p1), T = pl.T;
+  const int nst = pl.nst;
+  double* Wp = sm + wp_off;
+  if (threadIdx.x == 0) {
+    for (int k = 0; k < nst; ++k) mbar_init(&bar[k], 1);
+    asm volatile("fence.mbarrier_init.release.cluster;" ::: "memory");
+  }
+  auto issue = [&](i64 tile, int s) {
+    const i64 c0 = tile * T;
+    const i64 Tc = min(static_cast<i64>(T), f.m - c0);
+    double* st = sm + static_cast<i64>(s) * pl.stage;
+    unsigned bytes = 0;
+    bytes += stage_manual(st + pl.offP, f.P + c0 * p1, p1 * Tc);
+    bytes += stage_manual(st + pl.offA, f.v + c0 * n1, n1 * Tc);
+    fence_proxy_async();
+    mbar_expect_tx(&bar[s], bytes);
+    stage_bulk(st + pl.offP, f.P + c0 * p1, p1 * Tc, &bar[s]);
+    stage_bulk(st + pl.offA, f.v + c0 * n1, n1 * Tc, &bar[s]);
+  };
+  const int tid = static_cast<int>(threadIdx.x), lane = tid & 31, warp = tid >> 5;
+  const int CGA = BS / n1;
+  const bool actA = tid < n1 * CGA;
+  const int iA = actA ? tid % n1 : 0, cgA = actA ? tid / n1 : 0;
+  // X1 row band as exactly 4 taps on a window clamped into [0, p1) (zeros
+  // outside the band; the host guarantees p1 >= 4)
+  int loA = 0;
+  double cA[4] = {0.0, 0.0, 0.0, 0.0};
+  if (actA) {
+    const int lo = __ldg(f.H.lo + iA), len = __ldg(f.H.len + iA);
+    const double* cf = f.H.coef + __ldg(f.H.off + iA);
+    loA = min(lo, p1 - 4);
+#pragma unroll
+    for (int t = 0; t < 4; ++t) {
+      const int j = loA + t - lo;
+      cA[t] = (j >= 0 && j < len) ? __ldg(cf + j) : 0.0;
+    }
+  }
+  // phase B: fragments of the warp's row group (fixed when groups divides NW)
+  const int groups = f.mg.groups;
+  int cur_g = -1, gbase = 0;
+  double afr[KS];
+  auto load_group = [&](int g) {
+    cur_g = g;
+    gbase = __ldg(f.mg.base + g);
+#pragma unroll
+    for (int s2 = 0; s2 < KS; ++s2) afr[s2] = __ldg(f.mg.afrag + (static_cast<i64>(g) * KS + s2) * 32 + lane);
+  };
+  const bool fixed = NW % groups == 0;
+  if (fixed) load_group(warp % groups);
+  __syncthreads();
+  double acc = 0.0;
+  int s = 0;
+  unsigned phase_bits = 0u;
+  i64 tile = blockIdx.x;
+  if (threadIdx.x == 0)
+    for (int k = 0; k < nst; ++k)
+      if (tile + static_cast<i64>(k) * gridDim.x < ntiles) issue(tile + static_cast<i64>(k) * gridDim.x, k);
+  for (; tile < ntiles; tile += gridDim.x) {
+    const i64 c0 = tile * T;
+    const int Tc = static_cast<int>(min(static_cast<i64>(T), f.m - c0));
+    double* st = sm + static_cast<i64>(s) * pl.stage;
+    const double* Ps = st + pl.offP + stage_shift(f.P + c0 * p1);
+    const double* As = st + pl.offA + stage_shift(f.v + c0 * n1);
+    mbar_wait(&bar[s], (phase_bits >> s) & 1u);
+    phase_bits ^= 1u << s;
+    if (actA) {
+      auto cell = [&](int col) {
+        const double* pc = Ps + p1 * col + loA;
+        const double eta = fma(cA[1], pc[1], cA[0] * pc[0]) + fma(cA[3], pc[3], cA[2] * pc[2]);
+        const double w = As[iA + n1 * col] * eta;
+        acc = fma(w, eta, acc);
+        Wp[iA + sw * col] = w;
+      };
+      int col = cgA;
+      for (; col + CGA < Tc; col += 2 * CGA) {
+        cell(col);
+        cell(col + CGA);
+      }
+      if (col < Tc) cell(col);
+    }
+    __syncthreads();
+    const int cbs = (Tc + 7) >> 3;
+    auto block = [&](int g, int cb) {
+      // B fragment: row (lane % 4) of the k-step, fibre 8 cb + lane / 4
+      const double* wb = Wp + sw * (8 * cb + (lane >> 2)) + gbase + (lane & 3);
+      double d0 = 0.0, d1 = 0.0;
+#pragma unroll
+      for (int s2 = 0; s2 < KS; ++s2) dmma_884(d0, d1, afr[s2], wb[4 * s2]);
+      // D fragment: row k = kMmaK g + lane / 4, fibres 8 cb + 2 (lane % 4) + {0, 1}
+      const int k = kMmaK * g + (lane >> 2), colq = 8 * cb + 2 * (lane & 3);
+      if (k < p1) {
+        double* q = f.Q + (c0 + colq) * p1 + k;
+        if (colq < Tc) q[0] = d0;
+        if (colq + 1 < Tc) q[p1] = d1;
+      }
+    };
+    if (fixed) {
+      for (int cb = warp / groups; cb < cbs; cb += NW / groups) block(cur_g, cb);
+    } else {
+      for (int task = warp; task < groups * cbs; task += NW) {
+        const int g = task % groups;
+        if (g != cur_g) load_group(g);
+        block(g, task / groups);
+      }
+    }
+    __syncthreads();  // stage s and Wp are free again
+    const i64 next = tile + static_cast<i64>(nst) * gridDim.x;
+    if (threadIdx.x == 0 && next < ntiles) issue(next, s);
+    s = s + 1 == nst ? 0 : s + 1;
+  }
+  const double r = block_sum(acc, red);
+  if (threadIdx.x == 0) f.partial[blockIdx.x] = r;
+}
+
+static LcPlan lc_plan(const FusedArgs& f) {
+  LcPlan P;
+  static const bool enabled = [] {
+    const char* e = std::getenv("KG_FUSED_MMA");
+    return e == nullptr || std::atoi(e) != 0;
+  }();
+  // CTA shape: threads and the shared-memory budget per CTA (measured best on B200:
+  // 256 threads, 72 KB, two stages -> three CTAs per SM for C5)
+  static const int bs = [] {
+    const char* e = std::getenv("KG_MMA_BS");
+    return (e && std::atoi(e) == 512) ? 512 : 256;
+  }();
+  static const i64 budget_kb = [] {
+    const char* e = std::getenv("KG_MMA_KB");
+    const long v = e ? std::atol(e) : 72;
+    return static_cast<i64>(v >= 24 && v <= 210 ? v : 72);
+  }();
+  static const int nst = [] {
+    const char* e = std::getenv("KG_MMA_STAGES");
+    const int v = e ? std::atoi(e) : 2;
+    return v >= 2 && v <= kMaxStages ? v : 2;
+  }();
+  if (!enabled || f.mg.ks == 0 || f.n1 > bs || f.H.maxlen > 4 || f.p1 < 4) return P;
+  P.mw = f.mg.ks;  // 8, 12 or 16 (padded on the host)
+  P.bs = bs;
+  P.sw = static_cast<int>((f.n1 + 15) / 16 * 16 + 4);  // >= n1, = 4 (mod 16)
+  if (P.sw - 16 >= f.n1) P.sw -= 16;
+  auto up2 = [](i64 x) { return (x + 2) & ~i64(1); };
+  // nst stages of (P tile, v tile), then the padded w tile (whole 8-fibre blocks)
+  const i64 per_fibre = nst * (f.p1 + f.n1) + P.sw;
+  i64 T = (budget_kb * 1024 / 8 - 64) / per_fibre;
+  if (T >= 8) T = T / 8 * 8;  // whole 8-fibre DMMA column blocks
+  T = std::min<i64>(T, f.m);
+  if (T < 4) return P;
+  FusedPlan& pl = P.pl;
+  pl.T = static_cast<int>(T);
+  pl.nst = nst;
+  pl.offP = 0;
+  pl.offA = static_cast<int>(up2(f.p1 * T));
+  pl.offB = pl.offA;
+  pl.stage = static_cast<int>(up2(f.p1 * T) + up2(f.n1 * T));
+  P.wp_off = nst * pl.stage;
+  const i64 wcols = (T + 7) / 8 * 8;
+  P.smem = sizeof(double) * static_cast<size_t>(P.wp_off + P.sw * wcols);
+  const int per_sm = std::max<int>(1, static_cast<int>((226 * 1024) / (P.smem + 2048)));
+  const i64 ntiles = (f.m + T - 1) / T;
+  P.grid = static_cast<int>(std::min<i64>(ntiles, 148LL * std::min(per_sm, 2048 / bs)));
+  P.ok = P.smem <= 210 * 1024;
+  return P;
+}
+
+template <int KS>
+static void launch_mma(const Launch& L, const FusedArgs& f, const LcPlan& P, i64 ntiles) {
+  if (P.bs == 512) {
+    KG_CUDA(cudaFuncSetAttribute(k_fused_mma<KS, 512>, cudaFuncAttributeMaxDynamicSharedMemorySize,
+                                 static_cast<int>(P.smem)));
+    k_fused_mma<KS, 512><<<P.grid, 512, P.smem, L.s>>>(f, P.pl, ntiles, P.sw, P.wp_off);
+  } else {
+    KG_CUDA(cudaFuncSetAttribute(k_fused_mma<KS, 256>, cudaFuncAttributeMaxDynamicSharedMemorySize,
+                                 static_cast<int>(P.smem)));
+    k_fused_mma<KS, 256><<<P.grid, 256, P.smem, L.s>>>(f, P.pl, ntiles, P.sw, P.wp_off);
+  }
+}
+
 void fused_tma(const Launch& L, int variant, const FusedArgs& f) {
+  if (variant == FV_FISTA_EXP) {
+    const LcPlan P = lc_plan(f);
+    if (P.ok) {
+      const i64 nt = (f.m + P.pl.T - 1) / P.pl.T;
+      switch (P.mw) {
+        case 8: launch_mma<8>(L, f, P, nt); break;
+        case 12: launch_mma<12>(L, f, P, nt); break;
+        default: launch_mma<16>(L, f, P, nt); break;
+      }
+      launched(L);
+      return;
+    }
+  }
   const FusedPlan pl = plan_for(f, variant);
   const i64 ntiles = (f.m + pl.T - 1) / pl.T;
   const size_t sm = static_cast<size_t>(pl.nst) * pl.stage * sizeof(double);

@@ -123,8 +123,21 @@ void contract(const Launch& L, const double* A, double* out, i64 a, i64 K, i64 M
 // objective sum v (eta - z)^2 = sum v eta^2 - 2 <b, x> + sum v z^2 with
 // b = X^T (v .* z) (the Gram route's identity, applied on the n-space route).
 enum FusedVariant { FV_FISTA = 0, FV_XTWZ = 1, FV_SCORE0 = 2, FV_FISTA_EXP = 3 };
+// X1^T of a banded factor as FP64 tensor-core (DMMA m8n8k4) A fragments for
+// the fused pass: output rows k in groups of kMmaK; group g reads the input
+// window [base[g], base[g] + 4 ks) and afrag[(g ks + s) 32 + lane] is the A
+// element lane holds at k-step s, X1[base[g] + 4 s + lane % 4, kMmaK g +
+// lane / 4] (zero outside the band).  Built on the host at factor upload.
+constexpr int kMmaK = 8;
+struct MmaOp {
+  const int* base = nullptr;
+  const double* afrag = nullptr;
+  int ks = 0, groups = 0;
+};
+
 struct FusedArgs {
   i64 n1 = 0, p1 = 0, m = 0;  // mode-1 extents and the number of mode-1 fibres (n / n1)
+  MmaOp mg;                    // the G operator as DMMA fragments (ks == 0: unavailable)
   int T = 1;                   // fibres per CTA
   BandOp H, G;                 // mode-1 operators
   const double* P = nullptr;   // p1 x m H-partial (FISTA)

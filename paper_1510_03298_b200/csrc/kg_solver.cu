@@ -214,7 +214,55 @@ struct FactorOwn {
   FactorDev dev;
   DBuf X, hlo, hlen, hoff, hcoef, glo, glen, goff, gcoef, rblo, rbcoef;
   std::vector<int> h_lo, h_len, g_lo, g_len;  // host copies for launch planning
+  DBuf mbase, mfrag;                          // X^T as DMMA fragments (fused pass)
+  MmaOp mg;
 };
+
+// X^T as DMMA A fragments for the fused pass (see MmaOp).
+static void build_mma(const FactorHost& h, const std::vector<int>& glo, const std::vector<int>& glen, FactorOwn& f,
+                      cudaStream_t st) {
+  const i64 p = h.p, n = h.n;
+  const int groups = static_cast<int>((p + kMmaK - 1) / kMmaK);
+  int W = 0;
+  std::vector<int> lo(static_cast<size_t>(groups), 0);
+  for (int g = 0; g < groups; ++g) {
+    int a = INT32_MAX, b = 0;
+    for (i64 k = static_cast<i64>(g) * kMmaK; k < std::min<i64>(p, (g + 1) * kMmaK); ++k)
+      if (glen[k] > 0) {
+        a = std::min(a, glo[k]);
+        b = std::max(b, glo[k] + glen[k]);
+      }
+    if (a == INT32_MAX) a = b = 0;
+    lo[static_cast<size_t>(g)] = a;
+    W = std::max(W, b - a);
+  }
+  // k-steps padded to the kernel's unrolled counts (8, 12, 16), zero fragments
+  // past the band, so the DMMA loop carries no predicates
+  const int need = (std::max(W, 1) + 3) / 4;
+  const int ks = need <= 8 ? 8 : need <= 12 ? 12 : need <= 16 ? 16 : 0;
+  if (ks == 0 || 4 * ks > n) return;  // window too wide or the factor too short: k_fused_fast only
+  std::vector<int> base(static_cast<size_t>(groups));
+  std::vector<double> frag(static_cast<size_t>(groups) * ks * 32, 0.0);
+  for (int g = 0; g < groups; ++g) {
+    const int b0 = static_cast<int>(std::min<i64>(lo[static_cast<size_t>(g)], n - 4 * ks));
+    base[static_cast<size_t>(g)] = b0;
+    for (int s2 = 0; s2 < ks; ++s2)
+      for (int lane = 0; lane < 32; ++lane) {
+        const i64 k = static_cast<i64>(g) * kMmaK + lane / 4;
+        const int r = b0 + 4 * s2 + lane % 4;
+        if (k < p && r >= glo[k] && r < glo[k] + glen[k])
+          frag[(static_cast<size_t>(g) * ks + s2) * 32 + lane] = h.X[r + n * k];
+      }
+  }
+  f.mbase.alloc(sizeof(int) * base.size());
+  f.mfrag.alloc(sizeof(double) * frag.size());
+  KG_CUDA(cudaMemcpyAsync(f.mbase.p, base.data(), sizeof(int) * base.size(), cudaMemcpyHostToDevice, st));
+  KG_CUDA(cudaMemcpyAsync(f.mfrag.p, frag.data(), sizeof(double) * frag.size(), cudaMemcpyHostToDevice, st));
+  f.mg.base = static_cast<const int*>(f.mbase.p);
+  f.mg.afrag = f.mfrag.d();
+  f.mg.ks = ks;
+  f.mg.groups = groups;
+}
 
 static uint64_t next_band_uid() {
   static uint64_t uid = 0;
@@ -256,6 +304,7 @@ static void upload_factor(const FactorHost& h, FactorOwn& f, cudaStream_t s) {
   };
   up(true, f.hlo, f.hlen, f.hoff, f.hcoef, f.dev.H, f.h_lo, f.h_len);
   up(false, f.glo, f.glen, f.goff, f.gcoef, f.dev.G, f.g_lo, f.g_len);
+  build_mma(h, f.g_lo, f.g_len, f, s);
   // row-blocked copy of the H operator when every group of kRB rows reads a
   // window of at most kRW inputs (B-spline rows: 4 nonzeros, slowly moving)
   const i64 rows = h.n, groups = (rows + kRB - 1) / kRB;
@@ -647,6 +696,7 @@ static FusedArgs fused_args(const Fit& F) {
   a.T = D.T;
   a.H = D.f[0][0]->dev.H;
   a.G = D.f[0][0]->dev.G;
+  a.mg = D.f[0][0]->mg;
   a.cell_base = D.cell_base;
   return a;
 }
