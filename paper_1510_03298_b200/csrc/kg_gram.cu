@@ -21,6 +21,8 @@ namespace {
 
 constexpr int NT = 256;  // p-space reduction kernels
 constexpr int kPollRows = 10;  // partial / flag rows per lane: up to 320 CTAs
+constexpr int kPathBS = 512;  // default worker width of k_gauss_path
+constexpr bool kPathCW = true;  // k_gauss_path runs a control warp beside the workers
 constexpr int kFlagCTAs = 64;  // k_gauss_path uses the flag barrier up to this many CTAs (measured: C1 gains, C2/C4 do not)
 
 __device__ __forceinline__ double soft(double z, double g) {
@@ -390,6 +392,37 @@ __device__ __forceinline__ void grid_sync(unsigned* bar, unsigned nb) {
   __syncthreads();
 }
 
+template <int ID, int N>
+__device__ __forceinline__ void named_sync() {
+  asm volatile("bar.sync %0, %1;" ::"n"(ID), "n"(N) : "memory");
+}
+template <int ID, int N>
+__device__ __forceinline__ void named_arrive() {
+  asm volatile("bar.arrive %0, %1;" ::"n"(ID), "n"(N) : "memory");
+}
+
+// grid_sync's arrive + wait for one thread (the caller orders the CTA's writes
+// before it, e.g. through a named barrier)
+__device__ __forceinline__ void grid_arrive_wait(unsigned* bar, unsigned nb) {
+  unsigned g, old;
+  asm volatile("ld.relaxed.gpu.global.u32 %0, [%1];" : "=r"(g) : "l"(bar + 1) : "memory");
+  asm volatile("atom.acq_rel.gpu.global.add.u32 %0, [%1], 1;" : "=r"(old) : "l"(bar) : "memory");
+  if (old == nb - 1) {
+    asm volatile("st.relaxed.gpu.global.u32 [%0], 0;" ::"l"(bar) : "memory");
+    asm volatile("red.release.gpu.global.add.u32 [%0], 1;" ::"l"(bar + 1) : "memory");
+  } else {
+    unsigned cur;
+    const long long t0 = clock64();
+    do {
+      asm volatile("ld.acquire.gpu.global.u32 %0, [%1];" : "=r"(cur) : "l"(bar + 1) : "memory");
+      if (clock64() - t0 > async::kWatchdogCycles) {
+        printf("kg watchdog: grid barrier (block %d of %u, generation %u)\n", blockIdx.x, nb, g);
+        __trap();
+      }
+    } while (cur == g);
+  }
+}
+
 }  // namespace
 
 template <int BS>
@@ -563,9 +596,30 @@ __global__ void __launch_bounds__(BS) k_fista_persist(PersistArgs P) {
 //   f_new from (<best,b>, <best,S'best>, |best|) -> accept if f_new <= f_cur;
 //   status / truncation / first-model failure as path.cpp:64-73;
 //   the model's coefficients are written straight into the result buffer.
-template <int BS>
-__global__ void __launch_bounds__(BS) k_gauss_path(PersistArgs P) {
+constexpr int kMmLD = 36;  // padded leading dimension (= 4 mod 16 doubles: conflict-free DMMA fragments)
+
+// DMMA in-slab contraction of k_gauss_path: d = 3, both in-slab extents <= 32,
+// staged bands
+__host__ __device__ inline bool path_mm(const GramStepArgs& A) {
+  return A.d == 3 && A.dims[0] <= 32 && A.dims[1] <= 32 && A.G[0].maxlen <= kPathTaps && A.G[1].maxlen <= kPathTaps;
+}
+__host__ __device__ inline int path_qb(const GramStepArgs& A) {  // size of each contraction buffer
+  return path_mm(A) ? (A.q > kMmLD * 32 ? A.q : kMmLD * 32) : A.q;
+}
+
+__device__ __forceinline__ void dmma_884(double& d0, double& d1, double a, double b) {
+  asm volatile("mma.sync.aligned.m8n8k4.row.col.f64.f64.f64.f64 {%0, %1}, {%2}, {%3}, {%0, %1};"
+               : "+d"(d0), "+d"(d1)
+               : "d"(a), "d"(b));
+}
+
+template <int BS, bool CW>
+__global__ void __launch_bounds__(BS + (CW ? 32 : 0), 1) k_gauss_path(PersistArgs P) {
   constexpr int MB = kPathTaps;
+  // CW: one extra control warp (threads BS..BS+31) runs the grid barrier, the
+  // band copy and the monitor of the nu = 1 loop while the BS worker threads
+  // contract; it owns no elements (tx is past every element / row range)
+  const int tx = (CW && threadIdx.x >= BS) ? (1 << 30) : static_cast<int>(threadIdx.x);
   extern __shared__ __align__(16) double sm[];
   __shared__ double red[3 * 32 + 3];
   __shared__ FistaCtl cs;
@@ -584,14 +638,22 @@ __global__ void __launch_bounds__(BS) k_gauss_path(PersistArgs P) {
   double* bs = sbst + q;
   double* th = bs + q;
   double* sth = th + q;
+  // mm: the two in-slab modes of a d = 3 design (p1, p2 <= 32) run as DMMA
+  // tiles over padded (ld kMmLD) buffers and dense padded Gram matrices
+  const bool mm = path_mm(A) && !(P.dbg & (1024 | 1));  // needs the staged bands (dbg & 1 disables staging)
+  const int qb = path_qb(A);
   double* u = sth + q;
-  double* t0 = u + q;
-  double* t1 = t0 + q;
-  double* band = t1 + q;  // maxlen * q + 2
+  double* t0 = u + qb;
+  double* t1 = t0 + qb;
+  double* band = t1 + qb;  // maxlen * q + 2
+  double* gd0 = band + static_cast<i64>(A.Gd.maxlen) * q + 2;  // mm: G_0 (kMmLD x 32), then G_1
+  double* gd1 = gd0 + kMmLD * 32;
+  __shared__ int2 kr[2][4];  // mm: k-step range of each 8-row block of G_0 / G_1
+  __shared__ double rbuf[3 * BS];  // per-thread objective partials of compute()
   // Gram bands of modes 0 .. d-2 staged in shared memory (K_j x MB
   // coefficients, zero padded, then lo / len per row); mode j starts at
   // sg + MB * (dims[0] + .. + dims[j-1]) and sgi + 2 * (same)
-  double* sg = band + static_cast<i64>(A.Gd.maxlen) * q + 2;
+  double* sg = band + static_cast<i64>(A.Gd.maxlen) * q + 2 + (path_mm(A) ? 2 * kMmLD * 32 : 0);
   int rows_all = 0;
   bool staged = true;
   for (int j = 0; j < A.d - 1; ++j) {
@@ -603,7 +665,7 @@ __global__ void __launch_bounds__(BS) k_gauss_path(PersistArgs P) {
     int r0 = 0;
     for (int j = 0; j < A.d - 1; ++j) {
       const int K = A.dims[j];
-      for (int r = threadIdx.x; r < K; r += BS) {
+      for (int r = tx; r < K; r += BS) {
         const int ln = __ldg(A.G[j].len + r);
         const double* c = A.G[j].coef + __ldg(A.G[j].off + r);
         sgi[2 * r0 + r] = __ldg(A.G[j].lo + r);
@@ -626,12 +688,42 @@ __global__ void __launch_bounds__(BS) k_gauss_path(PersistArgs P) {
   for (int t = 0; t < MB; ++t) gr[t] = (hoist && t < len) ? __ldg(gc + t) : 0.0;
   const i64 base = static_cast<i64>(s) * q;
   const i64 p = static_cast<i64>(q) * nb;
-  for (int e = threadIdx.x; e < q; e += BS) {
+  for (int e = tx; e < q; e += BS) {
     th[e] = 0.0;  // fit_path starts from zero blocks (path.cpp:63); S'(0) = 0
     sth[e] = 0.0;
     bs[e] = A.b[base + e];
   }
   __syncthreads();  // staged bands, mbarrier and the replicated theta state are read by every warp
+  if (mm) {
+    // dense G_j[r, c] at gdj[r + kMmLD c] (zero outside the band and past p_j),
+    // zeroed padding of u and t0 (never written below), k-step ranges
+    for (int i = tx; i < 2 * kMmLD * 32; i += BS) {
+      const int j = i / (kMmLD * 32), rc = i - j * (kMmLD * 32);
+      const int c = rc / kMmLD, r = rc - c * kMmLD;
+      const int K = A.dims[j], r0 = j == 0 ? 0 : A.dims[0];
+      double v = 0.0;
+      if (r < K && c < K) {
+        const int lo_r = sgi[2 * r0 + r], len_r = sgi[2 * r0 + K + r];
+        if (c >= lo_r && c < lo_r + len_r) v = sg[static_cast<i64>(r0) * MB + (c - lo_r) * K + r];
+      }
+      gd0[i] = v;
+    }
+    for (int i = tx; i < 2 * qb; i += BS) u[i] = 0.0;  // u and t0 are adjacent
+    if (tx < 8) {
+      const int j = tx >> 2, blk = tx & 3;
+      const int K = A.dims[j], r0 = j == 0 ? 0 : A.dims[0];
+      int kmin = 1 << 20, kmax = 0;
+      for (int r = 8 * blk; r < min(8 * blk + 8, K); ++r) {
+        const int lo_r = sgi[2 * r0 + r], len_r = sgi[2 * r0 + K + r];
+        if (len_r > 0) {
+          kmin = min(kmin, lo_r);
+          kmax = max(kmax, lo_r + len_r);
+        }
+      }
+      kr[j][blk] = kmin < kmax ? make_int2(kmin >> 2, (kmax + 3) >> 2) : make_int2(0, 0);
+    }
+    __syncthreads();
+  }
   unsigned parity = 0;
   const FistaCtl* tmpl = A.ctl;  // configuration (lambda filled per model); written back only at exit
   const double w = tmpl->sscale, n = tmpl->n, c0 = tmpl->ss_const;
@@ -646,15 +738,16 @@ __global__ void __launch_bounds__(BS) k_gauss_path(PersistArgs P) {
     }
   };
   // bulk-async copy of the neighbour band of slabs [lo, lo + len) of xsrc
-  auto issue = [&](const double* xsrc) {
+  auto issue_now = [&](const double* xsrc) {  // by one thread
     const double* xb = xsrc + static_cast<i64>(lo) * q;
-    if (threadIdx.x == 0) {
-      asm volatile("fence.proxy.async.global;" ::: "memory");
-      const unsigned bytes = async::stage_manual(band, xb, static_cast<i64>(len) * q);
-      async::fence_proxy_async();
-      async::mbar_expect_tx(&mb, bytes);
-      async::stage_bulk(band, xb, static_cast<i64>(len) * q, &mb);
-    }
+    asm volatile("fence.proxy.async.global;" ::: "memory");
+    const unsigned bytes = async::stage_manual(band, xb, static_cast<i64>(len) * q);
+    async::fence_proxy_async();
+    async::mbar_expect_tx(&mb, bytes);
+    async::stage_bulk(band, xb, static_cast<i64>(len) * q, &mb);
+  };
+  auto issue = [&](const double* xsrc) {
+    if (threadIdx.x == 0) issue_now(xsrc);
   };
   auto wait_band = [&]() {
     async::mbar_wait(&mb, parity);
@@ -662,9 +755,10 @@ __global__ void __launch_bounds__(BS) k_gauss_path(PersistArgs P) {
   };
   unsigned gen = 0;  // flag-barrier generation (same sequence in every CTA)
   // S'(x) of this slab from the staged band -> sxs; objective partials of xs -> dst
-  auto compute = [&](const double* xsrc, double* dst, int sc_, int ss_) {  // dst[c * sc_ + s * ss_]
+  auto compute = [&](const double* xsrc, double* dst, int sc_, int ss_, int skip = 0) {  // dst[c * sc_ + s * ss_]
+    if (CW && threadIdx.x >= BS) return;  // workers only (named barrier 3)
     const double* xin = band + async::stage_shift(xsrc + static_cast<i64>(lo) * q);
-    for (int e = threadIdx.x; e < q; e += BS) {
+    for (int e = (skip & 1) ? q : tx; e < q; e += BS) {
       const double* xe = xin + e;
       double a0 = 0.0, a1 = 0.0;
       if (hoist) {
@@ -681,13 +775,58 @@ __global__ void __launch_bounds__(BS) k_gauss_path(PersistArgs P) {
         }
         if (t < len) a0 = fma(__ldg(gc + t), xe[static_cast<i64>(t) * q], a0);
       }
-      u[e] = a0 + a1;
+      if (mm) {
+        const int m = static_cast<int>(A.fa[1].div(static_cast<uint32_t>(e)));
+        u[e - m * A.dims[0] + kMmLD * m] = a0 + a1;
+      } else {
+        u[e] = a0 + a1;
+      }
     }
-    __syncthreads();
+    named_sync<3, BS>();
     const double* res = u;
+    if (mm && !(skip & 2)) {
+      const int wp = threadIdx.x >> 5, ln = threadIdx.x & 31;
+      const int p1 = A.dims[0], p2 = A.dims[1];
+      const int n1t = (p1 + 7) >> 3, n2t = (p2 + 7) >> 3;
+      // mode 1: T = U G_1^T  (T[al, m] at t0[al + kMmLD m])
+      for (int tile = wp; tile < n1t * n2t; tile += BS / 32) {
+        const int tj = tile / n1t, ti = tile - tj * n1t;
+        const int al = 8 * ti + (ln >> 2);
+        const int2 r = kr[1][tj];
+        double d0 = 0.0, d1 = 0.0;
+        for (int ks = r.x; ks < r.y; ++ks) {
+          const int kk = 4 * ks + (ln & 3);
+          dmma_884(d0, d1, u[al + kMmLD * kk], gd1[8 * tj + (ln >> 2) + kMmLD * kk]);
+        }
+        const int m = 8 * tj + 2 * (ln & 3);
+        if (al < p1) {
+          if (m < p2) t0[al + kMmLD * m] = d0;
+          if (m + 1 < p2) t0[al + kMmLD * (m + 1)] = d1;
+        }
+      }
+      named_sync<3, BS>();
+      // mode 0: S = G_0 T, written unpadded (S[m, be] at t1[m + p1 be])
+      for (int tile = wp; tile < n1t * n2t; tile += BS / 32) {
+        const int tj = tile / n1t, ti = tile - tj * n1t;
+        const int m = 8 * ti + (ln >> 2);
+        const int2 r = kr[0][ti];
+        double d0 = 0.0, d1 = 0.0;
+        for (int ks = r.x; ks < r.y; ++ks) {
+          const int kk = 4 * ks + (ln & 3);
+          dmma_884(d0, d1, gd0[m + kMmLD * kk], t0[kk + kMmLD * (8 * tj + (ln >> 2))]);
+        }
+        const int be = 8 * tj + 2 * (ln & 3);
+        if (m < p1) {
+          if (be < p2) t1[m + p1 * be] = d0;
+          if (be + 1 < p2) t1[m + p1 * (be + 1)] = d1;
+        }
+      }
+      named_sync<3, BS>();
+      res = t1;
+    }
     int which = 0;
     int r0 = rows_all;
-    for (int j = A.d - 2; j >= 0; --j) {
+    for (int j = mm ? -1 : A.d - 2; j >= 0; --j) {
       double* dst2 = which ? t1 : t0;
       const int K = A.dims[j];
       r0 -= K;
@@ -696,21 +835,51 @@ __global__ void __launch_bounds__(BS) k_gauss_path(PersistArgs P) {
                              sgi + 2 * r0 + K);
       else
         smem_mode<BS>(res, dst2, A.dims, j, A.G[j], q, A.fa[j], A.fk[j]);
-      __syncthreads();
+      named_sync<3, BS>();
       res = dst2;
       which ^= 1;
     }
+    if (skip & 4) return;
     double dots = 0.0, l1 = 0.0, l2 = 0.0;
-    for (int e = threadIdx.x; e < q; e += BS) {
+    for (int e = tx; e < q; e += BS) {
       const double sv = res[e], xv = xs[e];
       sxs[e] = sv;
       dots += xv * (w * sv - 2.0 * bs[e]);
       l1 += fabs(xv);
       l2 = fma(xv, xv, l2);
     }
-    // CTA partials for thread 0 only: one barrier (red is next written after
-    // the following grid barrier)
+    // CTA partials for thread 0 only: one barrier (red / rbuf are next written
+    // after the following grid barrier)
     const int wp = threadIdx.x >> 5, ln = threadIdx.x & 31;
+    if (!(P.dbg & 32768)) {
+      // per-thread partials to shared memory, then warp 0 sums them in a fixed
+      // order (lane-strided, then the warp tree): only the threads that own
+      // elements take part, and no shuffle traffic from idle warps
+      const int nact = q < BS ? q : BS;
+      if (static_cast<int>(threadIdx.x) < nact) {
+        rbuf[threadIdx.x] = dots;
+        rbuf[BS + threadIdx.x] = l1;
+        rbuf[2 * BS + threadIdx.x] = l2;
+      }
+      named_sync<3, BS>();
+      if (wp == 0) {
+        double r0 = 0.0, r1 = 0.0, r2 = 0.0;
+        for (int i = ln; i < nact; i += 32) {
+          r0 += rbuf[i];
+          r1 += rbuf[BS + i];
+          r2 += rbuf[2 * BS + i];
+        }
+        r0 = warp_sum(r0);
+        r1 = warp_sum(r1);
+        r2 = warp_sum(r2);
+        if (ln == 0) {
+          dst[s * ss_] = r0;
+          dst[sc_ + s * ss_] = r1;
+          dst[2 * sc_ + s * ss_] = r2;
+        }
+      }
+      return;
+    }
     dots = warp_sum(dots);
     l1 = warp_sum(l1);
     l2 = warp_sum(l2);
@@ -719,7 +888,7 @@ __global__ void __launch_bounds__(BS) k_gauss_path(PersistArgs P) {
       red[32 + wp] = l1;
       red[64 + wp] = l2;
     }
-    __syncthreads();
+    named_sync<3, BS>();
     if (wp == 0) {
       double r0 = ln < (BS >> 5) ? red[ln] : 0.0;
       double r1 = ln < (BS >> 5) ? red[32 + ln] : 0.0;
@@ -742,7 +911,7 @@ __global__ void __launch_bounds__(BS) k_gauss_path(PersistArgs P) {
   };
   auto gather3 = [&](double* out) {  // fixed-order sum of every CTA's 3 partials
     double a = 0.0, b = 0.0, c = 0.0;
-    for (int r = threadIdx.x; r < static_cast<int>(nb); r += BS) {
+    for (int r = tx; r < static_cast<int>(nb); r += BS) {
       a += __ldcg(P.part + 3 * r);
       b += __ldcg(P.part + 3 * r + 1);
       c += __ldcg(P.part + 3 * r + 2);
@@ -751,11 +920,21 @@ __global__ void __launch_bounds__(BS) k_gauss_path(PersistArgs P) {
   };
 
   int stop = 0;  // 1 truncated, 2 first model failed
+  // phase timers (dbg & 128): update | grid barrier | monitor gather + control | band wait | contraction
+  const bool tim = (P.dbg & 128) && threadIdx.x == 0 && (s == 0 || s == static_cast<int>(nb) / 2);
+  long long ph[5] = {0, 0, 0, 0, 0}, tc = clock64(), nsteps = 0;
+  auto mark = [&](int i) {
+    if (tim) {
+      const long long now = clock64();
+      ph[i] += now - tc;
+      tc = now;
+    }
+  };
   for (int t = 0; t < P.n_lambda && !stop; ++t) {
     const double lam = P.lambdas[t];
     const double j_th = penalty_of(A.pen, A.alpha, tl1, tl2);
     const double f_cur = -(tb - 0.5 * w * tst) / n + lam * j_th;
-    for (int e = threadIdx.x; e < q; e += BS) {
+    for (int e = tx; e < q; e += BS) {
       xs[e] = xps[e] = bst[e] = th[e];
       sxs[e] = sxps[e] = sbst[e] = sth[e];
     }
@@ -768,7 +947,143 @@ __global__ void __launch_bounds__(BS) k_gauss_path(PersistArgs P) {
       ctl_setup(cs, g0, w);
     }
     __syncthreads();
-    if (!bt_div) {
+    if (CW && !bt_div && !cs.done) {
+      // nu = 1 with a control warp.  Workers: update -> arrive(1) -> wait for
+      // the band (issued by the control warp once the grid barrier passed) ->
+      // contract -> sync(2) for the monitor decision of step k-1.  Control warp:
+      // sync(1) -> grid barrier -> band copy -> gather + ctl_step of step k-1 ->
+      // arrive(2).  The decision therefore overlaps the band copy and the
+      // contraction instead of preceding them; the iterates and decisions are
+      // those of the single-role loop below.
+      const double delta = cs.delta, gamma = delta * lam;
+      const bool flagbar = nb <= kFlagCTAs && !(P.dbg & 64);
+      if (threadIdx.x >= BS) {
+        const int lane = threadIdx.x & 31;
+        bool done = false;
+        const bool ctim = (P.dbg & 512) && lane == 0 && (s == 0 || s == static_cast<int>(nb) / 2);
+        long long cph[4] = {0, 0, 0, 0}, cst = 0, cta_ = 0;
+        auto cmark = [&](int i) {
+          if (ctim) {
+            const long long now = clock64();
+            cph[i] += now - cta_;
+            cta_ = now;
+          }
+        };
+        for (i64 k = 1; !done; ++k) {
+          double* Xk = P.X + (k & 1) * p;
+          named_sync<1, BS + 32>();  // every worker's x_k is written
+          if (ctim) cta_ = clock64();
+          ++cst;
+          ++gen;
+          if (flagbar) {
+            if (lane == 0) asm volatile("st.release.gpu.global.u32 [%0], %1;" ::"l"(P.flags + s), "r"(gen) : "memory");
+            cmark(0);
+            const long long w0 = clock64();
+            for (;;) {
+              bool mine = true;
+#pragma unroll
+              for (int i = 0; i < kPollRows; ++i) {
+                const int r = lane + 32 * i;
+                if (r < static_cast<int>(nb)) {
+                  unsigned f;
+                  asm volatile("ld.acquire.gpu.global.u32 %0, [%1];" : "=r"(f) : "l"(P.flags + r) : "memory");
+                  mine = mine && f >= gen;
+                }
+              }
+              if (__all_sync(0xffffffffu, mine)) break;
+              if (!(P.dbg & 256)) __nanosleep(20);
+              if (clock64() - w0 > async::kWatchdogCycles) {
+                if (lane == 0) printf("kg watchdog: flag barrier (block %d, generation %u)\n", s, gen);
+                __trap();
+              }
+            }
+          } else {
+            if (lane == 0) grid_arrive_wait(P.bar, nb);
+            __syncwarp();
+          }
+          cmark(1);
+          double a = 0.0, b = 0.0, c = 0.0;  // objective partials of step k-1
+          if (k >= 2) {
+            const double* pp = P.part + ((k - 1) & 1) * 3 * static_cast<i64>(nb);
+#pragma unroll
+            for (int i = 0; i < kPollRows; ++i) {
+              const int r = lane + 32 * i;
+              if (r < static_cast<int>(nb)) {
+                a += __ldcg(pp + r);
+                b += __ldcg(pp + nb + r);
+                c += __ldcg(pp + 2 * nb + r);
+              }
+            }
+          }
+          __syncwarp();
+          if (lane == 0) issue_now(Xk);
+          cmark(2);
+          if (k >= 2) {
+            a = warp_sum(a);
+            b = warp_sum(b);
+            c = warp_sum(c);
+            if (lane == 0) ctl_step(cs, 0.5 * (a + c0) / n + lam * penalty_of(A.pen, A.alpha, b, c));
+          }
+          __syncwarp();
+          done = cs.done;
+          cmark(3);
+          named_arrive<2, BS + 32>();  // decision of step k-1 (or none at k = 1) is in cs
+        }
+        if (ctim && (t == 5 || t == 20))
+          printf("ctl cta %d lambda %d: %lld steps, cycles/step: release %lld poll %lld gather+issue %lld monitor %lld\n", s,
+                 t, cst, cph[0] / cst, cph[1] / cst, cph[2] / cst, cph[3] / cst);
+      } else {
+        for (i64 k = 1;; ++k) {
+          const double omega =
+              extrapolation == 0 ? static_cast<double>(k - 1) / static_cast<double>(k + 2) : 0.0;
+          double* Xk = P.X + (k & 1) * p;
+          mark(4);
+          for (int e = tx; e < q; e += BS) {
+            const double xi = xs[e], xpi = xps[e], sxi = sxs[e], sxpi = sxps[e];
+            const double yi = xi + omega * (xi - xpi);
+            const double syi = sxi + omega * (sxi - sxpi);
+            const double g = (w * syi - bs[e]) / n;
+            double ci = yi - delta * g;
+            if (lam > 0.0) ci = prox1(A.pen, A.alpha, gamma, ci);
+            xps[e] = xi;
+            xs[e] = ci;
+            sxps[e] = sxi;
+            Xk[base + e] = ci;
+          }
+          mark(0);
+          ++nsteps;
+          named_arrive<1, BS + 32>();
+          async::mbar_wait(&mb, parity);
+          parity ^= 1u;
+          mark(3);
+          compute(Xk, P.part + (k & 1) * 3 * static_cast<i64>(nb), static_cast<int>(nb), 1);
+          if ((P.dbg & 2048) && t == 5 && k == 5) {  // isolated cost of the contraction (workers only)
+            named_sync<3, BS>();
+            const long long c0_ = clock64();
+            for (int rep = 0; rep < 64; ++rep)
+              compute(Xk, P.part + (k & 1) * 3 * static_cast<i64>(nb), static_cast<int>(nb), 1, (P.dbg >> 12) & 7);
+            named_sync<3, BS>();
+            const long long c1_ = clock64();
+            if (threadIdx.x == 0 && (s == 0 || s == static_cast<int>(nb) / 2))
+              printf("cta %d: compute() alone %lld cycles\n", s, (c1_ - c0_) / 64);
+          }
+          mark(4);
+          named_sync<2, BS + 32>();
+          mark(2);
+          if (cs.copy_best) {  // best := x_{k-1} (still in the x_prev slot)
+            for (int e = tx; e < q; e += BS) {
+              bst[e] = xps[e];
+              sbst[e] = sxps[e];
+            }
+          }
+          if (cs.done) break;
+        }
+      }
+      __syncthreads();
+      if (threadIdx.x == 0) cs.copy_best = 0;  // applied above
+      __syncthreads();
+    }
+    if (!CW && !bt_div) {
       // nu = 1 (no restarts): x_k depends only on earlier iterates, omega_k =
       // (k-1)/(k+2) and the fixed step, so the monitor decision of iteration
       // k-1 is taken one step late, after the single grid barrier of step k,
@@ -779,7 +1094,8 @@ __global__ void __launch_bounds__(BS) k_gauss_path(PersistArgs P) {
         const double omega =
             extrapolation == 0 ? static_cast<double>(k - 1) / static_cast<double>(k + 2) : 0.0;
         double* Xk = P.X + (k & 1) * p;
-        for (int e = threadIdx.x; e < q; e += BS) {
+        mark(4);
+        for (int e = tx; e < q; e += BS) {
           const double xi = xs[e], xpi = xps[e], sxi = sxs[e], sxpi = sxps[e];
           const double yi = xi + omega * (xi - xpi);
           const double syi = sxi + omega * (sxi - sxpi);
@@ -796,6 +1112,8 @@ __global__ void __launch_bounds__(BS) k_gauss_path(PersistArgs P) {
         // pass, that CTA's objective partials of step k-1 (component-major,
         // double-buffered by parity), so the grid barrier and the monitor gather
         // cost one round trip after the last arrival
+        mark(0);
+        ++nsteps;
         ++gen;
         const bool flagbar = nb <= kFlagCTAs && !(P.dbg & 64);  // flag barrier for small grids, atomic otherwise
         if (flagbar)
@@ -820,13 +1138,14 @@ __global__ void __launch_bounds__(BS) k_gauss_path(PersistArgs P) {
                 }
               }
               if (__all_sync(0xffffffffu, mine)) break;
-              __nanosleep(20);
+              if (!(P.dbg & 256)) __nanosleep(20);
               if (clock64() - w0 > async::kWatchdogCycles) {
                 if (lane == 0) printf("kg watchdog: flag barrier (block %d, generation %u)\n", s, gen);
                 __trap();
               }
             }
           }
+          if (lane == 0) mark(1);
           double a = 0.0, b = 0.0, c = 0.0;  // objective partials of step k-1 (after the barrier)
           if (k >= 2) {
 #pragma unroll
@@ -856,14 +1175,16 @@ __global__ void __launch_bounds__(BS) k_gauss_path(PersistArgs P) {
         if (k >= 2) {
           __syncthreads();  // cs is read by every thread (written again only after the next barrier)
           if (cs.copy_best) {  // best := x_{k-1} (now in the x_prev slot; own elements only)
-            for (int e = threadIdx.x; e < q; e += BS) {
+            for (int e = tx; e < q; e += BS) {
               bst[e] = xps[e];
               sbst[e] = sxps[e];
             }
           }
         }
+        mark(2);
         async::mbar_wait(&mb, parity);  // always consume the copy (keeps the barrier phase)
         parity ^= 1u;
+        mark(3);
         if (cs.done) break;
         compute(Xk, P.part + (k & 1) * 3 * static_cast<i64>(nb), static_cast<int>(nb), 1);
       }
@@ -874,7 +1195,7 @@ __global__ void __launch_bounds__(BS) k_gauss_path(PersistArgs P) {
       const double omega = cs.omega, delta = cs.delta;
       const int restart = cs.restart, copy_best = cs.copy_best;
       const double gamma = delta * lam;
-      for (int e = threadIdx.x; e < q; e += BS) {
+      for (int e = tx; e < q; e += BS) {
         if (copy_best) {
           bst[e] = xs[e];
           sbst[e] = sxs[e];
@@ -904,7 +1225,7 @@ __global__ void __launch_bounds__(BS) k_gauss_path(PersistArgs P) {
     }
     // best := x if the last monitor left a copy pending (k_fista_finalize)
     double bb = 0.0, bsb = 0.0, bl1 = 0.0, bl2 = 0.0;
-    for (int e = threadIdx.x; e < q; e += BS) {
+    for (int e = tx; e < q; e += BS) {
       if (cs.copy_best) {
         bst[e] = xs[e];
         sbst[e] = sxs[e];
@@ -928,7 +1249,7 @@ __global__ void __launch_bounds__(BS) k_gauss_path(PersistArgs P) {
     double g4[4] = {0.0, 0.0, 0.0, 0.0};
     for (int k = 0; k < 4; ++k) {
       double a = 0.0;
-      for (int rr = threadIdx.x; rr < static_cast<int>(nb); rr += BS) a += __ldcg(P.part2 + 4 * rr + k);
+      for (int rr = tx; rr < static_cast<int>(nb); rr += BS) a += __ldcg(P.part2 + 4 * rr + k);
       g4[k] = cta_sum<BS>(a, red);
     }
     const int status = cs.converged ? KG_S_CONVERGED : (cs.diverged ? KG_S_INNER_DIVERGENCE : KG_S_MAX_ITERATIONS);
@@ -936,7 +1257,7 @@ __global__ void __launch_bounds__(BS) k_gauss_path(PersistArgs P) {
     if (!cs.diverged) {
       const double f_new = -(g4[0] - 0.5 * w * g4[1]) / n + lam * penalty_of(A.pen, A.alpha, g4[2], g4[3]);
       if (f_new <= f_cur) {  // outer.cpp:216-219
-        for (int e = threadIdx.x; e < q; e += BS) {
+        for (int e = tx; e < q; e += BS) {
           th[e] = bst[e];
           sth[e] = sbst[e];
         }
@@ -957,7 +1278,7 @@ __global__ void __launch_bounds__(BS) k_gauss_path(PersistArgs P) {
         P.iters_out[t] = cs.iterations;
       }
     } else {
-      for (int e = threadIdx.x; e < q; e += BS) P.coefs[static_cast<i64>(t) * p + base + e] = th[e];
+      for (int e = tx; e < q; e += BS) P.coefs[static_cast<i64>(t) * p + base + e] = th[e];
       if (s == 0 && threadIdx.x == 0) {
         P.obj_out[t] = f;
         P.iters_out[t] = cs.iterations;
@@ -971,24 +1292,64 @@ __global__ void __launch_bounds__(BS) k_gauss_path(PersistArgs P) {
     P.nmodels[1] = stop;
     *A.ctl = cs;
   }
+  if (tim && nsteps > 0)
+    printf("k_gauss_path cta %d: %lld steps, cycles/step: update %lld barrier %lld monitor %lld band %lld contract %lld\n", s,
+           nsteps, ph[0] / nsteps, ph[1] / nsteps, ph[2] / nsteps, ph[3] / nsteps, ph[4] / nsteps);
 }
 
 static size_t path_smem(const GramStepArgs& A) {
   size_t staged = 0;  // staged Gram bands of modes 0 .. d-2
   for (int j = 0; j < A.d - 1; ++j) staged += static_cast<size_t>(A.dims[j]) * (kPathTaps * sizeof(double) + 2 * sizeof(int));
-  return (static_cast<size_t>(12 + A.Gd.maxlen) * A.q + 4) * sizeof(double) + staged;
+  const size_t dense = path_mm(A) ? 2 * kMmLD * 32 : 0;  // padded G_0, G_1
+  return (static_cast<size_t>(9 + A.Gd.maxlen) * A.q + 3 * static_cast<size_t>(path_qb(A)) + 4 + dense) *
+             sizeof(double) +
+         staged;
 }
+
+// KG_PATH_CW=0 drops the control warp (single-role nu = 1 loop)
+static bool path_cw() {
+  static const bool cw = [] {
+    const char* e = std::getenv("KG_PATH_CW");
+    return e ? e[0] != '0' : kPathCW;
+  }();
+  return cw;
+}
+
+// CTA width of k_gauss_path: more threads per slab shorten each FISTA step's
+// dependent chain (fewer elements per thread, more warps to hide smem and FMA
+// latency); KG_PATH_BS overrides
+static int path_bs() {
+  static const int bs = [] {
+    const char* e = std::getenv("KG_PATH_BS");
+    const int v = e ? std::atoi(e) : kPathBS;
+    if (v == 1024 && path_cw()) return 512;  // 1024 + the control warp exceeds the CTA limit
+    return (v == 256 || v == 512 || v == 1024) ? v : kPathBS;
+  }();
+  return bs;
+}
+
+static const void* path_kernel(int bs) {
+  if (path_cw()) {
+    if (bs == 512) return reinterpret_cast<const void*>(k_gauss_path<512, true>);
+    return reinterpret_cast<const void*>(k_gauss_path<256, true>);
+  }
+  if (bs == 1024) return reinterpret_cast<const void*>(k_gauss_path<1024, false>);
+  if (bs == 512) return reinterpret_cast<const void*>(k_gauss_path<512, false>);
+  return reinterpret_cast<const void*>(k_gauss_path<256, false>);
+}
+
+static int path_threads() { return path_bs() + (path_cw() ? 32 : 0); }
 
 bool gauss_path_ok(const GramStepArgs& A) {
   const size_t sm = path_smem(A);
   if (sm > 200 * 1024 || A.pd > 32 * kPollRows) return false;  // the flag barrier polls <= 320 CTAs
   static bool attr = false;
   if (!attr) {
-    KG_CUDA(cudaFuncSetAttribute(k_gauss_path<256>, cudaFuncAttributeMaxDynamicSharedMemorySize, 210 * 1024));
+    KG_CUDA(cudaFuncSetAttribute(path_kernel(path_bs()), cudaFuncAttributeMaxDynamicSharedMemorySize, 210 * 1024));
     attr = true;
   }
   int per_sm = 0, dev = 0, nsm = 0;
-  KG_CUDA(cudaOccupancyMaxActiveBlocksPerMultiprocessor(&per_sm, k_gauss_path<256>, 256, sm));
+  KG_CUDA(cudaOccupancyMaxActiveBlocksPerMultiprocessor(&per_sm, path_kernel(path_bs()), path_threads(), sm));
   KG_CUDA(cudaGetDevice(&dev));
   KG_CUDA(cudaDeviceGetAttribute(&nsm, cudaDevAttrMultiProcessorCount, dev));
   return static_cast<i64>(per_sm) * nsm >= A.pd;
@@ -998,8 +1359,8 @@ void gauss_path(const Launch& L, const PersistArgs& P) {
   const size_t sm = path_smem(P.g);
   PersistArgs args = P;
   void* kargs[] = {&args};
-  KG_CUDA(cudaLaunchCooperativeKernel(reinterpret_cast<const void*>(k_gauss_path<256>),
-                                      dim3(static_cast<unsigned>(P.g.pd)), dim3(256), kargs, sm, L.s));
+  KG_CUDA(cudaLaunchCooperativeKernel(path_kernel(path_bs()), dim3(static_cast<unsigned>(P.g.pd)), dim3(path_threads()),
+                                      kargs, sm, L.s));
   launched(L);
 }
 
