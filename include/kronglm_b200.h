@@ -173,6 +173,12 @@ kg_status kg_result_coef(kg_path_result* res, int64_t t, double* out);
 kg_status kg_result_coefs(kg_path_result* res, int64_t first, int64_t count, double* out);
 void kg_result_free(kg_path_result* res);
 
+/* Page-locked host memory for result downloads (cudaHostAlloc): a
+ * kg_result_coefs copy into it runs at PCIe speed instead of through the
+ * driver's pageable staging.  Free with kg_host_free. */
+kg_status kg_host_alloc(size_t bytes, void** ptr);
+void kg_host_free(void* ptr);
+
 /* predict (path.cpp:83-89): eta = H(coef), mu = g^{-1}(eta).  Host buffers. */
 kg_status kg_predict(kg_ctx* ctx, const kg_design* design, int family, const double* coef, double* eta, double* mu);
 

@@ -79,6 +79,8 @@ _SIGS = {
     "kg_result_coef": (C.c_int, [_vp, _i64, _pd]),
     "kg_result_coefs": (C.c_int, [_vp, _i64, _i64, _pd]),
     "kg_result_free": (None, [_vp]),
+    "kg_host_alloc": (C.c_int, [C.c_size_t, _P(_vp)]),
+    "kg_host_free": (None, [_vp]),
     "kg_predict": (C.c_int, [_vp, _vp, C.c_int, _pd, _pd, _pd]),
     "kg_bspline_design": (C.c_int, [_i64, _pd, _i64, _i64, _pd]),
     "kg_default_basis_count": (_i64, [_i64, _i64]),

@@ -23,7 +23,9 @@ constexpr int NT = 256;  // p-space reduction kernels
 constexpr int kPollRows = 10;  // partial / flag rows per lane: up to 320 CTAs
 constexpr int kPathBS = 512;  // default worker width of k_gauss_path
 constexpr bool kPathCW = true;  // k_gauss_path runs a control warp beside the workers
-constexpr int kFlagCTAs = 64;  // k_gauss_path uses the flag barrier up to this many CTAs (measured: C1 gains, C2/C4 do not)
+constexpr int kFlagCTAs = 64;
+constexpr int kFlagStride = 32;  // one 128-byte line per CTA flag
+constexpr int kMonitorNap = 200;  // ns between polls of the grid-wide monitor wait  // k_gauss_path uses the flag barrier up to this many CTAs (measured: C1 gains, C2/C4 do not)
 
 __device__ __forceinline__ double soft(double z, double g) {
   const double m = fabs(z) - g;
@@ -650,6 +652,8 @@ __global__ void __launch_bounds__(BS + (CW ? 32 : 0), 1) k_gauss_path(PersistArg
   double* gd1 = gd0 + kMmLD * 32;
   __shared__ int2 kr[2][4];  // mm: k-step range of each 8-row block of G_0 / G_1
   __shared__ double rbuf[3 * BS];  // per-thread objective partials of compute()
+  // dbg & 65536: barrier / copy-issue / copy-latency / arrive-to-band cycles (one SM clock)
+  __shared__ long long tw1, tc1, tc2, dph[4];
   // Gram bands of modes 0 .. d-2 staged in shared memory (K_j x MB
   // coefficients, zero padded, then lo / len per row); mode j starts at
   // sg + MB * (dims[0] + .. + dims[j-1]) and sgi + 2 * (same)
@@ -679,6 +683,7 @@ __global__ void __launch_bounds__(BS + (CW ? 32 : 0), 1) k_gauss_path(PersistArg
     async::mbar_init(&mb, 1);
     async::mbar_init_fence();
     tb = tst = tl1 = tl2 = 0.0;
+    dph[0] = dph[1] = dph[2] = dph[3] = 0;
   }
   const int lo = __ldg(A.Gd.lo + s), len = __ldg(A.Gd.len + s);
   const double* gc = A.Gd.coef + __ldg(A.Gd.off + s);
@@ -755,7 +760,9 @@ __global__ void __launch_bounds__(BS + (CW ? 32 : 0), 1) k_gauss_path(PersistArg
   };
   unsigned gen = 0;  // flag-barrier generation (same sequence in every CTA)
   // S'(x) of this slab from the staged band -> sxs; objective partials of xs -> dst
-  auto compute = [&](const double* xsrc, double* dst, int sc_, int ss_, int skip = 0) {  // dst[c * sc_ + s * ss_]
+  // defer: leave the per-thread objective partials in rbuf for the control
+  // warp (no CTA reduction here)
+  auto compute = [&](const double* xsrc, double* dst, int sc_, int ss_, int skip = 0, bool defer = false) {  // dst[c * sc_ + s * ss_]
     if (CW && threadIdx.x >= BS) return;  // workers only (named barrier 3)
     const double* xin = band + async::stage_shift(xsrc + static_cast<i64>(lo) * q);
     for (int e = (skip & 1) ? q : tx; e < q; e += BS) {
@@ -851,6 +858,14 @@ __global__ void __launch_bounds__(BS + (CW ? 32 : 0), 1) k_gauss_path(PersistArg
     // CTA partials for thread 0 only: one barrier (red / rbuf are next written
     // after the following grid barrier)
     const int wp = threadIdx.x >> 5, ln = threadIdx.x & 31;
+    if (defer) {
+      if (static_cast<int>(threadIdx.x) < (q < BS ? q : BS)) {
+        rbuf[threadIdx.x] = dots;
+        rbuf[BS + threadIdx.x] = l1;
+        rbuf[2 * BS + threadIdx.x] = l2;
+      }
+      return;
+    }
     if (!(P.dbg & 32768)) {
       // per-thread partials to shared memory, then warp 0 sums them in a fixed
       // order (lane-strided, then the warp tree): only the threads that own
@@ -958,7 +973,17 @@ __global__ void __launch_bounds__(BS + (CW ? 32 : 0), 1) k_gauss_path(PersistArg
       const double delta = cs.delta, gamma = delta * lam;
       const bool flagbar = nb <= kFlagCTAs && !(P.dbg & 64);
       if (threadIdx.x >= BS) {
+        // control iteration k: (a) workers' x_k and the per-thread partials of
+        // step k-1 are in place; (b) reduce those into this CTA's partials of
+        // k-1 (triple-buffered by k mod 3); (c) release flag[s] = gen, which
+        // publishes x_k and the partials; (d) wait for the flags of the
+        // neighbour slabs this CTA's Gram band reads, then bulk-copy the band;
+        // (e) wait for every flag (all partials of k-1 are published), gather
+        // them and advance the replicated control block; (f) hand the decision
+        // of step k-1 to the workers.  Only (d) is on the workers' critical
+        // path; the grid-wide wait of (e) overlaps the contraction.
         const int lane = threadIdx.x & 31;
+        const int nact = q < BS ? q : BS;
         bool done = false;
         const bool ctim = (P.dbg & 512) && lane == 0 && (s == 0 || s == static_cast<int>(nb) / 2);
         long long cph[4] = {0, 0, 0, 0}, cst = 0, cta_ = 0;
@@ -969,42 +994,65 @@ __global__ void __launch_bounds__(BS + (CW ? 32 : 0), 1) k_gauss_path(PersistArg
             cta_ = now;
           }
         };
+        auto poll = [&](int r0_, int r1_, unsigned g_, int nap) {  // all flags in [r0_, r1_) reach g_
+          const long long w0 = clock64();
+          for (;; __nanosleep(nap)) {
+            bool mine = true;
+            for (int r = r0_ + lane; r < r1_; r += 32) {
+              unsigned f;
+              asm volatile("ld.acquire.gpu.global.u32 %0, [%1];" : "=r"(f) : "l"(P.flags + kFlagStride * r) : "memory");
+              mine = mine && f >= g_;
+            }
+            if (__all_sync(0xffffffffu, mine)) break;
+            if (clock64() - w0 > async::kWatchdogCycles) {
+              if (lane == 0) printf("kg watchdog: slab flags (block %d, generation %u)\n", s, g_);
+              __trap();
+            }
+          }
+        };
         for (i64 k = 1; !done; ++k) {
           double* Xk = P.X + (k & 1) * p;
-          named_sync<1, BS + 32>();  // every worker's x_k is written
+          named_sync<1, BS + 32>();  // every worker's x_k (and step k-1's partials) is written
+          long long w1_ = 0;
+          if ((P.dbg & 65536) && lane == 0) w1_ = *reinterpret_cast<volatile long long*>(&tw1);
           if (ctim) cta_ = clock64();
           ++cst;
           ++gen;
-          if (flagbar) {
-            if (lane == 0) asm volatile("st.release.gpu.global.u32 [%0], %1;" ::"l"(P.flags + s), "r"(gen) : "memory");
-            cmark(0);
-            const long long w0 = clock64();
-            for (;;) {
-              bool mine = true;
-#pragma unroll
-              for (int i = 0; i < kPollRows; ++i) {
-                const int r = lane + 32 * i;
-                if (r < static_cast<int>(nb)) {
-                  unsigned f;
-                  asm volatile("ld.acquire.gpu.global.u32 %0, [%1];" : "=r"(f) : "l"(P.flags + r) : "memory");
-                  mine = mine && f >= gen;
-                }
-              }
-              if (__all_sync(0xffffffffu, mine)) break;
-              if (!(P.dbg & 256)) __nanosleep(20);
-              if (clock64() - w0 > async::kWatchdogCycles) {
-                if (lane == 0) printf("kg watchdog: flag barrier (block %d, generation %u)\n", s, gen);
-                __trap();
-              }
-            }
-          } else {
-            if (lane == 0) grid_arrive_wait(P.bar, nb);
-            __syncwarp();
-          }
-          cmark(1);
-          double a = 0.0, b = 0.0, c = 0.0;  // objective partials of step k-1
           if (k >= 2) {
-            const double* pp = P.part + ((k - 1) & 1) * 3 * static_cast<i64>(nb);
+            double r0 = 0.0, r1 = 0.0, r2 = 0.0;  // fixed order: lane-strided, then the warp tree
+            for (int i = lane; i < nact; i += 32) {
+              r0 += rbuf[i];
+              r1 += rbuf[BS + i];
+              r2 += rbuf[2 * BS + i];
+            }
+            r0 = warp_sum(r0);
+            r1 = warp_sum(r1);
+            r2 = warp_sum(r2);
+            if (lane == 0) {
+              double* dst = P.part + ((k - 1) % 3) * 3 * static_cast<i64>(nb);
+              dst[s] = r0;
+              dst[nb + s] = r1;
+              dst[2 * nb + s] = r2;
+            }
+          }
+          if (lane == 0) asm volatile("st.release.gpu.global.u32 [%0], %1;" ::"l"(P.flags + kFlagStride * s), "r"(gen) : "memory");
+          cmark(0);
+          poll(lo, lo + len, gen, 0);
+          cmark(1);
+          if ((P.dbg & 65536) && lane == 0) {
+            const long long now = clock64();
+            dph[0] += now - w1_;
+            tc1 = now;
+          }
+          if (lane == 0) issue_now(Xk);
+          if ((P.dbg & 65536) && lane == 0) {
+            tc2 = clock64();
+            dph[1] += tc2 - tc1;
+          }
+          if (k >= 2) {
+            poll(0, static_cast<int>(nb), gen, kMonitorNap);  // off the critical path: back off
+            const double* pp = P.part + ((k - 1) % 3) * 3 * static_cast<i64>(nb);
+            double a = 0.0, b = 0.0, c = 0.0;  // objective partials of step k-1
 #pragma unroll
             for (int i = 0; i < kPollRows; ++i) {
               const int r = lane + 32 * i;
@@ -1014,11 +1062,7 @@ __global__ void __launch_bounds__(BS + (CW ? 32 : 0), 1) k_gauss_path(PersistArg
                 c += __ldcg(pp + 2 * nb + r);
               }
             }
-          }
-          __syncwarp();
-          if (lane == 0) issue_now(Xk);
-          cmark(2);
-          if (k >= 2) {
+            cmark(2);
             a = warp_sum(a);
             b = warp_sum(b);
             c = warp_sum(c);
@@ -1030,7 +1074,7 @@ __global__ void __launch_bounds__(BS + (CW ? 32 : 0), 1) k_gauss_path(PersistArg
           named_arrive<2, BS + 32>();  // decision of step k-1 (or none at k = 1) is in cs
         }
         if (ctim && (t == 5 || t == 20))
-          printf("ctl cta %d lambda %d: %lld steps, cycles/step: release %lld poll %lld gather+issue %lld monitor %lld\n", s,
+          printf("ctl cta %d lambda %d: %lld steps, cycles/step: reduce+release %lld neighbours %lld monitor wait+gather %lld control %lld\n", s,
                  t, cst, cph[0] / cst, cph[1] / cst, cph[2] / cst, cph[3] / cst);
       } else {
         for (i64 k = 1;; ++k) {
@@ -1052,11 +1096,19 @@ __global__ void __launch_bounds__(BS + (CW ? 32 : 0), 1) k_gauss_path(PersistArg
           }
           mark(0);
           ++nsteps;
+          if ((P.dbg & 65536) && threadIdx.x == 0) tw1 = clock64();
           named_arrive<1, BS + 32>();
           async::mbar_wait(&mb, parity);
           parity ^= 1u;
+          if ((P.dbg & 65536) && threadIdx.x == 0) {
+            const long long now = clock64();
+            if (k >= 2) {
+              dph[2] += now - tc2;
+              dph[3] += now - tw1;
+            }
+          }
           mark(3);
-          compute(Xk, P.part + (k & 1) * 3 * static_cast<i64>(nb), static_cast<int>(nb), 1);
+          compute(Xk, nullptr, 0, 0, 0, true);  // partials stay in rbuf for the control warp
           if ((P.dbg & 2048) && t == 5 && k == 5) {  // isolated cost of the contraction (workers only)
             named_sync<3, BS>();
             const long long c0_ = clock64();
@@ -1124,7 +1176,7 @@ __global__ void __launch_bounds__(BS + (CW ? 32 : 0), 1) k_gauss_path(PersistArg
           const int lane = threadIdx.x;
           const double* pp = P.part + ((k - 1) & 1) * 3 * static_cast<i64>(nb);
           if (flagbar) {
-            if (lane == 0) asm volatile("st.release.gpu.global.u32 [%0], %1;" ::"l"(P.flags + s), "r"(gen) : "memory");
+            if (lane == 0) asm volatile("st.release.gpu.global.u32 [%0], %1;" ::"l"(P.flags + kFlagStride * s), "r"(gen) : "memory");
             const long long w0 = clock64();
             for (;;) {  // flags only: light polling while the slowest CTA finishes
               bool mine = true;
@@ -1133,7 +1185,7 @@ __global__ void __launch_bounds__(BS + (CW ? 32 : 0), 1) k_gauss_path(PersistArg
                 const int r = lane + 32 * i;
                 if (r < static_cast<int>(nb)) {
                   unsigned f;
-                  asm volatile("ld.acquire.gpu.global.u32 %0, [%1];" : "=r"(f) : "l"(P.flags + r) : "memory");
+                  asm volatile("ld.acquire.gpu.global.u32 %0, [%1];" : "=r"(f) : "l"(P.flags + kFlagStride * r) : "memory");
                   mine = mine && f >= gen;
                 }
               }
@@ -1292,6 +1344,9 @@ __global__ void __launch_bounds__(BS + (CW ? 32 : 0), 1) k_gauss_path(PersistArg
     P.nmodels[1] = stop;
     *A.ctl = cs;
   }
+  if ((P.dbg & 65536) && threadIdx.x == 0 && (s == 0 || s == static_cast<int>(nb) / 2) && nsteps > 0)
+    printf("cta %d cycles/step: arrive->barrier done %lld, copy issue %lld, copy latency %lld, arrive->band %lld\n", s,
+           dph[0] / nsteps, dph[1] / nsteps, dph[2] / nsteps, dph[3] / nsteps);
   if (tim && nsteps > 0)
     printf("k_gauss_path cta %d: %lld steps, cycles/step: update %lld barrier %lld monitor %lld band %lld contract %lld\n", s,
            nsteps, ph[0] / nsteps, ph[1] / nsteps, ph[2] / nsteps, ph[3] / nsteps, ph[4] / nsteps);

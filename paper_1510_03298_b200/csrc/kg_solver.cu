@@ -671,11 +671,11 @@ static void alloc_fit(Fit& F) {
   const i64 pd = D.p[0][D.d - 1];
   F.gstep = D.c == 1 && D.d <= 4 && gram_step_fits(D.P / pd);
   if (F.gstep) {
-    F.gpart.alloc(sizeof(double) * 6 * pd);  // 3 per CTA, double-buffered (k_gauss_path)
+    F.gpart.alloc(sizeof(double) * 9 * pd);  // 3 per CTA, triple-buffered (k_gauss_path)
     F.pX.alloc(2 * pb);
     F.pbar.alloc(sizeof(unsigned) * 4);
     KG_CUDA(cudaMemsetAsync(F.pbar.p, 0, sizeof(unsigned) * 4, F.ctx->s));
-    F.pflags.alloc(sizeof(unsigned) * pd);
+    F.pflags.alloc(sizeof(unsigned) * 32 * pd);  // one 128-byte line per CTA (kFlagStride)
     F.gcount.alloc(sizeof(unsigned) * 4);
     KG_CUDA(cudaMemsetAsync(F.gcount.p, 0, sizeof(unsigned) * 4, F.ctx->s));
   }
@@ -2406,6 +2406,20 @@ kg_status kg_result_coefs(kg_path_result* r, int64_t first, int64_t count, doubl
   });
 }
 void kg_result_free(kg_path_result* r) { delete r; }
+
+kg_status kg_host_alloc(size_t bytes, void** ptr) {
+  if (!ptr) return KG_EINVAL;
+  *ptr = nullptr;
+  if (cudaHostAlloc(ptr, bytes ? bytes : 1, cudaHostAllocDefault) != cudaSuccess) {
+    cudaGetLastError();
+    *ptr = nullptr;
+    return KG_ENOMEM;
+  }
+  return KG_OK;
+}
+void kg_host_free(void* ptr) {
+  if (ptr) cudaFreeHost(ptr);
+}
 
 }  // extern "C"
 

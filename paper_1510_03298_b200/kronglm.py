@@ -399,25 +399,68 @@ def lambda_max(design, family, y, weights=None):
     return out.value
 
 
+class _PinnedBlock:
+    """One page-locked host block (kg_host_alloc).  Arrays handed out over it
+    keep it alive through their ``base`` chain; when the last one dies the
+    block returns to a small free list instead of being unpinned, so repeated
+    fits reuse it (pinning costs far more than the download it speeds up)."""
+    _free: list = []
+    _lock = threading.Lock()
+    _keep = 4  # cached blocks
+
+    def __init__(self, nbytes):
+        self.nbytes = nbytes
+        ptr = C.c_void_p()
+        if _lib.load().kg_host_alloc(nbytes, C.byref(ptr)) != 0:
+            raise MemoryError("kg_host_alloc(%d) failed" % nbytes)
+        self.ptr = ptr.value
+
+    @classmethod
+    def take(cls, nbytes):
+        with cls._lock:
+            for i, b in enumerate(cls._free):
+                if b.nbytes >= nbytes:
+                    return cls._free.pop(i)
+        return cls(nbytes)
+
+    def array(self, shape):
+        n = int(np.prod(shape))
+        raw = (C.c_double * n).from_address(self.ptr)
+        raw._block = self  # the ndarray's base keeps the block alive
+        return np.frombuffer(raw, dtype=np.float64).reshape(shape)
+
+    def __del__(self):
+        try:
+            with _PinnedBlock._lock:
+                if len(_PinnedBlock._free) < _PinnedBlock._keep:
+                    # resurrect into the free list (re-collected only when evicted)
+                    _PinnedBlock._free.append(_PinnedBlock._clone(self))
+                    return
+            _lib.load().kg_host_free(self.ptr)
+        except Exception:
+            pass
+
+    @classmethod
+    def _clone(cls, b):
+        c = cls.__new__(cls)
+        c.nbytes, c.ptr = b.nbytes, b.ptr
+        return c
+
+
 def fit_path(design, family, y, weights=None, penalty="lasso", alpha=0.0, n_lambda=100, lambda_min_ratio=1e-4,
              lambdas=None, iwls="exact", nu=1.0, tol=1e-8, maxit=100, inner_tol=1e-8, inner_maxit=2000):
     """Warm-started regularization path (path.cpp:29-81); same kwargs and result
     keys as kronglm_py.cpp:159-217, plus ``inner_iters`` and ``status``."""
     D = _design(design)
     obs = Observation(D, y, weights)
-    # The coefficient buffer's first-touch page faults (~9 ms for C2's 43 MB)
-    # are taken on a helper thread while the device fits the path (the ctypes
-    # calls release the GIL), so the download lands in resident pages.
+    # The coefficients land in a page-locked block (one PCIe-speed copy, no
+    # pageable staging); the returned arrays are views into it.
     n_max = len(lambdas) if lambdas is not None else int(n_lambda)
-    buf = np.empty((max(n_max, 1), D.p))
-    toucher = threading.Thread(target=C.memset, args=(buf.ctypes.data, 0, buf.nbytes), daemon=True)
-    toucher.start()
-    try:
-        res = fit_path_resident(D, obs, family, penalty, alpha, lambdas, n_lambda=n_lambda,
-                                lambda_min_ratio=lambda_min_ratio, iwls=iwls, nu=nu, tol=tol, maxit=maxit,
-                                inner_tol=inner_tol, inner_maxit=inner_maxit)
-    finally:
-        toucher.join()
+    shape = (max(n_max, 1), D.p)
+    buf = _PinnedBlock.take(8 * shape[0] * shape[1]).array(shape)
+    res = fit_path_resident(D, obs, family, penalty, alpha, lambdas, n_lambda=n_lambda,
+                            lambda_min_ratio=lambda_min_ratio, iwls=iwls, nu=nu, tol=tol, maxit=maxit,
+                            inner_tol=inner_tol, inner_maxit=inner_maxit)
     out = {"lambdas": list(res.lambdas), "objectives": list(res.objectives), "lambda_max": res.lambda_max,
            "truncated": res.truncated, "coefficients": [], "nonzero": [], "outer_iters": list(res.outer_iters),
            "converged": [s == "converged" for s in res.status], "inner_iters": list(res.inner_iters),

@@ -57,13 +57,14 @@ __global__ void k_probe(int mode, int rounds, int nstore, int fs, unsigned* flag
         for (;;) {
           bool mine = true;
           for (int r = lane; r < nb; r += 32) {
-            if (mode == 2 && (r < s - 3 || r > s + 3)) continue;
-            const unsigned f = (mode == 3) ? ld_relaxed(flags + r * fs) : ld_acquire(flags + r * fs);
+            if ((mode == 2 || mode >= 5) && (r < s - 3 || r > s + 3)) continue;
+            const unsigned f = (mode == 3 || mode == 6) ? ld_relaxed(flags + r * fs) : ld_acquire(flags + r * fs);
             mine = mine && f >= (unsigned)k;
           }
           if (__all_sync(0xffffffffu, mine)) break;
+          if (mode == 5) __nanosleep(100);
         }
-        if (mode == 3) asm volatile("fence.acq_rel.gpu;" ::: "memory");
+        if (mode == 3 || mode == 6) asm volatile("fence.acq_rel.gpu;" ::: "memory");
       }
     }
     __syncthreads();
@@ -83,11 +84,10 @@ int main() {
   long long h[4096];
   const int grids[] = {10, 120, 148};
   const int stores[] = {0, 900};
-  for (int fs : {1, 32})
-  for (int nst : stores)
-    for (int g : grids)
-      for (int mode = 0; mode < 5; ++mode) {
-        if (mode == 1 && fs == 32) continue;
+  for (int fs : {32})
+  for (int nst : {900})
+    for (int g : {10, 30, 60, 90, 120})
+      for (int mode : {1, 2, 5, 6}) {
         cudaMemset(flags, 0, 4096 * 4 * 32);
         cudaMemset(bar, 0, 64);
         k_probe<<<g, 544>>>(mode, 2000, nst, fs, flags, bar, data, out);
