@@ -640,11 +640,13 @@ __global__ void __launch_bounds__(BS + (CW ? 32 : 0), 1) k_gauss_path(PersistArg
   double* bs = sbst + q;
   double* th = bs + q;
   double* sth = th + q;
+  double* xpp = sth + q;  // CW: x_{k-2} and S'x_{k-2} (the monitor decision runs two steps late)
+  double* sxpp = xpp + q;
   // mm: the two in-slab modes of a d = 3 design (p1, p2 <= 32) run as DMMA
   // tiles over padded (ld kMmLD) buffers and dense padded Gram matrices
   const bool mm = path_mm(A) && !(P.dbg & (1024 | 1));  // needs the staged bands (dbg & 1 disables staging)
   const int qb = path_qb(A);
-  double* u = sth + q;
+  double* u = sxpp + q;
   double* t0 = u + qb;
   double* t1 = t0 + qb;
   double* band = t1 + qb;  // maxlen * q + 2
@@ -975,13 +977,14 @@ __global__ void __launch_bounds__(BS + (CW ? 32 : 0), 1) k_gauss_path(PersistArg
       if (threadIdx.x >= BS) {
         // control iteration k: (a) workers' x_k and the per-thread partials of
         // step k-1 are in place; (b) reduce those into this CTA's partials of
-        // k-1 (triple-buffered by k mod 3); (c) release flag[s] = gen, which
+        // k-1 (four buffers by k mod 4); (c) release flag[s] = gen, which
         // publishes x_k and the partials; (d) wait for the flags of the
-        // neighbour slabs this CTA's Gram band reads, then bulk-copy the band;
-        // (e) wait for every flag (all partials of k-1 are published), gather
+        // neighbour slabs this CTA's Gram band reads (the same CTAs read this
+        // slab: the band is symmetric), then bulk-copy the band; (e) wait for
+        // every flag of step k-1 (all partials of k-2 are published), gather
         // them and advance the replicated control block; (f) hand the decision
-        // of step k-1 to the workers.  Only (d) is on the workers' critical
-        // path; the grid-wide wait of (e) overlaps the contraction.
+        // of step k-2 to the workers.  Only (d) is on the workers' critical
+        // path; (e) waits on flags released a step earlier.
         const int lane = threadIdx.x & 31;
         const int nact = q < BS ? q : BS;
         bool done = false;
@@ -994,16 +997,26 @@ __global__ void __launch_bounds__(BS + (CW ? 32 : 0), 1) k_gauss_path(PersistArg
             cta_ = now;
           }
         };
-        auto poll = [&](int r0_, int r1_, unsigned g_, int nap) {  // all flags in [r0_, r1_) reach g_
+        // all flags in [r0_, r1_) reach g_.  A lane with several flags polls
+        // them with relaxed loads (an acquire load would serialise them: one
+        // L2 round trip each) and the acquire is one fence after success.
+        auto poll = [&](int r0_, int r1_, unsigned g_, int nap) {
           const long long w0 = clock64();
+          const bool multi = r1_ - r0_ > 32;
           for (;; __nanosleep(nap)) {
             bool mine = true;
             for (int r = r0_ + lane; r < r1_; r += 32) {
               unsigned f;
-              asm volatile("ld.acquire.gpu.global.u32 %0, [%1];" : "=r"(f) : "l"(P.flags + kFlagStride * r) : "memory");
+              if (multi)
+                asm volatile("ld.relaxed.gpu.global.u32 %0, [%1];" : "=r"(f) : "l"(P.flags + kFlagStride * r) : "memory");
+              else
+                asm volatile("ld.acquire.gpu.global.u32 %0, [%1];" : "=r"(f) : "l"(P.flags + kFlagStride * r) : "memory");
               mine = mine && f >= g_;
             }
-            if (__all_sync(0xffffffffu, mine)) break;
+            if (__all_sync(0xffffffffu, mine)) {
+              if (multi) asm volatile("fence.acq_rel.gpu;" ::: "memory");
+              break;
+            }
             if (clock64() - w0 > async::kWatchdogCycles) {
               if (lane == 0) printf("kg watchdog: slab flags (block %d, generation %u)\n", s, g_);
               __trap();
@@ -1029,7 +1042,7 @@ __global__ void __launch_bounds__(BS + (CW ? 32 : 0), 1) k_gauss_path(PersistArg
             r1 = warp_sum(r1);
             r2 = warp_sum(r2);
             if (lane == 0) {
-              double* dst = P.part + ((k - 1) % 3) * 3 * static_cast<i64>(nb);
+              double* dst = P.part + ((k - 1) % 4) * 3 * static_cast<i64>(nb);
               dst[s] = r0;
               dst[nb + s] = r1;
               dst[2 * nb + s] = r2;
@@ -1049,10 +1062,12 @@ __global__ void __launch_bounds__(BS + (CW ? 32 : 0), 1) k_gauss_path(PersistArg
             tc2 = clock64();
             dph[1] += tc2 - tc1;
           }
-          if (k >= 2) {
-            poll(0, static_cast<int>(nb), gen, kMonitorNap);  // off the critical path: back off
-            const double* pp = P.part + ((k - 1) % 3) * 3 * static_cast<i64>(nb);
-            double a = 0.0, b = 0.0, c = 0.0;  // objective partials of step k-1
+          if (k >= 3) {
+            // monitor of step k-2: its partials were published with flag k-1,
+            // which every CTA released about one step ago
+            poll(0, static_cast<int>(nb), gen - 1, (P.dbg >> 20) ? (P.dbg >> 20) - 1 : kMonitorNap);
+            const double* pp = P.part + ((k - 2) % 4) * 3 * static_cast<i64>(nb);
+            double a = 0.0, b = 0.0, c = 0.0;  // objective partials of step k-2
 #pragma unroll
             for (int i = 0; i < kPollRows; ++i) {
               const int r = lane + 32 * i;
@@ -1071,7 +1086,7 @@ __global__ void __launch_bounds__(BS + (CW ? 32 : 0), 1) k_gauss_path(PersistArg
           __syncwarp();
           done = cs.done;
           cmark(3);
-          named_arrive<2, BS + 32>();  // decision of step k-1 (or none at k = 1) is in cs
+          named_arrive<2, BS + 32>();  // decision of step k-2 (or none at k < 3) is in cs
         }
         if (ctim && (t == 5 || t == 20))
           printf("ctl cta %d lambda %d: %lld steps, cycles/step: reduce+release %lld neighbours %lld monitor wait+gather %lld control %lld\n", s,
@@ -1089,6 +1104,8 @@ __global__ void __launch_bounds__(BS + (CW ? 32 : 0), 1) k_gauss_path(PersistArg
             const double g = (w * syi - bs[e]) / n;
             double ci = yi - delta * g;
             if (lam > 0.0) ci = prox1(A.pen, A.alpha, gamma, ci);
+            xpp[e] = xpi;
+            sxpp[e] = sxpi;
             xps[e] = xi;
             xs[e] = ci;
             sxps[e] = sxi;
@@ -1122,10 +1139,10 @@ __global__ void __launch_bounds__(BS + (CW ? 32 : 0), 1) k_gauss_path(PersistArg
           mark(4);
           named_sync<2, BS + 32>();
           mark(2);
-          if (cs.copy_best) {  // best := x_{k-1} (still in the x_prev slot)
+          if (cs.copy_best) {  // best := x_{k-2} (in the x_prev_prev slot)
             for (int e = tx; e < q; e += BS) {
-              bst[e] = xps[e];
-              sbst[e] = sxps[e];
+              bst[e] = xpp[e];
+              sbst[e] = sxpp[e];
             }
           }
           if (cs.done) break;
@@ -1356,7 +1373,7 @@ static size_t path_smem(const GramStepArgs& A) {
   size_t staged = 0;  // staged Gram bands of modes 0 .. d-2
   for (int j = 0; j < A.d - 1; ++j) staged += static_cast<size_t>(A.dims[j]) * (kPathTaps * sizeof(double) + 2 * sizeof(int));
   const size_t dense = path_mm(A) ? 2 * kMmLD * 32 : 0;  // padded G_0, G_1
-  return (static_cast<size_t>(9 + A.Gd.maxlen) * A.q + 3 * static_cast<size_t>(path_qb(A)) + 4 + dense) *
+  return (static_cast<size_t>(11 + A.Gd.maxlen) * A.q + 3 * static_cast<size_t>(path_qb(A)) + 4 + dense) *
              sizeof(double) +
          staged;
 }

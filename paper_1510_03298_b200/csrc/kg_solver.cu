@@ -671,7 +671,7 @@ static void alloc_fit(Fit& F) {
   const i64 pd = D.p[0][D.d - 1];
   F.gstep = D.c == 1 && D.d <= 4 && gram_step_fits(D.P / pd);
   if (F.gstep) {
-    F.gpart.alloc(sizeof(double) * 9 * pd);  // 3 per CTA, triple-buffered (k_gauss_path)
+    F.gpart.alloc(sizeof(double) * 12 * pd);  // 3 per CTA, four buffers (k_gauss_path)
     F.pX.alloc(2 * pb);
     F.pbar.alloc(sizeof(unsigned) * 4);
     KG_CUDA(cudaMemsetAsync(F.pbar.p, 0, sizeof(unsigned) * 4, F.ctx->s));
