@@ -21,8 +21,14 @@ namespace {
 
 constexpr int NT = 256;  // p-space reduction kernels
 constexpr int kPollRows = 10;  // partial / flag rows per lane: up to 320 CTAs
-constexpr int kPathBS = 512;  // default worker width of k_gauss_path
+// default worker width of k_gauss_path: 15 worker warps + the control warp =
+// 512 threads, so ptxas may give each thread 128 registers (17 warps get 96)
+constexpr int kPathBS = 480;
 constexpr bool kPathCW = true;  // k_gauss_path runs a control warp beside the workers
+// phase timers and timing experiments of k_gauss_path (KG_PATH_DBG bits 128,
+// 512, 2048, 65536, 8192, 1<<17..19); compiled out by default because their
+// live state costs registers in the hot loop
+constexpr bool kPathTimers = false;
 constexpr int kFlagCTAs = 64;
 constexpr int kFlagStride = 32;  // one 128-byte line per CTA flag
 constexpr int kMonitorNap = 200;  // ns between polls of the grid-wide monitor wait  // k_gauss_path uses the flag barrier up to this many CTAs (measured: C1 gains, C2/C4 do not)
@@ -860,12 +866,10 @@ __global__ void __launch_bounds__(BS + (CW ? 32 : 0), 1) k_gauss_path(PersistArg
     // CTA partials for thread 0 only: one barrier (red / rbuf are next written
     // after the following grid barrier)
     const int wp = threadIdx.x >> 5, ln = threadIdx.x & 31;
-    if (defer) {
-      if (static_cast<int>(threadIdx.x) < (q < BS ? q : BS)) {
-        rbuf[threadIdx.x] = dots;
-        rbuf[BS + threadIdx.x] = l1;
-        rbuf[2 * BS + threadIdx.x] = l2;
-      }
+    if (defer) {  // every worker writes (zeros when it owns no element): the control sums all BS
+      rbuf[threadIdx.x] = dots;
+      rbuf[BS + threadIdx.x] = l1;
+      rbuf[2 * BS + threadIdx.x] = l2;
       return;
     }
     if (!(P.dbg & 32768)) {
@@ -920,6 +924,89 @@ __global__ void __launch_bounds__(BS + (CW ? 32 : 0), 1) k_gauss_path(PersistArg
       }
     }
   };
+  // CW-loop contraction for mm designs: the last mode over the staged band
+  // (two elements per pass), one CTA barrier, then warp (ti, tj) owns output
+  // tile (ti, tj) of both DMMA modes; the column-block group tj (n1t warps)
+  // syncs on its own named barrier between them, and the mode-0 fragments go
+  // straight into S'x and the objective partial (no further pass or barrier).
+  // ul1 / ul2: |x|_1 and |x|^2 partials of the thread's own elements.
+  const int n1t_ = (A.dims[0] + 7) >> 3, n2t_ = (A.dims[1] + 7) >> 3;
+  const bool fused = mm && hoist && n2t_ <= BS / 32 && n2t_ <= 12 && !(P.dbg & 4096);
+  auto compute_fused = [&](const double* xsrc, double ul1, double ul2) {
+    const double* xin = band + async::stage_shift(xsrc + static_cast<i64>(lo) * q);
+    const int p1 = A.dims[0], p2 = A.dims[1];
+    for (int e = tx; e < q; e += 2 * BS) {
+      const int f = e + BS;
+      const bool two = f < q;
+      const double* xe = xin + e;
+      const double* xf = xin + (two ? f : e);
+      double a0 = 0.0, a1 = 0.0, b0 = 0.0, b1 = 0.0;
+#pragma unroll
+      for (int t = 0; t < MB; t += 2) {
+        if (t < len) {
+          a0 = fma(gr[t], xe[static_cast<i64>(t) * q], a0);
+          b0 = fma(gr[t], xf[static_cast<i64>(t) * q], b0);
+        }
+        if (t + 1 < len) {
+          a1 = fma(gr[t + 1], xe[static_cast<i64>(t + 1) * q], a1);
+          b1 = fma(gr[t + 1], xf[static_cast<i64>(t + 1) * q], b1);
+        }
+      }
+      const int m = static_cast<int>(A.fa[1].div(static_cast<uint32_t>(e)));
+      u[e - m * p1 + kMmLD * m] = a0 + a1;
+      if (two) {
+        const int m2 = static_cast<int>(A.fa[1].div(static_cast<uint32_t>(f)));
+        u[f - m2 * p1 + kMmLD * m2] = b0 + b1;
+      }
+    }
+    named_sync<3, BS>();
+    const int wp = threadIdx.x >> 5, ln = threadIdx.x & 31;
+    // column-block groups: warp wp serves tj = wp mod n2t and the row tiles
+    // ti = gi, gi + gs, ... of that block (gi = wp / n2t, gs = group size)
+    constexpr int NW = BS / 32;
+    const int tj = wp % n2t_, gi = wp / n2t_, gs = (NW - tj + n2t_ - 1) / n2t_;
+    double dots = 0.0;
+    for (int ti = gi; ti < n1t_; ti += gs) {  // mode 1: T tile (ti, tj) = U G_1^T
+        const int al = 8 * ti + (ln >> 2);
+        const int2 r = kr[1][tj];
+        double d0 = 0.0, d1 = 0.0;
+        for (int ks = r.x; ks < r.y; ++ks) {
+          const int kk = 4 * ks + (ln & 3);
+          dmma_884(d0, d1, u[al + kMmLD * kk], gd1[8 * tj + (ln >> 2) + kMmLD * kk]);
+        }
+        const int m = 8 * tj + 2 * (ln & 3);
+        if (al < p1) {
+          if (m < p2) t0[al + kMmLD * m] = d0;
+          if (m + 1 < p2) t0[al + kMmLD * (m + 1)] = d1;
+        }
+    }
+    asm volatile("bar.sync %0, %1;" ::"r"(4 + tj), "r"(32 * gs) : "memory");  // column block tj of T is complete
+    for (int ti = gi; ti < n1t_; ti += gs) {  // mode 0: S tile (ti, tj) = G_0 T, fragments -> S'x and the partial
+        const int m = 8 * ti + (ln >> 2);
+        const int2 r = kr[0][ti];
+        double d0 = 0.0, d1 = 0.0;
+        for (int ks = r.x; ks < r.y; ++ks) {
+          const int kk = 4 * ks + (ln & 3);
+          dmma_884(d0, d1, gd0[m + kMmLD * kk], t0[kk + kMmLD * (8 * tj + (ln >> 2))]);
+        }
+        const int be = 8 * tj + 2 * (ln & 3);
+        if (m < p1) {
+          if (be < p2) {
+            const int e = m + p1 * be;
+            sxs[e] = d0;
+            dots += xs[e] * (w * d0 - 2.0 * bs[e]);
+          }
+          if (be + 1 < p2) {
+            const int e = m + p1 * (be + 1);
+            sxs[e] = d1;
+            dots += xs[e] * (w * d1 - 2.0 * bs[e]);
+          }
+        }
+    }
+    rbuf[threadIdx.x] = dots;
+    rbuf[BS + threadIdx.x] = ul1;
+    rbuf[2 * BS + threadIdx.x] = ul2;
+  };
   auto apply = [&]() {
     issue(P.X);
     __syncthreads();
@@ -938,7 +1025,7 @@ __global__ void __launch_bounds__(BS + (CW ? 32 : 0), 1) k_gauss_path(PersistArg
 
   int stop = 0;  // 1 truncated, 2 first model failed
   // phase timers (dbg & 128): update | grid barrier | monitor gather + control | band wait | contraction
-  const bool tim = (P.dbg & 128) && threadIdx.x == 0 && (s == 0 || s == static_cast<int>(nb) / 2);
+  const bool tim = kPathTimers && (P.dbg & 128) && threadIdx.x == 0 && (s == 0 || s == static_cast<int>(nb) / 2);
   long long ph[5] = {0, 0, 0, 0, 0}, tc = clock64(), nsteps = 0;
   auto mark = [&](int i) {
     if (tim) {
@@ -986,9 +1073,9 @@ __global__ void __launch_bounds__(BS + (CW ? 32 : 0), 1) k_gauss_path(PersistArg
         // of step k-2 to the workers.  Only (d) is on the workers' critical
         // path; (e) waits on flags released a step earlier.
         const int lane = threadIdx.x & 31;
-        const int nact = q < BS ? q : BS;
+        const int nact = BS;  // rbuf entries (the deferred contractions write all of them)
         bool done = false;
-        const bool ctim = (P.dbg & 512) && lane == 0 && (s == 0 || s == static_cast<int>(nb) / 2);
+        const bool ctim = kPathTimers && (P.dbg & 512) && lane == 0 && (s == 0 || s == static_cast<int>(nb) / 2);
         long long cph[4] = {0, 0, 0, 0}, cst = 0, cta_ = 0;
         auto cmark = [&](int i) {
           if (ctim) {
@@ -1027,11 +1114,11 @@ __global__ void __launch_bounds__(BS + (CW ? 32 : 0), 1) k_gauss_path(PersistArg
           double* Xk = P.X + (k & 1) * p;
           named_sync<1, BS + 32>();  // every worker's x_k (and step k-1's partials) is written
           long long w1_ = 0;
-          if ((P.dbg & 65536) && lane == 0) w1_ = *reinterpret_cast<volatile long long*>(&tw1);
+          if ((kPathTimers && (P.dbg & 65536)) && lane == 0) w1_ = *reinterpret_cast<volatile long long*>(&tw1);
           if (ctim) cta_ = clock64();
           ++cst;
           ++gen;
-          if (k >= 2) {
+          if (k >= 2 && !(kPathTimers && (P.dbg & (1 << 19)))) {
             double r0 = 0.0, r1 = 0.0, r2 = 0.0;  // fixed order: lane-strided, then the warp tree
             for (int i = lane; i < nact; i += 32) {
               r0 += rbuf[i];
@@ -1048,21 +1135,31 @@ __global__ void __launch_bounds__(BS + (CW ? 32 : 0), 1) k_gauss_path(PersistArg
               dst[2 * nb + s] = r2;
             }
           }
-          if (lane == 0) asm volatile("st.release.gpu.global.u32 [%0], %1;" ::"l"(P.flags + kFlagStride * s), "r"(gen) : "memory");
+          if (lane == 0) {
+            if (kPathTimers && (P.dbg & (1 << 17)))
+              asm volatile("st.relaxed.gpu.global.u32 [%0], %1;" ::"l"(P.flags + kFlagStride * s), "r"(gen) : "memory");
+            else
+              asm volatile("st.release.gpu.global.u32 [%0], %1;" ::"l"(P.flags + kFlagStride * s), "r"(gen) : "memory");
+          }
           cmark(0);
-          poll(lo, lo + len, gen, 0);
+          if (!(kPathTimers && (P.dbg & 32768))) poll(lo, lo + len, gen, 0);
           cmark(1);
-          if ((P.dbg & 65536) && lane == 0) {
+          if ((kPathTimers && (P.dbg & 65536)) && lane == 0) {
             const long long now = clock64();
             dph[0] += now - w1_;
             tc1 = now;
           }
           if (lane == 0) issue_now(Xk);
-          if ((P.dbg & 65536) && lane == 0) {
+          if ((kPathTimers && (P.dbg & 65536)) && lane == 0) {
             tc2 = clock64();
             dph[1] += tc2 - tc1;
           }
-          if (k >= 3) {
+          if (kPathTimers && (P.dbg & (1 << 18))) {  // timing experiment: no monitor, 50 steps per lambda
+            if (lane == 0) {
+              cs.copy_best = 0;
+              cs.done = cs.converged = k >= 52;
+            }
+          } else if (k >= 3) {
             // monitor of step k-2: its partials were published with flag k-1,
             // which every CTA released about one step ago
             poll(0, static_cast<int>(nb), gen - 1, (P.dbg >> 20) ? (P.dbg >> 20) - 1 : kMonitorNap);
@@ -1097,6 +1194,7 @@ __global__ void __launch_bounds__(BS + (CW ? 32 : 0), 1) k_gauss_path(PersistArg
               extrapolation == 0 ? static_cast<double>(k - 1) / static_cast<double>(k + 2) : 0.0;
           double* Xk = P.X + (k & 1) * p;
           mark(4);
+          double ul1 = 0.0, ul2 = 0.0;
           for (int e = tx; e < q; e += BS) {
             const double xi = xs[e], xpi = xps[e], sxi = sxs[e], sxpi = sxps[e];
             const double yi = xi + omega * (xi - xpi);
@@ -1104,6 +1202,8 @@ __global__ void __launch_bounds__(BS + (CW ? 32 : 0), 1) k_gauss_path(PersistArg
             const double g = (w * syi - bs[e]) / n;
             double ci = yi - delta * g;
             if (lam > 0.0) ci = prox1(A.pen, A.alpha, gamma, ci);
+            ul1 += fabs(ci);
+            ul2 = fma(ci, ci, ul2);
             xpp[e] = xpi;
             sxpp[e] = sxpi;
             xps[e] = xi;
@@ -1113,11 +1213,11 @@ __global__ void __launch_bounds__(BS + (CW ? 32 : 0), 1) k_gauss_path(PersistArg
           }
           mark(0);
           ++nsteps;
-          if ((P.dbg & 65536) && threadIdx.x == 0) tw1 = clock64();
+          if ((kPathTimers && (P.dbg & 65536)) && threadIdx.x == 0) tw1 = clock64();
           named_arrive<1, BS + 32>();
           async::mbar_wait(&mb, parity);
           parity ^= 1u;
-          if ((P.dbg & 65536) && threadIdx.x == 0) {
+          if ((kPathTimers && (P.dbg & 65536)) && threadIdx.x == 0) {
             const long long now = clock64();
             if (k >= 2) {
               dph[2] += now - tc2;
@@ -1125,8 +1225,13 @@ __global__ void __launch_bounds__(BS + (CW ? 32 : 0), 1) k_gauss_path(PersistArg
             }
           }
           mark(3);
-          compute(Xk, nullptr, 0, 0, 0, true);  // partials stay in rbuf for the control warp
-          if ((P.dbg & 2048) && t == 5 && k == 5) {  // isolated cost of the contraction (workers only)
+          if (kPathTimers && (P.dbg & 8192)) {
+          } else if (fused) {
+            compute_fused(Xk, ul1, ul2);  // partials stay in rbuf for the control warp
+          } else {
+            compute(Xk, nullptr, 0, 0, 0, true);
+          }
+          if ((kPathTimers && (P.dbg & 2048)) && t == 5 && k == 5) {  // isolated cost of the contraction (workers only)
             named_sync<3, BS>();
             const long long c0_ = clock64();
             for (int rep = 0; rep < 64; ++rep)
@@ -1361,7 +1466,7 @@ __global__ void __launch_bounds__(BS + (CW ? 32 : 0), 1) k_gauss_path(PersistArg
     P.nmodels[1] = stop;
     *A.ctl = cs;
   }
-  if ((P.dbg & 65536) && threadIdx.x == 0 && (s == 0 || s == static_cast<int>(nb) / 2) && nsteps > 0)
+  if ((kPathTimers && (P.dbg & 65536)) && threadIdx.x == 0 && (s == 0 || s == static_cast<int>(nb) / 2) && nsteps > 0)
     printf("cta %d cycles/step: arrive->barrier done %lld, copy issue %lld, copy latency %lld, arrive->band %lld\n", s,
            dph[0] / nsteps, dph[1] / nsteps, dph[2] / nsteps, dph[3] / nsteps);
   if (tim && nsteps > 0)
@@ -1395,13 +1500,15 @@ static int path_bs() {
     const char* e = std::getenv("KG_PATH_BS");
     const int v = e ? std::atoi(e) : kPathBS;
     if (v == 1024 && path_cw()) return 512;  // 1024 + the control warp exceeds the CTA limit
-    return (v == 256 || v == 512 || v == 1024) ? v : kPathBS;
+    if (v == 480 && !path_cw()) return 512;
+    return (v == 256 || v == 480 || v == 512 || v == 1024) ? v : kPathBS;
   }();
   return bs;
 }
 
 static const void* path_kernel(int bs) {
   if (path_cw()) {
+    if (bs == 480) return reinterpret_cast<const void*>(k_gauss_path<480, true>);
     if (bs == 512) return reinterpret_cast<const void*>(k_gauss_path<512, true>);
     return reinterpret_cast<const void*>(k_gauss_path<256, true>);
   }
