@@ -931,9 +931,13 @@ __global__ void __launch_bounds__(BS + (CW ? 32 : 0), 1) k_gauss_path(PersistArg
   // straight into S'x and the objective partial (no further pass or barrier).
   // ul1 / ul2: |x|_1 and |x|^2 partials of the thread's own elements.
   const int n1t_ = (A.dims[0] + 7) >> 3, n2t_ = (A.dims[1] + 7) >> 3;
-  const bool fused = mm && hoist && n2t_ <= BS / 32 && n2t_ <= 12 && !(P.dbg & 4096);
+  const bool fused = mm && hoist && n2t_ <= BS / 32 && n2t_ <= 10 && !(P.dbg & 4096);
+  // direct: the neighbour band is read straight from L2 (ld.global.cg) once the
+  // control warp has seen the neighbours' flags (named barrier 4), instead of
+  // a bulk copy into shared memory
+  const bool direct = fused;
   auto compute_fused = [&](const double* xsrc, double ul1, double ul2) {
-    const double* xin = band + async::stage_shift(xsrc + static_cast<i64>(lo) * q);
+    const double* xin = xsrc + static_cast<i64>(lo) * q;  // global (L2), see direct
     const int p1 = A.dims[0], p2 = A.dims[1];
     for (int e = tx; e < q; e += 2 * BS) {
       const int f = e + BS;
@@ -944,12 +948,12 @@ __global__ void __launch_bounds__(BS + (CW ? 32 : 0), 1) k_gauss_path(PersistArg
 #pragma unroll
       for (int t = 0; t < MB; t += 2) {
         if (t < len) {
-          a0 = fma(gr[t], xe[static_cast<i64>(t) * q], a0);
-          b0 = fma(gr[t], xf[static_cast<i64>(t) * q], b0);
+          a0 = fma(gr[t], __ldcg(xe + static_cast<i64>(t) * q), a0);
+          b0 = fma(gr[t], __ldcg(xf + static_cast<i64>(t) * q), b0);
         }
         if (t + 1 < len) {
-          a1 = fma(gr[t + 1], xe[static_cast<i64>(t + 1) * q], a1);
-          b1 = fma(gr[t + 1], xf[static_cast<i64>(t + 1) * q], b1);
+          a1 = fma(gr[t + 1], __ldcg(xe + static_cast<i64>(t + 1) * q), a1);
+          b1 = fma(gr[t + 1], __ldcg(xf + static_cast<i64>(t + 1) * q), b1);
         }
       }
       const int m = static_cast<int>(A.fa[1].div(static_cast<uint32_t>(e)));
@@ -980,7 +984,7 @@ __global__ void __launch_bounds__(BS + (CW ? 32 : 0), 1) k_gauss_path(PersistArg
           if (m + 1 < p2) t0[al + kMmLD * (m + 1)] = d1;
         }
     }
-    asm volatile("bar.sync %0, %1;" ::"r"(4 + tj), "r"(32 * gs) : "memory");  // column block tj of T is complete
+    asm volatile("bar.sync %0, %1;" ::"r"(5 + tj), "r"(32 * gs) : "memory");  // column block tj of T is complete
     for (int ti = gi; ti < n1t_; ti += gs) {  // mode 0: S tile (ti, tj) = G_0 T, fragments -> S'x and the partial
         const int m = 8 * ti + (ln >> 2);
         const int2 r = kr[0][ti];
@@ -1149,7 +1153,10 @@ __global__ void __launch_bounds__(BS + (CW ? 32 : 0), 1) k_gauss_path(PersistArg
             dph[0] += now - w1_;
             tc1 = now;
           }
-          if (lane == 0) issue_now(Xk);
+          if (direct)
+            named_arrive<4, BS + 32>();  // the neighbours' x_k is published: workers read it from L2
+          else if (lane == 0)
+            issue_now(Xk);
           if ((kPathTimers && (P.dbg & 65536)) && lane == 0) {
             tc2 = clock64();
             dph[1] += tc2 - tc1;
@@ -1215,8 +1222,12 @@ __global__ void __launch_bounds__(BS + (CW ? 32 : 0), 1) k_gauss_path(PersistArg
           ++nsteps;
           if ((kPathTimers && (P.dbg & 65536)) && threadIdx.x == 0) tw1 = clock64();
           named_arrive<1, BS + 32>();
-          async::mbar_wait(&mb, parity);
-          parity ^= 1u;
+          if (direct) {
+            named_sync<4, BS + 32>();
+          } else {
+            async::mbar_wait(&mb, parity);
+            parity ^= 1u;
+          }
           if ((kPathTimers && (P.dbg & 65536)) && threadIdx.x == 0) {
             const long long now = clock64();
             if (k >= 2) {
