@@ -33,8 +33,12 @@ constexpr int kFlagCTAs = 64;
 constexpr int kFlagStride = 32;  // one 128-byte line per CTA flag
 constexpr int kMonitorNap = 200;  // ns between polls of the grid-wide monitor wait  // k_gauss_path uses the flag barrier up to this many CTAs (measured: C1 gains, C2/C4 do not)
 
+// The step, threshold and soft-threshold use explicitly rounded operations
+// (never contracted into FMAs, like the -ffp-contract=off oracle): at
+// lambda = lambda_max the first step must land exactly on zero, which needs
+// |y - delta g| <= delta lambda to be decided on separately rounded values.
 __device__ __forceinline__ double soft(double z, double g) {
-  const double m = fabs(z) - g;
+  const double m = __dsub_rn(fabs(z), g);
   if (m <= 0.0) return 0.0;
   return z > 0.0 ? m : -m;
 }
@@ -554,7 +558,7 @@ __global__ void __launch_bounds__(BS) k_fista_persist(PersistArgs P) {
   while (!cs.done) {
     const double omega = cs.omega, delta = cs.delta, lambda = cs.lambda, n = cs.n;
     const int restart = cs.restart, copy_best = cs.copy_best;
-    const double gamma = delta * lambda;
+    const double gamma = __dmul_rn(delta, lambda);
     for (int e = threadIdx.x; e < q; e += BS) {
       if (copy_best) {
         bst[e] = xs[e];
@@ -568,7 +572,7 @@ __global__ void __launch_bounds__(BS) k_fista_persist(PersistArgs P) {
       const double yi = xi + omega * (xi - xpi);
       const double syi = sxi + omega * (sxi - sxpi);
       const double g = (w * syi - bs[e]) / n;
-      double ci = yi - delta * g;
+      double ci = __dsub_rn(yi, __dmul_rn(delta, g));
       if (lambda > 0.0) ci = prox1(A.pen, A.alpha, gamma, ci);
       xps[e] = xi;
       xs[e] = ci;
@@ -1063,7 +1067,7 @@ __global__ void __launch_bounds__(BS + (CW ? 32 : 0), 1) k_gauss_path(PersistArg
       // arrive(2).  The decision therefore overlaps the band copy and the
       // contraction instead of preceding them; the iterates and decisions are
       // those of the single-role loop below.
-      const double delta = cs.delta, gamma = delta * lam;
+      const double delta = cs.delta, gamma = __dmul_rn(delta, lam);
       const bool flagbar = nb <= kFlagCTAs && !(P.dbg & 64);
       if (threadIdx.x >= BS) {
         // control iteration k: (a) workers' x_k and the per-thread partials of
@@ -1207,7 +1211,7 @@ __global__ void __launch_bounds__(BS + (CW ? 32 : 0), 1) k_gauss_path(PersistArg
             const double yi = xi + omega * (xi - xpi);
             const double syi = sxi + omega * (sxi - sxpi);
             const double g = (w * syi - bs[e]) / n;
-            double ci = yi - delta * g;
+            double ci = __dsub_rn(yi, __dmul_rn(delta, g));
             if (lam > 0.0) ci = prox1(A.pen, A.alpha, gamma, ci);
             ul1 += fabs(ci);
             ul2 = fma(ci, ci, ul2);
@@ -1274,7 +1278,7 @@ __global__ void __launch_bounds__(BS + (CW ? 32 : 0), 1) k_gauss_path(PersistArg
       // k-1 is taken one step late, after the single grid barrier of step k,
       // while the neighbour band of x_k is in flight.  X and the partials are
       // double-buffered by the parity of k.
-      const double delta = cs.delta, gamma = delta * lam;
+      const double delta = cs.delta, gamma = __dmul_rn(delta, lam);
       for (i64 k = 1; !cs.done; ++k) {
         const double omega =
             extrapolation == 0 ? static_cast<double>(k - 1) / static_cast<double>(k + 2) : 0.0;
@@ -1285,7 +1289,7 @@ __global__ void __launch_bounds__(BS + (CW ? 32 : 0), 1) k_gauss_path(PersistArg
           const double yi = xi + omega * (xi - xpi);
           const double syi = sxi + omega * (sxi - sxpi);
           const double g = (w * syi - bs[e]) / n;
-          double ci = yi - delta * g;
+          double ci = __dsub_rn(yi, __dmul_rn(delta, g));
           if (lam > 0.0) ci = prox1(A.pen, A.alpha, gamma, ci);
           xps[e] = xi;
           xs[e] = ci;
@@ -1379,7 +1383,7 @@ __global__ void __launch_bounds__(BS + (CW ? 32 : 0), 1) k_gauss_path(PersistArg
     while (!cs.done) {
       const double omega = cs.omega, delta = cs.delta;
       const int restart = cs.restart, copy_best = cs.copy_best;
-      const double gamma = delta * lam;
+      const double gamma = __dmul_rn(delta, lam);
       for (int e = tx; e < q; e += BS) {
         if (copy_best) {
           bst[e] = xs[e];
@@ -1393,7 +1397,7 @@ __global__ void __launch_bounds__(BS + (CW ? 32 : 0), 1) k_gauss_path(PersistArg
         const double yi = xi + omega * (xi - xpi);
         const double syi = sxi + omega * (sxi - sxpi);
         const double g = (w * syi - bs[e]) / n;
-        double ci = yi - delta * g;
+        double ci = __dsub_rn(yi, __dmul_rn(delta, g));
         if (lam > 0.0) ci = prox1(A.pen, A.alpha, gamma, ci);
         xps[e] = xi;
         xs[e] = ci;
@@ -1662,7 +1666,7 @@ __global__ void __launch_bounds__(BS) k_nspace_persist(NPersistArgs A) {
   while (!cs.done) {
     mark(0);
     // P0: update (k_fista_update; a pending best copy first)
-    const double omega = cs.omega, delta = cs.delta, gamma = delta * lam;
+    const double omega = cs.omega, delta = cs.delta, gamma = __dmul_rn(delta, lam);
     const int copy_best = cs.copy_best;
     double l1 = 0.0, l2 = 0.0, bx = 0.0;
     for (i64 i = gtid; i < p; i += gsz) {
@@ -1674,7 +1678,7 @@ __global__ void __launch_bounds__(BS) k_nspace_persist(NPersistArgs A) {
       const double yi = xi + omega * (xi - xpi);
       const double syi = sxi + omega * (sxi - sxpi);
       const double g = (w * syi - A.b[i]) / n;
-      double ci = yi - delta * g;
+      double ci = __dsub_rn(yi, __dmul_rn(delta, g));
       if (lam > 0.0) ci = prox1(cs.pen, cs.alpha, gamma, ci);
       A.xp[i] = xi;
       A.x[i] = ci;

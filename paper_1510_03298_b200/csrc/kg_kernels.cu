@@ -657,8 +657,12 @@ void fill(const Launch& L, i64 n, double v, double* x) {
 }
 
 // ---------------------------------------------------------------- p-space
+// The step, threshold and soft-threshold use explicitly rounded operations
+// (never contracted into FMAs, like the -ffp-contract=off oracle): at
+// lambda = lambda_max the first step must land exactly on zero, which needs
+// |y - delta g| <= delta lambda to be decided on separately rounded values.
 __device__ __forceinline__ double soft(double z, double g) {
-  const double m = fabs(z) - g;
+  const double m = __dsub_rn(fabs(z), g);
   if (m <= 0.0) return 0.0;
   return z > 0.0 ? m : -m;
 }
@@ -686,7 +690,7 @@ __global__ void __launch_bounds__(NT) k_fista_update(const FistaCtl* __restrict_
   __shared__ double red[32];
   const double omega = ctl->omega, delta = ctl->delta, lambda = ctl->lambda, n = ctl->n, sscale = ctl->sscale;
   const int copy_best = ctl->copy_best, restart = ctl->restart;
-  const double gamma = delta * lambda;
+  const double gamma = __dmul_rn(delta, lambda);
   double l1 = 0.0, l2 = 0.0, bx = 0.0;
   for (i64 i = static_cast<i64>(blockIdx.x) * NT + threadIdx.x; i < p; i += static_cast<i64>(gridDim.x) * NT) {
     double xi = x[i], xpi = xp[i], sxi = Sx[i], sxpi = Sxp[i];
@@ -701,7 +705,7 @@ __global__ void __launch_bounds__(NT) k_fista_update(const FistaCtl* __restrict_
     const double yi = xi + omega * (xi - xpi);
     const double syi = sxi + omega * (sxi - sxpi);
     const double g = (sscale * syi - b[i]) / n;
-    double ci = yi - delta * g;
+    double ci = __dsub_rn(yi, __dmul_rn(delta, g));
     if (lambda > 0.0) ci = prox1(pen, alpha, gamma, ci);
     xp[i] = xi;
     x[i] = ci;
@@ -892,9 +896,9 @@ __global__ void __launch_bounds__(NT) k_bt_trial(i64 p, double delta, double lam
                                                  const double* y, const double* grad, double* cand, double* part) {
   __shared__ double red[32];
   double a0 = 0.0, a1 = 0.0, l1 = 0.0, l2 = 0.0;
-  const double gamma = delta * lambda;
+  const double gamma = __dmul_rn(delta, lambda);
   for (i64 i = static_cast<i64>(blockIdx.x) * NT + threadIdx.x; i < p; i += static_cast<i64>(gridDim.x) * NT) {
-    double c = y[i] - delta * grad[i];
+    double c = __dsub_rn(y[i], __dmul_rn(delta, grad[i]));
     if (lambda > 0.0) c = prox1(pen, alpha, gamma, c);
     cand[i] = c;
     const double st = c - y[i];
