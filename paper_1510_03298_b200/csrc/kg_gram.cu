@@ -626,7 +626,7 @@ __device__ __forceinline__ void dmma_884(double& d0, double& d1, double a, doubl
 }
 
 template <int BS, bool CW>
-__global__ void __launch_bounds__(BS + (CW ? 32 : 0), 1) k_gauss_path(PersistArgs P) {
+__global__ void __launch_bounds__(BS + (CW ? 32 : 0), (!CW && BS <= 256) ? 2 : 1) k_gauss_path(PersistArgs P) {
   constexpr int MB = kPathTaps;
   // CW: one extra control warp (threads BS..BS+31) runs the grid barrier, the
   // band copy and the monitor of the nu = 1 loop while the BS worker threads
@@ -1521,40 +1521,52 @@ static int path_bs() {
   return bs;
 }
 
-static const void* path_kernel(int bs) {
-  if (path_cw()) {
-    if (bs == 480) return reinterpret_cast<const void*>(k_gauss_path<480, true>);
-    if (bs == 512) return reinterpret_cast<const void*>(k_gauss_path<512, true>);
-    return reinterpret_cast<const void*>(k_gauss_path<256, true>);
+struct PathVariant {
+  const void* fn;
+  int threads;
+};
+
+static PathVariant path_variant(bool cw, int bs) {
+  if (cw) {
+    if (bs == 480) return {reinterpret_cast<const void*>(k_gauss_path<480, true>), 512};
+    if (bs == 512) return {reinterpret_cast<const void*>(k_gauss_path<512, true>), 544};
+    return {reinterpret_cast<const void*>(k_gauss_path<256, true>), 288};
   }
-  if (bs == 1024) return reinterpret_cast<const void*>(k_gauss_path<1024, false>);
-  if (bs == 512) return reinterpret_cast<const void*>(k_gauss_path<512, false>);
-  return reinterpret_cast<const void*>(k_gauss_path<256, false>);
+  if (bs == 1024) return {reinterpret_cast<const void*>(k_gauss_path<1024, false>), 1024};
+  if (bs == 512) return {reinterpret_cast<const void*>(k_gauss_path<512, false>), 512};
+  return {reinterpret_cast<const void*>(k_gauss_path<256, false>), 256};
 }
 
-static int path_threads() { return path_bs() + (path_cw() ? 32 : 0); }
+// The configured variant when its grid (one CTA per slab) is co-resident,
+// otherwise the narrow single-role variant (two CTAs per SM: C4's 256 slabs);
+// threads == 0 when neither fits.
+static PathVariant pick_variant(const GramStepArgs& A) {
+  const size_t sm = path_smem(A);
+  int dev = 0, nsm = 0;
+  KG_CUDA(cudaGetDevice(&dev));
+  KG_CUDA(cudaDeviceGetAttribute(&nsm, cudaDevAttrMultiProcessorCount, dev));
+  const PathVariant cands[2] = {path_variant(path_cw(), path_bs()), path_variant(false, 256)};
+  for (const PathVariant& v : cands) {
+    KG_CUDA(cudaFuncSetAttribute(v.fn, cudaFuncAttributeMaxDynamicSharedMemorySize, 210 * 1024));
+    int per_sm = 0;
+    KG_CUDA(cudaOccupancyMaxActiveBlocksPerMultiprocessor(&per_sm, v.fn, v.threads, sm));
+    if (static_cast<i64>(per_sm) * nsm >= A.pd) return v;
+  }
+  return {nullptr, 0};
+}
 
 bool gauss_path_ok(const GramStepArgs& A) {
   const size_t sm = path_smem(A);
   if (sm > 200 * 1024 || A.pd > 32 * kPollRows) return false;  // the flag barrier polls <= 320 CTAs
-  static bool attr = false;
-  if (!attr) {
-    KG_CUDA(cudaFuncSetAttribute(path_kernel(path_bs()), cudaFuncAttributeMaxDynamicSharedMemorySize, 210 * 1024));
-    attr = true;
-  }
-  int per_sm = 0, dev = 0, nsm = 0;
-  KG_CUDA(cudaOccupancyMaxActiveBlocksPerMultiprocessor(&per_sm, path_kernel(path_bs()), path_threads(), sm));
-  KG_CUDA(cudaGetDevice(&dev));
-  KG_CUDA(cudaDeviceGetAttribute(&nsm, cudaDevAttrMultiProcessorCount, dev));
-  return static_cast<i64>(per_sm) * nsm >= A.pd;
+  return pick_variant(A).threads > 0;
 }
 
 void gauss_path(const Launch& L, const PersistArgs& P) {
   const size_t sm = path_smem(P.g);
+  const PathVariant v = pick_variant(P.g);
   PersistArgs args = P;
   void* kargs[] = {&args};
-  KG_CUDA(cudaLaunchCooperativeKernel(path_kernel(path_bs()), dim3(static_cast<unsigned>(P.g.pd)), dim3(path_threads()),
-                                      kargs, sm, L.s));
+  KG_CUDA(cudaLaunchCooperativeKernel(v.fn, dim3(static_cast<unsigned>(P.g.pd)), dim3(v.threads), kargs, sm, L.s));
   launched(L);
 }
 
