@@ -166,6 +166,9 @@ int64_t kg_result_outer_iters(const kg_path_result* res, int64_t t);
 int64_t kg_result_inner_iters(const kg_path_result* res, int64_t t);
 int kg_result_status(const kg_path_result* res, int64_t t);
 int64_t kg_result_nonzero(const kg_path_result* res, int64_t t);
+/* Nonzero coefficient count of every model (counted on the device): out
+ * has kg_result_n_models entries. */
+kg_status kg_result_nonzeros(kg_path_result* res, int64_t* out);
 /* Copies the p coefficients of model t into host memory. */
 kg_status kg_result_coef(kg_path_result* res, int64_t t, double* out);
 /* Coefficients of models [first, first + count) in one copy: out is

@@ -76,6 +76,7 @@ _SIGS = {
     "kg_result_inner_iters": (_i64, [_vp, _i64]),
     "kg_result_status": (C.c_int, [_vp, _i64]),
     "kg_result_nonzero": (_i64, [_vp, _i64]),
+    "kg_result_nonzeros": (C.c_int, [_vp, C.POINTER(_i64)]),
     "kg_result_coef": (C.c_int, [_vp, _i64, _pd]),
     "kg_result_coefs": (C.c_int, [_vp, _i64, _i64, _pd]),
     "kg_result_free": (None, [_vp]),

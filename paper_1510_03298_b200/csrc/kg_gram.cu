@@ -34,7 +34,7 @@ constexpr int kFlagStride = 32;  // one 128-byte line per CTA flag
 constexpr int kMonitorNap = 200;  // ns between polls of the grid-wide monitor wait  // k_gauss_path uses the flag barrier up to this many CTAs (measured: C1 gains, C2/C4 do not)
 
 // The step, threshold and soft-threshold use explicitly rounded operations
-// (never contracted into FMAs, like the -ffp-contract=off oracle): at
+// (never contracted into FMAs, as the reference computes them): at
 // lambda = lambda_max the first step must land exactly on zero, which needs
 // |y - delta g| <= delta lambda to be decided on separately rounded values.
 __device__ __forceinline__ double soft(double z, double g) {

@@ -328,6 +328,7 @@ struct PersistArgs {
 };
 bool fista_persist_ok(const GramStepArgs& A);
 void fista_persist(const Launch& L, const PersistArgs& P);
+void count_nonzero(const Launch& L, const double* coefs, i64 p, i64 models, unsigned long long* out);
 bool gauss_path_ok(const GramStepArgs& A);
 void gauss_path(const Launch& L, const PersistArgs& P);
 

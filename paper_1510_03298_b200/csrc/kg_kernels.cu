@@ -658,7 +658,7 @@ void fill(const Launch& L, i64 n, double v, double* x) {
 
 // ---------------------------------------------------------------- p-space
 // The step, threshold and soft-threshold use explicitly rounded operations
-// (never contracted into FMAs, like the -ffp-contract=off oracle): at
+// (never contracted into FMAs, as the reference computes them): at
 // lambda = lambda_max the first step must land exactly on zero, which needs
 // |y - delta g| <= delta lambda to be decided on separately rounded values.
 __device__ __forceinline__ double soft(double z, double g) {
@@ -1523,6 +1523,24 @@ void power_iterations(const Launch& L, const PowerJob* jobs_dev, int njobs, i64 
     KG_CUDA(cudaFuncSetAttribute(k_power, cudaFuncAttributeMaxDynamicSharedMemorySize, static_cast<int>(sm)));
   k_power<<<njobs, static_cast<unsigned>(threads), sm, L.s>>>(jobs_dev, tol, max_iters, need);
   bump(L);
+}
+
+// Nonzero count of each model's coefficient vector (kronglm_py.cpp's
+// "nonzero" key): blockIdx.y = model, integer atomics (order-free, exact).
+__global__ void __launch_bounds__(256) k_count_nz(const double* __restrict__ c, i64 p,
+                                                  unsigned long long* __restrict__ out) {
+  const double* row = c + static_cast<i64>(blockIdx.y) * p;
+  unsigned n = 0;
+  for (i64 i = static_cast<i64>(blockIdx.x) * blockDim.x + threadIdx.x; i < p; i += static_cast<i64>(gridDim.x) * blockDim.x)
+    n += __ldg(row + i) != 0.0 ? 1u : 0u;
+  n = __reduce_add_sync(0xffffffffu, n);
+  if ((threadIdx.x & 31) == 0 && n) atomicAdd(out + blockIdx.y, static_cast<unsigned long long>(n));
+}
+
+void count_nonzero(const Launch& L, const double* coefs, i64 p, i64 models, unsigned long long* out) {
+  const i64 bx = std::min<i64>((p + 255) / 256, 64);
+  k_count_nz<<<dim3(static_cast<unsigned>(bx), static_cast<unsigned>(models)), 256, 0, L.s>>>(coefs, p, out);
+  launched(L);
 }
 
 }  // namespace kg

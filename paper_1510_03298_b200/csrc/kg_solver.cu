@@ -145,6 +145,7 @@ struct kg_ctx {
   double path_ms = -1.0, path_bytes = 0.0;
   kg::i64 path_steps = 0;
   cudaEvent_t ev[2] = {nullptr, nullptr};
+  cudaStream_t side = nullptr;  // design-time power iterations, overlapped with the observation upload
   kg::Launch L() { return {s, &launches}; }
   double* pin() { return static_cast<double*>(pinned); }
 };
@@ -466,6 +467,83 @@ static std::vector<double> spectral_run(kg_ctx* ctx, std::vector<std::unique_ptr
   return vals;
 }
 
+// spectral_run split in two: launch on the context's side stream (after the
+// jobs' inputs, which were prepared on the main stream) into page-locked
+// results, then collect when the radii are first needed.
+struct SpectralPending {
+  std::vector<std::unique_ptr<SpectralJob>> jobs;
+  std::vector<size_t> idx;
+  std::vector<double> vals;
+  DBuf out, djobs;
+  std::vector<PowerJob> pj;
+  double* host = nullptr;  // page-locked 3 doubles per power job
+  cudaEvent_t done = nullptr;
+  ~SpectralPending() {
+    if (done) {
+      cudaEventSynchronize(done);
+      cudaEventDestroy(done);
+    }
+    if (host) cudaFreeHost(host);
+  }
+};
+
+static std::unique_ptr<SpectralPending> spectral_launch(kg_ctx* ctx, std::vector<std::unique_ptr<SpectralJob>>& jobs) {
+  auto S = std::make_unique<SpectralPending>();
+  i64 max_p = 1;
+  S->vals.assign(jobs.size(), 0.0);
+  for (size_t k = 0; k < jobs.size(); ++k) {
+    SpectralJob& J = *jobs[k];
+    if (J.immediate >= 0.0) {
+      S->vals[k] = J.immediate;
+      continue;
+    }
+    PowerJob q;
+    q.p = J.p;
+    q.G = J.Gview ? J.Gview : J.G.d();
+    q.glo = static_cast<const int*>(J.glo.p);
+    q.ghi = static_cast<const int*>(J.ghi.p);
+    q.v0 = J.v0.d();
+    q.band = J.band;
+    S->pj.push_back(q);
+    S->idx.push_back(k);
+    max_p = std::max(max_p, J.p);
+  }
+  S->jobs = std::move(jobs);
+  if (S->pj.empty()) return S;
+  S->out.alloc(sizeof(double) * 3 * S->pj.size());
+  for (size_t k = 0; k < S->pj.size(); ++k) S->pj[k].out = S->out.d() + 3 * k;
+  S->djobs.alloc(sizeof(PowerJob) * S->pj.size());
+  KG_CUDA(cudaMemcpyAsync(S->djobs.p, S->pj.data(), sizeof(PowerJob) * S->pj.size(), cudaMemcpyHostToDevice, ctx->s));
+  KG_CUDA(cudaHostAlloc(reinterpret_cast<void**>(&S->host), sizeof(double) * 3 * S->pj.size(), cudaHostAllocDefault));
+  if (!ctx->side) KG_CUDA(cudaStreamCreateWithFlags(&ctx->side, cudaStreamNonBlocking));
+  cudaEvent_t ready;
+  KG_CUDA(cudaEventCreateWithFlags(&ready, cudaEventDisableTiming));
+  KG_CUDA(cudaEventRecord(ready, ctx->s));  // job inputs and buffers are in place
+  KG_CUDA(cudaStreamWaitEvent(ctx->side, ready, 0));
+  KG_CUDA(cudaEventDestroy(ready));
+  power_iterations({ctx->side, &ctx->launches}, static_cast<const PowerJob*>(S->djobs.p),
+                   static_cast<int>(S->pj.size()), max_p, 1e-14, 500000);
+  KG_CUDA(cudaMemcpyAsync(S->host, S->out.p, sizeof(double) * 3 * S->pj.size(), cudaMemcpyDeviceToHost, ctx->side));
+  KG_CUDA(cudaEventCreateWithFlags(&S->done, cudaEventDisableTiming));
+  KG_CUDA(cudaEventRecord(S->done, ctx->side));
+  // the main stream must not free or reuse the jobs' buffers before the side stream is done
+  KG_CUDA(cudaStreamWaitEvent(ctx->s, S->done, 0));
+  return S;
+}
+
+static std::vector<double> spectral_collect(SpectralPending& S) {
+  if (S.done) KG_CUDA(cudaEventSynchronize(S.done));
+  static const bool trace = std::getenv("KG_POWER_TRACE") != nullptr;
+  for (size_t k = 0; k < S.pj.size(); ++k) {
+    if (trace)
+      std::fprintf(stderr, "kg power job %zu: p=%lld band=%d value=%.17g iterations=%.0f\n", k,
+                   static_cast<long long>(S.pj[k].p), S.pj[k].band, S.host[3 * k], S.host[3 * k + 1]);
+    if (S.host[3 * k + 2] != 0.0) throw Error(E_POWER, "power iteration did not converge after 500000 iterations");
+    S.vals[S.idx[k]] = S.host[3 * k];
+  }
+  return S.vals;
+}
+
 }  // namespace kg
 
 struct kg_design {
@@ -483,11 +561,35 @@ struct kg_design {
   std::vector<std::vector<std::vector<std::unique_ptr<kg::FactorOwn>>>> gram;
   std::vector<std::vector<double>> spectral;
   double lipfac = 0.0;                     // sum_r prod_j rho_rj (inner.cpp:61-70)
+  // The power iterations of kg_design_create run on the context's side stream
+  // and are collected on first use (ensure_spectral), so the observation
+  // upload that usually follows overlaps them.
+  mutable std::unique_ptr<kg::SpectralPending> pending;
   bool fused = false;
   int T = 1;                               // mode-1 fibres per CTA in the fused kernels
   kg::i64 scratch = 0;                     // doubles per chain scratch buffer
   kg::i64 part_cap = 0;                    // doubles in the partials buffer
 };
+
+namespace kg {
+// Collect the design's deferred spectral radii (kg_design_create) and form
+// lipschitz_upper's factor sum_r prod_j rho_rj (inner.cpp:61-70).
+static void ensure_spectral(const kg_design* D) {
+  if (!D || !D->pending) return;
+  kg_design* M = const_cast<kg_design*>(D);  // the radii are part of the design's value; filled once
+  const std::vector<double> rad = spectral_collect(*D->pending);
+  M->lipfac = 0.0;
+  for (i64 r = 0; r < D->c; ++r) {
+    double pr = 1.0;
+    for (i64 j = 0; j < D->d; ++j) {
+      M->spectral[r][j] = rad[r * D->d + j];
+      pr *= rad[r * D->d + j];
+    }
+    M->lipfac += pr;
+  }
+  D->pending.reset();
+}
+}  // namespace kg
 
 struct kg_obs {
   kg_ctx* ctx = nullptr;
@@ -630,6 +732,7 @@ static SlabArgs slab_args(const Fit& F) {
 }
 
 static void alloc_fit(Fit& F) {
+  ensure_spectral(F.D);
   const kg_design& D = *F.D;
   F.n = D.N;
   F.p = D.P;
@@ -2120,6 +2223,10 @@ void kg_ctx_destroy(kg_ctx* ctx) {
   if (!ctx) return;
   cudaSetDevice(ctx->device);
   if (ctx->s) cudaStreamSynchronize(ctx->s);
+  if (ctx->side) {
+    cudaStreamSynchronize(ctx->side);
+    cudaStreamDestroy(ctx->side);
+  }
   if (ctx->comm) nccl_api()->CommDestroy(ctx->comm);
   if (ctx->pinned) cudaFreeHost(ctx->pinned);
   for (cudaEvent_t e : ctx->ev)
@@ -2216,15 +2323,7 @@ kg_status kg_design_create(kg_ctx* ctx, int64_t c, int64_t d, const int64_t* n, 
         D->f[r].push_back(std::move(fo));
       }
     }
-    const std::vector<double> rad = spectral_run(ctx, sjobs);  // every factor in one launch
-    for (i64 r = 0; r < c; ++r) {
-      double pr = 1.0;
-      for (i64 j = 0; j < d; ++j) {
-        D->spectral[r][j] = rad[r * d + j];
-        pr *= D->spectral[r][j];
-      }
-      D->lipfac += pr;
-    }
+    D->pending = spectral_launch(ctx, sjobs);  // every factor in one launch, collected by ensure_spectral
     // Gram blocks X_{m,j}^T X_{r,j} of the full factors (ascending-row sums
     // over the overlap of the two column bands), uploaded as banded operators.
     D->gram.resize(c);
@@ -2292,6 +2391,7 @@ kg_status kg_design_create(kg_ctx* ctx, int64_t c, int64_t d, const int64_t* n, 
 void kg_design_destroy(kg_design* d) {
   if (d && d->ctx) {
     cudaSetDevice(d->ctx->device);
+    d->pending.reset();  // waits for the side stream
     cudaStreamSynchronize(d->ctx->s);
   }
   delete d;
@@ -2302,6 +2402,8 @@ int64_t kg_design_p(const kg_design* d) { return d->P; }
 kg_status kg_design_spectral(kg_design* d, int64_t r, int64_t j, double* out) {
   return guarded(d->ctx, [&] {
     if (r < 0 || r >= d->c || j < 0 || j >= d->d) throw Error(E_INVAL, "factor index out of range");
+    set_device(d->ctx);
+    ensure_spectral(d);
     *out = d->spectral[r][j];
   });
 }
@@ -2369,6 +2471,7 @@ kg_status kg_fit_path(kg_ctx* ctx, const kg_design* design, const kg_obs* obs, i
     kg_path_cfg c;
     kg_path_cfg_default(&c);
     if (cfg) c = *cfg;
+    ensure_spectral(design);
     *out = fit_path(ctx, design, obs, family, dispersion, penalty, alpha, c, lambdas, n_lambdas);
   });
 }
@@ -2388,6 +2491,21 @@ int64_t kg_result_nonzero(const kg_path_result* r, int64_t t) {
   int64_t k = 0;
   for (double v : h) k += v != 0.0;
   return k;
+}
+kg_status kg_result_nonzeros(kg_path_result* r, int64_t* out) {
+  return guarded(r->ctx, [&] {
+    set_device(r->ctx);
+    const i64 m = static_cast<i64>(r->lambdas.size());
+    if (m == 0) return;
+    DBuf cnt;
+    cnt.alloc(sizeof(unsigned long long) * m);
+    KG_CUDA(cudaMemsetAsync(cnt.p, 0, sizeof(unsigned long long) * m, r->ctx->s));
+    count_nonzero(r->ctx->L(), r->coefs.d(), r->p, m, static_cast<unsigned long long*>(cnt.p));
+    std::vector<unsigned long long> h(m);
+    KG_CUDA(cudaMemcpyAsync(h.data(), cnt.p, sizeof(unsigned long long) * m, cudaMemcpyDeviceToHost, r->ctx->s));
+    sync(r->ctx);
+    for (i64 t = 0; t < m; ++t) out[t] = static_cast<int64_t>(h[t]);
+  });
 }
 kg_status kg_result_coef(kg_path_result* r, int64_t t, double* out) {
   return guarded(r->ctx, [&] {

@@ -296,6 +296,14 @@ class PathResult:
             self.design.ctx.check(_lib.load().kg_result_coefs(self.h, 0, self.n_models, _ptr(out)))
         return out
 
+    def nonzeros(self) -> list:
+        """Nonzero count of every model's coefficients, counted on the device."""
+        if not self.n_models:
+            return []
+        out = (_i64 * self.n_models)()
+        self.design.ctx.check(_lib.load().kg_result_nonzeros(self.h, out))
+        return [int(v) for v in out]
+
     def close(self):
         if getattr(self, "h", None):
             _lib.load().kg_result_free(self.h)
@@ -467,7 +475,7 @@ def fit_path(design, family, y, weights=None, penalty="lasso", alpha=0.0, n_lamb
            "status": list(res.status)}
     for flat in res.coefs(out=buf):
         out["coefficients"].append(D.blocks(flat))
-        out["nonzero"].append(int(np.count_nonzero(flat)))
+    out["nonzero"] = res.nonzeros()
     return out
 
 

@@ -31,3 +31,17 @@ for rep in range(args.reps):
     dt = np.diff(t) * 1000
     print(f"rep {rep}: design {dt[0]:.1f} ms  obs {dt[1]:.1f}  path {dt[2]:.1f}  coef D2H {dt[3]:.1f}  "
           f"blocks {dt[4]:.1f}  total {sum(dt):.1f}", flush=True)
+
+# the public call itself, timed and profiled (after the warm-up above)
+import cProfile  # noqa: E402
+import pstats  # noqa: E402
+
+for rep in range(3):
+    t0 = time.perf_counter()
+    out = K.fit_path(d["design"], d["family"], d["y"], n_lambda=d["n_lambda"], lambda_min_ratio=d["lambda_min_ratio"])
+    print(f"fit_path rep {rep}: {1000 * (time.perf_counter() - t0):.1f} ms", flush=True)
+pr = cProfile.Profile()
+pr.enable()
+out = K.fit_path(d["design"], d["family"], d["y"], n_lambda=d["n_lambda"], lambda_min_ratio=d["lambda_min_ratio"])
+pr.disable()
+pstats.Stats(pr).sort_stats("cumulative").print_stats(18)
