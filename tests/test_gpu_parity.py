@@ -129,6 +129,23 @@ def test_gaussian_path_matches_oracle_c1_shape():
     compare_paths(got, want)
 
 
+def test_nonzero_counts_and_pinned_result_arrays():
+    """fit_path's "nonzero" key (counted on the device) equals the counts of the
+    returned coefficient arrays, which are views of a recycled page-locked
+    block; a second fit must not overwrite the first fit's arrays."""
+    d = configs.make("C1")
+    kw = dict(n_lambda=20, lambda_min_ratio=1e-2)
+    a = K.fit_path(d["design"], "gaussian", d["y"], **kw)
+    first = [c.copy() for c in a["coefficients"][-1]]  # one array per component
+    b = K.fit_path(d["design"], "gaussian", 2.0 * d["y"], **kw)
+    for got in (a, b):
+        for coef, nz in zip(got["coefficients"], got["nonzero"]):
+            assert nz == int(sum(np.count_nonzero(c) for c in coef))
+    for x, y in zip(first, a["coefficients"][-1]):
+        assert np.array_equal(x, y)
+    assert max(b["nonzero"]) > 0
+
+
 def test_poisson_path_matches_oracle_small():
     rng = np.random.default_rng(5)
     design = bspline_design((24, 20, 30), (8, 6, 9))
