@@ -22,6 +22,7 @@
 #include <limits>
 #include <memory>
 #include <mutex>
+#include <thread>
 #include <unordered_set>
 #include <random>
 #include <string>
@@ -146,6 +147,8 @@ struct kg_ctx {
   kg::i64 path_steps = 0;
   cudaEvent_t ev[2] = {nullptr, nullptr};
   cudaStream_t side = nullptr;  // design-time power iterations, overlapped with the observation upload
+  void* stage = nullptr;        // page-locked upload ring (kStageLanes x kStageSlots x kStageChunk bytes)
+  cudaEvent_t stage_ev[16] = {};
   kg::Launch L() { return {s, &launches}; }
   double* pin() { return static_cast<double*>(pinned); }
 };
@@ -572,6 +575,60 @@ struct kg_design {
 };
 
 namespace kg {
+// Host -> device upload of a pageable array.  The driver stages pageable copies
+// through its own small buffer at ~11 GB/s; here kStageLanes host threads each
+// copy their share of the array chunk by chunk into their own page-locked ring
+// slots and queue the DMA, so host copies and PCIe transfers overlap.
+// Page-locked or small sources go straight to cudaMemcpyAsync.
+constexpr int kStageLanes = 4, kStageSlots = 2;
+constexpr size_t kStageChunk = size_t(4) << 20;
+static void upload(kg_ctx* ctx, void* dst, const void* src, size_t bytes) {
+  cudaPointerAttributes at{};
+  const bool pageable = cudaPointerGetAttributes(&at, src) == cudaSuccess && at.type == cudaMemoryTypeUnregistered;
+  cudaGetLastError();
+  if (!pageable || bytes < 2 * kStageChunk || std::getenv("KG_NO_STAGE")) {
+    KG_CUDA(cudaMemcpyAsync(dst, src, bytes, cudaMemcpyHostToDevice, ctx->s));
+    return;
+  }
+  if (!ctx->stage) {
+    KG_CUDA(cudaHostAlloc(&ctx->stage, kStageLanes * kStageSlots * kStageChunk, cudaHostAllocDefault));
+    for (int i = 0; i < kStageLanes * kStageSlots; ++i)
+      KG_CUDA(cudaEventCreateWithFlags(&ctx->stage_ev[i], cudaEventDisableTiming));
+  }
+  const size_t nchunks = (bytes + kStageChunk - 1) / kStageChunk;
+  std::vector<std::string> errs(kStageLanes);
+  auto lane = [&](int l) {
+    int dev = 0;
+    cudaGetDevice(&dev);
+    if (cudaSetDevice(ctx->device) != cudaSuccess) {
+      errs[l] = "cudaSetDevice";
+      return;
+    }
+    int slot = 0;
+    for (size_t c = l; c < nchunks; c += kStageLanes, slot ^= 1) {
+      const int id = l * kStageSlots + slot;
+      char* buf = static_cast<char*>(ctx->stage) + static_cast<size_t>(id) * kStageChunk;
+      const size_t off = c * kStageChunk, len = std::min(kStageChunk, bytes - off);
+      if (cudaEventSynchronize(ctx->stage_ev[id]) != cudaSuccess) {  // the slot's previous DMA is done
+        errs[l] = "cudaEventSynchronize";
+        return;
+      }
+      std::memcpy(buf, static_cast<const char*>(src) + off, len);
+      if (cudaMemcpyAsync(static_cast<char*>(dst) + off, buf, len, cudaMemcpyHostToDevice, ctx->s) != cudaSuccess ||
+          cudaEventRecord(ctx->stage_ev[id], ctx->s) != cudaSuccess) {
+        errs[l] = "cudaMemcpyAsync";
+        return;
+      }
+    }
+  };
+  std::vector<std::thread> th;
+  for (int l = 1; l < kStageLanes; ++l) th.emplace_back(lane, l);
+  lane(0);
+  for (auto& t : th) t.join();
+  for (const std::string& e : errs)
+    if (!e.empty()) throw Error(E_CUDA, "staged upload: " + e + " failed");
+}
+
 // Collect the design's deferred spectral radii (kg_design_create) and form
 // lipschitz_upper's factor sum_r prod_j rho_rj (inner.cpp:61-70).
 static void ensure_spectral(const kg_design* D) {
@@ -2227,6 +2284,9 @@ void kg_ctx_destroy(kg_ctx* ctx) {
     cudaStreamSynchronize(ctx->side);
     cudaStreamDestroy(ctx->side);
   }
+  if (ctx->stage) cudaFreeHost(ctx->stage);
+  for (cudaEvent_t e : ctx->stage_ev)
+    if (e) cudaEventDestroy(e);
   if (ctx->comm) nccl_api()->CommDestroy(ctx->comm);
   if (ctx->pinned) cudaFreeHost(ctx->pinned);
   for (cudaEvent_t e : ctx->ev)
@@ -2420,9 +2480,15 @@ kg_status kg_obs_create(kg_ctx* ctx, const kg_design* design, const double* y, c
     O->y.alloc(nb);
     O->a.alloc(nb);
     const cudaMemcpyKind k = on_device ? cudaMemcpyDeviceToDevice : cudaMemcpyHostToDevice;
-    KG_CUDA(cudaMemcpyAsync(O->y.p, y, nb, k, ctx->s));
+    if (on_device)
+      KG_CUDA(cudaMemcpyAsync(O->y.p, y, nb, k, ctx->s));
+    else
+      upload(ctx, O->y.p, y, nb);
     if (a) {
-      KG_CUDA(cudaMemcpyAsync(O->a.p, a, nb, k, ctx->s));
+      if (on_device)
+        KG_CUDA(cudaMemcpyAsync(O->a.p, a, nb, k, ctx->s));
+      else
+        upload(ctx, O->a.p, a, nb);
       O->unit_a = false;
       // are all prior weights equal?  (then W is a constant and the Gram route applies)
       DBuf part;
