@@ -223,6 +223,26 @@ struct FactorOwn {
 };
 
 // X^T as DMMA A fragments for the fused pass (see MmaOp).
+// Small host->device copies of kg_design_create (factor bands, Gram blocks,
+// power-iteration jobs) go through a page-locked arena when one is active:
+// a pageable cudaMemcpyAsync synchronises the stream first, and design
+// creation issues dozens of them behind its own kernels.
+struct HostArena {
+  char* base = nullptr;
+  size_t cap = 0, off = 0;
+};
+static thread_local HostArena* g_arena = nullptr;
+static void h2d(void* dst, const void* src, size_t bytes, cudaStream_t st) {
+  if (g_arena && g_arena->off + bytes <= g_arena->cap) {
+    char* b = g_arena->base + g_arena->off;
+    std::memcpy(b, src, bytes);
+    g_arena->off += (bytes + 255) & ~size_t(255);
+    KG_CUDA(cudaMemcpyAsync(dst, b, bytes, cudaMemcpyHostToDevice, st));
+  } else {
+    KG_CUDA(cudaMemcpyAsync(dst, src, bytes, cudaMemcpyHostToDevice, st));
+  }
+}
+
 static void build_mma(const FactorHost& h, const std::vector<int>& glo, const std::vector<int>& glen, FactorOwn& f,
                       cudaStream_t st) {
   const i64 p = h.p, n = h.n;
@@ -260,8 +280,8 @@ static void build_mma(const FactorHost& h, const std::vector<int>& glo, const st
   }
   f.mbase.alloc(sizeof(int) * base.size());
   f.mfrag.alloc(sizeof(double) * frag.size());
-  KG_CUDA(cudaMemcpyAsync(f.mbase.p, base.data(), sizeof(int) * base.size(), cudaMemcpyHostToDevice, st));
-  KG_CUDA(cudaMemcpyAsync(f.mfrag.p, frag.data(), sizeof(double) * frag.size(), cudaMemcpyHostToDevice, st));
+  h2d(f.mbase.p, base.data(), sizeof(int) * base.size(), st);
+  h2d(f.mfrag.p, frag.data(), sizeof(double) * frag.size(), st);
   f.mg.base = static_cast<const int*>(f.mbase.p);
   f.mg.afrag = f.mfrag.d();
   f.mg.ks = ks;
@@ -277,7 +297,7 @@ static void upload_factor(const FactorHost& h, FactorOwn& f, cudaStream_t s) {
   f.dev.n = h.n;
   f.dev.p = h.p;
   f.X.alloc(sizeof(double) * h.n * h.p);
-  KG_CUDA(cudaMemcpyAsync(f.X.p, h.X.data(), sizeof(double) * h.n * h.p, cudaMemcpyHostToDevice, s));
+  h2d(f.X.p, h.X.data(), sizeof(double) * h.n * h.p, s);
   f.dev.X = f.X.d();
   auto up = [&](bool rows, DBuf& blo, DBuf& blen, DBuf& boff, DBuf& bcoef, BandOp& op, std::vector<int>& lo,
                 std::vector<int>& len) {
@@ -290,11 +310,11 @@ static void upload_factor(const FactorHost& h, FactorOwn& f, cudaStream_t s) {
     boff.alloc(sizeof(i64) * off.size());
     bcoef.alloc(sizeof(double) * std::max<size_t>(coef.size(), 1));
     // pageable sources: cudaMemcpyAsync returns once the host data is staged
-    KG_CUDA(cudaMemcpyAsync(blo.p, lo.data(), sizeof(int) * lo.size(), cudaMemcpyHostToDevice, blo.s));
-    KG_CUDA(cudaMemcpyAsync(blen.p, len.data(), sizeof(int) * len.size(), cudaMemcpyHostToDevice, blen.s));
-    KG_CUDA(cudaMemcpyAsync(boff.p, off.data(), sizeof(i64) * off.size(), cudaMemcpyHostToDevice, boff.s));
+    h2d(blo.p, lo.data(), sizeof(int) * lo.size(), blo.s);
+    h2d(blen.p, len.data(), sizeof(int) * len.size(), blen.s);
+    h2d(boff.p, off.data(), sizeof(i64) * off.size(), boff.s);
     if (!coef.empty())
-      KG_CUDA(cudaMemcpyAsync(bcoef.p, coef.data(), sizeof(double) * coef.size(), cudaMemcpyHostToDevice, bcoef.s));
+      h2d(bcoef.p, coef.data(), sizeof(double) * coef.size(), bcoef.s);
     op.lo = static_cast<const int*>(blo.p);
     op.len = static_cast<const int*>(blen.p);
     op.off = static_cast<const i64*>(boff.p);
@@ -335,8 +355,8 @@ static void upload_factor(const FactorHost& h, FactorOwn& f, cudaStream_t s) {
   if (ok) {
     f.rblo.alloc(sizeof(int) * groups);
     f.rbcoef.alloc(sizeof(double) * wc.size());
-    KG_CUDA(cudaMemcpyAsync(f.rblo.p, wlo.data(), sizeof(int) * groups, cudaMemcpyHostToDevice, f.rblo.s));
-    KG_CUDA(cudaMemcpyAsync(f.rbcoef.p, wc.data(), sizeof(double) * wc.size(), cudaMemcpyHostToDevice, f.rbcoef.s));
+    h2d(f.rblo.p, wlo.data(), sizeof(int) * groups, f.rblo.s);
+    h2d(f.rbcoef.p, wc.data(), sizeof(double) * wc.size(), f.rbcoef.s);
     f.dev.H.blo = static_cast<const int*>(f.rblo.p);
     f.dev.H.bcoef = f.rbcoef.d();
   }
@@ -405,9 +425,9 @@ static void spectral_prepare(kg_ctx* ctx, const FactorHost& h, FactorOwn& f, Spe
   J.glo.alloc(sizeof(int) * p);
   J.ghi.alloc(sizeof(int) * p);
   J.v0.alloc(sizeof(double) * p);
-  KG_CUDA(cudaMemcpyAsync(J.glo.p, glo.data(), sizeof(int) * p, cudaMemcpyHostToDevice, ctx->s));
-  KG_CUDA(cudaMemcpyAsync(J.ghi.p, ghi.data(), sizeof(int) * p, cudaMemcpyHostToDevice, ctx->s));
-  KG_CUDA(cudaMemcpyAsync(J.v0.p, v0.data(), sizeof(double) * p, cudaMemcpyHostToDevice, ctx->s));
+  h2d(J.glo.p, glo.data(), sizeof(int) * p, ctx->s);
+  h2d(J.ghi.p, ghi.data(), sizeof(int) * p, ctx->s);
+  h2d(J.v0.p, v0.data(), sizeof(double) * p, ctx->s);
   gram(ctx->L(), f.dev, J.G.d(), static_cast<int*>(J.glo.p), static_cast<int*>(J.ghi.p));
 }
 
@@ -453,7 +473,7 @@ static std::vector<double> spectral_run(kg_ctx* ctx, std::vector<std::unique_ptr
   out.alloc(sizeof(double) * 3 * pj.size());
   for (size_t k = 0; k < pj.size(); ++k) pj[k].out = out.d() + 3 * k;
   djobs.alloc(sizeof(PowerJob) * pj.size());
-  KG_CUDA(cudaMemcpyAsync(djobs.p, pj.data(), sizeof(PowerJob) * pj.size(), cudaMemcpyHostToDevice, ctx->s));
+  h2d(djobs.p, pj.data(), sizeof(PowerJob) * pj.size(), ctx->s);
   power_iterations(ctx->L(), static_cast<const PowerJob*>(djobs.p), static_cast<int>(pj.size()), max_p, 1e-14,
                    500000);
   std::vector<double> res(3 * pj.size());
@@ -516,7 +536,7 @@ static std::unique_ptr<SpectralPending> spectral_launch(kg_ctx* ctx, std::vector
   S->out.alloc(sizeof(double) * 3 * S->pj.size());
   for (size_t k = 0; k < S->pj.size(); ++k) S->pj[k].out = S->out.d() + 3 * k;
   S->djobs.alloc(sizeof(PowerJob) * S->pj.size());
-  KG_CUDA(cudaMemcpyAsync(S->djobs.p, S->pj.data(), sizeof(PowerJob) * S->pj.size(), cudaMemcpyHostToDevice, ctx->s));
+  h2d(S->djobs.p, S->pj.data(), sizeof(PowerJob) * S->pj.size(), ctx->s);
   KG_CUDA(cudaHostAlloc(reinterpret_cast<void**>(&S->host), sizeof(double) * 3 * S->pj.size(), cudaHostAllocDefault));
   if (!ctx->side) KG_CUDA(cudaStreamCreateWithFlags(&ctx->side, cudaStreamNonBlocking));
   cudaEvent_t ready;
@@ -529,8 +549,7 @@ static std::unique_ptr<SpectralPending> spectral_launch(kg_ctx* ctx, std::vector
   KG_CUDA(cudaMemcpyAsync(S->host, S->out.p, sizeof(double) * 3 * S->pj.size(), cudaMemcpyDeviceToHost, ctx->side));
   KG_CUDA(cudaEventCreateWithFlags(&S->done, cudaEventDisableTiming));
   KG_CUDA(cudaEventRecord(S->done, ctx->side));
-  // the main stream must not free or reuse the jobs' buffers before the side stream is done
-  KG_CUDA(cudaStreamWaitEvent(ctx->s, S->done, 0));
+  // the jobs' buffers live in S until spectral_collect has waited for `done`
   return S;
 }
 
@@ -582,6 +601,13 @@ namespace kg {
 // Page-locked or small sources go straight to cudaMemcpyAsync.
 constexpr int kStageLanes = 4, kStageSlots = 2;
 constexpr size_t kStageChunk = size_t(4) << 20;
+static void ensure_stage(kg_ctx* ctx) {
+  if (ctx->stage) return;
+  KG_CUDA(cudaHostAlloc(&ctx->stage, kStageLanes * kStageSlots * kStageChunk, cudaHostAllocDefault));
+  for (int i = 0; i < kStageLanes * kStageSlots; ++i)
+    KG_CUDA(cudaEventCreateWithFlags(&ctx->stage_ev[i], cudaEventDisableTiming));
+}
+
 static void upload(kg_ctx* ctx, void* dst, const void* src, size_t bytes) {
   cudaPointerAttributes at{};
   const bool pageable = cudaPointerGetAttributes(&at, src) == cudaSuccess && at.type == cudaMemoryTypeUnregistered;
@@ -590,11 +616,7 @@ static void upload(kg_ctx* ctx, void* dst, const void* src, size_t bytes) {
     KG_CUDA(cudaMemcpyAsync(dst, src, bytes, cudaMemcpyHostToDevice, ctx->s));
     return;
   }
-  if (!ctx->stage) {
-    KG_CUDA(cudaHostAlloc(&ctx->stage, kStageLanes * kStageSlots * kStageChunk, cudaHostAllocDefault));
-    for (int i = 0; i < kStageLanes * kStageSlots; ++i)
-      KG_CUDA(cudaEventCreateWithFlags(&ctx->stage_ev[i], cudaEventDisableTiming));
-  }
+  ensure_stage(ctx);
   const size_t nchunks = (bytes + kStageChunk - 1) / kStageChunk;
   std::vector<std::string> errs(kStageLanes);
   auto lane = [&](int l) {
@@ -2327,6 +2349,16 @@ kg_status kg_design_create(kg_ctx* ctx, int64_t c, int64_t d, const int64_t* n, 
   auto D = std::make_unique<kg_design>();
   kg_status st = guarded(ctx, [&] {
     set_device(ctx);
+    ensure_stage(ctx);
+    HostArena arena{static_cast<char*>(ctx->stage), kStageLanes * kStageSlots * kStageChunk, 0};
+    g_arena = &arena;
+    struct ArenaGuard {  // the arena is free again only once the stream has consumed it
+      kg_ctx* c;
+      ~ArenaGuard() {
+        g_arena = nullptr;
+        cudaStreamSynchronize(c->s);
+      }
+    } arena_guard{ctx};
     if (c < 1) throw Error(E_INVAL, "TensorDesign: need at least one component");
     if (d < 1) throw Error(E_INVAL, "TensorDesign: need at least one marginal factor");
     D->ctx = ctx;
