@@ -67,8 +67,14 @@ struct BandOp {
   // 4g + r uses bcoef[(g * kRB + r) * kRW + w] (zero outside its band)
   const int* blo = nullptr;
   const double* bcoef = nullptr;
+  // wide-window row-blocked form (G operators X_j^T of B-spline factors):
+  // rows in groups of kGB, group g reads [wblo[g], wblo[g] + kGW) and row
+  // kGB g + r uses wbcoef[(g * kGB + r) * kGW + w] (zero outside its band)
+  const int* wblo = nullptr;
+  const double* wbcoef = nullptr;
 };
 constexpr int kRB = 4, kRW = 8;
+constexpr int kGB = 4, kGW = 32;
 
 // Device + host copies of one factor's operators.
 struct FactorDev {

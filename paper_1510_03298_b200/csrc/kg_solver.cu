@@ -216,7 +216,7 @@ static void build_band(const FactorHost& h, bool rows_of_x, std::vector<int>& lo
 
 struct FactorOwn {
   FactorDev dev;
-  DBuf X, hlo, hlen, hoff, hcoef, glo, glen, goff, gcoef, rblo, rbcoef;
+  DBuf X, hlo, hlen, hoff, hcoef, glo, glen, goff, gcoef, rblo, rbcoef, wblo, wbcoef;
   std::vector<int> h_lo, h_len, g_lo, g_len;  // host copies for launch planning
   DBuf mbase, mfrag;                          // X^T as DMMA fragments (fused pass)
   MmaOp mg;
@@ -359,6 +359,39 @@ static void upload_factor(const FactorHost& h, FactorOwn& f, cudaStream_t s) {
     h2d(f.rbcoef.p, wc.data(), sizeof(double) * wc.size(), f.rbcoef.s);
     f.dev.H.blo = static_cast<const int*>(f.rblo.p);
     f.dev.H.bcoef = f.rbcoef.d();
+  }
+  // wide-window row-blocked copy of the G operator (rows = columns of X):
+  // kGB consecutive basis functions read one window of at most kGW grid rows
+  {
+    const i64 grows = h.p, ggroups = (grows + kGB - 1) / kGB;
+    bool gok = std::getenv("KG_NO_GB") == nullptr && h.n >= kGW;
+    std::vector<int> glo_w(static_cast<size_t>(ggroups), 0);
+    std::vector<double> gwc(static_cast<size_t>(ggroups * kGB * kGW), 0.0);
+    for (i64 g = 0; g < ggroups && gok; ++g) {
+      int lo = INT32_MAX, hi = 0;
+      for (i64 r = g * kGB; r < std::min(grows, (g + 1) * kGB); ++r)
+        if (f.g_len[r] > 0) {
+          lo = std::min(lo, f.g_lo[r]);
+          hi = std::max(hi, f.g_lo[r] + f.g_len[r]);
+        }
+      if (lo == INT32_MAX) lo = hi = 0;
+      if (hi - lo > kGW) gok = false;
+      lo = static_cast<int>(std::max<i64>(0, std::min<i64>(lo, h.n - kGW)));  // window inside the input extent
+      if (hi > lo + kGW) gok = false;
+      glo_w[static_cast<size_t>(g)] = lo;
+      for (i64 r = g * kGB; r < std::min(grows, (g + 1) * kGB) && gok; ++r)
+        for (int t = 0; t < f.g_len[r]; ++t)  // X^T[r, i] = X[i, r]
+          gwc[static_cast<size_t>(((g * kGB + (r - g * kGB)) * kGW) + (f.g_lo[r] + t - lo))] =
+              h.X[(f.g_lo[r] + t) + h.n * r];
+    }
+    if (gok) {
+      f.wblo.alloc(sizeof(int) * ggroups);
+      f.wbcoef.alloc(sizeof(double) * gwc.size());
+      h2d(f.wblo.p, glo_w.data(), sizeof(int) * ggroups, f.wblo.s);
+      h2d(f.wbcoef.p, gwc.data(), sizeof(double) * gwc.size(), f.wbcoef.s);
+      f.dev.G.wblo = static_cast<const int*>(f.wblo.p);
+      f.dev.G.wbcoef = f.wbcoef.d();
+    }
   }
 }
 
