@@ -72,9 +72,13 @@ struct BandOp {
   // kGB g + r uses wbcoef[(g * kGB + r) * kGW + w] (zero outside its band)
   const int* wblo = nullptr;
   const double* wbcoef = nullptr;
+  // the same for H operators (rows of X_j): kHB rows per group, kHW-wide window
+  const int* hblo = nullptr;
+  const double* hbcoef = nullptr;
 };
 constexpr int kRB = 4, kRW = 8;
 constexpr int kGB = 4, kGW = 32;
+constexpr int kHB = 16, kHW = 8;
 
 // Device + host copies of one factor's operators.
 struct FactorDev {

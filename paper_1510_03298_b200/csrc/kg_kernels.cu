@@ -224,36 +224,37 @@ __global__ void __launch_bounds__(NT) k_contract_rs(const double* __restrict__ A
 // produces kGB outputs from it, so an input element is fetched once per group
 // instead of once per output row (~2.3x less L2 traffic than the
 // row-stationary kernel).  Sums ascend over the window (zeros included).
+template <int RB, int RW>
 __global__ void __launch_bounds__(NT) k_contract_gb(const double* __restrict__ A, double* __restrict__ out, uint32_t a,
                                                     uint32_t K, uint32_t M, uint32_t b, uint32_t ab, uint32_t bspan,
                                                     const int* __restrict__ wblo, const double* __restrict__ wbcoef,
                                                     int accumulate) {
-  __shared__ double cs[kGB * kGW];
+  __shared__ double cs[RB * RW];
   const uint32_t g = blockIdx.x;
-  for (int i = threadIdx.x; i < kGB * kGW; i += NT) cs[i] = __ldg(wbcoef + static_cast<size_t>(g) * kGB * kGW + i);
+  for (int i = threadIdx.x; i < RB * RW; i += NT) cs[i] = __ldg(wbcoef + static_cast<size_t>(g) * RB * RW + i);
   __syncthreads();
   const uint32_t nbl = NT / ab;  // beta lanes per CTA
   const uint32_t lane_a = threadIdx.x % ab, lane_b = threadIdx.x / ab;
   const uint32_t al = blockIdx.y * ab + lane_a;
   if (lane_b >= nbl || al >= a) return;
   const int wlo = __ldg(wblo + g);
-  const int nr = static_cast<int>(min(static_cast<uint32_t>(kGB), M - g * kGB));
+  const int nr = static_cast<int>(min(static_cast<uint32_t>(RB), M - g * RB));
   const size_t in_step = static_cast<size_t>(a) * K, out_step = static_cast<size_t>(a) * M;
   const uint32_t b0 = blockIdx.z * bspan, b1 = min(b, b0 + bspan);
   for (uint32_t be = b0 + lane_b; be < b1; be += nbl) {
     const double* src = A + al + static_cast<size_t>(a) * wlo + in_step * be;
-    double win[kGW];
+    double win[RW];
 #pragma unroll
-    for (int w = 0; w < kGW; ++w) win[w] = __ldg(src + static_cast<size_t>(w) * a);
-    double* dst = out + al + static_cast<size_t>(a) * (g * kGB) + out_step * be;
+    for (int w = 0; w < RW; ++w) win[w] = __ldg(src + static_cast<size_t>(w) * a);
+    double* dst = out + al + static_cast<size_t>(a) * (g * RB) + out_step * be;
 #pragma unroll
-    for (int r = 0; r < kGB; ++r) {
+    for (int r = 0; r < RB; ++r) {
       if (r < nr) {
         double s0 = 0.0, s1 = 0.0;
 #pragma unroll
-        for (int w = 0; w < kGW; w += 2) {
-          s0 = fma(cs[r * kGW + w], win[w], s0);
-          s1 = fma(cs[r * kGW + w + 1], win[w + 1], s1);
+        for (int w = 0; w < RW; w += 2) {
+          s0 = fma(cs[r * RW + w], win[w], s0);
+          s1 = fma(cs[r * RW + w + 1], win[w + 1], s1);
         }
         const double v = s0 + s1;
         double* d = dst + static_cast<size_t>(r) * a;
@@ -266,6 +267,29 @@ __global__ void __launch_bounds__(NT) k_contract_gb(const double* __restrict__ A
 static bool gb_enabled() {
   static const bool on = std::getenv("KG_NO_GB") == nullptr;
   return on;
+}
+
+template <int RB, int RW>
+static bool launch_blk(const Launch& L, const double* A, double* out, i64 a, i64 K, i64 M, i64 b, const int* blo,
+                       const double* bcoef, bool accumulate) {
+  const i64 groups = (M + RB - 1) / RB;
+  const i64 ab = std::min<i64>(a, NT);
+  const i64 nbl = NT / ab;
+  const i64 gy = (a + ab - 1) / ab;
+  // beta span per CTA: about 148 x 8 CTAs in total, a multiple of the beta lanes
+  i64 gz = std::max<i64>(1, (148 * 8 + groups * gy - 1) / (groups * gy));
+  gz = std::min<i64>(gz, std::max<i64>(1, (b + nbl - 1) / nbl));
+  i64 bspan = (b + gz - 1) / gz;
+  bspan = (bspan + nbl - 1) / nbl * nbl;
+  gz = (b + bspan - 1) / bspan;
+  if (groups > 0x7fffffff || gy > 65535 || gz > 65535) return false;
+  if (groups * gy * gz < 2 * 148) return false;  // too few CTAs to fill the GPU: the row-stationary kernel
+  k_contract_gb<RB, RW><<<dim3(static_cast<unsigned>(groups), static_cast<unsigned>(gy), static_cast<unsigned>(gz)),
+                          NT, 0, L.s>>>(A, out, static_cast<uint32_t>(a), static_cast<uint32_t>(K),
+                                        static_cast<uint32_t>(M), static_cast<uint32_t>(b), static_cast<uint32_t>(ab),
+                                        static_cast<uint32_t>(bspan), blo, bcoef, accumulate);
+  bump(L);
+  return true;
 }
 
 // Row-blocked banded contraction (H operators): a thread computes kRB
@@ -346,26 +370,11 @@ void contract(const Launch& L, const double* A, double* out, i64 a, i64 K, i64 M
     bump(L);
     return;
   }
-  // wide-window row-blocked kernel for G operators with a blocked copy
-  if (op.wblo && gb_enabled() && K >= kGW && a >= 64 && a < (i64(1) << 31) && b < (i64(1) << 31) && a * K * b < (i64(1) << 31) * 4) {
-    const i64 groups = (M + kGB - 1) / kGB;
-    const i64 ab = std::min<i64>(a, NT);
-    const i64 nbl = NT / ab;
-    const i64 gy = (a + ab - 1) / ab;
-    // beta span per CTA: about 148 x 8 CTAs in total, a multiple of the beta lanes
-    i64 gz = std::max<i64>(1, (148 * 8 + groups * gy - 1) / (groups * gy));
-    gz = std::min<i64>(gz, std::max<i64>(1, (b + nbl - 1) / nbl));
-    i64 bspan = (b + gz - 1) / gz;
-    bspan = (bspan + nbl - 1) / nbl * nbl;
-    gz = (b + bspan - 1) / bspan;
-    if (groups <= 0x7fffffff && gy <= 65535 && gz <= 65535) {
-      k_contract_gb<<<dim3(static_cast<unsigned>(groups), static_cast<unsigned>(gy), static_cast<unsigned>(gz)), NT, 0,
-                      L.s>>>(A, out, static_cast<uint32_t>(a), static_cast<uint32_t>(K), static_cast<uint32_t>(M),
-                             static_cast<uint32_t>(b), static_cast<uint32_t>(ab), static_cast<uint32_t>(bspan), op.wblo,
-                             op.wbcoef, accumulate);
-      bump(L);
-      return;
-    }
+  // row-blocked kernels from the operators' blocked copies: G (kGB rows,
+  // kGW-wide windows) and H (kHB rows, kHW-wide windows)
+  if (gb_enabled() && a >= 64 && a < (i64(1) << 31) && b < (i64(1) << 31) && a * K * b < (i64(1) << 31) * 4) {
+    if (op.wblo && K >= kGW && launch_blk<kGB, kGW>(L, A, out, a, K, M, b, op.wblo, op.wbcoef, accumulate)) return;
+    if (op.hblo && K >= kHW && launch_blk<kHB, kHW>(L, A, out, a, K, M, b, op.hblo, op.hbcoef, accumulate)) return;
   }
   // register-hoisted row-stationary kernel for banded operators (all B-spline factors)
   if (op.maxlen <= 64 && a * M < (i64(1) << 31) && a * K * b < (i64(1) << 31) * 4 && b < (i64(1) << 31) &&

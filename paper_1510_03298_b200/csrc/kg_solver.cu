@@ -216,7 +216,7 @@ static void build_band(const FactorHost& h, bool rows_of_x, std::vector<int>& lo
 
 struct FactorOwn {
   FactorDev dev;
-  DBuf X, hlo, hlen, hoff, hcoef, glo, glen, goff, gcoef, rblo, rbcoef, wblo, wbcoef;
+  DBuf X, hlo, hlen, hoff, hcoef, glo, glen, goff, gcoef, rblo, rbcoef, wblo, wbcoef, hblo, hbcoef;
   std::vector<int> h_lo, h_len, g_lo, g_len;  // host copies for launch planning
   DBuf mbase, mfrag;                          // X^T as DMMA fragments (fused pass)
   MmaOp mg;
@@ -360,39 +360,43 @@ static void upload_factor(const FactorHost& h, FactorOwn& f, cudaStream_t s) {
     f.dev.H.blo = static_cast<const int*>(f.rblo.p);
     f.dev.H.bcoef = f.rbcoef.d();
   }
-  // wide-window row-blocked copy of the G operator (rows = columns of X):
-  // kGB consecutive basis functions read one window of at most kGW grid rows
-  {
-    const i64 grows = h.p, ggroups = (grows + kGB - 1) / kGB;
-    bool gok = std::getenv("KG_NO_GB") == nullptr && h.n >= kGW;
-    std::vector<int> glo_w(static_cast<size_t>(ggroups), 0);
-    std::vector<double> gwc(static_cast<size_t>(ggroups * kGB * kGW), 0.0);
-    for (i64 g = 0; g < ggroups && gok; ++g) {
+  // wide-window row-blocked copies: G (rows = columns of X, kGB basis
+  // functions per window of kGW grid rows) and H (rows of X, kHB grid rows per
+  // window of kHW basis functions)
+  auto blocked = [&](int RB, int RW, i64 rows, i64 in_ext, const std::vector<int>& blo_r, const std::vector<int>& blen_r,
+                     bool transpose, DBuf& dlo, DBuf& dcoef, const int*& olo, const double*& ocoef) {
+    const i64 groups = (rows + RB - 1) / RB;
+    bool ok = std::getenv("KG_NO_GB") == nullptr && in_ext >= RW;
+    std::vector<int> wl(static_cast<size_t>(groups), 0);
+    std::vector<double> wc(static_cast<size_t>(groups * RB * RW), 0.0);
+    for (i64 g = 0; g < groups && ok; ++g) {
       int lo = INT32_MAX, hi = 0;
-      for (i64 r = g * kGB; r < std::min(grows, (g + 1) * kGB); ++r)
-        if (f.g_len[r] > 0) {
-          lo = std::min(lo, f.g_lo[r]);
-          hi = std::max(hi, f.g_lo[r] + f.g_len[r]);
+      for (i64 r = g * RB; r < std::min(rows, (g + 1) * RB); ++r)
+        if (blen_r[r] > 0) {
+          lo = std::min(lo, blo_r[r]);
+          hi = std::max(hi, blo_r[r] + blen_r[r]);
         }
       if (lo == INT32_MAX) lo = hi = 0;
-      if (hi - lo > kGW) gok = false;
-      lo = static_cast<int>(std::max<i64>(0, std::min<i64>(lo, h.n - kGW)));  // window inside the input extent
-      if (hi > lo + kGW) gok = false;
-      glo_w[static_cast<size_t>(g)] = lo;
-      for (i64 r = g * kGB; r < std::min(grows, (g + 1) * kGB) && gok; ++r)
-        for (int t = 0; t < f.g_len[r]; ++t)  // X^T[r, i] = X[i, r]
-          gwc[static_cast<size_t>(((g * kGB + (r - g * kGB)) * kGW) + (f.g_lo[r] + t - lo))] =
-              h.X[(f.g_lo[r] + t) + h.n * r];
+      if (hi - lo > RW) ok = false;
+      lo = static_cast<int>(std::max<i64>(0, std::min<i64>(lo, in_ext - RW)));  // window inside the input extent
+      if (hi > lo + RW) ok = false;
+      wl[static_cast<size_t>(g)] = lo;
+      for (i64 r = g * RB; r < std::min(rows, (g + 1) * RB) && ok; ++r)
+        for (int t = 0; t < blen_r[r]; ++t) {
+          const i64 c = blo_r[r] + t;  // G: X^T[r, c] = X[c, r]; H: X[r, c]
+          wc[static_cast<size_t>(((g * RB + (r - g * RB)) * RW) + (c - lo))] = transpose ? h.X[c + h.n * r] : h.X[r + h.n * c];
+        }
     }
-    if (gok) {
-      f.wblo.alloc(sizeof(int) * ggroups);
-      f.wbcoef.alloc(sizeof(double) * gwc.size());
-      h2d(f.wblo.p, glo_w.data(), sizeof(int) * ggroups, f.wblo.s);
-      h2d(f.wbcoef.p, gwc.data(), sizeof(double) * gwc.size(), f.wbcoef.s);
-      f.dev.G.wblo = static_cast<const int*>(f.wblo.p);
-      f.dev.G.wbcoef = f.wbcoef.d();
-    }
-  }
+    if (!ok) return;
+    dlo.alloc(sizeof(int) * groups);
+    dcoef.alloc(sizeof(double) * wc.size());
+    h2d(dlo.p, wl.data(), sizeof(int) * groups, dlo.s);
+    h2d(dcoef.p, wc.data(), sizeof(double) * wc.size(), dcoef.s);
+    olo = static_cast<const int*>(dlo.p);
+    ocoef = dcoef.d();
+  };
+  blocked(kGB, kGW, h.p, h.n, f.g_lo, f.g_len, true, f.wblo, f.wbcoef, f.dev.G.wblo, f.dev.G.wbcoef);
+  blocked(kHB, kHW, h.n, h.p, f.h_lo, f.h_len, false, f.hblo, f.hbcoef, f.dev.H.hblo, f.dev.H.hbcoef);
 }
 
 // Spectral radius of X^T X for one factor: banded Gram + single-warp power
