@@ -241,6 +241,7 @@ def run_ours(args):
     hbm, peak_kind = peaks()
     f_ms, f_bytes = K_time(ctx, design, obs, 0)
     c_ms, c_bytes = K_time(ctx, design, obs, 1)
+    g_ms, g_bytes = K_time(ctx, design, obs, 5) if len(data["n"]) >= 2 else (None, None)
     traffic = None
     tfile = os.path.join(ROOT, "profiles", f"traffic_{args.config}.json")
     if os.path.exists(tfile):
@@ -252,6 +253,10 @@ def run_ours(args):
            "contraction": {"kernel": "k_contract_rs (largest banded H-chain step)", "bytes_per_launch": c_bytes,
                            "avg_launch_ms": c_ms, "achieved": c_bytes / (c_ms / 1000.0) / 1e9,
                            "frac": c_bytes / (c_ms / 1000.0) / 1e9 / hbm},
+           "g_contraction": None if g_ms is None else {
+               "kernel": "mode-2 G-chain step (k_contract_gb row-blocked when the grid fills the GPU)",
+               "bytes_per_launch": g_bytes, "avg_launch_ms": g_ms, "achieved": g_bytes / (g_ms / 1000.0) / 1e9,
+               "frac": g_bytes / (g_ms / 1000.0) / 1e9 / hbm},
            "peak": hbm, "unit": "GB/s",
            "dram_bytes_ncu": traffic.get("fused_pass_dram_bytes") if traffic else None}
     if pk_launches:

@@ -2929,6 +2929,16 @@ kg_status kg_time_kernel(kg_ctx* ctx, const kg_design* D, const kg_obs* O, int w
         launch = [&, sa] { slab12(ctx->L(), sa); };
         b = 8.0 * (static_cast<double>(F.n) + 2.0 * static_cast<double>(sa.p1) * sa.p2 * static_cast<double>(sa.n3));
       }
+    } else if (which == 5) {
+      // G-chain step of mode 1 (after the fused mode-0 pass): (p0, n1, rest) -> (p0, p1, rest)
+      if (D->d < 2) throw Error(E_INVAL, "kg_time_kernel: the G-chain step needs d >= 2");
+      const i64 a_ = D->p[0][0], K = D->n[1], M = D->p[0][1], b_ = prod(D->n, 2, D->d);
+      double* in = F.eta.d();
+      double* outp = F.s0.d();
+      KG_CUDA(cudaMemsetAsync(in, 0, sizeof(double) * a_ * K * b_, ctx->s));
+      const BandOp op = D->f[0][1]->dev.G;
+      launch = [&, in, outp, a_, K, M, b_, op] { contract(ctx->L(), in, outp, a_, K, M, b_, op, false); };
+      b = 8.0 * static_cast<double>(a_ * K * b_ + a_ * M * b_);
     } else {
       // largest H-chain step of component 0 (modes d-1 .. 0 applied to theta)
       std::vector<i64> dims = D->p[0];

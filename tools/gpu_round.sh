@@ -17,3 +17,6 @@ echo "ncu launches rc=$?"
 timeout 400 ncu --set full --import-source on --clock-control none -k regex:k_gauss_path -c 1 \
   -o gpurun_out/r01_c2_path_final python tools/prof_path.py --config C2 --paths 1 > gpurun_out/ncu_path.log 2>&1
 echo "ncu path rc=$?"
+KG_HOST_LOOP=1 timeout 400 ncu --set full --clock-control none -k regex:k_contract_gb -s 4 -c 2 \
+  -o gpurun_out/r01_c5_contract_gb python tools/prof_path.py --config C5 --paths 1 --n-lambda 2 > gpurun_out/ncu_gb.log 2>&1
+echo "ncu contract_gb rc=$?"
