@@ -225,7 +225,7 @@ __global__ void __launch_bounds__(NT) k_contract_rs(const double* __restrict__ A
 // instead of once per output row (~2.3x less L2 traffic than the
 // row-stationary kernel).  Sums ascend over the window (zeros included).
 template <int RB, int RW>
-__global__ void __launch_bounds__(NT) k_contract_gb(const double* __restrict__ A, double* __restrict__ out, uint32_t a,
+__global__ void __launch_bounds__(NT, RB <= 4 ? 4 : 1) k_contract_gb(const double* __restrict__ A, double* __restrict__ out, uint32_t a,
                                                     uint32_t K, uint32_t M, uint32_t b, uint32_t ab, uint32_t bspan,
                                                     const int* __restrict__ wblo, const double* __restrict__ wbcoef,
                                                     int accumulate) {
@@ -243,22 +243,47 @@ __global__ void __launch_bounds__(NT) k_contract_gb(const double* __restrict__ A
   const uint32_t b0 = blockIdx.z * bspan, b1 = min(b, b0 + bspan);
   for (uint32_t be = b0 + lane_b; be < b1; be += nbl) {
     const double* src = A + al + static_cast<size_t>(a) * wlo + in_step * be;
-    double win[RW];
-#pragma unroll
-    for (int w = 0; w < RW; ++w) win[w] = __ldg(src + static_cast<size_t>(w) * a);
     double* dst = out + al + static_cast<size_t>(a) * (g * RB) + out_step * be;
+    if constexpr (RB <= 4) {
+      double s0[RB], s1[RB];
 #pragma unroll
-    for (int r = 0; r < RB; ++r) {
-      if (r < nr) {
-        double s0 = 0.0, s1 = 0.0;
+      for (int r = 0; r < RB; ++r) s0[r] = s1[r] = 0.0;
+      // stream the wide window: every loaded pair feeds all RB rows (even /
+      // odd window positions into separate sums, then their sum per row)
 #pragma unroll
-        for (int w = 0; w < RW; w += 2) {
-          s0 = fma(cs[r * RW + w], win[w], s0);
-          s1 = fma(cs[r * RW + w + 1], win[w + 1], s1);
+      for (int w = 0; w < RW; w += 2) {
+        const double x0 = __ldg(src + static_cast<size_t>(w) * a), x1 = __ldg(src + static_cast<size_t>(w + 1) * a);
+#pragma unroll
+        for (int r = 0; r < RB; ++r) {
+          s0[r] = fma(cs[r * RW + w], x0, s0[r]);
+          s1[r] = fma(cs[r * RW + w + 1], x1, s1[r]);
         }
-        const double v = s0 + s1;
-        double* d = dst + static_cast<size_t>(r) * a;
-        *d = accumulate ? *d + v : v;
+      }
+#pragma unroll
+      for (int r = 0; r < RB; ++r) {
+        if (r < nr) {
+          const double v = s0[r] + s1[r];
+          double* d = dst + static_cast<size_t>(r) * a;
+          *d = accumulate ? *d + v : v;
+        }
+      }
+    } else {  // narrow window, many rows: keep the window, one row at a time
+      double win[RW];
+#pragma unroll
+      for (int w = 0; w < RW; ++w) win[w] = __ldg(src + static_cast<size_t>(w) * a);
+#pragma unroll
+      for (int r = 0; r < RB; ++r) {
+        if (r < nr) {
+          double s0 = 0.0, s1 = 0.0;
+#pragma unroll
+          for (int w = 0; w < RW; w += 2) {
+            s0 = fma(cs[r * RW + w], win[w], s0);
+            s1 = fma(cs[r * RW + w + 1], win[w + 1], s1);
+          }
+          const double v = s0 + s1;
+          double* d = dst + static_cast<size_t>(r) * a;
+          *d = accumulate ? *d + v : v;
+        }
       }
     }
   }
