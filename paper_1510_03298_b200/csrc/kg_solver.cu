@@ -1879,10 +1879,19 @@ static ModelTrace outer_loop(Fit& F, double lambda, const OuterCfg& oc) {
     xtwz_pass(F);
     fista_enqueue(F, lambda, oc.inner, vmax_part, n_vmax);
     // eta_tilde = H(theta_tilde) with Delta_k's inner product and the first trials.
+    // The fused pass carries only the full step t = alpha0 (accepted in the
+    // common case, test_outer.cpp:107-138): every extra trial costs an exp per
+    // cell.  Rejections fall through to the batched trial passes below, which
+    // compute the same per-trial sums (KG_TRIALS0 sets the first batch size).
+    static const int first_batch = [] {
+      const char* e = std::getenv("KG_TRIALS0");
+      const int v = e ? std::atoi(e) : 1;
+      return v < 1 ? 1 : (v > kMaxTrials ? kMaxTrials : v);
+    }();
     double t_list[kMaxTrials];
     double t = oc.alpha0;
     int nt = 0;
-    for (; nt < kMaxTrials && nt <= oc.max_bt; ++nt, t *= oc.b) t_list[nt] = t;
+    for (; nt < first_batch && nt <= oc.max_bt; ++nt, t *= oc.b) t_list[nt] = t;
     HlastArgs h = hlast_args(F);
     h.flags = HL_DOT | HL_TRIALS;
     h.eta_old = F.eta.d();
