@@ -1397,7 +1397,34 @@ __global__ void k_reduce_cols(const double* part, int nrows, int ncols, int op, 
   }
 }
 
+// Many rows (the per-CTA partials of the n-space passes: up to 32K CTAs): one
+// 1024-thread CTA per column, thread t sums rows t, t + 1024, ... in order,
+// then a fixed shuffle tree and a fixed-order sum over the warps.
+__global__ void __launch_bounds__(1024) k_reduce_cols_wide(const double* part, int nrows, int ncols, int op,
+                                                           double* out) {
+  __shared__ double ws[32];
+  const int c = blockIdx.x, l = threadIdx.x & 31, w = threadIdx.x >> 5;
+  double r = op ? -DBL_MAX : 0.0;
+  for (int i = threadIdx.x; i < nrows; i += 1024) {
+    const double v = part[static_cast<i64>(i) * ncols + c];
+    r = op ? fmax(r, v) : r + v;
+  }
+  r = op ? warp_max(r) : warp_sum(r);
+  if (l == 0) ws[w] = r;
+  __syncthreads();
+  if (w == 0) {
+    r = ws[l];
+    r = op ? warp_max(r) : warp_sum(r);
+    if (l == 0) out[c] = r;
+  }
+}
+
 void reduce_cols(const Launch& L, const double* part, int nrows, int ncols, int op, double* out) {
+  if (nrows >= 4096) {
+    k_reduce_cols_wide<<<ncols, 1024, 0, L.s>>>(part, nrows, ncols, op, out);
+    bump(L);
+    return;
+  }
   const int warps = ncols < 16 ? ncols : 16;
   k_reduce_cols<<<1, 32 * warps, 0, L.s>>>(part, nrows, ncols, op, out);
   bump(L);
