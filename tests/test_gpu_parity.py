@@ -45,6 +45,24 @@ def test_h_g_rho_match_dense_and_oracle_on_random_corpus():  # acceptance.cpp:53
         assert np.max(np.abs(H.flat(K.xtwx_apply(design, v, th)) - want)) <= 1e-12
 
 
+def test_row_blocked_chain_contractions_match_oracle():
+    """Shapes large enough for the row-blocked H/G chain kernels (k_contract_gb:
+    mode-3 steps with alpha = p1 p2 = 2048 and 64 row groups): h_map, g_map
+    and the adjoint identity against the oracle's banded maps."""
+    rng = np.random.default_rng(77)
+    design = bspline_design((40, 80, 1024), (32, 64, 256))
+    th = [rng.uniform(-1, 1, (32, 64, 256))]
+    u = rng.uniform(-1, 1, (40, 80, 1024))
+    h = K.h_map(design, th)
+    hw = O.h_map(design, th)
+    assert np.max(np.abs(h - hw)) <= 1e-12 * max(1.0, np.max(np.abs(hw)))
+    g = H.flat(K.g_map(design, u))
+    gw = H.flat(O.g_map(design, u))
+    assert np.max(np.abs(g - gw)) <= 1e-12 * max(1.0, np.max(np.abs(gw)))
+    lhs, rhs = float(np.vdot(h, u)), float(H.flat(th) @ g)
+    assert abs(lhs - rhs) <= 1e-12 * max(1.0, abs(rhs))
+
+
 def test_rho_matches_oracle_and_rotates():
     rng = np.random.default_rng(13)
     a = rng.uniform(-1, 1, (3, 4, 2))
