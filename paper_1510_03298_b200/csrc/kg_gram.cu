@@ -25,9 +25,8 @@ constexpr int kPollRows = 10;  // partial / flag rows per lane: up to 320 CTAs
 // 512 threads, so ptxas may give each thread 128 registers (17 warps get 96)
 constexpr int kPathBS = 480;
 constexpr bool kPathCW = true;  // k_gauss_path runs a control warp beside the workers
-// phase timers and timing experiments of k_gauss_path (KG_PATH_DBG bits 128,
-// 512, 2048, 65536, 8192, 1<<17..19); compiled out by default because their
-// live state costs registers in the hot loop
+// phase timers of k_gauss_path (KG_PATH_DBG bits 128, 512, 65536); compiled
+// out by default because their live state costs registers in the hot loop
 constexpr bool kPathTimers = false;
 constexpr int kFlagCTAs = 64;
 constexpr int kFlagStride = 32;  // one 128-byte line per CTA flag
@@ -774,10 +773,10 @@ __global__ void __launch_bounds__(BS + (CW ? 32 : 0), (!CW && BS <= 256) ? 2 : 1
   // S'(x) of this slab from the staged band -> sxs; objective partials of xs -> dst
   // defer: leave the per-thread objective partials in rbuf for the control
   // warp (no CTA reduction here)
-  auto compute = [&](const double* xsrc, double* dst, int sc_, int ss_, int skip = 0, bool defer = false) {  // dst[c * sc_ + s * ss_]
+  auto compute = [&](const double* xsrc, double* dst, int sc_, int ss_, bool defer = false) {  // dst[c * sc_ + s * ss_]
     if (CW && threadIdx.x >= BS) return;  // workers only (named barrier 3)
     const double* xin = band + async::stage_shift(xsrc + static_cast<i64>(lo) * q);
-    for (int e = (skip & 1) ? q : tx; e < q; e += BS) {
+    for (int e = tx; e < q; e += BS) {
       const double* xe = xin + e;
       double a0 = 0.0, a1 = 0.0;
       if (hoist) {
@@ -803,7 +802,7 @@ __global__ void __launch_bounds__(BS + (CW ? 32 : 0), (!CW && BS <= 256) ? 2 : 1
     }
     named_sync<3, BS>();
     const double* res = u;
-    if (mm && !(skip & 2)) {
+    if (mm) {
       const int wp = threadIdx.x >> 5, ln = threadIdx.x & 31;
       const int p1 = A.dims[0], p2 = A.dims[1];
       const int n1t = (p1 + 7) >> 3, n2t = (p2 + 7) >> 3;
@@ -858,7 +857,6 @@ __global__ void __launch_bounds__(BS + (CW ? 32 : 0), (!CW && BS <= 256) ? 2 : 1
       res = dst2;
       which ^= 1;
     }
-    if (skip & 4) return;
     double dots = 0.0, l1 = 0.0, l2 = 0.0;
     for (int e = tx; e < q; e += BS) {
       const double sv = res[e], xv = xs[e];
@@ -1126,7 +1124,7 @@ __global__ void __launch_bounds__(BS + (CW ? 32 : 0), (!CW && BS <= 256) ? 2 : 1
           if (ctim) cta_ = clock64();
           ++cst;
           ++gen;
-          if (k >= 2 && !(kPathTimers && (P.dbg & (1 << 19)))) {
+          if (k >= 2) {
             double r0 = 0.0, r1 = 0.0, r2 = 0.0;  // fixed order: lane-strided, then the warp tree
             for (int i = lane; i < nact; i += 32) {
               r0 += rbuf[i];
@@ -1143,14 +1141,10 @@ __global__ void __launch_bounds__(BS + (CW ? 32 : 0), (!CW && BS <= 256) ? 2 : 1
               dst[2 * nb + s] = r2;
             }
           }
-          if (lane == 0) {
-            if (kPathTimers && (P.dbg & (1 << 17)))
-              asm volatile("st.relaxed.gpu.global.u32 [%0], %1;" ::"l"(P.flags + kFlagStride * s), "r"(gen) : "memory");
-            else
-              asm volatile("st.release.gpu.global.u32 [%0], %1;" ::"l"(P.flags + kFlagStride * s), "r"(gen) : "memory");
-          }
+          if (lane == 0)
+            asm volatile("st.release.gpu.global.u32 [%0], %1;" ::"l"(P.flags + kFlagStride * s), "r"(gen) : "memory");
           cmark(0);
-          if (!(kPathTimers && (P.dbg & 32768))) poll(lo, lo + len, gen, 0);
+          poll(lo, lo + len, gen, 0);
           cmark(1);
           if ((kPathTimers && (P.dbg & 65536)) && lane == 0) {
             const long long now = clock64();
@@ -1165,12 +1159,7 @@ __global__ void __launch_bounds__(BS + (CW ? 32 : 0), (!CW && BS <= 256) ? 2 : 1
             tc2 = clock64();
             dph[1] += tc2 - tc1;
           }
-          if (kPathTimers && (P.dbg & (1 << 18))) {  // timing experiment: no monitor, 50 steps per lambda
-            if (lane == 0) {
-              cs.copy_best = 0;
-              cs.done = cs.converged = k >= 52;
-            }
-          } else if (k >= 3) {
+          if (k >= 3) {
             // monitor of step k-2: its partials were published with flag k-1,
             // which every CTA released about one step ago
             poll(0, static_cast<int>(nb), gen - 1, (P.dbg >> 20) ? (P.dbg >> 20) - 1 : kMonitorNap);
@@ -1240,21 +1229,10 @@ __global__ void __launch_bounds__(BS + (CW ? 32 : 0), (!CW && BS <= 256) ? 2 : 1
             }
           }
           mark(3);
-          if (kPathTimers && (P.dbg & 8192)) {
-          } else if (fused) {
+          if (fused) {
             compute_fused(Xk, ul1, ul2);  // partials stay in rbuf for the control warp
           } else {
-            compute(Xk, nullptr, 0, 0, 0, true);
-          }
-          if ((kPathTimers && (P.dbg & 2048)) && t == 5 && k == 5) {  // isolated cost of the contraction (workers only)
-            named_sync<3, BS>();
-            const long long c0_ = clock64();
-            for (int rep = 0; rep < 64; ++rep)
-              compute(Xk, P.part + (k & 1) * 3 * static_cast<i64>(nb), static_cast<int>(nb), 1, (P.dbg >> 12) & 7);
-            named_sync<3, BS>();
-            const long long c1_ = clock64();
-            if (threadIdx.x == 0 && (s == 0 || s == static_cast<int>(nb) / 2))
-              printf("cta %d: compute() alone %lld cycles\n", s, (c1_ - c0_) / 64);
+            compute(Xk, nullptr, 0, 0, true);
           }
           mark(4);
           named_sync<2, BS + 32>();
