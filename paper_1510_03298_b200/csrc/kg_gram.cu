@@ -651,11 +651,12 @@ __global__ void __launch_bounds__(BS + (CW ? 32 : 0), (!CW && BS <= 256) ? 2 : 1
   double* sth = th + q;
   double* xpp = sth + q;  // CW: x_{k-2} and S'x_{k-2} (the monitor decision runs two steps late)
   double* sxpp = xpp + q;
+  double* bn = sxpp + q;  // b / n: the gradient is w/n S'y - b/n, one FMA per element
   // mm: the two in-slab modes of a d = 3 design (p1, p2 <= 32) run as DMMA
   // tiles over padded (ld kMmLD) buffers and dense padded Gram matrices
   const bool mm = path_mm(A) && !(P.dbg & (1024 | 1));  // needs the staged bands (dbg & 1 disables staging)
   const int qb = path_qb(A);
-  double* u = sxpp + q;
+  double* u = bn + q;
   double* t0 = u + qb;
   double* t1 = t0 + qb;
   double* band = t1 + qb;  // maxlen * q + 2
@@ -743,6 +744,8 @@ __global__ void __launch_bounds__(BS + (CW ? 32 : 0), (!CW && BS <= 256) ? 2 : 1
   unsigned parity = 0;
   const FistaCtl* tmpl = A.ctl;  // configuration (lambda filled per model); written back only at exit
   const double w = tmpl->sscale, n = tmpl->n, c0 = tmpl->ss_const;
+  const double wn = w / n;
+  for (int e = tx; e < q; e += BS) bn[e] = bs[e] / n;  // own elements only: no barrier
   const int bt_div = tmpl->bt_div, extrapolation = tmpl->extrapolation;
   auto reduce3 = [&](double a, double b, double c, double* out) {
     if (P.dbg & 4) {
@@ -1199,7 +1202,7 @@ __global__ void __launch_bounds__(BS + (CW ? 32 : 0), (!CW && BS <= 256) ? 2 : 1
             const double xi = xs[e], xpi = xps[e], sxi = sxs[e], sxpi = sxps[e];
             const double yi = xi + omega * (xi - xpi);
             const double syi = sxi + omega * (sxi - sxpi);
-            const double g = (w * syi - bs[e]) / n;
+            const double g = fma(wn, syi, -bn[e]);  // = -b/n exactly at S'y = 0 (the lambda_max step)
             double ci = __dsub_rn(yi, __dmul_rn(delta, g));
             if (lam > 0.0) ci = prox1(A.pen, A.alpha, gamma, ci);
             ul1 += fabs(ci);
@@ -1266,7 +1269,7 @@ __global__ void __launch_bounds__(BS + (CW ? 32 : 0), (!CW && BS <= 256) ? 2 : 1
           const double xi = xs[e], xpi = xps[e], sxi = sxs[e], sxpi = sxps[e];
           const double yi = xi + omega * (xi - xpi);
           const double syi = sxi + omega * (sxi - sxpi);
-          const double g = (w * syi - bs[e]) / n;
+          const double g = fma(wn, syi, -bn[e]);  // = -b/n exactly at S'y = 0 (the lambda_max step)
           double ci = __dsub_rn(yi, __dmul_rn(delta, g));
           if (lam > 0.0) ci = prox1(A.pen, A.alpha, gamma, ci);
           xps[e] = xi;
@@ -1374,7 +1377,7 @@ __global__ void __launch_bounds__(BS + (CW ? 32 : 0), (!CW && BS <= 256) ? 2 : 1
         const double xi = xs[e], xpi = xps[e], sxi = sxs[e], sxpi = sxps[e];
         const double yi = xi + omega * (xi - xpi);
         const double syi = sxi + omega * (sxi - sxpi);
-        const double g = (w * syi - bs[e]) / n;
+        const double g = fma(wn, syi, -bn[e]);  // = -b/n exactly at S'y = 0 (the lambda_max step)
         double ci = __dsub_rn(yi, __dmul_rn(delta, g));
         if (lam > 0.0) ci = prox1(A.pen, A.alpha, gamma, ci);
         xps[e] = xi;
@@ -1471,7 +1474,7 @@ static size_t path_smem(const GramStepArgs& A) {
   size_t staged = 0;  // staged Gram bands of modes 0 .. d-2
   for (int j = 0; j < A.d - 1; ++j) staged += static_cast<size_t>(A.dims[j]) * (kPathTaps * sizeof(double) + 2 * sizeof(int));
   const size_t dense = path_mm(A) ? 2 * kMmLD * 32 : 0;  // padded G_0, G_1
-  return (static_cast<size_t>(11 + A.Gd.maxlen) * A.q + 3 * static_cast<size_t>(path_qb(A)) + 4 + dense) *
+  return (static_cast<size_t>(12 + A.Gd.maxlen) * A.q + 3 * static_cast<size_t>(path_qb(A)) + 4 + dense) *
              sizeof(double) +
          staged;
 }
