@@ -160,12 +160,32 @@ kg_status kg_fit_path(kg_ctx* ctx, const kg_design* design, const kg_obs* obs, i
 int64_t kg_result_n_models(const kg_path_result* res);
 int kg_result_truncated(const kg_path_result* res);
 double kg_result_lambda_max(const kg_path_result* res);
+/* Per-model accessors (FitPath fields, path.hpp:18-27): t in [0, n_models);
+ * an out-of-range t returns NaN (doubles) or -1 (integers). */
 double kg_result_lambda(const kg_path_result* res, int64_t t);
 double kg_result_objective(const kg_path_result* res, int64_t t);
 int64_t kg_result_outer_iters(const kg_path_result* res, int64_t t);
 int64_t kg_result_inner_iters(const kg_path_result* res, int64_t t);
 int kg_result_status(const kg_path_result* res, int64_t t);
 int64_t kg_result_nonzero(const kg_path_result* res, int64_t t);
+
+/* One OuterRecord of OuterTrace (outer.hpp:26-47): the per-outer-iteration
+ * diagnostics of model t (FitPath::diagnostics, path.hpp:23). */
+typedef struct {
+  double objective;          /* F after the iteration (f_cur if the line search failed) */
+  double alpha;              /* accepted Armijo step t (0 if the line search failed; 1 on the Gaussian shortcut) */
+  double delta_k;            /* -<u(eta), eta~ - eta>/n + lambda (J(theta~) - J(theta)) (outer.cpp:118-120) */
+  double lipschitz;          /* L-hat of the inner solve (inner.cpp:132-135) */
+  int64_t inner_iterations;  /* fista_solve iterations */
+  int32_t inner_converged;   /* 1 if the inner solve met its tolerance */
+  int32_t armijo_j;          /* accepted backtracking index j (-1 if the line search failed) */
+} kg_outer_record;
+/* OuterTrace::initial_objective of model t (F at the warm start); NaN if t is out of range. */
+double kg_result_initial_objective(const kg_path_result* res, int64_t t);
+/* Number of OuterRecords of model t (-1 if t is out of range). */
+int64_t kg_result_n_outer(const kg_path_result* res, int64_t t);
+/* Copies the kg_result_n_outer(res, t) records of model t into out. */
+kg_status kg_result_trace(const kg_path_result* res, int64_t t, kg_outer_record* out);
 /* Nonzero coefficient count of every model (counted on the device): out
  * has kg_result_n_models entries. */
 kg_status kg_result_nonzeros(kg_path_result* res, int64_t* out);
@@ -216,6 +236,17 @@ int64_t kg_linear_index(int64_t d, const int64_t* multi_index, const int64_t* di
  * Predictions are computed on the device from the resident coefficients. */
 kg_status kg_mse_heldout(kg_ctx* ctx, const kg_design* design, const kg_path_result* res, int family,
                          const double* y_full, const double* mask, double* mse, int64_t* argmin);
+
+/* Deviance of every model of `res` against `obs` into out[0 .. n_models):
+ * eta_t = H(theta_t) computed on the device from the resident coefficients,
+ * then Gaussian sum a (y - mu)^2, Poisson 2 sum a [y log(y/mu) - (y - mu)],
+ * binomial 2 sum a [y log(y/mu) + (1-y) log((1-y)/(1-mu))], gamma 2 sum a
+ * [-log(y/mu) + (y - mu)/mu] (mu with the +-30 clamp, a = 0 cells skipped,
+ * 0 log 0 = 0).  Not a reference output: it is the derived quantity of the
+ * parity protocol (north_star "deviance within 1e-8"), with family.cpp's
+ * conventions (family.cpp:111-162).  Sharded contexts sum over the slabs. */
+kg_status kg_result_deviance(kg_ctx* ctx, const kg_design* design, const kg_obs* obs, const kg_path_result* res,
+                             int family, double* out);
 
 /* --------------------------------------------------------- measurement -- */
 /* Times `reps` launches of one hot-path kernel on the context stream with

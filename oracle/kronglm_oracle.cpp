@@ -399,6 +399,44 @@ double loglik(const Spec& s, const Data& d, const Arr& eta) {
   return sum / s.disp;
 }
 
+// Deviance of the fit (not a reference output; SURVEY 8(d) "Parity protocol"
+// defines it from eta with family.cpp's conventions): mu = mean(eta) with the
+// +-30 clamp, sequential sum over cells in flat order, a = 0 cells skipped,
+// 0 log 0 = 0.  Gaussian sum a (y - mu)^2; Poisson 2 sum a [y log(y/mu) -
+// (y - mu)]; binomial 2 sum a [y log(y/mu) + (1-y) log((1-y)/(1-mu))];
+// gamma 2 sum a [-log(y/mu) + (y - mu)/mu].
+static double xlogy_ratio(double y, double m) { return y == 0.0 ? 0.0 : y * std::log(y / m); }
+double deviance(const Spec& s, const Data& d, const Arr& eta) {
+  if (eta.ext != d.y.ext) throw Invalid("deviance: eta dims do not match the data");
+  double sum = 0.0;
+  for (I i = 0; i < eta.size(); ++i) {
+    const double ai = d.a[i];
+    if (ai == 0.0) continue;
+    const double yi = d.y[i], e = eta[i];
+    double t = 0.0;
+    switch (s.fam) {
+      case GAUSSIAN: t = ai * ((yi - e) * (yi - e)); break;
+      case BINOMIAL: {
+        const double mu = logistic(e);
+        t = 2.0 * ai * (xlogy_ratio(yi, mu) + xlogy_ratio(1.0 - yi, 1.0 - mu));
+        break;
+      }
+      case POISSON: {
+        const double mu = std::exp(clampe(e));
+        t = 2.0 * ai * (xlogy_ratio(yi, mu) - (yi - mu));
+        break;
+      }
+      case GAMMA: {
+        const double mu = std::exp(clampe(e));
+        t = 2.0 * ai * (-std::log(yi / mu) + (yi - mu) / mu);
+        break;
+      }
+    }
+    sum += t;
+  }
+  return sum;
+}
+
 // family.cpp:164-196
 Arr score(const Spec& s, const Data& d, const Arr& eta) {
   if (eta.ext != d.y.ext) throw Invalid("score: eta dims do not match the data");
@@ -1397,6 +1435,17 @@ int orc_loglik(int fam, double disp, int64_t n, const double* y, const double* a
   });
 }
 
+int orc_deviance(int fam, int64_t n, const double* y, const double* a, const double* eta, double* out) {
+  return guard([&] {
+    Spec s{fam, 1.0};
+    std::vector<I> ext{n};
+    Data d;
+    d.y = arr_from(ext, y);
+    d.a = arr_from(ext, a);
+    *out = deviance(s, d, arr_from(ext, eta));
+  });
+}
+
 int orc_validate(int fam, int64_t n, const double* y, const double* a) {
   return guard([&] {
     std::vector<I> ext{n};
@@ -1549,6 +1598,22 @@ void orc_path_coef(const orc_path* r, int64_t t, double* out) {
   std::memcpy(out, f.data(), sizeof(double) * f.size());
 }
 void orc_path_free(orc_path* r) { delete r; }
+// per-outer-iteration records of model t (OuterTrace, outer.hpp:26-47)
+int64_t orc_path_n_outer(const orc_path* r, int64_t t) {
+  return static_cast<int64_t>(r->fp.diag[static_cast<size_t>(t)].its.size());
+}
+// rec: objective, alpha, delta_k, lipschitz, inner_iterations, inner_converged, armijo_j
+void orc_path_trace(const orc_path* r, int64_t t, int64_t k, double* rec) {
+  const auto& o = r->fp.diag[static_cast<size_t>(t)].its[static_cast<size_t>(k)];
+  rec[0] = o.objective;
+  rec[1] = o.alpha;
+  rec[2] = o.delta_k;
+  rec[3] = o.lipschitz;
+  rec[4] = static_cast<double>(o.inner_iterations);
+  rec[5] = o.inner_converged ? 1.0 : 0.0;
+  rec[6] = static_cast<double>(o.armijo_j);
+}
+
 
 int orc_bspline_design(int64_t npts, const double* pts, int64_t order, int64_t nb, double* out) {
   return guard([&] {

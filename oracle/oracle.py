@@ -26,6 +26,7 @@ _lock = threading.Lock()
 FAMILIES = {"gaussian": 0, "binomial": 1, "poisson": 2, "gamma": 3}
 PENALTIES = {"lasso": 0, "ridge": 1, "elasticnet": 2, "elastic_net": 2}
 WEIGHT_MODES = {"exact": 0, "unit": 1, "one": 1, "tensor": 2, "tensor_approx": 2}
+TRACE_KEYS = ["objective", "alpha", "delta_k", "lipschitz", "inner_iterations", "inner_converged", "armijo_j"]
 STATUS = ["converged", "max_iterations", "line_search_failed", "inner_divergence"]
 
 _P = C.POINTER
@@ -80,6 +81,8 @@ def _declare(L):
         "orc_family_map": [C.c_int, _d, _i64, pd, pd, pd, C.c_int, pd],
         "orc_loglik": [C.c_int, _d, _i64, pd, pd, pd, pd],
         "orc_validate": [C.c_int, _i64, pd, pd],
+        "orc_deviance": [C.c_int, _i64, pd, pd, pd, pd],
+        "orc_path_n_outer": [vp, _i64], "orc_path_trace": [vp, _i64, _i64, pd],
         "orc_penalty_value": [C.c_int, _d, _i64, pd, pd],
         "orc_prox": [C.c_int, _d, _d, _i64, pd, pd],
         "orc_lambda_max": D + [C.c_int, _d, pd, pd, C.c_int, _d, pd],
@@ -98,7 +101,7 @@ def _declare(L):
     for name, args in sig.items():
         getattr(L, name).argtypes = args
     for name in ["orc_linear_index", "orc_rho", "orc_h_map", "orc_g_map", "orc_xtwx_apply", "orc_family_map",
-                 "orc_loglik", "orc_validate", "orc_penalty_value", "orc_prox", "orc_lambda_max",
+                 "orc_loglik", "orc_validate", "orc_deviance", "orc_penalty_value", "orc_prox", "orc_lambda_max",
                  "orc_spectral_radius", "orc_lipschitz_upper", "orc_fista_solve", "orc_outer_solve",
                  "orc_fit_path", "orc_bspline_design", "orc_default_basis_count", "orc_mse_heldout", "orc_bin_scatter"]:
         getattr(L, name).restype = C.c_int
@@ -121,6 +124,7 @@ def lib():
             L.orc_path_n_models.restype = _i64
             L.orc_path_lambda_max.restype = _d
             L.orc_path_truncated.restype = C.c_int
+            L.orc_path_n_outer.restype = _i64
             _declare(L)
             _lib = L
     return _lib
@@ -297,6 +301,17 @@ def loglik(family, y, eta, a=None, dispersion=1.0):
     return out.value
 
 
+def deviance(family, y, eta, a=None):
+    """Deviance from eta (SURVEY 8(d) parity protocol; family.cpp conventions)."""
+    eta = np.ascontiguousarray(np.asarray(eta, np.float64).ravel(order="F"))
+    n = eta.size
+    y = np.ascontiguousarray(np.asarray(y, np.float64).ravel(order="F"))
+    a = np.ones(n) if a is None else np.ascontiguousarray(np.asarray(a, np.float64).ravel(order="F"))
+    out = _d()
+    _check(lib().orc_deviance(FAMILIES[family], n, _ptr(y), _ptr(a), _ptr(eta), C.byref(out)))
+    return out.value
+
+
 def validate(family, y, a=None):
     y = np.ascontiguousarray(np.asarray(y, np.float64).ravel(order="F"))
     a = np.ones(y.size) if a is None else np.ascontiguousarray(np.asarray(a, np.float64).ravel(order="F"))
@@ -420,7 +435,7 @@ def fit_path(design, family, y, weights=None, penalty="lasso", alpha=0.0, n_lamb
         info = np.zeros(6)
         out = {"lambdas": [], "objectives": [], "lambda_max": L.orc_path_lambda_max(h),
                "truncated": bool(L.orc_path_truncated(h)), "coefficients": [], "nonzero": [],
-               "outer_iters": [], "converged": [], "inner_iters": [], "status": []}
+               "outer_iters": [], "converged": [], "inner_iters": [], "status": [], "traces": []}
         for t in range(m):
             L.orc_path_model(h, _i64(t), _ptr(info))
             flat = np.zeros(D.p_total)
@@ -433,6 +448,13 @@ def fit_path(design, family, y, weights=None, penalty="lasso", alpha=0.0, n_lamb
             out["converged"].append(bool(info[5]))
             out["coefficients"].append(D.blocks(flat))
             out["nonzero"].append(int(np.count_nonzero(flat)))
+            rec = np.zeros(7)
+            tr = []
+            for k in range(L.orc_path_n_outer(h, _i64(t))):
+                L.orc_path_trace(h, _i64(t), _i64(k), _ptr(rec))
+                tr.append(dict(zip(TRACE_KEYS, [float(rec[0]), float(rec[1]), float(rec[2]), float(rec[3]),
+                                                int(rec[4]), bool(rec[5]), int(rec[6])])))
+            out["traces"].append(tr)
         return out
     finally:
         L.orc_path_free(h)

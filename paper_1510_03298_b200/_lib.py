@@ -33,6 +33,12 @@ class InvalidArgument(KgError, ValueError):
     """std::invalid_argument -> Python ValueError (as pybind11 maps it)."""
 
 
+class OuterRecord(C.Structure):
+    """kg_outer_record: one OuterRecord of OuterTrace (outer.hpp:26-47)."""
+    _fields_ = [("objective", _d), ("alpha", _d), ("delta_k", _d), ("lipschitz", _d),
+                ("inner_iterations", _i64), ("inner_converged", C.c_int32), ("armijo_j", C.c_int32)]
+
+
 class PathCfg(C.Structure):
     _fields_ = [
         ("n_lambda", _i64), ("lambda_min_ratio", _d), ("max_outer", _i64),
@@ -76,6 +82,10 @@ _SIGS = {
     "kg_result_inner_iters": (_i64, [_vp, _i64]),
     "kg_result_status": (C.c_int, [_vp, _i64]),
     "kg_result_nonzero": (_i64, [_vp, _i64]),
+    "kg_result_initial_objective": (_d, [_vp, _i64]),
+    "kg_result_n_outer": (_i64, [_vp, _i64]),
+    "kg_result_trace": (C.c_int, [_vp, _i64, _P(OuterRecord)]),
+    "kg_result_deviance": (C.c_int, [_vp, _vp, _vp, _vp, C.c_int, _pd]),
     "kg_result_nonzeros": (C.c_int, [_vp, C.POINTER(_i64)]),
     "kg_result_coef": (C.c_int, [_vp, _i64, _pd]),
     "kg_result_coefs": (C.c_int, [_vp, _i64, _i64, _pd]),

@@ -1,6 +1,7 @@
 """In-tree build of libkronglm_b200.so for sm_100a (nvcc cross-compiles without a GPU)."""
 import os
 import subprocess
+from concurrent.futures import ThreadPoolExecutor
 
 HERE = os.path.dirname(os.path.abspath(__file__))
 ROOT = os.path.dirname(HERE)
@@ -8,7 +9,8 @@ CSRC = os.path.join(HERE, "csrc")
 LIB = os.path.join(HERE, "libkronglm_b200.so")
 SOURCES = ["kg_kernels.cu", "kg_fused.cu", "kg_gram.cu", "kg_slab.cu", "kg_builders.cu", "kg_solver.cu", "kg_host.cpp"]
 NVCC_FLAGS = ["-gencode", "arch=compute_100a,code=sm_100a", "-O3", "-std=c++17", "-lineinfo",
-              "-Xcompiler", "-fPIC,-Wno-nonnull", "-shared", "-diag-suppress", "177"]
+              "-Xcompiler", "-fPIC,-Wno-nonnull", "-diag-suppress", "177"]
+OBJ = os.path.join(HERE, "build")
 
 
 def nvcc():
@@ -27,10 +29,23 @@ def needs_build():
 def build(force=False, verbose=False):
     if not force and not needs_build():
         return LIB
-    cmd = [nvcc()] + NVCC_FLAGS + ["-o", LIB] + [os.path.join(CSRC, s) for s in SOURCES] + ["-ldl"]
-    if verbose:
-        print(" ".join(cmd))
-    subprocess.run(cmd, check=True)
+    # one nvcc per translation unit, in parallel, then one shared link
+    os.makedirs(OBJ, exist_ok=True)
+
+    def compile_one(src):
+        obj = os.path.join(OBJ, os.path.splitext(src)[0] + ".o")
+        cmd = [nvcc()] + NVCC_FLAGS + ["-c", "-o", obj, os.path.join(CSRC, src)]
+        if verbose:
+            print(" ".join(cmd))
+        subprocess.run(cmd, check=True)
+        return obj
+
+    with ThreadPoolExecutor(max_workers=len(SOURCES)) as ex:
+        objs = list(ex.map(compile_one, SOURCES))
+    tmp = LIB + ".tmp"
+    subprocess.run([nvcc(), "-gencode", "arch=compute_100a,code=sm_100a", "-shared", "-o", tmp] + objs + ["-ldl"],
+                   check=True)
+    os.replace(tmp, LIB)
     return LIB
 
 

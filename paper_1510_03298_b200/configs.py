@@ -8,20 +8,37 @@ from __future__ import annotations
 
 import numpy as np
 
-from . import kronglm as K
-
 SEED0 = 1510032980
 
 
-def _factors(n, p):
-    return [K.bspline_design(np.linspace(0.0, 1.0, nj), 4, pj) for nj, pj in zip(n, p)]
+def _factors(n, p, bspline=None):
+    if bspline is None:
+        from . import kronglm as K
+        bspline = K.bspline_design
+    return [bspline(np.linspace(0.0, 1.0, nj), 4, pj) for nj, pj in zip(n, p)]
 
 
 def tensor_h(factors, B):
-    """eta = H(X, B) by successive mode products (numpy; input generation only)."""
-    out = np.asarray(B)
+    """eta = H(X, B) by successive mode products (input generation only).
+
+    Each mode product is accumulated column by column of the factor in
+    ascending order with separate elementwise multiplies and adds, over the
+    rows where that column is nonzero, so the result is bit-reproducible on
+    any host (no BLAS, whose kernel choice and summation order depend on the
+    CPU): the parity fixtures in tests/golden/ are keyed to these bytes."""
+    out = np.asarray(B, dtype=np.float64)
     for j, X in enumerate(factors):
-        out = np.moveaxis(np.tensordot(X, out, axes=([1], [j])), 0, j)
+        X = np.asarray(X, dtype=np.float64)
+        src = np.moveaxis(out, j, 0)
+        acc = np.zeros((X.shape[0],) + src.shape[1:])
+        for k in range(X.shape[1]):
+            rows = np.flatnonzero(X[:, k])
+            if rows.size == 0:
+                continue
+            lo, hi = rows[0], rows[-1] + 1
+            col = X[lo:hi, k].reshape((hi - lo,) + (1,) * (src.ndim - 1))
+            acc[lo:hi] = acc[lo:hi] + col * src[k][None]
+        out = np.moveaxis(acc, 0, j)
     return np.asfortranarray(out)
 
 
@@ -41,13 +58,18 @@ CONFIGS = {
 }
 
 
-def make(name: str, scale: float | None = None):
-    """Returns dict(design=[[X1..Xd]], y, family, n_lambda, lambda_min_ratio, meta)."""
+def make(name: str, bspline=None):
+    """Returns dict(design=[[X1..Xd]], y, family, n_lambda, lambda_min_ratio, meta).
+
+    `bspline` builds the factors (default: the product's kg_bspline_design;
+    the CPU-only callers -- the reference arm of bench.py and the fixture
+    script -- pass their own bit-identical builder so they never load the
+    product library)."""
     cfg = dict(CONFIGS[name])
     k = int(name[1])
     rng = np.random.default_rng(SEED0 + k)
     n, p = cfg["n"], cfg["p"]
-    X = _factors(n, p)
+    X = _factors(n, p, bspline)
     meta = {}
     if name == "C1":
         B = _sparse_coef(rng, p, 0.05)

@@ -197,7 +197,7 @@ template <int D, bool HIST>
 void launch_bin_t(const Launch& L, const BinArgs& A, bool staged, int n_sm) {
   const size_t shmem = bin_smem_bytes(A, HIST, staged);
   auto kern = staged ? k_bin_staged<D, HIST> : k_bin_direct<D, HIST>;
-  KG_CUDA(cudaFuncSetAttribute(kern, cudaFuncAttributeMaxDynamicSharedMemorySize, static_cast<int>(shmem)));
+  smem_attr(kern, static_cast<int>(shmem));
   int occ = 0;
   KG_CUDA(cudaOccupancyMaxActiveBlocksPerMultiprocessor(&occ, kern, kBinThreads, shmem));
   occ = std::max(occ, 1);

@@ -480,14 +480,8 @@ static int fused_bs() {
 
 template <int VAR, int MG>
 static void launch_fast_one(const Launch& L, const FusedArgs& f, const FusedPlan& pl, i64 ntiles, int g, size_t sm) {
-  static bool attr = false;
-  if (!attr) {
-    KG_CUDA(cudaFuncSetAttribute(k_fused_fast<VAR, MG, 256>, cudaFuncAttributeMaxDynamicSharedMemorySize,
-                                 210 * 1024));
-    KG_CUDA(cudaFuncSetAttribute(k_fused_fast<VAR, MG, 512>, cudaFuncAttributeMaxDynamicSharedMemorySize,
-                                 210 * 1024));
-    attr = true;
-  }
+  smem_attr(k_fused_fast<VAR, MG, 256>, 210 * 1024);
+  smem_attr(k_fused_fast<VAR, MG, 512>, 210 * 1024);
   if (fused_bs() == 512 && f.n1 <= 512 && f.p1 <= 512)
     k_fused_fast<VAR, MG, 512><<<g, 512, sm, L.s>>>(f, pl, ntiles);
   else
@@ -711,12 +705,10 @@ static LcPlan lc_plan(const FusedArgs& f) {
 template <int KS>
 static void launch_mma(const Launch& L, const FusedArgs& f, const LcPlan& P, i64 ntiles) {
   if (P.bs == 512) {
-    KG_CUDA(cudaFuncSetAttribute(k_fused_mma<KS, 512>, cudaFuncAttributeMaxDynamicSharedMemorySize,
-                                 static_cast<int>(P.smem)));
+    smem_attr(k_fused_mma<KS, 512>, static_cast<int>(P.smem));
     k_fused_mma<KS, 512><<<P.grid, 512, P.smem, L.s>>>(f, P.pl, ntiles, P.sw, P.wp_off);
   } else {
-    KG_CUDA(cudaFuncSetAttribute(k_fused_mma<KS, 256>, cudaFuncAttributeMaxDynamicSharedMemorySize,
-                                 static_cast<int>(P.smem)));
+    smem_attr(k_fused_mma<KS, 256>, static_cast<int>(P.smem));
     k_fused_mma<KS, 256><<<P.grid, 256, P.smem, L.s>>>(f, P.pl, ntiles, P.sw, P.wp_off);
   }
 }
@@ -739,13 +731,9 @@ void fused_tma(const Launch& L, int variant, const FusedArgs& f) {
   const i64 ntiles = (f.m + pl.T - 1) / pl.T;
   const size_t sm = static_cast<size_t>(pl.nst) * pl.stage * sizeof(double);
   const int g = fused_tma_grid(f, variant);
-  static bool attr = false;
-  if (!attr) {
-    KG_CUDA(cudaFuncSetAttribute(k_fused_tma<FV_FISTA>, cudaFuncAttributeMaxDynamicSharedMemorySize, 210 * 1024));
-    KG_CUDA(cudaFuncSetAttribute(k_fused_tma<FV_XTWZ>, cudaFuncAttributeMaxDynamicSharedMemorySize, 210 * 1024));
-    KG_CUDA(cudaFuncSetAttribute(k_fused_tma<FV_SCORE0>, cudaFuncAttributeMaxDynamicSharedMemorySize, 210 * 1024));
-    attr = true;
-  }
+  smem_attr(k_fused_tma<FV_FISTA>, 210 * 1024);
+  smem_attr(k_fused_tma<FV_XTWZ>, 210 * 1024);
+  smem_attr(k_fused_tma<FV_SCORE0>, 210 * 1024);
   const bool fast = f.n1 <= NT && f.p1 <= NT && f.H.maxlen <= 4 && f.G.maxlen <= 64;
   if (fast) {
     const int mg = f.G.maxlen <= 8 ? 8 : f.G.maxlen <= 16 ? 16 : f.G.maxlen <= 24 ? 24 : f.G.maxlen <= 32 ? 32 : 64;
@@ -860,11 +848,7 @@ void contract_tiled(const Launch& L, const double* A, double* out, i64 a, i64 K,
   const i64 ntiles = pl.nab * pl.nmb * b;
   const int g = static_cast<int>(std::min<i64>(ntiles, 148LL * 8));
   const size_t sm = static_cast<size_t>(pl.AB) * pl.WMAX * sizeof(double);
-  static bool attr = false;
-  if (!attr) {
-    KG_CUDA(cudaFuncSetAttribute(k_contract_tiled, cudaFuncAttributeMaxDynamicSharedMemorySize, 200 * 1024));
-    attr = true;
-  }
+  smem_attr(k_contract_tiled, 200 * 1024);
   k_contract_tiled<<<g, NT, sm, L.s>>>(A, out, a, K, M, op, pl, accumulate);
   launched(L);
 }

@@ -345,12 +345,8 @@ __global__ void __launch_bounds__(BS) k_gram_apply(GramStepArgs A) {
 bool gram_step_fits(i64 q) { return 3 * q * static_cast<i64>(sizeof(double)) <= 200 * 1024; }
 
 void gram_step(const Launch& L, const GramStepArgs& A) {
-  static bool attr = false;
-  if (!attr) {
-    KG_CUDA(cudaFuncSetAttribute(k_gram_apply<256, true>, cudaFuncAttributeMaxDynamicSharedMemorySize, 210 * 1024));
-    KG_CUDA(cudaFuncSetAttribute(k_gram_apply<256, false>, cudaFuncAttributeMaxDynamicSharedMemorySize, 210 * 1024));
-    attr = true;
-  }
+  smem_attr(k_gram_apply<256, true>, 210 * 1024);
+  smem_attr(k_gram_apply<256, false>, 210 * 1024);
   const size_t base = 3 * static_cast<size_t>(A.q) * sizeof(double);
   const size_t staged = base + (static_cast<size_t>(A.Gd.maxlen + 1) * A.q + 4) * sizeof(double);
   if (staged <= 200 * 1024) {
@@ -1394,7 +1390,7 @@ __global__ void __launch_bounds__(BS + (CW ? 32 : 0), (!CW && BS <= 256) ? 2 : 1
       __syncthreads();
     }
     // best := x if the last monitor left a copy pending (k_fista_finalize)
-    double bb = 0.0, bsb = 0.0, bl1 = 0.0, bl2 = 0.0;
+    double bb = 0.0, bsb = 0.0, bl1 = 0.0, bl2 = 0.0, tsb = 0.0;
     for (int e = tx; e < q; e += BS) {
       if (cs.copy_best) {
         bst[e] = xs[e];
@@ -1405,22 +1401,33 @@ __global__ void __launch_bounds__(BS + (CW ? 32 : 0), (!CW && BS <= 256) ? 2 : 1
       bsb += v * sbst[e];
       bl1 += fabs(v);
       bl2 = fma(v, v, bl2);
+      tsb += sth[e] * v;  // <S' theta, best> for Delta_k
     }
     double r[3];
     reduce3(bb, bsb, bl1, r);
     const double rl2 = cta_sum<BS>(bl2, red);
+    const double rts = cta_sum<BS>(tsb, red);
     if (threadIdx.x == 0) {
-      P.part2[4 * s] = r[0];
-      P.part2[4 * s + 1] = r[1];
-      P.part2[4 * s + 2] = r[2];
-      P.part2[4 * s + 3] = rl2;
+      P.part2[5 * s] = r[0];
+      P.part2[5 * s + 1] = r[1];
+      P.part2[5 * s + 2] = r[2];
+      P.part2[5 * s + 3] = rl2;
+      P.part2[5 * s + 4] = rts;
     }
     grid_sync(P.bar, nb);
-    double g4[4] = {0.0, 0.0, 0.0, 0.0};
-    for (int k = 0; k < 4; ++k) {
+    double g4[5] = {0.0, 0.0, 0.0, 0.0, 0.0};
+    for (int k = 0; k < 5; ++k) {
       double a = 0.0;
-      for (int rr = tx; rr < static_cast<int>(nb); rr += BS) a += __ldcg(P.part2 + 4 * rr + k);
+      for (int rr = tx; rr < static_cast<int>(nb); rr += BS) a += __ldcg(P.part2 + 5 * rr + k);
       g4[k] = cta_sum<BS>(a, red);
+    }
+    // Delta_k = -<u(eta), eta_t - eta>/n + lambda (J(best) - J(theta)) with
+    // X^T u(eta) = b - w S' theta: <b - w S' theta, best - theta>
+    const double dk = -((g4[0] - tb) - w * (g4[4] - tst)) / n +
+                      lam * (penalty_of(A.pen, A.alpha, g4[2], g4[3]) - j_th);
+    if (s == 0 && threadIdx.x == 0 && P.dk_out) {
+      P.dk_out[2 * t] = dk;
+      P.dk_out[2 * t + 1] = f_cur;
     }
     const int status = cs.converged ? KG_S_CONVERGED : (cs.diverged ? KG_S_INNER_DIVERGENCE : KG_S_MAX_ITERATIONS);
     double f = f_cur;
@@ -1528,7 +1535,7 @@ static PathVariant pick_variant(const GramStepArgs& A) {
   KG_CUDA(cudaDeviceGetAttribute(&nsm, cudaDevAttrMultiProcessorCount, dev));
   const PathVariant cands[2] = {path_variant(path_cw(), path_bs()), path_variant(false, 256)};
   for (const PathVariant& v : cands) {
-    KG_CUDA(cudaFuncSetAttribute(v.fn, cudaFuncAttributeMaxDynamicSharedMemorySize, 210 * 1024));
+    smem_attr(v.fn, 210 * 1024);
     int per_sm = 0;
     KG_CUDA(cudaOccupancyMaxActiveBlocksPerMultiprocessor(&per_sm, v.fn, v.threads, sm));
     if (static_cast<i64>(per_sm) * nsm >= A.pd) return v;
@@ -1558,11 +1565,7 @@ static size_t persist_smem(const GramStepArgs& A) {
 bool fista_persist_ok(const GramStepArgs& A) {
   const size_t sm = persist_smem(A);
   if (sm > 200 * 1024) return false;
-  static bool attr = false;
-  if (!attr) {
-    KG_CUDA(cudaFuncSetAttribute(k_fista_persist<256>, cudaFuncAttributeMaxDynamicSharedMemorySize, 210 * 1024));
-    attr = true;
-  }
+  smem_attr(k_fista_persist<256>, 210 * 1024);
   int per_sm = 0, dev = 0, nsm = 0;
   KG_CUDA(cudaOccupancyMaxActiveBlocksPerMultiprocessor(&per_sm, k_fista_persist<256>, 256, sm));
   KG_CUDA(cudaGetDevice(&dev));

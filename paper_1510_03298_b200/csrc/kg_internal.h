@@ -29,6 +29,15 @@ enum { E_INVAL = 1, E_EVAL = 2, E_RUNTIME = 3, E_DIVERGE = 4, E_POWER = 5, E_CUD
                         std::string(#expr) + ": " + cudaGetErrorString(e__));                         \
   } while (0)
 
+// cudaFuncAttributeMaxDynamicSharedMemorySize is a per-device attribute:
+// raise it once per (current device, kernel) to at least `bytes`.  Thread
+// safe; contexts on several devices each get it set (kg_solver.cu).
+void smem_attr_raw(const void* fn, int bytes);
+template <class K>
+inline void smem_attr(K* fn, int bytes) {
+  smem_attr_raw(reinterpret_cast<const void*>(fn), bytes);
+}
+
 // Division by a loop-invariant divisor as multiply-high + shift (valid for
 // numerators < 2^31); built on the host, used in kernels.
 struct FastDiv {
@@ -260,6 +269,9 @@ void band_dense(const Launch& L, const BandOp& g, const double* coef, i64 p, dou
 // per-CTA (elem_grid(n)) partials of sum_{mask == 1} (mu - y)^2
 void masked_sse(const Launch& L, i64 n, const double* mu, const double* y, const double* mask, double* part);
 void fill(const Launch& L, i64 n, double v, double* x);
+// per-CTA (elem_grid(n)) partials of the deviance of eta (kg_result_deviance)
+void deviance_pass(const Launch& L, i64 n, int fam, const double* y, const double* a, const double* eta,
+                   double* part);
 
 // p-space
 int pgrid(i64 p);
@@ -328,7 +340,8 @@ struct PersistArgs {
   // whole-path mode (k_gauss_path)
   const double* lambdas = nullptr;
   int n_lambda = 0;
-  double* part2 = nullptr;    // 4 per CTA
+  double* part2 = nullptr;    // 5 per CTA
+  double* dk_out = nullptr;   // 2 n_lambda: Delta_k (outer.cpp:224-226) and the initial objective per model
   double* coefs = nullptr;    // n_lambda x p result buffer
   double* obj_out = nullptr;  // n_lambda
   i64* iters_out = nullptr;   // n_lambda

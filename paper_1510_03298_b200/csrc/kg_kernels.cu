@@ -496,13 +496,9 @@ int fused_grid(const FusedArgs& f) { return static_cast<int>((f.m + f.T - 1) / f
 void fused_mode1(const Launch& L, int variant, const FusedArgs& f) {
   const size_t sm = fused_smem(f);
   const int g = fused_grid(f);
-  static bool attr = false;
-  if (!attr) {
-    KG_CUDA(cudaFuncSetAttribute(k_fused1<FV_FISTA>, cudaFuncAttributeMaxDynamicSharedMemorySize, 200 * 1024));
-    KG_CUDA(cudaFuncSetAttribute(k_fused1<FV_XTWZ>, cudaFuncAttributeMaxDynamicSharedMemorySize, 200 * 1024));
-    KG_CUDA(cudaFuncSetAttribute(k_fused1<FV_SCORE0>, cudaFuncAttributeMaxDynamicSharedMemorySize, 200 * 1024));
-    attr = true;
-  }
+  smem_attr(k_fused1<FV_FISTA>, 200 * 1024);
+  smem_attr(k_fused1<FV_XTWZ>, 200 * 1024);
+  smem_attr(k_fused1<FV_SCORE0>, 200 * 1024);
   switch (variant) {
     case FV_FISTA: k_fused1<FV_FISTA><<<g, NT, sm, L.s>>>(f); break;
     case FV_XTWZ: k_fused1<FV_XTWZ><<<g, NT, sm, L.s>>>(f); break;
@@ -585,11 +581,7 @@ __global__ void __launch_bounds__(NT) k_hlast(HlastArgs h) {
 int hlast_grid(const HlastArgs& h) { return static_cast<int>((h.m + h.T - 1) / h.T); }
 
 void hlast_mode1(const Launch& L, const HlastArgs& h) {
-  static bool attr = false;
-  if (!attr) {
-    KG_CUDA(cudaFuncSetAttribute(k_hlast, cudaFuncAttributeMaxDynamicSharedMemorySize, 200 * 1024));
-    attr = true;
-  }
+  smem_attr(k_hlast, 200 * 1024);
   const size_t sm = h.P ? static_cast<size_t>(h.p1) * h.T * sizeof(double) : 0;
   k_hlast<<<hlast_grid(h), NT, sm, L.s>>>(h);
   bump(L);
@@ -964,6 +956,44 @@ __global__ void __launch_bounds__(NT) k_masked_sse(i64 n, const double* mu, cons
 
 void masked_sse(const Launch& L, i64 n, const double* mu, const double* y, const double* mask, double* part) {
   k_masked_sse<<<elem_grid(n), NT, 0, L.s>>>(n, mu, y, mask, part);
+  bump(L);
+}
+
+// Deviance terms of eta (SURVEY 8(d) parity protocol, family.cpp conventions:
+// mu with the +-30 clamp, a = 0 cells skipped, 0 log 0 = 0), per-CTA partials.
+__device__ __forceinline__ double xlogy_ratio(double y, double m) { return y == 0.0 ? 0.0 : y * log(y / m); }
+__global__ void __launch_bounds__(NT) k_deviance(i64 n, int fam, const double* __restrict__ y,
+                                                 const double* __restrict__ a, const double* __restrict__ eta,
+                                                 double* part) {
+  __shared__ double red[32];
+  double s = 0.0;
+  for (i64 i = static_cast<i64>(blockIdx.x) * NT + threadIdx.x; i < n; i += static_cast<i64>(gridDim.x) * NT) {
+    const double ai = a[i];
+    if (ai == 0.0) continue;
+    const double yi = y[i], e = eta[i];
+    double t;
+    if (fam == 0) {
+      const double r = yi - e;
+      t = ai * (r * r);
+    } else if (fam == 1) {
+      const double mu = logistic(e);
+      t = 2.0 * ai * (xlogy_ratio(yi, mu) + xlogy_ratio(1.0 - yi, 1.0 - mu));
+    } else if (fam == 2) {
+      const double mu = exp(clampe(e));
+      t = 2.0 * ai * (xlogy_ratio(yi, mu) - (yi - mu));
+    } else {
+      const double mu = exp(clampe(e));
+      t = 2.0 * ai * (-log(yi / mu) + (yi - mu) / mu);
+    }
+    s += t;
+  }
+  const double r = block_reduce<false>(s, red);
+  if (threadIdx.x == 0) part[blockIdx.x] = r;
+}
+
+void deviance_pass(const Launch& L, i64 n, int fam, const double* y, const double* a, const double* eta,
+                   double* part) {
+  k_deviance<<<elem_grid(n), NT, 0, L.s>>>(n, fam, y, a, eta, part);
   bump(L);
 }
 
@@ -1653,8 +1683,7 @@ void power_iterations(const Launch& L, const PowerJob* jobs_dev, int njobs, i64 
   need = std::min<i64>(need, 220 * 1024 / 8);
   if (2 * max_p > need) throw Error(E_INVAL, "spectral_radius: factor too large for the device power iteration");
   const size_t sm = sizeof(double) * static_cast<size_t>(need);
-  if (sm > 48 * 1024)
-    KG_CUDA(cudaFuncSetAttribute(k_power, cudaFuncAttributeMaxDynamicSharedMemorySize, static_cast<int>(sm)));
+  if (sm > 48 * 1024) smem_attr(k_power, static_cast<int>(sm));
   k_power<<<njobs, static_cast<unsigned>(threads), sm, L.s>>>(jobs_dev, tol, max_iters, need);
   bump(L);
 }

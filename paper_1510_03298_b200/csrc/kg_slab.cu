@@ -276,11 +276,7 @@ SlabShape slab_shape(const SlabArgs& a) {
 
 template <int R, int KS>
 void launch_slab(const Launch& L, SlabArgs a, const SlabShape& s, int grid) {
-  static bool attr = false;
-  if (!attr) {
-    KG_CUDA(cudaFuncSetAttribute(k_slab12<R, KS>, cudaFuncAttributeMaxDynamicSharedMemorySize, 220 * 1024));
-    attr = true;
-  }
+  smem_attr(k_slab12<R, KS>, 220 * 1024);
   a.CG = s.CG;
   k_slab12<R, KS><<<grid, SB, s.smem, L.s>>>(a);
 }

@@ -127,6 +127,23 @@ static NcclApi* nccl_api() {
   return &api;
 }
 
+void smem_attr_raw(const void* fn, int bytes) {
+  static std::mutex mu;
+  static std::vector<std::pair<std::pair<int, const void*>, int>> done;  // (device, kernel) -> bytes set
+  int dev = 0;
+  KG_CUDA(cudaGetDevice(&dev));
+  std::lock_guard<std::mutex> lk(mu);
+  for (auto& e : done)
+    if (e.first.first == dev && e.first.second == fn) {
+      if (e.second >= bytes) return;
+      KG_CUDA(cudaFuncSetAttribute(fn, cudaFuncAttributeMaxDynamicSharedMemorySize, bytes));
+      e.second = bytes;
+      return;
+    }
+  KG_CUDA(cudaFuncSetAttribute(fn, cudaFuncAttributeMaxDynamicSharedMemorySize, bytes));
+  done.push_back({{dev, fn}, bytes});
+}
+
 static void nccl_check(ncclResult_t r, const char* what) {
   if (r != ncclSuccess) throw Error(E_NCCL, std::string(what) + ": " + nccl_api()->GetErrorString(r));
 }
@@ -1563,7 +1580,8 @@ static double lambda_max_fit(Fit& F) {
 struct kg_path_result {
   kg_ctx* ctx = nullptr;
   kg::i64 p = 0;
-  std::vector<double> lambdas, objectives;
+  std::vector<double> lambdas, objectives, initial_objectives;
+  std::vector<std::vector<kg_outer_record>> traces;  // OuterTrace.iterations per model (outer.hpp:26-47)
   std::vector<kg::i64> outer_iters, inner_iters, nnz;
   std::vector<int> status;
   bool truncated = false;
@@ -1576,8 +1594,22 @@ namespace kg {
 struct ModelTrace {
   int status = 1;
   i64 outer = 0, inner = 0;
-  double final_objective = 0.0;
+  double initial_objective = 0.0, final_objective = 0.0;
+  std::vector<kg_outer_record> recs;  // one per outer iteration (OuterRecord, outer.hpp:26-33)
 };
+
+static kg_outer_record outer_rec(double objective, double alpha, double delta_k, double lip, i64 inner, bool conv,
+                                 int j) {
+  kg_outer_record r;
+  r.objective = objective;
+  r.alpha = alpha;
+  r.delta_k = delta_k;
+  r.lipschitz = lip;
+  r.inner_iterations = inner;
+  r.inner_converged = conv ? 1 : 0;
+  r.armijo_j = j;
+  return r;
+}
 
 // ------------------------------------------------------------ outer_solve
 struct OuterCfg {
@@ -1608,8 +1640,10 @@ static ModelTrace gaussian_step_gram(Fit& F, double lambda, const OuterCfg& oc, 
   const double n = static_cast<double>(F.D->N_full);
   const double w = F.wconst;
   const double ll_cur = st.tb - 0.5 * w * st.tst;
-  const double f_cur = -ll_cur / n + lambda * penalty_of(F.pen, F.alpha, st.l1, st.l2);
+  const double J_cur = penalty_of(F.pen, F.alpha, st.l1, st.l2);
+  const double f_cur = -ll_cur / n + lambda * J_cur;
   ModelTrace tr;
+  tr.initial_objective = f_cur;
   fista_enqueue(F, lambda, oc.inner, F.part.d() + F.D->part_cap - n_vmax, n_vmax);
   const int g = gauss_dots(ctx->L(), F.p, w, F.theta.d(), F.stheta.d(), F.best.d(), F.Sbest.d(), F.b.d(),
                            F.part.d());
@@ -1627,7 +1661,10 @@ static ModelTrace gaussian_step_gram(Fit& F, double lambda, const OuterCfg& oc, 
   }
   const double tb = pin[2], tst = pin[3], l1 = pin[5], l2 = pin[6];
   const double ll_new = tb - 0.5 * w * tst;
-  const double f_new = -ll_new / n + lambda * penalty_of(F.pen, F.alpha, l1, l2);
+  const double J_t = penalty_of(F.pen, F.alpha, l1, l2);
+  const double f_new = -ll_new / n + lambda * J_t;
+  // Delta_k (outer.cpp:224-226): X^T u(eta) = b - w S' theta
+  const double delta_k = -pin[4] / n + lambda * (J_t - J_cur);
   double f = f_cur;
   if (f_new <= f_cur) {
     pcopy(ctx->L(), F.p, F.best.d(), F.theta.d(), nullptr, nullptr);
@@ -1640,6 +1677,7 @@ static ModelTrace gaussian_step_gram(Fit& F, double lambda, const OuterCfg& oc, 
   }
   tr.outer = 1;
   tr.final_objective = f;
+  tr.recs.push_back(outer_rec(f, 1.0, delta_k, fo.lip, fo.iterations, fo.converged, 0));
   tr.status = fo.converged ? KG_S_CONVERGED : KG_S_MAX_ITERATIONS;
   return tr;
 }
@@ -1648,8 +1686,10 @@ static ModelTrace gaussian_step(Fit& F, double lambda, const OuterCfg& oc, PathS
   if (F.route == 1) return gaussian_step_gram(F, lambda, oc, st, n_vmax);
   kg_ctx* ctx = F.ctx;
   const double n = static_cast<double>(F.D->N_full);
-  const double f_cur = -st.ll / n + lambda * penalty_of(F.pen, F.alpha, st.l1, st.l2);
+  const double J_cur = penalty_of(F.pen, F.alpha, st.l1, st.l2);
+  const double f_cur = -st.ll / n + lambda * J_cur;
   ModelTrace tr;
+  tr.initial_objective = f_cur;
   reset_errs(F);
   fista_enqueue(F, lambda, oc.inner, F.part.d() + F.D->part_cap - n_vmax, n_vmax);
   // eta_tilde = H(best); loglik(eta_tilde) and <u(eta), eta_tilde - eta> in the same pass.
@@ -1679,7 +1719,9 @@ static ModelTrace gaussian_step(Fit& F, double lambda, const OuterCfg& oc, PathS
   check_ll_errs(F, errs);
   if (errs[1] != kNoErr) throw Error(E_EVAL, "non-finite score entry at cell " + std::to_string(errs[1]), errs[1]);
   const double ll_new = pin[0] / F.disp, l1 = pin[16], l2 = pin[17];
-  const double f_new = -ll_new / n + lambda * penalty_of(F.pen, F.alpha, l1, l2);
+  const double J_t = penalty_of(F.pen, F.alpha, l1, l2);
+  const double f_new = -ll_new / n + lambda * J_t;
+  const double delta_k = -pin[1] / n + lambda * (J_t - J_cur);  // outer.cpp:224-226
   double f = f_cur;
   if (f_new <= f_cur) {
     pcopy(ctx->L(), F.p, F.best.d(), F.theta.d(), nullptr, nullptr);
@@ -1691,6 +1733,7 @@ static ModelTrace gaussian_step(Fit& F, double lambda, const OuterCfg& oc, PathS
   }
   tr.outer = 1;
   tr.final_objective = f;
+  tr.recs.push_back(outer_rec(f, 1.0, delta_k, fo.lip, fo.iterations, fo.converged, 0));
   tr.status = fo.converged ? KG_S_CONVERGED : KG_S_MAX_ITERATIONS;
   return tr;
 }
@@ -1848,6 +1891,7 @@ static ModelTrace outer_loop(Fit& F, double lambda, const OuterCfg& oc) {
   }
   double J_cur = penalty_of(F.pen, F.alpha, pin[16], pin[17]);
   double f_cur = -(pin[0] / F.disp) / n + lambda * J_cur;
+  tr.initial_objective = f_cur;
   tr.final_objective = f_cur;
 
   const int n_vmax = elem_grid(F.n);
@@ -1929,7 +1973,7 @@ static ModelTrace outer_loop(Fit& F, double lambda, const OuterCfg& oc) {
     // Armijo (outer.cpp:118-143): trials in order, batches of kMaxTrials.
     bool accepted = false;
     double t_acc = 0.0, f_acc = 0.0;
-    int base = 0;
+    int base = 0, j_acc = -1;
     std::vector<double> lls(pin + 2, pin + 2 + nt), Js(nt);
     for (int j = 0; j < nt; ++j) Js[j] = penalty_of(F.pen, F.alpha, pin[16 + 2 + 2 * j], pin[16 + 3 + 2 * j]);
     std::vector<i64> terr(errs + 2, errs + 2 + nt);
@@ -1972,14 +2016,17 @@ static ModelTrace outer_loop(Fit& F, double lambda, const OuterCfg& oc) {
         t_acc = t;
         f_acc = f_trial;
         J_cur = Js[q];
+        j_acc = static_cast<int>(j);
         break;
       }
     }
     tr.outer += 1;
     if (!accepted) {
+      tr.recs.push_back(outer_rec(f_cur, 0.0, delta_k, fo.lip, fo.iterations, fo.converged, -1));
       tr.status = KG_S_LINE_SEARCH_FAILED;
       return tr;
     }
+    tr.recs.push_back(outer_rec(f_acc, t_acc, delta_k, fo.lip, fo.iterations, fo.converged, j_acc));
     ptheta_update(ctx->L(), F.p, t_acc, F.best.d(), F.theta.d());
     eta_combine(ctx->L(), F.n, t_acc, F.eta_t.d(), F.eta.d());
     tr.final_objective = f_acc;
@@ -2143,10 +2190,11 @@ static kg_path_result* fit_path(kg_ctx* ctx, const kg_design* D, const kg_obs* O
     wzz(ctx->L(), F->n, F->v.d(), F->zptr, F->part.d());  // sum v z^2
     reduce_cols(ctx->L(), F->part.d(), elem_grid(F->n), 1, 0, &static_cast<FistaCtl*>(F->ctl.p)->ss_const);
     ar_sum(ctx, &static_cast<FistaCtl*>(F->ctl.p)->ss_const, 1);
-    DBuf dl, p2, obj, its, stat;
+    DBuf dl, p2, obj, its, stat, dks;
     dl.alloc(sizeof(double) * nl);
-    p2.alloc(sizeof(double) * 4 * D->p[0][D->d - 1]);
+    p2.alloc(sizeof(double) * 5 * D->p[0][D->d - 1]);
     obj.alloc(sizeof(double) * nl);
+    dks.alloc(sizeof(double) * 2 * nl);
     its.alloc(sizeof(i64) * nl);
     stat.alloc(sizeof(int) * (nl + 2));
     KG_CUDA(cudaMemcpyAsync(dl.p, lambdas.data(), sizeof(double) * nl, cudaMemcpyHostToDevice, ctx->s));
@@ -2163,6 +2211,7 @@ static kg_path_result* fit_path(kg_ctx* ctx, const kg_design* D, const kg_obs* O
     P.part2 = p2.d();
     P.coefs = res->coefs.d();
     P.obj_out = obj.d();
+    P.dk_out = dks.d();
     P.iters_out = static_cast<i64*>(its.p);
     P.status_out = static_cast<int*>(stat.p) + 2;
     P.nmodels = static_cast<int*>(stat.p);
@@ -2174,10 +2223,13 @@ static kg_path_result* fit_path(kg_ctx* ctx, const kg_design* D, const kg_obs* O
     KG_CUDA(cudaEventRecord(ctx->ev[0], ctx->s));
     gauss_path(ctx->L(), P);
     KG_CUDA(cudaEventRecord(ctx->ev[1], ctx->s));
-    std::vector<double> ho(nl);
+    std::vector<double> ho(nl), hdk(2 * nl);
     std::vector<i64> hi(nl);
     std::vector<int> hs(nl + 2);
+    FistaCtl* hctl = reinterpret_cast<FistaCtl*>(ctx->pin() + PIN_CTL);
     KG_CUDA(cudaMemcpyAsync(ho.data(), obj.p, sizeof(double) * nl, cudaMemcpyDeviceToHost, ctx->s));
+    KG_CUDA(cudaMemcpyAsync(hdk.data(), dks.p, sizeof(double) * 2 * nl, cudaMemcpyDeviceToHost, ctx->s));
+    KG_CUDA(cudaMemcpyAsync(hctl, F->ctl.p, sizeof(FistaCtl), cudaMemcpyDeviceToHost, ctx->s));
     KG_CUDA(cudaMemcpyAsync(hi.data(), its.p, sizeof(i64) * nl, cudaMemcpyDeviceToHost, ctx->s));
     KG_CUDA(cudaMemcpyAsync(hs.data(), stat.p, sizeof(int) * (nl + 2), cudaMemcpyDeviceToHost, ctx->s));
     sync(ctx);
@@ -2203,9 +2255,11 @@ static kg_path_result* fit_path(kg_ctx* ctx, const kg_design* D, const kg_obs* O
     for (int t = 0; t < models; ++t) {
       res->lambdas.push_back(lambdas[t]);
       res->objectives.push_back(ho[t]);
+      res->initial_objectives.push_back(hdk[2 * t + 1]);
       res->outer_iters.push_back(1);
       res->inner_iters.push_back(hi[t]);
       res->status.push_back(hs[2 + t]);
+      res->traces.push_back({outer_rec(ho[t], 1.0, hdk[2 * t], hctl->lip, hi[t], hs[2 + t] == KG_S_CONVERGED, 0)});
     }
     return res.release();
   }
@@ -2221,6 +2275,8 @@ static kg_path_result* fit_path(kg_ctx* ctx, const kg_design* D, const kg_obs* O
                             ctx->s));
     res->lambdas.push_back(lambdas[t]);
     res->objectives.push_back(tr.final_objective);
+    res->initial_objectives.push_back(tr.initial_objective);
+    res->traces.push_back(std::move(tr.recs));
     res->outer_iters.push_back(tr.outer);
     res->inner_iters.push_back(tr.inner);
     res->status.push_back(tr.status);
@@ -2623,12 +2679,31 @@ kg_status kg_fit_path(kg_ctx* ctx, const kg_design* design, const kg_obs* obs, i
 int64_t kg_result_n_models(const kg_path_result* r) { return static_cast<int64_t>(r->lambdas.size()); }
 int kg_result_truncated(const kg_path_result* r) { return r->truncated ? 1 : 0; }
 double kg_result_lambda_max(const kg_path_result* r) { return r->lambda_max; }
-double kg_result_lambda(const kg_path_result* r, int64_t t) { return r->lambdas[t]; }
-double kg_result_objective(const kg_path_result* r, int64_t t) { return r->objectives[t]; }
-int64_t kg_result_outer_iters(const kg_path_result* r, int64_t t) { return r->outer_iters[t]; }
-int64_t kg_result_inner_iters(const kg_path_result* r, int64_t t) { return r->inner_iters[t]; }
-int kg_result_status(const kg_path_result* r, int64_t t) { return r->status[t]; }
+// Per-model accessors: an out-of-range t (or a NULL result) gives NaN / -1
+// instead of indexing past the vectors.
+static bool model_ok(const kg_path_result* r, int64_t t) {
+  return r && t >= 0 && t < static_cast<int64_t>(r->lambdas.size());
+}
+static constexpr double kNaN = std::numeric_limits<double>::quiet_NaN();
+double kg_result_lambda(const kg_path_result* r, int64_t t) { return model_ok(r, t) ? r->lambdas[t] : kNaN; }
+double kg_result_objective(const kg_path_result* r, int64_t t) { return model_ok(r, t) ? r->objectives[t] : kNaN; }
+double kg_result_initial_objective(const kg_path_result* r, int64_t t) {
+  return model_ok(r, t) ? r->initial_objectives[t] : kNaN;
+}
+int64_t kg_result_outer_iters(const kg_path_result* r, int64_t t) { return model_ok(r, t) ? r->outer_iters[t] : -1; }
+int64_t kg_result_inner_iters(const kg_path_result* r, int64_t t) { return model_ok(r, t) ? r->inner_iters[t] : -1; }
+int kg_result_status(const kg_path_result* r, int64_t t) { return model_ok(r, t) ? r->status[t] : -1; }
+int64_t kg_result_n_outer(const kg_path_result* r, int64_t t) {
+  return model_ok(r, t) ? static_cast<int64_t>(r->traces[t].size()) : -1;
+}
+kg_status kg_result_trace(const kg_path_result* r, int64_t t, kg_outer_record* out) {
+  if (!model_ok(r, t) || !out) return KG_EINVAL;
+  std::copy(r->traces[t].begin(), r->traces[t].end(), out);
+  return KG_OK;
+}
 int64_t kg_result_nonzero(const kg_path_result* r, int64_t t) {
+  if (!model_ok(r, t)) return -1;
+  if (cudaSetDevice(r->ctx->device) != cudaSuccess) return -1;
   std::vector<double> h(r->p);
   if (cudaMemcpy(h.data(), r->coefs.d() + r->p * t, sizeof(double) * r->p, cudaMemcpyDeviceToHost) != cudaSuccess)
     return -1;
@@ -2885,6 +2960,32 @@ kg_status kg_mse_heldout(kg_ctx* ctx, const kg_design* D, const kg_path_result* 
       if (h[m] < h[best]) best = m;  // first minimum (path.cpp:120)
     }
     *argmin = best;
+  });
+}
+
+kg_status kg_result_deviance(kg_ctx* ctx, const kg_design* D, const kg_obs* O, const kg_path_result* R, int family,
+                             double* out) {
+  return guarded(ctx, [&] {
+    set_device(ctx);
+    if (family < KG_GAUSSIAN || family > KG_GAMMA) throw Error(E_INVAL, "unknown family");
+    if (!R || !O || O->design != D) throw Error(E_INVAL, "deviance: observation was created for another design");
+    if (R->p != D->P) throw Error(E_INVAL, "deviance: result does not match the design");
+    const i64 models = static_cast<i64>(R->lambdas.size());
+    if (models == 0) return;
+    Tmp t;
+    double* de = t.get(D->N);
+    double *s0 = t.get(D->scratch), *s1 = t.get(D->scratch);
+    const int g = elem_grid(D->N);
+    double* part = t.get(static_cast<i64>(g));
+    double* dv = t.get(models);
+    for (i64 m = 0; m < models; ++m) {  // eta = H(theta_m) on the device, then the deviance terms
+      h_map_dev(ctx, D, R->coefs.d() + R->p * m, de, s0, s1);
+      deviance_pass(ctx->L(), D->N, family, O->y.d(), O->a.d(), de, part);
+      reduce_cols(ctx->L(), part, g, 1, 0, dv + m);
+    }
+    ar_sum(ctx, dv, static_cast<size_t>(models));  // sharded: summed over the slabs
+    KG_CUDA(cudaMemcpyAsync(out, dv, sizeof(double) * models, cudaMemcpyDeviceToHost, ctx->s));
+    sync(ctx);
   });
 }
 

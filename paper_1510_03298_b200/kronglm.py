@@ -276,6 +276,28 @@ class PathResult:
         self.outer_iters = [int(L.kg_result_outer_iters(h, t)) for t in range(self.n_models)]
         self.inner_iters = [int(L.kg_result_inner_iters(h, t)) for t in range(self.n_models)]
         self.status = [STATUS[L.kg_result_status(h, t)] for t in range(self.n_models)]
+        self.initial_objectives = [L.kg_result_initial_objective(h, t) for t in range(self.n_models)]
+        self.traces = [self._trace(L, t) for t in range(self.n_models)]
+
+    def _trace(self, L, t):
+        """OuterTrace records of model t (outer.hpp:26-47; FitPath::diagnostics, path.hpp:23)."""
+        k = int(L.kg_result_n_outer(self.h, t))
+        recs = (_lib.OuterRecord * max(k, 1))()
+        if k > 0 and L.kg_result_trace(self.h, t, recs) != 0:
+            raise RuntimeError("kg_result_trace failed")
+        return [{"objective": r.objective, "alpha": r.alpha, "delta_k": r.delta_k, "lipschitz": r.lipschitz,
+                 "inner_iterations": int(r.inner_iterations), "inner_converged": bool(r.inner_converged),
+                 "armijo_j": int(r.armijo_j)} for r in recs[:k]]
+
+    def deviance(self, obs: "Observation", family: str) -> list:
+        """Deviance of every model against ``obs`` (family.cpp conventions),
+        eta = H(theta_t) and the sum computed on the device."""
+        if family not in FAMILIES:
+            raise ValueError("unknown family: " + str(family))
+        out = np.zeros(max(self.n_models, 1))
+        D = self.design
+        D.ctx.check(_lib.load().kg_result_deviance(D.ctx.h, D.h, obs.h, self.h, FAMILIES[family], _ptr(out)))
+        return [float(v) for v in out[:self.n_models]]
 
     def coef(self, t) -> np.ndarray:
         out = np.zeros(self.design.p)
@@ -472,7 +494,7 @@ def fit_path(design, family, y, weights=None, penalty="lasso", alpha=0.0, n_lamb
     out = {"lambdas": list(res.lambdas), "objectives": list(res.objectives), "lambda_max": res.lambda_max,
            "truncated": res.truncated, "coefficients": [], "nonzero": [], "outer_iters": list(res.outer_iters),
            "converged": [s == "converged" for s in res.status], "inner_iters": list(res.inner_iters),
-           "status": list(res.status)}
+           "status": list(res.status), "traces": res.traces}
     for flat in res.coefs(out=buf):
         out["coefficients"].append(D.blocks(flat))
     out["nonzero"] = res.nonzeros()
