@@ -157,6 +157,13 @@ kg_status kg_lambda_max(kg_ctx* ctx, const kg_design* design, const kg_obs* obs,
 kg_status kg_fit_path(kg_ctx* ctx, const kg_design* design, const kg_obs* obs, int family, double dispersion,
                       int penalty, double alpha, const kg_path_cfg* cfg, const double* lambdas, int64_t n_lambdas,
                       kg_path_result** out);
+/* outer_solve (outer.hpp:56-60, outer.cpp:159-303) at one lambda from
+ * theta = 0 (the path's first warm start, path.cpp:63): the result holds one
+ * model with whatever status the solve ended in (converged, max_iterations,
+ * line_search_failed, inner_divergence) -- no first-model exception -- and
+ * its OuterTrace (kg_result_trace). */
+kg_status kg_outer_solve(kg_ctx* ctx, const kg_design* design, const kg_obs* obs, int family, double dispersion,
+                         int penalty, double alpha, const kg_path_cfg* cfg, double lambda, kg_path_result** out);
 int64_t kg_result_n_models(const kg_path_result* res);
 int kg_result_truncated(const kg_path_result* res);
 double kg_result_lambda_max(const kg_path_result* res);
@@ -254,8 +261,10 @@ kg_status kg_result_deviance(kg_ctx* ctx, const kg_design* design, const kg_obs*
  *   which = 0: the fused FISTA n-array pass (mode-1 H-last + weighted SS +
  *              V.* + G-first), the dominant kernel of every prox-grad step;
  *   which = 1: one banded mode contraction (the largest H-chain step).
- * avg_ms = mean device time per launch; bytes = algorithmic HBM bytes per
- * launch ("roofline"). */
+ * avg_ms = mean device time per launch, each launch bracketed by its own
+ * CUDA events after a 256 MB write that evicts L2 (so the inputs come from
+ * HBM, as inside a path step); bytes = algorithmic HBM bytes per launch
+ * ("roofline"). */
 kg_status kg_time_kernel(kg_ctx* ctx, const kg_design* design, const kg_obs* obs, int which, int reps,
                          double* avg_ms, double* bytes);
 /* Device time of the last whole-path kernel (k_gauss_path: one cooperative

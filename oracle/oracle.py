@@ -19,7 +19,7 @@ import threading
 import numpy as np
 
 _HERE = os.path.dirname(os.path.abspath(__file__))
-_LIB_PATH = os.path.join(_HERE, "liborc.so")
+_LIB_PATH = os.path.join(_HERE, os.environ.get("KRONGLM_ORACLE_LIB", "liborc.so"))
 _lib = None
 _lock = threading.Lock()
 

@@ -73,6 +73,7 @@ _SIGS = {
     "kg_rho": (C.c_int, [_vp, _i64, _pd, _i64, _pi, _pd, _pd]),
     "kg_lambda_max": (C.c_int, [_vp, _vp, _vp, C.c_int, _d, C.c_int, _d, _pd]),
     "kg_fit_path": (C.c_int, [_vp, _vp, _vp, C.c_int, _d, C.c_int, _d, _P(PathCfg), _pd, _i64, _P(_vp)]),
+    "kg_outer_solve": (C.c_int, [_vp, _vp, _vp, C.c_int, _d, C.c_int, _d, _P(PathCfg), _d, _P(_vp)]),
     "kg_result_n_models": (_i64, [_vp]),
     "kg_result_truncated": (C.c_int, [_vp]),
     "kg_result_lambda_max": (_d, [_vp]),

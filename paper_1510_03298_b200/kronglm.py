@@ -356,6 +356,28 @@ def fit_path_resident(design: Design, obs: Observation, family="gaussian", penal
     return PathResult(design, h)
 
 
+def outer_solve(design, family, y, lam, weights=None, penalty="lasso", alpha=0.0, dispersion=1.0, **cfg):
+    """kronglm::outer_solve (outer.hpp:56-60) at one lambda from theta = 0.
+    Returns {"coef", "coef_flat", "status", "iterations" (OuterTrace records),
+    "initial_objective", "final_objective"} like the C++ OuterResult."""
+    if family not in FAMILIES:
+        raise ValueError("unknown family: " + str(family))
+    if penalty not in PENALTIES:
+        raise ValueError("unknown penalty: " + str(penalty))
+    D = _design(design)
+    obs = Observation(D, y, weights)
+    c = make_cfg(**cfg)
+    h = C.c_void_p()
+    D.ctx.check(_lib.load().kg_outer_solve(D.ctx.h, D.h, obs.h, FAMILIES[family], float(dispersion),
+                                           PENALTIES[penalty], float(alpha), C.byref(c), float(lam), C.byref(h)))
+    res = PathResult(D, h)
+    flat = res.coef(0)
+    out = {"coef": D.blocks(flat), "coef_flat": flat, "status": res.status[0], "iterations": res.traces[0],
+           "initial_objective": res.initial_objectives[0], "final_objective": res.objectives[0]}
+    res.close()
+    return out
+
+
 # ----------------------------------------------- reference module surface
 def linear_index(multi_index, dims):
     """Column-major 1-based linear position (array.cpp:22-36)."""

@@ -55,3 +55,29 @@ def test_host_builders_match_oracle():
         K.linear_index([0, 1], [2, 3])
     with pytest.raises(ValueError):
         K.bspline_design([0.0, 0.0, 1.0], 4, 5)
+
+
+def test_import_kronglm_exposes_the_reference_module_surface():
+    """`import kronglm` works like the pybind11 module (kronglm_py.cpp:115-249):
+    every in-scope function of the reference module is there (dense_materialize
+    and simulate are the test oracle and the data generator, out of scope)."""
+    import kronglm
+    for name in ("linear_index", "rho", "h_map", "g_map", "lambda_max", "fit_path", "predict", "bspline_design",
+                 "default_basis_count", "outer_solve", "mse_heldout"):
+        assert callable(getattr(kronglm, name)), name
+    assert kronglm.fit_path is K.fit_path
+    assert issubclass(kronglm.EvalError, RuntimeError)
+
+
+def test_result_accessors_reject_out_of_range_models():
+    """kg_result_* accessors on a NULL result / bad index return NaN or -1
+    instead of indexing past the vectors (no device work)."""
+    L = _lib.load()
+    assert np.isnan(L.kg_result_lambda(None, 0))
+    assert np.isnan(L.kg_result_objective(None, 3))
+    assert L.kg_result_inner_iters(None, 0) == -1
+    assert L.kg_result_outer_iters(None, -1) == -1
+    assert L.kg_result_status(None, 0) == -1
+    assert L.kg_result_nonzero(None, 0) == -1
+    assert L.kg_result_n_outer(None, 0) == -1
+    assert L.kg_result_trace(None, 0, None) == _lib.KG_EINVAL
