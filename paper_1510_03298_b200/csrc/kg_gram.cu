@@ -1582,219 +1582,6 @@ void fista_persist(const Launch& L, const PersistArgs& P) {
   launched(L);
 }
 
-namespace {
-
-// one banded mode contraction of an (a, K, b) array into (a, M, b) as a
-// grid-stride loop (summation ascending over the band, as k_contract_rs);
-// 32-bit indices with multiply-high division (sizes checked on the host)
-template <int MB>
-__device__ __forceinline__ double band_dot(const double* __restrict__ c, const double* __restrict__ src, uint32_t a,
-                                           int len) {
-  double s = 0.0;
-#pragma unroll
-  for (int t = 0; t < MB; ++t)
-    if (t < len) s = fma(__ldg(c + t), __ldcg(src + a * t), s);
-  return s;
-}
-
-template <int MB>
-__device__ __forceinline__ void band_mode_t(const double* __restrict__ in, double* __restrict__ out, uint32_t a,
-                                            uint32_t K, uint32_t M, uint32_t b, const FastDiv& fa, const FastDiv& fm,
-                                            const BandOp& op, uint32_t gtid, uint32_t gsz) {
-  const uint32_t total = a * M * b;
-  for (uint32_t o0 = gtid; o0 < total; o0 += 2 * gsz) {  // two outputs in flight per thread
-    const uint32_t o1 = o0 + gsz < total ? o0 + gsz : o0;
-    const uint32_t r0 = fa.div(o0), al0 = o0 - r0 * a, be0 = fm.div(r0), m0 = r0 - be0 * M;
-    const uint32_t r1 = fa.div(o1), al1 = o1 - r1 * a, be1 = fm.div(r1), m1 = r1 - be1 * M;
-    const double* s0 = in + al0 + a * (__ldg(op.lo + m0) + K * be0);
-    const double* s1 = in + al1 + a * (__ldg(op.lo + m1) + K * be1);
-    const double v0 = band_dot<MB>(op.coef + __ldg(op.off + m0), s0, a, __ldg(op.len + m0));
-    const double v1 = band_dot<MB>(op.coef + __ldg(op.off + m1), s1, a, __ldg(op.len + m1));
-    out[o0] = v0;
-    if (o1 != o0) out[o1] = v1;
-  }
-}
-
-// one banded mode contraction of an (a, K, b) array into (a, M, b) as a
-// grid-stride loop (summation ascending over the band, as k_contract_rs);
-// 32-bit indices with multiply-high division (sizes checked on the host)
-__device__ __forceinline__ void band_mode(const double* __restrict__ in, double* __restrict__ out, uint32_t a,
-                                          uint32_t K, uint32_t M, uint32_t b, const FastDiv& fa, const FastDiv& fm,
-                                          const BandOp& op, uint32_t gtid, uint32_t gsz) {
-  if (op.maxlen <= 4)
-    band_mode_t<4>(in, out, a, K, M, b, fa, fm, op, gtid, gsz);
-  else if (op.maxlen <= 16)
-    band_mode_t<16>(in, out, a, K, M, b, fa, fm, op, gtid, gsz);
-  else if (op.maxlen <= 32)
-    band_mode_t<32>(in, out, a, K, M, b, fa, fm, op, gtid, gsz);
-  else
-    band_mode_t<64>(in, out, a, K, M, b, fa, fm, op, gtid, gsz);
-}
-
-}  // namespace
-
-template <int BS>
-__global__ void __launch_bounds__(BS) k_nspace_persist(NPersistArgs A) {
-  extern __shared__ __align__(16) double smw[];  // BS / 32 warps x n1 doubles (w of one fibre)
-  __shared__ double red[3 * 32 + 3];
-  __shared__ FistaCtl cs;
-  const int s = blockIdx.x;
-  const unsigned nb = gridDim.x;
-  const i64 gtid = static_cast<i64>(s) * BS + threadIdx.x, gsz = static_cast<i64>(nb) * BS;
-  const uint32_t ug = static_cast<uint32_t>(gtid), us = static_cast<uint32_t>(gsz);
-  const int warp = threadIdx.x >> 5, lane = threadIdx.x & 31;
-  const i64 n1 = A.n1, n2 = A.n2, n3 = A.n3, p1 = A.p1, p2 = A.p2, p3 = A.p3;
-  const i64 p = p1 * p2 * p3, m1 = n2 * n3;  // coefficients, mode-1 fibres
-  const FastDiv f12(static_cast<uint32_t>(p1 * p2)), fn3(static_cast<uint32_t>(n3)), f1(static_cast<uint32_t>(p1)),
-      fn2(static_cast<uint32_t>(n2)), fp2(static_cast<uint32_t>(p2)), fp3(static_cast<uint32_t>(p3));
-  if (threadIdx.x == 0) cs = *A.ctl;
-  __syncthreads();
-  const double n = cs.n, w = cs.sscale, c0 = cs.ss_const, lam = cs.lambda;
-  const bool tim = A.dbg && s == 0 && threadIdx.x == 0;
-  long long ph[8] = {0, 0, 0, 0, 0, 0, 0, 0}, nph = 0, t0c = 0;
-  auto mark = [&](int i) {
-    if (tim) {
-      const long long c = clock64();
-      if (i > 0) ph[i - 1] += c - t0c;
-      t0c = c;
-    }
-  };
-  while (!cs.done) {
-    mark(0);
-    // P0: update (k_fista_update; a pending best copy first)
-    const double omega = cs.omega, delta = cs.delta, gamma = __dmul_rn(delta, lam);
-    const int copy_best = cs.copy_best;
-    double l1 = 0.0, l2 = 0.0, bx = 0.0;
-    for (i64 i = gtid; i < p; i += gsz) {
-      const double xi = A.x[i], xpi = A.xp[i], sxi = A.Sx[i], sxpi = A.Sxp[i];
-      if (copy_best) {
-        A.best[i] = xi;
-        A.Sbest[i] = sxi;
-      }
-      const double yi = xi + omega * (xi - xpi);
-      const double syi = sxi + omega * (sxi - sxpi);
-      const double g = (w * syi - A.b[i]) / n;
-      double ci = __dsub_rn(yi, __dmul_rn(delta, g));
-      if (lam > 0.0) ci = prox1(cs.pen, cs.alpha, gamma, ci);
-      A.xp[i] = xi;
-      A.x[i] = ci;
-      A.Sxp[i] = sxi;
-      l1 += fabs(ci);
-      l2 = fma(ci, ci, l2);
-      bx = fma(A.b[i], ci, bx);
-    }
-    double r[3];
-    cta_sum3<BS>(l1, l2, bx, red, r);
-    if (threadIdx.x == 0) {
-      A.part[4 * s] = r[0];
-      A.part[4 * s + 1] = r[1];
-      A.part[4 * s + 2] = r[2];
-    }
-    mark(1);
-    grid_sync(A.bar, nb);
-    mark(2);
-    // P1, P2: H modes 3 and 2 (x -> A1 -> P)
-    band_mode(A.x, A.A1, p1 * p2, p3, n3, 1, f12, fn3, A.H3, ug, us);
-    grid_sync(A.bar, nb);
-    mark(3);
-    band_mode(A.A1, A.P, p1, p2, n2, n3, f1, fn2, A.H2, ug, us);
-    grid_sync(A.bar, nb);
-    mark(4);
-    // P3: mode 1 on tiles of TF fibres per CTA: eta = X1 P_f, w = v eta (shared), Q_f = X1^T w
-    double ss = 0.0;
-    constexpr int TF = 32;
-    for (i64 f0 = static_cast<i64>(s) * TF; f0 < m1; f0 += static_cast<i64>(nb) * TF) {
-      const int tf = static_cast<int>(m1 - f0 < TF ? m1 - f0 : TF);
-      for (int e = threadIdx.x; e < n1 * tf; e += BS) {  // rows fastest: coalesced v
-        const int f = e / static_cast<int>(n1), i = e - f * static_cast<int>(n1);
-        const double* Pf = A.P + p1 * (f0 + f);
-        const int lo = __ldg(A.H1.lo + i), len = __ldg(A.H1.len + i);
-        const double eta = band_dot<4>(A.H1.coef + __ldg(A.H1.off + i), Pf + lo, 1, len);
-        const double wi = __ldcg(A.v + n1 * (f0 + f) + i) * eta;
-        ss = fma(wi, eta, ss);
-        smw[f * n1 + i] = wi;
-      }
-      __syncthreads();
-      for (int e = threadIdx.x; e < p1 * tf; e += BS) {
-        const int f = e / static_cast<int>(p1), kk = e - f * static_cast<int>(p1);
-        const int lo = __ldg(A.G1.lo + kk), len = __ldg(A.G1.len + kk);
-        const double* c = A.G1.coef + __ldg(A.G1.off + kk);
-        const double* wf = smw + f * n1 + lo;
-        double q = 0.0;
-        for (int t = 0; t < len; ++t) q = fma(__ldg(c + t), wf[t], q);
-        A.Q[p1 * (f0 + f) + kk] = q;
-      }
-      __syncthreads();
-    }
-    const double sse = cta_sum<BS>(ss, red);
-    if (threadIdx.x == 0) A.part[4 * s + 3] = sse;
-    grid_sync(A.bar, nb);
-    mark(5);
-    // monitor of this step (warp 0, fixed order) while the other warps start G mode 2
-    if (warp == 0) {
-      double a0 = 0.0, a1 = 0.0, a2 = 0.0, a3 = 0.0;
-      for (int q = lane; q < static_cast<int>(nb); q += 32) {
-        a0 += __ldcg(A.part + 4 * q);
-        a1 += __ldcg(A.part + 4 * q + 1);
-        a2 += __ldcg(A.part + 4 * q + 2);
-        a3 += __ldcg(A.part + 4 * q + 3);
-      }
-      a0 = warp_sum(a0);
-      a1 = warp_sum(a1);
-      a2 = warp_sum(a2);
-      a3 = warp_sum(a3);
-      if (lane == 0) {
-        const double g = 0.5 * ((a3 + (-2.0 * a2)) + c0) / n + lam * penalty_of(cs.pen, cs.alpha, a0, a1);
-        ctl_step(cs, g);
-      }
-    }
-    // P4, P5: G modes 2 and 3 (Q -> B1 -> S x)
-    band_mode(A.Q, A.B1, p1, n2, p2, n3, f1, fp2, A.G2, ug, us);
-    grid_sync(A.bar, nb);  // also publishes cs (thread 0 wrote it before this CTA barrier)
-    mark(6);
-    band_mode(A.B1, A.Sx, p1 * p2, n3, p3, 1, f12, fp3, A.G3, ug, us);
-    grid_sync(A.bar, nb);
-    mark(7);
-    ++nph;
-  }
-  if (tim && nph)
-    printf("k_nspace_persist CTA0 cycles/step: update %lld bar %lld H3 %lld H2 %lld mode1 %lld G2+monitor %lld G3 %lld (%lld steps)\n",
-           ph[0] / nph, ph[1] / nph, ph[2] / nph, ph[3] / nph, ph[4] / nph, ph[5] / nph, ph[6] / nph, nph);
-  if (cs.copy_best) {  // fista_finalize: the last monitor's pending copy
-    for (i64 i = gtid; i < p; i += gsz) {
-      A.best[i] = A.x[i];
-      A.Sbest[i] = A.Sx[i];
-    }
-  }
-  if (s == 0 && threadIdx.x == 0) {
-    cs.copy_best = 0;
-    *A.ctl = cs;
-  }
-}
-
-bool npersist_ok(const NPersistArgs& A, int* grid) {
-  const size_t sm = sizeof(double) * 32 * static_cast<size_t>(A.n1);  // a tile of 32 fibres of w
-  if (sm > 48 * 1024) return false;
-  const i64 big = std::max(static_cast<i64>(A.p1) * A.n2 * A.n3, static_cast<i64>(A.p1) * A.p2 * A.n3);
-  if (big >= (i64(1) << 31)) return false;  // 32-bit index arithmetic
-  int per_sm = 0, dev = 0, nsm = 0;
-  KG_CUDA(cudaOccupancyMaxActiveBlocksPerMultiprocessor(&per_sm, k_nspace_persist<256>, 256, sm));
-  KG_CUDA(cudaGetDevice(&dev));
-  KG_CUDA(cudaDeviceGetAttribute(&nsm, cudaDevAttrMultiProcessorCount, dev));
-  if (per_sm < 1) return false;
-  *grid = nsm * std::min(per_sm, 2);
-  return *grid <= 32 * 40;  // the monitor gathers up to ~1280 partials per lane pass
-}
-
-void npersist(const Launch& L, const NPersistArgs& A, int grid) {
-  const size_t sm = sizeof(double) * 32 * static_cast<size_t>(A.n1);
-  NPersistArgs args = A;
-  void* kargs[] = {&args};
-  KG_CUDA(cudaLaunchCooperativeKernel(reinterpret_cast<const void*>(k_nspace_persist<256>),
-                                      dim3(static_cast<unsigned>(grid)), dim3(256), kargs, sm, L.s));
-  launched(L);
-}
-
 // Gaussian constant-weight bookkeeping in p-space (outer.cpp:197-231 via
 // eta = X theta): per-CTA partials of
 //   0 <th,b>  1 <th,S th>  2 <bt,b>  3 <bt,S bt>  4 <b - w S th, bt - th>

@@ -185,22 +185,6 @@ bool fused_fast_ok(const FusedArgs& f, int variant);
 void contract_tiled(const Launch& L, const double* A, double* out, i64 a, i64 K, i64 M, i64 b, const BandOp& op,
                     bool accumulate);
 
-// Modes 1 and 2 of one prox-grad step fused per last-mode slab (kg_slab.cu):
-// B1[:, :, k3] = X1^T V X1-and-X2 contractions of A1[:, :, k3] (d = 3),
-// partial[cta] = sum v eta^2 of the CTA's cells (expanded objective).
-struct SlabArgs {
-  int n1 = 0, n2 = 0, p1 = 0, p2 = 0;
-  i64 n3 = 0;                   // slabs (local extent of the last mode)
-  BandOp H1, G1, H2, G2;        // X1 rows, X1^T rows, X2 rows, X2^T rows
-  const double* A1 = nullptr;   // p1 x p2 x n3
-  double* B1 = nullptr;         // p1 x p2 x n3 (out)
-  const double* v = nullptr;    // n1 x n2 x n3
-  double* partial = nullptr;    // one per CTA
-  int CG = 0;                   // column groups of 32 per tile (set by the launcher)
-};
-bool slab_ok(const SlabArgs& a);
-int slab_grid(const SlabArgs& a);
-void slab12(const Launch& L, const SlabArgs& a);
 
 // H-last (+ reductions) over mode 1.  If P is null, eta_new is an input
 // (already computed by a full H chain) and only the reductions run.
@@ -355,24 +339,6 @@ void count_nonzero(const Launch& L, const double* coefs, i64 p, i64 models, unsi
 bool gauss_path_ok(const GramStepArgs& A);
 void gauss_path(const Launch& L, const PersistArgs& P);
 
-// Persistent cooperative n-space FISTA loop (route 0, d = 3, c = 1, nu = 1):
-// every phase of a step (update, H mode 3, H mode 2, fused mode-1 pass with
-// v, G mode 2, G mode 3) as a grid-stride loop between grid barriers, the
-// monitor replicated in every CTA.  For problems whose arrays sit in L2 (C3).
-struct NPersistArgs {
-  FistaCtl* ctl = nullptr;     // initialised (k_fista_init); state written back at exit
-  int n1 = 0, n2 = 0, n3 = 0, p1 = 0, p2 = 0, p3 = 0;
-  BandOp H1, G1, H2, G2, H3, G3;  // rows of X_j (H) and of X_j^T (G)
-  double *x = nullptr, *xp = nullptr, *Sx = nullptr, *Sxp = nullptr, *best = nullptr, *Sbest = nullptr;
-  const double* b = nullptr;   // X^T (v z)
-  const double* v = nullptr;   // n-array weights
-  double *A1 = nullptr, *P = nullptr, *Q = nullptr, *B1 = nullptr;  // p1p2n3, p1n2n3, p1n2n3, p1p2n3
-  double* part = nullptr;      // 4 per CTA: l1, l2, <b, x>, sum v eta^2
-  unsigned* bar = nullptr;     // grid barrier {count, generation}
-  int dbg = 0;                 // KG_NP_DBG=1: phase clocks of CTA 0
-};
-bool npersist_ok(const NPersistArgs& A, int* grid);
-void npersist(const Launch& L, const NPersistArgs& A, int grid);
 int gauss_dots(const Launch& L, i64 p, double w, const double* th, const double* Sth, const double* bt,
                const double* Sbt, const double* b, double* part);
 

@@ -819,14 +819,10 @@ struct Fit {
   bool tensor = false;
   double lipfac_t = 0.0;
   DBuf bt_y, bt_g, bt_c, bt_sc, bt_part;  // nu = 0: y, grad, candidate, S(candidate), partials
-  DBuf nppart, npbar;                     // persistent n-space loop (k_nspace_persist)
   std::vector<BandOp> wg;             // [(m * c + r) * d + j]
   std::vector<std::unique_ptr<DBuf>> wgcoef;
   DBuf tS, tf, text, tdense;
   std::vector<std::unique_ptr<SpectralJob>> tjobs;  // power iterations of the weighted Grams (c = 1)
-  // d = 3, banded: modes 1 and 2 fused per last-mode slab (kg_slab.cu); opt-in with KG_SLAB=1
-  // (experimental: parity-tested, slower than the fused-pass route so far)
-  bool slab = false;
   DBuf bxpart;
   double wconst = 1.0;     // the constant weight (route 1)
   bool c0_valid = false;   // F.scal[48] holds sum v z^2 for the current (v, z)
@@ -849,20 +845,6 @@ struct Fit {
 
 static FusedArgs fused_args(const Fit& F);
 
-static SlabArgs slab_args(const Fit& F) {
-  const kg_design& D = *F.D;
-  SlabArgs a;
-  a.n1 = static_cast<int>(D.n[0]);
-  a.n2 = static_cast<int>(D.n[1]);
-  a.p1 = static_cast<int>(D.p[0][0]);
-  a.p2 = static_cast<int>(D.p[0][1]);
-  a.n3 = D.n[2];
-  a.H1 = D.f[0][0]->dev.H;
-  a.G1 = D.f[0][0]->dev.G;
-  a.H2 = D.f[0][1]->dev.H;
-  a.G2 = D.f[0][1]->dev.G;
-  return a;
-}
 
 static void alloc_fit(Fit& F) {
   ensure_spectral(F.D);
@@ -889,15 +871,7 @@ static void alloc_fit(Fit& F) {
   F.Jpart.alloc(sizeof(double) * 2 * pgrid(F.p));
   F.bxpart.alloc(sizeof(double) * pgrid(F.p));
   F.expand = false;
-  F.slab = false;
-  if (D.fused && std::getenv("KG_ROUTE0_DIRECT") == nullptr) {
-    FusedArgs a = fused_args(F);
-    F.expand = fused_fast_ok(a, FV_FISTA_EXP);
-    if (D.d == 3 && std::getenv("KG_SLAB") != nullptr && std::getenv("KG_SLAB")[0] == '1') {  // experimental
-      F.slab = slab_ok(slab_args(F));
-      if (F.slab) F.expand = true;
-    }
-  }
+  if (D.fused && std::getenv("KG_ROUTE0_DIRECT") == nullptr) F.expand = fused_fast_ok(fused_args(F), FV_FISTA_EXP);
   F.tpart.alloc(sizeof(double) * 2 * (1 + kMaxTrials) * pgrid(F.p));
   F.scal.alloc(sizeof(double) * 64);
   F.errs.alloc(sizeof(i64) * 16);
@@ -972,18 +946,6 @@ static int run_fused(kg_ctx* ctx, int variant, const FusedArgs& a) {
 static int xwx_pass_local(Fit& F, const double* x, double* Sx) {
   const kg_design& D = *F.D;
   kg_ctx* ctx = F.ctx;
-  if (F.slab) {  // A1 = x x_3 X3 -> slab kernel (modes 1, 2, v) -> S x = B1 x_3 X3^T
-    const i64 pp = D.p[0][0] * D.p[0][1], p3 = D.p[0][2], n3 = D.n[2];
-    contract(ctx->L(), x, F.P.d(), pp, p3, n3, 1, D.f[0][2]->dev.H, false);
-    SlabArgs a = slab_args(F);
-    a.A1 = F.P.d();
-    a.B1 = F.Q.d();
-    a.v = F.v.d();
-    a.partial = F.part.d();
-    slab12(ctx->L(), a);
-    contract(ctx->L(), F.Q.d(), Sx, pp, n3, p3, 1, D.f[0][2]->dev.G, false);
-    return slab_grid(a);
-  }
   if (D.fused) {
     const double* P = x;
     if (D.d > 1) {
@@ -1422,54 +1384,7 @@ static void fista_enqueue(Fit& F, double lambda, const InnerCfg& ic, const doubl
     fista_init(ctx->L(), static_cast<FistaCtl*>(F.ctl.p), F.part.d(), n_ss, F.Jpart.d(), pgrid(F.p), vmax_part,
                n_vmax, 0, ex ? F.bxpart.d() : nullptr, pgrid(F.p));
   }
-  // small d = 3 n-space problems: the whole loop in one cooperative launch (experimental)
-  const kg_design& Dd = *F.D;
-  // opt-in (KG_NPERSIST=1): parity-tested, slower than the graph route so far
-  const char* npe = std::getenv("KG_NPERSIST");
-  const bool np_on = npe != nullptr && npe[0] == '1';
-  int np_grid = 0;
-  NPersistArgs NA;
-  const bool np = np_on && ic.max_iters >= 1 && F.route == 0 && F.expand && !F.slab && Dd.c == 1 && Dd.d == 3 &&
-                  !(ic.nu > 0.0 && ic.nu < 1.0) && !sharded(ctx) && !host_loop_mode() && F.n <= (i64(8) << 20);
-  if (np) {
-    NA.n1 = static_cast<int>(Dd.n[0]);
-    NA.n2 = static_cast<int>(Dd.n[1]);
-    NA.n3 = static_cast<int>(Dd.n[2]);
-    NA.p1 = static_cast<int>(Dd.p[0][0]);
-    NA.p2 = static_cast<int>(Dd.p[0][1]);
-    NA.p3 = static_cast<int>(Dd.p[0][2]);
-  }
-  if (np && npersist_ok(NA, &np_grid)) {
-    NA.ctl = static_cast<FistaCtl*>(F.ctl.p);
-    NA.H1 = Dd.f[0][0]->dev.H;
-    NA.G1 = Dd.f[0][0]->dev.G;
-    NA.H2 = Dd.f[0][1]->dev.H;
-    NA.G2 = Dd.f[0][1]->dev.G;
-    NA.H3 = Dd.f[0][2]->dev.H;
-    NA.G3 = Dd.f[0][2]->dev.G;
-    NA.x = F.x.d();
-    NA.xp = F.xp.d();
-    NA.Sx = F.Sx.d();
-    NA.Sxp = F.Sxp.d();
-    NA.best = F.best.d();
-    NA.Sbest = F.Sbest.d();
-    NA.b = F.b.d();
-    NA.v = F.v.d();
-    NA.A1 = F.s0.d();
-    NA.P = F.P.d();
-    NA.Q = F.Q.d();
-    NA.B1 = F.s1.d();
-    F.nppart.alloc(sizeof(double) * 4 * np_grid);
-    NA.part = F.nppart.d();
-    if (!F.npbar.p) {
-      F.npbar.alloc(sizeof(unsigned) * 4);
-      KG_CUDA(cudaMemsetAsync(F.npbar.p, 0, sizeof(unsigned) * 4, ctx->s));
-    }
-    NA.bar = static_cast<unsigned*>(F.npbar.p);
-    if (const char* e = std::getenv("KG_NP_DBG")) NA.dbg = std::atoi(e);
-    npersist(ctx->L(), NA, np_grid);
-    F.kernels_per_iter[F.route] = 0;  // one launch for the whole loop
-  } else if (ic.max_iters >= 1) {
+  if (ic.max_iters >= 1) {
     // a sharded n-space loop is driven from the host: its all-reduces stay out of graph capture
     if (host_loop_mode() || (sharded(ctx) && F.route == 0)) {
       const FistaCtl* hc = reinterpret_cast<const FistaCtl*>(ctx->pin() + PIN_CTL);
@@ -3048,15 +2963,6 @@ kg_status kg_time_kernel(kg_ctx* ctx, const kg_design* D, const kg_obs* O, int w
       launch = [&, a, var] { run_fused(ctx, var, a); };
       // P (p1 x m) read, v (and z unless expanded) read, Q (p1 x m) written
       b = 8.0 * ((F.expand ? 1.0 : 2.0) * static_cast<double>(F.n) + 2.0 * static_cast<double>(a.p1 * a.m));
-      if (F.slab && which == 0) {  // the slab kernel: v read, A1 read, B1 written
-        SlabArgs sa = slab_args(F);
-        sa.A1 = F.P.d();
-        sa.B1 = F.Q.d();
-        sa.v = F.v.d();
-        sa.partial = F.part.d();
-        launch = [&, sa] { slab12(ctx->L(), sa); };
-        b = 8.0 * (static_cast<double>(F.n) + 2.0 * static_cast<double>(sa.p1) * sa.p2 * static_cast<double>(sa.n3));
-      }
     } else if (which == 5) {
       // G-chain step of mode 1 (after the fused mode-0 pass): (p0, n1, rest) -> (p0, p1, rest)
       if (D->d < 2) throw Error(E_INVAL, "kg_time_kernel: the G-chain step needs d >= 2");

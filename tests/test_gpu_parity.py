@@ -376,38 +376,6 @@ def _fused_pass_bytes(D, obs):
     return b.value
 
 
-def test_slab_route_matches_oracle(monkeypatch):
-    """d = 3 n-space route through the slab kernel (modes 1 and 2 fused per
-    last-mode slab, expanded objective): Poisson path and a non-constant-weight
-    Gaussian path against the oracle, and against the unfused kernels."""
-    rng = np.random.default_rng(91)
-    n, p = (64, 24, 20), (20, 8, 6)
-    design = bspline_design(n, p)
-    B = np.zeros(p)
-    m = rng.random(p) < 0.15
-    B[m] = rng.standard_normal(m.sum())
-    eta = configs.tensor_h(design[0], B)
-    y = rng.poisson(np.exp(np.log(30.0) / eta.max() * eta)).astype(float)
-    monkeypatch.setenv("KG_SLAB", "1")  # opt-in route
-    D = K.Design(design)
-    obs = K.Observation(D, y)
-    N = int(np.prod(n))
-    assert _fused_pass_bytes(D, obs) == 8.0 * (N + 2 * p[0] * p[1] * n[2])  # the slab kernel is in use
-    kw = dict(n_lambda=10, lambda_min_ratio=1e-3)
-    got = K.fit_path(design, "poisson", y, **kw)
-    compare_paths(got, O.fit_path(design, "poisson", y, **kw))
-    monkeypatch.delenv("KG_SLAB")
-    ref = K.fit_path(design, "poisson", y, **kw)  # default route
-    monkeypatch.setenv("KG_SLAB", "1")
-    compare_paths(got, ref)
-    # Gaussian, weights not all equal: the n-space route with v = a
-    yg = eta + rng.normal(0, 0.3, n)
-    w = np.asfortranarray(rng.uniform(0.5, 2.0, n))
-    kw = dict(n_lambda=8, lambda_min_ratio=1e-3)
-    compare_paths(K.fit_path(design, "gaussian", yg, weights=w, **kw),
-                  O.fit_path(design, "gaussian", yg, weights=w, **kw))
-
-
 def test_sharded_context_world1_nccl_matches_unsharded():
     """kg_ctx_create_sharded with a real one-rank NCCL communicator: every
     cross-slab all-reduce runs (identity on one rank) and the sharded n-space
@@ -517,30 +485,3 @@ def test_tensor_weights_match_oracle(case):
         fam = "poisson"
     kw = dict(n_lambda=6, lambda_min_ratio=1e-2, iwls="tensor")
     compare_paths(K.fit_path(design, fam, y, **kw), O.fit_path(design, fam, y, **kw))
-
-
-def test_persistent_nspace_loop_matches_oracle(monkeypatch):
-    """Opt-in cooperative n-space FISTA loop (k_nspace_persist, KG_NPERSIST=1):
-    a Poisson d = 3 path through it matches the oracle."""
-    rng = np.random.default_rng(5)
-    design = bspline_design((24, 20, 30), (8, 6, 9))
-    B = np.zeros((8, 6, 9))
-    m = rng.random(B.shape) < 0.15
-    B[m] = rng.standard_normal(m.sum())
-    eta = configs.tensor_h(design[0], B)
-    y = rng.poisson(np.exp(np.log(20.0) / eta.max() * eta)).astype(float)
-    kw = dict(n_lambda=8, lambda_min_ratio=1e-3)
-    ctx = K.Context(0)
-    D = K.Design(design, ctx)
-    obs = K.Observation(D, y)
-    ctx.reset_launches()
-    K.fit_path_resident(D, obs, "poisson", **kw)
-    graph_launches = ctx.launches
-    monkeypatch.setenv("KG_NPERSIST", "1")
-    ctx.reset_launches()
-    res = K.fit_path_resident(D, obs, "poisson", **kw)
-    assert ctx.launches < graph_launches / 2  # one launch per inner solve, not one per iteration
-    got = {"lambdas": res.lambdas, "objectives": res.objectives, "truncated": res.truncated,
-           "coefficients": [D.blocks(c) for c in res.coefs()], "outer_iters": res.outer_iters,
-           "inner_iters": res.inner_iters}
-    compare_paths(got, O.fit_path(design, "poisson", y, **kw))
