@@ -787,6 +787,7 @@ __global__ void __launch_bounds__(NT) k_fista_update(const FistaCtl* __restrict_
                                                      double* best, double* Sbest, double* Jpart,
                                                      double* bxpart) {
   __shared__ double red[32];
+  if (ctl->done) return;  // batched host loops (sharded contexts) enqueue steps past the stop
   const double omega = ctl->omega, delta = ctl->delta, lambda = ctl->lambda, n = ctl->n, sscale = ctl->sscale;
   const int copy_best = ctl->copy_best, restart = ctl->restart;
   const double gamma = __dmul_rn(delta, lambda);
@@ -1294,6 +1295,40 @@ __device__ __forceinline__ double penalty_of(int pen, double alpha, double l1, d
   return l1 + alpha * l2;
 }
 
+// The four sums the monitor needs -- sum v eta^2 (or sum v (eta - z)^2), the
+// l1 and squared-l2 parts of J and <b, x> -- in one pass: every thread reads
+// its rows of all four columns, then four fixed shuffle trees and one
+// fixed-order pass over the warps (deterministic, two barriers).
+__device__ void cta_sums4(const double* ss_part, int n_ss, const double* J_part, int n_J, const double* bx_part,
+                          int n_bx, double* sh, double out[4]) {
+  double a[4] = {0.0, 0.0, 0.0, 0.0};
+  for (int r = threadIdx.x; r < n_ss; r += CT) a[0] += ss_part[r];
+  for (int r = threadIdx.x; r < n_J; r += CT) {
+    a[1] += J_part[2 * r];
+    a[2] += J_part[2 * r + 1];
+  }
+  if (bx_part)
+    for (int r = threadIdx.x; r < n_bx; r += CT) a[3] += bx_part[r];
+  const int w = threadIdx.x >> 5, l = threadIdx.x & 31;
+#pragma unroll
+  for (int k = 0; k < 4; ++k) a[k] = warp_sum(a[k]);
+  if (l == 0)
+#pragma unroll
+    for (int k = 0; k < 4; ++k) sh[4 * w + k] = a[k];
+  __syncthreads();
+  if (w == 0) {
+#pragma unroll
+    for (int k = 0; k < 4; ++k) {
+      double v = sh[4 * l + k];
+      v = warp_sum(v);
+      if (l == 0) sh[128 + k] = v;
+    }
+  }
+  __syncthreads();
+#pragma unroll
+  for (int k = 0; k < 4; ++k) out[k] = sh[128 + k];
+}
+
 __global__ void __launch_bounds__(CT) k_fista_init(FistaCtl* c, const double* ss_part, int n_ss, const double* J_part,
                                                    int n_J, const double* vmax_part, int n_vmax, int bt_always,
                                                    const double* bx_part, int n_bx) {
@@ -1337,11 +1372,13 @@ __global__ void __launch_bounds__(CT) k_fista_control(FistaCtl* c, const double*
                                                       const double* J_part, int n_J,
                                                       cudaGraphConditionalHandle h, int use_handle,
                                                       const double* bx_part, int n_bx) {
-  __shared__ double sh[33];
-  double ss = cta_sum_col(ss_part, n_ss, 1, 0, sh);
-  if (bx_part) ss += -2.0 * cta_sum_col(bx_part, n_bx, 1, 0, sh);  // expanded objective (FV_FISTA_EXP)
-  const double l1 = cta_sum_col(J_part, n_J, 2, 0, sh);
-  const double l2 = cta_sum_col(J_part, n_J, 2, 1, sh);
+  __shared__ double sh[132];
+  if (c->done) return;  // batched host loops (sharded contexts) enqueue steps past the stop
+  double s4[4];
+  cta_sums4(ss_part, n_ss, J_part, n_J, bx_part, n_bx, sh, s4);
+  double ss = s4[0];
+  if (bx_part) ss += -2.0 * s4[3];  // expanded objective (FV_FISTA_EXP)
+  const double l1 = s4[1], l2 = s4[2];
   if (threadIdx.x != 0) return;
   c->copy_best = 0;
   c->restart = 0;

@@ -1112,6 +1112,8 @@ static void enqueue_body(Fit& F, cudaGraphConditionalHandle h, int use_handle) {
 // KG_HOST_LOOP=1: drive the FISTA loop from the host (one sync per
 // iteration) instead of the conditional graph, so profilers can see the
 // individual kernels.  Same kernels, same arithmetic.
+constexpr int kHostBatch = 8;  // FISTA steps per host round trip of a sharded n-space loop
+
 static bool host_loop_mode() {
   static const bool on = [] {
     const char* e = std::getenv("KG_HOST_LOOP");
@@ -1385,15 +1387,22 @@ static void fista_enqueue(Fit& F, double lambda, const InnerCfg& ic, const doubl
                n_vmax, 0, ex ? F.bxpart.d() : nullptr, pgrid(F.p));
   }
   if (ic.max_iters >= 1) {
-    // a sharded n-space loop is driven from the host: its all-reduces stay out of graph capture
+    // A sharded n-space loop is driven from the host (its all-reduces stay out
+    // of graph capture) in batches of kHostBatch steps with one stream sync per
+    // batch: the update and control kernels are no-ops once the device control
+    // block says done, so steps enqueued past the stop leave the state as it is
+    // (x is unchanged, so S(x) and its all-reduce recompute the same values),
+    // and every rank enqueues the same collectives.  KG_HOST_LOOP (profiling)
+    // keeps one step per batch.
     if (host_loop_mode() || (sharded(ctx) && F.route == 0)) {
       const FistaCtl* hc = reinterpret_cast<const FistaCtl*>(ctx->pin() + PIN_CTL);
-      i64 before = ctx->launches;
+      const int batch = host_loop_mode() ? 1 : kHostBatch;
+      const i64 before = ctx->launches;
       for (;;) {
         KG_CUDA(cudaMemcpyAsync(ctx->pin() + PIN_CTL, F.ctl.p, sizeof(FistaCtl), cudaMemcpyDeviceToHost, ctx->s));
         sync(ctx);
         if (hc->done) break;
-        enqueue_body(F, cudaGraphConditionalHandle{}, 0);
+        for (int k = 0; k < batch; ++k) enqueue_body(F, cudaGraphConditionalHandle{}, 0);
       }
       // fista_read() adds iterations * kernels_per_iter; undo the direct count
       const i64 its = hc->iterations;
