@@ -201,7 +201,8 @@ struct HlastArgs {
   const double* eta_old = nullptr;
   const double* u = nullptr;
   const double* y = nullptr;
-  const double* a = nullptr;
+  const double* a = nullptr;          // prior weights; nullptr: every cell has weight a_val
+  double a_val = 1.0;
   int fam = 0;
   double disp = 1.0;
   int flags = 0;
@@ -219,8 +220,9 @@ struct FamilyArgs {
   i64 n = 0;
   int fam = 0, mode = 0;  // mode: 0 exact, 1 unit
   double disp = 1.0;
-  const double *y = nullptr, *a = nullptr, *eta = nullptr;
-  double *u = nullptr, *v = nullptr, *z = nullptr;
+  const double *y = nullptr, *a = nullptr, *eta = nullptr;  // a == nullptr: every cell has weight a_val
+  double a_val = 1.0;
+  double *u = nullptr, *v = nullptr, *z = nullptr;  // u may be nullptr (not stored)
   double* partial = nullptr;  // max(v) per CTA
   i64* err = nullptr;         // [score, working response]
   i64 cell_base = 0;

@@ -542,7 +542,7 @@ __global__ void __launch_bounds__(NT) k_hlast(HlastArgs h) {
       en = __ldg(h.eta_new + g);
     }
     if (h.flags & (HL_LL_NEW | HL_DOT | HL_TRIALS)) {
-      const double yy = __ldg(h.y + g), aa = __ldg(h.a + g);
+      const double yy = __ldg(h.y + g), aa = h.a ? __ldg(h.a + g) : h.a_val;
       if ((h.flags & HL_LL_NEW) && aa != 0.0) {
         const double t = ll_term(h.fam, yy, aa, en);
         if (!isfinite(t)) record_min(h.err + 0, h.cell_base + g);
@@ -592,10 +592,10 @@ __global__ void __launch_bounds__(NT) k_family(FamilyArgs f) {
   __shared__ double red[32];
   double vmax = -DBL_MAX;
   for (i64 i = static_cast<i64>(blockIdx.x) * NT + threadIdx.x; i < f.n; i += static_cast<i64>(gridDim.x) * NT) {
-    const double yy = f.y[i], aa = f.a[i], e = f.eta[i], ec = clampe(e);
+    const double yy = f.y[i], aa = f.a ? f.a[i] : f.a_val, e = f.eta[i], ec = clampe(e);
     const double u = score_of(f.fam, yy, aa, e) / f.disp;
     if (!isfinite(u)) record_min(f.err + 0, f.cell_base + i);
-    f.u[i] = u;
+    if (f.u) f.u[i] = u;
     double v, z;
     if (f.mode == 1) {  // unit weights, generic working response (outer.cpp:148-155)
       v = 1.0;

@@ -920,7 +920,8 @@ static HlastArgs hlast_args(const Fit& F) {
   h.T = D.T;
   h.H = D.f[0][0]->dev.H;
   h.y = F.O->y.d();
-  h.a = F.O->a.d();
+  h.a = F.O->a_const ? nullptr : F.O->a.d();  // constant prior weights are not streamed
+  h.a_val = F.O->a_val;
   h.fam = F.fam;
   h.disp = F.disp;
   h.partial = F.part.d();
@@ -1828,9 +1829,10 @@ static ModelTrace outer_loop(Fit& F, double lambda, const OuterCfg& oc) {
     fa.mode = oc.wmode == KG_W_UNIT ? 1 : 0;
     fa.disp = F.disp;
     fa.y = F.O->y.d();
-    fa.a = F.O->a.d();
+    fa.a = F.O->a_const ? nullptr : F.O->a.d();
+    fa.a_val = F.O->a_val;
     fa.eta = F.eta.d();
-    fa.u = F.u.d();
+    fa.u = oc.wmode == KG_W_TENSOR ? F.u.d() : nullptr;  // the score is only kept for the tensor weights
     fa.v = F.v.d();
     fa.z = F.z.d();
     fa.partial = vmax_part;
@@ -1861,9 +1863,8 @@ static ModelTrace outer_loop(Fit& F, double lambda, const OuterCfg& oc) {
     int nt = 0;
     for (; nt < first_batch && nt <= oc.max_bt; ++nt, t *= oc.b) t_list[nt] = t;
     HlastArgs h = hlast_args(F);
-    h.flags = HL_DOT | HL_TRIALS;
+    h.flags = HL_DOT | HL_TRIALS | HL_U_FLY;  // u = score(eta) recomputed from y, a, eta (not streamed)
     h.eta_old = F.eta.d();
-    h.u = F.u.d();
     h.ntrial = nt;
     for (int j = 0; j < nt; ++j) h.t[j] = t_list[j];
     g = h_full(F, F.best.d(), F.eta_t.d(), h);
