@@ -154,7 +154,9 @@ def test_path_matches_oracle_fixture(name):
             assert r["inner_iterations"] == int(ref["inner_iterations"])
             assert r["inner_converged"] == bool(ref["inner_converged"])
             assert rel(r["objective"], ref["objective"]) <= REL
-            assert rel(r["lipschitz"], ref["lipschitz"]) <= 1e-11  # spectral radii: see the spectral test
+            # L-hat = max(v)/n * prod(rho_j): the spectral radii agree to ~1e-13 (spectral
+            # test); max(v) follows the coefficients, so it gets the model's coefficient tolerance
+            assert rel(r["lipschitz"], ref["lipschitz"]) <= max(1e-11, tol[t])
             assert abs(r["delta_k"] - ref["delta_k"]) <= REL * max(1.0, abs(ref["objective"]))
     res.close()
     obs.close()
