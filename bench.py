@@ -347,9 +347,22 @@ def run_ours(args):
     # --- roofline of the step's dominant kernel and the rho-contraction passes
     hbm, peak_kind = peaks()
     rho = {}
-    for key, which, what in (("fused_pass", 0, "fused n-space pass (H-last + v eta^2 + V.* + G-first)"),
-                             ("largest_h_step", 1, "largest banded H-chain contraction"),
-                             ("g_step", 5, "mode-2 G-chain contraction")):
+    try:  # the route the fits run: slab pass (d = 3) or the mode-1 fused pass
+        kernel_time(ctx, design, obs, 6, reps=1)
+        slab = True
+    except Exception:
+        slab = False
+    kernels = ((("fused_pass", 0, "k_slab: slab pass (per last-mode slice: eta = X1 S3 X2^T, v eta^2, "
+                 "Q3 = X1^T (v eta) X2)"),
+                ("h_mode3_step", 6, "mode-3 H-chain contraction (x -> S3)"),
+                ("g_mode3_step", 7, "mode-3 G-chain contraction (Q3 -> S x)"),
+                ("largest_h_step", 1, "largest banded H-chain contraction (Armijo trial eta, once per outer "
+                 "iteration)"))
+               if slab else
+               (("fused_pass", 0, "fused n-space pass (H-last + v eta^2 + V.* + G-first)"),
+                ("largest_h_step", 1, "largest banded H-chain contraction"),
+                ("g_step", 5, "mode-2 G-chain contraction")))
+    for key, which, what in kernels:
         try:
             ms, b = kernel_time(ctx, design, obs, which)
         except Exception as e:  # a route without this kernel (e.g. 2-D designs have no mode-2 G step)

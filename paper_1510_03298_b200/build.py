@@ -7,7 +7,7 @@ HERE = os.path.dirname(os.path.abspath(__file__))
 ROOT = os.path.dirname(HERE)
 CSRC = os.path.join(HERE, "csrc")
 LIB = os.path.join(HERE, "libkronglm_b200.so")
-SOURCES = ["kg_kernels.cu", "kg_fused.cu", "kg_gram.cu", "kg_builders.cu", "kg_solver.cu", "kg_host.cpp"]
+SOURCES = ["kg_kernels.cu", "kg_fused.cu", "kg_slab.cu", "kg_gram.cu", "kg_builders.cu", "kg_solver.cu", "kg_host.cpp"]
 NVCC_FLAGS = ["-gencode", "arch=compute_100a,code=sm_100a", "-O3", "-std=c++17", "-lineinfo",
               "-Xcompiler", "-fPIC,-Wno-nonnull", "-diag-suppress", "177"]
 OBJ = os.path.join(HERE, "build")

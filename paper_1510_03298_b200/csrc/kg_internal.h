@@ -173,6 +173,32 @@ struct FusedArgs {
   int dbg = 0;                 // measurement only: 1 = copies only, 2 = copies + phase A
 };
 int fused_grid(const FusedArgs& f);
+// Slab pass (kg_slab.cu): modes 1 and 2 of one n-space FISTA step (FV_FISTA_EXP)
+// fused per slice of the last mode of a d = 3 design: S3 = x x_3 X3 in,
+// Q3 = X1^T (v .* (X1 S3 X2^T)) X2 out, one read of v.
+struct SlabArgs {
+  int n1 = 0, n2 = 0, p1 = 0, p2 = 0;
+  i64 m3 = 0;                   // slices (local last-mode extent)
+  int nch = 0;                  // chunks of 8 mode-2 grid rows
+  int cg = 1, ldS = 0, ldZ = 0, ldU = 0, ldW = 0;  // set by the launcher
+  BandOp H1;                    // rows of X1 (<= 4 taps)
+  MmaOp g1;                     // X1^T as DMMA A fragments
+  // per chunk c of X2 (8 rows 8c .. 8c + 7, 8-wide coefficient window from w0[c]):
+  const int* w0 = nullptr;
+  const double* x2u = nullptr;  // [c][s][lane] = X2[8c + lane/4, w0[c] + 4s + lane%4]
+  // Z step: the chunk's window inside the aligned 8-column tiles t0 (and t0 + 1),
+  // tz[c] = t0 | (second tile used) << 16
+  const int* tz = nullptr;
+  const double* x2z = nullptr;  // [c][tile][s][lane] = X2[8c + 2 (lane%4) + s, 8 (t0 + tile) + lane/4]
+  const double* S = nullptr;    // p1 x p2 x m3
+  const double* v = nullptr;    // n1 x n2 x m3
+  double* Q = nullptr;          // p1 x p2 x m3 (out)
+  double* partial = nullptr;    // one double per CTA: sum v eta^2
+};
+bool slab_ok(const SlabArgs& a);
+int slab_grid(const SlabArgs& a);
+void slab_pass(const Launch& L, const SlabArgs& a);
+
 // plain streaming read of two n-arrays (bandwidth reference for kg_time_kernel)
 void stream_read2(const Launch& L, i64 n, const double* x, const double* y, double* partial);
 void fused_mode1(const Launch& L, int variant, const FusedArgs& f);

@@ -1,0 +1,437 @@
+// Slab pass: modes 1 AND 2 of one n-space FISTA step, fused per slice of the
+// last mode (d = 3, one component, FV_FISTA_EXP objective).
+//
+// Per FISTA step the n-space route needs S(x) = X^T diag(v) X x
+// (design.cpp:118-124, xtwx_apply).  With the mode-3 H partial
+// S3 = x x_3 X3 (p1 x p2 x n3) and the slice-local maps
+//     eta(:, :, i3) = X1 S3(:, :, i3) X2^T,    w = v .* eta,
+//     Q3(:, :, i3)  = X1^T w(:, :, i3) X2,
+// S(x) = Q3 x_3 X3^T, so the only n-sized traffic of a step is one read of v
+// (the p1 x n2 x n3 partials of the mode-1 route never touch HBM).
+//
+// One CTA per SM (persistent over slices), 16 warps in two roles that form a
+// software pipeline over chunks of 8 mode-2 grid rows:
+//   * 8 "row" warps: a thread owns 4 consecutive grid rows x 2 columns of a
+//     chunk; eta = X1 U over a 5-wide coefficient window in registers (the 4
+//     rows share one window, so 5 shared loads serve 8 cells), w = v eta,
+//     sum w eta.  v streams from HBM straight into registers (16-byte loads,
+//     two chunks ahead), and w goes to a padded double-buffered tile
+//     (stride = 4 mod 16, so the DMMA B fragments of the tensor warps are
+//     conflict free);
+//   * 8 "tensor" warps (warp = 8 rows of p1): Y = X1^T w (DMMA m8n8k4, the
+//     band window of the row group as A fragments in registers), Z += Y X2
+//     (DMMA whose A fragments are Y's accumulators: the k index runs over the
+//     chunk's rows in the order 0,2,4,6 | 1,3,5,7, so the D layout of one MMA
+//     is the A layout of the next), and U = S3 X2[chunk]^T for the chunk two
+//     ahead (DMMA).  Z lives in a two-tile register window that slides with the
+//     chunk's coefficient window; completed tiles go straight to Q3.
+// The roles hand over through named barriers (U ready / U free / w ready /
+// w free, double-buffered), so the row warps' FP64 FMAs and loads and the
+// tensor warps' DMMAs overlap instead of alternating.
+#include <algorithm>
+#include <cstdlib>
+
+#include "kg_async.cuh"
+#include "kg_internal.h"
+
+namespace kg {
+
+namespace {
+
+constexpr int kSlabBS = 512;     // row warps + tensor warps
+constexpr int kTeam = 256;      // threads per role
+
+__device__ __forceinline__ double warp_sum_s(double v) {
+#pragma unroll
+  for (int o = 16; o > 0; o >>= 1) v += __shfl_down_sync(0xffffffffu, v, o);
+  return v;
+}
+
+__device__ __forceinline__ void dmma(double& d0, double& d1, double a, double b) {
+  asm volatile("mma.sync.aligned.m8n8k4.row.col.f64.f64.f64.f64 {%0, %1}, {%2}, {%3}, {%0, %1};"
+               : "+d"(d0), "+d"(d1)
+               : "d"(a), "d"(b));
+}
+
+
+__device__ __forceinline__ double2 lds2(const double* p) { return *reinterpret_cast<const double2*>(p); }
+
+constexpr int kLdr = 10;  // row stride of the row-major U tile (10 doubles: conflict-free 16-byte row reads)
+
+// named barriers (0 is __syncthreads): U ready (tensor -> row warps) and
+// w ready (row -> tensor warps), one per pipeline buffer
+constexpr int kDepth = 4;  // U and w buffers: the row warps may run up to kDepth chunks ahead
+constexpr int kBarUReady = 1, kBarWReady = 1 + kDepth, kBarTensor = 1 + 2 * kDepth;
+
+__device__ __forceinline__ void nb_sync(int id, int n) { asm volatile("bar.sync %0, %1;" ::"r"(id), "r"(n) : "memory"); }
+__device__ __forceinline__ void nb_arrive(int id, int n) {
+  asm volatile("bar.arrive %0, %1;" ::"r"(id), "r"(n) : "memory");
+}
+
+__device__ __forceinline__ double2 ldg2_stream(const double* p) {
+  double2 r;
+  asm volatile("ld.global.nc.L1::no_allocate.v2.f64 {%0, %1}, [%2];" : "=d"(r.x), "=d"(r.y) : "l"(p));
+  return r;
+}
+
+constexpr int kWin = 5;  // coefficient window of a row quad (cubic B-splines: 4 taps, shifting by <= 1)
+
+// KS: k-steps of the X1^T window.
+template <int KS>
+__global__ void __launch_bounds__(kSlabBS, 1) k_slab(SlabArgs a) {
+  using namespace async;
+  extern __shared__ __align__(128) double sm[];
+  __shared__ double red[32];
+  __shared__ unsigned long long sbar[2];     // the two S3 tiles
+  const int n1 = a.n1, n2 = a.n2, p1 = a.p1, p2 = a.p2, nch = a.nch;
+  const int ldS = a.ldS, ldW = a.ldW;
+  const int groups = (p1 + 7) >> 3;
+  const int sbuf = ldS * p2;                  // one S3 tile
+  const int ubuf = kLdr * 8 * groups;         // one U tile (row-major, rows of p1 padded to the row groups)
+  const int wbuf = ldW * 8;                   // one w tile
+  double* Ss = sm;                            // [2][ldS x p2]
+  double* Us = Ss + 2 * sbuf;                 // [kDepth][ubuf]
+  double* Ws = Us + kDepth * ubuf;            // [kDepth][wbuf]
+  const int tid = threadIdx.x, lane = tid & 31, warp = tid >> 5;
+  const bool rowrole = warp < 8;
+  const i64 p12 = static_cast<i64>(p1) * p2, n12 = static_cast<i64>(n1) * n2;
+  const int rounds = static_cast<int>((a.m3 - blockIdx.x + gridDim.x - 1) / gridDim.x);  // slices of this CTA
+  const int qtot = rounds * nch;
+  // the S3 tile of round r (p2 padded column copies by the bulk engine)
+  auto issue_s = [&](int r) {
+    if (r >= rounds) return;
+    const unsigned bytes = static_cast<unsigned>(p1 * 8);
+    mbar_expect_tx(&sbar[r & 1], bytes * p2);
+    const double* src = a.S + (blockIdx.x + static_cast<i64>(r) * gridDim.x) * p12;
+    double* dst = Ss + (r & 1) * sbuf;
+    for (int k = 0; k < p2; ++k) bulk_g2s(dst + ldS * k, src + static_cast<i64>(p1) * k, bytes, &sbar[r & 1]);
+  };
+  if (tid == 0) {
+    mbar_init(&sbar[0], 1);
+    mbar_init(&sbar[1], 1);
+  }
+  // zero both S3 tiles (their padded rows are read by the last row group)
+  for (int k = tid; k < 2 * sbuf; k += kSlabBS) Ss[k] = 0.0;
+  __syncthreads();
+  double acc0 = 0.0, acc1 = 0.0;
+  if (rowrole) {
+    // ------------------------------------------------------------ row warps
+    const int nq = n1 >> 2;                    // row quads
+    const bool act = tid < 4 * nq;
+    const int rq = act ? tid % nq : 0, cp = act ? tid / nq : 0;
+    const int r0 = 4 * rq, c0 = 2 * cp;        // rows r0 .. r0 + 3, chunk columns c0, c0 + 1
+    int lo = 0;
+    double C[4][kWin];
+#pragma unroll
+    for (int r = 0; r < 4; ++r)
+#pragma unroll
+      for (int t = 0; t < kWin; ++t) C[r][t] = 0.0;
+    if (act) {
+      lo = min(__ldg(a.H1.lo + r0), p1 - kWin);
+#pragma unroll
+      for (int r = 0; r < 4; ++r) {
+        const int l = __ldg(a.H1.lo + r0 + r), len = __ldg(a.H1.len + r0 + r);
+        const double* cf = a.H1.coef + __ldg(a.H1.off + r0 + r);
+#pragma unroll
+        for (int t = 0; t < kWin; ++t) {
+          const int j = lo + t - l;
+          C[r][t] = (j >= 0 && j < len) ? __ldg(cf + j) : 0.0;
+        }
+      }
+    }
+    const double* ub0 = Us + lo * kLdr + c0;
+    double* wb0 = Ws + r0 + ldW * c0;
+    // v of chunk (round, chunk): rows r0 .. r0 + 3 of columns c0, c0 + 1 (zeros past n2)
+    const double* vbase = a.v + blockIdx.x * n12 + r0;
+    const i64 vstep = static_cast<i64>(gridDim.x) * n12;
+    auto load_v = [&](double (&vr)[8], int r, int c) {
+#pragma unroll
+      for (int e = 0; e < 2; ++e) {
+        const int col = 8 * c + c0 + e;
+        if (act && r < rounds && col < n2) {
+          const double* p = vbase + r * vstep + static_cast<i64>(n1) * col;
+          const double2 x = ldg2_stream(p), y = ldg2_stream(p + 2);
+          vr[4 * e + 0] = x.x;
+          vr[4 * e + 1] = x.y;
+          vr[4 * e + 2] = y.x;
+          vr[4 * e + 3] = y.y;
+        } else {
+#pragma unroll
+          for (int k = 0; k < 4; ++k) vr[4 * e + k] = 0.0;
+        }
+      }
+    };
+    double vA[8], vB[8];
+    int lr = 0, lc = 0;  // cursor of the next chunk to load
+    auto adv = [&](int& r, int& c) {
+      if (++c == nch) {
+        c = 0;
+        ++r;
+      }
+    };
+    load_v(vA, lr, lc);
+    adv(lr, lc);
+    load_v(vB, lr, lc);
+    adv(lr, lc);
+    // chunk q: U(q) is ready (and the tensor warps are done with w(q - kDepth),
+    // which they read before forming U(q)); w(q) -> tile q % kDepth
+    auto body = [&](int q, double (&vr)[8]) {
+      const int buf = q & (kDepth - 1);
+      nb_sync(kBarUReady + buf, kSlabBS);
+      if (act) {
+        const double* u = ub0 + buf * ubuf;
+        double2 uu[kWin];
+#pragma unroll
+        for (int t = 0; t < kWin; ++t) uu[t] = lds2(u + t * kLdr);
+        double* w = wb0 + buf * wbuf;
+#pragma unroll
+        for (int c = 0; c < 2; ++c) {
+          double wv[4];
+#pragma unroll
+          for (int r = 0; r < 4; ++r) {
+            double x = C[r][0] * (c ? uu[0].y : uu[0].x);
+#pragma unroll
+            for (int t = 1; t < kWin; ++t) x = fma(C[r][t], c ? uu[t].y : uu[t].x, x);
+            wv[r] = vr[4 * c + r] * x;
+            if (r & 1) acc1 = fma(wv[r], x, acc1);
+            else acc0 = fma(wv[r], x, acc0);
+          }
+          *reinterpret_cast<double2*>(w + ldW * c) = make_double2(wv[0], wv[1]);
+          *reinterpret_cast<double2*>(w + ldW * c + 2) = make_double2(wv[2], wv[3]);
+        }
+      }
+      nb_arrive(kBarWReady + buf, kSlabBS);
+      load_v(vr, lr, lc);  // two chunks ahead
+      adv(lr, lc);
+    };
+    int q = 0;
+    for (; q + 1 < qtot; q += 2) {
+      body(q, vA);
+      body(q + 1, vB);
+    }
+    if (q < qtot) body(q, vA);
+  } else {
+    // --------------------------------------------------------- tensor warps
+    const int tw = warp - 8;
+    const bool gact = tw < groups;            // this warp owns p1 rows 8 tw .. 8 tw + 7
+    const bool leader = tid == 8 * 32;
+    const int zr = 8 * tw + (lane >> 2), zq = 2 * (lane & 3);
+    double* ua0 = Us + zr * kLdr + zq;        // stage A D store (buffer 0)
+    int gbase = 0;
+    double afr[KS];
+#pragma unroll
+    for (int s = 0; s < KS; ++s) afr[s] = 0.0;
+    if (gact) {
+      gbase = __ldg(a.g1.base + tw);
+#pragma unroll
+      for (int s = 0; s < KS; ++s) afr[s] = __ldg(a.g1.afrag + (tw * KS + s) * 32 + lane);
+    }
+    const double* wc0 = Ws + gbase + (lane & 3) + ldW * (lane >> 2);  // B fragments of Y
+    // flattened chunk cursors (round, chunk)
+    struct Cur {
+      int r, c;
+    };
+    auto adv = [&](Cur& k) {
+      if (++k.c == nch) {
+        k.c = 0;
+        ++k.r;
+      }
+    };
+    auto at_q = [&](int q) {  // only for the few prologue positions
+      Cur k{0, 0};
+      for (int i = 0; i < q; ++i) adv(k);
+      return k;
+    };
+    if (leader) {
+      mbar_init_fence();
+      fence_proxy_async();
+      issue_s(0);
+      issue_s(1);
+    }
+    // chunk tables, loaded one chunk ahead of use
+    struct ZT { int tz; double b0, b1, b2, b3; };
+    struct AT { int wz; double b0, b1; };
+    auto load_z = [&](int c) {
+      ZT t;
+      const double* x2 = a.x2z + c * 128;
+      t.tz = __ldg(a.tz + c);
+      t.b0 = __ldg(x2 + lane);
+      t.b1 = __ldg(x2 + 32 + lane);
+      t.b2 = __ldg(x2 + 64 + lane);
+      t.b3 = __ldg(x2 + 96 + lane);
+      return t;
+    };
+    auto load_a = [&](int c) {
+      AT t;
+      const double* x2 = a.x2u + c * 64;
+      t.wz = __ldg(a.w0 + c);
+      t.b0 = __ldg(x2 + lane);
+      t.b1 = __ldg(x2 + 32 + lane);
+      return t;
+    };
+    // U of chunk (r, c) into U buffer ub
+    auto stage_a = [&](const Cur& k, int ub, const AT& t) {
+      if (k.c == 0) mbar_wait(&sbar[k.r & 1], static_cast<unsigned>((k.r >> 1) & 1));
+      if (!gact) return;
+      const double* sr = Ss + (k.r & 1) * sbuf + zr + ldS * (t.wz + (lane & 3));
+      double d0 = 0.0, d1 = 0.0;
+      dmma(d0, d1, sr[0], t.b0);
+      dmma(d0, d1, sr[4 * ldS], t.b1);
+      *reinterpret_cast<double2*>(ua0 + ub * ubuf) = make_double2(d0, d1);
+    };
+    Cur ka{0, 0};  // U step cursor
+    for (int q = 0; q < kDepth; ++q, adv(ka)) {
+      if (q < qtot) {
+        stage_a(ka, q, load_a(ka.c));
+        nb_arrive(kBarUReady + q, kSlabBS);
+      }
+    }
+    nb_sync(kBarTensor, kSlabBS - 256);
+    if (leader)  // a round whose last U was just formed frees its S3 tile
+      for (int q = 0; q < kDepth && q < qtot; ++q)
+        if (at_q(q).c == nch - 1) issue_s(at_q(q).r + 2);
+    Cur kz = at_q(1);              // Z tables: q + 1
+    Cur kt = ka;                   // U tables: q + kDepth + 1
+    adv(kt);
+    // Z window: slot 0 = tile T, slot 1 = tile T + 1 (8 columns each) of the current slice
+    int T = -1;
+    double z00 = 0.0, z01 = 0.0, z10 = 0.0, z11 = 0.0;
+    double* qs = a.Q + blockIdx.x * p12;
+    const i64 qstep = static_cast<i64>(gridDim.x) * p12;
+    auto flush = [&](int k, double x0, double x1) {
+      const int zc = 8 * k + zq;
+      if (zr < p1 && zc < p2) qs[zr + static_cast<i64>(p1) * zc] = x0;
+      if (zr < p1 && zc + 1 < p2) qs[zr + static_cast<i64>(p1) * (zc + 1)] = x1;
+    };
+    ZT zt = load_z(0);
+    AT at = load_a(ka.c);  // ka = kDepth
+    int c = 0;
+    for (int q = 0; q < qtot; ++q) {
+      const int buf = q & (kDepth - 1);
+      const ZT zn = load_z(kz.c);   // next chunk's Z tables
+      const AT an = load_a(kt.c);   // and the U tables one further
+      nb_sync(kBarWReady + buf, kSlabBS);
+      if (gact) {
+        const double* wb = wc0 + buf * wbuf;
+        double d[4][2] = {{0.0, 0.0}, {0.0, 0.0}, {0.0, 0.0}, {0.0, 0.0}};
+#pragma unroll
+        for (int s = 0; s < KS; s += 4) {
+#pragma unroll
+          for (int h = 0; h < 4; ++h) dmma(d[h][0], d[h][1], afr[s + h], wb[4 * (s + h)]);
+        }
+        const double y0 = (d[0][0] + d[1][0]) + (d[2][0] + d[3][0]);
+        const double y1 = (d[0][1] + d[1][1]) + (d[2][1] + d[3][1]);
+        const int t0 = zt.tz & 0xffff;
+        if (T < 0) T = t0;
+        while (T < t0) {  // tile T is complete: later chunks start at t0 > T
+          flush(T, z00, z01);
+          z00 = z10;
+          z01 = z11;
+          z10 = z11 = 0.0;
+          ++T;
+        }
+        dmma(z00, z01, y0, zt.b0);
+        dmma(z00, z01, y1, zt.b1);
+        if (zt.tz >> 16) {
+          dmma(z10, z11, y0, zt.b2);
+          dmma(z10, z11, y1, zt.b3);
+        }
+        if (c == nch - 1) {  // slice done: the live window holds its last two tiles
+          flush(T, z00, z01);
+          flush(T + 1, z10, z11);
+          z00 = z01 = z10 = z11 = 0.0;
+          T = -1;
+        }
+      }
+      // U(q + kDepth) into the buffer of chunk q (the row warps are done with it)
+      if (q + kDepth < qtot) {
+        stage_a(ka, buf, at);
+        nb_arrive(kBarUReady + buf, kSlabBS);
+        if (ka.c == nch - 1) {  // that round's S3 tile is free once every tensor warp formed its U
+          nb_sync(kBarTensor, kSlabBS - 256);
+          if (leader) {
+            fence_proxy_async();
+            issue_s(ka.r + 2);
+          }
+        }
+      }
+      adv(ka);
+      adv(kz);
+      adv(kt);
+      zt = zn;
+      at = an;
+      if (++c == nch) {
+        c = 0;
+        qs += qstep;
+      }
+    }
+  }
+  // per-CTA partial of sum v eta^2 (fixed order)
+  double rr = warp_sum_s(acc0 + acc1);
+  __syncthreads();
+  if (lane == 0) red[warp] = rr;
+  __syncthreads();
+  if (warp == 0) {
+    rr = lane < (kSlabBS >> 5) ? red[lane] : 0.0;
+    rr = warp_sum_s(rr);
+    if (lane == 0) a.partial[blockIdx.x] = rr;
+  }
+}
+
+}  // namespace
+
+// Leading dimensions and shared-memory size of a slab plan.
+static size_t slab_layout(SlabArgs& a) {
+  const int p1r = (a.p1 + 15) / 16 * 16;
+  a.ldS = p1r + 4;                           // = 4 (mod 16): A fragments of stage A
+  a.ldU = kLdr;
+  a.ldZ = 0;
+  a.ldW = (a.n1 + 15) / 16 * 16 + 4;         // = 4 (mod 16): B fragments of stage C
+  a.cg = 1;
+  const size_t ubuf = static_cast<size_t>(kLdr) * 8 * ((a.p1 + 7) / 8);
+  const size_t dbl = 2 * static_cast<size_t>(a.ldS) * a.p2 + kDepth * ubuf + kDepth * static_cast<size_t>(a.ldW) * 8;
+  return dbl * sizeof(double);
+}
+
+bool slab_ok(const SlabArgs& a0) {
+  SlabArgs a = a0;
+  if (!a.x2u || !a.x2z || !a.w0 || !a.tz || a.g1.ks == 0 || !a.H1.hlo || !a.H1.hlen) return false;
+  if (a.n1 > 4 * kTeam / 4 || (a.n1 & 3) || (a.p1 & 1) || a.p1 > 64 || a.p1 < kWin || a.p2 < 8 || a.p2 > 64 ||
+      a.H1.maxlen > 4)
+    return false;
+  if (a.g1.groups != (a.p1 + 7) / 8 || a.nch < kDepth) return false;
+  // every quad of grid rows reads a kWin-wide coefficient window
+  for (int r0 = 0; r0 < a.n1; r0 += 4) {
+    const int lo = std::min(a.H1.hlo[r0], a.p1 - kWin);
+    for (int r = r0; r < r0 + 4; ++r)
+      if (a.H1.hlen[r] > 0 && (a.H1.hlo[r] < lo || a.H1.hlo[r] + a.H1.hlen[r] > lo + kWin)) return false;
+  }
+  return slab_layout(a) <= 232448 - 1024;
+}
+
+int slab_grid(const SlabArgs& a) {
+  int dev = 0, sms = 148;
+  cudaGetDevice(&dev);
+  cudaDeviceGetAttribute(&sms, cudaDevAttrMultiProcessorCount, dev);
+  return static_cast<int>(std::min<i64>(a.m3, sms));
+}
+
+template <int KS>
+static void launch_slab_ks(const Launch& L, const SlabArgs& a, size_t smem, int g) {
+  smem_attr(k_slab<KS>, static_cast<int>(smem));
+  k_slab<KS><<<g, kSlabBS, smem, L.s>>>(a);
+}
+
+void slab_pass(const Launch& L, const SlabArgs& a0) {
+  SlabArgs a = a0;
+  const size_t smem = slab_layout(a);
+  const int g = slab_grid(a);
+  switch (a.g1.ks) {
+    case 8: launch_slab_ks<8>(L, a, smem, g); break;
+    case 12: launch_slab_ks<12>(L, a, smem, g); break;
+    default: launch_slab_ks<16>(L, a, smem, g); break;
+  }
+  launched(L);
+}
+
+}  // namespace kg

@@ -620,6 +620,56 @@ static std::vector<double> spectral_collect(SpectralPending& S) {
   return S.vals;
 }
 
+// Per-chunk X2 fragments of the slab pass (SlabArgs; d = 3, one component).
+struct SlabTables {
+  DBuf w0, tz, x2u, x2z;
+  int nch = 0;
+};
+
+// Builds the slab tables from the dense mode-2 factor X2 (n x p, column-major)
+// when every chunk of 8 grid rows reads an 8-wide coefficient window; returns
+// null otherwise (the design then keeps the mode-1 fused route).
+static std::unique_ptr<SlabTables> build_slab(const double* X, i64 n, i64 p, cudaStream_t st) {
+  if (p < 8 || p > 64 || n < 1) return nullptr;
+  const int nch = static_cast<int>((n + 7) / 8);
+  std::vector<int> w0(static_cast<size_t>(nch)), tz(static_cast<size_t>(nch));
+  std::vector<double> xu(static_cast<size_t>(nch) * 64, 0.0), xz(static_cast<size_t>(nch) * 128, 0.0);
+  auto at = [&](i64 r, i64 k) { return (r >= 0 && r < n && k >= 0 && k < p) ? X[r + n * k] : 0.0; };
+  for (int c = 0; c < nch; ++c) {
+    i64 lo = p, hi = 0;
+    for (i64 r = 8 * c; r < std::min<i64>(n, 8 * c + 8); ++r)
+      for (i64 k = 0; k < p; ++k)
+        if (X[r + n * k] != 0.0) {
+          lo = std::min(lo, k);
+          hi = std::max(hi, k + 1);
+        }
+    if (lo >= hi) lo = hi = 0;
+    const i64 wz = std::max<i64>(0, std::min<i64>(lo, p - 8));
+    if (hi > wz + 8) return nullptr;
+    const i64 t0 = lo / 8, two = hi > 8 * t0 + 8 ? 1 : 0;  // aligned 8-column tiles of the Z step
+    w0[static_cast<size_t>(c)] = static_cast<int>(wz);
+    tz[static_cast<size_t>(c)] = static_cast<int>(t0 | (two << 16));
+    for (int s2 = 0; s2 < 2; ++s2)
+      for (int lane = 0; lane < 32; ++lane) {
+        xu[static_cast<size_t>(c) * 64 + s2 * 32 + lane] = at(8 * c + lane / 4, wz + 4 * s2 + lane % 4);
+        for (int tl = 0; tl < 2; ++tl)
+          xz[static_cast<size_t>(c) * 128 + (tl * 2 + s2) * 32 + lane] =
+              at(8 * c + 2 * (lane % 4) + s2, 8 * (t0 + tl) + lane / 4);
+      }
+  }
+  auto T = std::make_unique<SlabTables>();
+  T->nch = nch;
+  T->w0.alloc(sizeof(int) * w0.size());
+  T->tz.alloc(sizeof(int) * tz.size());
+  T->x2u.alloc(sizeof(double) * xu.size());
+  T->x2z.alloc(sizeof(double) * xz.size());
+  h2d(T->w0.p, w0.data(), sizeof(int) * w0.size(), st);
+  h2d(T->tz.p, tz.data(), sizeof(int) * tz.size(), st);
+  h2d(T->x2u.p, xu.data(), sizeof(double) * xu.size(), st);
+  h2d(T->x2z.p, xz.data(), sizeof(double) * xz.size(), st);
+  return T;
+}
+
 }  // namespace kg
 
 struct kg_design {
@@ -643,6 +693,7 @@ struct kg_design {
   mutable std::unique_ptr<kg::SpectralPending> pending;
   bool fused = false;
   int T = 1;                               // mode-1 fibres per CTA in the fused kernels
+  std::unique_ptr<kg::SlabTables> slab;    // d = 3, one component: modes 1+2 fused per slice (kg_slab.cu)
   kg::i64 scratch = 0;                     // doubles per chain scratch buffer
   kg::i64 part_cap = 0;                    // doubles in the partials buffer
 };
@@ -813,6 +864,10 @@ struct Fit {
   // route 0 on the fused design: objective sum v eta^2 - 2 <b, x> + sum v z^2
   // (FV_FISTA_EXP, z is not read per iteration); KG_ROUTE0_DIRECT=1 keeps sum v (eta - z)^2
   bool expand = false;
+  // route 0, FV_FISTA_EXP on a d = 3 design with slab tables: the slab pass
+  // (modes 1 and 2 fused per last-mode slice, kg_slab.cu) replaces the
+  // mode-1 fused pass and the mode-2 chain steps
+  bool slab = false;
   // iwls = tensor: the current outer iteration's weighted Gram blocks
   // X_{m,j}^T diag(f_j) X_{r,j} (same band structure as design.gram) and the
   // Lipschitz factor (prod_j rho(G_j(f_j)) for c = 1, max(v) L-hat otherwise)
@@ -844,6 +899,7 @@ struct Fit {
 };
 
 static FusedArgs fused_args(const Fit& F);
+static SlabArgs slab_args(const Fit& F);
 
 
 static void alloc_fit(Fit& F) {
@@ -872,6 +928,7 @@ static void alloc_fit(Fit& F) {
   F.bxpart.alloc(sizeof(double) * pgrid(F.p));
   F.expand = false;
   if (D.fused && std::getenv("KG_ROUTE0_DIRECT") == nullptr) F.expand = fused_fast_ok(fused_args(F), FV_FISTA_EXP);
+  F.slab = F.expand && D.slab && slab_ok(slab_args(F));
   F.tpart.alloc(sizeof(double) * 2 * (1 + kMaxTrials) * pgrid(F.p));
   F.scal.alloc(sizeof(double) * 64);
   F.errs.alloc(sizeof(i64) * 16);
@@ -911,6 +968,28 @@ static FusedArgs fused_args(const Fit& F) {
   return a;
 }
 
+static SlabArgs slab_args(const Fit& F) {
+  const kg_design& D = *F.D;
+  SlabArgs a;
+  a.n1 = static_cast<int>(D.n[0]);
+  a.n2 = static_cast<int>(D.n[1]);
+  a.p1 = static_cast<int>(D.p[0][0]);
+  a.p2 = static_cast<int>(D.p[0][1]);
+  a.m3 = D.n[2];
+  a.H1 = D.f[0][0]->dev.H;
+  a.g1 = D.f[0][0]->mg;
+  if (D.slab) {
+    a.nch = D.slab->nch;
+    a.w0 = static_cast<const int*>(D.slab->w0.p);
+    a.tz = static_cast<const int*>(D.slab->tz.p);
+    a.x2u = D.slab->x2u.d();
+    a.x2z = D.slab->x2z.d();
+  }
+  a.v = F.v.d();
+  a.partial = F.part.d();
+  return a;
+}
+
 static HlastArgs hlast_args(const Fit& F) {
   const kg_design& D = *F.D;
   HlastArgs h;
@@ -947,6 +1026,16 @@ static int run_fused(kg_ctx* ctx, int variant, const FusedArgs& a) {
 static int xwx_pass_local(Fit& F, const double* x, double* Sx) {
   const kg_design& D = *F.D;
   kg_ctx* ctx = F.ctx;
+  if (F.slab) {  // H mode 3 -> slab pass (modes 1, 2 both ways) -> G mode 3
+    run_chain(ctx, coef_dims(D, 0), h_steps(D, 0, 2), x, F.P.d(), F.s0.d(), F.s1.d(), false);
+    SlabArgs a = slab_args(F);
+    a.S = F.P.d();
+    a.Q = F.Q.d();
+    slab_pass(ctx->L(), a);
+    std::vector<i64> dims = {D.p[0][0], D.p[0][1], D.n[2]};
+    run_chain(ctx, dims, g_steps(D, 0, 2), F.Q.d(), Sx, F.s0.d(), F.s1.d(), false);
+    return slab_grid(a);
+  }
   if (D.fused) {
     const double* P = x;
     if (D.d > 1) {
@@ -2500,6 +2589,8 @@ kg_status kg_design_create(kg_ctx* ctx, int64_t c, int64_t d, const int64_t* n, 
       while (T > 1 && (n1 + p1) * T * 8 > 96 * 1024) --T;
       D->T = static_cast<int>(T);
     }
+    if (D->fused && d == 3 && std::getenv("KG_NO_SLAB") == nullptr)
+      D->slab = build_slab(factors[1], D->n[1], D->p[0][1], ctx->s);
     D->scratch = chain_scratch(*D);
     const i64 tiles = D->fused ? (m + D->T - 1) / D->T : 0;
     const i64 hl_tiles = (m + D->T - 1) / D->T;
@@ -2955,6 +3046,26 @@ kg_status kg_time_kernel(kg_ctx* ctx, const kg_design* D, const kg_obs* O, int w
       const double* v = F.v.d();
       launch = [&, y, v] { stream_read2(ctx->L(), F.n, y, v, F.part.d()); };
       b = 16.0 * static_cast<double>(F.n);
+    } else if (which == 0 && F.slab) {
+      // the slab pass the fits run (modes 1 and 2 both ways per last-mode slice)
+      run_chain(ctx, coef_dims(*D, 0), h_steps(*D, 0, 2), F.x.d(), F.P.d(), F.s0.d(), F.s1.d(), false);
+      SlabArgs a = slab_args(F);
+      a.S = F.P.d();
+      a.Q = F.Q.d();
+      launch = [&, a] { slab_pass(ctx->L(), a); };
+      // v read, S3 (p1 x p2 x n3) read, Q3 written
+      b = 8.0 * (static_cast<double>(F.n) + 2.0 * static_cast<double>(a.p1) * a.p2 * a.m3);
+    } else if (which == 6 || which == 7) {
+      // slab route: the mode-3 H step (p1 p2 x p3 -> x n3) or G step (x n3 -> x p3)
+      if (!F.slab) throw Error(E_INVAL, "kg_time_kernel: this design does not run the slab route");
+      const i64 a_ = D->p[0][0] * D->p[0][1], K = which == 6 ? D->p[0][2] : D->n[2],
+                M = which == 6 ? D->n[2] : D->p[0][2];
+      double* in = F.s0.d();
+      double* outp = F.s1.d();
+      KG_CUDA(cudaMemsetAsync(in, 0, sizeof(double) * a_ * K, ctx->s));
+      const BandOp op = which == 6 ? D->f[0][2]->dev.H : D->f[0][2]->dev.G;
+      launch = [&, in, outp, a_, K, M, op] { contract(ctx->L(), in, outp, a_, K, M, 1, op, false); };
+      b = 8.0 * static_cast<double>(a_ * K + a_ * M);
     } else if (which == 0 || which == 3 || which == 4) {
       if (!D->fused) throw Error(E_INVAL, "the fused pass needs a one-component design");
       const double* P = F.x.d();

@@ -81,6 +81,17 @@ def rel(a, b):
     return abs(a - b) / max(abs(b), 1e-300)
 
 
+def unstable_supports(name):
+    """Models whose support differs between the two valid oracle builds of the
+    conditioning probe (C3: the last, least-penalised models 47-48, where a
+    coefficient sits on the soft-threshold boundary to within the 1e-5 floor)."""
+    path = os.path.join(GOLDEN, f"conditioning_{name}.json")
+    if not os.path.exists(path):
+        return set()
+    with open(path) as f:
+        return {r["t"] for r in json.load(f)["rows"] if not r["same_support"]}
+
+
 def coef_tolerance(name, m):
     """Per-model coefficient tolerance: 1e-8 relative (north_star), or 4x the
     conditioning floor where the problem amplifies rounding beyond it -- the
@@ -129,10 +140,17 @@ def test_path_matches_oracle_fixture(name):
     got = res.coefs()
     dev = res.deviance(obs, fam)
     tol = coef_tolerance(name, m)
+    unstable = unstable_supports(name)
     for t in range(m):
         g = got[t]
-        assert np.array_equal(g != 0, supp[t]), f"model {t}: support differs"
-        assert int(np.count_nonzero(g)) == int(fx["nonzero"][t])
+        if t in unstable:
+            # the two oracle builds themselves disagree on this model's support: an
+            # entry may flip only where it is zero within the model's tolerance
+            diff = (g != 0) != supp[t]
+            assert np.all(np.abs(g[diff]) <= tol[t] * float(fx["fingerprints"][t][0])), f"model {t}: support differs"
+        else:
+            assert np.array_equal(g != 0, supp[t]), f"model {t}: support differs"
+            assert int(np.count_nonzero(g)) == int(fx["nonzero"][t])
         if t in want:
             w = want[t]
             scale = max(np.max(np.abs(w)), 1e-300)
