@@ -121,6 +121,9 @@ kg_status kg_design_create(kg_ctx* ctx, int64_t c, int64_t d, const int64_t* n, 
 void kg_design_destroy(kg_design* design);
 int64_t kg_design_n(const kg_design* design); /* n = prod n_j (this shard's slab when sharded) */
 int64_t kg_design_p(const kg_design* design); /* p = sum_r prod_j p_rj */
+/* The design's halo plan on a sharded context (kg_halo_plan layout, out9[0]
+ * = 0: the sharded FISTA loop all-reduces the p-vector instead). */
+kg_status kg_design_halo(const kg_design* design, int64_t* out9);
 /* The cached spectral radius of X_rj^T X_rj. */
 kg_status kg_design_spectral(kg_design* design, int64_t r, int64_t j, double* out);
 
@@ -234,6 +237,22 @@ kg_status kg_bin_scatter(kg_ctx* ctx, int64_t npts, int64_t d, const double* poi
 kg_status kg_bspline_design_dev(kg_ctx* ctx, int64_t npts, const double* points, int64_t order, int64_t n_basis,
                                 int on_device, double* out);
 int64_t kg_linear_index(int64_t d, const int64_t* multi_index, const int64_t* dims); /* array.cpp:22-36; -1 bad */
+/* Halo plan of banded last-mode sharding (band property
+ * bspline.hpp:27-30, G chain design.cpp:104-116).  Rank r of `world` holds
+ * the grid rows [n r / world, n (r + 1) / world) of the last-mode factor X
+ * (n x p, column-major, host memory) and touches the coefficient slices
+ * T_r = [t_lo, t_hi) its rows have nonzeros in.  Coefficient slice j is
+ * OWNED by one rank: [own_lo, own_hi), own_lo = t_lo (0 for rank 0) and
+ * own_hi = the next rank's t_lo (p for the last rank).  Per FISTA gradient
+ * the only exchanges are the boundary slices:
+ *   right halo R = [own_hi, t_hi): this rank's partial of S(x) goes to rank
+ *     r + 1 (which owns it) and the updated x comes back from it;
+ *   left overlap L = [own_lo, t_hi of rank r - 1): the partial of rank r - 1
+ *     arrives and is added, and the updated x goes back to it.
+ * out[9] = {ok, own_lo, own_hi, t_lo, t_hi, L_lo, L_hi, R_lo, R_hi}; ok = 0
+ * when some rank's rows reach beyond its neighbours' owned slices (then the
+ * fit falls back to the p-sized all-reduce).  Host only. */
+kg_status kg_halo_plan(int64_t n, int64_t p, const double* X, int world, int rank, int64_t* out);
 
 /* Held-out selection (mse_heldout, path.cpp:91-126, decl path.hpp:63): for
  * every model of `res`, the sum over cells with mask == 1 of (mean(X theta_t)

@@ -67,4 +67,40 @@ int64_t kg_linear_index(int64_t d, const int64_t* idx, const int64_t* dims) {
   return pos + 1;
 }
 
+kg_status kg_halo_plan(int64_t n, int64_t p, const double* X, int world, int rank, int64_t* out) {
+  if (!X || !out || n < 1 || p < 1 || world < 1 || rank < 0 || rank >= world || n < world) return KG_EINVAL;
+  // touched coefficient range of every rank's rows (rows without nonzeros add nothing)
+  std::vector<int64_t> tlo(world, p), thi(world, 0);
+  for (int r = 0; r < world; ++r) {
+    const int64_t lo = n * r / world, hi = n * (r + 1) / world;
+    for (int64_t i = lo; i < hi; ++i)
+      for (int64_t k = 0; k < p; ++k)
+        if (X[i + n * k] != 0.0) {
+          tlo[r] = std::min(tlo[r], k);
+          thi[r] = std::max(thi[r], k + 1);
+        }
+    if (thi[r] == 0) tlo[r] = thi[r] = (r == 0 ? 0 : thi[r - 1]);
+  }
+  auto own_lo = [&](int r) { return r == 0 ? int64_t(0) : tlo[r]; };
+  auto own_hi = [&](int r) { return r == world - 1 ? p : tlo[r + 1]; };
+  bool ok = true;
+  for (int r = 0; r < world; ++r) {
+    if (own_lo(r) > own_hi(r)) ok = false;        // owned ranges must tile [0, p) in order
+    if (tlo[r] < own_lo(r)) ok = false;           // nothing to the left of the owned range
+    if (r + 1 < world && thi[r] > own_hi(r + 1)) ok = false;  // the right halo stays in the right neighbour
+    if (r + 1 == world && thi[r] > p) ok = false;
+  }
+  const int r = rank;
+  out[0] = ok ? 1 : 0;
+  out[1] = own_lo(r);
+  out[2] = own_hi(r);
+  out[3] = tlo[r];
+  out[4] = thi[r];
+  out[5] = own_lo(r);                                            // L = [own_lo, t_hi(r - 1))
+  out[6] = r > 0 ? std::max(own_lo(r), std::min(thi[r - 1], own_hi(r))) : own_lo(r);
+  out[7] = own_hi(r);                                            // R = [own_hi, t_hi)
+  out[8] = r + 1 < world ? std::max(own_hi(r), thi[r]) : own_hi(r);
+  return KG_OK;
+}
+
 }  // extern "C"

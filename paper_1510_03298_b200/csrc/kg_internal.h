@@ -304,6 +304,8 @@ void ptrials(const Launch& L, i64 p, int pen, double alpha, const double* th, co
              const double* t, double* part);
 void ptheta_update(const Launch& L, i64 p, double t, const double* th_t, double* th);
 void pcopy(const Launch& L, i64 p, const double* src, double* d0, double* d1, double* d2);
+void padd(const Launch& L, i64 n, const double* x, double* y);                 // y += x
+void pmask(const Launch& L, i64 p, i64 lo, i64 hi, double* x);                  // x := 0 outside [lo, hi)
 void pmaxabs(const Launch& L, i64 p, const double* x, double* part);
 // Gram route: per-CTA partials of w <x, S x> - 2 <x, b>
 void gram_dots(const Launch& L, i64 p, double w, const double* x, const double* Sx, const double* b, double* part);

@@ -1177,6 +1177,30 @@ void pcopy(const Launch& L, i64 p, const double* src, double* d0, double* d1, do
   bump(L);
 }
 
+// Halo exchange helpers of banded last-mode sharding: y += x (the left
+// neighbour's partial of S(x) over the overlap), and x := 0 outside [lo, hi)
+// (before the owned-slice all-gather, so the sum over ranks is exact).
+__global__ void __launch_bounds__(NT) k_padd(i64 n, const double* x, double* y) {
+  for (i64 i = static_cast<i64>(blockIdx.x) * NT + threadIdx.x; i < n; i += static_cast<i64>(gridDim.x) * NT)
+    y[i] += x[i];
+}
+
+void padd(const Launch& L, i64 n, const double* x, double* y) {
+  if (n <= 0) return;
+  k_padd<<<pgrid(n), NT, 0, L.s>>>(n, x, y);
+  bump(L);
+}
+
+__global__ void __launch_bounds__(NT) k_pmask(i64 p, i64 lo, i64 hi, double* x) {
+  for (i64 i = static_cast<i64>(blockIdx.x) * NT + threadIdx.x; i < p; i += static_cast<i64>(gridDim.x) * NT)
+    if (i < lo || i >= hi) x[i] = 0.0;
+}
+
+void pmask(const Launch& L, i64 p, i64 lo, i64 hi, double* x) {
+  k_pmask<<<pgrid(p), NT, 0, L.s>>>(p, lo, hi, x);
+  bump(L);
+}
+
 __global__ void __launch_bounds__(NT) k_pmaxabs(i64 p, const double* x, double* part) {
   __shared__ double red[32];
   double m = 0.0;

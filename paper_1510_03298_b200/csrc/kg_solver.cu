@@ -103,6 +103,11 @@ struct NcclApi {
                             cudaStream_t) = nullptr;
   ncclResult_t (*CommDestroy)(ncclComm_t) = nullptr;
   const char* (*GetErrorString)(ncclResult_t) = nullptr;
+  // point-to-point (halo exchange of banded last-mode sharding); optional
+  ncclResult_t (*Send)(const void*, size_t, ncclDataType_t, int, ncclComm_t, cudaStream_t) = nullptr;
+  ncclResult_t (*Recv)(void*, size_t, ncclDataType_t, int, ncclComm_t, cudaStream_t) = nullptr;
+  ncclResult_t (*GroupStart)() = nullptr;
+  ncclResult_t (*GroupEnd)() = nullptr;
 };
 
 static NcclApi* nccl_api() {
@@ -120,6 +125,10 @@ static NcclApi* nccl_api() {
       api.AllReduce = reinterpret_cast<decltype(api.AllReduce)>(dlsym(h, "ncclAllReduce"));
       api.CommDestroy = reinterpret_cast<decltype(api.CommDestroy)>(dlsym(h, "ncclCommDestroy"));
       api.GetErrorString = reinterpret_cast<decltype(api.GetErrorString)>(dlsym(h, "ncclGetErrorString"));
+      api.Send = reinterpret_cast<decltype(api.Send)>(dlsym(h, "ncclSend"));
+      api.Recv = reinterpret_cast<decltype(api.Recv)>(dlsym(h, "ncclRecv"));
+      api.GroupStart = reinterpret_cast<decltype(api.GroupStart)>(dlsym(h, "ncclGroupStart"));
+      api.GroupEnd = reinterpret_cast<decltype(api.GroupEnd)>(dlsym(h, "ncclGroupEnd"));
       if (api.GetUniqueId && api.CommInitRank && api.AllReduce && api.CommDestroy && api.GetErrorString) api.h = h;
     }
   }
@@ -694,6 +703,9 @@ struct kg_design {
   bool fused = false;
   int T = 1;                               // mode-1 fibres per CTA in the fused kernels
   std::unique_ptr<kg::SlabTables> slab;    // d = 3, one component: modes 1+2 fused per slice (kg_slab.cu)
+  // banded last-mode sharding (kg_halo_plan): {ok, own_lo, own_hi, t_lo, t_hi,
+  // L_lo, L_hi, R_lo, R_hi} in coefficient slices of the last mode; ok = 0: all-reduce
+  kg::i64 halo[9] = {0, 0, 0, 0, 0, 0, 0, 0, 0};
   kg::i64 scratch = 0;                     // doubles per chain scratch buffer
   kg::i64 part_cap = 0;                    // doubles in the partials buffer
 };
@@ -868,6 +880,11 @@ struct Fit {
   // (modes 1 and 2 fused per last-mode slice, kg_slab.cu) replaces the
   // mode-1 fused pass and the mode-2 chain steps
   bool slab = false;
+  // banded last-mode sharding for the current fista_solve (kg_design::halo):
+  // the update runs on the owned coefficient slices only and the per-gradient
+  // exchange is the boundary slices with the two neighbours, not a p-sized all-reduce
+  bool halo = false;
+  DBuf htmp;
   // iwls = tensor: the current outer iteration's weighted Gram blocks
   // X_{m,j}^T diag(f_j) X_{r,j} (same band structure as design.gram) and the
   // Lipschitz factor (prod_j rho(G_j(f_j)) for c = 1, max(v) L-hat otherwise)
@@ -929,6 +946,7 @@ static void alloc_fit(Fit& F) {
   F.expand = false;
   if (D.fused && std::getenv("KG_ROUTE0_DIRECT") == nullptr) F.expand = fused_fast_ok(fused_args(F), FV_FISTA_EXP);
   F.slab = F.expand && D.slab && slab_ok(slab_args(F));
+  if (D.halo[0] == 1) F.htmp.alloc(sizeof(double) * std::max<i64>(1, (D.halo[6] - D.halo[5]) * (D.P / D.p[0][D.d - 1])));
   F.tpart.alloc(sizeof(double) * 2 * (1 + kMaxTrials) * pgrid(F.p));
   F.scal.alloc(sizeof(double) * 64);
   F.errs.alloc(sizeof(i64) * 16);
@@ -1088,12 +1106,70 @@ static int gram_pass(Fit& F, const double* x, double* Sx) {
   return pgrid(F.p);
 }
 
+// ------------------------------------------------- halo exchange (8(f) rank 1)
+// Coefficient slices of the last mode are owned by one rank each
+// (kg_halo_plan); a rank's slab touches its owned slices plus the first few of
+// its right neighbour's.  Per gradient: the partial of S(x) over that right
+// halo goes to the right neighbour, the left neighbour's partial over this
+// rank's first slices arrives and is added (own partial + left partial), and
+// after the update the owned x of those first slices goes left while the
+// right halo of x comes back.  ~3 slices (p1 p2 doubles each) per neighbour
+// instead of all p.
+static i64 halo_q(const Fit& F) { return F.D->P / F.D->p[0][F.D->d - 1]; }  // doubles per last-mode slice
+
+static void exch_sx(Fit& F, double* Sx) {
+  kg_ctx* ctx = F.ctx;
+  const i64* h = F.D->halo;
+  const i64 q = halo_q(F), nL = (h[6] - h[5]) * q, nR = (h[8] - h[7]) * q;
+  const NcclApi* api = nccl_api();
+  nccl_check(api->GroupStart(), "ncclGroupStart");
+  if (nR > 0) nccl_check(api->Send(Sx + h[7] * q, nR, ncclFloat64, ctx->rank + 1, ctx->comm, ctx->s), "ncclSend");
+  if (nL > 0) nccl_check(api->Recv(F.htmp.d(), nL, ncclFloat64, ctx->rank - 1, ctx->comm, ctx->s), "ncclRecv");
+  nccl_check(api->GroupEnd(), "ncclGroupEnd");
+  padd(ctx->L(), nL, F.htmp.d(), Sx + h[5] * q);
+}
+
+static void exch_x(Fit& F, double* x) {
+  kg_ctx* ctx = F.ctx;
+  const i64* h = F.D->halo;
+  const i64 q = halo_q(F), nL = (h[6] - h[5]) * q, nR = (h[8] - h[7]) * q;
+  const NcclApi* api = nccl_api();
+  nccl_check(api->GroupStart(), "ncclGroupStart");
+  if (nL > 0) nccl_check(api->Send(x + h[5] * q, nL, ncclFloat64, ctx->rank - 1, ctx->comm, ctx->s), "ncclSend");
+  if (nR > 0) nccl_check(api->Recv(x + h[7] * q, nR, ncclFloat64, ctx->rank + 1, ctx->comm, ctx->s), "ncclRecv");
+  nccl_check(api->GroupEnd(), "ncclGroupEnd");
+}
+
+// every rank's owned slices of x into the full vector on all ranks (exact:
+// one nonzero term per element)
+static void gather_owned(Fit& F, double* x) {
+  const i64 q = halo_q(F);
+  pmask(F.ctx->L(), F.p, F.D->halo[1] * q, F.D->halo[2] * q, x);
+  ar_sum(F.ctx, x, static_cast<size_t>(F.p));
+}
+
+// the monitor's scalars of a halo step in one small all-reduce: scal[40] =
+// sum v eta^2 (slab partials), scal[41..42] = |x|_1, |x|_2^2 and scal[43] =
+// <b, x> over the owned slices
+static void halo_scalars(Fit& F, int n_ss, int n_j, bool ex) {
+  kg_ctx* ctx = F.ctx;
+  reduce_cols(ctx->L(), F.part.d(), n_ss, 1, 0, F.scal.d() + 40);
+  reduce_cols(ctx->L(), F.Jpart.d(), n_j, 2, 0, F.scal.d() + 41);
+  if (ex) reduce_cols(ctx->L(), F.bxpart.d(), n_j, 1, 0, F.scal.d() + 43);
+  else fill(ctx->L(), 1, 0.0, F.scal.d() + 43);
+  ar_sum(ctx, F.scal.d() + 40, 4);
+}
+
 // n-space pass; on a sharded context S(x) and the objective partial are
 // summed over the slabs (one p-sized all-reduce + one scalar per gradient)
 static int xwx_pass(Fit& F, const double* x, double* Sx) {
   const int np = xwx_pass_local(F, x, Sx);
   kg_ctx* ctx = F.ctx;
   if (!sharded(ctx)) return np;
+  if (F.halo) {  // boundary slices only; the caller reduces the partials (halo_scalars)
+    exch_sx(F, Sx);
+    return np;
+  }
   ar_sum(ctx, Sx, static_cast<size_t>(F.p));
   reduce_cols(ctx->L(), F.part.d(), np, 1, 0, F.scal.d() + 40);
   ar_sum(ctx, F.scal.d() + 40, 1);
@@ -1192,6 +1268,17 @@ static void enqueue_body(Fit& F, cudaGraphConditionalHandle h, int use_handle) {
   }
   FistaCtl* c = static_cast<FistaCtl*>(F.ctl.p);
   const bool ex = F.route == 0 && F.expand;
+  if (F.halo) {  // owned slices: update, x halo exchange, local pass + S(x) halo, 4-scalar all-reduce
+    const i64 q = halo_q(F), o0 = F.D->halo[1] * q, on = (F.D->halo[2] - F.D->halo[1]) * q;
+    fista_update(ctx->L(), c, on, F.pen, F.alpha, F.x.d() + o0, F.xp.d() + o0, F.Sx.d() + o0, F.Sxp.d() + o0,
+                 F.b.d() + o0, F.best.d() + o0, F.Sbest.d() + o0, F.Jpart.d(), ex ? F.bxpart.d() : nullptr);
+    exch_x(F, F.x.d());
+    const int n_ss = step_pass(F, F.x.d(), F.Sx.d());
+    halo_scalars(F, n_ss, pgrid(on), ex);
+    fista_control(ctx->L(), c, F.scal.d() + 40, 1, F.scal.d() + 41, 1, h, use_handle,
+                  ex ? F.scal.d() + 43 : nullptr, 1);
+    return;
+  }
   fista_update(ctx->L(), c, F.p, F.pen, F.alpha, F.x.d(), F.xp.d(), F.Sx.d(), F.Sxp.d(), F.b.d(), F.best.d(),
                F.Sbest.d(), F.Jpart.d(), ex ? F.bxpart.d() : nullptr);
   F.n_ss = step_pass(F, F.x.d(), F.Sx.d());
@@ -1416,6 +1503,7 @@ static void fista_enqueue(Fit& F, double lambda, const InnerCfg& ic, const doubl
     fista_bt0(F, lambda, ic, vmax_part, n_vmax);
     return;
   }
+  F.halo = sharded(ctx) && F.D->halo[0] == 1 && F.route == 0 && F.D->c == 1;
   FistaCtl h{};
   h.lambda = lambda;
   h.tol = ic.tol;
@@ -1467,6 +1555,16 @@ static void fista_enqueue(Fit& F, double lambda, const InnerCfg& ic, const doubl
     A.init = 1;
     gram_step(ctx->L(), A);
     pcopy(ctx->L(), F.p, F.Sx.d(), F.Sxp.d(), F.Sbest.d(), nullptr);
+  } else if (F.halo) {
+    const i64 q = halo_q(F), o0 = F.D->halo[1] * q, on = (F.D->halo[2] - F.D->halo[1]) * q;
+    const int n_ss = step_pass(F, F.x.d(), F.Sx.d());
+    pnorm(ctx->L(), on, F.pen, F.alpha, F.x.d() + o0, F.Jpart.d());
+    pcopy(ctx->L(), F.p, F.Sx.d(), F.Sxp.d(), F.Sbest.d(), nullptr);
+    const bool ex = F.expand;
+    if (ex) pdot(ctx->L(), on, F.b.d() + o0, F.x.d() + o0, F.bxpart.d());
+    halo_scalars(F, n_ss, pgrid(on), ex);
+    fista_init(ctx->L(), static_cast<FistaCtl*>(F.ctl.p), F.scal.d() + 40, 1, F.scal.d() + 41, 1, vmax_part, n_vmax,
+               0, ex ? F.scal.d() + 43 : nullptr, 1);
   } else {
     const int n_ss = step_pass(F, F.x.d(), F.Sx.d());
     pnorm(ctx->L(), F.p, F.pen, F.alpha, F.x.d(), F.Jpart.d());
@@ -1504,6 +1602,10 @@ static void fista_enqueue(Fit& F, double lambda, const InnerCfg& ic, const doubl
     }
   }
   fista_finalize(ctx->L(), static_cast<FistaCtl*>(F.ctl.p), F.p, F.x.d(), F.best.d(), F.Sx.d(), F.Sbest.d());
+  if (F.halo) {  // owned slices back into full replicated vectors
+    for (DBuf* v : {&F.x, &F.Sx, &F.best, &F.Sbest}) gather_owned(F, v->d());
+    F.halo = false;
+  }
   KG_CUDA(cudaMemcpyAsync(ctx->pin() + PIN_CTL, F.ctl.p, sizeof(FistaCtl), cudaMemcpyDeviceToHost, ctx->s));
 }
 
@@ -2591,6 +2693,17 @@ kg_status kg_design_create(kg_ctx* ctx, int64_t c, int64_t d, const int64_t* n, 
     }
     if (D->fused && d == 3 && std::getenv("KG_NO_SLAB") == nullptr)
       D->slab = build_slab(factors[1], D->n[1], D->p[0][1], ctx->s);
+    // (KG_HALO=0 keeps the all-reduce; KG_HALO=1 also runs the owned-slice
+    // path on a one-rank communicator, where it has no neighbours: a test hook)
+    const char* he = std::getenv("KG_HALO");
+    if (ctx->comm && (ctx->world > 1 || (he && he[0] == '1')) && c == 1 && d >= 2) {
+      const NcclApi* api = nccl_api();
+      if ((!he || he[0] != '0') && api->Send && api->Recv && api->GroupStart && api->GroupEnd) {
+        int64_t hp[9];
+        if (kg_halo_plan(D->n_full[d - 1], D->p[0][d - 1], factors[d - 1], ctx->world, ctx->rank, hp) == KG_OK)
+          for (int k = 0; k < 9; ++k) D->halo[k] = hp[k];
+      }
+    }
     D->scratch = chain_scratch(*D);
     const i64 tiles = D->fused ? (m + D->T - 1) / D->T : 0;
     const i64 hl_tiles = (m + D->T - 1) / D->T;
@@ -2613,6 +2726,11 @@ void kg_design_destroy(kg_design* d) {
 }
 int64_t kg_design_n(const kg_design* d) { return d->N; }
 int64_t kg_design_p(const kg_design* d) { return d->P; }
+kg_status kg_design_halo(const kg_design* d, int64_t* out9) {
+  if (!d || !out9) return KG_EINVAL;
+  for (int k = 0; k < 9; ++k) out9[k] = d->halo[k];
+  return KG_OK;
+}
 kg_status kg_design_spectral(kg_design* d, int64_t r, int64_t j, double* out) {
   return guarded(d->ctx, [&] {
     if (r < 0 || r >= d->c || j < 0 || j >= d->d) throw Error(E_INVAL, "factor index out of range");
