@@ -196,8 +196,11 @@ __global__ void __launch_bounds__(kSlabBS, 1) k_slab(SlabArgs a) {
             if (r & 1) acc1 = fma(wv[r], x, acc1);
             else acc0 = fma(wv[r], x, acc0);
           }
-          *reinterpret_cast<double2*>(w + ldW * c) = make_double2(wv[0], wv[1]);
-          *reinterpret_cast<double2*>(w + ldW * c + 2) = make_double2(wv[2], wv[3]);
+          // quads 4 apart are 128 bytes apart: the upper half of the quad-group
+          // stores its second 16 bytes first, so a quarter warp hits 8 distinct bank groups
+          const bool sw = (rq >> 2) & 1;
+          *reinterpret_cast<double2*>(w + ldW * c + (sw ? 2 : 0)) = sw ? make_double2(wv[2], wv[3]) : make_double2(wv[0], wv[1]);
+          *reinterpret_cast<double2*>(w + ldW * c + (sw ? 0 : 2)) = sw ? make_double2(wv[0], wv[1]) : make_double2(wv[2], wv[3]);
         }
       }
       nb_arrive(kBarWReady + buf, kSlabBS);

@@ -1,4 +1,5 @@
-"""Summarise an ncu --csv launch list (gpu__time_duration.sum) by kernel."""
+"""Summarise an ncu --csv launch list by kernel: time (gpu__time_duration.sum),
+and, when captured, DRAM bytes (dram__bytes_read.sum + dram__bytes_write.sum)."""
 import collections
 import csv
 import sys
@@ -18,14 +19,21 @@ def load(path):
 
 def main(path):
     data = load(path)
-    agg = collections.defaultdict(list)
+    launches = collections.OrderedDict()  # ID -> {name, metrics}
     for d in data:
-        name = d["Kernel Name"].split("(")[0][:70]
-        agg[name].append(float(d["Metric Value"]))
-    tot = sum(sum(v) for v in agg.values())
-    print(f"{len(data)} launches, {tot / 1000:.1f} us total")
-    for k, v in sorted(agg.items(), key=lambda x: -sum(x[1])):
-        print(f"{k:70s} n={len(v):4d} avg={sum(v) / len(v) / 1000:9.2f} us share={sum(v) / tot:6.1%}")
+        e = launches.setdefault(d["ID"], {"name": d["Kernel Name"].split("(")[0][:70], "m": {}})
+        e["m"][d["Metric Name"]] = float(d["Metric Value"].replace(",", ""))
+    agg = collections.defaultdict(lambda: [0, 0.0, 0.0])
+    for e in launches.values():
+        a = agg[e["name"]]
+        a[0] += 1
+        a[1] += e["m"].get("gpu__time_duration.sum", 0.0)
+        a[2] += e["m"].get("dram__bytes_read.sum", 0.0) + e["m"].get("dram__bytes_write.sum", 0.0)
+    tot = sum(v[1] for v in agg.values()) or 1.0
+    print(f"{len(launches)} launches, {tot / 1000:.1f} us total")
+    for k, (n, t, b) in sorted(agg.items(), key=lambda x: -x[1][1]):
+        extra = f" dram/launch={b / n / 1e6:8.1f} MB {b / (t * 1e-9) / 1e9:6.0f} GB/s" if b else ""
+        print(f"{k:70s} n={n:5d} avg={t / n / 1000:9.2f} us share={t / tot:6.1%}{extra}")
 
 
 if __name__ == "__main__":
