@@ -402,11 +402,14 @@ def run_ours(args):
     e2e_iters, e2e_ms = 0, 0.0
     n_e2e = max(1, min(args.steps, 3))
     if not shard:
-        for i in range(1 + n_e2e):
+        # two untimed calls first: the coefficients land in page-locked blocks that
+        # the library recycles, and a caller holding the previous result uses a
+        # second one, so steady state starts at the third call
+        for i in range(2 + n_e2e):
             torch.cuda.synchronize()
             t0 = time.perf_counter()
             out = K.fit_path(data["design"], fam, y, n_lambda=nl, lambda_min_ratio=ratio)
-            if i >= 1:
+            if i >= 2:
                 e2e_ms += 1000.0 * (time.perf_counter() - t0)
                 e2e_iters += sum(out["inner_iters"])
         n_models = len(out["lambdas"])
