@@ -421,12 +421,12 @@ static FusedPlan plan_for(const FusedArgs& f, int variant) {
   const i64 nB = variant == FV_FISTA_EXP ? 1 : 2;  // staged n-arrays per fibre
   const i64 per_col = (hasP ? f.p1 : 0) + nB * f.n1;
   static const i64 stage_kb = [] {
-    const char* e = std::getenv("KG_FUSED_STAGE_KB");
+    const char* e = dev_env("KG_FUSED_STAGE_KB");
     const long v = e ? std::atol(e) : 48;
     return static_cast<i64>(v >= 4 && v <= 100 ? v : 48);
   }();
   static const int stages = [] {
-    const char* e = std::getenv("KG_FUSED_STAGES");
+    const char* e = dev_env("KG_FUSED_STAGES");
     const int v = e ? std::atoi(e) : 2;
     return v >= 2 && v <= kMaxStages ? v : 2;
   }();
@@ -472,7 +472,7 @@ bool fused_tma_fits(const FusedArgs& f, int variant) {
 // Block size of the register-hoisted fused kernel (KG_FUSED_BS = 256 | 512).
 static int fused_bs() {
   static const int bs = [] {
-    const char* e = std::getenv("KG_FUSED_BS");
+    const char* e = dev_env("KG_FUSED_BS");
     return (e && std::atoi(e) == 512) ? 512 : 256;
   }();
   return bs;
@@ -654,22 +654,22 @@ __global__ void __launch_bounds__(BS) k_fused_mma(FusedArgs f, FusedPlan pl, i64
 static LcPlan lc_plan(const FusedArgs& f) {
   LcPlan P;
   static const bool enabled = [] {
-    const char* e = std::getenv("KG_FUSED_MMA");
+    const char* e = dev_env("KG_FUSED_MMA");
     return e == nullptr || std::atoi(e) != 0;
   }();
   // CTA shape: threads and the shared-memory budget per CTA (measured best on B200:
   // 256 threads, 72 KB, two stages -> three CTAs per SM for C5)
   static const int bs = [] {
-    const char* e = std::getenv("KG_MMA_BS");
+    const char* e = dev_env("KG_MMA_BS");
     return (e && std::atoi(e) == 512) ? 512 : 256;
   }();
   static const i64 budget_kb = [] {
-    const char* e = std::getenv("KG_MMA_KB");
+    const char* e = dev_env("KG_MMA_KB");
     const long v = e ? std::atol(e) : 72;
     return static_cast<i64>(v >= 24 && v <= 210 ? v : 72);
   }();
   static const int nst = [] {
-    const char* e = std::getenv("KG_MMA_STAGES");
+    const char* e = dev_env("KG_MMA_STAGES");
     const int v = e ? std::atoi(e) : 2;
     return v >= 2 && v <= kMaxStages ? v : 2;
   }();

@@ -1489,7 +1489,7 @@ static size_t path_smem(const GramStepArgs& A) {
 // KG_PATH_CW=0 drops the control warp (single-role nu = 1 loop)
 static bool path_cw() {
   static const bool cw = [] {
-    const char* e = std::getenv("KG_PATH_CW");
+    const char* e = dev_env("KG_PATH_CW");
     return e ? e[0] != '0' : kPathCW;
   }();
   return cw;
@@ -1500,7 +1500,7 @@ static bool path_cw() {
 // latency); KG_PATH_BS overrides
 static int path_bs() {
   static const int bs = [] {
-    const char* e = std::getenv("KG_PATH_BS");
+    const char* e = dev_env("KG_PATH_BS");
     const int v = e ? std::atoi(e) : kPathBS;
     if (v == 1024 && path_cw()) return 512;  // 1024 + the control warp exceeds the CTA limit
     if (v == 480 && !path_cw()) return 512;

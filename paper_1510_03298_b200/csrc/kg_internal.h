@@ -4,6 +4,7 @@
 #include <cuda_runtime.h>
 
 #include <cstdint>
+#include <cstdlib>
 #include <stdexcept>
 #include <string>
 #include <vector>
@@ -54,6 +55,19 @@ struct FastDiv {
   __device__ __forceinline__ uint32_t div(uint32_t n) const { return d == 1 ? n : (__umulhi(n, m) >> s); }
 #endif
 };
+
+// Developer switches (tuning sweeps, measurement-only variants, debug traces)
+// are read only when KG_DEV=1, so a production process always runs the
+// default routes.  The two operational switches, KG_HOST_LOOP (drive the FISTA
+// loop from the host so profilers can see its kernels) and KG_HALO (0: keep
+// the p-sized all-reduce on sharded contexts), are read directly.
+inline const char* dev_env(const char* name) {
+  static const bool dev = [] {
+    const char* e = std::getenv("KG_DEV");
+    return e && e[0] == '1';
+  }();
+  return dev ? std::getenv(name) : nullptr;
+}
 
 // ------------------------------------------------------------ band operators
 // One banded operator C (rows x cols): row m has nonzeros at columns

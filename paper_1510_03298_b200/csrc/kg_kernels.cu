@@ -290,7 +290,7 @@ __global__ void __launch_bounds__(NT, RB <= 4 ? 4 : 1) k_contract_gb(const doubl
 }
 
 static bool gb_enabled() {
-  static const bool on = std::getenv("KG_NO_GB") == nullptr;
+  static const bool on = dev_env("KG_NO_GB") == nullptr;
   return on;
 }
 
@@ -352,7 +352,7 @@ __global__ void __launch_bounds__(NT) k_contract_rb(const double* __restrict__ A
 }
 
 static bool rb_enabled() {  // opt-in (KG_RB=1): slower than k_contract_rs on the C5 path so far
-  static const bool on = std::getenv("KG_RB") != nullptr && std::getenv("KG_RB")[0] == '1';
+  static const bool on = dev_env("KG_RB") != nullptr && dev_env("KG_RB")[0] == '1';
   return on;
 }
 
@@ -362,7 +362,7 @@ static void launch_rs(const Launch& L, const double* A, double* out, i64 a, i64 
   const i64 pairs = a * M;
   const i64 gx = (pairs + NT - 1) / NT;
   static const i64 cap = [] {
-    const char* e = std::getenv("KG_RS_BLOCKS");
+    const char* e = dev_env("KG_RS_BLOCKS");
     return e ? std::max<i64>(148, std::atoll(e)) : 148 * 32;
   }();
   // ~cap CTAs; each thread's beta chunk a multiple of the 4-slab pass (no scalar tail)

@@ -392,7 +392,7 @@ static void upload_factor(const FactorHost& h, FactorOwn& f, cudaStream_t s) {
   auto blocked = [&](int RB, int RW, i64 rows, i64 in_ext, const std::vector<int>& blo_r, const std::vector<int>& blen_r,
                      bool transpose, DBuf& dlo, DBuf& dcoef, const int*& olo, const double*& ocoef) {
     const i64 groups = (rows + RB - 1) / RB;
-    bool ok = std::getenv("KG_NO_GB") == nullptr && in_ext >= RW;
+    bool ok = dev_env("KG_NO_GB") == nullptr && in_ext >= RW;
     std::vector<int> wl(static_cast<size_t>(groups), 0);
     std::vector<double> wc(static_cast<size_t>(groups * RB * RW), 0.0);
     for (i64 g = 0; g < groups && ok; ++g) {
@@ -542,7 +542,7 @@ static std::vector<double> spectral_run(kg_ctx* ctx, std::vector<std::unique_ptr
   std::vector<double> res(3 * pj.size());
   KG_CUDA(cudaMemcpyAsync(res.data(), out.p, sizeof(double) * res.size(), cudaMemcpyDeviceToHost, ctx->s));
   sync(ctx);
-  static const bool trace = std::getenv("KG_POWER_TRACE") != nullptr;
+  static const bool trace = dev_env("KG_POWER_TRACE") != nullptr;
   for (size_t k = 0; k < pj.size(); ++k) {
     if (trace)
       std::fprintf(stderr, "kg power job %zu: p=%lld band=%d value=%.17g iterations=%.0f\n", k,
@@ -618,7 +618,7 @@ static std::unique_ptr<SpectralPending> spectral_launch(kg_ctx* ctx, std::vector
 
 static std::vector<double> spectral_collect(SpectralPending& S) {
   if (S.done) KG_CUDA(cudaEventSynchronize(S.done));
-  static const bool trace = std::getenv("KG_POWER_TRACE") != nullptr;
+  static const bool trace = dev_env("KG_POWER_TRACE") != nullptr;
   for (size_t k = 0; k < S.pj.size(); ++k) {
     if (trace)
       std::fprintf(stderr, "kg power job %zu: p=%lld band=%d value=%.17g iterations=%.0f\n", k,
@@ -729,7 +729,7 @@ static void upload(kg_ctx* ctx, void* dst, const void* src, size_t bytes) {
   cudaPointerAttributes at{};
   const bool pageable = cudaPointerGetAttributes(&at, src) == cudaSuccess && at.type == cudaMemoryTypeUnregistered;
   cudaGetLastError();
-  if (!pageable || bytes < 2 * kStageChunk || std::getenv("KG_NO_STAGE")) {
+  if (!pageable || bytes < 2 * kStageChunk || dev_env("KG_NO_STAGE")) {
     KG_CUDA(cudaMemcpyAsync(dst, src, bytes, cudaMemcpyHostToDevice, ctx->s));
     return;
   }
@@ -944,7 +944,7 @@ static void alloc_fit(Fit& F) {
   F.Jpart.alloc(sizeof(double) * 2 * pgrid(F.p));
   F.bxpart.alloc(sizeof(double) * pgrid(F.p));
   F.expand = false;
-  if (D.fused && std::getenv("KG_ROUTE0_DIRECT") == nullptr) F.expand = fused_fast_ok(fused_args(F), FV_FISTA_EXP);
+  if (D.fused && dev_env("KG_ROUTE0_DIRECT") == nullptr) F.expand = fused_fast_ok(fused_args(F), FV_FISTA_EXP);
   F.slab = F.expand && D.slab && slab_ok(slab_args(F));
   if (D.halo[0] == 1) F.htmp.alloc(sizeof(double) * std::max<i64>(1, (D.halo[6] - D.halo[5]) * (D.P / D.p[0][D.d - 1])));
   F.tpart.alloc(sizeof(double) * 2 * (1 + kMaxTrials) * pgrid(F.p));
@@ -2045,7 +2045,7 @@ static ModelTrace outer_loop(Fit& F, double lambda, const OuterCfg& oc) {
     // cell.  Rejections fall through to the batched trial passes below, which
     // compute the same per-trial sums (KG_TRIALS0 sets the first batch size).
     static const int first_batch = [] {
-      const char* e = std::getenv("KG_TRIALS0");
+      const char* e = dev_env("KG_TRIALS0");
       const int v = e ? std::atoi(e) : 1;
       return v < 1 ? 1 : (v > kMaxTrials ? kMaxTrials : v);
     }();
@@ -2288,7 +2288,7 @@ static kg_path_result* fit_path(kg_ctx* ctx, const kg_design* D, const kg_obs* O
   // Gaussian, constant weights, one component: the whole path in one cooperative launch
   if (!single_solve && gauss_shortcut && F->route == 1 && F->gstep && !host_loop_mode() && oc.inner.max_iters >= 1 &&
       oc.inner.nu != 0.0 &&
-      std::getenv("KG_NO_DEVICE_PATH") == nullptr && gauss_path_ok(gstep_args(*F))) {
+      dev_env("KG_NO_DEVICE_PATH") == nullptr && gauss_path_ok(gstep_args(*F))) {
     if (!(F->wconst > 0.0)) throw Error(E_INVAL, "lipschitz_upper: weights must not be all zero");
     if (!(oc.inner.nu >= 0.0 && oc.inner.nu <= 1.0)) throw Error(E_INVAL, "fista_solve: nu must lie in [0,1]");
     FistaCtl h{};
@@ -2335,7 +2335,7 @@ static kg_path_result* fit_path(kg_ctx* ctx, const kg_design* D, const kg_obs* O
     P.iters_out = static_cast<i64*>(its.p);
     P.status_out = static_cast<int*>(stat.p) + 2;
     P.nmodels = static_cast<int*>(stat.p);
-    if (const char* e = std::getenv("KG_PATH_DBG")) P.dbg = std::atoi(e);
+    if (const char* e = dev_env("KG_PATH_DBG")) P.dbg = std::atoi(e);
     if (!ctx->ev[0]) {
       KG_CUDA(cudaEventCreate(&ctx->ev[0]));
       KG_CUDA(cudaEventCreate(&ctx->ev[1]));
@@ -2691,7 +2691,7 @@ kg_status kg_design_create(kg_ctx* ctx, int64_t c, int64_t d, const int64_t* n, 
       while (T > 1 && (n1 + p1) * T * 8 > 96 * 1024) --T;
       D->T = static_cast<int>(T);
     }
-    if (D->fused && d == 3 && std::getenv("KG_NO_SLAB") == nullptr)
+    if (D->fused && d == 3 && dev_env("KG_NO_SLAB") == nullptr)
       D->slab = build_slab(factors[1], D->n[1], D->p[0][1], ctx->s);
     // (KG_HALO=0 keeps the all-reduce; KG_HALO=1 also runs the owned-slice
     // path on a one-rank communicator, where it has no neighbours: a test hook)
@@ -3271,7 +3271,7 @@ kg_status kg_bin_scatter(kg_ctx* ctx, int64_t npts, int64_t d, const double* poi
     BinArgs A;
     A.d = static_cast<int>(d);
     A.npts = npts;
-    static const int bin_mode = [] { const char* e = std::getenv("KG_BIN_MODE"); return e ? std::atoi(e) : 0; }();
+    static const int bin_mode = [] { const char* e = dev_env("KG_BIN_MODE"); return e ? std::atoi(e) : 0; }();
     A.mode = bin_mode;
     A.cells = 1;
     for (int64_t j = 0; j < d; ++j) {

@@ -4,6 +4,7 @@ import os
 import sys
 import time
 
+os.environ.setdefault("KG_DEV", "1")
 os.environ.setdefault("KG_POWER_TRACE", "1")
 sys.path.insert(0, os.path.dirname(os.path.dirname(os.path.abspath(__file__))))
 from paper_1510_03298_b200 import configs  # noqa: E402
