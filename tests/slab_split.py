@@ -1,4 +1,4 @@
-"""Host-side plan for sharding the observation array along its LAST mode
+"""Test-only host-side slab split for sharding the observation array along its LAST mode
 (SURVEY.md §8(e)), the same slicing kg_design_create applies per rank:
 rank g owns the contiguous slab [lo_g, hi_g) of mode d, i.e. rows lo_g..hi_g of
 X_d, and the flat cells [cell_base_g, cell_base_g + n_g) of every n-array.

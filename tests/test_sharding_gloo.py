@@ -11,7 +11,7 @@ import torch.distributed as dist
 import torch.multiprocessing as mp
 
 from oracle import oracle as O
-from paper_1510_03298_b200 import sharding as S
+from tests import slab_split as S
 
 ROOT = os.path.dirname(os.path.dirname(os.path.abspath(__file__)))
 
