@@ -529,10 +529,35 @@ __global__ void __launch_bounds__(NT) k_hlast(HlastArgs h) {
   double acc[kHlastCols];
 #pragma unroll
   for (int q = 0; q < kHlastCols; ++q) acc[q] = 0.0;
+  // a thread keeps one grid row when n1 divides the block: its (<= 4) band
+  // coefficients live in registers, zero-padded at the end, so the sequential
+  // FMA chain is band_dot's to the bit
+  const bool fixed_row = h.P && (NT % n1) == 0 && h.H.maxlen <= 4;
+  const int frow = threadIdx.x % n1;
+  int flo = 0;
+  bool fast_row = false;
+  double fc[4] = {0.0, 0.0, 0.0, 0.0};
+  if (fixed_row) {
+    flo = __ldg(h.H.lo + frow);
+    fast_row = flo <= p1 - 4;  // the 4-wide window fits in the tile row
+    const int len = __ldg(h.H.len + frow);
+    const double* cf = h.H.coef + __ldg(h.H.off + frow);
+#pragma unroll
+    for (int t = 0; t < 4; ++t) fc[t] = (t < len) ? __ldg(cf + t) : 0.0;
+  }
   for (int e = threadIdx.x; e < n1 * Tc; e += NT) {
     const i64 g = base + e;
     double en;
-    if (h.P) {
+    if (fixed_row) {
+      const double* pc = sm + (e / n1) * p1;
+      if (fast_row) {  // zeros after the band: fma(0, p, s) == s
+        const double* q = pc + flo;
+        en = fma(fc[3], q[3], fma(fc[2], q[2], fma(fc[1], q[1], fma(fc[0], q[0], 0.0))));
+      } else {
+        en = band_dot(h.H, frow, [&](int k) { return pc[k]; });
+      }
+      if (h.flags & HL_WRITE) h.eta_new[g] = en;
+    } else if (h.P) {
       const int col = e / n1;
       const int i = e - col * n1;
       const double* pc = sm + col * p1;

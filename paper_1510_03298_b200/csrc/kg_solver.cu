@@ -1014,7 +1014,11 @@ static HlastArgs hlast_args(const Fit& F) {
   h.n1 = D.n[0];
   h.p1 = D.p[0][0];
   h.m = D.N / D.n[0];
+  // longer tiles than the fused kernels': a CTA's P-tile load and barrier are
+  // amortised over 4x the cells (P tile <= 48 KB; fewer partials than part_cap)
   h.T = D.T;
+  while (h.T * 2 <= 4 * D.T && D.p[0][0] * h.T * 2 * 8 <= 48 * 1024 && (h.m + h.T * 2 - 1) / (h.T * 2) >= 2 * 148)
+    h.T *= 2;
   h.H = D.f[0][0]->dev.H;
   h.y = F.O->y.d();
   h.a = F.O->a_const ? nullptr : F.O->a.d();  // constant prior weights are not streamed
