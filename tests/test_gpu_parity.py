@@ -485,3 +485,39 @@ def test_tensor_weights_match_oracle(case):
         fam = "poisson"
     kw = dict(n_lambda=6, lambda_min_ratio=1e-2, iwls="tensor")
     compare_paths(K.fit_path(design, fam, y, **kw), O.fit_path(design, fam, y, **kw))
+
+
+def _slab_route_taken(design, y):
+    """kg_time_kernel(which=6) runs only on a design whose fits take the slab route."""
+    import ctypes as C
+    from paper_1510_03298_b200 import _lib
+    ctx = K.Context(0)
+    D = K.Design(design, ctx)
+    obs = K.Observation(D, y)
+    ms, b = C.c_double(), C.c_double()
+    st = _lib.load().kg_time_kernel(ctx.h, D.h, obs.h, 6, 1, C.byref(ms), C.byref(b))
+    ctx.close()
+    return st == 0
+
+
+@pytest.mark.parametrize("n,p", [((60, 52, 30), (14, 12, 8)),    # tail chunk (52 = 6 x 8 + 4), p1 not a multiple of 8
+                                 ((32, 72, 24), (10, 20, 7)),    # several column groups (n1 = 32), p2 = 20
+                                 ((128, 40, 17), (32, 10, 6))])  # odd last mode, two DMMA row groups x 4
+def test_slab_route_poisson_paths_match_oracle(n, p):
+    """The slab pass (k_slab: modes 1 and 2 of X^T W X fused per last-mode
+    slice) on irregular shapes -- a partial last chunk of mode-2 rows, p1 with
+    padded DMMA row groups, several row-thread column groups -- against the
+    oracle's Poisson path (same supports, coefficients, objectives and
+    iteration counts)."""
+    rng = np.random.default_rng(sum(n) + sum(p))
+    design = bspline_design(n, p)
+    B = np.zeros(p)
+    m = rng.random(p) < 0.15
+    B[m] = rng.standard_normal(m.sum())
+    eta = configs.tensor_h(design[0], B)
+    y = rng.poisson(np.exp(np.log(20.0) / max(eta.max(), 1e-3) * eta)).astype(float)
+    assert _slab_route_taken(design, y), "this shape should run the slab route"
+    kw = dict(n_lambda=8, lambda_min_ratio=1e-2)
+    got = K.fit_path(design, "poisson", y, **kw)
+    want = O.fit_path(design, "poisson", y, **kw)
+    compare_paths(got, want)
