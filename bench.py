@@ -82,15 +82,18 @@ def world_info():
 
 
 def sharded_mode(args, world):
-    return world > 1 and not args.replicas
+    # --shard at N = 1 runs the sharded machinery on one rank (NCCL communicator,
+    # host-driven loop, owned-slice path with KG_HALO=1): a single-GPU check
+    return (world > 1 or args.shard) and not args.replicas
 
 
 def config_obj(args, data, world):
     """The workload description, identical in both arms (the driver compares them)."""
-    if world == 1:
+    if world == 1 and not args.shard:
         par = "single GPU"
     elif sharded_mode(args, world):
-        par = f"last-mode shards x{world} (NCCL all-reduce per gradient)"
+        par = (f"last-mode shards x{world} (per gradient: NCCL send/recv of the ~3 boundary coefficient "
+               f"slices with each neighbour + a 4-double all-reduce)")
     else:
         par = f"replicas x{world}"
     return {"workload": args.config, "family": data["family"], "n": list(data["n"]), "p": list(data["p"]),
@@ -287,7 +290,8 @@ def run_ours(args):
     if shard:
         uid = K.nccl_unique_id() if rank == 0 else None
         box = [uid]
-        dist.broadcast_object_list(box, src=0)
+        if world > 1:
+            dist.broadcast_object_list(box, src=0)
         ctx = K.Context.sharded(local, rank, world, box[0])
         lo, hi = K.shard_rows(data["n"][-1], rank, world)
         y = np.asfortranarray(y[..., lo:hi])
@@ -420,7 +424,8 @@ def run_ours(args):
         n_models = len(out["lambdas"])
     else:  # sharded: the slab upload + path + coefficient download through the same objects
         torch.cuda.synchronize()
-        dist.barrier()
+        if world > 1:
+            dist.barrier()
         for i in range(n_e2e):
             t0 = time.perf_counter()
             o2 = K.Observation(design, y)
@@ -429,9 +434,10 @@ def run_ours(args):
             e2e_ms += 1000.0 * (time.perf_counter() - t0)
             e2e_iters += sum(r2.inner_iters)
             n_models = r2.n_models
-        t = torch.tensor([e2e_ms], dtype=torch.float64, device="cuda")
-        dist.all_reduce(t, op=dist.ReduceOp.MAX)
-        e2e_ms = float(t.item())
+        if world > 1:
+            t = torch.tensor([e2e_ms], dtype=torch.float64, device="cuda")
+            dist.all_reduce(t, op=dist.ReduceOp.MAX)
+            e2e_ms = float(t.item())
     h2d = 8 * (y.size + sum(x.size for x in data["design"][0]))
     d2h = 8 * design.p * n_models
 

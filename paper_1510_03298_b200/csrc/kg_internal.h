@@ -318,7 +318,10 @@ void ptrials(const Launch& L, i64 p, int pen, double alpha, const double* th, co
              const double* t, double* part);
 void ptheta_update(const Launch& L, i64 p, double t, const double* th_t, double* th);
 void pcopy(const Launch& L, i64 p, const double* src, double* d0, double* d1, double* d2);
-void padd(const Launch& L, i64 n, const double* x, double* y);                 // y += x
+void padd(const Launch& L, i64 n, const double* x, double* y);
+// {sum ss_part, sum J_part[2r], sum J_part[2r+1], sum bx_part} into out[0..3] (one CTA, fixed order)
+void sums4(const Launch& L, const double* ss_part, int n_ss, const double* J_part, int n_J, const double* bx_part,
+           int n_bx, double* out);                 // y += x
 void pmask(const Launch& L, i64 p, i64 lo, i64 hi, double* x);                  // x := 0 outside [lo, hi)
 void pmaxabs(const Launch& L, i64 p, const double* x, double* part);
 // Gram route: per-CTA partials of w <x, S x> - 2 <x, b>

@@ -1378,6 +1378,23 @@ __device__ void cta_sums4(const double* ss_part, int n_ss, const double* J_part,
   for (int k = 0; k < 4; ++k) out[k] = sh[128 + k];
 }
 
+// The four objective pieces of a halo-sharded FISTA step in one launch:
+// out = {sum ss_part, sum J_part[2r], sum J_part[2r+1], sum bx_part} (bx 0 if null).
+__global__ void __launch_bounds__(CT) k_sums4(const double* ss_part, int n_ss, const double* J_part, int n_J,
+                                              const double* bx_part, int n_bx, double* out) {
+  __shared__ double sh[132];
+  double s4[4];
+  cta_sums4(ss_part, n_ss, J_part, n_J, bx_part, n_bx, sh, s4);
+  if (threadIdx.x == 0)
+    for (int k = 0; k < 4; ++k) out[k] = s4[k];
+}
+
+void sums4(const Launch& L, const double* ss_part, int n_ss, const double* J_part, int n_J, const double* bx_part,
+           int n_bx, double* out) {
+  k_sums4<<<1, CT, 0, L.s>>>(ss_part, n_ss, J_part, n_J, bx_part, n_bx, out);
+  bump(L);
+}
+
 __global__ void __launch_bounds__(CT) k_fista_init(FistaCtl* c, const double* ss_part, int n_ss, const double* J_part,
                                                    int n_J, const double* vmax_part, int n_vmax, int bt_always,
                                                    const double* bx_part, int n_bx) {

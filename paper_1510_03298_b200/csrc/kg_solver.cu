@@ -175,6 +175,7 @@ struct kg_ctx {
   cudaStream_t side = nullptr;  // design-time power iterations, overlapped with the observation upload
   void* stage = nullptr;        // page-locked upload ring (kStageLanes x kStageSlots x kStageChunk bytes)
   cudaEvent_t stage_ev[16] = {};
+  cudaEvent_t loop_ev[2] = {nullptr, nullptr};  // pipelined host loop of sharded n-space solves
   kg::Launch L() { return {s, &launches}; }
   double* pin() { return static_cast<double*>(pinned); }
 };
@@ -200,6 +201,8 @@ constexpr int PIN_SCAL = 0;    // [0, 64): reduced scalars
 constexpr int PIN_ERR = 64;    // [64, 96): error words (i64)
 constexpr int PIN_CTL = 128;   // FistaCtl read back
 constexpr int PIN_STAGE = 256; // FistaCtl staged for upload
+constexpr int PIN_CTL2 = 384;  // second FistaCtl read-back slot (pipelined host loop)
+static_assert(sizeof(FistaCtl) <= 1024, "a FistaCtl must fit one pinned slot");
 constexpr int ERR_FAM = 12;    // errs[12], errs[13]: family score / working response
 }  // namespace kg
 
@@ -1157,10 +1160,7 @@ static void gather_owned(Fit& F, double* x) {
 // <b, x> over the owned slices
 static void halo_scalars(Fit& F, int n_ss, int n_j, bool ex) {
   kg_ctx* ctx = F.ctx;
-  reduce_cols(ctx->L(), F.part.d(), n_ss, 1, 0, F.scal.d() + 40);
-  reduce_cols(ctx->L(), F.Jpart.d(), n_j, 2, 0, F.scal.d() + 41);
-  if (ex) reduce_cols(ctx->L(), F.bxpart.d(), n_j, 1, 0, F.scal.d() + 43);
-  else fill(ctx->L(), 1, 0.0, F.scal.d() + 43);
+  sums4(ctx->L(), F.part.d(), n_ss, F.Jpart.d(), n_j, ex ? F.bxpart.d() : nullptr, n_j, F.scal.d() + 40);
   ar_sum(ctx, F.scal.d() + 40, 4);
 }
 
@@ -1590,11 +1590,40 @@ static void fista_enqueue(Fit& F, double lambda, const InnerCfg& ic, const doubl
       const FistaCtl* hc = reinterpret_cast<const FistaCtl*>(ctx->pin() + PIN_CTL);
       const int batch = host_loop_mode() ? 1 : kHostBatch;
       const i64 before = ctx->launches;
-      for (;;) {
+      KG_CUDA(cudaMemcpyAsync(ctx->pin() + PIN_CTL, F.ctl.p, sizeof(FistaCtl), cudaMemcpyDeviceToHost, ctx->s));
+      sync(ctx);
+      if (!hc->done && host_loop_mode()) {
+        for (;;) {  // profiling: one step per host round trip
+          for (int k = 0; k < batch; ++k) enqueue_body(F, cudaGraphConditionalHandle{}, 0);
+          KG_CUDA(cudaMemcpyAsync(ctx->pin() + PIN_CTL, F.ctl.p, sizeof(FistaCtl), cudaMemcpyDeviceToHost, ctx->s));
+          sync(ctx);
+          if (hc->done) break;
+        }
+      } else if (!hc->done) {
+        // Two batches in flight: batch j is enqueued before the host looks at
+        // the control block read back after batch j - 1, so the GPU never
+        // drains at a batch boundary.  Steps past the stop are no-ops for the
+        // state (update and control check done; x unchanged), and every rank
+        // enqueues the same collectives.
+        for (cudaEvent_t& e : ctx->loop_ev)
+          if (!e) KG_CUDA(cudaEventCreateWithFlags(&e, cudaEventDisableTiming));
+        const FistaCtl* slot[2] = {reinterpret_cast<const FistaCtl*>(ctx->pin() + PIN_CTL),
+                                   reinterpret_cast<const FistaCtl*>(ctx->pin() + PIN_CTL2)};
+        auto issue = [&](int j) {
+          for (int k = 0; k < batch; ++k) enqueue_body(F, cudaGraphConditionalHandle{}, 0);
+          KG_CUDA(cudaMemcpyAsync(const_cast<FistaCtl*>(slot[j & 1]), F.ctl.p, sizeof(FistaCtl),
+                                  cudaMemcpyDeviceToHost, ctx->s));
+          KG_CUDA(cudaEventRecord(ctx->loop_ev[j & 1], ctx->s));
+        };
+        issue(0);
+        for (int j = 1;; ++j) {
+          issue(j);
+          KG_CUDA(cudaEventSynchronize(ctx->loop_ev[(j - 1) & 1]));
+          if (slot[(j - 1) & 1]->done) break;
+        }
+        sync(ctx);  // the batch still in flight only repeats the stopped state
         KG_CUDA(cudaMemcpyAsync(ctx->pin() + PIN_CTL, F.ctl.p, sizeof(FistaCtl), cudaMemcpyDeviceToHost, ctx->s));
         sync(ctx);
-        if (hc->done) break;
-        for (int k = 0; k < batch; ++k) enqueue_body(F, cudaGraphConditionalHandle{}, 0);
       }
       // fista_read() adds iterations * kernels_per_iter; undo the direct count
       const i64 its = hc->iterations;
@@ -2538,6 +2567,8 @@ void kg_ctx_destroy(kg_ctx* ctx) {
   if (ctx->comm) nccl_api()->CommDestroy(ctx->comm);
   if (ctx->pinned) cudaFreeHost(ctx->pinned);
   for (cudaEvent_t e : ctx->ev)
+    if (e) cudaEventDestroy(e);
+  for (cudaEvent_t e : ctx->loop_ev)
     if (e) cudaEventDestroy(e);
   if (ctx->s) {
     {
