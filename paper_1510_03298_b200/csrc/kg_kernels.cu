@@ -616,47 +616,72 @@ void hlast_mode1(const Launch& L, const HlastArgs& h) {
 __global__ void __launch_bounds__(NT) k_family(FamilyArgs f) {
   __shared__ double red[32];
   double vmax = -DBL_MAX;
-  for (i64 i = static_cast<i64>(blockIdx.x) * NT + threadIdx.x; i < f.n; i += static_cast<i64>(gridDim.x) * NT) {
-    const double yy = f.y[i], aa = f.a ? f.a[i] : f.a_val, e = f.eta[i], ec = clampe(e);
-    const double u = score_of(f.fam, yy, aa, e) / f.disp;
-    if (!isfinite(u)) record_min(f.err + 0, f.cell_base + i);
-    if (f.u) f.u[i] = u;
-    double v, z;
-    if (f.mode == 1) {  // unit weights, generic working response (outer.cpp:148-155)
-      v = 1.0;
-      z = u / v + e;
+  auto cell = [&](i64 i, double yy, double aa, double e) {
+    const double ec = clampe(e);
+    double u, v, z;
+    if (f.fam == 2 && f.mode != 1) {  // Poisson, exact weights: one exp(clamp(eta)) serves score, weight and z
+      const double mu = exp(ec);
+      u = aa * (yy - mu) / f.disp;   // score_of (family.cpp:164-196)
+      v = fmax(mu, kFloor) / f.disp;
+      z = aa * (yy - mu) / fmax(mu, kFloor) + e;
     } else {
-      double w = 1.0;
-      if (f.fam == 1) {
-        const double mu = logistic(e);
-        w = mu * (1.0 - mu);
-      } else if (f.fam == 2) {
-        w = exp(ec);
+      u = score_of(f.fam, yy, aa, e) / f.disp;
+      if (f.mode == 1) {  // unit weights, generic working response (outer.cpp:148-155)
+        v = 1.0;
+        z = u / v + e;
+      } else {
+        double w = 1.0;
+        if (f.fam == 1) {
+          const double mu = logistic(e);
+          w = mu * (1.0 - mu);
+        } else if (f.fam == 2) {
+          w = exp(ec);
+        }
+        v = fmax(w, kFloor) / f.disp;
+        switch (f.fam) {
+          case 0: z = aa * (yy - e) + e; break;
+          case 1: {
+            const double mu = logistic(ec);
+            z = aa * (yy - mu) / fmax(mu * (1.0 - mu), kFloor) + e;
+            break;
+          }
+          case 2: {
+            const double mu = exp(ec);
+            z = aa * (yy - mu) / fmax(mu, kFloor) + e;
+            break;
+          }
+          default: {
+            const double mu = exp(ec);
+            z = aa * (yy - mu) / mu + e;
+            break;
+          }
+        }
       }
-      v = fmax(w, kFloor) / f.disp;
-      switch (f.fam) {
-        case 0: z = aa * (yy - e) + e; break;
-        case 1: {
-          const double mu = logistic(ec);
-          z = aa * (yy - mu) / fmax(mu * (1.0 - mu), kFloor) + e;
-          break;
-        }
-        case 2: {
-          const double mu = exp(ec);
-          z = aa * (yy - mu) / fmax(mu, kFloor) + e;
-          break;
-        }
-        default: {
-          const double mu = exp(ec);
-          z = aa * (yy - mu) / mu + e;
-          break;
-        }
-      }
-      if (!isfinite(z)) record_min(f.err + 1, f.cell_base + i);
     }
+    if (!isfinite(u)) record_min(f.err + 0, f.cell_base + i);
+    if (f.mode != 1 && !isfinite(z)) record_min(f.err + 1, f.cell_base + i);
+    if (f.u) f.u[i] = u;
     f.v[i] = v;
     f.z[i] = z;
     vmax = fmax(vmax, v);
+  };
+  // four cells per thread and trip, their loads issued together
+  const i64 G = static_cast<i64>(gridDim.x) * NT;
+  for (i64 i0 = static_cast<i64>(blockIdx.x) * NT + threadIdx.x; i0 < f.n; i0 += 4 * G) {
+    double yy[4], aa[4], ee[4];
+#pragma unroll
+    for (int k = 0; k < 4; ++k) {
+      const i64 i = i0 + k * G;
+      yy[k] = aa[k] = ee[k] = 0.0;
+      if (i < f.n) {
+        yy[k] = __ldcs(f.y + i);
+        ee[k] = __ldcs(f.eta + i);
+        aa[k] = f.a ? __ldcs(f.a + i) : f.a_val;
+      }
+    }
+#pragma unroll
+    for (int k = 0; k < 4; ++k)
+      if (i0 + k * G < f.n) cell(i0 + k * G, yy[k], aa[k], ee[k]);
   }
   const double m = block_reduce<true>(vmax, red);
   if (threadIdx.x == 0) f.partial[blockIdx.x] = m;
