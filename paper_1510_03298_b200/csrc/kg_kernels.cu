@@ -545,8 +545,24 @@ __global__ void __launch_bounds__(NT) k_hlast(HlastArgs h) {
 #pragma unroll
     for (int t = 0; t < 4; ++t) fc[t] = (t < len) ? __ldg(cf + t) : 0.0;
   }
+  // the global operands of a cell are loaded one cell ahead (software pipeline)
+  const bool need_y = (h.flags & (HL_LL_NEW | HL_DOT | HL_TRIALS)) != 0;
+  const bool need_eo = (h.flags & (HL_DOT | HL_TRIALS)) != 0;
+  double nyy = 0.0, naa = h.a_val, neo = 0.0;
+  auto fetch = [&](int e) {
+    if (e >= n1 * Tc) return;
+    const i64 g = base + e;
+    if (need_y) {
+      nyy = __ldcs(h.y + g);
+      if (h.a) naa = __ldcs(h.a + g);
+    }
+    if (need_eo) neo = __ldcs(h.eta_old + g);
+  };
+  fetch(threadIdx.x);
   for (int e = threadIdx.x; e < n1 * Tc; e += NT) {
     const i64 g = base + e;
+    const double cyy = nyy, caa = naa, ceo = neo;
+    fetch(e + NT);
     double en;
     if (fixed_row) {
       const double* pc = sm + (e / n1) * p1;
@@ -566,15 +582,15 @@ __global__ void __launch_bounds__(NT) k_hlast(HlastArgs h) {
     } else {
       en = __ldg(h.eta_new + g);
     }
-    if (h.flags & (HL_LL_NEW | HL_DOT | HL_TRIALS)) {
-      const double yy = __ldg(h.y + g), aa = h.a ? __ldg(h.a + g) : h.a_val;
+    if (need_y) {
+      const double yy = cyy, aa = caa;
       if ((h.flags & HL_LL_NEW) && aa != 0.0) {
         const double t = ll_term(h.fam, yy, aa, en);
         if (!isfinite(t)) record_min(h.err + 0, h.cell_base + g);
         acc[0] += t;
       }
-      if (h.flags & (HL_DOT | HL_TRIALS)) {
-        const double eo = __ldg(h.eta_old + g);
+      if (need_eo) {
+        const double eo = ceo;
         if (h.flags & HL_DOT) {
           double u;
           if (h.flags & HL_U_FLY) {
