@@ -858,8 +858,28 @@ __global__ void __launch_bounds__(NT) k_fista_update(const FistaCtl* __restrict_
   const int copy_best = ctl->copy_best, restart = ctl->restart;
   const double gamma = __dmul_rn(delta, lambda);
   double l1 = 0.0, l2 = 0.0, bx = 0.0;
-  for (i64 i = static_cast<i64>(blockIdx.x) * NT + threadIdx.x; i < p; i += static_cast<i64>(gridDim.x) * NT) {
-    double xi = x[i], xpi = xp[i], sxi = Sx[i], sxpi = Sxp[i];
+  // the thread's elements in grid-stride order (so the partials are summed in
+  // the same order), four per trip with their loads issued together
+  const i64 G = static_cast<i64>(gridDim.x) * NT;
+  for (i64 i0 = static_cast<i64>(blockIdx.x) * NT + threadIdx.x; i0 < p; i0 += 4 * G) {
+    double lx[4], lxp[4], lsx[4], lsxp[4], lb[4];
+#pragma unroll
+    for (int k = 0; k < 4; ++k) {
+      const i64 i = i0 + k * G;
+      if (i < p) {
+        lx[k] = x[i];
+        lxp[k] = xp[i];
+        lsx[k] = Sx[i];
+        lsxp[k] = Sxp[i];
+        lb[k] = b[i];
+      }
+    }
+#pragma unroll
+    for (int k = 0; k < 4; ++k) {
+    const i64 i = i0 + k * G;
+    if (i >= p) break;
+    double xi = lx[k], xpi = lxp[k], sxi = lsx[k], sxpi = lsxp[k];
+    const double bi = lb[k];
     if (copy_best) {
       best[i] = xi;
       Sbest[i] = sxi;
@@ -870,14 +890,15 @@ __global__ void __launch_bounds__(NT) k_fista_update(const FistaCtl* __restrict_
     }
     const double yi = xi + omega * (xi - xpi);
     const double syi = sxi + omega * (sxi - sxpi);
-    const double g = (sscale * syi - b[i]) / n;
+    const double g = (sscale * syi - bi) / n;
     double ci = __dsub_rn(yi, __dmul_rn(delta, g));
     if (lambda > 0.0) ci = prox1(pen, alpha, gamma, ci);
     xp[i] = xi;
     x[i] = ci;
     Sxp[i] = sxi;
     jacc(ci, l1, l2);
-    if (bxpart) bx = fma(b[i], ci, bx);
+    if (bxpart) bx = fma(bi, ci, bx);
+    }
   }
   const double s1 = block_reduce<false>(l1, red);
   const double s2 = block_reduce<false>(l2, red);
