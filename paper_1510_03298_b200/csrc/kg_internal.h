@@ -301,6 +301,7 @@ void deviance_pass(const Launch& L, i64 n, int fam, const double* y, const doubl
 
 // p-space
 int pgrid(i64 p);
+int ugrid(i64 p);  // k_fista_update's grid (its J / <b, x> partial count)
 // bxpart (nullable): per-CTA partials of <b, x_new> for the expanded objective
 void fista_update(const Launch& L, const FistaCtl* ctl, i64 p, int pen, double alpha, double* x, double* xp,
                   double* Sx, double* Sxp, const double* b, double* best, double* Sbest, double* Jpart,

@@ -108,6 +108,9 @@ inline void bump(const Launch& L) {
 
 int elem_grid(i64 n) { return grid_for(n, NT * 4, 148 * 8); }
 int pgrid(i64 p) { return grid_for(p, NT, 148 * 8); }
+// k_fista_update's grid (2 CTAs per SM, 4 elements per thread and trip): fewer
+// per-CTA partials for the single-CTA control kernel to reduce
+int ugrid(i64 p) { return grid_for(p, NT * 4, 148 * 2); }
 
 // ------------------------------------------------------------ contraction
 // Mode-k banded contraction of A (a x K x b, column-major) with the operator
@@ -915,7 +918,7 @@ __global__ void __launch_bounds__(NT) k_fista_update(const FistaCtl* __restrict_
 void fista_update(const Launch& L, const FistaCtl* ctl, i64 p, int pen, double alpha, double* x, double* xp,
                   double* Sx, double* Sxp, const double* b, double* best, double* Sbest, double* Jpart,
                   double* bxpart) {
-  k_fista_update<<<pgrid(p), NT, 0, L.s>>>(ctl, p, pen, alpha, x, xp, Sx, Sxp, b, best, Sbest, Jpart, bxpart);
+  k_fista_update<<<ugrid(p), NT, 0, L.s>>>(ctl, p, pen, alpha, x, xp, Sx, Sxp, b, best, Sbest, Jpart, bxpart);
   bump(L);
 }
 

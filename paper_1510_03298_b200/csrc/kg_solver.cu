@@ -1278,7 +1278,7 @@ static void enqueue_body(Fit& F, cudaGraphConditionalHandle h, int use_handle) {
                  F.b.d() + o0, F.best.d() + o0, F.Sbest.d() + o0, F.Jpart.d(), ex ? F.bxpart.d() : nullptr);
     exch_x(F, F.x.d());
     const int n_ss = step_pass(F, F.x.d(), F.Sx.d());
-    halo_scalars(F, n_ss, pgrid(on), ex);
+    halo_scalars(F, n_ss, ugrid(on), ex);
     fista_control(ctx->L(), c, F.scal.d() + 40, 1, F.scal.d() + 41, 1, h, use_handle,
                   ex ? F.scal.d() + 43 : nullptr, 1);
     return;
@@ -1286,8 +1286,8 @@ static void enqueue_body(Fit& F, cudaGraphConditionalHandle h, int use_handle) {
   fista_update(ctx->L(), c, F.p, F.pen, F.alpha, F.x.d(), F.xp.d(), F.Sx.d(), F.Sxp.d(), F.b.d(), F.best.d(),
                F.Sbest.d(), F.Jpart.d(), ex ? F.bxpart.d() : nullptr);
   F.n_ss = step_pass(F, F.x.d(), F.Sx.d());
-  fista_control(ctx->L(), c, F.part.d(), F.n_ss, F.Jpart.d(), pgrid(F.p), h, use_handle,
-                ex ? F.bxpart.d() : nullptr, pgrid(F.p));
+  fista_control(ctx->L(), c, F.part.d(), F.n_ss, F.Jpart.d(), ugrid(F.p), h, use_handle,
+                ex ? F.bxpart.d() : nullptr, ugrid(F.p));
 }
 
 // KG_HOST_LOOP=1: drive the FISTA loop from the host (one sync per
