@@ -204,6 +204,12 @@ struct SlabArgs {
   // tz[c] = t0 | (second tile used) << 16
   const int* tz = nullptr;
   const double* x2z = nullptr;  // [c][tile][s][lane] = X2[8c + 2 (lane%4) + s, 8 (t0 + tile) + lane/4]
+  // scatter/gather form of Y = X1^T w (k_slab2): basis function k sums the
+  // partials of the row quads whose window holds it; gat[4k .. 4k+3] = up to 8
+  // 16-bit slots (quad * 5 + tap, or the zero slot), gmax = most slots of any k
+  // (0: unavailable), PL = slots per column-pair plane (= 2 mod 8, zero slot last)
+  const int* gat = nullptr;
+  int gmax = 0, PL = 0;
   const double* S = nullptr;    // p1 x p2 x m3
   const double* v = nullptr;    // n1 x n2 x m3
   double* Q = nullptr;          // p1 x p2 x m3 (out)

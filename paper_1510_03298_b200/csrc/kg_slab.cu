@@ -381,7 +381,326 @@ __global__ void __launch_bounds__(kSlabBS, 1) k_slab(SlabArgs a) {
   }
 }
 
+
+// k_slab2: the same pass with Y = X1^T w in scatter/gather form instead of
+// DMMA over the (35% dense) band window.  A row thread already holds the
+// window coefficients C[r][t] of its 4 rows, so after w it also forms the five
+// window partials sum_r C[r][t] w[r] of its two columns (40 FMAs, no extra
+// operands) and stores them to slots 5 quad .. 5 quad + 4 of its column pair's
+// plane; a tensor-warp lane (basis function k, column pair) sums the <= 8
+// slots of the quads whose rows hold k (SlabArgs::gat, ascending quads: a
+// fixed order), which lands Y directly in the A-fragment layout of the Z step.
+// FP64-pipe time per chunk drops from ~800 to ~620 SM-cycles and the tensor
+// warps' critical path from 12 to 0 Y DMMAs.
+__global__ void __launch_bounds__(kSlabBS, 1) k_slab2(SlabArgs a) {
+  using namespace async;
+  extern __shared__ __align__(128) double sm[];
+  __shared__ double red[32];
+  __shared__ unsigned long long sbar[2];     // the two S3 tiles
+  const int n1 = a.n1, n2 = a.n2, p1 = a.p1, p2 = a.p2, nch = a.nch;
+  const int ldS = a.ldS, PL = a.PL;
+  const int groups = (p1 + 7) >> 3;
+  const int sbuf = ldS * p2;                  // one S3 tile
+  const int ubuf = kLdr * 8 * groups;         // one U tile
+  const int pbuf = 8 * PL;                    // one partial tile: 4 column-pair planes of PL double2 slots
+  double* Ss = sm;                            // [2][ldS x p2]
+  double* Us = Ss + 2 * sbuf;                 // [kDepth][ubuf]
+  double* Ps = Us + kDepth * ubuf;            // [kDepth][pbuf]
+  const int tid = threadIdx.x, lane = tid & 31, warp = tid >> 5;
+  const bool rowrole = warp < 8;
+  const i64 p12 = static_cast<i64>(p1) * p2, n12 = static_cast<i64>(n1) * n2;
+  const int rounds = static_cast<int>((a.m3 - blockIdx.x + gridDim.x - 1) / gridDim.x);  // slices of this CTA
+  const int qtot = rounds * nch;
+  auto issue_s = [&](int r) {
+    if (r >= rounds) return;
+    const unsigned bytes = static_cast<unsigned>(p1 * 8);
+    mbar_expect_tx(&sbar[r & 1], bytes * p2);
+    const double* src = a.S + (blockIdx.x + static_cast<i64>(r) * gridDim.x) * p12;
+    double* dst = Ss + (r & 1) * sbuf;
+    for (int k = 0; k < p2; ++k) bulk_g2s(dst + ldS * k, src + static_cast<i64>(p1) * k, bytes, &sbar[r & 1]);
+  };
+  if (tid == 0) {
+    mbar_init(&sbar[0], 1);
+    mbar_init(&sbar[1], 1);
+  }
+  for (int k = tid; k < 2 * sbuf; k += kSlabBS) Ss[k] = 0.0;
+  if (tid < 4 * kDepth) {  // the zero slot of every plane
+    Ps[2 * (tid * PL + PL - 1)] = 0.0;
+    Ps[2 * (tid * PL + PL - 1) + 1] = 0.0;
+  }
+  __syncthreads();
+  double acc0 = 0.0, acc1 = 0.0;
+  if (rowrole) {
+    // ------------------------------------------------------------ row warps
+    const int nq = n1 >> 2;                    // row quads
+    const bool act = tid < 4 * nq;
+    const int rq = act ? tid % nq : 0, cp = act ? tid / nq : 0;
+    const int r0 = 4 * rq, c0 = 2 * cp;        // rows r0 .. r0 + 3, chunk columns c0, c0 + 1
+    int lo = 0;
+    double C[4][kWin];
+#pragma unroll
+    for (int r = 0; r < 4; ++r)
+#pragma unroll
+      for (int t = 0; t < kWin; ++t) C[r][t] = 0.0;
+    if (act) {
+      lo = min(__ldg(a.H1.lo + r0), p1 - kWin);
+#pragma unroll
+      for (int r = 0; r < 4; ++r) {
+        const int l = __ldg(a.H1.lo + r0 + r), len = __ldg(a.H1.len + r0 + r);
+        const double* cf = a.H1.coef + __ldg(a.H1.off + r0 + r);
+#pragma unroll
+        for (int t = 0; t < kWin; ++t) {
+          const int j = lo + t - l;
+          C[r][t] = (j >= 0 && j < len) ? __ldg(cf + j) : 0.0;
+        }
+      }
+    }
+    const double* ub0 = Us + lo * kLdr + c0;
+    double2* pb0 = reinterpret_cast<double2*>(Ps) + cp * PL + rq * kWin;
+    const double* vbase = a.v + blockIdx.x * n12 + r0;
+    const i64 vstep = static_cast<i64>(gridDim.x) * n12;
+    auto load_v = [&](double (&vr)[8], int r, int c) {
+#pragma unroll
+      for (int e = 0; e < 2; ++e) {
+        const int col = 8 * c + c0 + e;
+        if (act && r < rounds && col < n2) {
+          const double* p = vbase + r * vstep + static_cast<i64>(n1) * col;
+          const double2 x = ldg2_stream(p), y = ldg2_stream(p + 2);
+          vr[4 * e + 0] = x.x;
+          vr[4 * e + 1] = x.y;
+          vr[4 * e + 2] = y.x;
+          vr[4 * e + 3] = y.y;
+        } else {
+#pragma unroll
+          for (int k = 0; k < 4; ++k) vr[4 * e + k] = 0.0;
+        }
+      }
+    };
+    double vA[8], vB[8];
+    int lr = 0, lc = 0;  // cursor of the next chunk to load
+    auto adv = [&](int& r, int& c) {
+      if (++c == nch) {
+        c = 0;
+        ++r;
+      }
+    };
+    load_v(vA, lr, lc);
+    adv(lr, lc);
+    load_v(vB, lr, lc);
+    adv(lr, lc);
+    auto body = [&](int q, double (&vr)[8]) {
+      const int buf = q & (kDepth - 1);
+      nb_sync(kBarUReady + buf, kSlabBS);
+      if (act) {
+        const double* u = ub0 + buf * ubuf;
+        double2 uu[kWin];
+#pragma unroll
+        for (int t = 0; t < kWin; ++t) uu[t] = lds2(u + t * kLdr);
+        double pt[2][kWin];
+#pragma unroll
+        for (int c = 0; c < 2; ++c) {
+#pragma unroll
+          for (int r = 0; r < 4; ++r) {
+            double x = C[r][0] * (c ? uu[0].y : uu[0].x);
+#pragma unroll
+            for (int t = 1; t < kWin; ++t) x = fma(C[r][t], c ? uu[t].y : uu[t].x, x);
+            const double wv = vr[4 * c + r] * x;
+            if (r & 1) acc1 = fma(wv, x, acc1);
+            else acc0 = fma(wv, x, acc0);
+#pragma unroll
+            for (int t = 0; t < kWin; ++t) pt[c][t] = r == 0 ? C[0][t] * wv : fma(C[r][t], wv, pt[c][t]);
+          }
+        }
+        double2* P = pb0 + buf * (pbuf >> 1);
+#pragma unroll
+        for (int t = 0; t < kWin; ++t) P[t] = make_double2(pt[0][t], pt[1][t]);
+      }
+      nb_arrive(kBarWReady + buf, kSlabBS);
+      load_v(vr, lr, lc);  // two chunks ahead
+      adv(lr, lc);
+    };
+    int q = 0;
+    for (; q + 1 < qtot; q += 2) {
+      body(q, vA);
+      body(q + 1, vB);
+    }
+    if (q < qtot) body(q, vA);
+  } else {
+    // --------------------------------------------------------- tensor warps
+    const int tw = warp - 8;
+    const bool gact = tw < groups;            // this warp owns p1 rows 8 tw .. 8 tw + 7
+    const bool leader = tid == 8 * 32;
+    const int zr = 8 * tw + (lane >> 2), zq = 2 * (lane & 3);
+    double* ua0 = Us + zr * kLdr + zq;        // stage A D store (buffer 0)
+    // gather slots of basis function zr (column pair lane & 3)
+    int4 gs = make_int4(0, 0, 0, 0);
+    if (gact) gs = __ldg(reinterpret_cast<const int4*>(a.gat) + zr);
+    else gs.x = gs.y = gs.z = gs.w = (PL - 1) | ((PL - 1) << 16);
+    const int gmax = a.gmax;
+    const double2* pg0 = reinterpret_cast<const double2*>(Ps) + (lane & 3) * PL;
+    struct Cur {
+      int r, c;
+    };
+    auto adv = [&](Cur& k) {
+      if (++k.c == nch) {
+        k.c = 0;
+        ++k.r;
+      }
+    };
+    auto at_q = [&](int q) {  // only for the few prologue positions
+      Cur k{0, 0};
+      for (int i = 0; i < q; ++i) adv(k);
+      return k;
+    };
+    if (leader) {
+      mbar_init_fence();
+      fence_proxy_async();
+      issue_s(0);
+      issue_s(1);
+    }
+    struct ZT { int tz; double b0, b1, b2, b3; };
+    struct AT { int wz; double b0, b1; };
+    auto load_z = [&](int c) {
+      ZT t;
+      const double* x2 = a.x2z + c * 128;
+      t.tz = __ldg(a.tz + c);
+      t.b0 = __ldg(x2 + lane);
+      t.b1 = __ldg(x2 + 32 + lane);
+      t.b2 = __ldg(x2 + 64 + lane);
+      t.b3 = __ldg(x2 + 96 + lane);
+      return t;
+    };
+    auto load_a = [&](int c) {
+      AT t;
+      const double* x2 = a.x2u + c * 64;
+      t.wz = __ldg(a.w0 + c);
+      t.b0 = __ldg(x2 + lane);
+      t.b1 = __ldg(x2 + 32 + lane);
+      return t;
+    };
+    auto stage_a = [&](const Cur& k, int ub, const AT& t) {
+      if (k.c == 0) mbar_wait(&sbar[k.r & 1], static_cast<unsigned>((k.r >> 1) & 1));
+      if (!gact) return;
+      const double* sr = Ss + (k.r & 1) * sbuf + zr + ldS * (t.wz + (lane & 3));
+      double d0 = 0.0, d1 = 0.0;
+      dmma(d0, d1, sr[0], t.b0);
+      dmma(d0, d1, sr[4 * ldS], t.b1);
+      *reinterpret_cast<double2*>(ua0 + ub * ubuf) = make_double2(d0, d1);
+    };
+    Cur ka{0, 0};  // U step cursor
+    for (int q = 0; q < kDepth; ++q, adv(ka)) {
+      if (q < qtot) {
+        stage_a(ka, q, load_a(ka.c));
+        nb_arrive(kBarUReady + q, kSlabBS);
+      }
+    }
+    nb_sync(kBarTensor, kSlabBS - 256);
+    if (leader)  // a round whose last U was just formed frees its S3 tile
+      for (int q = 0; q < kDepth && q < qtot; ++q)
+        if (at_q(q).c == nch - 1) issue_s(at_q(q).r + 2);
+    Cur kz = at_q(1);              // Z tables: q + 1
+    Cur kt = ka;                   // U tables: q + kDepth + 1
+    adv(kt);
+    int T = -1;
+    double z00 = 0.0, z01 = 0.0, z10 = 0.0, z11 = 0.0;
+    double* qs = a.Q + blockIdx.x * p12;
+    const i64 qstep = static_cast<i64>(gridDim.x) * p12;
+    auto flush = [&](int k, double x0, double x1) {
+      const int zc = 8 * k + zq;
+      if (zr < p1 && zc < p2) qs[zr + static_cast<i64>(p1) * zc] = x0;
+      if (zr < p1 && zc + 1 < p2) qs[zr + static_cast<i64>(p1) * (zc + 1)] = x1;
+    };
+    ZT zt = load_z(0);
+    AT at = load_a(ka.c);  // ka = kDepth
+    int c = 0;
+    for (int q = 0; q < qtot; ++q) {
+      const int buf = q & (kDepth - 1);
+      const ZT zn = load_z(kz.c);   // next chunk's Z tables
+      const AT an = load_a(kt.c);   // and the U tables one further
+      nb_sync(kBarWReady + buf, kSlabBS);
+      if (gact) {
+        const double2* pg = pg0 + buf * (pbuf >> 1);
+        // Y(zr, columns zq, zq + 1) = sum of the quads' partials, ascending quads
+        double2 g0 = pg[gs.x & 0xffff], g1 = pg[static_cast<unsigned>(gs.x) >> 16];
+        double2 g2 = pg[gs.y & 0xffff], g3 = pg[static_cast<unsigned>(gs.y) >> 16];
+        double y0 = ((g0.x + g1.x) + g2.x) + g3.x;
+        double y1 = ((g0.y + g1.y) + g2.y) + g3.y;
+        if (gmax > 4) {
+          g0 = pg[gs.z & 0xffff];
+          g1 = pg[static_cast<unsigned>(gs.z) >> 16];
+          y0 = (y0 + g0.x) + g1.x;
+          y1 = (y1 + g0.y) + g1.y;
+          if (gmax > 6) {
+            g2 = pg[gs.w & 0xffff];
+            g3 = pg[static_cast<unsigned>(gs.w) >> 16];
+            y0 = (y0 + g2.x) + g3.x;
+            y1 = (y1 + g2.y) + g3.y;
+          }
+        }
+        const int t0 = zt.tz & 0xffff;
+        if (T < 0) T = t0;
+        while (T < t0) {  // tile T is complete: later chunks start at t0 > T
+          flush(T, z00, z01);
+          z00 = z10;
+          z01 = z11;
+          z10 = z11 = 0.0;
+          ++T;
+        }
+        dmma(z00, z01, y0, zt.b0);
+        dmma(z00, z01, y1, zt.b1);
+        if (zt.tz >> 16) {
+          dmma(z10, z11, y0, zt.b2);
+          dmma(z10, z11, y1, zt.b3);
+        }
+        if (c == nch - 1) {  // slice done: the live window holds its last two tiles
+          flush(T, z00, z01);
+          flush(T + 1, z10, z11);
+          z00 = z01 = z10 = z11 = 0.0;
+          T = -1;
+        }
+      }
+      // U(q + kDepth) into the buffer of chunk q (the row warps are done with it)
+      if (q + kDepth < qtot) {
+        stage_a(ka, buf, at);
+        nb_arrive(kBarUReady + buf, kSlabBS);
+        if (ka.c == nch - 1) {  // that round's S3 tile is free once every tensor warp formed its U
+          nb_sync(kBarTensor, kSlabBS - 256);
+          if (leader) {
+            fence_proxy_async();
+            issue_s(ka.r + 2);
+          }
+        }
+      }
+      adv(ka);
+      adv(kz);
+      adv(kt);
+      zt = zn;
+      at = an;
+      if (++c == nch) {
+        c = 0;
+        qs += qstep;
+      }
+    }
+  }
+  double rr = warp_sum_s(acc0 + acc1);
+  __syncthreads();
+  if (lane == 0) red[warp] = rr;
+  __syncthreads();
+  if (warp == 0) {
+    rr = lane < (kSlabBS >> 5) ? red[lane] : 0.0;
+    rr = warp_sum_s(rr);
+    if (lane == 0) a.partial[blockIdx.x] = rr;
+  }
+}
+
 }  // namespace
+
+// Y in scatter/gather form (k_slab2) when the design has a gather table;
+// KG_SLAB_DMMA=1 (developer switch) keeps the DMMA form (k_slab).
+static bool slab_gather(const SlabArgs& a) {
+  static const bool dmma_y = dev_env("KG_SLAB_DMMA") != nullptr;
+  return !dmma_y && a.gat && a.gmax > 0 && a.gmax <= 8 && a.PL > 0;
+}
 
 // Leading dimensions and shared-memory size of a slab plan.
 static size_t slab_layout(SlabArgs& a) {
@@ -392,7 +711,8 @@ static size_t slab_layout(SlabArgs& a) {
   a.ldW = (a.n1 + 15) / 16 * 16 + 4;         // = 4 (mod 16): B fragments of stage C
   a.cg = 1;
   const size_t ubuf = static_cast<size_t>(kLdr) * 8 * ((a.p1 + 7) / 8);
-  const size_t dbl = 2 * static_cast<size_t>(a.ldS) * a.p2 + kDepth * ubuf + kDepth * static_cast<size_t>(a.ldW) * 8;
+  const size_t tile = slab_gather(a) ? static_cast<size_t>(8) * a.PL : static_cast<size_t>(a.ldW) * 8;
+  const size_t dbl = 2 * static_cast<size_t>(a.ldS) * a.p2 + kDepth * ubuf + kDepth * tile;
   return dbl * sizeof(double);
 }
 
@@ -429,10 +749,15 @@ void slab_pass(const Launch& L, const SlabArgs& a0) {
   SlabArgs a = a0;
   const size_t smem = slab_layout(a);
   const int g = slab_grid(a);
-  switch (a.g1.ks) {
-    case 8: launch_slab_ks<8>(L, a, smem, g); break;
-    case 12: launch_slab_ks<12>(L, a, smem, g); break;
-    default: launch_slab_ks<16>(L, a, smem, g); break;
+  if (slab_gather(a)) {
+    smem_attr(k_slab2, static_cast<int>(smem));
+    k_slab2<<<g, kSlabBS, smem, L.s>>>(a);
+  } else {
+    switch (a.g1.ks) {
+      case 8: launch_slab_ks<8>(L, a, smem, g); break;
+      case 12: launch_slab_ks<12>(L, a, smem, g); break;
+      default: launch_slab_ks<16>(L, a, smem, g); break;
+    }
   }
   launched(L);
 }
