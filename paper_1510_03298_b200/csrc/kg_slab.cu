@@ -392,11 +392,15 @@ __global__ void __launch_bounds__(kSlabBS, 1) k_slab(SlabArgs a) {
 // fixed order), which lands Y directly in the A-fragment layout of the Z step.
 // FP64-pipe time per chunk drops from ~800 to ~620 SM-cycles and the tensor
 // warps' critical path from 12 to 0 Y DMMAs.
+template <int VS, bool MB>
 __global__ void __launch_bounds__(kSlabBS, 1) k_slab2(SlabArgs a) {
   using namespace async;
   extern __shared__ __align__(128) double sm[];
   __shared__ double red[32];
   __shared__ unsigned long long sbar[2];     // the two S3 tiles
+  // MB: the U / partial-tile hand-over through mbarriers (one arrival per warp)
+  // instead of named barriers, so the warps of a role do not rendezvous per chunk
+  __shared__ unsigned long long ubar[kDepth], wbar[kDepth];
   const int n1 = a.n1, n2 = a.n2, p1 = a.p1, p2 = a.p2, nch = a.nch;
   const int ldS = a.ldS, PL = a.PL;
   const int groups = (p1 + 7) >> 3;
@@ -422,6 +426,11 @@ __global__ void __launch_bounds__(kSlabBS, 1) k_slab2(SlabArgs a) {
   if (tid == 0) {
     mbar_init(&sbar[0], 1);
     mbar_init(&sbar[1], 1);
+    for (int k = 0; k < kDepth; ++k) {
+      mbar_init(&ubar[k], 8);
+      mbar_init(&wbar[k], 8);
+    }
+    mbar_init_fence();
   }
   for (int k = tid; k < 2 * sbuf; k += kSlabBS) Ss[k] = 0.0;
   if (tid < 4 * kDepth) {  // the zero slot of every plane
@@ -432,6 +441,7 @@ __global__ void __launch_bounds__(kSlabBS, 1) k_slab2(SlabArgs a) {
   double acc0 = 0.0, acc1 = 0.0;
   if (rowrole) {
     // ------------------------------------------------------------ row warps
+    if (VS > 2) asm volatile("setmaxnreg.inc.sync.aligned.u32 168;");
     const int nq = n1 >> 2;                    // row quads
     const bool act = tid < 4 * nq;
     const int rq = act ? tid % nq : 0, cp = act ? tid / nq : 0;
@@ -463,7 +473,7 @@ __global__ void __launch_bounds__(kSlabBS, 1) k_slab2(SlabArgs a) {
 #pragma unroll
       for (int e = 0; e < 2; ++e) {
         const int col = 8 * c + c0 + e;
-        if (act && r < rounds && col < n2) {
+        if (act && r < rounds && col < n2 && !(a.dbg & 1)) {
           const double* p = vbase + r * vstep + static_cast<i64>(n1) * col;
           const double2 x = ldg2_stream(p), y = ldg2_stream(p + 2);
           vr[4 * e + 0] = x.x;
@@ -476,7 +486,7 @@ __global__ void __launch_bounds__(kSlabBS, 1) k_slab2(SlabArgs a) {
         }
       }
     };
-    double vA[8], vB[8];
+    double vv[VS][8];
     int lr = 0, lc = 0;  // cursor of the next chunk to load
     auto adv = [&](int& r, int& c) {
       if (++c == nch) {
@@ -484,13 +494,30 @@ __global__ void __launch_bounds__(kSlabBS, 1) k_slab2(SlabArgs a) {
         ++r;
       }
     };
-    load_v(vA, lr, lc);
-    adv(lr, lc);
-    load_v(vB, lr, lc);
-    adv(lr, lc);
+    // one thread pulls the v chunks a.pf ahead into L2 (a chunk is contiguous:
+    // 8 columns of n1), so the register loads VS chunks ahead find them there
+    int fr = 0, fc = 0;
+    auto prefetch_v = [&]() {
+      if (fr < rounds) {
+        const int cols = min(8, n2 - 8 * fc);
+        bulk_prefetch_l2(a.v + (blockIdx.x + static_cast<i64>(fr) * gridDim.x) * n12 + static_cast<i64>(n1) * 8 * fc,
+                         static_cast<unsigned>(cols * n1 * 8));
+      }
+      adv(fr, fc);
+    };
+    const bool pfl = tid == 0 && a.pf > 0;
+    if (pfl)
+      for (int k = 0; k < a.pf; ++k) prefetch_v();
+#pragma unroll
+    for (int s = 0; s < VS; ++s) {
+      load_v(vv[s], lr, lc);
+      adv(lr, lc);
+    }
     auto body = [&](int q, double (&vr)[8]) {
       const int buf = q & (kDepth - 1);
-      nb_sync(kBarUReady + buf, kSlabBS);
+      if (pfl) prefetch_v();
+      if (MB) mbar_wait(&ubar[buf], static_cast<unsigned>(q / kDepth) & 1u);
+      else nb_sync(kBarUReady + buf, kSlabBS);
       if (act) {
         const double* u = ub0 + buf * ubuf;
         double2 uu[kWin];
@@ -502,31 +529,46 @@ __global__ void __launch_bounds__(kSlabBS, 1) k_slab2(SlabArgs a) {
 #pragma unroll
           for (int r = 0; r < 4; ++r) {
             double x = C[r][0] * (c ? uu[0].y : uu[0].x);
+            if (!(a.dbg & 8)) {
 #pragma unroll
-            for (int t = 1; t < kWin; ++t) x = fma(C[r][t], c ? uu[t].y : uu[t].x, x);
+              for (int t = 1; t < kWin; ++t) x = fma(C[r][t], c ? uu[t].y : uu[t].x, x);
+            }
             const double wv = vr[4 * c + r] * x;
             if (r & 1) acc1 = fma(wv, x, acc1);
             else acc0 = fma(wv, x, acc0);
+            if (a.dbg & 4) {
 #pragma unroll
-            for (int t = 0; t < kWin; ++t) pt[c][t] = r == 0 ? C[0][t] * wv : fma(C[r][t], wv, pt[c][t]);
+              for (int t = 0; t < kWin; ++t) pt[c][t] = wv;
+            } else {
+#pragma unroll
+              for (int t = 0; t < kWin; ++t) pt[c][t] = r == 0 ? C[0][t] * wv : fma(C[r][t], wv, pt[c][t]);
+            }
           }
         }
         double2* P = pb0 + buf * (pbuf >> 1);
 #pragma unroll
         for (int t = 0; t < kWin; ++t) P[t] = make_double2(pt[0][t], pt[1][t]);
       }
-      nb_arrive(kBarWReady + buf, kSlabBS);
-      load_v(vr, lr, lc);  // two chunks ahead
+      if (MB) {
+        __syncwarp();
+        if (lane == 0) mbar_arrive(&wbar[buf]);
+      } else {
+        nb_arrive(kBarWReady + buf, kSlabBS);
+      }
+      load_v(vr, lr, lc);  // VS chunks ahead
       adv(lr, lc);
     };
     int q = 0;
-    for (; q + 1 < qtot; q += 2) {
-      body(q, vA);
-      body(q + 1, vB);
+    for (; q + VS <= qtot; q += VS) {
+#pragma unroll
+      for (int s = 0; s < VS; ++s) body(q + s, vv[s]);
     }
-    if (q < qtot) body(q, vA);
+#pragma unroll
+    for (int s = 0; s < VS; ++s)
+      if (q + s < qtot) body(q + s, vv[s]);
   } else {
     // --------------------------------------------------------- tensor warps
+    if (VS > 2) asm volatile("setmaxnreg.dec.sync.aligned.u32 88;");
     const int tw = warp - 8;
     const bool gact = tw < groups;            // this warp owns p1 rows 8 tw .. 8 tw + 7
     const bool leader = tid == 8 * 32;
@@ -591,7 +633,12 @@ __global__ void __launch_bounds__(kSlabBS, 1) k_slab2(SlabArgs a) {
     for (int q = 0; q < kDepth; ++q, adv(ka)) {
       if (q < qtot) {
         stage_a(ka, q, load_a(ka.c));
-        nb_arrive(kBarUReady + q, kSlabBS);
+        if (MB) {
+          __syncwarp();
+          if (lane == 0) mbar_arrive(&ubar[q]);
+        } else {
+          nb_arrive(kBarUReady + q, kSlabBS);
+        }
       }
     }
     nb_sync(kBarTensor, kSlabBS - 256);
@@ -617,8 +664,9 @@ __global__ void __launch_bounds__(kSlabBS, 1) k_slab2(SlabArgs a) {
       const int buf = q & (kDepth - 1);
       const ZT zn = load_z(kz.c);   // next chunk's Z tables
       const AT an = load_a(kt.c);   // and the U tables one further
-      nb_sync(kBarWReady + buf, kSlabBS);
-      if (gact) {
+      if (MB) mbar_wait(&wbar[buf], static_cast<unsigned>(q / kDepth) & 1u);
+      else nb_sync(kBarWReady + buf, kSlabBS);
+      if (gact && !(a.dbg & 2)) {
         const double2* pg = pg0 + buf * (pbuf >> 1);
         // Y(zr, columns zq, zq + 1) = sum of the quads' partials, ascending quads
         double2 g0 = pg[gs.x & 0xffff], g1 = pg[static_cast<unsigned>(gs.x) >> 16];
@@ -662,7 +710,12 @@ __global__ void __launch_bounds__(kSlabBS, 1) k_slab2(SlabArgs a) {
       // U(q + kDepth) into the buffer of chunk q (the row warps are done with it)
       if (q + kDepth < qtot) {
         stage_a(ka, buf, at);
-        nb_arrive(kBarUReady + buf, kSlabBS);
+        if (MB) {
+          __syncwarp();
+          if (lane == 0) mbar_arrive(&ubar[buf]);
+        } else {
+          nb_arrive(kBarUReady + buf, kSlabBS);
+        }
         if (ka.c == nch - 1) {  // that round's S3 tile is free once every tensor warp formed its U
           nb_sync(kBarTensor, kSlabBS - 256);
           if (leader) {
@@ -750,8 +803,22 @@ void slab_pass(const Launch& L, const SlabArgs& a0) {
   const size_t smem = slab_layout(a);
   const int g = slab_grid(a);
   if (slab_gather(a)) {
-    smem_attr(k_slab2, static_cast<int>(smem));
-    k_slab2<<<g, kSlabBS, smem, L.s>>>(a);
+    static const int vs = [] { const char* e = dev_env("KG_SLAB_VS"); return e ? std::atoi(e) : 2; }();
+    static const int pf = [] { const char* e = dev_env("KG_SLAB_PF"); return e ? std::atoi(e) : 6; }();
+    a.pf = pf;
+    static const int dbg = [] { const char* e = dev_env("KG_SLAB_DBG"); return e ? std::atoi(e) : 0; }();
+    a.dbg = dbg;
+    static const bool mb = dev_env("KG_SLAB_NB") == nullptr;
+    if (vs == 3 && mb) {
+      smem_attr(k_slab2<3, true>, static_cast<int>(smem));
+      k_slab2<3, true><<<g, kSlabBS, smem, L.s>>>(a);
+    } else if (mb) {
+      smem_attr(k_slab2<2, true>, static_cast<int>(smem));
+      k_slab2<2, true><<<g, kSlabBS, smem, L.s>>>(a);
+    } else {
+      smem_attr(k_slab2<2, false>, static_cast<int>(smem));
+      k_slab2<2, false><<<g, kSlabBS, smem, L.s>>>(a);
+    }
   } else {
     switch (a.g1.ks) {
       case 8: launch_slab_ks<8>(L, a, smem, g); break;
