@@ -748,11 +748,486 @@ __global__ void __launch_bounds__(kSlabBS, 1) k_slab2(SlabArgs a) {
 
 }  // namespace
 
+// k_slab4: k_slab2 with the per-chunk instruction count of both roles cut to
+// the arithmetic.  The pass is bound by issue latency (16 warps per SM, ~10
+// cycles between a warp's instructions), not by HBM or the FP64 pipe: with
+// every FP64 instruction removed it still took 75% of its time.  So:
+//   * the U and partial tiles have fixed strides (kUBuf, kPBuf) and the chunk
+//     loops are unrolled over the kDepth buffers: buffer offsets and barrier
+//     parities are immediates;
+//   * barriers are addressed by precomputed 32-bit shared addresses;
+//   * v is read through a running pointer, with an unpredicated path for full
+//     chunks;
+//   * the X2 chunk tables sit in shared memory (one copy per CTA instead of
+//     eight L1-missing global loads per tensor warp and chunk) and are read
+//     through running pointers; the gather slots are byte offsets in registers;
+//   * the L2 prefetch of v is issued by the tensor-warp leader;
+//   * setmaxnreg: tensor warpgroups 104 registers, row warpgroups 152.
+constexpr int kPLMax = 322;                 // slots per column-pair plane at n1 = 256
+constexpr int kPBuf = 8 * kPLMax;           // doubles per partial tile
+constexpr int kUBuf = kLdr * 64;            // doubles per U tile (p1 <= 64)
+
+__device__ __forceinline__ bool mbar_try_s(unsigned bar, unsigned parity) {
+  unsigned ok;
+  asm volatile(
+      "{\n"
+      ".reg .pred p;\n"
+      "mbarrier.try_wait.parity.shared::cta.b64 p, [%1], %2;\n"
+      "selp.u32 %0, 1, 0, p;\n"
+      "}\n"
+      : "=r"(ok)
+      : "r"(bar), "r"(parity)
+      : "memory");
+  return ok != 0;
+}
+__device__ __forceinline__ void mbar_spin_s(unsigned bar, unsigned parity) {
+  const long long t0 = clock64();
+  while (!mbar_try_s(bar, parity)) {
+    if (clock64() - t0 > async::kWatchdogCycles) {
+      printf("kg watchdog: slab mbarrier wait (block %d thread %d parity %u)\n", blockIdx.x, threadIdx.x, parity);
+      __trap();
+    }
+  }
+}
+__device__ __forceinline__ void mbar_wait_s(unsigned bar, unsigned parity) {
+  if (!mbar_try_s(bar, parity)) mbar_spin_s(bar, parity);
+}
+__device__ __forceinline__ void mbar_arrive_s(unsigned bar) {
+  asm volatile("mbarrier.arrive.shared::cta.b64 _, [%0];" ::"r"(bar) : "memory");
+}
+__device__ __forceinline__ double2 lds2_s(unsigned addr) {
+  double2 r;
+  asm volatile("ld.shared.v2.f64 {%0, %1}, [%2];" : "=d"(r.x), "=d"(r.y) : "r"(addr));
+  return r;
+}
+__device__ __forceinline__ double lds_s(unsigned addr) {
+  double r;
+  asm volatile("ld.shared.f64 %0, [%1];" : "=d"(r) : "r"(addr));
+  return r;
+}
+__device__ __forceinline__ int ldsi_s(unsigned addr) {
+  int r;
+  asm volatile("ld.shared.s32 %0, [%1];" : "=r"(r) : "r"(addr));
+  return r;
+}
+__device__ __forceinline__ void sts2_s(unsigned addr, double x, double y) {
+  asm volatile("st.shared.v2.f64 [%0], {%1, %2};" ::"r"(addr), "d"(x), "d"(y) : "memory");
+}
+
+// G: gather slots per basis function (6 or 8).
+template <int G>
+__global__ void __launch_bounds__(kSlabBS, 1) k_slab4(SlabArgs a) {
+  using namespace async;
+  extern __shared__ __align__(128) double sm[];
+  __shared__ double red[32];
+  __shared__ unsigned long long sbar[2];     // the two S3 tiles
+  __shared__ unsigned long long ubar[kDepth], wbar[kDepth];  // U(q) formed / partials of chunk q stored (one arrival per warp)
+  const int n1 = a.n1, n2 = a.n2, p1 = a.p1, p2 = a.p2, nch = a.nch;
+  const int ldS = a.ldS, PL = a.PL;
+  const int sbuf = ldS * p2;                  // one S3 tile
+  double* Ss = sm;                            // [2][ldS x p2]
+  double* Us = Ss + 2 * sbuf;                 // [kDepth][kUBuf]
+  double* Ps = Us + kDepth * kUBuf;           // [kDepth][kPBuf]
+  double* Tz = Ps + kDepth * kPBuf;           // [nch][128]  Z-step B fragments
+  double* Tu = Tz + nch * 128;                // [nch][64]   U-step B fragments
+  int* Ti = reinterpret_cast<int*>(Tu + nch * 64);  // [nch][2] = {tz, w0}
+  const int tid = threadIdx.x, lane = tid & 31, warp = tid >> 5;
+  const i64 p12 = static_cast<i64>(p1) * p2, n12 = static_cast<i64>(n1) * n2;
+  const int rounds = static_cast<int>((a.m3 - blockIdx.x + gridDim.x - 1) / gridDim.x);  // slices of this CTA
+  const int qtot = rounds * nch;
+  const unsigned ubar0 = smem_u32(&ubar[0]), wbar0 = smem_u32(&wbar[0]);
+  if (tid == 0) {
+    mbar_init(&sbar[0], 1);
+    mbar_init(&sbar[1], 1);
+    for (int k = 0; k < kDepth; ++k) {
+      mbar_init(&ubar[k], 8);
+      mbar_init(&wbar[k], 8);
+    }
+    mbar_init_fence();
+  }
+  for (int k = tid; k < 2 * sbuf; k += kSlabBS) Ss[k] = 0.0;
+  for (int k = tid; k < nch * 128; k += kSlabBS) Tz[k] = __ldg(a.x2z + k);
+  for (int k = tid; k < nch * 64; k += kSlabBS) Tu[k] = __ldg(a.x2u + k);
+  for (int k = tid; k < nch; k += kSlabBS) {
+    Ti[2 * k] = __ldg(a.tz + k);
+    Ti[2 * k + 1] = __ldg(a.w0 + k);
+  }
+  if (tid < 4 * kDepth) {  // the zero slot of every plane
+    double* z = Ps + (tid >> 2) * kPBuf + 2 * ((tid & 3) * PL + PL - 1);
+    z[0] = z[1] = 0.0;
+  }
+  __syncthreads();
+  double acc0 = 0.0, acc1 = 0.0, acc2 = 0.0, acc3 = 0.0;
+  if (warp < 8) {
+    // ------------------------------------------------------------ row warps
+    asm volatile("setmaxnreg.inc.sync.aligned.u32 152;");
+    const int nq = n1 >> 2;                    // row quads
+    const bool act = tid < 4 * nq;
+    const int rq = act ? tid % nq : 0, cp = act ? tid / nq : 0;
+    const int r0 = 4 * rq, c0 = 2 * cp;        // rows r0 .. r0 + 3, chunk columns c0, c0 + 1
+    int lo = 0;
+    double C[4][kWin];
+#pragma unroll
+    for (int r = 0; r < 4; ++r)
+#pragma unroll
+      for (int t = 0; t < kWin; ++t) C[r][t] = 0.0;
+    if (act) {
+      lo = min(__ldg(a.H1.lo + r0), p1 - kWin);
+#pragma unroll
+      for (int r = 0; r < 4; ++r) {
+        const int l = __ldg(a.H1.lo + r0 + r), len = __ldg(a.H1.len + r0 + r);
+        const double* cf = a.H1.coef + __ldg(a.H1.off + r0 + r);
+#pragma unroll
+        for (int t = 0; t < kWin; ++t) {
+          const int j = lo + t - l;
+          C[r][t] = (j >= 0 && j < len) ? __ldg(cf + j) : 0.0;
+        }
+      }
+    }
+    const unsigned ub0 = smem_u32(Us + lo * kLdr + c0);
+    const unsigned pb0 = smem_u32(Ps) + 16u * static_cast<unsigned>(cp * PL + rq * kWin);
+    // v of the next chunk to load: rows r0 .. r0 + 3 of chunk columns c0, c0 + 1
+    const double* vp = a.v + blockIdx.x * n12 + r0 + static_cast<i64>(n1) * c0;
+    const i64 vchunk = static_cast<i64>(n1) * 8;
+    const i64 vjump = static_cast<i64>(gridDim.x) * n12 - vchunk * (nch - 1);  // last chunk of a slice -> first of the next
+    const bool lastfull = 8 * nch == n2;       // the last chunk of a slice has all 8 columns
+    const int lcols = n2 - 8 * (nch - 1) - c0; // valid columns of this thread's pair in the last chunk
+    int lr = 0, lc = 0;                        // (round, chunk) of vp
+    auto load_v = [&](double (&vr)[8]) {
+      if (lr < rounds && (lastfull || lc != nch - 1)) {
+        if (act && !(a.dbg & 1)) {
+          const double2 x0 = ldg2_stream(vp), x1 = ldg2_stream(vp + 2);
+          const double2 y0 = ldg2_stream(vp + n1), y1 = ldg2_stream(vp + n1 + 2);
+          vr[0] = x0.x, vr[1] = x0.y, vr[2] = x1.x, vr[3] = x1.y;
+          vr[4] = y0.x, vr[5] = y0.y, vr[6] = y1.x, vr[7] = y1.y;
+        }
+      } else {
+#pragma unroll
+        for (int k = 0; k < 8; ++k) vr[k] = 0.0;
+        if (act && lr < rounds) {
+          if (lcols > 0) {
+            const double2 x0 = ldg2_stream(vp), x1 = ldg2_stream(vp + 2);
+            vr[0] = x0.x, vr[1] = x0.y, vr[2] = x1.x, vr[3] = x1.y;
+          }
+          if (lcols > 1) {
+            const double2 y0 = ldg2_stream(vp + n1), y1 = ldg2_stream(vp + n1 + 2);
+            vr[4] = y0.x, vr[5] = y0.y, vr[6] = y1.x, vr[7] = y1.y;
+          }
+        }
+      }
+      if (++lc == nch) {
+        lc = 0;
+        ++lr;
+        vp += vjump;
+      } else {
+        vp += vchunk;
+      }
+    };
+    double vv[2][8];
+#pragma unroll
+    for (int k = 0; k < 8; ++k) vv[0][k] = vv[1][k] = 0.0;
+    load_v(vv[0]);
+    load_v(vv[1]);
+    // chunk q = 4 i + B: U(q) in U tile B, its partials into partial tile B, barrier parity i & 1
+#ifdef KG_SLAB_TIMING
+    long long tw_ = 0, tc_ = 0, tl_ = 0;
+#define TCK(x) x = clock64()
+    long long t0_, t1_, t2_, t3_;
+#else
+#define TCK(x)
+#endif
+    auto body = [&](const int B, unsigned par, double (&vr)[8]) {
+      TCK(t0_);
+      mbar_wait_s(ubar0 + 8 * B, par);
+      TCK(t1_);
+      if (act && !(a.dbg & 4)) {
+        double2 uu[kWin];
+#pragma unroll
+        for (int t = 0; t < kWin; ++t) uu[t] = lds2_s(ub0 + 8 * (B * kUBuf + t * kLdr));
+        // level by level over the 8 cells (8 to 10 independent FP64 chains in
+        // flight: the pass is bound by FP64 latency x chain depth otherwise)
+        double x[2][4];
+#pragma unroll
+        for (int c = 0; c < 2; ++c)
+#pragma unroll
+          for (int r = 0; r < 4; ++r) x[c][r] = C[r][0] * (c ? uu[0].y : uu[0].x);
+#pragma unroll
+        for (int t = 1; t < kWin; ++t)
+#pragma unroll
+          for (int c = 0; c < 2; ++c)
+#pragma unroll
+            for (int r = 0; r < 4; ++r) x[c][r] = fma(C[r][t], c ? uu[t].y : uu[t].x, x[c][r]);
+        double wv[2][4];
+#pragma unroll
+        for (int c = 0; c < 2; ++c)
+#pragma unroll
+          for (int r = 0; r < 4; ++r) wv[c][r] = vr[4 * c + r] * x[c][r];
+#pragma unroll
+        for (int r = 0; r < 4; ++r) {
+          if (r & 1) {
+            acc1 = fma(wv[0][r], x[0][r], acc1);
+            acc3 = fma(wv[1][r], x[1][r], acc3);
+          } else {
+            acc0 = fma(wv[0][r], x[0][r], acc0);
+            acc2 = fma(wv[1][r], x[1][r], acc2);
+          }
+        }
+        double pt[2][kWin];
+#pragma unroll
+        for (int c = 0; c < 2; ++c)
+#pragma unroll
+          for (int t = 0; t < kWin; ++t) pt[c][t] = C[0][t] * wv[c][0];
+#pragma unroll
+        for (int r = 1; r < 4; ++r)
+#pragma unroll
+          for (int c = 0; c < 2; ++c)
+#pragma unroll
+            for (int t = 0; t < kWin; ++t) pt[c][t] = fma(C[r][t], wv[c][r], pt[c][t]);
+#pragma unroll
+        for (int t = 0; t < kWin; ++t) sts2_s(pb0 + 8 * B * kPBuf + 16 * t, pt[0][t], pt[1][t]);
+      }
+      __syncwarp();
+      if (lane == 0) mbar_arrive_s(wbar0 + 8 * B);
+      TCK(t2_);
+      load_v(vr);  // two chunks ahead
+      TCK(t3_);
+#ifdef KG_SLAB_TIMING
+      tw_ += t1_ - t0_, tc_ += t2_ - t1_, tl_ += t3_ - t2_;
+#endif
+    };
+    int q = 0;
+    unsigned par = 0;
+    for (; q + kDepth <= qtot; q += kDepth, par ^= 1u) {
+      body(0, par, vv[0]);
+      body(1, par, vv[1]);
+      body(2, par, vv[0]);
+      body(3, par, vv[1]);
+    }
+    if (q < qtot) body(0, par, vv[0]);
+    if (q + 1 < qtot) body(1, par, vv[1]);
+    if (q + 2 < qtot) body(2, par, vv[0]);
+#ifdef KG_SLAB_TIMING
+    if (blockIdx.x == 0 && lane == 0)
+      printf("row warp %d: chunks %d wait U %lld compute %lld load_v %lld (cycles per chunk)\n", warp, qtot, tw_ / qtot,
+             tc_ / qtot, tl_ / qtot);
+#endif
+  } else {
+    // --------------------------------------------------------- tensor warps
+    asm volatile("setmaxnreg.dec.sync.aligned.u32 104;");
+    const int tw = warp - 8;
+    const bool gact = tw < ((p1 + 7) >> 3);   // this warp owns p1 rows 8 tw .. 8 tw + 7
+    const bool leader = tid == 8 * 32;
+    const int zr = 8 * tw + (lane >> 2), zq = 2 * (lane & 3);
+    const unsigned ua0 = smem_u32(Us + zr * kLdr + zq);  // U store (tile 0)
+    const unsigned sbar0 = smem_u32(&sbar[0]);
+    // S3 tile of round r: the leader posts the byte count, then lane 0 of every
+    // tensor warp issues its share of the p2 column copies (issue_s_cols)
+    auto issue_s_tx = [&](int r) {
+      if (r < rounds) mbar_expect_tx(&sbar[r & 1], static_cast<unsigned>(p1 * 8) * p2);
+    };
+    auto issue_s_cols = [&](int r) {
+      if (r >= rounds) return;
+      const unsigned bytes = static_cast<unsigned>(p1 * 8);
+      const double* src = a.S + (blockIdx.x + static_cast<i64>(r) * gridDim.x) * p12;
+      double* dst = Ss + (r & 1) * sbuf;
+      for (int k = tw; k < p2; k += 8) bulk_g2s(dst + ldS * k, src + static_cast<i64>(p1) * k, bytes, &sbar[r & 1]);
+    };
+    // gather slots of basis function zr as byte addresses in partial tile 0 (column pair lane & 3)
+    unsigned gs[G];
+    {
+      int4 g4 = make_int4(0, 0, 0, 0);
+      const int zs = PL - 1;
+      if (gact) g4 = __ldg(reinterpret_cast<const int4*>(a.gat) + zr);
+      else g4.x = g4.y = g4.z = g4.w = zs | (zs << 16);
+      const unsigned pl0 = smem_u32(Ps) + 16u * static_cast<unsigned>((lane & 3) * PL);
+      const int w4[4] = {g4.x, g4.y, g4.z, g4.w};
+#pragma unroll
+      for (int k = 0; k < G; ++k) gs[k] = pl0 + 16u * ((static_cast<unsigned>(w4[k >> 1]) >> (16 * (k & 1))) & 0xffffu);
+    }
+    // L2 prefetch of the v chunks a.pf ahead (a chunk is contiguous: 8 columns of n1)
+    const bool pfl = lane == 0 && a.pf > 0;  // lane 0 of tensor warp tw prefetches the chunks = tw (mod 8)
+    int fq = 0;
+    const double* fp = a.v + blockIdx.x * n12;
+    int fr = 0, fc = 0;
+    auto prefetch_v = [&]() {
+      if (fr < rounds && (fq++ & 7) == tw) bulk_prefetch_l2(fp, static_cast<unsigned>(min(8, n2 - 8 * fc) * n1 * 8));
+      if (++fc == nch) {
+        fc = 0;
+        ++fr;
+        fp += static_cast<i64>(gridDim.x) * n12 - static_cast<i64>(n1) * 8 * (nch - 1);
+      } else {
+        fp += static_cast<i64>(n1) * 8;
+      }
+    };
+    if (leader) {
+      fence_proxy_async();
+      issue_s_tx(0);
+      issue_s_tx(1);
+    }
+    nb_sync(kBarTensor, kSlabBS - 256);
+    if (lane == 0) {
+      issue_s_cols(0);
+      issue_s_cols(1);
+    }
+    if (pfl)
+      for (int k = 0; k < a.pf; ++k) prefetch_v();
+    // U-step cursor: chunk ca of round ra; tables through running shared addresses
+    int ra = 0, ca = 0;
+    const unsigned tu0 = smem_u32(Tu) + 8u * lane, tz0 = smem_u32(Tz) + 8u * lane, ti0 = smem_u32(Ti);
+    unsigned tup = tu0, tia = ti0 + 4;        // Tu[ca][.][lane], w0 of chunk ca
+    unsigned sa = smem_u32(Ss + zr + ldS * (lane & 3));  // S3 tile of round ra: rows zr, columns (lane & 3) + .
+    const unsigned sflip = 8u * static_cast<unsigned>(sbuf);
+    auto stage_a = [&](const int B) {  // U(ra, ca) into U tile B
+      if (ca == 0) mbar_wait_s(sbar0 + 8 * (ra & 1), static_cast<unsigned>((ra >> 1) & 1));
+      if (gact && !(a.dbg & 16)) {
+        const int wz = ldsi_s(tia);
+        const double b0 = lds_s(tup), b1 = lds_s(tup + 256);
+        const unsigned sr = sa + 8u * static_cast<unsigned>(ldS * wz);
+        double d0 = 0.0, d1 = 0.0, e0 = 0.0, e1 = 0.0;  // two independent DMMAs
+        dmma(d0, d1, lds_s(sr), b0);
+        dmma(e0, e1, lds_s(sr + 32u * static_cast<unsigned>(ldS)), b1);
+        sts2_s(ua0 + 8 * B * kUBuf, d0 + e0, d1 + e1);
+      }
+      __syncwarp();
+      if (lane == 0) mbar_arrive_s(ubar0 + 8 * B);
+      if (++ca == nch) {
+        ca = 0;
+        tup = tu0;
+        tia = ti0 + 4;
+        // that round's S3 tile is free once every tensor warp formed its last U
+        nb_sync(kBarTensor, kSlabBS - 256);
+        if (leader) {
+          fence_proxy_async();
+          issue_s_tx(ra + 2);
+        }
+        nb_sync(kBarTensor, kSlabBS - 256);
+        if (lane == 0) {
+          fence_proxy_async();
+          issue_s_cols(ra + 2);
+        }
+        ++ra;
+        sa = (ra & 1) ? sa + sflip : sa - sflip;
+      } else {
+        tup += 512;
+        tia += 8;
+      }
+    };
+    stage_a(0);
+    stage_a(1);
+    stage_a(2);
+    stage_a(3);
+    int T = -1, c = 0, nst = qtot - kDepth;   // nst: U steps left
+    unsigned tzp = tz0, tiz = ti0;            // Tz[c][.][lane], tz of chunk c
+    double z00 = 0.0, z01 = 0.0, z10 = 0.0, z11 = 0.0;
+    double* qs = a.Q + blockIdx.x * p12 + zr + static_cast<i64>(p1) * zq;
+    const i64 qstep = static_cast<i64>(gridDim.x) * p12;
+    auto flush = [&](int k, double x0, double x1) {
+      const int zc = 8 * k + zq;
+      if (zr < p1 && zc < p2) qs[static_cast<i64>(p1) * (8 * k)] = x0;
+      if (zr < p1 && zc + 1 < p2) qs[static_cast<i64>(p1) * (8 * k + 1)] = x1;
+    };
+#ifdef KG_SLAB_TIMING
+    long long tw_ = 0, tc_ = 0, tl_ = 0;
+    long long t0_, t1_, t2_, t3_;
+#endif
+    auto body = [&](const int B, unsigned par) {
+      if (pfl) prefetch_v();
+      TCK(t0_);
+      mbar_wait_s(wbar0 + 8 * B, par);
+      TCK(t1_);
+      if (gact && !(a.dbg & 2)) {
+        // Y(zr, columns zq, zq + 1) = sum of the quads' partials, ascending quads
+        double2 g[G];
+#pragma unroll
+        for (int k = 0; k < G; ++k) g[k] = lds2_s(gs[k] + 8 * B * kPBuf);
+        const int tz = ldsi_s(tiz);
+        const double zb0 = lds_s(tzp), zb1 = lds_s(tzp + 256);
+        // pairwise (a fixed order; depth 3 instead of G - 1)
+        double y0 = (g[0].x + g[1].x) + (g[2].x + g[3].x);
+        double y1 = (g[0].y + g[1].y) + (g[2].y + g[3].y);
+        if (G > 6) {
+          y0 += (g[4].x + g[5].x) + (g[G - 2].x + g[G - 1].x);
+          y1 += (g[4].y + g[5].y) + (g[G - 2].y + g[G - 1].y);
+        } else {
+          y0 += g[4].x + g[5].x;
+          y1 += g[4].y + g[5].y;
+        }
+        const int t0 = tz & 0xffff;
+        if (T < 0) T = t0;
+        while (T < t0) {  // tile T is complete: later chunks start at t0 > T
+          flush(T, z00, z01);
+          z00 = z10;
+          z01 = z11;
+          z10 = z11 = 0.0;
+          ++T;
+        }
+        dmma(z00, z01, y0, zb0);
+        dmma(z00, z01, y1, zb1);
+        if (tz >> 16) {
+          dmma(z10, z11, y0, lds_s(tzp + 512));
+          dmma(z10, z11, y1, lds_s(tzp + 768));
+        }
+      }
+      if (++c == nch) {  // slice done: the live window holds its last two tiles
+        if (gact) {
+          flush(T, z00, z01);
+          flush(T + 1, z10, z11);
+          z00 = z01 = z10 = z11 = 0.0;
+          T = -1;
+        }
+        c = 0;
+        qs += qstep;
+        tzp = tz0;
+        tiz = ti0;
+      } else {
+        tzp += 1024;
+        tiz += 8;
+      }
+      // U(q + kDepth) into U tile B (every row warp has read it: their arrivals
+      // on wbar[B] were observed above)
+      TCK(t2_);
+      if (nst > 0) {
+        --nst;
+        stage_a(B);
+      }
+      TCK(t3_);
+#ifdef KG_SLAB_TIMING
+      tw_ += t1_ - t0_, tc_ += t2_ - t1_, tl_ += t3_ - t2_;
+#endif
+    };
+    int q = 0;
+    unsigned par = 0;
+    for (; q + kDepth <= qtot; q += kDepth, par ^= 1u) {
+      body(0, par);
+      body(1, par);
+      body(2, par);
+      body(3, par);
+    }
+    if (q < qtot) body(0, par);
+    if (q + 1 < qtot) body(1, par);
+    if (q + 2 < qtot) body(2, par);
+#ifdef KG_SLAB_TIMING
+    if (blockIdx.x == 0 && lane == 0)
+      printf("tensor warp %d: chunks %d wait W %lld gather+Z %lld U step %lld (cycles per chunk)\n", warp, qtot, tw_ / qtot,
+             tc_ / qtot, tl_ / qtot);
+#endif
+  }
+  double rr = warp_sum_s((acc0 + acc1) + (acc2 + acc3));
+  __syncthreads();
+  if (lane == 0) red[warp] = rr;
+  __syncthreads();
+  if (warp == 0) {
+    rr = lane < (kSlabBS >> 5) ? red[lane] : 0.0;
+    rr = warp_sum_s(rr);
+    if (lane == 0) a.partial[blockIdx.x] = rr;
+  }
+}
+
 // Y in scatter/gather form (k_slab2) when the design has a gather table;
 // KG_SLAB_DMMA=1 (developer switch) keeps the DMMA form (k_slab).
 static bool slab_gather(const SlabArgs& a) {
   static const bool dmma_y = dev_env("KG_SLAB_DMMA") != nullptr;
-  return !dmma_y && a.gat && a.gmax > 0 && a.gmax <= 8 && a.PL > 0;
+  return !dmma_y && a.gat && a.gmax > 0 && a.gmax <= 8 && a.PL > 0 && a.PL <= kPLMax;
 }
 
 // Leading dimensions and shared-memory size of a slab plan.
@@ -764,8 +1239,10 @@ static size_t slab_layout(SlabArgs& a) {
   a.ldW = (a.n1 + 15) / 16 * 16 + 4;         // = 4 (mod 16): B fragments of stage C
   a.cg = 1;
   const size_t ubuf = static_cast<size_t>(kLdr) * 8 * ((a.p1 + 7) / 8);
-  const size_t tile = slab_gather(a) ? static_cast<size_t>(8) * a.PL : static_cast<size_t>(a.ldW) * 8;
-  const size_t dbl = 2 * static_cast<size_t>(a.ldS) * a.p2 + kDepth * ubuf + kDepth * tile;
+  if (slab_gather(a))  // k_slab4: fixed-stride U / partial tiles and the X2 chunk tables
+    return (2 * static_cast<size_t>(a.ldS) * a.p2 + kDepth * static_cast<size_t>(kUBuf + kPBuf) +
+            static_cast<size_t>(a.nch) * (128 + 64 + 1)) * sizeof(double);
+  const size_t dbl = 2 * static_cast<size_t>(a.ldS) * a.p2 + kDepth * ubuf + kDepth * static_cast<size_t>(a.ldW) * 8;
   return dbl * sizeof(double);
 }
 
@@ -809,7 +1286,14 @@ void slab_pass(const Launch& L, const SlabArgs& a0) {
     static const int dbg = [] { const char* e = dev_env("KG_SLAB_DBG"); return e ? std::atoi(e) : 0; }();
     a.dbg = dbg;
     static const bool mb = dev_env("KG_SLAB_NB") == nullptr;
-    if (vs == 3 && mb) {
+    static const bool k2 = dev_env("KG_SLAB_K2") != nullptr;
+    if (!k2 && a.gmax <= 6) {
+      smem_attr(k_slab4<6>, static_cast<int>(smem));
+      k_slab4<6><<<g, kSlabBS, smem, L.s>>>(a);
+    } else if (!k2) {
+      smem_attr(k_slab4<8>, static_cast<int>(smem));
+      k_slab4<8><<<g, kSlabBS, smem, L.s>>>(a);
+    } else if (vs == 3 && mb) {
       smem_attr(k_slab2<3, true>, static_cast<int>(smem));
       k_slab2<3, true><<<g, kSlabBS, smem, L.s>>>(a);
     } else if (mb) {
