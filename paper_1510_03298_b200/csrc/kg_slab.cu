@@ -748,21 +748,24 @@ __global__ void __launch_bounds__(kSlabBS, 1) k_slab2(SlabArgs a) {
 
 }  // namespace
 
-// k_slab4: k_slab2 with the per-chunk instruction count of both roles cut to
-// the arithmetic.  The pass is bound by issue latency (16 warps per SM, ~10
-// cycles between a warp's instructions), not by HBM or the FP64 pipe: with
-// every FP64 instruction removed it still took 75% of its time.  So:
-//   * the U and partial tiles have fixed strides (kUBuf, kPBuf) and the chunk
-//     loops are unrolled over the kDepth buffers: buffer offsets and barrier
-//     parities are immediates;
-//   * barriers are addressed by precomputed 32-bit shared addresses;
-//   * v is read through a running pointer, with an unpredicated path for full
-//     chunks;
-//   * the X2 chunk tables sit in shared memory (one copy per CTA instead of
-//     eight L1-missing global loads per tensor warp and chunk) and are read
-//     through running pointers; the gather slots are byte offsets in registers;
-//   * the L2 prefetch of v is issued by the tensor-warp leader;
-//   * setmaxnreg: tensor warpgroups 104 registers, row warpgroups 152.
+// k_slab4: the scatter/gather pass with every operand stream on the engine
+// that suits it (measured on B200: the register-staged v stream of k_slab2 is
+// capped by the warp's scoreboards at two chunks in flight, ~32 KB per SM,
+// which bounds the pass at ~140 us before any arithmetic; the issue latency of
+// 16 resident warps bounds the rest):
+//   * v arrives by cp.async.bulk (one 16 KB copy per chunk, contiguous in the
+//     array) into a four-chunk shared ring behind mbarriers, issued two pairs
+//     ahead by the tensor-warp leader, plus an L2 prefetch further ahead; row
+//     threads read their 4 x 2 cells with swizzled 16-byte loads (the upper
+//     half of each quad group takes rows 2,3 first: conflict free);
+//   * the S3 operands of the U step (2 doubles per lane and chunk) come
+//     straight from L2 one pair ahead, so no S3 tile, no tile barrier;
+//   * chunks are handed over in pairs through mbarriers (one arrival per
+//     warp); U and partial tiles have fixed strides, so all buffer offsets are
+//     immediates; the X2 chunk tables sit in shared memory; the gather slots
+//     are shared addresses in registers;
+//   * the FP64 chains of a chunk are issued level by level (8 to 10
+//     independent chains); setmaxnreg: tensor warpgroups 104, row warpgroups 152.
 constexpr int kPLMax = 322;                 // slots per column-pair plane at n1 = 256
 constexpr int kPBuf = 8 * kPLMax;           // doubles per partial tile
 constexpr int kUBuf = kLdr * 64;            // doubles per U tile (p1 <= 64)
@@ -814,19 +817,20 @@ __device__ __forceinline__ void sts2_s(unsigned addr, double x, double y) {
   asm volatile("st.shared.v2.f64 [%0], {%1, %2};" ::"r"(addr), "d"(x), "d"(y) : "memory");
 }
 
+constexpr int kVBuf = 8 * 256;              // doubles per v chunk tile (n1 <= 256)
+
 // G: gather slots per basis function (6 or 8).
 template <int G>
 __global__ void __launch_bounds__(kSlabBS, 1) k_slab4(SlabArgs a) {
   using namespace async;
   extern __shared__ __align__(128) double sm[];
   __shared__ double red[32];
-  __shared__ unsigned long long sbar[2];     // the two S3 tiles
-  __shared__ unsigned long long ubar[kDepth], wbar[kDepth];  // U(q) formed / partials of chunk q stored (one arrival per warp)
+  // pair hb: U(pair) formed / its partials stored (one arrival per warp) / its v chunks landed
+  __shared__ unsigned long long ubar[2], wbar[2], vbar[2];
   const int n1 = a.n1, n2 = a.n2, p1 = a.p1, p2 = a.p2, nch = a.nch;
-  const int ldS = a.ldS, PL = a.PL;
-  const int sbuf = ldS * p2;                  // one S3 tile
-  double* Ss = sm;                            // [2][ldS x p2]
-  double* Us = Ss + 2 * sbuf;                 // [kDepth][kUBuf]
+  const int PL = a.PL;
+  double* Vs = sm;                            // [kDepth][kVBuf]  v chunks (8 columns of n1)
+  double* Us = Vs + kDepth * kVBuf;           // [kDepth][kUBuf]
   double* Ps = Us + kDepth * kUBuf;           // [kDepth][kPBuf]
   double* Tz = Ps + kDepth * kPBuf;           // [nch][128]  Z-step B fragments
   double* Tu = Tz + nch * 128;                // [nch][64]   U-step B fragments
@@ -834,18 +838,16 @@ __global__ void __launch_bounds__(kSlabBS, 1) k_slab4(SlabArgs a) {
   const int tid = threadIdx.x, lane = tid & 31, warp = tid >> 5;
   const i64 p12 = static_cast<i64>(p1) * p2, n12 = static_cast<i64>(n1) * n2;
   const int rounds = static_cast<int>((a.m3 - blockIdx.x + gridDim.x - 1) / gridDim.x);  // slices of this CTA
-  const int qtot = rounds * nch;
-  const unsigned ubar0 = smem_u32(&ubar[0]), wbar0 = smem_u32(&wbar[0]);
+  const int qtot = rounds * nch, np = qtot >> 1;
+  const unsigned ubar0 = smem_u32(&ubar[0]), wbar0 = smem_u32(&wbar[0]), vbar0 = smem_u32(&vbar[0]);
   if (tid == 0) {
-    mbar_init(&sbar[0], 1);
-    mbar_init(&sbar[1], 1);
-    for (int k = 0; k < kDepth; ++k) {
+    for (int k = 0; k < 2; ++k) {
       mbar_init(&ubar[k], 8);
       mbar_init(&wbar[k], 8);
+      mbar_init(&vbar[k], 1);
     }
     mbar_init_fence();
   }
-  for (int k = tid; k < 2 * sbuf; k += kSlabBS) Ss[k] = 0.0;
   for (int k = tid; k < nch * 128; k += kSlabBS) Tz[k] = __ldg(a.x2z + k);
   for (int k = tid; k < nch * 64; k += kSlabBS) Tu[k] = __ldg(a.x2u + k);
   for (int k = tid; k < nch; k += kSlabBS) {
@@ -865,6 +867,10 @@ __global__ void __launch_bounds__(kSlabBS, 1) k_slab4(SlabArgs a) {
     const bool act = tid < 4 * nq;
     const int rq = act ? tid % nq : 0, cp = act ? tid / nq : 0;
     const int r0 = 4 * rq, c0 = 2 * cp;        // rows r0 .. r0 + 3, chunk columns c0, c0 + 1
+    // quads 4 apart are 128 bytes apart in a v column: the upper half of each
+    // group of 8 quads holds its rows in the order 2, 3, 0, 1, so that the
+    // 16-byte v loads of a quarter warp hit 8 distinct bank groups
+    const bool sw = (rq >> 2) & 1;
     int lo = 0;
     double C[4][kWin];
 #pragma unroll
@@ -875,8 +881,9 @@ __global__ void __launch_bounds__(kSlabBS, 1) k_slab4(SlabArgs a) {
       lo = min(__ldg(a.H1.lo + r0), p1 - kWin);
 #pragma unroll
       for (int r = 0; r < 4; ++r) {
-        const int l = __ldg(a.H1.lo + r0 + r), len = __ldg(a.H1.len + r0 + r);
-        const double* cf = a.H1.coef + __ldg(a.H1.off + r0 + r);
+        const int row = r0 + (sw ? (r ^ 2) : r);
+        const int l = __ldg(a.H1.lo + row), len = __ldg(a.H1.len + row);
+        const double* cf = a.H1.coef + __ldg(a.H1.off + row);
 #pragma unroll
         for (int t = 0; t < kWin; ++t) {
           const int j = lo + t - l;
@@ -886,66 +893,23 @@ __global__ void __launch_bounds__(kSlabBS, 1) k_slab4(SlabArgs a) {
     }
     const unsigned ub0 = smem_u32(Us + lo * kLdr + c0);
     const unsigned pb0 = smem_u32(Ps) + 16u * static_cast<unsigned>(cp * PL + rq * kWin);
-    // v of the next chunk to load: rows r0 .. r0 + 3 of chunk columns c0, c0 + 1
-    const double* vp = a.v + blockIdx.x * n12 + r0 + static_cast<i64>(n1) * c0;
-    const i64 vchunk = static_cast<i64>(n1) * 8;
-    const i64 vjump = static_cast<i64>(gridDim.x) * n12 - vchunk * (nch - 1);  // last chunk of a slice -> first of the next
-    const bool lastfull = 8 * nch == n2;       // the last chunk of a slice has all 8 columns
-    const int lcols = n2 - 8 * (nch - 1) - c0; // valid columns of this thread's pair in the last chunk
-    int lr = 0, lc = 0;                        // (round, chunk) of vp
-    auto load_v = [&](double (&vr)[8]) {
-      if (lr < rounds && (lastfull || lc != nch - 1)) {
-        if (act && !(a.dbg & 1)) {
-          const double2 x0 = ldg2_stream(vp), x1 = ldg2_stream(vp + 2);
-          const double2 y0 = ldg2_stream(vp + n1), y1 = ldg2_stream(vp + n1 + 2);
-          vr[0] = x0.x, vr[1] = x0.y, vr[2] = x1.x, vr[3] = x1.y;
-          vr[4] = y0.x, vr[5] = y0.y, vr[6] = y1.x, vr[7] = y1.y;
-        }
-      } else {
-#pragma unroll
-        for (int k = 0; k < 8; ++k) vr[k] = 0.0;
-        if (act && lr < rounds) {
-          if (lcols > 0) {
-            const double2 x0 = ldg2_stream(vp), x1 = ldg2_stream(vp + 2);
-            vr[0] = x0.x, vr[1] = x0.y, vr[2] = x1.x, vr[3] = x1.y;
-          }
-          if (lcols > 1) {
-            const double2 y0 = ldg2_stream(vp + n1), y1 = ldg2_stream(vp + n1 + 2);
-            vr[4] = y0.x, vr[5] = y0.y, vr[6] = y1.x, vr[7] = y1.y;
-          }
-        }
-      }
-      if (++lc == nch) {
-        lc = 0;
-        ++lr;
-        vp += vjump;
-      } else {
-        vp += vchunk;
-      }
-    };
-    double vv[2][8];
-#pragma unroll
-    for (int k = 0; k < 8; ++k) vv[0][k] = vv[1][k] = 0.0;
-    load_v(vv[0]);
-    load_v(vv[1]);
-    // chunk q = 4 i + B: U(q) in U tile B, its partials into partial tile B, barrier parity i & 1
-#ifdef KG_SLAB_TIMING
-    long long tw_ = 0, tc_ = 0, tl_ = 0;
-#define TCK(x) x = clock64()
-    long long t0_, t1_, t2_, t3_;
-#else
-#define TCK(x)
-#endif
-    auto body = [&](const int B, unsigned par, double (&vr)[8]) {
-      TCK(t0_);
-      mbar_wait_s(ubar0 + 8 * B, par);
-      TCK(t1_);
+    const unsigned vb0 = smem_u32(Vs + r0 + n1 * c0) + (sw ? 16u : 0u);   // rows (sw ? 2,3 : 0,1) of column c0
+    const unsigned vb1 = smem_u32(Vs + r0 + n1 * c0) + (sw ? 0u : 16u);   // the other two rows
+    const unsigned vcol = 8u * static_cast<unsigned>(n1);
+    // chunk j of a pair: U window at uo, partials to po, v tile at byte offset vo
+    auto body = [&](const int j, const unsigned uo, const unsigned po, const unsigned vo) {
       if (act && !(a.dbg & 4)) {
         double2 uu[kWin];
 #pragma unroll
-        for (int t = 0; t < kWin; ++t) uu[t] = lds2_s(ub0 + 8 * (B * kUBuf + t * kLdr));
-        // level by level over the 8 cells (8 to 10 independent FP64 chains in
-        // flight: the pass is bound by FP64 latency x chain depth otherwise)
+        for (int t = 0; t < kWin; ++t) uu[t] = lds2_s(uo + 8 * (j * kUBuf + t * kLdr));
+        double vr[8];
+        {
+          const double2 x0 = lds2_s(vb0 + vo + 8 * j * kVBuf), x1 = lds2_s(vb1 + vo + 8 * j * kVBuf);
+          const double2 y0 = lds2_s(vb0 + vo + 8 * j * kVBuf + vcol), y1 = lds2_s(vb1 + vo + 8 * j * kVBuf + vcol);
+          vr[0] = x0.x, vr[1] = x0.y, vr[2] = x1.x, vr[3] = x1.y;
+          vr[4] = y0.x, vr[5] = y0.y, vr[6] = y1.x, vr[7] = y1.y;
+        }
+        // level by level over the 8 cells (8 to 10 independent FP64 chains in flight)
         double x[2][4];
 #pragma unroll
         for (int c = 0; c < 2; ++c)
@@ -984,33 +948,19 @@ __global__ void __launch_bounds__(kSlabBS, 1) k_slab4(SlabArgs a) {
 #pragma unroll
             for (int t = 0; t < kWin; ++t) pt[c][t] = fma(C[r][t], wv[c][r], pt[c][t]);
 #pragma unroll
-        for (int t = 0; t < kWin; ++t) sts2_s(pb0 + 8 * B * kPBuf + 16 * t, pt[0][t], pt[1][t]);
+        for (int t = 0; t < kWin; ++t) sts2_s(po + 8 * j * kPBuf + 16 * t, pt[0][t], pt[1][t]);
       }
-      __syncwarp();
-      if (lane == 0) mbar_arrive_s(wbar0 + 8 * B);
-      TCK(t2_);
-      load_v(vr);  // two chunks ahead
-      TCK(t3_);
-#ifdef KG_SLAB_TIMING
-      tw_ += t1_ - t0_, tc_ += t2_ - t1_, tl_ += t3_ - t2_;
-#endif
     };
-    int q = 0;
-    unsigned par = 0;
-    for (; q + kDepth <= qtot; q += kDepth, par ^= 1u) {
-      body(0, par, vv[0]);
-      body(1, par, vv[1]);
-      body(2, par, vv[0]);
-      body(3, par, vv[1]);
+    for (int ip = 0; ip < np; ++ip) {
+      const unsigned hb = static_cast<unsigned>(ip & 1), par = static_cast<unsigned>(ip >> 1) & 1u;
+      mbar_wait_s(ubar0 + 8 * hb, par);
+      mbar_wait_s(vbar0 + 8 * hb, par);
+      const unsigned uo = ub0 + hb * (16 * kUBuf), po = pb0 + hb * (16 * kPBuf), vo = hb * (16 * kVBuf);
+      body(0, uo, po, vo);
+      body(1, uo, po, vo);
+      __syncwarp();
+      if (lane == 0) mbar_arrive_s(wbar0 + 8 * hb);
     }
-    if (q < qtot) body(0, par, vv[0]);
-    if (q + 1 < qtot) body(1, par, vv[1]);
-    if (q + 2 < qtot) body(2, par, vv[0]);
-#ifdef KG_SLAB_TIMING
-    if (blockIdx.x == 0 && lane == 0)
-      printf("row warp %d: chunks %d wait U %lld compute %lld load_v %lld (cycles per chunk)\n", warp, qtot, tw_ / qtot,
-             tc_ / qtot, tl_ / qtot);
-#endif
   } else {
     // --------------------------------------------------------- tensor warps
     asm volatile("setmaxnreg.dec.sync.aligned.u32 104;");
@@ -1018,21 +968,9 @@ __global__ void __launch_bounds__(kSlabBS, 1) k_slab4(SlabArgs a) {
     const bool gact = tw < ((p1 + 7) >> 3);   // this warp owns p1 rows 8 tw .. 8 tw + 7
     const bool leader = tid == 8 * 32;
     const int zr = 8 * tw + (lane >> 2), zq = 2 * (lane & 3);
+    const bool zok = zr < p1;
     const unsigned ua0 = smem_u32(Us + zr * kLdr + zq);  // U store (tile 0)
-    const unsigned sbar0 = smem_u32(&sbar[0]);
-    // S3 tile of round r: the leader posts the byte count, then lane 0 of every
-    // tensor warp issues its share of the p2 column copies (issue_s_cols)
-    auto issue_s_tx = [&](int r) {
-      if (r < rounds) mbar_expect_tx(&sbar[r & 1], static_cast<unsigned>(p1 * 8) * p2);
-    };
-    auto issue_s_cols = [&](int r) {
-      if (r >= rounds) return;
-      const unsigned bytes = static_cast<unsigned>(p1 * 8);
-      const double* src = a.S + (blockIdx.x + static_cast<i64>(r) * gridDim.x) * p12;
-      double* dst = Ss + (r & 1) * sbuf;
-      for (int k = tw; k < p2; k += 8) bulk_g2s(dst + ldS * k, src + static_cast<i64>(p1) * k, bytes, &sbar[r & 1]);
-    };
-    // gather slots of basis function zr as byte addresses in partial tile 0 (column pair lane & 3)
+    // gather slots of basis function zr as shared addresses in partial tile 0 (column pair lane & 3)
     unsigned gs[G];
     {
       int4 g4 = make_int4(0, 0, 0, 0);
@@ -1044,102 +982,112 @@ __global__ void __launch_bounds__(kSlabBS, 1) k_slab4(SlabArgs a) {
 #pragma unroll
       for (int k = 0; k < G; ++k) gs[k] = pl0 + 16u * ((static_cast<unsigned>(w4[k >> 1]) >> (16 * (k & 1))) & 0xffffu);
     }
-    // L2 prefetch of the v chunks a.pf ahead (a chunk is contiguous: 8 columns of n1)
-    const bool pfl = lane == 0 && a.pf > 0;  // lane 0 of tensor warp tw prefetches the chunks = tw (mod 8)
-    int fq = 0;
-    const double* fp = a.v + blockIdx.x * n12;
-    int fr = 0, fc = 0;
+    // v stream (leader): chunk pairs by bulk copy into the ring, L2 prefetch a.pf chunks ahead
+    const i64 vchunk = static_cast<i64>(n1) * 8;
+    const i64 vjump = static_cast<i64>(gridDim.x) * n12 - vchunk * (nch - 1);  // last chunk of a slice -> first of the next
+    const double* vp = a.v + blockIdx.x * n12;   // next chunk to copy
+    int vc = 0, vq = 0;
+    const unsigned vbytes = static_cast<unsigned>(vchunk * 8);
+    const unsigned vs0 = smem_u32(Vs);
+    auto copy_pair = [&](unsigned hb) {          // the next two chunks into pair hb's tiles
+      if (vq >= qtot) return;
+      const unsigned bar = vbar0 + 8 * hb;
+      asm volatile("mbarrier.arrive.expect_tx.shared::cta.b64 _, [%0], %1;" ::"r"(bar), "r"(2 * vbytes) : "memory");
+#pragma unroll
+      for (int j = 0; j < 2; ++j) {
+        asm volatile("cp.async.bulk.shared::cluster.global.mbarrier::complete_tx::bytes [%0], [%1], %2, [%3];" ::"r"(
+                         vs0 + 8u * static_cast<unsigned>((2 * hb + j) * kVBuf)),
+                     "l"(vp), "r"(vbytes), "r"(bar)
+                     : "memory");
+        ++vq;
+        if (++vc == nch) {
+          vc = 0;
+          vp += vjump;
+        } else {
+          vp += vchunk;
+        }
+      }
+    };
+    const double* fp = a.v + blockIdx.x * n12;   // next chunk to prefetch
+    int fc = 0, fq = 0;
     auto prefetch_v = [&]() {
-      if (fr < rounds && (fq++ & 7) == tw) bulk_prefetch_l2(fp, static_cast<unsigned>(min(8, n2 - 8 * fc) * n1 * 8));
+      if (fq < qtot) bulk_prefetch_l2(fp, vbytes);
+      ++fq;
       if (++fc == nch) {
         fc = 0;
-        ++fr;
-        fp += static_cast<i64>(gridDim.x) * n12 - static_cast<i64>(n1) * 8 * (nch - 1);
+        fp += vjump;
       } else {
-        fp += static_cast<i64>(n1) * 8;
+        fp += vchunk;
       }
     };
     if (leader) {
       fence_proxy_async();
-      issue_s_tx(0);
-      issue_s_tx(1);
+      copy_pair(0);
+      copy_pair(1);
+      for (int k = 0; k < 4 + a.pf; ++k) prefetch_v();  // the ring's four chunks are on their way already
     }
-    nb_sync(kBarTensor, kSlabBS - 256);
-    if (lane == 0) {
-      issue_s_cols(0);
-      issue_s_cols(1);
-    }
-    if (pfl)
-      for (int k = 0; k < a.pf; ++k) prefetch_v();
-    // U-step cursor: chunk ca of round ra; tables through running shared addresses
-    int ra = 0, ca = 0;
+    // U step: chunk ca of the slice at sp; S3 operands from L2, loaded one pair ahead
     const unsigned tu0 = smem_u32(Tu) + 8u * lane, tz0 = smem_u32(Tz) + 8u * lane, ti0 = smem_u32(Ti);
-    unsigned tup = tu0, tia = ti0 + 4;        // Tu[ca][.][lane], w0 of chunk ca
-    unsigned sa = smem_u32(Ss + zr + ldS * (lane & 3));  // S3 tile of round ra: rows zr, columns (lane & 3) + .
-    const unsigned sflip = 8u * static_cast<unsigned>(sbuf);
-    auto stage_a = [&](const int B) {  // U(ra, ca) into U tile B
-      if (ca == 0) mbar_wait_s(sbar0 + 8 * (ra & 1), static_cast<unsigned>((ra >> 1) & 1));
-      if (gact && !(a.dbg & 16)) {
+    int ca = 0, sleft = rounds;                  // sleft: slices left for the U step
+    unsigned tup = tu0, tia = ti0 + 4;           // Tu[ca][.][lane], w0 of chunk ca
+    const double* sp = a.S + blockIdx.x * p12 + zr + static_cast<i64>(p1) * (lane & 3);
+    const i64 sstep = static_cast<i64>(gridDim.x) * p12;
+    struct UOp { double s0, s1, b0, b1; };
+    auto load_u = [&]() {                        // operands of U(ca), then advance the cursor
+      UOp o{0.0, 0.0, 0.0, 0.0};
+      if (gact && sleft > 0 && !(a.dbg & 16)) {
         const int wz = ldsi_s(tia);
-        const double b0 = lds_s(tup), b1 = lds_s(tup + 256);
-        const unsigned sr = sa + 8u * static_cast<unsigned>(ldS * wz);
-        double d0 = 0.0, d1 = 0.0, e0 = 0.0, e1 = 0.0;  // two independent DMMAs
-        dmma(d0, d1, lds_s(sr), b0);
-        dmma(e0, e1, lds_s(sr + 32u * static_cast<unsigned>(ldS)), b1);
-        sts2_s(ua0 + 8 * B * kUBuf, d0 + e0, d1 + e1);
+        o.b0 = lds_s(tup);
+        o.b1 = lds_s(tup + 256);
+        if (zok) {
+          const double* s = sp + static_cast<i64>(p1) * wz;
+          o.s0 = __ldg(s);
+          o.s1 = __ldg(s + 4 * static_cast<i64>(p1));
+        }
       }
-      __syncwarp();
-      if (lane == 0) mbar_arrive_s(ubar0 + 8 * B);
       if (++ca == nch) {
         ca = 0;
         tup = tu0;
         tia = ti0 + 4;
-        // that round's S3 tile is free once every tensor warp formed its last U
-        nb_sync(kBarTensor, kSlabBS - 256);
-        if (leader) {
-          fence_proxy_async();
-          issue_s_tx(ra + 2);
-        }
-        nb_sync(kBarTensor, kSlabBS - 256);
-        if (lane == 0) {
-          fence_proxy_async();
-          issue_s_cols(ra + 2);
-        }
-        ++ra;
-        sa = (ra & 1) ? sa + sflip : sa - sflip;
+        sp += sstep;
+        --sleft;
       } else {
         tup += 512;
         tia += 8;
       }
+      return o;
     };
-    stage_a(0);
-    stage_a(1);
-    stage_a(2);
-    stage_a(3);
-    int T = -1, c = 0, nst = qtot - kDepth;   // nst: U steps left
+    auto store_u = [&](const UOp& o, const unsigned uoff) {
+      if (gact) {
+        double d0 = 0.0, d1 = 0.0, e0 = 0.0, e1 = 0.0;  // two independent DMMAs
+        dmma(d0, d1, o.s0, o.b0);
+        dmma(e0, e1, o.s1, o.b1);
+        sts2_s(ua0 + uoff, d0 + e0, d1 + e1);
+      }
+    };
+    for (int hb = 0; hb < 2; ++hb) {  // U of the first two pairs
+      const UOp o0 = load_u(), o1 = load_u();
+      store_u(o0, hb * (16 * kUBuf));
+      store_u(o1, hb * (16 * kUBuf) + 8 * kUBuf);
+      __syncwarp();
+      if (lane == 0) mbar_arrive_s(ubar0 + 8 * hb);
+    }
+    int T = -1, c = 0;
     unsigned tzp = tz0, tiz = ti0;            // Tz[c][.][lane], tz of chunk c
     double z00 = 0.0, z01 = 0.0, z10 = 0.0, z11 = 0.0;
     double* qs = a.Q + blockIdx.x * p12 + zr + static_cast<i64>(p1) * zq;
     const i64 qstep = static_cast<i64>(gridDim.x) * p12;
     auto flush = [&](int k, double x0, double x1) {
       const int zc = 8 * k + zq;
-      if (zr < p1 && zc < p2) qs[static_cast<i64>(p1) * (8 * k)] = x0;
-      if (zr < p1 && zc + 1 < p2) qs[static_cast<i64>(p1) * (8 * k + 1)] = x1;
+      if (zok && zc < p2) qs[static_cast<i64>(p1) * (8 * k)] = x0;
+      if (zok && zc + 1 < p2) qs[static_cast<i64>(p1) * (8 * k + 1)] = x1;
     };
-#ifdef KG_SLAB_TIMING
-    long long tw_ = 0, tc_ = 0, tl_ = 0;
-    long long t0_, t1_, t2_, t3_;
-#endif
-    auto body = [&](const int B, unsigned par) {
-      if (pfl) prefetch_v();
-      TCK(t0_);
-      mbar_wait_s(wbar0 + 8 * B, par);
-      TCK(t1_);
+    auto body = [&](const unsigned po) {
       if (gact && !(a.dbg & 2)) {
         // Y(zr, columns zq, zq + 1) = sum of the quads' partials, ascending quads
         double2 g[G];
 #pragma unroll
-        for (int k = 0; k < G; ++k) g[k] = lds2_s(gs[k] + 8 * B * kPBuf);
+        for (int k = 0; k < G; ++k) g[k] = lds2_s(gs[k] + po);
         const int tz = ldsi_s(tiz);
         const double zb0 = lds_s(tzp), zb1 = lds_s(tzp + 256);
         // pairwise (a fixed order; depth 3 instead of G - 1)
@@ -1169,7 +1117,7 @@ __global__ void __launch_bounds__(kSlabBS, 1) k_slab4(SlabArgs a) {
         }
       }
       if (++c == nch) {  // slice done: the live window holds its last two tiles
-        if (gact) {
+        if (gact && !(a.dbg & 2)) {
           flush(T, z00, z01);
           flush(T + 1, z10, z11);
           z00 = z01 = z10 = z11 = 0.0;
@@ -1183,34 +1131,27 @@ __global__ void __launch_bounds__(kSlabBS, 1) k_slab4(SlabArgs a) {
         tzp += 1024;
         tiz += 8;
       }
-      // U(q + kDepth) into U tile B (every row warp has read it: their arrivals
-      // on wbar[B] were observed above)
-      TCK(t2_);
-      if (nst > 0) {
-        --nst;
-        stage_a(B);
-      }
-      TCK(t3_);
-#ifdef KG_SLAB_TIMING
-      tw_ += t1_ - t0_, tc_ += t2_ - t1_, tl_ += t3_ - t2_;
-#endif
     };
-    int q = 0;
-    unsigned par = 0;
-    for (; q + kDepth <= qtot; q += kDepth, par ^= 1u) {
-      body(0, par);
-      body(1, par);
-      body(2, par);
-      body(3, par);
+    for (int ip = 0; ip < np; ++ip) {
+      const unsigned hb = static_cast<unsigned>(ip & 1);
+      // operands of the U step of pair ip + 2 (latency hidden behind the wait and the gather)
+      const UOp o0 = load_u(), o1 = load_u();
+      mbar_wait_s(wbar0 + 8 * hb, static_cast<unsigned>(ip >> 1) & 1u);
+      if (leader) {  // every row warp is done with pair ip's v tiles
+        copy_pair(hb);
+        prefetch_v();
+        prefetch_v();
+      }
+      body(hb * (16 * kPBuf));
+      body(hb * (16 * kPBuf) + 8 * kPBuf);
+      // U of pair ip + 2 into this pair's U tiles (every row warp has read them)
+      if (ip + 2 < np) {
+        store_u(o0, hb * (16 * kUBuf));
+        store_u(o1, hb * (16 * kUBuf) + 8 * kUBuf);
+        __syncwarp();
+        if (lane == 0) mbar_arrive_s(ubar0 + 8 * hb);
+      }
     }
-    if (q < qtot) body(0, par);
-    if (q + 1 < qtot) body(1, par);
-    if (q + 2 < qtot) body(2, par);
-#ifdef KG_SLAB_TIMING
-    if (blockIdx.x == 0 && lane == 0)
-      printf("tensor warp %d: chunks %d wait W %lld gather+Z %lld U step %lld (cycles per chunk)\n", warp, qtot, tw_ / qtot,
-             tc_ / qtot, tl_ / qtot);
-#endif
   }
   double rr = warp_sum_s((acc0 + acc1) + (acc2 + acc3));
   __syncthreads();
@@ -1227,7 +1168,7 @@ __global__ void __launch_bounds__(kSlabBS, 1) k_slab4(SlabArgs a) {
 // KG_SLAB_DMMA=1 (developer switch) keeps the DMMA form (k_slab).
 static bool slab_gather(const SlabArgs& a) {
   static const bool dmma_y = dev_env("KG_SLAB_DMMA") != nullptr;
-  return !dmma_y && a.gat && a.gmax > 0 && a.gmax <= 8 && a.PL > 0 && a.PL <= kPLMax;
+  return !dmma_y && a.gat && a.gmax > 0 && a.gmax <= 8 && a.PL > 0 && a.PL <= kPLMax;  // (k_slab4 also needs an even chunk count)
 }
 
 // Leading dimensions and shared-memory size of a slab plan.
@@ -1240,8 +1181,8 @@ static size_t slab_layout(SlabArgs& a) {
   a.cg = 1;
   const size_t ubuf = static_cast<size_t>(kLdr) * 8 * ((a.p1 + 7) / 8);
   if (slab_gather(a))  // k_slab4: fixed-stride U / partial tiles and the X2 chunk tables
-    return (2 * static_cast<size_t>(a.ldS) * a.p2 + kDepth * static_cast<size_t>(kUBuf + kPBuf) +
-            static_cast<size_t>(a.nch) * (128 + 64 + 1)) * sizeof(double);
+    return (kDepth * static_cast<size_t>(kVBuf + kUBuf + kPBuf) + static_cast<size_t>(a.nch) * (128 + 64 + 1)) *
+           sizeof(double);
   const size_t dbl = 2 * static_cast<size_t>(a.ldS) * a.p2 + kDepth * ubuf + kDepth * static_cast<size_t>(a.ldW) * 8;
   return dbl * sizeof(double);
 }
@@ -1287,10 +1228,11 @@ void slab_pass(const Launch& L, const SlabArgs& a0) {
     a.dbg = dbg;
     static const bool mb = dev_env("KG_SLAB_NB") == nullptr;
     static const bool k2 = dev_env("KG_SLAB_K2") != nullptr;
-    if (!k2 && a.gmax <= 6) {
+    const bool k4 = !k2 && !(a.nch & 1) && a.n2 == 8 * a.nch;  // whole chunk pairs
+    if (k4 && a.gmax <= 6) {
       smem_attr(k_slab4<6>, static_cast<int>(smem));
       k_slab4<6><<<g, kSlabBS, smem, L.s>>>(a);
-    } else if (!k2) {
+    } else if (k4) {
       smem_attr(k_slab4<8>, static_cast<int>(smem));
       k_slab4<8><<<g, kSlabBS, smem, L.s>>>(a);
     } else if (vs == 3 && mb) {
