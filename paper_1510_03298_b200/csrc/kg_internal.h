@@ -210,7 +210,6 @@ struct SlabArgs {
   // (0: unavailable), PL = slots per column-pair plane (= 2 mod 8, zero slot last)
   const int* gat = nullptr;
   int gmax = 0, PL = 0;
-  int dbg = 0;                  // timing experiments (developer switch KG_SLAB_DBG; results are wrong)
   int pf = 0;                   // v chunks prefetched into L2 ahead of the register loads (set by the launcher)
   const double* S = nullptr;    // p1 x p2 x m3
   const double* v = nullptr;    // n1 x n2 x m3

@@ -392,14 +392,13 @@ __global__ void __launch_bounds__(kSlabBS, 1) k_slab(SlabArgs a) {
 // fixed order), which lands Y directly in the A-fragment layout of the Z step.
 // FP64-pipe time per chunk drops from ~800 to ~620 SM-cycles and the tensor
 // warps' critical path from 12 to 0 Y DMMAs.
-template <int VS, bool MB>
 __global__ void __launch_bounds__(kSlabBS, 1) k_slab2(SlabArgs a) {
   using namespace async;
   extern __shared__ __align__(128) double sm[];
   __shared__ double red[32];
   __shared__ unsigned long long sbar[2];     // the two S3 tiles
-  // MB: the U / partial-tile hand-over through mbarriers (one arrival per warp)
-  // instead of named barriers, so the warps of a role do not rendezvous per chunk
+  // the U / partial-tile hand-over goes through mbarriers (one arrival per warp),
+  // so the warps of a role do not rendezvous per chunk
   __shared__ unsigned long long ubar[kDepth], wbar[kDepth];
   const int n1 = a.n1, n2 = a.n2, p1 = a.p1, p2 = a.p2, nch = a.nch;
   const int ldS = a.ldS, PL = a.PL;
@@ -441,7 +440,6 @@ __global__ void __launch_bounds__(kSlabBS, 1) k_slab2(SlabArgs a) {
   double acc0 = 0.0, acc1 = 0.0;
   if (rowrole) {
     // ------------------------------------------------------------ row warps
-    if (VS > 2) asm volatile("setmaxnreg.inc.sync.aligned.u32 168;");
     const int nq = n1 >> 2;                    // row quads
     const bool act = tid < 4 * nq;
     const int rq = act ? tid % nq : 0, cp = act ? tid / nq : 0;
@@ -473,7 +471,7 @@ __global__ void __launch_bounds__(kSlabBS, 1) k_slab2(SlabArgs a) {
 #pragma unroll
       for (int e = 0; e < 2; ++e) {
         const int col = 8 * c + c0 + e;
-        if (act && r < rounds && col < n2 && !(a.dbg & 1)) {
+        if (act && r < rounds && col < n2) {
           const double* p = vbase + r * vstep + static_cast<i64>(n1) * col;
           const double2 x = ldg2_stream(p), y = ldg2_stream(p + 2);
           vr[4 * e + 0] = x.x;
@@ -486,6 +484,7 @@ __global__ void __launch_bounds__(kSlabBS, 1) k_slab2(SlabArgs a) {
         }
       }
     };
+    constexpr int VS = 2;  // v register stages (more are capped by the warp's scoreboards)
     double vv[VS][8];
     int lr = 0, lc = 0;  // cursor of the next chunk to load
     auto adv = [&](int& r, int& c) {
@@ -516,8 +515,7 @@ __global__ void __launch_bounds__(kSlabBS, 1) k_slab2(SlabArgs a) {
     auto body = [&](int q, double (&vr)[8]) {
       const int buf = q & (kDepth - 1);
       if (pfl) prefetch_v();
-      if (MB) mbar_wait(&ubar[buf], static_cast<unsigned>(q / kDepth) & 1u);
-      else nb_sync(kBarUReady + buf, kSlabBS);
+      mbar_wait(&ubar[buf], static_cast<unsigned>(q / kDepth) & 1u);
       if (act) {
         const double* u = ub0 + buf * ubuf;
         double2 uu[kWin];
@@ -529,32 +527,21 @@ __global__ void __launch_bounds__(kSlabBS, 1) k_slab2(SlabArgs a) {
 #pragma unroll
           for (int r = 0; r < 4; ++r) {
             double x = C[r][0] * (c ? uu[0].y : uu[0].x);
-            if (!(a.dbg & 8)) {
 #pragma unroll
-              for (int t = 1; t < kWin; ++t) x = fma(C[r][t], c ? uu[t].y : uu[t].x, x);
-            }
+            for (int t = 1; t < kWin; ++t) x = fma(C[r][t], c ? uu[t].y : uu[t].x, x);
             const double wv = vr[4 * c + r] * x;
             if (r & 1) acc1 = fma(wv, x, acc1);
             else acc0 = fma(wv, x, acc0);
-            if (a.dbg & 4) {
 #pragma unroll
-              for (int t = 0; t < kWin; ++t) pt[c][t] = wv;
-            } else {
-#pragma unroll
-              for (int t = 0; t < kWin; ++t) pt[c][t] = r == 0 ? C[0][t] * wv : fma(C[r][t], wv, pt[c][t]);
-            }
+            for (int t = 0; t < kWin; ++t) pt[c][t] = r == 0 ? C[0][t] * wv : fma(C[r][t], wv, pt[c][t]);
           }
         }
         double2* P = pb0 + buf * (pbuf >> 1);
 #pragma unroll
         for (int t = 0; t < kWin; ++t) P[t] = make_double2(pt[0][t], pt[1][t]);
       }
-      if (MB) {
-        __syncwarp();
-        if (lane == 0) mbar_arrive(&wbar[buf]);
-      } else {
-        nb_arrive(kBarWReady + buf, kSlabBS);
-      }
+      __syncwarp();
+      if (lane == 0) mbar_arrive(&wbar[buf]);
       load_v(vr, lr, lc);  // VS chunks ahead
       adv(lr, lc);
     };
@@ -568,7 +555,6 @@ __global__ void __launch_bounds__(kSlabBS, 1) k_slab2(SlabArgs a) {
       if (q + s < qtot) body(q + s, vv[s]);
   } else {
     // --------------------------------------------------------- tensor warps
-    if (VS > 2) asm volatile("setmaxnreg.dec.sync.aligned.u32 88;");
     const int tw = warp - 8;
     const bool gact = tw < groups;            // this warp owns p1 rows 8 tw .. 8 tw + 7
     const bool leader = tid == 8 * 32;
@@ -633,12 +619,8 @@ __global__ void __launch_bounds__(kSlabBS, 1) k_slab2(SlabArgs a) {
     for (int q = 0; q < kDepth; ++q, adv(ka)) {
       if (q < qtot) {
         stage_a(ka, q, load_a(ka.c));
-        if (MB) {
-          __syncwarp();
-          if (lane == 0) mbar_arrive(&ubar[q]);
-        } else {
-          nb_arrive(kBarUReady + q, kSlabBS);
-        }
+        __syncwarp();
+        if (lane == 0) mbar_arrive(&ubar[q]);
       }
     }
     nb_sync(kBarTensor, kSlabBS - 256);
@@ -664,9 +646,8 @@ __global__ void __launch_bounds__(kSlabBS, 1) k_slab2(SlabArgs a) {
       const int buf = q & (kDepth - 1);
       const ZT zn = load_z(kz.c);   // next chunk's Z tables
       const AT an = load_a(kt.c);   // and the U tables one further
-      if (MB) mbar_wait(&wbar[buf], static_cast<unsigned>(q / kDepth) & 1u);
-      else nb_sync(kBarWReady + buf, kSlabBS);
-      if (gact && !(a.dbg & 2)) {
+      mbar_wait(&wbar[buf], static_cast<unsigned>(q / kDepth) & 1u);
+      if (gact) {
         const double2* pg = pg0 + buf * (pbuf >> 1);
         // Y(zr, columns zq, zq + 1) = sum of the quads' partials, ascending quads
         double2 g0 = pg[gs.x & 0xffff], g1 = pg[static_cast<unsigned>(gs.x) >> 16];
@@ -710,12 +691,8 @@ __global__ void __launch_bounds__(kSlabBS, 1) k_slab2(SlabArgs a) {
       // U(q + kDepth) into the buffer of chunk q (the row warps are done with it)
       if (q + kDepth < qtot) {
         stage_a(ka, buf, at);
-        if (MB) {
-          __syncwarp();
-          if (lane == 0) mbar_arrive(&ubar[buf]);
-        } else {
-          nb_arrive(kBarUReady + buf, kSlabBS);
-        }
+        __syncwarp();
+        if (lane == 0) mbar_arrive(&ubar[buf]);
         if (ka.c == nch - 1) {  // that round's S3 tile is free once every tensor warp formed its U
           nb_sync(kBarTensor, kSlabBS - 256);
           if (leader) {
@@ -765,7 +742,8 @@ __global__ void __launch_bounds__(kSlabBS, 1) k_slab2(SlabArgs a) {
 //     immediates; the X2 chunk tables sit in shared memory; the gather slots
 //     are shared addresses in registers;
 //   * the FP64 chains of a chunk are issued level by level (8 to 10
-//     independent chains); setmaxnreg: tensor warpgroups 104, row warpgroups 152.
+//     independent chains), the shared loads of a pair's gather up front;
+//     setmaxnreg: tensor warpgroups 120, row warpgroups 136.
 constexpr int kPLMax = 322;                 // slots per column-pair plane at n1 = 256
 constexpr int kPBuf = 8 * kPLMax;           // doubles per partial tile
 constexpr int kUBuf = kLdr * 64;            // doubles per U tile (p1 <= 64)
@@ -862,7 +840,7 @@ __global__ void __launch_bounds__(kSlabBS, 1) k_slab4(SlabArgs a) {
   double acc0 = 0.0, acc1 = 0.0, acc2 = 0.0, acc3 = 0.0;
   if (warp < 8) {
     // ------------------------------------------------------------ row warps
-    asm volatile("setmaxnreg.inc.sync.aligned.u32 152;");
+    asm volatile("setmaxnreg.inc.sync.aligned.u32 136;");
     const int nq = n1 >> 2;                    // row quads
     const bool act = tid < 4 * nq;
     const int rq = act ? tid % nq : 0, cp = act ? tid / nq : 0;
@@ -898,7 +876,7 @@ __global__ void __launch_bounds__(kSlabBS, 1) k_slab4(SlabArgs a) {
     const unsigned vcol = 8u * static_cast<unsigned>(n1);
     // chunk j of a pair: U window at uo, partials to po, v tile at byte offset vo
     auto body = [&](const int j, const unsigned uo, const unsigned po, const unsigned vo) {
-      if (act && !(a.dbg & 4)) {
+      if (act) {
         double2 uu[kWin];
 #pragma unroll
         for (int t = 0; t < kWin; ++t) uu[t] = lds2_s(uo + 8 * (j * kUBuf + t * kLdr));
@@ -963,7 +941,7 @@ __global__ void __launch_bounds__(kSlabBS, 1) k_slab4(SlabArgs a) {
     }
   } else {
     // --------------------------------------------------------- tensor warps
-    asm volatile("setmaxnreg.dec.sync.aligned.u32 104;");
+    asm volatile("setmaxnreg.dec.sync.aligned.u32 120;");
     const int tw = warp - 8;
     const bool gact = tw < ((p1 + 7) >> 3);   // this warp owns p1 rows 8 tw .. 8 tw + 7
     const bool leader = tid == 8 * 32;
@@ -1035,7 +1013,7 @@ __global__ void __launch_bounds__(kSlabBS, 1) k_slab4(SlabArgs a) {
     struct UOp { double s0, s1, b0, b1; };
     auto load_u = [&]() {                        // operands of U(ca), then advance the cursor
       UOp o{0.0, 0.0, 0.0, 0.0};
-      if (gact && sleft > 0 && !(a.dbg & 16)) {
+      if (gact && sleft > 0) {
         const int wz = ldsi_s(tia);
         o.b0 = lds_s(tup);
         o.b1 = lds_s(tup + 256);
@@ -1082,42 +1060,60 @@ __global__ void __launch_bounds__(kSlabBS, 1) k_slab4(SlabArgs a) {
       if (zok && zc < p2) qs[static_cast<i64>(p1) * (8 * k)] = x0;
       if (zok && zc + 1 < p2) qs[static_cast<i64>(p1) * (8 * k + 1)] = x1;
     };
-    auto body = [&](const unsigned po) {
-      if (gact && !(a.dbg & 2)) {
-        // Y(zr, columns zq, zq + 1) = sum of the quads' partials, ascending quads
-        double2 g[G];
+    // gather + Z of a pair (its chunks 2k, 2k + 1 lie in one slice: nch is even).
+    // All shared loads of both chunks are issued up front: the tensor warps are
+    // bound by the latency of their dependent shared loads otherwise.
+    auto body2 = [&](const unsigned po) {
+      if (gact) {
+        double2 g[2][G];
 #pragma unroll
-        for (int k = 0; k < G; ++k) g[k] = lds2_s(gs[k] + po);
-        const int tz = ldsi_s(tiz);
-        const double zb0 = lds_s(tzp), zb1 = lds_s(tzp + 256);
-        // pairwise (a fixed order; depth 3 instead of G - 1)
-        double y0 = (g[0].x + g[1].x) + (g[2].x + g[3].x);
-        double y1 = (g[0].y + g[1].y) + (g[2].y + g[3].y);
-        if (G > 6) {
-          y0 += (g[4].x + g[5].x) + (g[G - 2].x + g[G - 1].x);
-          y1 += (g[4].y + g[5].y) + (g[G - 2].y + g[G - 1].y);
-        } else {
-          y0 += g[4].x + g[5].x;
-          y1 += g[4].y + g[5].y;
+        for (int j = 0; j < 2; ++j)
+#pragma unroll
+          for (int k = 0; k < G; ++k) g[j][k] = lds2_s(gs[k] + po + 8 * j * kPBuf);
+        int tz[2];
+        double zb[2][4];
+#pragma unroll
+        for (int j = 0; j < 2; ++j) {
+          tz[j] = ldsi_s(tiz + 8 * j);
+#pragma unroll
+          for (int h = 0; h < 4; ++h) zb[j][h] = lds_s(tzp + 1024 * j + 256 * h);
         }
-        const int t0 = tz & 0xffff;
-        if (T < 0) T = t0;
-        while (T < t0) {  // tile T is complete: later chunks start at t0 > T
-          flush(T, z00, z01);
-          z00 = z10;
-          z01 = z11;
-          z10 = z11 = 0.0;
-          ++T;
+        // Y(zr, columns zq, zq + 1) = sum of the quads' partials: pairwise, a fixed order
+        double y[2][2];
+#pragma unroll
+        for (int j = 0; j < 2; ++j) {
+          y[j][0] = (g[j][0].x + g[j][1].x) + (g[j][2].x + g[j][3].x);
+          y[j][1] = (g[j][0].y + g[j][1].y) + (g[j][2].y + g[j][3].y);
+          if (G > 6) {
+            y[j][0] += (g[j][4].x + g[j][5].x) + (g[j][G - 2].x + g[j][G - 1].x);
+            y[j][1] += (g[j][4].y + g[j][5].y) + (g[j][G - 2].y + g[j][G - 1].y);
+          } else {
+            y[j][0] += g[j][4].x + g[j][5].x;
+            y[j][1] += g[j][4].y + g[j][5].y;
+          }
         }
-        dmma(z00, z01, y0, zb0);
-        dmma(z00, z01, y1, zb1);
-        if (tz >> 16) {
-          dmma(z10, z11, y0, lds_s(tzp + 512));
-          dmma(z10, z11, y1, lds_s(tzp + 768));
+#pragma unroll
+        for (int j = 0; j < 2; ++j) {
+          const int t0 = tz[j] & 0xffff;
+          if (T < 0) T = t0;
+          while (T < t0) {  // tile T is complete: later chunks start at t0 > T
+            flush(T, z00, z01);
+            z00 = z10;
+            z01 = z11;
+            z10 = z11 = 0.0;
+            ++T;
+          }
+          dmma(z00, z01, y[j][0], zb[j][0]);
+          dmma(z00, z01, y[j][1], zb[j][1]);
+          if (tz[j] >> 16) {
+            dmma(z10, z11, y[j][0], zb[j][2]);
+            dmma(z10, z11, y[j][1], zb[j][3]);
+          }
         }
       }
-      if (++c == nch) {  // slice done: the live window holds its last two tiles
-        if (gact && !(a.dbg & 2)) {
+      c += 2;
+      if (c == nch) {  // slice done: the live window holds its last two tiles
+        if (gact) {
           flush(T, z00, z01);
           flush(T + 1, z10, z11);
           z00 = z01 = z10 = z11 = 0.0;
@@ -1128,8 +1124,8 @@ __global__ void __launch_bounds__(kSlabBS, 1) k_slab4(SlabArgs a) {
         tzp = tz0;
         tiz = ti0;
       } else {
-        tzp += 1024;
-        tiz += 8;
+        tzp += 2048;
+        tiz += 16;
       }
     };
     for (int ip = 0; ip < np; ++ip) {
@@ -1142,8 +1138,7 @@ __global__ void __launch_bounds__(kSlabBS, 1) k_slab4(SlabArgs a) {
         prefetch_v();
         prefetch_v();
       }
-      body(hb * (16 * kPBuf));
-      body(hb * (16 * kPBuf) + 8 * kPBuf);
+      body2(hb * (16 * kPBuf));
       // U of pair ip + 2 into this pair's U tiles (every row warp has read them)
       if (ip + 2 < np) {
         store_u(o0, hb * (16 * kUBuf));
@@ -1221,29 +1216,20 @@ void slab_pass(const Launch& L, const SlabArgs& a0) {
   const size_t smem = slab_layout(a);
   const int g = slab_grid(a);
   if (slab_gather(a)) {
-    static const int vs = [] { const char* e = dev_env("KG_SLAB_VS"); return e ? std::atoi(e) : 2; }();
-    static const int pf = [] { const char* e = dev_env("KG_SLAB_PF"); return e ? std::atoi(e) : 6; }();
-    a.pf = pf;
-    static const int dbg = [] { const char* e = dev_env("KG_SLAB_DBG"); return e ? std::atoi(e) : 0; }();
-    a.dbg = dbg;
-    static const bool mb = dev_env("KG_SLAB_NB") == nullptr;
+    // KG_SLAB_K2=1 (developer switch): the register-staged kernel on every shape
     static const bool k2 = dev_env("KG_SLAB_K2") != nullptr;
     const bool k4 = !k2 && !(a.nch & 1) && a.n2 == 8 * a.nch;  // whole chunk pairs
+    a.pf = 0;  // the bulk-copy ring keeps enough of v in flight without an L2 prefetch
     if (k4 && a.gmax <= 6) {
       smem_attr(k_slab4<6>, static_cast<int>(smem));
       k_slab4<6><<<g, kSlabBS, smem, L.s>>>(a);
     } else if (k4) {
       smem_attr(k_slab4<8>, static_cast<int>(smem));
       k_slab4<8><<<g, kSlabBS, smem, L.s>>>(a);
-    } else if (vs == 3 && mb) {
-      smem_attr(k_slab2<3, true>, static_cast<int>(smem));
-      k_slab2<3, true><<<g, kSlabBS, smem, L.s>>>(a);
-    } else if (mb) {
-      smem_attr(k_slab2<2, true>, static_cast<int>(smem));
-      k_slab2<2, true><<<g, kSlabBS, smem, L.s>>>(a);
     } else {
-      smem_attr(k_slab2<2, false>, static_cast<int>(smem));
-      k_slab2<2, false><<<g, kSlabBS, smem, L.s>>>(a);
+      a.pf = 4;
+      smem_attr(k_slab2, static_cast<int>(smem));
+      k_slab2<<<g, kSlabBS, smem, L.s>>>(a);
     }
   } else {
     switch (a.g1.ks) {

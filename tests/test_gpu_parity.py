@@ -500,15 +500,22 @@ def _slab_route_taken(design, y):
     return st == 0
 
 
-@pytest.mark.parametrize("n,p", [((60, 52, 30), (14, 12, 8)),    # tail chunk (52 = 6 x 8 + 4), p1 not a multiple of 8
-                                 ((32, 72, 24), (10, 20, 7)),    # several column groups (n1 = 32), p2 = 20
-                                 ((128, 40, 17), (32, 10, 6))])  # odd last mode, two DMMA row groups x 4
+SLAB_SHAPES = [((60, 52, 30), (14, 12, 8)),    # tail chunk (52 = 6 x 8 + 4), p1 not a multiple of 8: k_slab2
+               ((32, 72, 24), (10, 20, 7)),    # odd chunk count (9), several column groups (n1 = 32): k_slab2
+               ((128, 40, 17), (32, 10, 6)),   # odd chunk count, odd last mode: k_slab2
+               ((64, 48, 20), (16, 12, 6)),    # whole chunk pairs: k_slab4 (bulk-copy v ring)
+               ((60, 48, 30), (14, 12, 8)),    # k_slab4 with a partly active row warp (15 quads), padded row groups
+               ((256, 32, 6), (64, 10, 4))]    # k_slab4 at the largest mode-1 extents (all 256 row threads)
+
+
+@pytest.mark.parametrize("n,p", SLAB_SHAPES)
 def test_slab_route_poisson_paths_match_oracle(n, p):
-    """The slab pass (k_slab: modes 1 and 2 of X^T W X fused per last-mode
-    slice) on irregular shapes -- a partial last chunk of mode-2 rows, p1 with
-    padded DMMA row groups, several row-thread column groups -- against the
-    oracle's Poisson path (same supports, coefficients, objectives and
-    iteration counts)."""
+    """The slab pass (modes 1 and 2 of X^T W X fused per last-mode slice:
+    k_slab4 on whole chunk pairs, k_slab2 otherwise) on irregular shapes -- a
+    partial last chunk of mode-2 rows, odd chunk counts, p1 with padded row
+    groups, several row-thread column groups, partly active row warps --
+    against the oracle's Poisson path (same supports, coefficients, objectives
+    and iteration counts)."""
     rng = np.random.default_rng(sum(n) + sum(p))
     design = bspline_design(n, p)
     B = np.zeros(p)
@@ -521,3 +528,22 @@ def test_slab_route_poisson_paths_match_oracle(n, p):
     got = K.fit_path(design, "poisson", y, **kw)
     want = O.fit_path(design, "poisson", y, **kw)
     compare_paths(got, want)
+
+
+@pytest.mark.gpu
+@pytest.mark.parametrize("switch", ["KG_SLAB_K2", "KG_SLAB_DMMA"])
+def test_slab_fallback_kernels_match_oracle(switch):
+    """The slab-pass kernels behind the default one -- k_slab2 (register-staged
+    v, taken on odd chunk counts) and k_slab (Y by DMMA, taken without a gather
+    table) -- forced by their developer switches onto the k_slab4 shapes, in a
+    fresh process (the switches are read once)."""
+    import os
+    import subprocess
+    import sys
+    root = os.path.dirname(os.path.dirname(os.path.abspath(__file__)))
+    env = dict(os.environ, KG_DEV="1", **{switch: "1"})
+    r = subprocess.run([sys.executable, "-m", "pytest", os.path.join(root, "tests", "test_gpu_parity.py"), "-m", "gpu",
+                        "-q", "-x", "-k", "test_slab_route_poisson_paths_match_oracle"],
+                       env=env, cwd=root, capture_output=True, text=True, timeout=900)
+    assert r.returncode == 0, r.stdout[-2000:] + r.stderr[-2000:]
+    assert "6 passed" in r.stdout, r.stdout[-500:]
