@@ -176,6 +176,9 @@ struct kg_ctx {
   void* stage = nullptr;        // page-locked upload ring (kStageLanes x kStageSlots x kStageChunk bytes)
   cudaEvent_t stage_ev[16] = {};
   cudaEvent_t loop_ev[2] = {nullptr, nullptr};  // pipelined host loop of sharded n-space solves
+  // fork / join of the FISTA body: the control kernel runs beside the last chain step
+  cudaStream_t fork = nullptr;
+  cudaEvent_t fork_ev[2] = {nullptr, nullptr};
   kg::Launch L() { return {s, &launches}; }
   double* pin() { return static_cast<double*>(pinned); }
 };
@@ -1324,6 +1327,32 @@ static void enqueue_body(Fit& F, cudaGraphConditionalHandle h, int use_handle) {
   }
   fista_update(ctx->L(), c, F.p, F.pen, F.alpha, F.x.d(), F.xp.d(), F.Sx.d(), F.Sxp.d(), F.b.d(), F.best.d(),
                F.Sbest.d(), F.Jpart.d(), ex ? F.bxpart.d() : nullptr);
+  static const bool no_fork = dev_env("KG_NO_FORK") != nullptr;
+  if (F.route == 0 && F.slab && !sharded(ctx) && !no_fork) {
+    // Slab route: H mode 3 -> slab pass -> G mode 3.  The control kernel needs
+    // only the partials of the update and of the slab pass, so it runs beside
+    // the mode-3 G step (a fork / join in the captured body) instead of after it.
+    const kg_design& D = *F.D;
+    if (!ctx->fork) {
+      KG_CUDA(cudaStreamCreateWithFlags(&ctx->fork, cudaStreamNonBlocking));
+      for (cudaEvent_t& e : ctx->fork_ev) KG_CUDA(cudaEventCreateWithFlags(&e, cudaEventDisableTiming));
+    }
+    run_chain(ctx, coef_dims(D, 0), h_steps(D, 0, 2), F.x.d(), F.P.d(), F.s0.d(), F.s1.d(), false);
+    SlabArgs a = slab_args(F);
+    a.S = F.P.d();
+    a.Q = F.Q.d();
+    slab_pass(ctx->L(), a);
+    F.n_ss = slab_grid(a);
+    KG_CUDA(cudaEventRecord(ctx->fork_ev[0], ctx->s));
+    KG_CUDA(cudaStreamWaitEvent(ctx->fork, ctx->fork_ev[0], 0));
+    fista_control(Launch{ctx->fork, &ctx->launches}, c, F.part.d(), F.n_ss, F.Jpart.d(), ugrid(F.p), h, use_handle,
+                  ex ? F.bxpart.d() : nullptr, ugrid(F.p));
+    KG_CUDA(cudaEventRecord(ctx->fork_ev[1], ctx->fork));
+    std::vector<i64> dims = {D.p[0][0], D.p[0][1], D.n[2]};
+    run_chain(ctx, dims, g_steps(D, 0, 2), F.Q.d(), F.Sx.d(), F.s0.d(), F.s1.d(), false);
+    KG_CUDA(cudaStreamWaitEvent(ctx->s, ctx->fork_ev[1], 0));
+    return;
+  }
   F.n_ss = step_pass(F, F.x.d(), F.Sx.d());
   fista_control(ctx->L(), c, F.part.d(), F.n_ss, F.Jpart.d(), ugrid(F.p), h, use_handle,
                 ex ? F.bxpart.d() : nullptr, ugrid(F.p));
@@ -2600,6 +2629,12 @@ void kg_ctx_destroy(kg_ctx* ctx) {
     cudaStreamSynchronize(ctx->side);
     cudaStreamDestroy(ctx->side);
   }
+  if (ctx->fork) {
+    cudaStreamSynchronize(ctx->fork);
+    cudaStreamDestroy(ctx->fork);
+  }
+  for (cudaEvent_t e : ctx->fork_ev)
+    if (e) cudaEventDestroy(e);
   if (ctx->stage) cudaFreeHost(ctx->stage);
   for (cudaEvent_t e : ctx->stage_ev)
     if (e) cudaEventDestroy(e);
