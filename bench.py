@@ -356,7 +356,7 @@ def run_ours(args):
         slab = True
     except Exception:
         slab = False
-    kernels = ((("fused_pass", 0, "k_slab: slab pass (per last-mode slice: eta = X1 S3 X2^T, v eta^2, "
+    kernels = ((("fused_pass", 0, "k_slab4: slab pass (per last-mode slice: eta = X1 S3 X2^T, v eta^2, "
                  "Q3 = X1^T (v eta) X2)"),
                 ("h_mode3_step", 6, "mode-3 H-chain contraction (x -> S3)"),
                 ("g_mode3_step", 7, "mode-3 G-chain contraction (Q3 -> S x)"),
@@ -398,10 +398,11 @@ def run_ours(args):
                 "launches_per_step": 1,
                 "share_of_step": (f["avg_launch_ms"] * iters / total_ms) if f.get("avg_launch_ms") else None}
         if slab:
-            roof["note"] = ("k_slab moves exactly its algorithmic bytes (traffic); it is bound in practice by the "
-                            "FP64 pipe its DMMA (X1^T w band tiles, 35% dense) and DFMA work share: ~770 SM-cycles "
-                            "per 2048-cell chunk, an ~86 us floor against ~93 us for HBM, issued from 16 resident "
-                            "warps (DESIGN.md 4b)")
+            roof["note"] = ("k_slab4 moves exactly its algorithmic bytes (traffic); with v streamed by bulk copies "
+                            "alone the kernel takes ~105 us (5.7 TB/s); the rest is issue latency of its 16 resident "
+                            "warps and shared-memory bandwidth (v, the U windows and the scatter/gather partials "
+                            "all cross shared memory: ~122 KB per 2048-cell chunk, L1/shared pipe 71% busy) "
+                            "(DESIGN.md 4b)")
     fp64 = fp64_peaks()
     if fp64:
         roof["fp64_peaks"] = fp64
