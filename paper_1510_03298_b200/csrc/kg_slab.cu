@@ -797,7 +797,7 @@ __device__ __forceinline__ void sts2_s(unsigned addr, double x, double y) {
 
 constexpr int kVBuf = 8 * 256;              // doubles per v chunk tile (n1 <= 256)
 
-// G: gather slots per basis function (6 or 8).
+// G: gather slots per basis function (5, 6 or 8; cubic B-spline factors on a 4x finer grid need 5).
 template <int G>
 __global__ void __launch_bounds__(kSlabBS, 1) k_slab4(SlabArgs a) {
   using namespace async;
@@ -1087,9 +1087,12 @@ __global__ void __launch_bounds__(kSlabBS, 1) k_slab4(SlabArgs a) {
           if (G > 6) {
             y[j][0] += (g[j][4].x + g[j][5].x) + (g[j][G - 2].x + g[j][G - 1].x);
             y[j][1] += (g[j][4].y + g[j][5].y) + (g[j][G - 2].y + g[j][G - 1].y);
+          } else if (G > 5) {
+            y[j][0] += g[j][4].x + g[j][G - 1].x;
+            y[j][1] += g[j][4].y + g[j][G - 1].y;
           } else {
-            y[j][0] += g[j][4].x + g[j][5].x;
-            y[j][1] += g[j][4].y + g[j][5].y;
+            y[j][0] += g[j][4].x;
+            y[j][1] += g[j][4].y;
           }
         }
 #pragma unroll
@@ -1220,7 +1223,10 @@ void slab_pass(const Launch& L, const SlabArgs& a0) {
     static const bool k2 = dev_env("KG_SLAB_K2") != nullptr;
     const bool k4 = !k2 && !(a.nch & 1) && a.n2 == 8 * a.nch;  // whole chunk pairs
     a.pf = 0;  // the bulk-copy ring keeps enough of v in flight without an L2 prefetch
-    if (k4 && a.gmax <= 6) {
+    if (k4 && a.gmax <= 5) {
+      smem_attr(k_slab4<5>, static_cast<int>(smem));
+      k_slab4<5><<<g, kSlabBS, smem, L.s>>>(a);
+    } else if (k4 && a.gmax <= 6) {
       smem_attr(k_slab4<6>, static_cast<int>(smem));
       k_slab4<6><<<g, kSlabBS, smem, L.s>>>(a);
     } else if (k4) {
