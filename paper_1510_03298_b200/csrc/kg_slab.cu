@@ -874,6 +874,40 @@ __global__ void __launch_bounds__(kSlabBS, 1) k_slab4(SlabArgs a) {
     const unsigned vb0 = smem_u32(Vs + r0 + n1 * c0) + (sw ? 16u : 0u);   // rows (sw ? 2,3 : 0,1) of column c0
     const unsigned vb1 = smem_u32(Vs + r0 + n1 * c0) + (sw ? 0u : 16u);   // the other two rows
     const unsigned vcol = 8u * static_cast<unsigned>(n1);
+    // v stream (row warp 0): chunk pairs by bulk copy into the ring.  Pair ip + 1
+    // goes into the tiles of pair ip - 1 once every row warp has arrived on that
+    // pair's partial barrier (they have all read its v by then); the tensor
+    // warps, which pace the pass, carry none of it.
+    const i64 vchunk = static_cast<i64>(n1) * 8;
+    const i64 vjump = static_cast<i64>(gridDim.x) * n12 - vchunk * (nch - 1);  // last chunk of a slice -> first of the next
+    const double* vp = a.v + blockIdx.x * n12;   // next chunk to copy
+    int vc = 0, vq = 0;
+    const unsigned vbytes = static_cast<unsigned>(vchunk * 8);
+    const unsigned vs0 = smem_u32(Vs);
+    auto copy_pair = [&](unsigned hb) {          // the next two chunks into pair hb's tiles (one lane)
+      if (vq >= qtot) return;
+      const unsigned bar = vbar0 + 8 * hb;
+      asm volatile("mbarrier.arrive.expect_tx.shared::cta.b64 _, [%0], %1;" ::"r"(bar), "r"(2 * vbytes) : "memory");
+#pragma unroll
+      for (int j = 0; j < 2; ++j) {
+        asm volatile("cp.async.bulk.shared::cluster.global.mbarrier::complete_tx::bytes [%0], [%1], %2, [%3];" ::"r"(
+                         vs0 + 8u * static_cast<unsigned>((2 * hb + j) * kVBuf)),
+                     "l"(vp), "r"(vbytes), "r"(bar)
+                     : "memory");
+        ++vq;
+        if (++vc == nch) {
+          vc = 0;
+          vp += vjump;
+        } else {
+          vp += vchunk;
+        }
+      }
+    };
+    if (tid == 0) {
+      fence_proxy_async();
+      copy_pair(0);
+      copy_pair(1);
+    }
     // chunk j of a pair: U window at uo, partials to po, v tile at byte offset vo
     auto body = [&](const int j, const unsigned uo, const unsigned po, const unsigned vo) {
       if (act) {
@@ -934,6 +968,10 @@ __global__ void __launch_bounds__(kSlabBS, 1) k_slab4(SlabArgs a) {
       mbar_wait_s(ubar0 + 8 * hb, par);
       mbar_wait_s(vbar0 + 8 * hb, par);
       const unsigned uo = ub0 + hb * (16 * kUBuf), po = pb0 + hb * (16 * kPBuf), vo = hb * (16 * kVBuf);
+      if (warp == 0 && ip > 0) {  // pair ip - 1 is read: pair ip + 1 into its v tiles
+        mbar_wait_s(wbar0 + 8 * (hb ^ 1u), static_cast<unsigned>((ip - 1) >> 1) & 1u);
+        if (lane == 0) copy_pair(hb ^ 1u);
+      }
       body(0, uo, po, vo);
       body(1, uo, po, vo);
       __syncwarp();
@@ -959,50 +997,6 @@ __global__ void __launch_bounds__(kSlabBS, 1) k_slab4(SlabArgs a) {
       const int w4[4] = {g4.x, g4.y, g4.z, g4.w};
 #pragma unroll
       for (int k = 0; k < G; ++k) gs[k] = pl0 + 16u * ((static_cast<unsigned>(w4[k >> 1]) >> (16 * (k & 1))) & 0xffffu);
-    }
-    // v stream (leader): chunk pairs by bulk copy into the ring, L2 prefetch a.pf chunks ahead
-    const i64 vchunk = static_cast<i64>(n1) * 8;
-    const i64 vjump = static_cast<i64>(gridDim.x) * n12 - vchunk * (nch - 1);  // last chunk of a slice -> first of the next
-    const double* vp = a.v + blockIdx.x * n12;   // next chunk to copy
-    int vc = 0, vq = 0;
-    const unsigned vbytes = static_cast<unsigned>(vchunk * 8);
-    const unsigned vs0 = smem_u32(Vs);
-    auto copy_pair = [&](unsigned hb) {          // the next two chunks into pair hb's tiles
-      if (vq >= qtot) return;
-      const unsigned bar = vbar0 + 8 * hb;
-      asm volatile("mbarrier.arrive.expect_tx.shared::cta.b64 _, [%0], %1;" ::"r"(bar), "r"(2 * vbytes) : "memory");
-#pragma unroll
-      for (int j = 0; j < 2; ++j) {
-        asm volatile("cp.async.bulk.shared::cluster.global.mbarrier::complete_tx::bytes [%0], [%1], %2, [%3];" ::"r"(
-                         vs0 + 8u * static_cast<unsigned>((2 * hb + j) * kVBuf)),
-                     "l"(vp), "r"(vbytes), "r"(bar)
-                     : "memory");
-        ++vq;
-        if (++vc == nch) {
-          vc = 0;
-          vp += vjump;
-        } else {
-          vp += vchunk;
-        }
-      }
-    };
-    const double* fp = a.v + blockIdx.x * n12;   // next chunk to prefetch
-    int fc = 0, fq = 0;
-    auto prefetch_v = [&]() {
-      if (fq < qtot) bulk_prefetch_l2(fp, vbytes);
-      ++fq;
-      if (++fc == nch) {
-        fc = 0;
-        fp += vjump;
-      } else {
-        fp += vchunk;
-      }
-    };
-    if (leader) {
-      fence_proxy_async();
-      copy_pair(0);
-      copy_pair(1);
-      for (int k = 0; k < 4 + a.pf; ++k) prefetch_v();  // the ring's four chunks are on their way already
     }
     // U step: chunk ca of the slice at sp; S3 operands from L2, loaded one pair ahead
     const unsigned tu0 = smem_u32(Tu) + 8u * lane, tz0 = smem_u32(Tz) + 8u * lane, ti0 = smem_u32(Ti);
@@ -1136,11 +1130,6 @@ __global__ void __launch_bounds__(kSlabBS, 1) k_slab4(SlabArgs a) {
       // operands of the U step of pair ip + 2 (latency hidden behind the wait and the gather)
       const UOp o0 = load_u(), o1 = load_u();
       mbar_wait_s(wbar0 + 8 * hb, static_cast<unsigned>(ip >> 1) & 1u);
-      if (leader) {  // every row warp is done with pair ip's v tiles
-        copy_pair(hb);
-        prefetch_v();
-        prefetch_v();
-      }
       body2(hb * (16 * kPBuf));
       // U of pair ip + 2 into this pair's U tiles (every row warp has read them)
       if (ip + 2 < np) {
