@@ -138,6 +138,28 @@ struct FistaCtl {
 struct Launch {
   cudaStream_t s;
   i64* counter;  // incremented per launch (host-side launch accounting)
+  // Programmatic dependent launch: kernels that support it (k_contract_gb,
+  // k_slab4: they execute griddepcontrol.wait before touching what earlier
+  // kernels wrote) are launched with programmatic stream serialization, so
+  // their launch and prologue overlap the tail of the kernel before them.
+  // Every other kernel ignores the flag and is launched normally.
+  bool pdl = false;
+};
+
+// Launch configuration of a PDL-capable kernel (see Launch::pdl).
+struct PdlConfig {
+  cudaLaunchConfig_t cfg = {};
+  cudaLaunchAttribute attr[1] = {};
+  PdlConfig(dim3 grid, dim3 block, size_t smem, const Launch& L) {
+    cfg.gridDim = grid;
+    cfg.blockDim = block;
+    cfg.dynamicSmemBytes = smem;
+    cfg.stream = L.s;
+    attr[0].id = cudaLaunchAttributeProgrammaticStreamSerialization;
+    attr[0].val.programmaticStreamSerializationAllowed = 1;
+    cfg.attrs = attr;
+    cfg.numAttrs = L.pdl ? 1 : 0;
+  }
 };
 
 // After every kernel launch: surface launch-configuration errors immediately

@@ -236,6 +236,10 @@ __global__ void __launch_bounds__(NT, RB <= 4 ? 4 : 1) k_contract_gb(const doubl
   const uint32_t g = blockIdx.x;
   for (int i = threadIdx.x; i < RB * RW; i += NT) cs[i] = __ldg(wbcoef + static_cast<size_t>(g) * RB * RW + i);
   __syncthreads();
+  // programmatic dependent launch (Launch::pdl): everything above reads design
+  // constants only; the input array belongs to the kernel before this one
+  asm volatile("griddepcontrol.wait;" ::: "memory");
+  asm volatile("griddepcontrol.launch_dependents;");
   const uint32_t nbl = NT / ab;  // beta lanes per CTA
   const uint32_t lane_a = threadIdx.x % ab, lane_b = threadIdx.x / ab;
   const uint32_t al = blockIdx.y * ab + lane_a;
@@ -312,10 +316,10 @@ static bool launch_blk(const Launch& L, const double* A, double* out, i64 a, i64
   gz = (b + bspan - 1) / bspan;
   if (groups > 0x7fffffff || gy > 65535 || gz > 65535) return false;
   if (groups * gy * gz < 2 * 148) return false;  // too few CTAs to fill the GPU: the row-stationary kernel
-  k_contract_gb<RB, RW><<<dim3(static_cast<unsigned>(groups), static_cast<unsigned>(gy), static_cast<unsigned>(gz)),
-                          NT, 0, L.s>>>(A, out, static_cast<uint32_t>(a), static_cast<uint32_t>(K),
-                                        static_cast<uint32_t>(M), static_cast<uint32_t>(b), static_cast<uint32_t>(ab),
-                                        static_cast<uint32_t>(bspan), blo, bcoef, accumulate);
+  PdlConfig pc(dim3(static_cast<unsigned>(groups), static_cast<unsigned>(gy), static_cast<unsigned>(gz)), dim3(NT), 0, L);
+  cudaLaunchKernelEx(&pc.cfg, k_contract_gb<RB, RW>, A, out, static_cast<uint32_t>(a), static_cast<uint32_t>(K),
+                     static_cast<uint32_t>(M), static_cast<uint32_t>(b), static_cast<uint32_t>(ab),
+                     static_cast<uint32_t>(bspan), blo, bcoef, static_cast<int>(accumulate));
   bump(L);
   return true;
 }

@@ -731,8 +731,8 @@ __global__ void __launch_bounds__(kSlabBS, 1) k_slab2(SlabArgs a) {
 // which bounds the pass at ~140 us before any arithmetic; the issue latency of
 // 16 resident warps bounds the rest):
 //   * v arrives by cp.async.bulk (one 16 KB copy per chunk, contiguous in the
-//     array) into a four-chunk shared ring behind mbarriers, issued two pairs
-//     ahead by the tensor-warp leader, plus an L2 prefetch further ahead; row
+//     array) into a four-chunk shared ring behind mbarriers, issued by row warp
+//     0 as soon as the tiles of the pair before last are read; row
 //     threads read their 4 x 2 cells with swizzled 16-byte loads (the upper
 //     half of each quad group takes rows 2,3 first: conflict free);
 //   * the S3 operands of the U step (2 doubles per lane and chunk) come
@@ -837,6 +837,11 @@ __global__ void __launch_bounds__(kSlabBS, 1) k_slab4(SlabArgs a) {
     z[0] = z[1] = 0.0;
   }
   __syncthreads();
+  // programmatic dependent launch (Launch::pdl): the kernel after this one may
+  // be scheduled as this one's CTAs retire; of this kernel's inputs only S3
+  // belongs to the kernel before it (the tensor warps wait below), v and the
+  // tables are older
+  asm volatile("griddepcontrol.launch_dependents;");
   double acc0 = 0.0, acc1 = 0.0, acc2 = 0.0, acc3 = 0.0;
   if (warp < 8) {
     // ------------------------------------------------------------ row warps
@@ -1037,6 +1042,7 @@ __global__ void __launch_bounds__(kSlabBS, 1) k_slab4(SlabArgs a) {
         sts2_s(ua0 + uoff, d0 + e0, d1 + e1);
       }
     };
+    asm volatile("griddepcontrol.wait;" ::: "memory");  // S3 is complete and visible
     for (int hb = 0; hb < 2; ++hb) {  // U of the first two pairs
       const UOp o0 = load_u(), o1 = load_u();
       store_u(o0, hb * (16 * kUBuf));
@@ -1212,15 +1218,16 @@ void slab_pass(const Launch& L, const SlabArgs& a0) {
     static const bool k2 = dev_env("KG_SLAB_K2") != nullptr;
     const bool k4 = !k2 && !(a.nch & 1) && a.n2 == 8 * a.nch;  // whole chunk pairs
     a.pf = 0;  // the bulk-copy ring keeps enough of v in flight without an L2 prefetch
+    PdlConfig pc(dim3(g), dim3(kSlabBS), smem, L);
     if (k4 && a.gmax <= 5) {
       smem_attr(k_slab4<5>, static_cast<int>(smem));
-      k_slab4<5><<<g, kSlabBS, smem, L.s>>>(a);
+      cudaLaunchKernelEx(&pc.cfg, k_slab4<5>, a);
     } else if (k4 && a.gmax <= 6) {
       smem_attr(k_slab4<6>, static_cast<int>(smem));
-      k_slab4<6><<<g, kSlabBS, smem, L.s>>>(a);
+      cudaLaunchKernelEx(&pc.cfg, k_slab4<6>, a);
     } else if (k4) {
       smem_attr(k_slab4<8>, static_cast<int>(smem));
-      k_slab4<8><<<g, kSlabBS, smem, L.s>>>(a);
+      cudaLaunchKernelEx(&pc.cfg, k_slab4<8>, a);
     } else {
       a.pf = 4;
       smem_attr(k_slab2, static_cast<int>(smem));

@@ -850,14 +850,16 @@ struct Step {
 };
 
 static void run_chain(kg_ctx* ctx, std::vector<i64> dims, const std::vector<Step>& steps, const double* in,
-                      double* out, double* s0, double* s1, bool accumulate_last) {
+                      double* out, double* s0, double* s1, bool accumulate_last, bool pdl = false) {
   const double* cur = in;
+  Launch L = ctx->L();
+  L.pdl = pdl;
   for (size_t k = 0; k < steps.size(); ++k) {
     const Step& st = steps[k];
     const bool last = k + 1 == steps.size();
     double* dst = last ? out : (k % 2 == 0 ? s0 : s1);
     const i64 a = prod(dims, 0, st.mode), K = dims[st.mode], b = prod(dims, st.mode + 1, dims.size());
-    contract(ctx->L(), cur, dst, a, K, st.next, b, *st.op, last && accumulate_last);
+    contract(L, cur, dst, a, K, st.next, b, *st.op, last && accumulate_last);
     dims[st.mode] = st.next;
     cur = dst;
   }
@@ -1337,11 +1339,15 @@ static void enqueue_body(Fit& F, cudaGraphConditionalHandle h, int use_handle) {
       KG_CUDA(cudaStreamCreateWithFlags(&ctx->fork, cudaStreamNonBlocking));
       for (cudaEvent_t& e : ctx->fork_ev) KG_CUDA(cudaEventCreateWithFlags(&e, cudaEventDisableTiming));
     }
-    run_chain(ctx, coef_dims(D, 0), h_steps(D, 0, 2), F.x.d(), F.P.d(), F.s0.d(), F.s1.d(), false);
+    // programmatic dependent launches along update -> H mode 3 -> slab pass -> G mode 3
+    static const bool pdl = dev_env("KG_NO_PDL") == nullptr;
+    run_chain(ctx, coef_dims(D, 0), h_steps(D, 0, 2), F.x.d(), F.P.d(), F.s0.d(), F.s1.d(), false, pdl);
     SlabArgs a = slab_args(F);
     a.S = F.P.d();
     a.Q = F.Q.d();
-    slab_pass(ctx->L(), a);
+    Launch Lp = ctx->L();
+    Lp.pdl = pdl;
+    slab_pass(Lp, a);
     F.n_ss = slab_grid(a);
     KG_CUDA(cudaEventRecord(ctx->fork_ev[0], ctx->s));
     KG_CUDA(cudaStreamWaitEvent(ctx->fork, ctx->fork_ev[0], 0));
@@ -1349,7 +1355,7 @@ static void enqueue_body(Fit& F, cudaGraphConditionalHandle h, int use_handle) {
                   ex ? F.bxpart.d() : nullptr, ugrid(F.p));
     KG_CUDA(cudaEventRecord(ctx->fork_ev[1], ctx->fork));
     std::vector<i64> dims = {D.p[0][0], D.p[0][1], D.n[2]};
-    run_chain(ctx, dims, g_steps(D, 0, 2), F.Q.d(), F.Sx.d(), F.s0.d(), F.s1.d(), false);
+    run_chain(ctx, dims, g_steps(D, 0, 2), F.Q.d(), F.Sx.d(), F.s0.d(), F.s1.d(), false, pdl);
     KG_CUDA(cudaStreamWaitEvent(ctx->s, ctx->fork_ev[1], 0));
     return;
   }
