@@ -254,6 +254,20 @@ int64_t kg_linear_index(int64_t d, const int64_t* multi_index, const int64_t* di
  * fit falls back to the p-sized all-reduce).  Host only. */
 kg_status kg_halo_plan(int64_t n, int64_t p, const double* X, int world, int rank, int64_t* out);
 
+/* Gather plan of the slab pass (the X^T W X step of xtwx_apply,
+ * design.cpp:118-124, fused per last-mode slice): the mode-1 factor X1 (n x p,
+ * column-major, host memory; rows with <= 4 nonzeros inside a 5-wide window
+ * per quad of grid rows).  Row quad q scatters its five window partials of
+ * X1^T w to slots 5 q .. 5 q + 4 of a plane; basis function k then sums, in
+ * ascending quad order, the slots of the quads that have a row with k inside
+ * its nonzero band.  slots[8 k + j] (k < 8 ceil(p / 8), j < 8) = slot j of
+ * basis function k, padded with the plane's always-zero slot plane - 1;
+ * *gmax = most slots of any k; *plane = slots per plane (5 n / 4 rounded up to
+ * = 2 mod 8, so the gather is bank-conflict free).  KG_EINVAL when n is not a
+ * multiple of 4, a band leaves its quad's window, or some k needs more than 8
+ * slots (the pass then keeps its DMMA form).  Host only. */
+kg_status kg_slab_gather_plan(int64_t n, int64_t p, const double* X, int32_t* slots, int32_t* gmax, int32_t* plane);
+
 /* Held-out selection (mse_heldout, path.cpp:91-126, decl path.hpp:63): for
  * every model of `res`, the sum over cells with mask == 1 of (mean(X theta_t)
  * - y_full)^2 into mse[0 .. n_models), and the first minimizing model in

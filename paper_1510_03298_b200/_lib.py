@@ -100,6 +100,8 @@ _SIGS = {
     "kg_bspline_design_dev": (C.c_int, [_vp, _i64, _vp, _i64, _i64, C.c_int, _vp]),
     "kg_linear_index": (_i64, [_i64, _pi, _pi]),
     "kg_halo_plan": (C.c_int, [_i64, _i64, _pd, C.c_int, C.c_int, C.POINTER(_i64)]),
+    "kg_slab_gather_plan": (C.c_int, [_i64, _i64, _pd, C.POINTER(C.c_int32), C.POINTER(C.c_int32),
+                                      C.POINTER(C.c_int32)]),
     "kg_design_halo": (C.c_int, [_vp, C.POINTER(_i64)]),
     "kg_time_kernel": (C.c_int, [_vp, _vp, _vp, C.c_int, C.c_int, _pd, _pd]),
     "kg_path_kernel_stats": (C.c_int, [_vp, _pd, _pd, C.POINTER(_i64)]),

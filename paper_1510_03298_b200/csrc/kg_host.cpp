@@ -67,6 +67,46 @@ int64_t kg_linear_index(int64_t d, const int64_t* idx, const int64_t* dims) {
   return pos + 1;
 }
 
+// Gather plan of the slab pass (kronglm_b200.h).  Shared with the design
+// builder (kg_solver.cu: build_slab_gather).
+kg_status kg_slab_gather_plan(int64_t n, int64_t p, const double* X, int32_t* slots, int32_t* gmax, int32_t* plane) {
+  constexpr int kW = 5, kG = 8;
+  if (!X || !slots || !gmax || !plane || n < 4 || (n & 3) || p < kW) return KG_EINVAL;
+  std::vector<int> lo(static_cast<size_t>(n), 0), len(static_cast<size_t>(n), 0);
+  for (int64_t r = 0; r < n; ++r) {  // row bands by an exact-zero test
+    int64_t a = p, b = 0;
+    for (int64_t k = 0; k < p; ++k)
+      if (X[r + n * k] != 0.0) {
+        a = std::min(a, k);
+        b = std::max(b, k + 1);
+      }
+    lo[static_cast<size_t>(r)] = a < b ? static_cast<int>(a) : 0;
+    len[static_cast<size_t>(r)] = a < b ? static_cast<int>(b - a) : 0;
+  }
+  const int nq = static_cast<int>(n / 4), groups = static_cast<int>((p + 7) / 8);
+  int PL = nq * kW + 1;
+  while ((PL & 7) != 2) ++PL;
+  if (PL > 0xffff) return KG_EINVAL;
+  int gm = 0;
+  for (int k = 0; k < groups * 8; ++k) {
+    int cnt = 0;
+    for (int j = 0; j < kG; ++j) slots[static_cast<size_t>(k) * kG + j] = PL - 1;  // the zero slot
+    for (int q = 0; q < nq && k < p; ++q) {
+      const int wlo = std::min<int>(lo[static_cast<size_t>(4 * q)], static_cast<int>(p) - kW);
+      bool hit = false;
+      for (int r = 4 * q; r < 4 * q + 4; ++r)
+        hit = hit || (lo[static_cast<size_t>(r)] <= k && k < lo[static_cast<size_t>(r)] + len[static_cast<size_t>(r)]);
+      if (!hit) continue;
+      if (k < wlo || k >= wlo + kW || cnt == kG) return KG_EINVAL;
+      slots[static_cast<size_t>(k) * kG + cnt++] = q * kW + (k - wlo);
+    }
+    gm = std::max(gm, cnt);
+  }
+  *gmax = gm;
+  *plane = PL;
+  return KG_OK;
+}
+
 kg_status kg_halo_plan(int64_t n, int64_t p, const double* X, int world, int rank, int64_t* out) {
   if (!X || !out || n < 1 || p < 1 || world < 1 || rank < 0 || rank >= world || n < world) return KG_EINVAL;
   // touched coefficient range of every rank's rows (rows without nonzeros add nothing)

@@ -641,36 +641,20 @@ struct SlabTables {
   int nch = 0, gmax = 0, PL = 0;
 };
 
-// Gather table of the scatter/gather Y step (SlabArgs::gat) from the row bands
-// of X1: row quad q scatters its five window partials to slots 5q .. 5q + 4 of
-// its column pair's plane; basis function k then sums, in ascending quad
-// order, the slots of the quads that have a row with k inside its band.
-static void build_slab_gather(SlabTables& T, const std::vector<int>& hlo, const std::vector<int>& hlen, i64 n1, i64 p1,
-                              cudaStream_t st) {
-  constexpr int kW = 5, kG = 8;
-  if ((n1 & 3) || p1 < kW) return;
-  const int nq = static_cast<int>(n1 / 4), groups = static_cast<int>((p1 + 7) / 8);
-  int PL = nq * kW + 1;
-  while ((PL & 7) != 2) ++PL;
-  if (PL > 0xffff) return;
-  std::vector<int> gat(static_cast<size_t>(groups) * 8 * 4, 0);
-  int gmax = 0;
-  for (int k = 0; k < groups * 8; ++k) {
-    unsigned short slot[kG];
-    for (int j = 0; j < kG; ++j) slot[j] = static_cast<unsigned short>(PL - 1);  // the zero slot
-    int cnt = 0;
-    for (int q = 0; q < nq && k < p1; ++q) {
-      const int lo = std::min<int>(hlo[static_cast<size_t>(4 * q)], static_cast<int>(p1) - kW);
-      bool hit = false;
-      for (int r = 4 * q; r < 4 * q + 4; ++r)
-        hit = hit || (hlo[static_cast<size_t>(r)] <= k && k < hlo[static_cast<size_t>(r)] + hlen[static_cast<size_t>(r)]);
-      if (!hit) continue;
-      if (k < lo || k >= lo + kW || cnt == kG) return;  // outside the quad's window / too many quads: keep k_slab
-      slot[cnt++] = static_cast<unsigned short>(q * kW + (k - lo));
-    }
-    gmax = std::max(gmax, cnt);
-    for (int j = 0; j < 4; ++j) gat[static_cast<size_t>(k) * 4 + j] = slot[2 * j] | (static_cast<int>(slot[2 * j + 1]) << 16);
-  }
+// Gather table of the scatter/gather Y step (SlabArgs::gat) from the dense
+// mode-1 factor X1 (n1 x p1, column-major): the host plan kg_slab_gather_plan
+// (row quad q scatters its five window partials to slots 5q .. 5q + 4 of its
+// column pair's plane; basis function k sums, in ascending quad order, the
+// slots of the quads that have a row with k inside its band), packed as 8
+// 16-bit slots per basis function.
+static void build_slab_gather(SlabTables& T, const double* X1, i64 n1, i64 p1, cudaStream_t st) {
+  const int groups = static_cast<int>((p1 + 7) / 8);
+  std::vector<int32_t> slots(static_cast<size_t>(groups) * 64);
+  int32_t gmax = 0, PL = 0;
+  if (kg_slab_gather_plan(n1, p1, X1, slots.data(), &gmax, &PL) != KG_OK) return;  // the pass keeps its DMMA form
+  std::vector<int> gat(static_cast<size_t>(groups) * 8 * 4);
+  for (size_t k = 0; k < static_cast<size_t>(groups) * 8; ++k)
+    for (int j = 0; j < 4; ++j) gat[k * 4 + j] = slots[k * 8 + 2 * j] | (slots[k * 8 + 2 * j + 1] << 16);
   T.gat.alloc(sizeof(int) * gat.size());
   h2d(T.gat.p, gat.data(), sizeof(int) * gat.size(), st);
   T.gmax = gmax;
@@ -2808,7 +2792,7 @@ kg_status kg_design_create(kg_ctx* ctx, int64_t c, int64_t d, const int64_t* n, 
     }
     if (D->fused && d == 3 && dev_env("KG_NO_SLAB") == nullptr)
       D->slab = build_slab(factors[1], D->n[1], D->p[0][1], ctx->s);
-    if (D->slab) build_slab_gather(*D->slab, D->f[0][0]->h_lo, D->f[0][0]->h_len, n1, p1, ctx->s);
+    if (D->slab) build_slab_gather(*D->slab, factors[0], n1, p1, ctx->s);
     // (KG_HALO=0 keeps the all-reduce; KG_HALO=1 also runs the owned-slice
     // path on a one-rank communicator, where it has no neighbours: a test hook)
     const char* he = std::getenv("KG_HALO");
