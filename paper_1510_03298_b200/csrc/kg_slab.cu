@@ -746,7 +746,15 @@ __global__ void __launch_bounds__(kSlabBS, 1) k_slab2(SlabArgs a) {
 //     setmaxnreg: tensor warpgroups 120, row warpgroups 136.
 constexpr int kPLMax = 322;                 // slots per column-pair plane at n1 = 256
 constexpr int kPBuf = 8 * kPLMax;           // doubles per partial tile
-constexpr int kUBuf = kLdr * 64;            // doubles per U tile (p1 <= 64)
+// U tile of k_slab4: 64 rows (p1 <= 64) of 8 doubles = four 16-byte column-pair
+// units, unit u of row r stored at unit u ^ ((r >> 1) & 3).  Both access
+// patterns are then conflict free: a tensor-warp quarter (rows 2q, 2q + 1, all
+// four units) writes 8 distinct bank groups, and a row-warp quarter (8
+// consecutive rows, one unit) reads 8 distinct bank groups.
+constexpr int kUBuf = 8 * 64;
+__device__ __forceinline__ unsigned u_tile_off(int row, int unit) {  // byte offset inside a U tile
+  return static_cast<unsigned>(row * 64 + ((unit ^ ((row >> 1) & 3)) << 4));
+}
 
 __device__ __forceinline__ bool mbar_try_s(unsigned bar, unsigned parity) {
   unsigned ok;
@@ -874,7 +882,9 @@ __global__ void __launch_bounds__(kSlabBS, 1) k_slab4(SlabArgs a) {
         }
       }
     }
-    const unsigned ub0 = smem_u32(Us + lo * kLdr + c0);
+    unsigned ub[kWin];  // this thread's five window rows of U tile 0 (column pair cp)
+#pragma unroll
+    for (int t = 0; t < kWin; ++t) ub[t] = smem_u32(Us) + u_tile_off(lo + t, cp);
     const unsigned pb0 = smem_u32(Ps) + 16u * static_cast<unsigned>(cp * PL + rq * kWin);
     const unsigned vb0 = smem_u32(Vs + r0 + n1 * c0) + (sw ? 16u : 0u);   // rows (sw ? 2,3 : 0,1) of column c0
     const unsigned vb1 = smem_u32(Vs + r0 + n1 * c0) + (sw ? 0u : 16u);   // the other two rows
@@ -918,7 +928,7 @@ __global__ void __launch_bounds__(kSlabBS, 1) k_slab4(SlabArgs a) {
       if (act) {
         double2 uu[kWin];
 #pragma unroll
-        for (int t = 0; t < kWin; ++t) uu[t] = lds2_s(uo + 8 * (j * kUBuf + t * kLdr));
+        for (int t = 0; t < kWin; ++t) uu[t] = lds2_s(ub[t] + uo + 8 * j * kUBuf);
         double vr[8];
         {
           const double2 x0 = lds2_s(vb0 + vo + 8 * j * kVBuf), x1 = lds2_s(vb1 + vo + 8 * j * kVBuf);
@@ -972,7 +982,7 @@ __global__ void __launch_bounds__(kSlabBS, 1) k_slab4(SlabArgs a) {
       const unsigned hb = static_cast<unsigned>(ip & 1), par = static_cast<unsigned>(ip >> 1) & 1u;
       mbar_wait_s(ubar0 + 8 * hb, par);
       mbar_wait_s(vbar0 + 8 * hb, par);
-      const unsigned uo = ub0 + hb * (16 * kUBuf), po = pb0 + hb * (16 * kPBuf), vo = hb * (16 * kVBuf);
+      const unsigned uo = hb * (16 * kUBuf), po = pb0 + hb * (16 * kPBuf), vo = hb * (16 * kVBuf);
       if (warp == 0 && ip > 0) {  // pair ip - 1 is read: pair ip + 1 into its v tiles
         mbar_wait_s(wbar0 + 8 * (hb ^ 1u), static_cast<unsigned>((ip - 1) >> 1) & 1u);
         if (lane == 0) copy_pair(hb ^ 1u);
@@ -990,7 +1000,7 @@ __global__ void __launch_bounds__(kSlabBS, 1) k_slab4(SlabArgs a) {
     const bool leader = tid == 8 * 32;
     const int zr = 8 * tw + (lane >> 2), zq = 2 * (lane & 3);
     const bool zok = zr < p1;
-    const unsigned ua0 = smem_u32(Us + zr * kLdr + zq);  // U store (tile 0)
+    const unsigned ua0 = smem_u32(Us) + u_tile_off(zr, lane & 3);  // U store (tile 0)
     // gather slots of basis function zr as shared addresses in partial tile 0 (column pair lane & 3)
     unsigned gs[G];
     {
@@ -1173,9 +1183,14 @@ static size_t slab_layout(SlabArgs& a) {
   a.ldW = (a.n1 + 15) / 16 * 16 + 4;         // = 4 (mod 16): B fragments of stage C
   a.cg = 1;
   const size_t ubuf = static_cast<size_t>(kLdr) * 8 * ((a.p1 + 7) / 8);
-  if (slab_gather(a))  // k_slab4: fixed-stride U / partial tiles and the X2 chunk tables
-    return (kDepth * static_cast<size_t>(kVBuf + kUBuf + kPBuf) + static_cast<size_t>(a.nch) * (128 + 64 + 1)) *
-           sizeof(double);
+  if (slab_gather(a)) {
+    // k_slab4: v ring, fixed-stride U / partial tiles, the X2 chunk tables; k_slab2
+    // (the same shapes with an odd chunk count or a partial last chunk): two S3
+    // tiles, U and partial tiles with the design's strides
+    const size_t k4 = kDepth * static_cast<size_t>(kVBuf + kUBuf + kPBuf) + static_cast<size_t>(a.nch) * (128 + 64 + 1);
+    const size_t k2 = 2 * static_cast<size_t>(a.ldS) * a.p2 + kDepth * ubuf + kDepth * static_cast<size_t>(8) * a.PL;
+    return std::max(k4, k2) * sizeof(double);
+  }
   const size_t dbl = 2 * static_cast<size_t>(a.ldS) * a.p2 + kDepth * ubuf + kDepth * static_cast<size_t>(a.ldW) * 8;
   return dbl * sizeof(double);
 }
