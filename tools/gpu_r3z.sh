@@ -10,4 +10,3 @@ timeout 600 python bench.py --impl reference --steps 3 --warmup 3 > gpurun_out/r
 for c in C2 C3 C4; do timeout 300 python bench.py --config $c --steps 5 --warmup 3 --no-cpu-baseline > gpurun_out/bench_${c}_r3z.json 2> gpurun_out/bench_${c}_r3z.err; echo "$c rc=$?"; done
 
 timeout 600 ncu --set full --import-source on --clock-control none -k regex:k_slab -s 2 -c 1 -o gpurun_out/r03_C5_k_slab4_last python tools/time_kernel.py --config C5 --which 0 --reps 3 > gpurun_out/ncu_slab_r3z.log 2>&1; echo "ncu slab rc=$?"
-KG_HOST_LOOP=1 timeout 1500 ncu --metrics gpu__time_duration.sum,dram__bytes_read.sum,dram__bytes_write.sum --clock-control none --csv --log-file gpurun_out/r03_launches_C5.csv python tools/prof_path.py --config C5 --paths 1 --n-lambda 3 > gpurun_out/ncu_C5_r3z.log 2>&1; echo "ncu list rc=$?"
