@@ -547,3 +547,43 @@ def test_slab_fallback_kernels_match_oracle(switch):
                        env=env, cwd=root, capture_output=True, text=True, timeout=900)
     assert r.returncode == 0, r.stdout[-2000:] + r.stderr[-2000:]
     assert "6 passed" in r.stdout, r.stdout[-500:]
+
+
+_FIT_DUMP = """
+import sys, numpy as np
+sys.path.insert(0, {root!r})
+from paper_1510_03298_b200 import configs
+from paper_1510_03298_b200 import kronglm as K
+n, p = (64, 48, 20), (16, 12, 6)
+design = [[K.bspline_design(np.linspace(0, 1, a), 4, b) for a, b in zip(n, p)]]
+rng = np.random.default_rng(7)
+B = np.zeros(p); m = rng.random(p) < 0.15; B[m] = rng.standard_normal(m.sum())
+eta = configs.tensor_h(design[0], B)
+y = rng.poisson(np.exp(np.log(20.0) / max(eta.max(), 1e-3) * eta)).astype(float)
+out = K.fit_path(design, "poisson", y, n_lambda=8, lambda_min_ratio=1e-2)
+np.savez({dst!r}, coef=np.stack([c[0].ravel(order="F") for c in out["coefficients"]]),
+         obj=np.array(out["objectives"]), inner=np.array(out["inner_iters"]))
+"""
+
+
+@pytest.mark.gpu
+def test_forked_control_and_dependent_launches_change_nothing(tmp_path):
+    """The slab route's FISTA body runs the control kernel beside the mode-3 G
+    step and chains its n-space kernels by programmatic dependent launch.  With
+    both switched off (KG_NO_FORK, KG_NO_PDL: the serial body) the fit must be
+    bitwise identical: the overlap may not reorder anything that is read."""
+    import subprocess
+    import sys
+    root = os.path.dirname(os.path.dirname(os.path.abspath(__file__)))
+    outs = []
+    for tag, extra in (("overlap", {}), ("serial", {"KG_DEV": "1", "KG_NO_FORK": "1", "KG_NO_PDL": "1"})):
+        dst = str(tmp_path / f"{tag}.npz")
+        r = subprocess.run([sys.executable, "-c", _FIT_DUMP.format(root=root, dst=dst)], env=dict(os.environ, **extra),
+                           cwd=root, capture_output=True, text=True, timeout=600)
+        assert r.returncode == 0, r.stderr[-2000:]
+        outs.append(np.load(dst))
+    a, b = outs
+    assert np.array_equal(a["inner"], b["inner"])
+    assert np.array_equal(a["obj"], b["obj"])
+    assert np.array_equal(a["coef"], b["coef"])
+    assert a["inner"].sum() > 100
