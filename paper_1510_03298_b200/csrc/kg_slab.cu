@@ -9,25 +9,24 @@
 // S(x) = Q3 x_3 X3^T, so the only n-sized traffic of a step is one read of v
 // (the p1 x n2 x n3 partials of the mode-1 route never touch HBM).
 //
-// One CTA per SM (persistent over slices), 16 warps in two roles that form a
-// software pipeline over chunks of 8 mode-2 grid rows:
-//   * 8 "row" warps: a thread owns 4 consecutive grid rows x 2 columns of a
-//     chunk; eta = X1 U over a 5-wide coefficient window in registers (the 4
-//     rows share one window, so 5 shared loads serve 8 cells), w = v eta,
-//     sum w eta.  v streams from HBM straight into registers (16-byte loads,
-//     two chunks ahead), and w goes to a padded double-buffered tile
-//     (stride = 4 mod 16, so the DMMA B fragments of the tensor warps are
-//     conflict free);
-//   * 8 "tensor" warps (warp = 8 rows of p1): Y = X1^T w (DMMA m8n8k4, the
-//     band window of the row group as A fragments in registers), Z += Y X2
-//     (DMMA whose A fragments are Y's accumulators: the k index runs over the
-//     chunk's rows in the order 0,2,4,6 | 1,3,5,7, so the D layout of one MMA
-//     is the A layout of the next), and U = S3 X2[chunk]^T for the chunk two
-//     ahead (DMMA).  Z lives in a two-tile register window that slides with the
-//     chunk's coefficient window; completed tiles go straight to Q3.
-// The roles hand over through named barriers (U ready / U free / w ready /
-// w free, double-buffered), so the row warps' FP64 FMAs and loads and the
-// tensor warps' DMMAs overlap instead of alternating.
+// Three kernels, all one persistent CTA per SM with 8 "row" warps (eta, w,
+// sum v eta^2 per 4 x 2 cells, coefficient windows in registers) and 8
+// "tensor" warps (U, Y -> Z, Q3; DMMA m8n8k4) pipelined over chunks of 8
+// mode-2 grid rows:
+//   * k_slab4 (the default; whole chunk pairs): Y by scatter/gather of the row
+//     threads' window partials, v by cp.async.bulk into a shared ring, S3
+//     operands straight from L2, mbarrier hand-over in chunk pairs, chunk
+//     tables in shared memory, setmaxnreg per role;
+//   * k_slab2 (odd chunk counts, partial last chunks): the same scatter/gather
+//     with v staged through registers and the S3 tile by bulk copies;
+//   * k_slab (designs without a gather table): Y = X1^T w by DMMA over the band
+//     window (A fragments in registers, w through a padded shared tile), named
+//     barriers.
+// In all three Z += Y X2 uses Y's accumulator layout as the A layout of the
+// next DMMA (the k index runs over the chunk's rows as 0,2,4,6 | 1,3,5,7) and
+// Z lives in a two-tile register window that slides with the chunk's
+// coefficient window; completed tiles go straight to Q3.  Every reduction has
+// a fixed order.
 #include <algorithm>
 #include <cstdlib>
 
