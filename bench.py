@@ -401,7 +401,7 @@ def run_ours(args):
             roof["note"] = ("k_slab4 moves exactly its algorithmic bytes (traffic); with v streamed by bulk copies "
                             "alone the kernel takes ~105 us (5.7 TB/s); the rest is issue latency of its 16 resident "
                             "warps and shared-memory bandwidth (v, the U windows and the scatter/gather partials "
-                            "all cross shared memory: ~122 KB per 2048-cell chunk, L1/shared pipe 71% busy) "
+                            "all cross shared memory: ~122 KB per 2048-cell chunk, L1/shared pipe 74% busy) "
                             "(DESIGN.md 4b)")
     fp64 = fp64_peaks()
     if fp64:
