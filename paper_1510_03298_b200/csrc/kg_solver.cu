@@ -228,21 +228,37 @@ static void build_band(const FactorHost& h, bool rows_of_x, std::vector<int>& lo
   off.assign(R, 0);
   coef.clear();
   maxlen = 0;
-  for (i64 r = 0; r < R; ++r) {
-    i64 first = -1, last = -1;
+  // first / last nonzero of every operator row; the factor is column-major, so
+  // the row bands of X come from one sweep down its columns (a row-wise scan
+  // strides by n doubles: 10 ms for a 4096 x 256 factor)
+  std::vector<i64> first(static_cast<size_t>(R), -1), last(static_cast<size_t>(R), -1);
+  if (rows_of_x) {
     for (i64 k = 0; k < K; ++k) {
-      const double v = rows_of_x ? h.X[r + h.n * k] : h.X[k + h.n * r];
-      if (v != 0.0) {
-        if (first < 0) first = k;
-        last = k;
-      }
+      const double* col = h.X.data() + h.n * k;
+      for (i64 r = 0; r < R; ++r)
+        if (col[r] != 0.0) {
+          if (first[static_cast<size_t>(r)] < 0) first[static_cast<size_t>(r)] = k;
+          last[static_cast<size_t>(r)] = k;
+        }
     }
+  } else {
+    for (i64 r = 0; r < R; ++r) {
+      const double* col = h.X.data() + h.n * r;
+      for (i64 k = 0; k < K; ++k)
+        if (col[k] != 0.0) {
+          if (first[static_cast<size_t>(r)] < 0) first[static_cast<size_t>(r)] = k;
+          last[static_cast<size_t>(r)] = k;
+        }
+    }
+  }
+  for (i64 r = 0; r < R; ++r) {
     off[r] = static_cast<i64>(coef.size());
-    if (first < 0) continue;
-    lo[r] = static_cast<int>(first);
-    len[r] = static_cast<int>(last - first + 1);
+    const i64 a = first[static_cast<size_t>(r)], b = last[static_cast<size_t>(r)];
+    if (a < 0) continue;
+    lo[r] = static_cast<int>(a);
+    len[r] = static_cast<int>(b - a + 1);
     maxlen = std::max(maxlen, len[r]);
-    for (i64 k = first; k <= last; ++k) coef.push_back(rows_of_x ? h.X[r + h.n * k] : h.X[k + h.n * r]);
+    for (i64 k = a; k <= b; ++k) coef.push_back(rows_of_x ? h.X[r + h.n * k] : h.X[k + h.n * r]);
   }
 }
 
