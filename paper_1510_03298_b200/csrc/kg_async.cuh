@@ -40,21 +40,6 @@ __device__ __forceinline__ bool mbar_try(unsigned long long* bar, unsigned parit
   return ok != 0;
 }
 
-// Non-blocking poll (test_wait never suspends the thread; try_wait may, up to a system time limit)
-__device__ __forceinline__ bool mbar_test(unsigned long long* bar, unsigned parity) {
-  unsigned ok;
-  asm volatile(
-      "{\n"
-      ".reg .pred p;\n"
-      "mbarrier.test_wait.parity.shared::cta.b64 p, [%1], %2;\n"
-      "selp.u32 %0, 1, 0, p;\n"
-      "}\n"
-      : "=r"(ok)
-      : "r"(smem_u32(bar)), "r"(parity)
-      : "memory");
-  return ok != 0;
-}
-
 // Spin budget of the device watchdogs (~4 s at 2 GHz): a barrier or copy that
 // never completes traps (a CUDA error on the host) instead of wedging the GPU.
 constexpr long long kWatchdogCycles = 1LL << 33;
