@@ -268,7 +268,8 @@ def relaunch_under_torchrun(args):
         sys.exit(1)
     cmd = [sys.executable, "-m", "torch.distributed.run", "--nnodes=1", f"--nproc-per-node={args.gpus}",
            "--master-addr", "127.0.0.1", "--master-port", str(29500 + os.getpid() % 1000)] + sys.argv
-    sys.exit(subprocess.call(cmd))
+    sys.stdout.flush()
+    sys.exit(subprocess.call(cmd, stdout=sys.stdout))  # the ranks inherit the real stdout (see _quiet_stdout)
 
 
 def run_ours(args):
@@ -470,8 +471,20 @@ def run_ours(args):
         dist.destroy_process_group()
 
 
+def _quiet_stdout():
+    """The contract is ONE JSON line on stdout.  Native libraries write there too
+    (NCCL prints its version banner to stdout when NCCL_DEBUG is set in the
+    environment), so file descriptor 1 is pointed at stderr for the whole run and
+    Python's sys.stdout keeps the original descriptor for the JSON line."""
+    sys.stdout.flush()
+    keep = os.dup(1)
+    os.dup2(2, 1)
+    sys.stdout = os.fdopen(keep, "w", buffering=1)
+
+
 def main():
     args = parse()
+    _quiet_stdout()
     if args.impl == "reference":
         run_reference(args)
         return

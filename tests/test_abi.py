@@ -81,3 +81,22 @@ def test_result_accessors_reject_out_of_range_models():
     assert L.kg_result_nonzero(None, 0) == -1
     assert L.kg_result_n_outer(None, 0) == -1
     assert L.kg_result_trace(None, 0, None) == _lib.KG_EINVAL
+
+
+def test_bench_refuses_missing_gpus_with_one_json_line():
+    """bench.py prints exactly one JSON line on stdout, whatever native libraries
+    write there (file descriptor 1 is pointed at stderr for the run), and a
+    --gpus N request on a box with fewer GPUs is refused, not run at N = 1."""
+    import json
+    import subprocess
+    import sys
+    import torch
+    if torch.cuda.device_count() >= 2:
+        pytest.skip("needs a box with fewer than 2 GPUs")
+    root = os.path.dirname(os.path.dirname(os.path.abspath(__file__)))
+    r = subprocess.run([sys.executable, os.path.join(root, "bench.py"), "--gpus", "2", "--steps", "1", "--warmup", "1"],
+                       capture_output=True, text=True, timeout=300)
+    lines = [ln for ln in r.stdout.splitlines() if ln.strip()]
+    assert len(lines) == 1
+    assert "refusing" in json.loads(lines[0])["error"]
+    assert r.returncode != 0
